@@ -1,0 +1,462 @@
+"""Reference-shaped Python host API over the C ABI (include/prenom/prenom_gpu.h).
+
+Names and argument meaning follow the reference's object-trainer surface in
+/root/reference/proj/core (namespace ``noma``):
+
+==========================  ==============================================
+this module                 reference
+==========================  ==============================================
+``FieldArch``               ``noma::FieldArch``      field.hpp:20-31
+``Camera`` / ``Pose``       ``noma::Camera`` / ``Pose`` render.hpp:13-23, geom.hpp:120-131
+``TrainConfig``             ``MapperConfig`` hot keys mapper.hpp:80-103
+``ObjectTrainer.create``    train_track CREATE block  mapper.cpp:133-143
+``ObjectTrainer.train_step`` train_track loop body    mapper.cpp:150-184
+``ObjectTrainer.render``    field_eval + composite    render.hpp:79
+``ObjectTrainer.density_query`` refresh_grid          density_grid.cpp:119-132
+``UsageError`` etc.         errors.hpp:9-24
+==========================  ==============================================
+
+Every compute call goes through the CUDA library; there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field, fields
+
+import numpy as np
+
+from . import _capi
+from ._capi import CameraC, FieldArchC, PoseC, StepStatsC, TrainCfgC, fptr, iptr, u8ptr, u32ptr
+
+
+# --------------------------------------------------------------- errors
+class PrenomError(RuntimeError):
+    code = -1
+
+
+class UsageError(PrenomError):  # noma::UsageError
+    code = _capi.PRENOM_USAGE
+
+
+class DataError(PrenomError):  # noma::DataError
+    code = _capi.PRENOM_DATA
+
+
+class NumericError(PrenomError):  # noma::NumericError
+    code = _capi.PRENOM_NUMERIC
+
+
+class CudaError(PrenomError):
+    code = _capi.PRENOM_CUDA
+
+
+_ERRORS = {c.code: c for c in (UsageError, DataError, NumericError, CudaError)}
+
+
+def _check(status: int):
+    if status != 0:
+        msg = _capi.load().prenom_last_error()
+        msg = msg.decode() if msg else ""
+        raise _ERRORS.get(status, PrenomError)(msg)
+
+
+# ---------------------------------------------------------- value types
+@dataclass
+class FieldArch:
+    """noma::FieldArch (field.hpp:20-31); defaults are the reference's."""
+
+    hash_levels: int = 8
+    features_per_level: int = 2
+    log2_table_size: int = 14
+    base_resolution: int = 4
+    per_level_scale: float = 1.45
+    hidden_width: int = 32
+    hidden_layers: int = 2
+    density_activation: int = _capi.ACT_EXP_CLAMPED
+
+    def to_c(self) -> FieldArchC:
+        return FieldArchC(*[getattr(self, f.name) for f in fields(self)])
+
+    # field.cpp:122-139
+    def hash_param_count(self) -> int:
+        return self.hash_levels * self.features_per_level * (1 << self.log2_table_size)
+
+    def mlp_param_count(self) -> int:
+        n, i = 0, self.hash_levels * self.features_per_level
+        for _ in range(self.hidden_layers):
+            n += self.hidden_width * i + self.hidden_width
+            i = self.hidden_width
+        return n + 4 * i + 4
+
+    def param_count(self) -> int:
+        return self.hash_param_count() + self.mlp_param_count()
+
+    def level_resolution(self, level: int) -> int:
+        """field.cpp:113-116 (double pow over the float scale)."""
+        r = self.base_resolution * math.pow(float(np.float32(self.per_level_scale)), level)
+        return max(1, int(r))
+
+    @staticmethod
+    def scale_for(base: int, max_res: int, levels: int) -> float:
+        """Per-level scale reaching max_res at the top level."""
+        s = float(np.float32((max_res / base) ** (1.0 / (levels - 1))))
+        # nudge up one float ulp at a time until the top level is not truncated below max_res
+        while FieldArch(hash_levels=levels, base_resolution=base, per_level_scale=s).level_resolution(levels - 1) < max_res:
+            s = float(np.nextafter(np.float32(s), np.float32(2.0)))
+        return s
+
+
+def _mat_rowmajor(R) -> list:
+    return [float(x) for x in np.asarray(R, np.float32).reshape(9)]
+
+
+@dataclass
+class Pose:
+    """noma::Pose: world = R @ local + t (geom.hpp:120-131)."""
+
+    R: np.ndarray = field(default_factory=lambda: np.eye(3, dtype=np.float32))
+    t: np.ndarray = field(default_factory=lambda: np.zeros(3, np.float32))
+
+    def to_c(self) -> PoseC:
+        p = PoseC()
+        p.R[:] = _mat_rowmajor(self.R)
+        p.t[:] = [float(x) for x in np.asarray(self.t, np.float32)]
+        return p
+
+
+@dataclass
+class Camera:
+    """noma::Camera (render.hpp:13-23); pose is camera -> world."""
+
+    fx: float
+    fy: float
+    cx: float
+    cy: float
+    width: int
+    height: int
+    pose: Pose = field(default_factory=Pose)
+
+    def to_c(self) -> CameraC:
+        c = CameraC()
+        c.fx, c.fy, c.cx, c.cy = self.fx, self.fy, self.cx, self.cy
+        c.width, c.height = self.width, self.height
+        c.R[:] = _mat_rowmajor(self.pose.R)
+        c.t[:] = [float(x) for x in np.asarray(self.pose.t, np.float32)]
+        return c
+
+
+@dataclass
+class TrainConfig:
+    """Hot keys of MapperConfig/InnerOptions/LossWeights (mapper.hpp:80-103,
+    meta.hpp:14-19, render.hpp:93-96). Defaults are the mapper's."""
+
+    rays_per_iter: int = 128
+    bg_fraction: float = 0.25
+    samples_per_ray: int = 24
+    lambda_d: float = 0.1
+    lambda_sigma: float = 1e-4
+    coarse_samples: int = 32
+    escape_eps: float = 1e-4
+    grid_refresh_every: int = 50
+    eta: float = 1e-2
+    prior_sampling: int = 1
+    band_px: int = 8
+    mlp_precision: int = _capi.MLP_FP32
+    adam_beta1: float = 0.9
+    adam_beta2: float = 0.999
+    adam_eps: float = 1e-8
+
+    def to_c(self) -> TrainCfgC:
+        return TrainCfgC(*[getattr(self, f.name) for f in fields(self)])
+
+
+def mix_seed(base: int, salt: int) -> int:
+    """mapper.cpp:20-26 (per-track seed derivation)."""
+    M = (1 << 64) - 1
+    s = (base * 0x9E3779B97F4A7C15 + salt * 0xC2B2AE3D27D4EB4F + 1) & M
+    s ^= s >> 31
+    s = (s * 0x94D049BB133111EB) & M
+    s ^= s >> 29
+    return (s ^ (s >> 32)) & 0xFFFFFFFF
+
+
+def derive_seed(base: int, salt: int) -> int:
+    """meta.cpp:14-20 (per-meta-step seed derivation)."""
+    M = (1 << 64) - 1
+    s = (base * 0x9E3779B97F4A7C15 + salt * 0xBF58476D1CE4E5B9 + 1) & M
+    s ^= s >> 31
+    s = (s * 0x94D049BB133111EB) & M
+    s ^= s >> 29
+    return (s ^ (s >> 32)) & 0xFFFFFFFF
+
+
+# -------------------------------------------------------------- context
+class Context:
+    """One per GPU (prenom_ctx_create)."""
+
+    def __init__(self, device: int = 0):
+        self.lib = _capi.load()
+        h = C.c_void_p()
+        _check(self.lib.prenom_ctx_create(device, C.byref(h)))
+        self.h = h
+        self.device = device
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.prenom_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def stream(self) -> int:
+        s = C.c_void_p()
+        _check(self.lib.prenom_ctx_stream(self.h, C.byref(s)))
+        return s.value or 0
+
+    def synchronize(self):
+        _check(self.lib.prenom_ctx_synchronize(self.h))
+
+    def launch_count(self) -> int:
+        n = C.c_int64()
+        _check(self.lib.prenom_ctx_launch_count(self.h, C.byref(n)))
+        return n.value
+
+
+def _f32(a):
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+# --------------------------------------------------------------- trainer
+class ObjectTrainer:
+    """A per-object NeRF (hash grid + MLP + density grid + Adam) resident on one GPU."""
+
+    def __init__(self, ctx: Context, handle, arch: FieldArch, cfg: TrainConfig, grid_res: int):
+        self.ctx, self.h, self.arch, self.cfg, self.grid_res = ctx, handle, arch, cfg, grid_res
+        self.lib = ctx.lib
+
+    @classmethod
+    def create(cls, ctx: Context, arch: FieldArch, theta=None, grid=None, grid_res: int = 48,
+               seed: int = 0, cfg: TrainConfig | None = None, box_min=(-0.5, -0.5, -0.5),
+               box_max=(0.5, 0.5, 0.5)) -> "ObjectTrainer":
+        """Create from a category prior (theta, grid) or from init_params(seed)."""
+        cfg = cfg or TrainConfig()
+        if grid is not None:
+            grid = _f32(grid)
+            grid_res = int(round(len(grid.reshape(-1)) ** (1 / 3)))
+        th = None if theta is None else _f32(theta)
+        h = C.c_void_p()
+        a = arch.to_c()
+        c = cfg.to_c()
+        _check(ctx.lib.prenom_object_create(ctx.h, C.byref(a), fptr(th),
+                                            fptr(None if grid is None else grid.reshape(-1)), grid_res, seed,
+                                            C.byref(c), fptr(_f32(box_min)), fptr(_f32(box_max)), C.byref(h)))
+        return cls(ctx, h, arch, cfg, grid_res)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.prenom_object_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_frames(self, cams, rgb, depth, mask, instance_value: int = 1, obj_pose: Pose | None = None):
+        arr = (CameraC * len(cams))()
+        for i, c in enumerate(cams):
+            arr[i] = c.to_c() if isinstance(c, Camera) else c
+        pose = (obj_pose or Pose()).to_c()
+        _check(self.lib.prenom_object_set_frames(self.h, len(cams), arr, fptr(_f32(rgb)), fptr(_f32(depth)),
+                                                 u8ptr(np.ascontiguousarray(mask, np.uint8)), instance_value,
+                                                 C.byref(pose)))
+
+    def upload_frame(self, frame: int, rgb, depth, mask):
+        _check(self.lib.prenom_object_upload_frame(self.h, frame, fptr(rgb), fptr(depth), u8ptr(mask)))
+
+    def train_step(self, n_steps: int = 1, stats: bool = True):
+        """n_steps iterations; returns per-step loss dicts (or None when stats=False: async)."""
+        if not stats:
+            _check(self.lib.prenom_train_step(self.h, n_steps, None))
+            return None
+        out = (StepStatsC * n_steps)()
+        _check(self.lib.prenom_train_step(self.h, n_steps, out))
+        return [_stats(s) for s in out]
+
+    def last_stats(self, n: int = 1):
+        out = (StepStatsC * n)()
+        _check(self.lib.prenom_object_last_stats(self.h, n, out))
+        return [_stats(s) for s in out]
+
+    def step(self) -> int:
+        s = C.c_int64()
+        _check(self.lib.prenom_object_step(self.h, C.byref(s)))
+        return s.value
+
+    def check(self):
+        _check(self.lib.prenom_object_check(self.h))
+
+    def render(self, origins, dirs):
+        o, d = _f32(origins).reshape(-1, 3), _f32(dirs).reshape(-1, 3)
+        n = len(o)
+        rgb, dep = np.zeros((n, 3), np.float32), np.zeros(n, np.float32)
+        _check(self.lib.prenom_render(self.h, n, fptr(o), fptr(d), fptr(rgb), fptr(dep)))
+        return rgb, dep
+
+    def density_query(self, R: int, update_sampling_grid: bool = False):
+        out = np.zeros((R, R, R), np.float32)
+        _check(self.lib.prenom_density_query(self.h, R, fptr(out.reshape(-1)), int(update_sampling_grid)))
+        return out
+
+    def field_eval(self, xyz):
+        x = _f32(xyz).reshape(-1, 3)
+        n = len(x)
+        sig, rgb = np.zeros(n, np.float32), np.zeros((n, 3), np.float32)
+        _check(self.lib.prenom_field_eval(self.h, n, fptr(x), fptr(sig), fptr(rgb)))
+        return sig, rgb
+
+    def get_params(self):
+        out = np.zeros(self.arch.param_count(), np.float32)
+        _check(self.lib.prenom_get_params(self.h, fptr(out)))
+        return out
+
+    def set_params(self, theta):
+        _check(self.lib.prenom_set_params(self.h, fptr(_f32(theta))))
+
+    def get_grid(self):
+        r = C.c_int32()
+        _check(self.lib.prenom_get_grid(self.h, C.byref(r), None))
+        out = np.zeros((r.value,) * 3, np.float32)
+        _check(self.lib.prenom_get_grid(self.h, C.byref(r), fptr(out.reshape(-1))))
+        return out
+
+    def set_grid(self, grid):
+        g = _f32(grid)
+        _check(self.lib.prenom_set_grid(self.h, g.shape[0], fptr(g.reshape(-1))))
+
+    def get_adam(self):
+        P = self.arch.param_count()
+        m, v = np.zeros(P, np.float32), np.zeros(P, np.float32)
+        s = C.c_int64()
+        _check(self.lib.prenom_get_adam(self.h, fptr(m), fptr(v), C.byref(s)))
+        return m, v, s.value
+
+    def reset_adam(self):
+        _check(self.lib.prenom_reset_adam(self.h))
+
+    def copy_params_from(self, other: "ObjectTrainer"):
+        _check(self.lib.prenom_object_copy_params(self.h, other.h))
+
+    def debug_generate_rays(self, frame: int, step: int):
+        n = self.cfg.rays_per_iter
+        out = dict(origins=np.zeros((n, 3), np.float32), dirs=np.zeros((n, 3), np.float32),
+                   kinds=np.zeros(n, np.int32), target_rgb=np.zeros((n, 3), np.float32),
+                   target_depth=np.zeros(n, np.float32), pick_px=np.zeros(n, np.int32))
+        _check(self.lib.prenom_debug_generate_rays(self.h, frame, step, fptr(out["origins"]), fptr(out["dirs"]),
+                                                   iptr(out["kinds"]), fptr(out["target_rgb"]),
+                                                   fptr(out["target_depth"]), iptr(out["pick_px"])))
+        return out
+
+
+def train_many(objs, n_steps: int = 1):
+    arr = (C.c_void_p * len(objs))(*[o.h for o in objs])
+    _check(objs[0].lib.prenom_train_step_many(arr, len(objs), n_steps))
+
+
+def reptile_delta(meta: ObjectTrainer, adapted: ObjectTrainer, delta_ptr: int):
+    _check(meta.lib.prenom_reptile_delta(meta.h, adapted.h, C.c_void_p(delta_ptr)))
+
+
+def reptile_apply(meta: ObjectTrainer, delta_ptr: int, n_tasks: int, beta: float):
+    _check(meta.lib.prenom_reptile_apply(meta.h, C.c_void_p(delta_ptr), n_tasks, beta))
+
+
+def _stats(s: StepStatsC) -> dict:
+    return dict(total=s.total, color=s.color_term, depth=s.depth_term, sigma=s.sigma_term,
+                n_samples=s.n_samples, escaped=s.n_rays_escaped, frame=s.frame_index)
+
+
+# ------------------------------------------------ single-stage debug calls
+def debug_philox(ctx: Context, ctr_key):
+    ck = np.ascontiguousarray(ctr_key, np.uint32).reshape(-1, 6)
+    out = np.zeros((len(ck), 4), np.uint32)
+    _check(ctx.lib.prenom_debug_philox(ctx.h, len(ck), u32ptr(ck), u32ptr(out)))
+    return out
+
+
+def debug_hash_encode(ctx: Context, arch: FieldArch, params, xyz):
+    x = _f32(xyz).reshape(-1, 3)
+    out = np.zeros((len(x), arch.hash_levels * arch.features_per_level), np.float32)
+    a = arch.to_c()
+    _check(ctx.lib.prenom_debug_hash_encode(ctx.h, C.byref(a), fptr(_f32(params)), len(x), fptr(x), fptr(out)))
+    return out
+
+
+def debug_field_eval(ctx: Context, arch: FieldArch, params, xyz, precision: int = _capi.MLP_FP32):
+    x = _f32(xyz).reshape(-1, 3)
+    n = len(x)
+    sig, rgb, raw = np.zeros(n, np.float32), np.zeros((n, 3), np.float32), np.zeros((n, 4), np.float32)
+    a = arch.to_c()
+    _check(ctx.lib.prenom_debug_field_eval(ctx.h, C.byref(a), fptr(_f32(params)), n, fptr(x), fptr(sig), fptr(rgb),
+                                           fptr(raw), precision))
+    return sig, rgb, raw
+
+
+def debug_field_backward(ctx: Context, arch: FieldArch, params, xyz, d_sigma, d_rgb,
+                         precision: int = _capi.MLP_FP32):
+    x = _f32(xyz).reshape(-1, 3)
+    g = np.zeros(arch.param_count(), np.float32)
+    a = arch.to_c()
+    _check(ctx.lib.prenom_debug_field_backward(ctx.h, C.byref(a), fptr(_f32(params)), len(x), fptr(x),
+                                               fptr(_f32(d_sigma)), fptr(_f32(d_rgb).reshape(-1)), fptr(g),
+                                               precision))
+    return g
+
+
+def debug_adam(ctx: Context, params, grads, m, v, step, lr=1e-2, b1=0.9, b2=0.999, eps=1e-8):
+    p, mm, vv = _f32(params).copy(), _f32(m).copy(), _f32(v).copy()
+    s = C.c_int64(step)
+    _check(ctx.lib.prenom_debug_adam(ctx.h, len(p), fptr(p), fptr(_f32(grads)), fptr(mm), fptr(vv), C.byref(s),
+                                     lr, b1, b2, eps))
+    return p, mm, vv, s.value
+
+
+def debug_sample_rays(ctx: Context, origins, dirs, box_min, box_max, prior: bool, grid, n_coarse: int,
+                      n_fine: int, eps: float, seed: int, step: int):
+    o, d = _f32(origins).reshape(-1, 3), _f32(dirs).reshape(-1, 3)
+    n = len(o)
+    g = None if grid is None else _f32(grid)
+    R = 0 if g is None else g.shape[0]
+    out = dict(depths=np.zeros((n, n_fine), np.float32), deltas=np.zeros((n, n_fine), np.float32),
+               positions=np.zeros((n, n_fine, 3), np.float32), count=np.zeros(n, np.int32),
+               t_entry=np.zeros(n, np.float32), t_exit=np.zeros(n, np.float32))
+    _check(ctx.lib.prenom_debug_sample_rays(ctx.h, n, fptr(o), fptr(d), fptr(_f32(box_min)), fptr(_f32(box_max)),
+                                            int(prior), R, fptr(None if g is None else g.reshape(-1)), n_coarse,
+                                            n_fine, eps, seed, step, fptr(out["depths"]), fptr(out["deltas"]),
+                                            fptr(out["positions"]), iptr(out["count"]), fptr(out["t_entry"]),
+                                            fptr(out["t_exit"])))
+    return out
+
+
+def debug_batch_loss(ctx: Context, S: int, kind, target_rgb, target_depth, count, deltas, depths, sigma, rgb,
+                     bg_colors, lambda_d=0.1, lambda_sigma=1e-4):
+    kind = np.ascontiguousarray(kind, np.int32)
+    n = len(kind)
+    terms = np.zeros(4, np.float64)
+    ds, dr = np.zeros(n * S, np.float32), np.zeros((n * S, 3), np.float32)
+    col, dep = np.zeros((n, 3), np.float32), np.zeros(n, np.float32)
+    _check(ctx.lib.prenom_debug_batch_loss(ctx.h, n, S, iptr(kind), fptr(_f32(target_rgb).reshape(-1)),
+                                           fptr(_f32(target_depth)), iptr(np.ascontiguousarray(count, np.int32)),
+                                           fptr(_f32(deltas).reshape(-1)), fptr(_f32(depths).reshape(-1)),
+                                           fptr(_f32(sigma).reshape(-1)), fptr(_f32(rgb).reshape(-1)),
+                                           fptr(_f32(bg_colors).reshape(-1)), lambda_d, lambda_sigma,
+                                           terms.ctypes.data_as(C.POINTER(C.c_double)), fptr(ds), fptr(dr),
+                                           fptr(col), fptr(dep)))
+    return dict(terms=terms, d_sigma=ds, d_rgb=dr, color=col, depth=dep)
