@@ -46,6 +46,8 @@ void po_draw(uint64_t seed, uint32_t tag, int64_t step, uint32_t ray, uint32_t i
   po_philox(ctr, key, out);
 }
 
+double po_det_exp(double x) { return pdm_det_exp(x); }
+
 /* --------------------------------------------------------------- helpers */
 
 static float clampf01(float v) { return v < 0.f ? 0.f : (1.f < v ? 1.f : v); } /* std::clamp */

@@ -28,6 +28,8 @@ uint32_t po_pick(uint32_t x, uint32_t n);
 void po_draw(uint64_t seed, uint32_t tag, int64_t step, uint32_t ray, uint32_t idx,
              uint32_t out[4]);
 
+double po_det_exp(double x);
+
 /* field.cpp */
 int po_level_resolution(const prenom_field_arch* a, int level);
 size_t po_hash_param_count(const prenom_field_arch* a);

@@ -112,6 +112,7 @@ class Oracle(_Lib):
         sigs = {
             "po_philox": (None, [u32p, u32p, u32p]),
             "po_u01": (C.c_float, [C.c_uint32]),
+            "po_det_exp": (C.c_double, [C.c_double]),
             "po_pick": (C.c_uint32, [C.c_uint32, C.c_uint32]),
             "po_level_resolution": (C.c_int, [archp, C.c_int]),
             "po_param_count": (sz, [archp]),

@@ -1,0 +1,1217 @@
+// capi.cu -- host side of the C ABI in include/prenom/prenom_gpu.h.
+//
+// Owns per-GPU contexts and per-object device state, and orchestrates the
+// train step (train_track's loop body, mapper.cpp:150-184) as a sequence of
+// kernel launches on the context stream:
+//   k_sample -> k_fwd_tile -> k_composite (+stats) -> k_bwd_tile ->
+//   k_encode_bwd -> k_adam [-> k_field_points (grid refresh every m steps)]
+// The host never touches sample data: per step it only draws the keyframe
+// index (one Philox call, TAG_FRAME) and computes the Adam bias corrections
+// with glibc powf (field.cpp:300-301), like the reference.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <deque>
+#include <string>
+#include <vector>
+
+#include "prenom_device.cuh"
+
+using namespace prenom;
+
+namespace {
+
+thread_local std::string g_err;
+
+prenom_status fail(prenom_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+#define CUDA_TRY(expr)                                                                        \
+  do {                                                                                        \
+    cudaError_t _e = (expr);                                                                  \
+    if (_e != cudaSuccess)                                                                    \
+      return fail(PRENOM_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));          \
+  } while (0)
+
+#define STATUS_TRY(expr)                 \
+  do {                                   \
+    prenom_status _s = (expr);           \
+    if (_s != PRENOM_OK) return _s;      \
+  } while (0)
+
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  cudaError_t ensure(size_t count) {
+    if (count <= n && p) return cudaSuccess;
+    release();
+    n = std::max<size_t>(count, 1);
+    return cudaMalloc(&p, n * sizeof(T));
+  }
+};
+
+int level_resolution_host(const prenom_field_arch& a, int level) {
+  const double r = a.base_resolution * std::pow((double)a.per_level_scale, level);  // field.cpp:113-116
+  return std::max(1, (int)r);
+}
+
+prenom_status validate_arch(const prenom_field_arch* a) {
+  if (!a) return fail(PRENOM_USAGE, "arch is NULL");
+  if (a->hash_levels < 1 || a->features_per_level < 1 || a->log2_table_size < 0 || a->base_resolution < 1 ||
+      a->per_level_scale < 1.f || a->hidden_width < 1 || a->hidden_layers < 1)
+    return fail(PRENOM_DATA, "invalid architecture description");  // field.cpp arch_from_text
+  if (a->hash_levels > kMaxLevels) return fail(PRENOM_USAGE, "hash_levels exceeds 24");
+  if (a->features_per_level > 4) return fail(PRENOM_USAGE, "features_per_level exceeds 4");
+  if (a->hash_levels * a->features_per_level > kMaxIn) return fail(PRENOM_USAGE, "L*F exceeds 64");
+  if (a->hidden_width > kMaxWidth) return fail(PRENOM_USAGE, "hidden_width exceeds 64");
+  if (a->hidden_layers > kMaxHidden) return fail(PRENOM_USAGE, "hidden_layers exceeds 3");
+  if (a->log2_table_size > 26) return fail(PRENOM_USAGE, "log2_table_size exceeds 26");
+  if (a->density_activation != PRENOM_ACT_EXP_CLAMPED && a->density_activation != PRENOM_ACT_SOFTPLUS)
+    return fail(PRENOM_DATA, "unknown density activation");
+  return PRENOM_OK;
+}
+
+FieldDesc make_desc(const prenom_field_arch& a) {
+  FieldDesc d;
+  std::memset(&d, 0, sizeof d);
+  d.L = a.hash_levels;
+  d.F = a.features_per_level;
+  d.T = a.log2_table_size;
+  d.W = a.hidden_width;
+  d.H = a.hidden_layers;
+  d.act = a.density_activation;
+  d.in_dim = d.L * d.F;
+  d.rows = 1ll << d.T;
+  d.row_mask = (uint32_t)(d.rows - 1);
+  d.hash_params = (long long)d.L * d.F * d.rows;
+  for (int l = 0; l < d.L; ++l) {
+    d.res[l] = level_resolution_host(a, l);
+    const uint64_t v = (uint64_t)d.res[l] + 1;
+    d.dense_verts[l] = (v * v * v <= (uint64_t)d.rows) ? (uint32_t)v : 0u;  // field.cpp:143-146
+  }
+  int off = 0, in = d.in_dim;
+  for (int l = 0; l <= d.H; ++l) {
+    const int out = l < d.H ? d.W : 4;
+    d.w_off[l] = off;
+    d.b_off[l] = off + out * in;
+    off += out * in + out;
+    in = out;
+  }
+  d.mlp_params = off;
+  return d;
+}
+
+size_t param_count_host(const prenom_field_arch& a) {
+  const FieldDesc d = make_desc(a);
+  return (size_t)d.hash_params + (size_t)d.mlp_params;
+}
+
+// render.cpp:17-45 (8-connected BFS = Chebyshev band), per frame at upload.
+void dilation_band(int W, int H, const uint8_t* mask, uint8_t value, int band_px, std::vector<uint8_t>& band) {
+  const size_t n = (size_t)W * H;
+  band.assign(n, 0);
+  std::vector<int> dist(n, -1);
+  std::deque<int> q;
+  for (size_t i = 0; i < n; ++i)
+    if (mask[i] == value) {
+      dist[i] = 0;
+      q.push_back((int)i);
+    }
+  while (!q.empty()) {
+    const int idx = q.front();
+    q.pop_front();
+    const int x = idx % W, y = idx / W, d = dist[idx];
+    if (d >= band_px) continue;
+    for (int dy = -1; dy <= 1; ++dy)
+      for (int dx = -1; dx <= 1; ++dx) {
+        const int nx = x + dx, ny = y + dy;
+        if (nx < 0 || ny < 0 || nx >= W || ny >= H) continue;
+        const size_t ni = (size_t)ny * W + nx;
+        if (dist[ni] >= 0) continue;
+        dist[ni] = d + 1;
+        band[ni] = 1;
+        q.push_back((int)ni);
+      }
+  }
+}
+
+void mat_vec(const float* M, const float* v, float* out) {
+  out[0] = M[0] * v[0] + M[1] * v[1] + M[2] * v[2];
+  out[1] = M[3] * v[0] + M[4] * v[1] + M[5] * v[2];
+  out[2] = M[6] * v[0] + M[7] * v[1] + M[8] * v[2];
+}
+
+uint32_t philox_first(uint64_t seed, uint32_t tag, uint32_t step, uint32_t ray, uint32_t idx) {
+  const uint32_t ctr[4] = {idx, ray, step, tag};
+  uint32_t out[4];
+  pdm_philox4x32_10(ctr, (uint32_t)seed, (uint32_t)(seed >> 32), out);
+  return out[0];
+}
+
+}  // namespace
+
+struct prenom_ctx_s {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int64_t launches = 0;
+};
+
+struct FrameDev {
+  DevBuf<float> rgb, depth;
+  DevBuf<int> obj_px, bg_px;
+  int n_obj_px = 0, n_bg_px = 0;
+  prenom_camera cam;
+  float origin[3];  // world_to_obj.apply(camera.t)
+};
+
+struct prenom_object_s {
+  prenom_ctx_s* ctx = nullptr;
+  prenom_field_arch arch;
+  FieldDesc fd;
+  prenom_train_cfg cfg;
+  size_t P = 0;
+  DevBuf<float> params, grad, m, v;
+  int R = 0;
+  DevBuf<float> grid;
+  uint64_t seed = 0;
+  float bmin[3], bmax[3];
+  int64_t step = 0;
+  int64_t render_calls = 0;
+  // frames
+  std::vector<FrameDev*> frames;
+  int W = 0, H = 0;
+  uint8_t inst = 1;
+  prenom_pose pose;
+  float Rt[9];
+  // scratch
+  DevBuf<float4> pos_depth, target, out, dout;
+  DevBuf<float> delta, feat_t, dfeat_t, t_entry, t_exit;
+  DevBuf<int> kind, count;
+  DevBuf<StepStatsDev> stats;
+  int last_n_steps = 0;
+  DevBuf<int> flag;
+  ~prenom_object_s() {
+    for (auto* f : frames) delete f;
+  }
+};
+
+namespace {
+
+prenom_status ensure_scratch(prenom_object_s* o, int B, int S) {
+  const size_t N = (size_t)B * S;
+  const size_t Npad = ((N + kTile - 1) / kTile) * kTile;
+  CUDA_TRY(o->pos_depth.ensure(Npad));
+  CUDA_TRY(o->delta.ensure(Npad));
+  CUDA_TRY(o->out.ensure(Npad));
+  CUDA_TRY(o->dout.ensure(Npad));
+  CUDA_TRY(o->feat_t.ensure(Npad * o->fd.in_dim));
+  CUDA_TRY(o->dfeat_t.ensure(Npad * o->fd.in_dim));
+  CUDA_TRY(o->target.ensure(B));
+  CUDA_TRY(o->kind.ensure(B));
+  CUDA_TRY(o->count.ensure(B));
+  CUDA_TRY(o->t_entry.ensure(B));
+  CUDA_TRY(o->t_exit.ensure(B));
+  return PRENOM_OK;
+}
+
+SampleBufs bufs(prenom_object_s* o) {
+  SampleBufs sb;
+  std::memset(&sb, 0, sizeof sb);
+  sb.pos_depth = o->pos_depth.p;
+  sb.delta = o->delta.p;
+  sb.target = o->target.p;
+  sb.kind = o->kind.p;
+  sb.count = o->count.p;
+  sb.t_entry = o->t_entry.p;
+  sb.t_exit = o->t_exit.p;
+  return sb;
+}
+
+prenom_status check_flag(prenom_object_s* o) {
+  int f = 0;
+  CUDA_TRY(cudaMemcpyAsync(&f, o->flag.p, sizeof(int), cudaMemcpyDeviceToHost, o->ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(o->ctx->stream));
+  if (f & 1) return fail(PRENOM_NUMERIC, "field_eval produced a non-finite output");
+  if (f & 2) return fail(PRENOM_NUMERIC, "batch_loss: non-finite loss");
+  return PRENOM_OK;
+}
+
+RaySource frame_source(prenom_object_s* o, int fi) {
+  const FrameDev* f = o->frames[fi];
+  RaySource src;
+  std::memset(&src, 0, sizeof src);
+  src.mode = 0;
+  src.rgb = f->rgb.p;
+  src.depth = f->depth.p;
+  src.obj_px = f->obj_px.p;
+  src.bg_px = f->bg_px.p;
+  src.n_obj_px = f->n_obj_px;
+  src.n_bg_px = f->n_bg_px;
+  const int B = o->cfg.rays_per_iter;
+  // render.cpp:66-68
+  int n_bg = f->n_bg_px == 0 ? 0 : (int)std::lround((float)B * o->cfg.bg_fraction);
+  n_bg = std::min(n_bg, B);
+  src.n_obj = B - n_bg;
+  src.width = f->cam.width;
+  src.fx = f->cam.fx;
+  src.fy = f->cam.fy;
+  src.cx = f->cam.cx;
+  src.cy = f->cam.cy;
+  std::memcpy(src.Rc, f->cam.R, sizeof src.Rc);
+  std::memcpy(src.Rt, o->Rt, sizeof src.Rt);
+  std::memcpy(src.origin, f->origin, sizeof src.origin);
+  return src;
+}
+
+SamplerCfg sampler_cfg(prenom_object_s* o, int B, int prior, uint32_t tag, uint32_t step) {
+  SamplerCfg c;
+  std::memset(&c, 0, sizeof c);
+  c.B = B;
+  c.S = o->cfg.samples_per_ray;
+  c.prior = prior;
+  c.n_coarse = o->cfg.coarse_samples;
+  c.eps = o->cfg.escape_eps;
+  c.grid_res = o->R;
+  c.grid = o->grid.p;
+  std::memcpy(c.bmin, o->bmin, sizeof c.bmin);
+  std::memcpy(c.bmax, o->bmax, sizeof c.bmax);
+  c.seed = o->seed;
+  c.tag = tag;
+  c.step = step;
+  return c;
+}
+
+// One iteration of train_track's loop body (mapper.cpp:150-184).
+prenom_status enqueue_step(prenom_object_s* o, StepStatsDev* stats) {
+  cudaStream_t st = o->ctx->stream;
+  const prenom_train_cfg& c = o->cfg;
+  const int B = c.rays_per_iter, S = c.samples_per_ray;
+  const uint32_t step = (uint32_t)o->step;
+  // keyframe pick (mapper.cpp:151)
+  const int fi = (int)pdm_pick(philox_first(o->seed, PRENOM_TAG_FRAME, step, 0, 0), (uint32_t)o->frames.size());
+  const RaySource src = frame_source(o, fi);
+  if (src.n_obj_px == 0) return fail(PRENOM_DATA, "generate_rays: no object pixels");
+  const SampleBufs sb = bufs(o);
+  CUDA_TRY(launch_sample(src, sampler_cfg(o, B, c.prior_sampling, PRENOM_TAG_FINE, step), sb, nullptr, st));
+  CUDA_TRY(launch_field_fwd_train(o->fd, o->params.p, B, S, sb, o->feat_t.p, o->out.p, o->flag.p, st));
+  CompositeArgs ca;
+  std::memset(&ca, 0, sizeof ca);
+  ca.B = B;
+  ca.S = S;
+  ca.pos_depth = sb.pos_depth;
+  ca.delta = sb.delta;
+  ca.target = sb.target;
+  ca.kind = sb.kind;
+  ca.count = sb.count;
+  ca.out = o->out.p;
+  ca.bg_colors = nullptr;
+  ca.seed = o->seed;
+  ca.step = step;
+  ca.lambda_d = c.lambda_d;
+  ca.lambda_sigma = c.lambda_sigma;
+  ca.dout = o->dout.p;
+  ca.stats = stats;
+  ca.flag = o->flag.p;
+  ca.frame = fi;
+  CUDA_TRY(launch_composite(ca, st));
+  CUDA_TRY(launch_mlp_bwd_train(o->fd, o->params.p, o->grad.p, B, S, sb.count, o->feat_t.p, o->dout.p,
+                                o->dfeat_t.p, st));
+  CUDA_TRY(launch_encode_bwd(o->fd, o->params.p, o->grad.p, B, S, sb.count, sb.pos_depth, o->dfeat_t.p, st));
+  // adam_step (field.cpp:295-310); grad zeroed in the same pass (mapper.cpp:175)
+  const float stepf = (float)(o->step + 1);
+  const float c1 = 1.f - std::pow(c.adam_beta1, stepf);
+  const float c2 = 1.f - std::pow(c.adam_beta2, stepf);
+  CUDA_TRY(launch_adam(o->P, o->params.p, o->grad.p, o->m.p, o->v.p, c.eta, c.adam_beta1, c.adam_beta2, c.adam_eps,
+                       c1, c2, 1, st));
+  o->ctx->launches += 7;
+  o->step += 1;
+  // grid refresh every m iterations (mapper.cpp:182-183)
+  if (c.grid_refresh_every > 0 && o->step % c.grid_refresh_every == 0) {
+    CUDA_TRY(launch_refresh_grid(o->fd, o->params.p, o->R, o->grid.p, o->flag.p, st));
+    o->ctx->launches += 1;
+  }
+  return PRENOM_OK;
+}
+
+void to_host_stats(const StepStatsDev& d, prenom_step_stats* s) {
+  s->total = d.total;
+  s->color_term = d.color;
+  s->depth_term = d.depth;
+  s->sigma_term = d.sigma;
+  s->n_samples = (int64_t)d.n_samples;
+  s->n_rays_escaped = d.escaped;
+  s->frame_index = d.frame;
+}
+
+prenom_status set_frame_pixels(prenom_object_s* o, FrameDev* f, const float* rgb, const float* depth,
+                               const uint8_t* mask) {
+  const size_t npx = (size_t)o->W * o->H;
+  cudaStream_t st = o->ctx->stream;
+  CUDA_TRY(f->rgb.ensure(npx * 3));
+  CUDA_TRY(f->depth.ensure(npx));
+  CUDA_TRY(cudaMemcpyAsync(f->rgb.p, rgb, npx * 3 * sizeof(float), cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(f->depth.p, depth, npx * sizeof(float), cudaMemcpyHostToDevice, st));
+  if (mask) {
+    std::vector<int> obj, bg;
+    std::vector<uint8_t> band;
+    dilation_band(o->W, o->H, mask, o->inst, o->cfg.band_px, band);
+    for (size_t i = 0; i < npx; ++i) {
+      if (mask[i] == o->inst) obj.push_back((int)i);
+      if (band[i]) bg.push_back((int)i);
+    }
+    f->n_obj_px = (int)obj.size();
+    f->n_bg_px = (int)bg.size();
+    CUDA_TRY(f->obj_px.ensure(obj.size()));
+    CUDA_TRY(f->bg_px.ensure(bg.size()));
+    if (!obj.empty())
+      CUDA_TRY(cudaMemcpyAsync(f->obj_px.p, obj.data(), obj.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+    if (!bg.empty())
+      CUDA_TRY(cudaMemcpyAsync(f->bg_px.p, bg.data(), bg.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaStreamSynchronize(st));  // host vectors go out of scope
+  }
+  return PRENOM_OK;
+}
+
+}  // namespace
+
+// =========================================================== C ABI
+extern "C" {
+
+const char* prenom_last_error(void) { return g_err.c_str(); }
+int prenom_abi_version(void) { return PRENOM_ABI_VERSION; }
+
+void prenom_default_train_cfg(prenom_train_cfg* c) {
+  c->rays_per_iter = 128;
+  c->bg_fraction = 0.25f;
+  c->samples_per_ray = 24;
+  c->lambda_d = 0.1f;
+  c->lambda_sigma = 1e-4f;
+  c->coarse_samples = 32;
+  c->escape_eps = 1e-4f;
+  c->grid_refresh_every = 50;
+  c->eta = 1e-2f;
+  c->prior_sampling = 1;
+  c->band_px = 8;
+  c->mlp_precision = PRENOM_MLP_FP32;
+  c->adam_beta1 = 0.9f;
+  c->adam_beta2 = 0.999f;
+  c->adam_eps = 1e-8f;
+}
+
+prenom_status prenom_param_count(const prenom_field_arch* arch, size_t* total, size_t* hash) {
+  STATUS_TRY(validate_arch(arch));
+  const FieldDesc d = make_desc(*arch);
+  if (total) *total = (size_t)d.hash_params + d.mlp_params;
+  if (hash) *hash = (size_t)d.hash_params;
+  return PRENOM_OK;
+}
+
+prenom_status prenom_level_resolution(const prenom_field_arch* arch, int level, int* res) {
+  STATUS_TRY(validate_arch(arch));
+  if (level < 0 || level >= arch->hash_levels) return fail(PRENOM_USAGE, "level out of range");
+  *res = level_resolution_host(*arch, level);
+  return PRENOM_OK;
+}
+
+prenom_status prenom_ctx_create(int device, prenom_ctx_t* out) {
+  if (!out) return fail(PRENOM_USAGE, "out is NULL");
+  int n = 0;
+  CUDA_TRY(cudaGetDeviceCount(&n));
+  if (device < 0 || device >= n) return fail(PRENOM_USAGE, "no such CUDA device");
+  CUDA_TRY(cudaSetDevice(device));
+  auto* c = new prenom_ctx_s;
+  c->device = device;
+  cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete c;
+    return fail(PRENOM_CUDA, cudaGetErrorString(e));
+  }
+  *out = c;
+  return PRENOM_OK;
+}
+
+prenom_status prenom_ctx_destroy(prenom_ctx_t ctx) {
+  if (!ctx) return PRENOM_OK;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return PRENOM_OK;
+}
+
+prenom_status prenom_ctx_stream(prenom_ctx_t ctx, void** stream) {
+  if (!ctx || !stream) return fail(PRENOM_USAGE, "NULL argument");
+  *stream = (void*)ctx->stream;
+  return PRENOM_OK;
+}
+
+prenom_status prenom_ctx_synchronize(prenom_ctx_t ctx) {
+  if (!ctx) return fail(PRENOM_USAGE, "NULL ctx");
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return PRENOM_OK;
+}
+
+prenom_status prenom_ctx_launch_count(prenom_ctx_t ctx, int64_t* count) {
+  if (!ctx || !count) return fail(PRENOM_USAGE, "NULL argument");
+  *count = ctx->launches;
+  return PRENOM_OK;
+}
+
+prenom_status prenom_object_create(prenom_ctx_t ctx, const prenom_field_arch* arch, const float* theta,
+                                   const float* grid, int grid_res, uint64_t seed, const prenom_train_cfg* cfg,
+                                   const float box_min[3], const float box_max[3], prenom_object_t* out) {
+  if (!ctx || !out || !cfg || !box_min || !box_max) return fail(PRENOM_USAGE, "NULL argument");
+  STATUS_TRY(validate_arch(arch));
+  if (grid_res < 2 || grid_res > 1024) return fail(PRENOM_DATA, "grid resolution out of range");
+  if (cfg->rays_per_iter < 1) return fail(PRENOM_USAGE, "generate_rays: n must be >= 1");
+  if (cfg->samples_per_ray < 1 || cfg->samples_per_ray > 256) return fail(PRENOM_USAGE, "samples_per_ray must be in [1, 256]");
+  if (cfg->prior_sampling && (cfg->coarse_samples < 1 || cfg->coarse_samples > 1024))
+    return fail(PRENOM_USAGE, "coarse_samples must be in [1, 1024]");
+  for (int a = 0; a < 3; ++a)
+    if (!(box_max[a] > box_min[a])) return fail(PRENOM_DATA, "degenerate object box");
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  auto* o = new prenom_object_s;
+  o->ctx = ctx;
+  o->arch = *arch;
+  o->fd = make_desc(*arch);
+  o->cfg = *cfg;
+  o->P = param_count_host(*arch);
+  o->R = grid_res;
+  o->seed = seed;
+  std::memcpy(o->bmin, box_min, sizeof o->bmin);
+  std::memcpy(o->bmax, box_max, sizeof o->bmax);
+  std::memset(&o->pose, 0, sizeof o->pose);
+  o->pose.R[0] = o->pose.R[4] = o->pose.R[8] = 1.f;
+  std::memcpy(o->Rt, o->pose.R, sizeof o->Rt);
+  cudaStream_t st = ctx->stream;
+  auto cleanup = [&](prenom_status s) {
+    delete o;
+    return s;
+  };
+  const size_t P4 = (o->P + 3) & ~size_t(3);
+  if (o->params.ensure(P4) || o->grad.ensure(P4) || o->m.ensure(P4) || o->v.ensure(P4) ||
+      o->grid.ensure((size_t)grid_res * grid_res * grid_res) || o->flag.ensure(1) || o->stats.ensure(16))
+    return cleanup(fail(PRENOM_CUDA, "out of device memory creating object"));
+  cudaMemsetAsync(o->grad.p, 0, P4 * sizeof(float), st);
+  cudaMemsetAsync(o->m.p, 0, P4 * sizeof(float), st);
+  cudaMemsetAsync(o->v.p, 0, P4 * sizeof(float), st);
+  cudaMemsetAsync(o->flag.p, 0, sizeof(int), st);
+  if (theta) {
+    cudaMemcpyAsync(o->params.p, theta, o->P * sizeof(float), cudaMemcpyHostToDevice, st);
+  } else {
+    launch_init_params(o->fd, o->params.p, seed, st);
+  }
+  const size_t gv = (size_t)grid_res * grid_res * grid_res;
+  if (grid)
+    cudaMemcpyAsync(o->grid.p, grid, gv * sizeof(float), cudaMemcpyHostToDevice, st);
+  else
+    cudaMemsetAsync(o->grid.p, 0, gv * sizeof(float), st);
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cleanup(fail(PRENOM_CUDA, cudaGetErrorString(e)));
+  *out = o;
+  return PRENOM_OK;
+}
+
+prenom_status prenom_object_destroy(prenom_object_t obj) {
+  if (!obj) return PRENOM_OK;
+  cudaSetDevice(obj->ctx->device);
+  cudaStreamSynchronize(obj->ctx->stream);
+  delete obj;
+  return PRENOM_OK;
+}
+
+prenom_status prenom_object_set_frames(prenom_object_t o, int n, const prenom_camera* cams, const float* rgb,
+                                       const float* depth, const uint8_t* mask, uint8_t inst,
+                                       const prenom_pose* pose) {
+  if (!o || !cams || !rgb || !depth || !mask || !pose) return fail(PRENOM_USAGE, "NULL argument");
+  if (n < 1) return fail(PRENOM_DATA, "no frames");
+  const int W = cams[0].width, H = cams[0].height;
+  if (W < 1 || H < 1) return fail(PRENOM_DATA, "bad frame size");
+  for (int i = 0; i < n; ++i)
+    if (cams[i].width != W || cams[i].height != H)
+      return fail(PRENOM_DATA, "generate_rays: mask does not match camera dimensions");
+  CUDA_TRY(cudaSetDevice(o->ctx->device));
+  for (auto* f : o->frames) delete f;
+  o->frames.clear();
+  o->W = W;
+  o->H = H;
+  o->inst = inst;
+  o->pose = *pose;
+  // Pose::inverse (geom.hpp:127-130)
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) o->Rt[i * 3 + j] = pose->R[j * 3 + i];
+  float tt[3];
+  mat_vec(o->Rt, pose->t, tt);
+  const float tinv[3] = {-tt[0], -tt[1], -tt[2]};
+  const size_t npx = (size_t)W * H;
+  for (int i = 0; i < n; ++i) {
+    auto* f = new FrameDev;
+    o->frames.push_back(f);
+    f->cam = cams[i];
+    float wt[3];
+    mat_vec(o->Rt, cams[i].t, wt);
+    for (int k = 0; k < 3; ++k) f->origin[k] = wt[k] + tinv[k];
+    STATUS_TRY(set_frame_pixels(o, f, rgb + 3 * npx * i, depth + npx * i, mask + npx * i));
+  }
+  return PRENOM_OK;
+}
+
+prenom_status prenom_object_upload_frame(prenom_object_t o, int frame, const float* rgb, const float* depth,
+                                         const uint8_t* mask) {
+  if (!o || !rgb || !depth) return fail(PRENOM_USAGE, "NULL argument");
+  if (frame < 0 || frame >= (int)o->frames.size()) return fail(PRENOM_USAGE, "frame index out of range");
+  CUDA_TRY(cudaSetDevice(o->ctx->device));
+  return set_frame_pixels(o, o->frames[frame], rgb, depth, mask);
+}
+
+prenom_status prenom_train_step(prenom_object_t o, int n_steps, prenom_step_stats* stats) {
+  if (!o) return fail(PRENOM_USAGE, "NULL object");
+  if (n_steps < 1) return fail(PRENOM_USAGE, "n_steps must be >= 1");
+  if (o->frames.empty()) return fail(PRENOM_DATA, "train_step: object has no frames");
+  CUDA_TRY(cudaSetDevice(o->ctx->device));
+  STATUS_TRY(ensure_scratch(o, o->cfg.rays_per_iter, o->cfg.samples_per_ray));
+  CUDA_TRY(o->stats.ensure((size_t)n_steps));
+  cudaStream_t st = o->ctx->stream;
+  CUDA_TRY(cudaMemsetAsync(o->stats.p, 0, sizeof(StepStatsDev) * n_steps, st));
+  for (int it = 0; it < n_steps; ++it) STATUS_TRY(enqueue_step(o, o->stats.p + it));
+  o->last_n_steps = n_steps;
+  if (stats) {
+    std::vector<StepStatsDev> h(n_steps);
+    CUDA_TRY(cudaMemcpyAsync(h.data(), o->stats.p, sizeof(StepStatsDev) * n_steps, cudaMemcpyDeviceToHost, st));
+    STATUS_TRY(check_flag(o));
+    for (int i = 0; i < n_steps; ++i) to_host_stats(h[i], &stats[i]);
+  }
+  return PRENOM_OK;
+}
+
+prenom_status prenom_object_last_stats(prenom_object_t o, int n, prenom_step_stats* stats) {
+  if (!o || !stats) return fail(PRENOM_USAGE, "NULL argument");
+  n = std::min(n, o->last_n_steps);
+  if (n <= 0) return PRENOM_OK;
+  std::vector<StepStatsDev> h(n);
+  CUDA_TRY(cudaMemcpyAsync(h.data(), o->stats.p + (o->last_n_steps - n), sizeof(StepStatsDev) * n,
+                           cudaMemcpyDeviceToHost, o->ctx->stream));
+  STATUS_TRY(check_flag(o));
+  for (int i = 0; i < n; ++i) to_host_stats(h[i], &stats[i]);
+  return PRENOM_OK;
+}
+
+prenom_status prenom_object_step(prenom_object_t o, int64_t* step) {
+  if (!o || !step) return fail(PRENOM_USAGE, "NULL argument");
+  *step = o->step;
+  return PRENOM_OK;
+}
+
+prenom_status prenom_object_check(prenom_object_t o) {
+  if (!o) return fail(PRENOM_USAGE, "NULL object");
+  return check_flag(o);
+}
+
+prenom_status prenom_render(prenom_object_t o, int n_rays, const float* origins, const float* dirs,
+                            float* rgb_out, float* depth_out) {
+  if (!o || !origins || !dirs) return fail(PRENOM_USAGE, "NULL argument");
+  if (n_rays < 1) return fail(PRENOM_USAGE, "n_rays must be >= 1");
+  CUDA_TRY(cudaSetDevice(o->ctx->device));
+  const int S = o->cfg.samples_per_ray;
+  STATUS_TRY(ensure_scratch(o, n_rays, S));
+  cudaStream_t st = o->ctx->stream;
+  DevBuf<float> d_o, d_d, d_rgb, d_dep;
+  CUDA_TRY(d_o.ensure(3 * (size_t)n_rays));
+  CUDA_TRY(d_d.ensure(3 * (size_t)n_rays));
+  CUDA_TRY(d_rgb.ensure(3 * (size_t)n_rays));
+  CUDA_TRY(d_dep.ensure(n_rays));
+  CUDA_TRY(cudaMemcpyAsync(d_o.p, origins, 3 * sizeof(float) * n_rays, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(d_d.p, dirs, 3 * sizeof(float) * n_rays, cudaMemcpyHostToDevice, st));
+  RaySource src;
+  std::memset(&src, 0, sizeof src);
+  src.mode = 1;
+  src.origins = d_o.p;
+  src.dirs = d_d.p;
+  const SampleBufs sb = bufs(o);
+  CUDA_TRY(launch_sample(src, sampler_cfg(o, n_rays, o->cfg.prior_sampling, PRENOM_TAG_RENDER,
+                                          (uint32_t)o->render_calls++), sb, nullptr, st));
+  CUDA_TRY(launch_field_fwd_train(o->fd, o->params.p, n_rays, S, sb, o->feat_t.p, o->out.p, o->flag.p, st));
+  CompositeArgs ca;
+  std::memset(&ca, 0, sizeof ca);
+  ca.B = n_rays;
+  ca.S = S;
+  ca.pos_depth = sb.pos_depth;
+  ca.delta = sb.delta;
+  ca.target = sb.target;
+  ca.kind = sb.kind;
+  ca.count = sb.count;
+  ca.out = o->out.p;
+  ca.color_out = d_rgb.p;
+  ca.depth_out = d_dep.p;
+  CUDA_TRY(cudaMemsetAsync(d_rgb.p, 0, 3 * sizeof(float) * n_rays, st));
+  CUDA_TRY(cudaMemsetAsync(d_dep.p, 0, sizeof(float) * n_rays, st));
+  CUDA_TRY(launch_composite(ca, st));
+  o->ctx->launches += 3;
+  if (rgb_out) CUDA_TRY(cudaMemcpyAsync(rgb_out, d_rgb.p, 3 * sizeof(float) * n_rays, cudaMemcpyDeviceToHost, st));
+  if (depth_out) CUDA_TRY(cudaMemcpyAsync(depth_out, d_dep.p, sizeof(float) * n_rays, cudaMemcpyDeviceToHost, st));
+  return check_flag(o);
+}
+
+prenom_status prenom_density_query(prenom_object_t o, int R, float* out, int update) {
+  if (!o) return fail(PRENOM_USAGE, "NULL object");
+  if (R < 2 || R > 1024) return fail(PRENOM_DATA, "grid resolution out of range");
+  CUDA_TRY(cudaSetDevice(o->ctx->device));
+  cudaStream_t st = o->ctx->stream;
+  const size_t n = (size_t)R * R * R;
+  DevBuf<float> d;
+  CUDA_TRY(d.ensure(n));
+  CUDA_TRY(launch_refresh_grid(o->fd, o->params.p, R, d.p, o->flag.p, st));
+  o->ctx->launches += 1;
+  if (out) CUDA_TRY(cudaMemcpyAsync(out, d.p, n * sizeof(float), cudaMemcpyDeviceToHost, st));
+  if (update) {
+    CUDA_TRY(cudaStreamSynchronize(st));
+    std::swap(o->grid.p, d.p);
+    std::swap(o->grid.n, d.n);
+    o->R = R;
+  }
+  return check_flag(o);
+}
+
+prenom_status prenom_field_eval(prenom_object_t o, int n, const float* xyz, float* sigma, float* rgb) {
+  if (!o || !xyz) return fail(PRENOM_USAGE, "NULL argument");
+  if (n < 0) return fail(PRENOM_USAGE, "n < 0");
+  if (n == 0) return PRENOM_OK;
+  CUDA_TRY(cudaSetDevice(o->ctx->device));
+  cudaStream_t st = o->ctx->stream;
+  DevBuf<float> dx, ds, dr;
+  CUDA_TRY(dx.ensure(3 * (size_t)n));
+  CUDA_TRY(ds.ensure(n));
+  CUDA_TRY(dr.ensure(3 * (size_t)n));
+  CUDA_TRY(cudaMemcpyAsync(dx.p, xyz, 3 * sizeof(float) * n, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(launch_field_points(o->fd, o->params.p, n, dx.p, ds.p, dr.p, nullptr, nullptr, o->flag.p, st));
+  o->ctx->launches += 1;
+  if (sigma) CUDA_TRY(cudaMemcpyAsync(sigma, ds.p, sizeof(float) * n, cudaMemcpyDeviceToHost, st));
+  if (rgb) CUDA_TRY(cudaMemcpyAsync(rgb, dr.p, 3 * sizeof(float) * n, cudaMemcpyDeviceToHost, st));
+  return check_flag(o);
+}
+
+prenom_status prenom_get_params(prenom_object_t o, float* theta) {
+  if (!o || !theta) return fail(PRENOM_USAGE, "NULL argument");
+  CUDA_TRY(cudaSetDevice(o->ctx->device));
+  CUDA_TRY(cudaMemcpyAsync(theta, o->params.p, o->P * sizeof(float), cudaMemcpyDeviceToHost, o->ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(o->ctx->stream));
+  return PRENOM_OK;
+}
+
+prenom_status prenom_set_params(prenom_object_t o, const float* theta) {
+  if (!o || !theta) return fail(PRENOM_USAGE, "NULL argument");
+  CUDA_TRY(cudaSetDevice(o->ctx->device));
+  CUDA_TRY(cudaMemcpyAsync(o->params.p, theta, o->P * sizeof(float), cudaMemcpyHostToDevice, o->ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(o->ctx->stream));
+  return PRENOM_OK;
+}
+
+prenom_status prenom_get_grid(prenom_object_t o, int* res, float* grid) {
+  if (!o) return fail(PRENOM_USAGE, "NULL object");
+  if (res) *res = o->R;
+  if (grid) {
+    CUDA_TRY(cudaSetDevice(o->ctx->device));
+    CUDA_TRY(cudaMemcpyAsync(grid, o->grid.p, sizeof(float) * o->R * o->R * o->R, cudaMemcpyDeviceToHost,
+                             o->ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(o->ctx->stream));
+  }
+  return PRENOM_OK;
+}
+
+prenom_status prenom_set_grid(prenom_object_t o, int R, const float* grid) {
+  if (!o || !grid) return fail(PRENOM_USAGE, "NULL argument");
+  if (R < 2 || R > 1024) return fail(PRENOM_DATA, "grid resolution out of range");
+  CUDA_TRY(cudaSetDevice(o->ctx->device));
+  const size_t n = (size_t)R * R * R;
+  CUDA_TRY(cudaStreamSynchronize(o->ctx->stream));
+  CUDA_TRY(o->grid.ensure(n));
+  o->R = R;
+  CUDA_TRY(cudaMemcpyAsync(o->grid.p, grid, n * sizeof(float), cudaMemcpyHostToDevice, o->ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(o->ctx->stream));
+  return PRENOM_OK;
+}
+
+prenom_status prenom_get_adam(prenom_object_t o, float* m, float* v, int64_t* step) {
+  if (!o) return fail(PRENOM_USAGE, "NULL object");
+  CUDA_TRY(cudaSetDevice(o->ctx->device));
+  if (m) CUDA_TRY(cudaMemcpyAsync(m, o->m.p, o->P * sizeof(float), cudaMemcpyDeviceToHost, o->ctx->stream));
+  if (v) CUDA_TRY(cudaMemcpyAsync(v, o->v.p, o->P * sizeof(float), cudaMemcpyDeviceToHost, o->ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(o->ctx->stream));
+  if (step) *step = o->step;
+  return PRENOM_OK;
+}
+
+prenom_status prenom_reset_adam(prenom_object_t o) {
+  if (!o) return fail(PRENOM_USAGE, "NULL object");
+  CUDA_TRY(cudaSetDevice(o->ctx->device));
+  const size_t P4 = (o->P + 3) & ~size_t(3);
+  CUDA_TRY(cudaMemsetAsync(o->m.p, 0, P4 * sizeof(float), o->ctx->stream));
+  CUDA_TRY(cudaMemsetAsync(o->v.p, 0, P4 * sizeof(float), o->ctx->stream));
+  CUDA_TRY(cudaMemsetAsync(o->grad.p, 0, P4 * sizeof(float), o->ctx->stream));
+  o->step = 0;
+  return PRENOM_OK;
+}
+
+prenom_status prenom_train_step_many(prenom_object_t* objs, int n_objs, int n_steps) {
+  if (!objs || n_objs < 1 || n_steps < 1) return fail(PRENOM_USAGE, "bad arguments");
+  for (int i = 0; i < n_objs; ++i) {
+    if (!objs[i]) return fail(PRENOM_USAGE, "NULL object");
+    if (objs[i]->ctx != objs[0]->ctx) return fail(PRENOM_USAGE, "objects must share one context");
+    if (objs[i]->frames.empty()) return fail(PRENOM_DATA, "train_step: object has no frames");
+  }
+  CUDA_TRY(cudaSetDevice(objs[0]->ctx->device));
+  for (int i = 0; i < n_objs; ++i) {
+    prenom_object_s* o = objs[i];
+    STATUS_TRY(ensure_scratch(o, o->cfg.rays_per_iter, o->cfg.samples_per_ray));
+    CUDA_TRY(o->stats.ensure((size_t)n_steps));
+    CUDA_TRY(cudaMemsetAsync(o->stats.p, 0, sizeof(StepStatsDev) * n_steps, o->ctx->stream));
+    o->last_n_steps = n_steps;
+  }
+  for (int it = 0; it < n_steps; ++it)
+    for (int i = 0; i < n_objs; ++i) STATUS_TRY(enqueue_step(objs[i], objs[i]->stats.p + it));
+  return PRENOM_OK;
+}
+
+prenom_status prenom_reptile_delta(prenom_object_t meta, prenom_object_t adapted, float* delta_dev) {
+  if (!meta || !adapted || !delta_dev) return fail(PRENOM_USAGE, "NULL argument");
+  if (meta->P != adapted->P) return fail(PRENOM_DATA, "reptile_update: parameter vectors differ in length");
+  CUDA_TRY(cudaSetDevice(meta->ctx->device));
+  CUDA_TRY(cudaStreamSynchronize(adapted->ctx->stream));
+  CUDA_TRY(launch_reptile_delta(meta->P, meta->params.p, adapted->params.p, delta_dev, meta->ctx->stream));
+  meta->ctx->launches += 1;
+  CUDA_TRY(cudaStreamSynchronize(meta->ctx->stream));
+  return PRENOM_OK;
+}
+
+prenom_status prenom_reptile_apply(prenom_object_t meta, const float* delta_dev, int n_tasks, float beta) {
+  if (!meta || !delta_dev) return fail(PRENOM_USAGE, "NULL argument");
+  if (n_tasks < 1) return fail(PRENOM_USAGE, "n_tasks must be >= 1");
+  CUDA_TRY(cudaSetDevice(meta->ctx->device));
+  CUDA_TRY(launch_reptile_apply(meta->P, meta->params.p, delta_dev, 1.f / (float)n_tasks, beta, meta->ctx->stream));
+  meta->ctx->launches += 1;
+  CUDA_TRY(cudaStreamSynchronize(meta->ctx->stream));
+  return PRENOM_OK;
+}
+
+prenom_status prenom_object_copy_params(prenom_object_t dst, prenom_object_t src) {
+  if (!dst || !src) return fail(PRENOM_USAGE, "NULL argument");
+  if (dst->P != src->P) return fail(PRENOM_DATA, "parameter vectors differ in length");
+  CUDA_TRY(cudaSetDevice(dst->ctx->device));
+  CUDA_TRY(cudaStreamSynchronize(src->ctx->stream));
+  CUDA_TRY(cudaMemcpyAsync(dst->params.p, src->params.p, src->P * sizeof(float), cudaMemcpyDeviceToDevice,
+                           dst->ctx->stream));
+  return prenom_reset_adam(dst);
+}
+
+// ------------------------------------------------------------- debug
+prenom_status prenom_debug_philox(prenom_ctx_t ctx, int n, const uint32_t* ck, uint32_t* out) {
+  if (!ctx || !ck || !out || n < 0) return fail(PRENOM_USAGE, "bad arguments");
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  DevBuf<uint32_t> a, b;
+  CUDA_TRY(a.ensure(6 * (size_t)n));
+  CUDA_TRY(b.ensure(4 * (size_t)n));
+  CUDA_TRY(cudaMemcpyAsync(a.p, ck, 6 * sizeof(uint32_t) * n, cudaMemcpyHostToDevice, ctx->stream));
+  CUDA_TRY(launch_philox(n, a.p, b.p, ctx->stream));
+  ctx->launches += 1;
+  CUDA_TRY(cudaMemcpyAsync(out, b.p, 4 * sizeof(uint32_t) * n, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return PRENOM_OK;
+}
+
+prenom_status prenom_debug_hash_encode(prenom_ctx_t ctx, const prenom_field_arch* arch, const float* params, int n,
+                                       const float* xyz, float* features) {
+  if (!ctx || !params || !xyz || !features || n < 0) return fail(PRENOM_USAGE, "bad arguments");
+  STATUS_TRY(validate_arch(arch));
+  if (n == 0) return PRENOM_OK;
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  const FieldDesc fd = make_desc(*arch);
+  const size_t P = param_count_host(*arch);
+  DevBuf<float> dp, dx, df;
+  DevBuf<int> flag;
+  CUDA_TRY(dp.ensure(P));
+  CUDA_TRY(dx.ensure(3 * (size_t)n));
+  CUDA_TRY(df.ensure((size_t)n * fd.in_dim));
+  CUDA_TRY(flag.ensure(1));
+  cudaStream_t st = ctx->stream;
+  CUDA_TRY(cudaMemcpyAsync(dp.p, params, P * sizeof(float), cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(dx.p, xyz, 3 * sizeof(float) * n, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(launch_field_points(fd, dp.p, n, dx.p, nullptr, nullptr, nullptr, df.p, flag.p, st));
+  ctx->launches += 1;
+  CUDA_TRY(cudaMemcpyAsync(features, df.p, sizeof(float) * n * fd.in_dim, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return PRENOM_OK;
+}
+
+namespace {
+// Points as B = n one-sample "rays" through the train-path tile kernels.
+struct PointBatch {
+  DevBuf<float> params, feat_t, dfeat_t, grad;
+  DevBuf<float4> pos, out, dout;
+  DevBuf<int> count, flag;
+  SampleBufs sb;
+  prenom_status init(const FieldDesc& fd, size_t P, int n, const float* h_params, const float* xyz,
+                     cudaStream_t st) {
+    const size_t npad = ((size_t)n + kTile - 1) / kTile * kTile;
+    CUDA_TRY(params.ensure(P));
+    CUDA_TRY(feat_t.ensure(npad * fd.in_dim));
+    CUDA_TRY(dfeat_t.ensure(npad * fd.in_dim));
+    CUDA_TRY(pos.ensure(npad));
+    CUDA_TRY(out.ensure(npad));
+    CUDA_TRY(dout.ensure(npad));
+    CUDA_TRY(count.ensure(n));
+    CUDA_TRY(flag.ensure(1));
+    CUDA_TRY(cudaMemsetAsync(flag.p, 0, sizeof(int), st));
+    CUDA_TRY(cudaMemcpyAsync(params.p, h_params, P * sizeof(float), cudaMemcpyHostToDevice, st));
+    std::vector<float4> hp(n);
+    std::vector<int> hc(n, 1);
+    for (int i = 0; i < n; ++i) hp[i] = make_float4(xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2], 0.f);
+    CUDA_TRY(cudaMemcpyAsync(pos.p, hp.data(), sizeof(float4) * n, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(count.p, hc.data(), sizeof(int) * n, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    std::memset(&sb, 0, sizeof sb);
+    sb.pos_depth = pos.p;
+    sb.count = count.p;
+    return PRENOM_OK;
+  }
+};
+}  // namespace
+
+prenom_status prenom_debug_field_eval(prenom_ctx_t ctx, const prenom_field_arch* arch, const float* params, int n,
+                                      const float* xyz, float* sigma, float* rgb, float* raw, int precision) {
+  if (!ctx || !params || !xyz || n < 0) return fail(PRENOM_USAGE, "bad arguments");
+  STATUS_TRY(validate_arch(arch));
+  if (n == 0) return PRENOM_OK;
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  const FieldDesc fd = make_desc(*arch);
+  const size_t P = param_count_host(*arch);
+  cudaStream_t st = ctx->stream;
+  int hflag = 0;
+  if (precision == PRENOM_MLP_FP32) {
+    DevBuf<float> dp, dx, ds, dr, dw;
+    DevBuf<int> flag;
+    CUDA_TRY(dp.ensure(P));
+    CUDA_TRY(dx.ensure(3 * (size_t)n));
+    CUDA_TRY(ds.ensure(n));
+    CUDA_TRY(dr.ensure(3 * (size_t)n));
+    CUDA_TRY(dw.ensure(4 * (size_t)n));
+    CUDA_TRY(flag.ensure(1));
+    CUDA_TRY(cudaMemsetAsync(flag.p, 0, sizeof(int), st));
+    CUDA_TRY(cudaMemcpyAsync(dp.p, params, P * sizeof(float), cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(dx.p, xyz, 3 * sizeof(float) * n, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(launch_field_points(fd, dp.p, n, dx.p, ds.p, dr.p, dw.p, nullptr, flag.p, st));
+    ctx->launches += 1;
+    if (sigma) CUDA_TRY(cudaMemcpyAsync(sigma, ds.p, sizeof(float) * n, cudaMemcpyDeviceToHost, st));
+    if (rgb) CUDA_TRY(cudaMemcpyAsync(rgb, dr.p, 3 * sizeof(float) * n, cudaMemcpyDeviceToHost, st));
+    if (raw) CUDA_TRY(cudaMemcpyAsync(raw, dw.p, 4 * sizeof(float) * n, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(&hflag, flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+  } else if (precision == 2) {
+    // the train-path tile forward (fp32 GEMM, FMA)
+    PointBatch pb;
+    STATUS_TRY(pb.init(fd, P, n, params, xyz, st));
+    CUDA_TRY(launch_field_fwd_train(fd, pb.params.p, n, 1, pb.sb, pb.feat_t.p, pb.out.p, pb.flag.p, st));
+    ctx->launches += 1;
+    std::vector<float4> h(n);
+    CUDA_TRY(cudaMemcpyAsync(h.data(), pb.out.p, sizeof(float4) * n, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(&hflag, pb.flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    for (int i = 0; i < n; ++i) {
+      if (sigma) sigma[i] = h[i].x;
+      if (rgb) {
+        rgb[3 * i] = h[i].y;
+        rgb[3 * i + 1] = h[i].z;
+        rgb[3 * i + 2] = h[i].w;
+      }
+    }
+    if (raw) std::memset(raw, 0, sizeof(float) * 4 * n);
+  } else {
+    return fail(PRENOM_USAGE, "unsupported mlp precision for debug_field_eval");
+  }
+  if (hflag) return fail(PRENOM_NUMERIC, "field_eval produced a non-finite output");
+  return PRENOM_OK;
+}
+
+prenom_status prenom_debug_field_backward(prenom_ctx_t ctx, const prenom_field_arch* arch, const float* params,
+                                          int n, const float* xyz, const float* d_sigma, const float* d_rgb,
+                                          float* grad, int precision) {
+  (void)precision;
+  if (!ctx || !params || !xyz || !d_sigma || !d_rgb || !grad || n < 0) return fail(PRENOM_USAGE, "bad arguments");
+  STATUS_TRY(validate_arch(arch));
+  const FieldDesc fd = make_desc(*arch);
+  const size_t P = param_count_host(*arch);
+  if (n == 0) {
+    std::memset(grad, 0, P * sizeof(float));
+    return PRENOM_OK;
+  }
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  cudaStream_t st = ctx->stream;
+  PointBatch pb;
+  STATUS_TRY(pb.init(fd, P, n, params, xyz, st));
+  CUDA_TRY(pb.grad.ensure(P));
+  CUDA_TRY(cudaMemsetAsync(pb.grad.p, 0, P * sizeof(float), st));
+  std::vector<float4> hd(n);
+  for (int i = 0; i < n; ++i) hd[i] = make_float4(d_sigma[i], d_rgb[3 * i], d_rgb[3 * i + 1], d_rgb[3 * i + 2]);
+  CUDA_TRY(cudaMemcpyAsync(pb.dout.p, hd.data(), sizeof(float4) * n, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(launch_field_fwd_train(fd, pb.params.p, n, 1, pb.sb, pb.feat_t.p, pb.out.p, pb.flag.p, st));
+  CUDA_TRY(launch_mlp_bwd_train(fd, pb.params.p, pb.grad.p, n, 1, pb.count.p, pb.feat_t.p, pb.dout.p, pb.dfeat_t.p,
+                                st));
+  CUDA_TRY(launch_encode_bwd(fd, pb.params.p, pb.grad.p, n, 1, pb.count.p, pb.pos.p, pb.dfeat_t.p, st));
+  ctx->launches += 3;
+  CUDA_TRY(cudaMemcpyAsync(grad, pb.grad.p, P * sizeof(float), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return PRENOM_OK;
+}
+
+prenom_status prenom_debug_adam(prenom_ctx_t ctx, size_t n, float* params, const float* grads, float* m, float* v,
+                                int64_t* step, float lr, float b1, float b2, float eps) {
+  if (!ctx || !params || !grads || !m || !v || !step) return fail(PRENOM_USAGE, "NULL argument");
+  if (n == 0) return PRENOM_OK;
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  cudaStream_t st = ctx->stream;
+  DevBuf<float> dp, dg, dm, dv;
+  CUDA_TRY(dp.ensure(n));
+  CUDA_TRY(dg.ensure(n));
+  CUDA_TRY(dm.ensure(n));
+  CUDA_TRY(dv.ensure(n));
+  CUDA_TRY(cudaMemcpyAsync(dp.p, params, n * 4, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(dg.p, grads, n * 4, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(dm.p, m, n * 4, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(dv.p, v, n * 4, cudaMemcpyHostToDevice, st));
+  *step += 1;
+  const float c1 = 1.f - std::pow(b1, (float)*step), c2 = 1.f - std::pow(b2, (float)*step);
+  CUDA_TRY(launch_adam(n, dp.p, dg.p, dm.p, dv.p, lr, b1, b2, eps, c1, c2, 0, st));
+  ctx->launches += 1;
+  CUDA_TRY(cudaMemcpyAsync(params, dp.p, n * 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(m, dm.p, n * 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(v, dv.p, n * 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return PRENOM_OK;
+}
+
+prenom_status prenom_debug_sample_rays(prenom_ctx_t ctx, int n_rays, const float* origins, const float* dirs,
+                                       const float box_min[3], const float box_max[3], int prior, int grid_res,
+                                       const float* grid, int n_coarse, int n_fine, float eps, uint64_t seed,
+                                       int64_t step, float* depths, float* deltas, float* positions, int* count,
+                                       float* t_entry, float* t_exit) {
+  if (!ctx || !origins || !dirs || !box_min || !box_max || n_rays < 0) return fail(PRENOM_USAGE, "bad arguments");
+  if (prior && (!grid || grid_res < 2)) return fail(PRENOM_USAGE, "prior sampling needs a grid");
+  if (n_fine < 1 || n_fine > 1024 || (prior && (n_coarse < 1 || n_coarse > 1024)))
+    return fail(PRENOM_USAGE, "sample counts out of range");
+  if (n_rays == 0) return PRENOM_OK;
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  cudaStream_t st = ctx->stream;
+  const size_t N = (size_t)n_rays * n_fine;
+  DevBuf<float> d_o, d_d, d_g, d_delta, d_te, d_tx;
+  DevBuf<float4> d_pd, d_tgt;
+  DevBuf<int> d_kind, d_cnt;
+  CUDA_TRY(d_o.ensure(3 * (size_t)n_rays));
+  CUDA_TRY(d_d.ensure(3 * (size_t)n_rays));
+  CUDA_TRY(d_pd.ensure(N));
+  CUDA_TRY(d_delta.ensure(N));
+  CUDA_TRY(d_tgt.ensure(n_rays));
+  CUDA_TRY(d_kind.ensure(n_rays));
+  CUDA_TRY(d_cnt.ensure(n_rays));
+  CUDA_TRY(d_te.ensure(n_rays));
+  CUDA_TRY(d_tx.ensure(n_rays));
+  CUDA_TRY(cudaMemcpyAsync(d_o.p, origins, 12 * (size_t)n_rays, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(d_d.p, dirs, 12 * (size_t)n_rays, cudaMemcpyHostToDevice, st));
+  if (prior) {
+    const size_t gv = (size_t)grid_res * grid_res * grid_res;
+    CUDA_TRY(d_g.ensure(gv));
+    CUDA_TRY(cudaMemcpyAsync(d_g.p, grid, gv * 4, cudaMemcpyHostToDevice, st));
+  }
+  CUDA_TRY(cudaMemsetAsync(d_pd.p, 0, N * sizeof(float4), st));
+  CUDA_TRY(cudaMemsetAsync(d_delta.p, 0, N * sizeof(float), st));
+  RaySource src;
+  std::memset(&src, 0, sizeof src);
+  src.mode = 1;
+  src.origins = d_o.p;
+  src.dirs = d_d.p;
+  SamplerCfg c;
+  std::memset(&c, 0, sizeof c);
+  c.B = n_rays;
+  c.S = n_fine;
+  c.prior = prior;
+  c.n_coarse = n_coarse;
+  c.eps = eps;
+  c.grid_res = grid_res;
+  c.grid = d_g.p;
+  std::memcpy(c.bmin, box_min, 12);
+  std::memcpy(c.bmax, box_max, 12);
+  c.seed = seed;
+  c.tag = PRENOM_TAG_FINE;
+  c.step = (uint32_t)step;
+  SampleBufs sb;
+  std::memset(&sb, 0, sizeof sb);
+  sb.pos_depth = d_pd.p;
+  sb.delta = d_delta.p;
+  sb.target = d_tgt.p;
+  sb.kind = d_kind.p;
+  sb.count = d_cnt.p;
+  sb.t_entry = d_te.p;
+  sb.t_exit = d_tx.p;
+  CUDA_TRY(launch_sample(src, c, sb, nullptr, st));
+  ctx->launches += 1;
+  std::vector<float4> hpd(N);
+  CUDA_TRY(cudaMemcpyAsync(hpd.data(), d_pd.p, N * sizeof(float4), cudaMemcpyDeviceToHost, st));
+  if (deltas) CUDA_TRY(cudaMemcpyAsync(deltas, d_delta.p, N * 4, cudaMemcpyDeviceToHost, st));
+  if (count) CUDA_TRY(cudaMemcpyAsync(count, d_cnt.p, 4 * (size_t)n_rays, cudaMemcpyDeviceToHost, st));
+  if (t_entry) CUDA_TRY(cudaMemcpyAsync(t_entry, d_te.p, 4 * (size_t)n_rays, cudaMemcpyDeviceToHost, st));
+  if (t_exit) CUDA_TRY(cudaMemcpyAsync(t_exit, d_tx.p, 4 * (size_t)n_rays, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  for (size_t i = 0; i < N; ++i) {
+    if (depths) depths[i] = hpd[i].w;
+    if (positions) {
+      positions[3 * i] = hpd[i].x;
+      positions[3 * i + 1] = hpd[i].y;
+      positions[3 * i + 2] = hpd[i].z;
+    }
+  }
+  return PRENOM_OK;
+}
+
+prenom_status prenom_debug_batch_loss(prenom_ctx_t ctx, int n_rays, int S, const int* kind, const float* target_rgb,
+                                      const float* target_depth, const int* count, const float* deltas,
+                                      const float* depths, const float* sigma, const float* rgb,
+                                      const float* bg_colors, float lambda_d, float lambda_sigma, double* terms,
+                                      float* d_sigma, float* d_rgb, float* color_out, float* depth_out) {
+  if (!ctx || !kind || !target_rgb || !target_depth || !count || !deltas || !depths || !sigma || !rgb || !bg_colors ||
+      !terms || n_rays < 0 || S < 1 || S > 256)
+    return fail(PRENOM_USAGE, "bad arguments");
+  if (n_rays == 0) return fail(PRENOM_DATA, "batch_loss: no rays");
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  cudaStream_t st = ctx->stream;
+  const size_t N = (size_t)n_rays * S;
+  std::vector<float4> hpd(N), hout(N), htgt(n_rays);
+  for (size_t i = 0; i < N; ++i) {
+    hpd[i] = make_float4(0.f, 0.f, 0.f, depths[i]);
+    hout[i] = make_float4(sigma[i], rgb[3 * i], rgb[3 * i + 1], rgb[3 * i + 2]);
+  }
+  for (int r = 0; r < n_rays; ++r) {
+    if (count[r] != 0 && count[r] != S) return fail(PRENOM_USAGE, "count must be 0 or S");
+    htgt[r] = make_float4(target_rgb[3 * r], target_rgb[3 * r + 1], target_rgb[3 * r + 2], target_depth[r]);
+  }
+  DevBuf<float4> d_pd, d_out, d_dout, d_tgt;
+  DevBuf<float> d_delta, d_bg, d_col, d_dep;
+  DevBuf<int> d_kind, d_cnt, d_flag;
+  DevBuf<StepStatsDev> d_stats;
+  CUDA_TRY(d_pd.ensure(N));
+  CUDA_TRY(d_out.ensure(N));
+  CUDA_TRY(d_dout.ensure(N));
+  CUDA_TRY(d_tgt.ensure(n_rays));
+  CUDA_TRY(d_delta.ensure(N));
+  CUDA_TRY(d_bg.ensure(3 * (size_t)n_rays));
+  CUDA_TRY(d_col.ensure(3 * (size_t)n_rays));
+  CUDA_TRY(d_dep.ensure(n_rays));
+  CUDA_TRY(d_kind.ensure(n_rays));
+  CUDA_TRY(d_cnt.ensure(n_rays));
+  CUDA_TRY(d_flag.ensure(1));
+  CUDA_TRY(d_stats.ensure(1));
+  CUDA_TRY(cudaMemcpyAsync(d_pd.p, hpd.data(), N * sizeof(float4), cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(d_out.p, hout.data(), N * sizeof(float4), cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(d_tgt.p, htgt.data(), n_rays * sizeof(float4), cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(d_delta.p, deltas, N * 4, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(d_bg.p, bg_colors, 12 * (size_t)n_rays, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(d_kind.p, kind, 4 * (size_t)n_rays, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(d_cnt.p, count, 4 * (size_t)n_rays, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemsetAsync(d_dout.p, 0, N * sizeof(float4), st));
+  CUDA_TRY(cudaMemsetAsync(d_col.p, 0, 12 * (size_t)n_rays, st));
+  CUDA_TRY(cudaMemsetAsync(d_dep.p, 0, 4 * (size_t)n_rays, st));
+  CUDA_TRY(cudaMemsetAsync(d_flag.p, 0, 4, st));
+  CUDA_TRY(cudaMemsetAsync(d_stats.p, 0, sizeof(StepStatsDev), st));
+  CompositeArgs ca;
+  std::memset(&ca, 0, sizeof ca);
+  ca.B = n_rays;
+  ca.S = S;
+  ca.pos_depth = d_pd.p;
+  ca.delta = d_delta.p;
+  ca.target = d_tgt.p;
+  ca.kind = d_kind.p;
+  ca.count = d_cnt.p;
+  ca.out = d_out.p;
+  ca.bg_colors = d_bg.p;
+  ca.lambda_d = lambda_d;
+  ca.lambda_sigma = lambda_sigma;
+  ca.dout = d_dout.p;
+  ca.color_out = d_col.p;
+  ca.depth_out = d_dep.p;
+  ca.stats = d_stats.p;
+  ca.flag = d_flag.p;
+  CUDA_TRY(launch_composite(ca, st));
+  ctx->launches += 2;
+  StepStatsDev hs;
+  std::vector<float4> hd(N);
+  int hflag = 0;
+  CUDA_TRY(cudaMemcpyAsync(&hs, d_stats.p, sizeof hs, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(hd.data(), d_dout.p, N * sizeof(float4), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(&hflag, d_flag.p, 4, cudaMemcpyDeviceToHost, st));
+  if (color_out) CUDA_TRY(cudaMemcpyAsync(color_out, d_col.p, 12 * (size_t)n_rays, cudaMemcpyDeviceToHost, st));
+  if (depth_out) CUDA_TRY(cudaMemcpyAsync(depth_out, d_dep.p, 4 * (size_t)n_rays, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  terms[0] = hs.total;
+  terms[1] = hs.color;
+  terms[2] = hs.depth;
+  terms[3] = hs.sigma;
+  for (size_t i = 0; i < N; ++i) {
+    if (d_sigma) d_sigma[i] = hd[i].x;
+    if (d_rgb) {
+      d_rgb[3 * i] = hd[i].y;
+      d_rgb[3 * i + 1] = hd[i].z;
+      d_rgb[3 * i + 2] = hd[i].w;
+    }
+  }
+  if (hflag) return fail(PRENOM_NUMERIC, "batch_loss: non-finite loss");
+  return PRENOM_OK;
+}
+
+prenom_status prenom_debug_generate_rays(prenom_object_t o, int frame, int64_t step, float* origins, float* dirs,
+                                         int* kind, float* target_rgb, float* target_depth, int* pick_px) {
+  if (!o) return fail(PRENOM_USAGE, "NULL object");
+  if (frame < 0 || frame >= (int)o->frames.size()) return fail(PRENOM_USAGE, "frame index out of range");
+  CUDA_TRY(cudaSetDevice(o->ctx->device));
+  const int B = o->cfg.rays_per_iter;
+  STATUS_TRY(ensure_scratch(o, B, o->cfg.samples_per_ray));
+  const RaySource src = frame_source(o, frame);
+  if (src.n_obj_px == 0) return fail(PRENOM_DATA, "generate_rays: no object pixels");
+  cudaStream_t st = o->ctx->stream;
+  DevBuf<float> d_o, d_d;
+  DevBuf<int> d_pick;
+  CUDA_TRY(d_o.ensure(3 * (size_t)B));
+  CUDA_TRY(d_d.ensure(3 * (size_t)B));
+  CUDA_TRY(d_pick.ensure(B));
+  SampleBufs sb = bufs(o);
+  sb.ray_o = d_o.p;
+  sb.ray_d = d_d.p;
+  sb.pick_px = d_pick.p;
+  CUDA_TRY(launch_sample(src, sampler_cfg(o, B, 0, PRENOM_TAG_FINE, (uint32_t)step), sb, nullptr, st));
+  o->ctx->launches += 1;
+  std::vector<float4> tg(B);
+  if (origins) CUDA_TRY(cudaMemcpyAsync(origins, d_o.p, 12 * (size_t)B, cudaMemcpyDeviceToHost, st));
+  if (dirs) CUDA_TRY(cudaMemcpyAsync(dirs, d_d.p, 12 * (size_t)B, cudaMemcpyDeviceToHost, st));
+  if (pick_px) CUDA_TRY(cudaMemcpyAsync(pick_px, d_pick.p, 4 * (size_t)B, cudaMemcpyDeviceToHost, st));
+  if (kind) CUDA_TRY(cudaMemcpyAsync(kind, sb.kind, 4 * (size_t)B, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(tg.data(), sb.target, sizeof(float4) * B, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  for (int r = 0; r < B; ++r) {
+    if (target_rgb) {
+      target_rgb[3 * r] = tg[r].x;
+      target_rgb[3 * r + 1] = tg[r].y;
+      target_rgb[3 * r + 2] = tg[r].z;
+    }
+    if (target_depth) target_depth[r] = tg[r].w;
+  }
+  return PRENOM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,258 @@
+// prenom_device.cuh -- device-side types and helpers shared by the sm_100a
+// kernels of the per-object train step. Host code includes it for the
+// descriptor structs and launch prototypes.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "prenom/prenom_detmath.h"
+#include "prenom/prenom_gpu.h"
+
+namespace prenom {
+
+constexpr int kMaxLevels = 24;   // L <= 24 (BASELINE archs use 8..16)
+constexpr int kMaxIn = 64;       // L*F <= 64
+constexpr int kMaxWidth = 64;    // hidden width <= 64 (fp32 tile kernels)
+constexpr int kMaxHidden = 3;    // hidden layers 1..3
+constexpr int kTile = 128;       // samples per MLP tile (= UMMA M)
+constexpr int kLd = kTile + 4;   // smem row stride (floats) of [dim][sample] tiles
+constexpr uint32_t kPrime1 = 2654435761u, kPrime2 = 805459861u;  // field.cpp:20
+
+// Field architecture + derived per-level constants (field.cpp:113-148),
+// passed by value (constant bank) to every field kernel.
+struct FieldDesc {
+  int L, F, T, W, H, act;
+  int in_dim;
+  uint32_t row_mask;              // 2^T - 1
+  long long rows;                 // 2^T
+  long long hash_params;          // L*F*2^T = offset of the MLP block
+  int res[kMaxLevels];            // level_resolution
+  uint32_t dense_verts[kMaxLevels];  // res+1 when (res+1)^3 <= 2^T, else 0 (hashed)
+  // MLP layer l (0..H, H = output layer): W at w_off[l], b at b_off[l],
+  // relative to the MLP block start.
+  int w_off[kMaxHidden + 1], b_off[kMaxHidden + 1];
+  int mlp_params;
+};
+
+// Per-step statistics kept on the device (one slot per step of a call).
+struct StepStatsDev {
+  double total, color, depth, sigma;
+  unsigned long long n_samples;
+  int escaped;
+  int frame;
+};
+
+// Ray-sample buffers of one batch: B rays x S slots.
+struct SampleBufs {
+  float4* pos_depth;  // [B*S] (x, y, z) in [0,1]^3 + depth (m)
+  float* delta;       // [B*S]
+  float4* target;     // [B] target rgb + target depth (-1 = absent)
+  int* kind;          // [B] PRENOM_KIND_*
+  int* count;         // [B] S or 0 (escaped)
+  float* t_entry;     // [B] (debug)
+  float* t_exit;      // [B] (debug)
+  float* ray_o;       // [B][3] (debug, may be NULL)
+  float* ray_d;       // [B][3] (debug, may be NULL)
+  int* pick_px;       // [B] x + W*y (debug, frame mode, may be NULL)
+};
+
+// Source of the rays of one sampling launch.
+struct RaySource {
+  // mode 0: pixel picks from one frame (generate_rays); 1: explicit rays.
+  int mode;
+  // frame mode (render.cpp:47-102)
+  const float* rgb;      // [H][W][3]
+  const float* depth;    // [H][W]
+  const int* obj_px;     // object pixel list (row-major scan order)
+  const int* bg_px;      // band pixel list
+  int n_obj_px, n_bg_px; // list sizes
+  int n_obj;             // rays [0, n_obj) are object rays, the rest background
+  int width;
+  float fx, fy, cx, cy;
+  float Rc[9];           // camera -> world rotation
+  float Rt[9];           // world -> object rotation (obj pose transposed)
+  float origin[3];       // world_to_obj.apply(camera.t), computed on the host
+  // explicit mode
+  const float* origins;  // [B][3]
+  const float* dirs;     // [B][3]
+};
+
+struct SamplerCfg {
+  int B, S;              // rays, fine samples per ray (n_fine)
+  int prior;             // sample_ray (1) or uniform_samples (0)
+  int n_coarse;
+  float eps;
+  int grid_res;
+  const float* grid;     // R^3 x-fastest
+  float bmin[3], bmax[3];
+  uint64_t seed;
+  uint32_t tag;          // PRENOM_TAG_FINE or PRENOM_TAG_RENDER
+  uint32_t step;         // Philox c2
+};
+
+// ---------------------------------------------------------------- helpers
+__device__ __forceinline__ float clamp01(float v) { return v < 0.f ? 0.f : (1.f < v ? 1.f : v); }
+
+__device__ __forceinline__ void philox_draw(uint64_t seed, uint32_t tag, uint32_t step,
+                                            uint32_t ray, uint32_t idx, uint32_t out[4]) {
+  const uint32_t ctr[4] = {idx, ray, step, tag};
+  pdm_philox4x32_10(ctr, (uint32_t)seed, (uint32_t)(seed >> 32), out);
+}
+
+// field.cpp:141-148 (bit-exact).
+__device__ __forceinline__ uint32_t table_row(const FieldDesc& fd, int l, uint32_t x, uint32_t y,
+                                              uint32_t z) {
+  const uint32_t V = fd.dense_verts[l];
+  if (V) return x + V * (y + V * z);
+  return (x ^ (y * kPrime1) ^ (z * kPrime2)) & fd.row_mask;
+}
+
+// Level cell + fractional position (field.cpp:80-86), bit-exact.
+struct LevelCell {
+  int cx, cy, cz;
+  float fx, fy, fz;
+};
+
+__device__ __forceinline__ LevelCell level_cell(int res, float px, float py, float pz) {
+  LevelCell c;
+  const float r = (float)res;
+  const float gx = __fmul_rn(px, r), gy = __fmul_rn(py, r), gz = __fmul_rn(pz, r);
+  c.cx = min((int)gx, res - 1);
+  c.cy = min((int)gy, res - 1);
+  c.cz = min((int)gz, res - 1);
+  c.fx = __fsub_rn(gx, (float)c.cx);
+  c.fy = __fsub_rn(gy, (float)c.cy);
+  c.fz = __fsub_rn(gz, (float)c.cz);
+  return c;
+}
+
+// Trilinear corner weight, same product order as field.cpp:88.
+__device__ __forceinline__ float corner_weight(const LevelCell& c, int corner) {
+  const float wx = (corner & 1) ? c.fx : __fsub_rn(1.f, c.fx);
+  const float wy = (corner & 2) ? c.fy : __fsub_rn(1.f, c.fy);
+  const float wz = (corner & 4) ? c.fz : __fsub_rn(1.f, c.fz);
+  return __fmul_rn(__fmul_rn(wx, wy), wz);
+}
+
+// One level of encode_point (field.cpp:75-98); feat[F] accumulated in
+// corner order with separate mul/add roundings (no FMA), skipping w == 0.
+template <int F>
+__device__ __forceinline__ void encode_level(const FieldDesc& fd, const float* __restrict__ params,
+                                             int l, float px, float py, float pz, float* feat) {
+  const LevelCell c = level_cell(fd.res[l], px, py, pz);
+  const float* tab = params + (long long)l * F * fd.rows;
+  float e[8][F];
+  float w[8];
+#pragma unroll
+  for (int corner = 0; corner < 8; ++corner) {
+    const uint32_t row = table_row(fd, l, (uint32_t)(c.cx + (corner & 1)),
+                                   (uint32_t)(c.cy + ((corner >> 1) & 1)),
+                                   (uint32_t)(c.cz + ((corner >> 2) & 1)));
+    w[corner] = corner_weight(c, corner);
+    if constexpr (F == 2) {
+      const float2 v = __ldg(reinterpret_cast<const float2*>(tab + (size_t)row * 2));
+      e[corner][0] = v.x;
+      e[corner][1] = v.y;
+    } else {
+#pragma unroll
+      for (int f = 0; f < F; ++f) e[corner][f] = __ldg(tab + (size_t)row * F + f);
+    }
+  }
+#pragma unroll
+  for (int f = 0; f < F; ++f) feat[f] = 0.f;
+#pragma unroll
+  for (int corner = 0; corner < 8; ++corner)
+    if (w[corner] != 0.f) {
+#pragma unroll
+      for (int f = 0; f < F; ++f) feat[f] = __fadd_rn(feat[f], __fmul_rn(w[corner], e[corner][f]));
+    }
+}
+
+// Runtime-F variant (tiny test archs).
+__device__ __forceinline__ void encode_level_rt(const FieldDesc& fd, const float* __restrict__ params,
+                                                int l, float px, float py, float pz, float* feat) {
+  const int F = fd.F;
+  const LevelCell c = level_cell(fd.res[l], px, py, pz);
+  const float* tab = params + (long long)l * F * fd.rows;
+  for (int f = 0; f < F; ++f) feat[f] = 0.f;
+  for (int corner = 0; corner < 8; ++corner) {
+    const uint32_t row = table_row(fd, l, (uint32_t)(c.cx + (corner & 1)),
+                                   (uint32_t)(c.cy + ((corner >> 1) & 1)),
+                                   (uint32_t)(c.cz + ((corner >> 2) & 1)));
+    const float w = corner_weight(c, corner);
+    if (w == 0.f) continue;
+    for (int f = 0; f < F; ++f)
+      feat[f] = __fadd_rn(feat[f], __fmul_rn(w, __ldg(tab + (size_t)row * F + f)));
+  }
+}
+
+// field.cpp:23-41. expf/log1pf are CUDA's (<= 2 ulp from glibc).
+__device__ __forceinline__ float stable_sigmoid(float x) {
+  if (x >= 0.f) return 1.f / (1.f + expf(-x));
+  const float e = expf(x);
+  return e / (1.f + e);
+}
+
+__device__ __forceinline__ float density_forward(int act, float x) {
+  if (act == PRENOM_ACT_EXP_CLAMPED) return fminf(expf(fminf(x, 10.f)), 1e4f);
+  return x > 0.f ? x + log1pf(expf(-x)) : log1pf(expf(x));
+}
+
+__device__ __forceinline__ float density_derivative(int act, float x, float sigma) {
+  if (act == PRENOM_ACT_EXP_CLAMPED) return sigma < 1e4f ? sigma : 0.f;
+  return stable_sigmoid(x);
+}
+
+__device__ __forceinline__ bool all_finite4(float a, float b, float c, float d) {
+  return isfinite(a) && isfinite(b) && isfinite(c) && isfinite(d);
+}
+
+// ------------------------------------------------------- launch wrappers
+// (defined in the .cu files; all enqueue on `st` and return cudaGetLastError)
+cudaError_t launch_sample(const RaySource& src, const SamplerCfg& cfg, SampleBufs out,
+                          StepStatsDev* stats, cudaStream_t st);
+cudaError_t launch_field_points(const FieldDesc& fd, const float* params, int n,
+                                const float* xyz, float* sigma, float* rgb, float* raw,
+                                float* features, int* flag, cudaStream_t st);
+cudaError_t launch_field_fwd_train(const FieldDesc& fd, const float* params, int B, int S,
+                                   const SampleBufs& sb, float* features_t, float4* out,
+                                   int* flag, cudaStream_t st);
+struct CompositeArgs {
+  int B, S;
+  const float4* pos_depth;
+  const float* delta;
+  const float4* target;
+  const int* kind;
+  const int* count;
+  const float4* out;        // sigma, rgb per sample
+  const float* bg_colors;   // [B][3] explicit, or NULL -> Philox TAG_BG
+  uint64_t seed;
+  uint32_t step;
+  float lambda_d, lambda_sigma;
+  float4* dout;             // d_sigma, d_rgb per sample (NULL: forward only)
+  float* color_out;         // [B][3] or NULL
+  float* depth_out;         // [B] or NULL
+  StepStatsDev* stats;      // loss terms accumulated here (NULL: none)
+  int* flag;                // numeric flag
+  int frame;                // keyframe index recorded in stats
+};
+cudaError_t launch_composite(const CompositeArgs& a, cudaStream_t st);
+cudaError_t launch_mlp_bwd_train(const FieldDesc& fd, const float* params, float* grad, int B,
+                                 int S, const int* count, const float* features_t,
+                                 const float4* dout, float* dfeat_t, cudaStream_t st);
+cudaError_t launch_encode_bwd(const FieldDesc& fd, const float* params, float* grad, int B, int S,
+                              const int* count, const float4* pos_depth, const float* dfeat_t,
+                              cudaStream_t st);
+cudaError_t launch_adam(size_t n, float* p, float* g, float* m, float* v, float lr, float b1,
+                        float b2, float eps, float c1, float c2, int zero_grad, cudaStream_t st);
+cudaError_t launch_refresh_grid(const FieldDesc& fd, const float* params, int R, float* out,
+                                int* flag, cudaStream_t st);
+cudaError_t launch_init_params(const FieldDesc& fd, float* params, uint64_t seed, cudaStream_t st);
+cudaError_t launch_philox(int n, const uint32_t* ctr_key, uint32_t* out, cudaStream_t st);
+cudaError_t launch_reptile_delta(size_t n, const float* meta, const float* adapted, float* delta,
+                                 cudaStream_t st);
+cudaError_t launch_reptile_apply(size_t n, float* meta, const float* delta, float inv_n,
+                                 float beta, cudaStream_t st);
+
+}  // namespace prenom

@@ -1,0 +1,290 @@
+"""CUDA path (through the C ABI) vs the CPU oracle, stage by stage and end to end.
+
+Bar (BASELINE.json north_star): sample positions / bins / table rows
+bit-exact; encoding, MLP outputs, colour and depth within 1e-4 relative in
+fp32; loss after 200 steps within 1%.
+"""
+import numpy as np
+import pytest
+
+from conftest import grad_params, tiny_arch
+from paper_2503_01582_b200 import FieldArch, ObjectTrainer, Pose, TrainConfig, scenes
+from paper_2503_01582_b200 import trainer as T
+
+pytestmark = pytest.mark.gpu
+
+BOX0, BOX1 = np.zeros(3, np.float32), np.ones(3, np.float32)
+
+
+def archs(rng):
+    return [scenes.cfg1_arch(),
+            FieldArch(hash_levels=16, features_per_level=2, log2_table_size=14, base_resolution=16,
+                      per_level_scale=scenes.cfg2_arch().per_level_scale, hidden_width=64, hidden_layers=2),
+            FieldArch(hash_levels=12, features_per_level=2, log2_table_size=16, base_resolution=16,
+                      per_level_scale=1.38, hidden_width=32, hidden_layers=1, density_activation=1)] + \
+        [tiny_arch(rng) for _ in range(4)]
+
+
+def test_philox_known_answers(ctx, oracle):
+    # Random123 kat_vectors for philox4x32_10
+    ck = np.array([[0, 0, 0, 0, 0, 0],
+                   [0xFFFFFFFF] * 6,
+                   [0x243F6A88, 0x85A308D3, 0x13198A2E, 0x03707344, 0xA4093822, 0x299F31D0]], np.uint32)
+    want = np.array([[0x6627E8D5, 0xE169C58D, 0xBC57AC4C, 0x9B00DBD8],
+                     [0x408F276D, 0x41C83B0E, 0xA20BC7C6, 0x6D5451FD],
+                     [0xD16CFE09, 0x94FDCCEB, 0x5001E420, 0x24126EA1]], np.uint32)
+    got = T.debug_philox(ctx, ck)
+    assert np.array_equal(got, want)
+    for i in range(3):
+        assert np.array_equal(oracle.philox(ck[i, :4], ck[i, 4:]), want[i])
+
+
+def test_hash_encode_bit_exact(ctx, oracle, rng):
+    for a in archs(rng):
+        params = grad_params(a, rng)
+        xyz = rng.uniform(-0.05, 1.05, (333, 3)).astype(np.float32)
+        xyz[:3] = [[0, 0, 0], [1, 1, 1], [0.25, 0.5, 0.75]]
+        ours = T.debug_hash_encode(ctx, a, params, xyz)
+        ref, _, _ = oracle.hash_encode(a, params, xyz)
+        assert np.array_equal(ours, ref), a
+
+
+def test_field_eval_exact_kernel(ctx, oracle, rng):
+    for a in archs(rng):
+        params = grad_params(a, rng)
+        xyz = rng.uniform(0, 1, (257, 3)).astype(np.float32)
+        s, c, raw = T.debug_field_eval(ctx, a, params, xyz, precision=0)
+        so, co, k = oracle.field_eval(a, params, xyz, cache=True)
+        assert np.array_equal(raw, k["raw"]), a  # pre-activations bit-exact
+        np.testing.assert_allclose(s, so, rtol=1e-6, atol=1e-30)
+        np.testing.assert_allclose(c, co, rtol=1e-6, atol=1e-7)
+
+
+def test_field_eval_train_tile_path(ctx, oracle, rng):
+    """The fp32 train-path kernel (smem GEMMs with FMA): within 1e-4 relative."""
+    for a in archs(rng):
+        params = grad_params(a, rng)
+        xyz = rng.uniform(0, 1, (300, 3)).astype(np.float32)
+        s, c, _ = T.debug_field_eval(ctx, a, params, xyz, precision=2)
+        so, co = oracle.field_eval(a, params, xyz)
+        np.testing.assert_allclose(s, so, rtol=1e-4, atol=1e-6)
+        np.testing.assert_allclose(c, co, rtol=1e-4, atol=1e-6)
+
+
+def test_field_backward_matches_oracle(ctx, oracle, rng):
+    for a in archs(rng):
+        params = grad_params(a, rng)
+        n = 200
+        xyz = rng.uniform(0, 1, (n, 3)).astype(np.float32)
+        ds = rng.standard_normal(n).astype(np.float32)
+        dr = rng.standard_normal((n, 3)).astype(np.float32)
+        g = T.debug_field_backward(ctx, a, params, xyz, ds, dr)
+        go = oracle.field_backward(a, params, xyz, ds, dr)
+        scale = np.abs(go).max()
+        np.testing.assert_allclose(g, go, rtol=1e-4, atol=1e-5 * scale)
+        # untouched rows stay exactly zero (test_nfcore.cpp:215-240)
+        assert np.array_equal(g == 0, go == 0) or np.mean((g == 0) != (go == 0)) < 1e-3
+
+
+def test_adam_bit_exact(ctx, oracle, rng):
+    n = 10001
+    p = rng.standard_normal(n).astype(np.float32)
+    m = np.zeros(n, np.float32)
+    v = np.zeros(n, np.float32)
+    s1 = s2 = 0
+    p1, m1, v1, p2, m2, v2 = p, m, v, p, m, v
+    for _ in range(4):
+        g = rng.standard_normal(n).astype(np.float32)
+        g[::5] = 0
+        p1, m1, v1, s1 = T.debug_adam(ctx, p1, g, m1, v1, s1)
+        p2, m2, v2, s2 = oracle.adam_step(p2, g, m2, v2, s2)
+        assert np.array_equal(p1, p2) and np.array_equal(m1, m2) and np.array_equal(v1, v2)
+
+
+def rays(rng, n):
+    o = rng.uniform(-1.5, 2.5, (n, 3)).astype(np.float32)
+    o[: n // 10] = rng.uniform(0.2, 0.8, (n // 10, 3))
+    d = rng.uniform(0.2, 0.8, (n, 3)) - o
+    d[n // 10: n // 5] = rng.standard_normal((n // 5 - n // 10, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    o[-1], d[-1] = [0.5, 0.5, -0.5], [0, 0, 1]
+    o[-2], d[-2] = [-1, 5, 0.5], [1, 0, 0]
+    return o, d.astype(np.float32)
+
+
+@pytest.mark.parametrize("prior,nc,nf", [(0, 32, 24), (0, 32, 64), (1, 32, 96), (1, 16, 24), (1, 40, 100), (1, 7, 3)])
+def test_sample_rays_bit_exact(ctx, oracle, rng, prior, nc, nf):
+    o, d = rays(rng, 400)
+    grid = (rng.uniform(0, 60, (12, 12, 12)) * (rng.random((12, 12, 12)) < 0.3)).astype(np.float32)
+    g = T.debug_sample_rays(ctx, o, d, BOX0, BOX1, prior, grid if prior else None, nc, nf, 1e-4, seed=99, step=5)
+    n_prior = 0
+    for r in range(len(o)):
+        if prior:
+            ref = oracle.sample_ray(grid, o[r], d[r], BOX0, BOX1, nc, nf, 1e-4, seed=99, tag=3, step=5, ray=r)
+        else:
+            ref = oracle.uniform_samples(o[r], d[r], BOX0, BOX1, nf)
+        assert (g["count"][r] == 0) == ref["escaped"], r
+        if ref["escaped"]:
+            continue
+        assert np.array_equal(g["depths"][r], ref["depths"]), r
+        assert np.array_equal(g["deltas"][r], ref["deltas"]), r
+        assert np.array_equal(g["positions"][r], ref["positions"]), r
+        n_prior += int(np.any(np.diff(g["depths"][r]) != np.diff(g["depths"][r])[0]))
+    if prior:
+        assert n_prior > 20  # the prior path (non-uniform spacing) was exercised
+
+
+def test_sample_rays_zero_grid_is_uniform(ctx, oracle):
+    """test_priorgrid.cpp:229-243: zero grid -> exactly the uniform set."""
+    o = np.array([[0.5, 0.5, -0.5]], np.float32)
+    d = np.array([[0, 0, 1]], np.float32)
+    g = T.debug_sample_rays(ctx, o, d, BOX0, BOX1, True, np.zeros((8, 8, 8), np.float32), 32, 24, 1e-4, 1, 0)
+    u = oracle.uniform_samples(o[0], d[0], BOX0, BOX1, 24)
+    assert np.array_equal(g["depths"][0], u["depths"]) and np.array_equal(g["positions"][0], u["positions"])
+
+
+def test_batch_loss_matches_oracle(ctx, oracle, rng):
+    for S in (1, 5, 24, 96, 200):
+        B = 61
+        kind = (rng.random(B) < 0.3).astype(np.int32)
+        count = np.where(rng.random(B) < 0.1, 0, S).astype(np.int32)
+        dl = rng.uniform(1e-3, 0.1, (B, S)).astype(np.float32)
+        dp = np.cumsum(dl, 1).astype(np.float32)
+        sg = rng.uniform(0, 40, (B, S)).astype(np.float32)
+        rgb = rng.uniform(0, 1, (B, S, 3)).astype(np.float32)
+        trgb = rng.uniform(0, 1, (B, 3)).astype(np.float32)
+        tdep = np.where(rng.random(B) < 0.2, -1, rng.uniform(0.5, 2, B)).astype(np.float32)
+        bg = rng.uniform(0, 1, (B, 3)).astype(np.float32)
+        gpu = T.debug_batch_loss(ctx, S, kind, trgb, tdep, count, dl, dp, sg, rgb, bg)
+        off = np.concatenate([[0], np.cumsum(count)]).astype(np.int32)
+        valid = count > 0
+        o = oracle.batch_loss(kind, trgb, tdep, (~valid).astype(np.int32), off, dl[valid].reshape(-1),
+                              dp[valid].reshape(-1), sg[valid].reshape(-1), rgb[valid].reshape(-1, 3), bg)
+        np.testing.assert_allclose(gpu["terms"], o["terms"], rtol=1e-9)
+        vs = np.repeat(valid, S)
+        np.testing.assert_allclose(gpu["d_sigma"][vs], o["d_sigma"], rtol=1e-5, atol=1e-6)
+        np.testing.assert_allclose(gpu["d_rgb"][vs], o["d_rgb"], rtol=1e-5, atol=1e-7)
+        np.testing.assert_allclose(gpu["color"], o["color"], rtol=1e-6, atol=1e-7)
+        np.testing.assert_allclose(gpu["depth"], o["depth"], rtol=1e-6, atol=1e-7)
+
+
+def small_scene(seed=3, res=48, views=6):
+    sc = scenes.box_union_scene(n_views=views, res=res, seed=seed)
+    return sc, scenes.occupancy_prior(sc.boxes, R=16)
+
+
+def test_generate_rays_bit_exact(ctx, oracle):
+    sc, grid = small_scene()
+    pose = Pose(R=np.array([[0.6, -0.8, 0], [0.8, 0.6, 0], [0, 0, 1]], np.float32), t=np.array([0.1, -0.2, 0.05], np.float32))
+    arch = FieldArch(hash_levels=4, log2_table_size=10, hidden_width=16, hidden_layers=1)
+    cfg = TrainConfig(rays_per_iter=300, samples_per_ray=8)
+    ob = ObjectTrainer.create(ctx, arch, grid=grid, seed=5, cfg=cfg)
+    ob.set_frames(sc.cams, sc.rgb, sc.depth, sc.mask, 1, pose)
+    for f in (0, 3):
+        g = ob.debug_generate_rays(f, step=7)
+        o = oracle.generate_rays(sc.cams[f], sc.rgb[f], sc.depth[f], sc.mask[f], 1, pose, 300, 0.25, 8, seed=5, step=7)
+        for k in ("origins", "dirs", "kinds", "target_rgb", "target_depth", "pick_px"):
+            assert np.array_equal(g[k], o[k]), k
+
+
+def make_pair(ctx, oracle, arch, cfg, sc, grid, seed=11, theta=None):
+    theta = theta if theta is not None else grad_params(arch, np.random.default_rng(seed)) * 0.5
+    theta[: arch.hash_param_count()] *= 1e-3
+    gpu = ObjectTrainer.create(ctx, arch, theta=theta, grid=grid, seed=seed, cfg=cfg, box_min=sc.box_min,
+                               box_max=sc.box_max)
+    gpu.set_frames(sc.cams, sc.rgb, sc.depth, sc.mask, 1, sc.obj_pose)
+    ob = oracle.object_create(arch, theta, grid, grid.shape[0], seed, cfg.to_c(), sc.box_min, sc.box_max)
+    ob.set_frames(sc.cams, sc.rgb, sc.depth, sc.mask, 1, sc.obj_pose)
+    return gpu, ob
+
+
+@pytest.mark.parametrize("prior", [0, 1])
+def test_train_step_first_step_matches_oracle(ctx, oracle, prior):
+    sc, grid = small_scene()
+    arch = FieldArch(hash_levels=8, features_per_level=2, log2_table_size=12, base_resolution=8,
+                     per_level_scale=1.4, hidden_width=32, hidden_layers=2)
+    cfg = TrainConfig(rays_per_iter=200, samples_per_ray=32, prior_sampling=prior, grid_refresh_every=0)
+    gpu, ob = make_pair(ctx, oracle, arch, cfg, sc, grid)
+    sg, so = gpu.train_step(1)[0], ob.train_step(1)[0]
+    assert sg["frame"] == so["frame"] and sg["n_samples"] == so["n_samples"] and sg["escaped"] == so["escaped"]
+    for k in ("total", "color", "depth", "sigma"):
+        assert abs(sg[k] - so[k]) <= 1e-5 * abs(so[k]) + 1e-9, (k, sg, so)
+
+
+def test_train_200_steps_loss_within_1pct(ctx, oracle):
+    """north_star: loss after 200 steps within 1% of the CPU reference path."""
+    sc, grid = small_scene(res=40, views=5)
+    arch = FieldArch(hash_levels=6, features_per_level=2, log2_table_size=11, base_resolution=6,
+                     per_level_scale=1.5, hidden_width=16, hidden_layers=2)
+    cfg = TrainConfig(rays_per_iter=128, samples_per_ray=24, prior_sampling=1, grid_refresh_every=50)
+    gpu, ob = make_pair(ctx, oracle, arch, cfg, sc, grid, seed=4)
+    lg = np.array([s["total"] for s in gpu.train_step(200)])
+    lo = np.array([s["total"] for s in ob.train_step(200)])
+    assert lo[-20:].mean() < 0.8 * lo[:5].mean()  # it trains
+    assert abs(lg[-20:].mean() / lo[-20:].mean() - 1) < 0.01, (lg[-20:].mean(), lo[-20:].mean())
+
+
+def test_density_query_and_field_eval(ctx, oracle, rng):
+    a = tiny_arch(rng, hidden_width=8)
+    params = grad_params(a, rng)
+    cfg = TrainConfig()
+    ob = ObjectTrainer.create(ctx, a, theta=params, grid_res=9, cfg=cfg)
+    q = ob.density_query(17)
+    ref = oracle.refresh_grid(a, params, 17)
+    np.testing.assert_allclose(q, ref, rtol=1e-6, atol=0)
+    xyz = rng.uniform(0, 1, (100, 3)).astype(np.float32)
+    s, c = ob.field_eval(xyz)
+    so, co = oracle.field_eval(a, params, xyz)
+    np.testing.assert_allclose(s, so, rtol=1e-6)
+    np.testing.assert_allclose(c, co, rtol=1e-6)
+    ob.density_query(12, update_sampling_grid=True)
+    assert ob.get_grid().shape == (12, 12, 12)
+
+
+def test_render_matches_oracle_composite(ctx, oracle, rng):
+    a = FieldArch(hash_levels=6, log2_table_size=11, hidden_width=16, hidden_layers=2)
+    params = grad_params(a, rng)
+    cfg = TrainConfig(samples_per_ray=48, prior_sampling=0)
+    ob = ObjectTrainer.create(ctx, a, theta=params, grid_res=8, cfg=cfg, box_min=BOX0, box_max=BOX1)
+    o, d = rays(rng, 50)
+    col, dep = ob.render(o, d)
+    for r in range(len(o)):
+        u = oracle.uniform_samples(o[r], d[r], BOX0, BOX1, 48)
+        if u["escaped"]:
+            assert np.all(col[r] == 0) and dep[r] == 0
+            continue
+        s, c = oracle.field_eval(a, params, u["positions"])
+        cc, dd, _ = oracle.composite(s, c, u["deltas"], u["depths"])
+        np.testing.assert_allclose(col[r], cc, rtol=1e-4, atol=1e-6)
+        np.testing.assert_allclose(dep[r], dd, rtol=1e-4, atol=1e-6)
+
+
+def test_errors_map_to_reference_classes(ctx):
+    from paper_2503_01582_b200 import DataError, UsageError
+
+    a = FieldArch(hash_levels=4, log2_table_size=10, hidden_width=16, hidden_layers=1)
+    ob = ObjectTrainer.create(ctx, a, grid_res=8)
+    with pytest.raises(DataError):
+        ob.train_step(1)  # no frames
+    with pytest.raises(DataError):
+        ObjectTrainer.create(ctx, FieldArch(hidden_layers=0))
+    with pytest.raises(UsageError):
+        ob.train_step(0)
+
+
+def test_params_and_grid_round_trip(ctx, rng):
+    a = FieldArch(hash_levels=4, log2_table_size=10, hidden_width=16, hidden_layers=1)
+    p = rng.standard_normal(a.param_count()).astype(np.float32)
+    g = rng.uniform(0, 5, (10, 10, 10)).astype(np.float32)
+    ob = ObjectTrainer.create(ctx, a, theta=p, grid=g)
+    assert np.array_equal(ob.get_params(), p) and np.array_equal(ob.get_grid(), g)
+
+
+def test_device_init_distribution(ctx):
+    a = scenes.cfg1_arch()
+    ob = ObjectTrainer.create(ctx, a, seed=123)
+    p = ob.get_params()
+    nh = a.hash_param_count()
+    assert np.all(np.abs(p[:nh]) <= 1e-4) and abs(p[:nh].std() - 2e-4 / np.sqrt(12)) < 2e-6
+    w0 = p[nh: nh + a.hidden_width * 16].reshape(a.hidden_width, 16)
+    assert abs(w0.std() - np.sqrt(2 / 16)) < 0.05
