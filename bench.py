@@ -1,0 +1,475 @@
+#!/usr/bin/env python
+"""Benchmark: PRENOM per-object NeRF train step on B200 (BASELINE config 2).
+
+Workload (BASELINE.json configs[1], "cfg2"): one object with a prior --
+union of 3-6 random boxes, 50 RGB-D views at 256x256, 32^3 sigma prior grid,
+meta-init parameters drawn from the seed; hash grid L=16 F=2 T=2^19 (base
+16 -> max res 1024), MLP W=64 H=2 (reference single-MLP family);
+8192 rays/step (25% background band), prior-CDF sampling 32 coarse grid
+lookups -> 96 MLP samples/ray; Adam lr 1e-2; grid refresh every
+50 steps. A "step" = one full train_track iteration (mapper.cpp:150-184):
+sampling, encode+MLP fwd, compositing+loss, MLP+encode bwd, dense Adam over
+16.78M parameters.
+
+value = evaluated ray-samples (MLP samples of non-escaped rays) per second
+over all ranks, inputs resident in HBM, device-timed with CUDA events on the
+library's stream. e2e = the same metric through the C-ABI with host buffers:
+each step uploads the keyframe it trains on from pinned host memory and
+reads the loss back. Multi-GPU: one independent object per rank (weak
+scaling, no data-path collective), max time over ranks.
+
+--impl reference times the reference's own CPU implementation
+(oracle/_ref/libnoma_ref.so built from the untouched reference sources) on
+the host cores: one reference train_track per thread, each step a bounded
+sample of rays (stated in `cpu_baseline.sample`).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "ray-samples/sec/GPU (fwd+bwd); objects·steps/sec at 1/2/4/8 B200 vs host CPU"
+UNIT = "ray-samples/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--width", type=int, default=64)
+    ap.add_argument("--mlp", default="fp32", choices=["fp32", "bf16"])
+    ap.add_argument("--rays", type=int, default=8192)
+    ap.add_argument("--samples", type=int, default=96)
+    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=20.0, help="budget of the cpu_baseline sample")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ setup
+def dist_info():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def make_workload(args, rank):
+    from paper_2503_01582_b200 import TrainConfig, scenes
+    from paper_2503_01582_b200._capi import MLP_BF16, MLP_FP32
+
+    sc = scenes.box_union_scene(n_views=50, res=256, seed=1000 + rank)
+    grid = scenes.occupancy_prior(sc.boxes, R=32)
+    arch = scenes.cfg2_arch(args.width)
+    cfg = TrainConfig(rays_per_iter=args.rays, samples_per_ray=args.samples, coarse_samples=32, prior_sampling=1,
+                      grid_refresh_every=50, eta=1e-2, bg_fraction=0.25,
+                      mlp_precision=MLP_BF16 if args.mlp == "bf16" else MLP_FP32)
+    return sc, grid, arch, cfg
+
+
+class ClockSampler:
+    """nvidia-smi-equivalent clocks + throttle reasons during the timed region (NVML)."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+        0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index):
+        self.samples, self.reasons = [], set()
+        self.stop = threading.Event()
+        self.ok = False
+        self.max_mhz = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            pass
+
+    def _run(self):
+        while not self.stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.02)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self.stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "n": 0}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "n": len(self.samples)}
+
+
+def peaks():
+    p = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "source": "fallback"}
+    f = ROOT / "MEASURED_PEAKS.json"
+    if f.exists():
+        d = json.loads(f.read_text())
+        p.update({k: d[k] for k in ("hbm_gbs", "bf16_tflops", "bf16_tflops_sustained") if k in d})
+        p["source"] = "measured"
+    return p
+
+
+def algorithmic_costs(arch, B, S, n_coarse, P):
+    """SURVEY.md §8(d) per-launch algorithmic bytes / flops (N = B*S samples)."""
+    N = B * S
+    L, F, W, H, IN = arch.hash_levels, arch.features_per_level, arch.hidden_width, arch.hidden_layers, \
+        arch.hash_levels * arch.features_per_level
+    mlp_fwd_flops = 2 * (IN * W + (H - 1) * W * W + 4 * W)
+    return {
+        # sampler: 8 grid corners x 4 B per coarse sample + ray (24 B) + 20 B/sample out
+        "sample": ("hbm", (32 * n_coarse + 24) * B + 20 * N),
+        # encode gathers 8*L*F*4 B/sample (the MLP forward rides in the same kernel, fused)
+        "field_fwd": ("hbm", 8 * L * F * 4 * N),
+        "composite": ("hbm", 40 * N),
+        # MLP backward: recompute fwd + 2x fwd for the backward
+        "mlp_bwd": ("tensor", 3 * mlp_fwd_flops * N),
+        # table-gradient RMW: 2 * 8*L*F*4 B/sample
+        "encode_bwd": ("hbm", 2 * 8 * L * F * 4 * N),
+        # dense Adam: p,m,v read+write, g read + zero = 32 B/param
+        "adam": ("hbm", 32 * P),
+        "refresh": ("hbm", 0),
+    }
+
+
+def load_traffic():
+    f = ROOT / "profiles" / "ncu_traffic.json"
+    if f.exists():
+        try:
+            return json.loads(f.read_text())
+        except Exception:
+            return {}
+    return {}
+
+
+# --------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+
+    ws, rank, local = dist_info()
+    if ws > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(local)
+    from paper_2503_01582_b200 import Context, ObjectTrainer
+    from paper_2503_01582_b200._capi import KERNEL_CLASSES
+
+    sc, grid, arch, cfg = make_workload(args, rank)
+    ctx = Context(local)
+    obj = ObjectTrainer.create(ctx, arch, theta=None, grid=grid, seed=7 + rank, cfg=cfg, box_min=sc.box_min,
+                               box_max=sc.box_max)
+    obj.set_frames(sc.cams, sc.rgb, sc.depth, sc.mask, 1, sc.obj_pose)
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    lib = ctx.lib
+    import ctypes as C
+
+    # warm-up (untimed)
+    obj.train_step(args.warmup, stats=False)
+    ctx.synchronize()
+
+    # timed region: K steps, one C call, per-kernel events on
+    launches0 = ctx.launch_count()
+    lib.prenom_ctx_profile(ctx.h, 1)
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    ctx.synchronize()
+    with ClockSampler(local) as clk:
+        t_start.record(stream)
+        obj.train_step(args.steps, stats=False)
+        t_end.record(stream)
+        ctx.synchronize()
+        torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    ms = t_start.elapsed_time(t_end)
+    launches = ctx.launch_count() - launches0
+    kms = (C.c_double * 7)()
+    kn = (C.c_int64 * 7)()
+    lib.prenom_ctx_kernel_times(ctx.h, kms, kn)
+    lib.prenom_ctx_profile(ctx.h, 0)
+    stats = obj.last_stats(args.steps)
+    n_samples = sum(s["n_samples"] for s in stats)
+    loss_first, loss_last = stats[0]["total"], stats[-1]["total"]
+
+    # e2e through the C-ABI with host buffers (pinned), loss read back every step
+    e2e = None
+    if args.e2e_steps > 0:
+        rgb_h = torch.from_numpy(np.ascontiguousarray(sc.rgb)).pin_memory()
+        dep_h = torch.from_numpy(np.ascontiguousarray(sc.depth)).pin_memory()
+        npx = sc.rgb.shape[1] * sc.rgb.shape[2]
+        fptr = C.POINTER(C.c_float)
+        fr = C.c_int32()
+        e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e_samples = 0
+        h2d = 0
+        if ws > 1:
+            torch.distributed.barrier()
+        ctx.synchronize()
+        e_start.record(stream)
+        for _ in range(args.e2e_steps):
+            lib.prenom_object_next_frame(obj.h, C.byref(fr))
+            f = fr.value
+            lib.prenom_object_upload_frame(obj.h, f, C.cast(rgb_h.data_ptr() + f * npx * 12, fptr),
+                                           C.cast(dep_h.data_ptr() + f * npx * 4, fptr), None)
+            h2d += npx * 16
+            st = obj.train_step(1, stats=True)[0]
+            e_samples += st["n_samples"]
+        e_end.record(stream)
+        ctx.synchronize()
+        e_ms = e_start.elapsed_time(e_end)
+        e2e = dict(ms=e_ms, samples=e_samples, h2d=h2d // args.e2e_steps, d2h=48)
+
+    # aggregate over ranks: max time, summed samples
+    t_dev = ms / 1e3
+    tot_samples = n_samples
+    if ws > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([t_dev, e2e["ms"] / 1e3 if e2e else 0.0], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        n = torch.tensor([float(n_samples), float(e2e["samples"] if e2e else 0)], device="cuda",
+                         dtype=torch.float64)
+        dist.all_reduce(n, op=dist.ReduceOp.SUM)
+        t_dev, e_t = t.tolist()
+        tot_samples, e_tot = n.tolist()
+        if e2e:
+            e2e["ms"], e2e["samples"] = e_t * 1e3, e_tot
+    value = tot_samples / t_dev
+    per_gpu = value / ws
+
+    # roofline of the dominant kernel (largest share of the step), live events
+    pk = peaks()
+    costs = algorithmic_costs(arch, cfg.rays_per_iter, cfg.samples_per_ray, cfg.coarse_samples,
+                              arch.param_count())
+    traffic = load_traffic()
+    kernels = {}
+    total_k = sum(kms[i] for i in range(7)) or 1.0
+    for i, name in enumerate(KERNEL_CLASSES):
+        if kn[i] == 0:
+            continue
+        avg_s = kms[i] / kn[i] / 1e3
+        bound, work = costs[name]
+        if bound == "hbm":
+            ach = work / avg_s / 1e9
+            peak, unit = pk["hbm_gbs"], "GB/s"
+        else:
+            ach = work / avg_s / 1e12
+            peak, unit = pk["bf16_tflops_sustained"], "TFLOP/s"
+        kernels[name] = {"ms_per_launch": round(kms[i] / kn[i], 4), "launches": int(kn[i]),
+                         "share": round(kms[i] / total_k, 4), "bound": bound, "achieved": round(ach, 2),
+                         "unit": unit, "frac": round(ach / peak, 4) if work else None,
+                         "work_per_launch": work}
+    dom = max((k for k in kernels if k != "refresh"), key=lambda k: kernels[k]["share"])
+    d = kernels[dom]
+    roofline = {"kernel": dom, "bound": d["bound"], "achieved": d["achieved"],
+                "peak": pk["hbm_gbs"] if d["bound"] == "hbm" else pk["bf16_tflops_sustained"],
+                "unit": d["unit"], "frac": d["frac"],
+                "traffic": traffic.get(dom, {}).get("dram_bytes_per_launch"),
+                "peak_source": pk["source"] + (" hbm_gbs" if d["bound"] == "hbm" else " bf16_tflops_sustained")}
+    # encode kernels (north_star: >= 50% of the memory roofline)
+    enc_bytes = costs["field_fwd"][1] + costs["encode_bwd"][1]
+    enc_t = (kernels.get("field_fwd", {}).get("ms_per_launch", 0) + kernels.get("encode_bwd", {}).get(
+        "ms_per_launch", 0)) / 1e3
+    encode_roofline = {"achieved": round(enc_bytes / enc_t / 1e9, 2) if enc_t else None, "unit": "GB/s",
+                       "peak": pk["hbm_gbs"], "frac": round(enc_bytes / enc_t / 1e9 / pk["hbm_gbs"], 4) if enc_t else None}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline(args, budget_s=args.cpu_seconds)
+        except Exception as e:  # reported, never fatal
+            cpu = {"value": None, "error": repr(e)[:200]}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(t_dev * 1e3 / args.steps, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32" if args.mlp == "fp32" else "f32+bf16-mlp",
+            "data": "synthetic (seeded box-union RGB-D scenes, BASELINE cfg2 shapes)",
+            "config": {"workload": "cfg2: single object with 32^3 prior, L16 F2 T19 max-res 1024, MLP "
+                                   f"W{arch.hidden_width} H{arch.hidden_layers}, {cfg.rays_per_iter} rays x "
+                                   f"{cfg.samples_per_ray} MLP samples (32 coarse grid lookups), 50 views 256^2, "
+                                   "Adam lr 1e-2, grid refresh every 50",
+                       "rays_per_step": cfg.rays_per_iter, "mlp_samples_per_ray": cfg.samples_per_ray,
+                       "coarse_samples": cfg.coarse_samples, "params": arch.param_count(),
+                       "mlp_precision": args.mlp, "objects_per_gpu": 1,
+                       "l2": "inputs larger than L2 (params+grad+Adam m,v = 256 MiB streamed every step); no flush"},
+            "per_gpu": round(per_gpu, 1),
+            "objects_steps_per_s": round(ws * args.steps / t_dev, 2),
+            "e2e": None if not e2e else {"value": round(e2e["samples"] / (e2e["ms"] / 1e3), 1), "unit": UNIT,
+                                         "h2d_bytes_per_step": int(e2e["h2d"]), "d2h_bytes_per_step": e2e["d2h"],
+                                         "steps": args.e2e_steps},
+            "gpu_launches": int(launches),
+            "roofline": roofline,
+            "encode_roofline": encode_roofline,
+            "kernels": kernels,
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+            "loss": {"first": loss_first, "last": loss_last},
+        }
+        print(json.dumps(line), flush=True)
+    obj.close()
+    ctx.close()
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+# ------------------------------------------------------ reference (CPU)
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def _ref_trainers(args, n, rays, seed0=0):
+    from oracle import pyoracle
+    from paper_2503_01582_b200 import TrainConfig
+
+    if not pyoracle.REF_SO.exists():
+        pyoracle.build_oracle(ref=True)
+    ref = pyoracle.Ref()
+    sc, grid, arch, cfg = make_workload(args, 0)
+    rcfg = TrainConfig(rays_per_iter=rays, samples_per_ray=cfg.samples_per_ray, coarse_samples=cfg.coarse_samples,
+                       prior_sampling=1, grid_refresh_every=cfg.grid_refresh_every, eta=cfg.eta)
+    out = []
+    for i in range(n):
+        theta = ref.init_params(arch, seed0 + i)  # noma::init_params (field.cpp:150-166)
+        out.append(ref.trainer(arch, theta, grid, 32, sc.cams, sc.rgb, sc.depth, sc.mask, 1, sc.obj_pose, sc.box_min,
+                               sc.box_max, rcfg, 1234 + i))
+    return out, arch
+
+
+def _parallel_steps(trainers, iters):
+    res = [0] * len(trainers)
+
+    def run(i):
+        n = 0
+        for _ in range(iters):
+            trainers[i].step(1)
+            n += trainers[i].last_samples()
+        res[i] = n
+
+    th = [threading.Thread(target=run, args=(i,)) for i in range(len(trainers))]
+    t0 = time.perf_counter()
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    return sum(res), time.perf_counter() - t0
+
+
+def _calibrate(args, threads):
+    """Seconds per reference iteration at `rays` rays, per thread (1 probe)."""
+    tr, arch = _ref_trainers(args, 1, 256, seed0=99)
+    t0 = time.perf_counter()
+    tr[0].step(1)
+    t_256 = time.perf_counter() - t0
+    tr2, _ = _ref_trainers(args, 1, 64, seed0=98)
+    t0 = time.perf_counter()
+    tr2[0].step(1)
+    t_64 = time.perf_counter() - t0
+    per_ray = max((t_256 - t_64) / 192.0, 1e-5)
+    fixed = max(t_64 - 64 * per_ray, 0.0)
+    return per_ray, fixed
+
+
+def cpu_baseline(args, budget_s=20.0):
+    """The reference train_track (mt19937) on the host cores: one object per
+    thread (mapper.cpp:572 parallel_for), bounded per-step ray count."""
+    cores = host_cores()
+    threads = max(1, min(cores, 32))
+    per_ray, fixed = _calibrate(args, threads)
+    iters = 2
+    rays = int(max(64, min(args.rays // 4, (budget_s / iters - fixed) / per_ray)))
+    trainers, _ = _ref_trainers(args, threads, rays)
+    n, dt = _parallel_steps(trainers, iters)
+    for t in trainers:
+        t.close()
+    return {"value": round(n / dt, 1), "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": f"{threads} threads x {iters} reference train_track iterations (mt19937) of cfg2, "
+                      f"{rays} rays x {args.samples} samples per iteration (of {args.rays}), each thread its own "
+                      f"object; {n} samples in {dt:.2f} s on {cores} host cores"}
+
+
+def run_reference(args):
+    ws, rank, local = dist_info()
+    if rank != 0:
+        return  # reference arm runs on rank 0 only
+    cores = host_cores()
+    threads = max(1, min(cores, 32))
+    per_ray, fixed = _calibrate(args, threads)
+    # size each step so warmup+steps end within ~3 minutes
+    budget = 180.0 / max(1, args.steps + args.warmup)
+    rays = int(max(16, min(args.rays, (budget - fixed) / per_ray)))
+    trainers, _ = _ref_trainers(args, threads, rays)
+    _parallel_steps(trainers, args.warmup)
+    n, dt = _parallel_steps(trainers, args.steps)
+    for t in trainers:
+        t.close()
+    value = n / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3 / args.steps, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded box-union RGB-D scenes, BASELINE cfg2 shapes)",
+        "config": {"workload": "cfg2 (see ours); reference CPU train_track, one object per host thread",
+                   "rays_per_step_per_thread": rays, "mlp_samples_per_ray": args.samples},
+        "cpu_baseline": {"value": round(value, 1), "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": f"{threads} threads x 1 iteration per step, {rays} rays x {args.samples} samples "
+                                   f"per iteration (of {args.rays}), oracle/_ref (unmodified reference sources)"},
+        "e2e": {"value": round(value, 1), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

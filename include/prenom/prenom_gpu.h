@@ -155,6 +155,23 @@ prenom_status prenom_ctx_synchronize(prenom_ctx_t ctx);
 /* Number of product kernels launched on this context so far. */
 prenom_status prenom_ctx_launch_count(prenom_ctx_t ctx, int64_t* count);
 
+/* Per-kernel device timing with CUDA events recorded on the context stream
+ * around every train-step launch (no reference counterpart; measurement
+ * only). prenom_ctx_kernel_times synchronizes, returns the summed
+ * milliseconds and launch counts per PRENOM_K_* class, and resets them. */
+enum {
+  PRENOM_K_SAMPLE = 0,     /* k_sample: rays + prior-CDF sampler        */
+  PRENOM_K_FIELD_FWD = 1,  /* k_fwd_tile: encode + MLP forward          */
+  PRENOM_K_COMPOSITE = 2,  /* k_composite: compositing + loss + bwd     */
+  PRENOM_K_MLP_BWD = 3,    /* k_bwd_tile: MLP backward + d_features     */
+  PRENOM_K_ENCODE_BWD = 4, /* k_encode_bwd: table-gradient scatter      */
+  PRENOM_K_ADAM = 5,       /* k_adam: dense Adam + grad zero            */
+  PRENOM_K_REFRESH = 6,    /* k_field_points: density-grid refresh      */
+  PRENOM_K_COUNT = 7
+};
+prenom_status prenom_ctx_profile(prenom_ctx_t ctx, int enable);
+prenom_status prenom_ctx_kernel_times(prenom_ctx_t ctx, double* ms, int64_t* launches);
+
 /* ---- object lifecycle ("create object from a category prior") ----------
  * Replaces train_track's CREATE block (mapper.cpp:133-143):
  *   arch = prior.arch; theta = prior.theta or init_params(arch, seed);
@@ -195,6 +212,8 @@ prenom_status prenom_train_step(prenom_object_t obj, int n_steps, prenom_step_st
 prenom_status prenom_object_last_stats(prenom_object_t obj, int n, prenom_step_stats* stats);
 /* Steps taken so far (AdamState::step). */
 prenom_status prenom_object_step(prenom_object_t obj, int64_t* step);
+/* Keyframe index the next train step will draw its rays from (TAG_FRAME). */
+prenom_status prenom_object_next_frame(prenom_object_t obj, int* frame);
 /* Check the device-side numeric flag (NumericError analogue). */
 prenom_status prenom_object_check(prenom_object_t obj);
 

@@ -407,6 +407,13 @@ class Ref(_Lib):
             "ref_train_object": (C.c_int, [rarch, f32p, C.c_int, f32p, C.c_int, rcam, f32p, f32p, u8p, C.c_uint8,
                                            f32p, f32p, f32p, f32p, C.POINTER(RefTrainCfg), C.c_uint32, C.c_int,
                                            f64p, f64p]),
+            "ref_trainer_create": (C.c_void_p, [rarch, f32p, C.c_int, f32p, C.c_int, rcam, f32p, f32p, u8p,
+                                                C.c_uint8, f32p, f32p, f32p, f32p, C.POINTER(RefTrainCfg),
+                                                C.c_uint32]),
+            "ref_trainer_destroy": (None, [C.c_void_p]),
+            "ref_trainer_step": (C.c_int, [C.c_void_p, C.c_int, f64p]),
+            "ref_trainer_last_samples": (C.c_longlong, [C.c_void_p]),
+            "ref_trainer_get_params": (None, [C.c_void_p, f32p]),
             "ref_inner_adapt": (C.c_int, [rarch, f32p, C.c_int, rcam, f32p, f32p, u8p, f32p, f32p, f32p, f32p,
                                           C.c_int, C.c_float, C.c_uint32, C.c_int, C.c_float, C.c_int, C.c_float,
                                           C.c_float, f32p, f64p]),
@@ -576,6 +583,10 @@ class Ref(_Lib):
         self._check(self.lib.ref_reptile_update(len(meta), fptr(meta), fptr(adapted), beta, fptr(out)))
         return out
 
+    def trainer(self, arch, params, grid, grid_R, cams, rgb, depth, mask, inst, pose, bmin, bmax, cfg, seed):
+        """Persistent reference train_track state (frames converted once)."""
+        return RefTrainer(self, arch, params, grid, grid_R, cams, rgb, depth, mask, inst, pose, bmin, bmax, cfg, seed)
+
     def train_object(self, arch, params, grid, grid_R, cams, rgb, depth, mask, inst, pose, bmin, bmax, cfg,
                      seed, iters):
         """Reference train_track loop (mt19937). Returns (params, grid, losses[iters,4], seconds)."""
@@ -600,3 +611,53 @@ class Ref(_Lib):
                                        iters, dptr(losses), dptr(secs))
         self._check(st)
         return p, (None if g is None else g.reshape(grid_R, grid_R, grid_R)), losses, float(secs[0])
+
+
+class RefTrainer:
+    """Handle over ref_trainer_* (oracle/ref_shim.cpp): the reference's
+    train_track loop with its own mt19937, stepped from Python; ctypes
+    releases the GIL, so several trainers can run on separate threads
+    (the reference's one-thread-per-object parallelism, mapper.cpp:572)."""
+
+    def __init__(self, ref, arch, params, grid, grid_R, cams, rgb, depth, mask, inst, pose, bmin, bmax, cfg, seed):
+        self.ref = ref
+        a = ref._a(arch)
+        self.P = ref.param_count(arch)
+        rc = (RefCamera * len(cams))()
+        for i, c in enumerate(cams):
+            cc = c if isinstance(c, CameraC) else c.to_c()
+            C.memmove(C.byref(rc[i]), C.byref(cc), C.sizeof(RefCamera))
+        pc = pose if isinstance(pose, PoseC) else pose.to_c()
+        R = np.array(list(pc.R), np.float32)
+        t = np.array(list(pc.t), np.float32)
+        rcfg = RefTrainCfg()
+        for name, _ in RefTrainCfg._fields_:
+            setattr(rcfg, name, getattr(cfg, name))
+        g = None if grid is None else f32(grid).reshape(-1)
+        self.h = ref.lib.ref_trainer_create(C.byref(a), fptr(f32(params)), grid_R, fptr(g), len(cams), rc,
+                                            fptr(f32(rgb)), fptr(f32(depth)), u8ptr(np.ascontiguousarray(mask, np.uint8)),
+                                            inst, fptr(R), fptr(t), fptr(f32(bmin)), fptr(f32(bmax)), C.byref(rcfg), seed)
+        if not self.h:
+            raise RuntimeError(ref.lib.ref_last_error().decode())
+
+    def step(self, iters=1):
+        losses = np.zeros((iters, 4), np.float64)
+        st = self.ref.lib.ref_trainer_step(self.h, iters, dptr(losses))
+        self.ref._check(st)
+        return losses
+
+    def last_samples(self):
+        return int(self.ref.lib.ref_trainer_last_samples(self.h))
+
+    def params(self):
+        out = zeros(self.P)
+        self.ref.lib.ref_trainer_get_params(self.h, fptr(out))
+        return out
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.ref.lib.ref_trainer_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()

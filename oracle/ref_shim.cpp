@@ -493,89 +493,150 @@ int ref_reptile_update(std::size_t n, const float* meta, const float* adapted, f
   REF_GUARD_END
 }
 
-// Restatement of train_track's loop body (mapper.cpp:130-184) on the public
-// API with the reference's own mt19937 stream. params (and grid, when
-// non-NULL) are updated in place. losses: iters x {total, color, depth,
-// sigma}. Frames are packed [n_frames][H][W] with one camera per frame.
+}  // extern "C"
+
+// Restatement of train_track (mapper.cpp:130-184) on the public API with
+// the reference's own mt19937 stream, as a persistent handle so repeated
+// steps time only reference compute (frames are converted once).
+struct RefTrainer {
+  FieldArch arch;
+  ParamVector theta, grad;
+  DensityGrid g;
+  int grid_R = 0;
+  AdamState adam;
+  Box3 box;
+  Pose pose;
+  std::uint8_t inst = 1;
+  std::vector<Camera> cameras;
+  std::vector<ColorImage> rgbs;
+  std::vector<DepthImage> depths;
+  std::vector<MaskImage> masks;
+  LossWeights weights;
+  RefTrainCfg cfg;
+  std::mt19937 rng;
+  std::vector<RaySampleSet> samples;
+  std::vector<std::vector<FieldOutput>> outputs;
+  std::vector<std::vector<FieldEvalCache>> caches;
+  int it = 0;
+};
+
+extern "C" {
+
+void* ref_trainer_create(const RefArch* a, const float* params, int grid_R, const float* grid, int n_frames,
+                         const RefCamera* cams, const float* rgb, const float* depth, const std::uint8_t* mask,
+                         std::uint8_t inst, const float* obj_R, const float* obj_t, const float* bmin,
+                         const float* bmax, const RefTrainCfg* cfg, std::uint32_t seed) {
+  try {
+    auto* t = new RefTrainer;
+    t->arch = to_arch(a);
+    const std::size_t P = param_count(t->arch);
+    t->theta.assign(params, params + P);
+    t->grad.assign(P, 0.f);
+    t->grid_R = grid_R;
+    t->g = grid ? to_grid(grid_R, grid) : DensityGrid(grid_R, 0.f);
+    t->adam = AdamState(P, cfg->eta);
+    t->box = Box3{v3(bmin), v3(bmax)};
+    t->pose = to_pose(obj_R, obj_t);
+    t->inst = inst;
+    for (int f = 0; f < n_frames; ++f) {
+      t->cameras.push_back(to_camera(cams + f));
+      const int W = cams[f].width, H = cams[f].height;
+      const std::size_t px = static_cast<std::size_t>(W) * H;
+      t->rgbs.push_back(to_color(W, H, rgb + 3 * px * f));
+      t->depths.push_back(to_depth(W, H, depth + px * f));
+      t->masks.push_back(to_mask(W, H, mask + px * f));
+    }
+    t->weights.lambda_d = cfg->lambda_d;
+    t->weights.lambda_sigma = cfg->lambda_sigma;
+    t->cfg = *cfg;
+    t->rng.seed(seed);
+    return t;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
+void ref_trainer_destroy(void* h) { delete static_cast<RefTrainer*>(h); }
+
+// `iters` iterations of train_track's loop body (mapper.cpp:150-184).
+// losses: iters x {total, color, depth, sigma} (may be NULL).
+int ref_trainer_step(void* h, int iters, double* losses) {
+  REF_GUARD_BEGIN
+  RefTrainer& t = *static_cast<RefTrainer*>(h);
+  std::uniform_int_distribution<std::size_t> pick_kf(0, t.cameras.size() - 1);
+  for (int k = 0; k < iters; ++k) {
+    const std::size_t fi = pick_kf(t.rng);
+    const auto rays = generate_rays(t.cameras[fi], t.rgbs[fi], t.depths[fi], t.masks[fi], t.inst, t.pose,
+                                    t.box.size(), t.cfg.rays_per_iter, t.cfg.bg_fraction, t.rng);
+    t.samples.clear();
+    t.outputs.clear();
+    t.caches.clear();
+    for (const ObjectRay& ray : rays) {
+      RaySampleSet set = t.cfg.prior_sampling
+                             ? sample_ray(t.g, ray, t.box, t.cfg.coarse_samples, t.cfg.samples_per_ray,
+                                          t.cfg.escape_eps, t.rng)
+                             : uniform_samples(ray, t.box, t.cfg.samples_per_ray);
+      std::vector<FieldOutput> outs(set.size());
+      std::vector<FieldEvalCache> cache(set.size());
+      for (std::size_t i = 0; i < set.size(); ++i)
+        outs[i] = field_eval(t.arch, t.theta, set.positions[i], &cache[i]);
+      t.samples.push_back(std::move(set));
+      t.outputs.push_back(std::move(outs));
+      t.caches.push_back(std::move(cache));
+    }
+    const LossResult loss = batch_loss(rays, t.samples, t.outputs, t.weights, t.rng);
+    std::fill(t.grad.begin(), t.grad.end(), 0.f);
+    for (std::size_t r = 0; r < rays.size(); ++r)
+      for (std::size_t i = 0; i < loss.grads[r].size(); ++i)
+        field_backward(t.arch, t.theta, t.caches[r][i], loss.grads[r][i].d_sigma, loss.grads[r][i].d_rgb,
+                       t.grad);
+    adam_step(t.adam, t.theta, t.grad);
+    if (losses) {
+      losses[4 * k + 0] = loss.total;
+      losses[4 * k + 1] = loss.color_term;
+      losses[4 * k + 2] = loss.depth_term;
+      losses[4 * k + 3] = loss.sigma_term;
+    }
+    t.it += 1;
+    if (t.cfg.grid_refresh_every > 0 && t.it % t.cfg.grid_refresh_every == 0)
+      t.g = refresh_grid(t.arch, t.theta, t.grid_R);
+  }
+  return 0;
+  REF_GUARD_END
+}
+
+// Samples evaluated in the last step (for throughput accounting).
+long long ref_trainer_last_samples(void* h) {
+  const RefTrainer& t = *static_cast<RefTrainer*>(h);
+  long long n = 0;
+  for (const auto& s : t.samples) n += static_cast<long long>(s.size());
+  return n;
+}
+
+void ref_trainer_get_params(void* h, float* out) {
+  const RefTrainer& t = *static_cast<RefTrainer*>(h);
+  std::memcpy(out, t.theta.data(), t.theta.size() * sizeof(float));
+}
+
 int ref_train_object(const RefArch* a, float* params, int grid_R, float* grid, int n_frames,
                      const RefCamera* cams, const float* rgb, const float* depth,
                      const std::uint8_t* mask, std::uint8_t inst, const float* obj_R,
                      const float* obj_t, const float* bmin, const float* bmax,
                      const RefTrainCfg* cfg, std::uint32_t seed, int iters, double* losses,
                      double* seconds) {
-  REF_GUARD_BEGIN
   const auto t0 = std::chrono::steady_clock::now();
-  const FieldArch arch = to_arch(a);
-  const std::size_t P = param_count(arch);
-  ParamVector theta(params, params + P);
-  DensityGrid g = grid ? to_grid(grid_R, grid) : DensityGrid(grid_R, 0.f);
-  AdamState adam(P, cfg->eta);
-  ParamVector grad(P, 0.f);
-  const Box3 box{v3(bmin), v3(bmax)};
-  const Pose pose = to_pose(obj_R, obj_t);
-  std::vector<Camera> cameras;
-  std::vector<ColorImage> rgbs;
-  std::vector<DepthImage> depths;
-  std::vector<MaskImage> masks;
-  for (int f = 0; f < n_frames; ++f) {
-    cameras.push_back(to_camera(cams + f));
-    const int W = cams[f].width, H = cams[f].height;
-    const std::size_t px = static_cast<std::size_t>(W) * H;
-    rgbs.push_back(to_color(W, H, rgb + 3 * px * f));
-    depths.push_back(to_depth(W, H, depth + px * f));
-    masks.push_back(to_mask(W, H, mask + px * f));
-  }
-  LossWeights weights;
-  weights.lambda_d = cfg->lambda_d;
-  weights.lambda_sigma = cfg->lambda_sigma;
-  std::mt19937 rng(seed);
-  std::uniform_int_distribution<std::size_t> pick_kf(0, static_cast<std::size_t>(n_frames) - 1);
-  std::vector<RaySampleSet> samples;
-  std::vector<std::vector<FieldOutput>> outputs;
-  std::vector<std::vector<FieldEvalCache>> caches;
-  for (int it = 0; it < iters; ++it) {
-    const std::size_t fi = pick_kf(rng);
-    const auto rays =
-        generate_rays(cameras[fi], rgbs[fi], depths[fi], masks[fi], inst, pose, box.size(),
-                      cfg->rays_per_iter, cfg->bg_fraction, rng);
-    samples.clear();
-    outputs.clear();
-    caches.clear();
-    for (const ObjectRay& ray : rays) {
-      RaySampleSet set = cfg->prior_sampling
-                             ? sample_ray(g, ray, box, cfg->coarse_samples, cfg->samples_per_ray,
-                                          cfg->escape_eps, rng)
-                             : uniform_samples(ray, box, cfg->samples_per_ray);
-      std::vector<FieldOutput> outs(set.size());
-      std::vector<FieldEvalCache> cache(set.size());
-      for (std::size_t i = 0; i < set.size(); ++i)
-        outs[i] = field_eval(arch, theta, set.positions[i], &cache[i]);
-      samples.push_back(std::move(set));
-      outputs.push_back(std::move(outs));
-      caches.push_back(std::move(cache));
-    }
-    const LossResult loss = batch_loss(rays, samples, outputs, weights, rng);
-    std::fill(grad.begin(), grad.end(), 0.f);
-    for (std::size_t r = 0; r < rays.size(); ++r)
-      for (std::size_t i = 0; i < loss.grads[r].size(); ++i)
-        field_backward(arch, theta, caches[r][i], loss.grads[r][i].d_sigma,
-                       loss.grads[r][i].d_rgb, grad);
-    adam_step(adam, theta, grad);
-    if (losses) {
-      losses[4 * it + 0] = loss.total;
-      losses[4 * it + 1] = loss.color_term;
-      losses[4 * it + 2] = loss.depth_term;
-      losses[4 * it + 3] = loss.sigma_term;
-    }
-    if (cfg->grid_refresh_every > 0 && (it + 1) % cfg->grid_refresh_every == 0)
-      g = refresh_grid(arch, theta, grid_R);
-  }
-  std::memcpy(params, theta.data(), P * sizeof(float));
-  if (grid) std::memcpy(grid, g.values.data(), g.values.size() * sizeof(float));
+  void* h = ref_trainer_create(a, params, grid_R, grid, n_frames, cams, rgb, depth, mask, inst, obj_R, obj_t,
+                               bmin, bmax, cfg, seed);
+  if (!h) return 5;
+  const int st = ref_trainer_step(h, iters, losses);
+  RefTrainer& t = *static_cast<RefTrainer*>(h);
+  std::memcpy(params, t.theta.data(), t.theta.size() * sizeof(float));
+  if (grid) std::memcpy(grid, t.g.values.data(), t.g.values.size() * sizeof(float));
+  ref_trainer_destroy(h);
   if (seconds)
     *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-  return 0;
-  REF_GUARD_END
+  return st;
 }
 
 // meta.cpp:24-81 (inner_adapt) on a one-task Task built from flat frames.

@@ -18,6 +18,7 @@ PRENOM_OK, PRENOM_USAGE, PRENOM_DATA, PRENOM_NUMERIC, PRENOM_CUDA = range(5)
 TAG_FRAME, TAG_PIXEL, TAG_FINE, TAG_BG, TAG_RENDER, TAG_INIT = 1, 2, 3, 4, 5, 6
 ACT_EXP_CLAMPED, ACT_SOFTPLUS = 0, 1
 MLP_FP32, MLP_BF16 = 0, 1
+KERNEL_CLASSES = ["sample", "field_fwd", "composite", "mlp_bwd", "encode_bwd", "adam", "refresh"]
 
 
 class FieldArchC(C.Structure):
@@ -129,7 +130,7 @@ EXPORTED = [
     "prenom_last_error", "prenom_abi_version", "prenom_default_train_cfg",
     "prenom_param_count", "prenom_level_resolution",
     "prenom_ctx_create", "prenom_ctx_destroy", "prenom_ctx_stream", "prenom_ctx_synchronize",
-    "prenom_ctx_launch_count",
+    "prenom_ctx_launch_count", "prenom_ctx_profile", "prenom_ctx_kernel_times", "prenom_object_next_frame",
     "prenom_object_create", "prenom_object_destroy", "prenom_object_set_frames",
     "prenom_object_upload_frame", "prenom_train_step", "prenom_object_last_stats",
     "prenom_object_step", "prenom_object_check",
@@ -180,6 +181,9 @@ def _declare(lib):
         "prenom_ctx_stream": (i32, [P, C.POINTER(P)]),
         "prenom_ctx_synchronize": (i32, [P]),
         "prenom_ctx_launch_count": (i32, [P, i64p]),
+        "prenom_ctx_profile": (i32, [P, i32]),
+        "prenom_ctx_kernel_times": (i32, [P, f64p, i64p]),
+        "prenom_object_next_frame": (i32, [P, i32p]),
         "prenom_object_create": (i32, [P, archp, f32p, f32p, i32, u64, C.POINTER(TrainCfgC),
                                        f32p, f32p, C.POINTER(P)]),
         "prenom_object_destroy": (i32, [P]),

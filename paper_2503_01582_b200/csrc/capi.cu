@@ -164,7 +164,42 @@ struct prenom_ctx_s {
   int device = 0;
   cudaStream_t stream = nullptr;
   int64_t launches = 0;
+  // optional per-kernel event timing
+  bool prof = false;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_used;
+  cudaEvent_t get_event() {
+    if (ev_pool.empty()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      return e;
+    }
+    cudaEvent_t e = ev_pool.back();
+    ev_pool.pop_back();
+    return e;
+  }
 };
+
+namespace {
+struct ProfScope {
+  prenom_ctx_s* c;
+  int k;
+  cudaEvent_t b = nullptr, e = nullptr;
+  ProfScope(prenom_ctx_s* ctx, int kind) : c(ctx), k(kind) {
+    if (c->prof) {
+      b = c->get_event();
+      e = c->get_event();
+      cudaEventRecord(b, c->stream);
+    }
+  }
+  ~ProfScope() {
+    if (c->prof) {
+      cudaEventRecord(e, c->stream);
+      c->ev_used.push_back({k, {b, e}});
+    }
+  }
+};
+}  // namespace
 
 struct FrameDev {
   DevBuf<float> rgb, depth;
@@ -302,8 +337,14 @@ prenom_status enqueue_step(prenom_object_s* o, StepStatsDev* stats) {
   const RaySource src = frame_source(o, fi);
   if (src.n_obj_px == 0) return fail(PRENOM_DATA, "generate_rays: no object pixels");
   const SampleBufs sb = bufs(o);
-  CUDA_TRY(launch_sample(src, sampler_cfg(o, B, c.prior_sampling, PRENOM_TAG_FINE, step), sb, nullptr, st));
-  CUDA_TRY(launch_field_fwd_train(o->fd, o->params.p, B, S, sb, o->feat_t.p, o->out.p, o->flag.p, st));
+  {
+    ProfScope ps(o->ctx, PRENOM_K_SAMPLE);
+    CUDA_TRY(launch_sample(src, sampler_cfg(o, B, c.prior_sampling, PRENOM_TAG_FINE, step), sb, nullptr, st));
+  }
+  {
+    ProfScope ps(o->ctx, PRENOM_K_FIELD_FWD);
+    CUDA_TRY(launch_field_fwd_train(o->fd, o->params.p, B, S, sb, o->feat_t.p, o->out.p, o->flag.p, st));
+  }
   CompositeArgs ca;
   std::memset(&ca, 0, sizeof ca);
   ca.B = B;
@@ -323,20 +364,33 @@ prenom_status enqueue_step(prenom_object_s* o, StepStatsDev* stats) {
   ca.stats = stats;
   ca.flag = o->flag.p;
   ca.frame = fi;
-  CUDA_TRY(launch_composite(ca, st));
-  CUDA_TRY(launch_mlp_bwd_train(o->fd, o->params.p, o->grad.p, B, S, sb.count, o->feat_t.p, o->dout.p,
-                                o->dfeat_t.p, st));
-  CUDA_TRY(launch_encode_bwd(o->fd, o->params.p, o->grad.p, B, S, sb.count, sb.pos_depth, o->dfeat_t.p, st));
+  {
+    ProfScope ps(o->ctx, PRENOM_K_COMPOSITE);
+    CUDA_TRY(launch_composite(ca, st));
+  }
+  {
+    ProfScope ps(o->ctx, PRENOM_K_MLP_BWD);
+    CUDA_TRY(launch_mlp_bwd_train(o->fd, o->params.p, o->grad.p, B, S, sb.count, o->feat_t.p, o->dout.p,
+                                  o->dfeat_t.p, st));
+  }
+  {
+    ProfScope ps(o->ctx, PRENOM_K_ENCODE_BWD);
+    CUDA_TRY(launch_encode_bwd(o->fd, o->params.p, o->grad.p, B, S, sb.count, sb.pos_depth, o->dfeat_t.p, st));
+  }
   // adam_step (field.cpp:295-310); grad zeroed in the same pass (mapper.cpp:175)
   const float stepf = (float)(o->step + 1);
   const float c1 = 1.f - std::pow(c.adam_beta1, stepf);
   const float c2 = 1.f - std::pow(c.adam_beta2, stepf);
-  CUDA_TRY(launch_adam(o->P, o->params.p, o->grad.p, o->m.p, o->v.p, c.eta, c.adam_beta1, c.adam_beta2, c.adam_eps,
-                       c1, c2, 1, st));
+  {
+    ProfScope ps(o->ctx, PRENOM_K_ADAM);
+    CUDA_TRY(launch_adam(o->P, o->params.p, o->grad.p, o->m.p, o->v.p, c.eta, c.adam_beta1, c.adam_beta2,
+                         c.adam_eps, c1, c2, 1, st));
+  }
   o->ctx->launches += 7;
   o->step += 1;
   // grid refresh every m iterations (mapper.cpp:182-183)
   if (c.grid_refresh_every > 0 && o->step % c.grid_refresh_every == 0) {
+    ProfScope ps(o->ctx, PRENOM_K_REFRESH);
     CUDA_TRY(launch_refresh_grid(o->fd, o->params.p, o->R, o->grid.p, o->flag.p, st));
     o->ctx->launches += 1;
   }
@@ -444,6 +498,11 @@ prenom_status prenom_ctx_destroy(prenom_ctx_t ctx) {
   if (!ctx) return PRENOM_OK;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
+  for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+  for (auto& u : ctx->ev_used) {
+    cudaEventDestroy(u.second.first);
+    cudaEventDestroy(u.second.second);
+  }
   cudaStreamDestroy(ctx->stream);
   delete ctx;
   return PRENOM_OK;
@@ -465,6 +524,39 @@ prenom_status prenom_ctx_synchronize(prenom_ctx_t ctx) {
 prenom_status prenom_ctx_launch_count(prenom_ctx_t ctx, int64_t* count) {
   if (!ctx || !count) return fail(PRENOM_USAGE, "NULL argument");
   *count = ctx->launches;
+  return PRENOM_OK;
+}
+
+prenom_status prenom_ctx_profile(prenom_ctx_t ctx, int enable) {
+  if (!ctx) return fail(PRENOM_USAGE, "NULL ctx");
+  ctx->prof = enable != 0;
+  return PRENOM_OK;
+}
+
+prenom_status prenom_ctx_kernel_times(prenom_ctx_t ctx, double* ms, int64_t* launches) {
+  if (!ctx || !ms || !launches) return fail(PRENOM_USAGE, "NULL argument");
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  for (int k = 0; k < PRENOM_K_COUNT; ++k) {
+    ms[k] = 0.0;
+    launches[k] = 0;
+  }
+  for (auto& u : ctx->ev_used) {
+    float t = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&t, u.second.first, u.second.second));
+    ms[u.first] += t;
+    launches[u.first] += 1;
+    ctx->ev_pool.push_back(u.second.first);
+    ctx->ev_pool.push_back(u.second.second);
+  }
+  ctx->ev_used.clear();
+  return PRENOM_OK;
+}
+
+prenom_status prenom_object_next_frame(prenom_object_t o, int* frame) {
+  if (!o || !frame) return fail(PRENOM_USAGE, "NULL argument");
+  if (o->frames.empty()) return fail(PRENOM_DATA, "object has no frames");
+  *frame = (int)pdm_pick(philox_first(o->seed, PRENOM_TAG_FRAME, (uint32_t)o->step, 0, 0), (uint32_t)o->frames.size());
   return PRENOM_OK;
 }
 
