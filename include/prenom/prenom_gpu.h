@@ -311,6 +311,13 @@ prenom_status prenom_debug_generate_rays(prenom_object_t obj, int frame, int64_t
                                          float* origins, float* dirs, int* kind,
                                          float* target_rgb, float* target_depth, int* pick_px);
 
+/* One tcgen05 tile GEMM D[M][N] = A[M][K] * B[N][K]^T (bf16 operands, fp32
+ * accumulate in TMEM), operands staged K-major or MN-major: unit test of the
+ * tensor-core building blocks the fused MLP kernels use. M in {64,128},
+ * N % 8 == 0 (16 for M=128), K % 16 == 0. */
+prenom_status prenom_debug_umma_gemm(prenom_ctx_t ctx, int M, int N, int K, int a_mn, int b_mn,
+                                     const float* A, const float* B, float* D);
+
 #ifdef __cplusplus
 }
 #endif

@@ -140,7 +140,7 @@ EXPORTED = [
     "prenom_reptile_delta", "prenom_reptile_apply", "prenom_object_copy_params",
     "prenom_debug_philox", "prenom_debug_hash_encode", "prenom_debug_field_eval",
     "prenom_debug_field_backward", "prenom_debug_adam", "prenom_debug_sample_rays",
-    "prenom_debug_batch_loss", "prenom_debug_generate_rays",
+    "prenom_debug_batch_loss", "prenom_debug_generate_rays", "prenom_debug_umma_gemm",
 ]
 
 _lib = None
@@ -220,6 +220,7 @@ def _declare(lib):
                                           f32p, f32p, C.c_float, C.c_float, f64p, f32p, f32p,
                                           f32p, f32p]),
         "prenom_debug_generate_rays": (i32, [P, i32, i64, f32p, f32p, i32p, f32p, f32p, i32p]),
+        "prenom_debug_umma_gemm": (i32, [P, i32, i32, i32, i32, i32, f32p, f32p, f32p]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(lib, name)

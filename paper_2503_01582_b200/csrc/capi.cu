@@ -1306,4 +1306,25 @@ prenom_status prenom_debug_generate_rays(prenom_object_t o, int frame, int64_t s
   return PRENOM_OK;
 }
 
+prenom_status prenom_debug_umma_gemm(prenom_ctx_t ctx, int M, int N, int K, int a_mn, int b_mn, const float* A,
+                                     const float* B, float* D) {
+  if (!ctx || !A || !B || !D) return fail(PRENOM_USAGE, "NULL argument");
+  if ((M != 64 && M != 128) || N < 8 || N > 256 || N % 8 || K < 16 || K % 16 || K > 256 ||
+      (M == 128 && N % 16))
+    return fail(PRENOM_USAGE, "unsupported UMMA shape");
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  cudaStream_t st = ctx->stream;
+  DevBuf<float> a, b, d;
+  CUDA_TRY(a.ensure((size_t)M * K));
+  CUDA_TRY(b.ensure((size_t)N * K));
+  CUDA_TRY(d.ensure((size_t)M * N));
+  CUDA_TRY(cudaMemcpyAsync(a.p, A, sizeof(float) * M * K, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(b.p, B, sizeof(float) * N * K, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(launch_umma_gemm(M, N, K, a_mn, b_mn, a.p, b.p, d.p, st));
+  ctx->launches += 1;
+  CUDA_TRY(cudaMemcpyAsync(D, d.p, sizeof(float) * M * N, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return PRENOM_OK;
+}
+
 }  // extern "C"

@@ -254,5 +254,7 @@ cudaError_t launch_reptile_delta(size_t n, const float* meta, const float* adapt
                                  cudaStream_t st);
 cudaError_t launch_reptile_apply(size_t n, float* meta, const float* delta, float inv_n,
                                  float beta, cudaStream_t st);
+cudaError_t launch_umma_gemm(int M, int N, int K, int a_mn, int b_mn, const float* A, const float* B,
+                             float* D, cudaStream_t st);
 
 }  // namespace prenom

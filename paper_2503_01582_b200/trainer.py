@@ -460,3 +460,13 @@ def debug_batch_loss(ctx: Context, S: int, kind, target_rgb, target_depth, count
                                            terms.ctypes.data_as(C.POINTER(C.c_double)), fptr(ds), fptr(dr),
                                            fptr(col), fptr(dep)))
     return dict(terms=terms, d_sigma=ds, d_rgb=dr, color=col, depth=dep)
+
+
+def debug_umma_gemm(ctx: Context, A, B, a_mn: bool = False, b_mn: bool = False):
+    """D = A @ B.T on one tcgen05 tile (bf16 in, fp32 out)."""
+    A, B = _f32(A), _f32(B)
+    M, K = A.shape
+    N = B.shape[0]
+    D = np.zeros((M, N), np.float32)
+    _check(ctx.lib.prenom_debug_umma_gemm(ctx.h, M, N, K, int(a_mn), int(b_mn), fptr(A), fptr(B), fptr(D)))
+    return D

@@ -288,3 +288,17 @@ def test_device_init_distribution(ctx):
     assert np.all(np.abs(p[:nh]) <= 1e-4) and abs(p[:nh].std() - 2e-4 / np.sqrt(12)) < 2e-6
     w0 = p[nh: nh + a.hidden_width * 16].reshape(a.hidden_width, 16)
     assert abs(w0.std() - np.sqrt(2 / 16)) < 0.05
+
+
+@pytest.mark.parametrize("M,N,K,a_mn,b_mn", [(128, 64, 32, 0, 0), (128, 16, 64, 0, 0), (128, 64, 64, 0, 1),
+                                             (128, 32, 64, 1, 1), (64, 64, 128, 1, 1), (64, 72, 128, 1, 1),
+                                             (64, 40, 128, 1, 0), (128, 256, 16, 0, 0), (64, 8, 16, 0, 0)])
+def test_tcgen05_tile_gemm(ctx, rng, M, N, K, a_mn, b_mn):
+    """tcgen05.mma building block (descriptors, K-/MN-major staging, TMEM layout)."""
+    A = rng.standard_normal((M, K)).astype(np.float32)
+    B = rng.standard_normal((N, K)).astype(np.float32)
+    D = T.debug_umma_gemm(ctx, A, B, a_mn, b_mn)
+    import torch
+
+    ref = (torch.from_numpy(A).bfloat16().float() @ torch.from_numpy(B).bfloat16().float().T).numpy()
+    np.testing.assert_allclose(D, ref, rtol=1e-3, atol=1e-3)
