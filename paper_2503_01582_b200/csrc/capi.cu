@@ -231,6 +231,7 @@ struct prenom_object_s {
   // scratch
   DevBuf<float4> pos_depth, target, out, dout;
   DevBuf<float> delta, feat_t, dfeat_t, t_entry, t_exit;
+  DevBuf<unsigned char> feat_tc;  // bf16 feature tiles (tensor-core path)
   DevBuf<int> kind, count;
   DevBuf<StepStatsDev> stats;
   int last_n_steps = 0;
@@ -249,8 +250,12 @@ prenom_status ensure_scratch(prenom_object_s* o, int B, int S) {
   CUDA_TRY(o->delta.ensure(Npad));
   CUDA_TRY(o->out.ensure(Npad));
   CUDA_TRY(o->dout.ensure(Npad));
-  CUDA_TRY(o->feat_t.ensure(Npad * o->fd.in_dim));
-  CUDA_TRY(o->dfeat_t.ensure(Npad * o->fd.in_dim));
+  if (o->cfg.mlp_precision == PRENOM_MLP_BF16) {
+    CUDA_TRY(o->feat_tc.ensure(tc_feature_bytes(o->fd, (long long)N)));
+  } else {
+    CUDA_TRY(o->feat_t.ensure(Npad * o->fd.in_dim));
+    CUDA_TRY(o->dfeat_t.ensure(Npad * o->fd.in_dim));
+  }
   CUDA_TRY(o->target.ensure(B));
   CUDA_TRY(o->kind.ensure(B));
   CUDA_TRY(o->count.ensure(B));
@@ -341,9 +346,14 @@ prenom_status enqueue_step(prenom_object_s* o, StepStatsDev* stats) {
     ProfScope ps(o->ctx, PRENOM_K_SAMPLE);
     CUDA_TRY(launch_sample(src, sampler_cfg(o, B, c.prior_sampling, PRENOM_TAG_FINE, step), sb, nullptr, st));
   }
+  const bool tc = c.mlp_precision == PRENOM_MLP_BF16;
   {
     ProfScope ps(o->ctx, PRENOM_K_FIELD_FWD);
-    CUDA_TRY(launch_field_fwd_train(o->fd, o->params.p, B, S, sb, o->feat_t.p, o->out.p, o->flag.p, st));
+    if (tc)
+      CUDA_TRY(launch_fwd_tc(o->fd, o->params.p, (long long)B * S, S, sb.count, sb.pos_depth, o->feat_tc.p, o->out.p,
+                             o->flag.p, st));
+    else
+      CUDA_TRY(launch_field_fwd_train(o->fd, o->params.p, B, S, sb, o->feat_t.p, o->out.p, o->flag.p, st));
   }
   CompositeArgs ca;
   std::memset(&ca, 0, sizeof ca);
@@ -368,14 +378,20 @@ prenom_status enqueue_step(prenom_object_s* o, StepStatsDev* stats) {
     ProfScope ps(o->ctx, PRENOM_K_COMPOSITE);
     CUDA_TRY(launch_composite(ca, st));
   }
-  {
-    ProfScope ps(o->ctx, PRENOM_K_MLP_BWD);
-    CUDA_TRY(launch_mlp_bwd_train(o->fd, o->params.p, o->grad.p, B, S, sb.count, o->feat_t.p, o->dout.p,
-                                  o->dfeat_t.p, st));
-  }
-  {
-    ProfScope ps(o->ctx, PRENOM_K_ENCODE_BWD);
-    CUDA_TRY(launch_encode_bwd(o->fd, o->params.p, o->grad.p, B, S, sb.count, sb.pos_depth, o->dfeat_t.p, st));
+  if (tc) {
+    ProfScope ps(o->ctx, PRENOM_K_MLP_BWD);  // MLP backward + fused table-gradient scatter
+    CUDA_TRY(launch_bwd_tc(o->fd, o->params.p, o->grad.p, (long long)B * S, S, sb.count, sb.pos_depth,
+                           o->feat_tc.p, o->dout.p, st));
+  } else {
+    {
+      ProfScope ps(o->ctx, PRENOM_K_MLP_BWD);
+      CUDA_TRY(launch_mlp_bwd_train(o->fd, o->params.p, o->grad.p, B, S, sb.count, o->feat_t.p, o->dout.p,
+                                    o->dfeat_t.p, st));
+    }
+    {
+      ProfScope ps(o->ctx, PRENOM_K_ENCODE_BWD);
+      CUDA_TRY(launch_encode_bwd(o->fd, o->params.p, o->grad.p, B, S, sb.count, sb.pos_depth, o->dfeat_t.p, st));
+    }
   }
   // adam_step (field.cpp:295-310); grad zeroed in the same pass (mapper.cpp:175)
   const float stepf = (float)(o->step + 1);
@@ -386,7 +402,7 @@ prenom_status enqueue_step(prenom_object_s* o, StepStatsDev* stats) {
     CUDA_TRY(launch_adam(o->P, o->params.p, o->grad.p, o->m.p, o->v.p, c.eta, c.adam_beta1, c.adam_beta2,
                          c.adam_eps, c1, c2, 1, st));
   }
-  o->ctx->launches += 7;
+  o->ctx->launches += tc ? 6 : 7;
   o->step += 1;
   // grid refresh every m iterations (mapper.cpp:182-183)
   if (c.grid_refresh_every > 0 && o->step % c.grid_refresh_every == 0) {
@@ -572,6 +588,10 @@ prenom_status prenom_object_create(prenom_ctx_t ctx, const prenom_field_arch* ar
     return fail(PRENOM_USAGE, "coarse_samples must be in [1, 1024]");
   for (int a = 0; a < 3; ++a)
     if (!(box_max[a] > box_min[a])) return fail(PRENOM_DATA, "degenerate object box");
+  if (cfg->mlp_precision == PRENOM_MLP_BF16 && !tc_supported(make_desc(*arch)))
+    return fail(PRENOM_USAGE, "bf16 tensor-core MLP needs F=2, L*F<=32, W in {32,64}, H in {1,2}");
+  if (cfg->mlp_precision != PRENOM_MLP_FP32 && cfg->mlp_precision != PRENOM_MLP_BF16)
+    return fail(PRENOM_USAGE, "unknown mlp_precision");
   CUDA_TRY(cudaSetDevice(ctx->device));
   auto* o = new prenom_object_s;
   o->ctx = ctx;
@@ -733,7 +753,11 @@ prenom_status prenom_render(prenom_object_t o, int n_rays, const float* origins,
   const SampleBufs sb = bufs(o);
   CUDA_TRY(launch_sample(src, sampler_cfg(o, n_rays, o->cfg.prior_sampling, PRENOM_TAG_RENDER,
                                           (uint32_t)o->render_calls++), sb, nullptr, st));
-  CUDA_TRY(launch_field_fwd_train(o->fd, o->params.p, n_rays, S, sb, o->feat_t.p, o->out.p, o->flag.p, st));
+  if (o->cfg.mlp_precision == PRENOM_MLP_BF16)
+    CUDA_TRY(launch_fwd_tc(o->fd, o->params.p, (long long)n_rays * S, S, sb.count, sb.pos_depth, o->feat_tc.p,
+                           o->out.p, o->flag.p, st));
+  else
+    CUDA_TRY(launch_field_fwd_train(o->fd, o->params.p, n_rays, S, sb, o->feat_t.p, o->out.p, o->flag.p, st));
   CompositeArgs ca;
   std::memset(&ca, 0, sizeof ca);
   ca.B = n_rays;
@@ -949,6 +973,7 @@ namespace {
 // Points as B = n one-sample "rays" through the train-path tile kernels.
 struct PointBatch {
   DevBuf<float> params, feat_t, dfeat_t, grad;
+  DevBuf<unsigned char> feat_tc;
   DevBuf<float4> pos, out, dout;
   DevBuf<int> count, flag;
   SampleBufs sb;
@@ -958,6 +983,7 @@ struct PointBatch {
     CUDA_TRY(params.ensure(P));
     CUDA_TRY(feat_t.ensure(npad * fd.in_dim));
     CUDA_TRY(dfeat_t.ensure(npad * fd.in_dim));
+    if (tc_supported(fd)) CUDA_TRY(feat_tc.ensure(tc_feature_bytes(fd, n)));
     CUDA_TRY(pos.ensure(npad));
     CUDA_TRY(out.ensure(npad));
     CUDA_TRY(dout.ensure(npad));
@@ -1008,11 +1034,15 @@ prenom_status prenom_debug_field_eval(prenom_ctx_t ctx, const prenom_field_arch*
     if (raw) CUDA_TRY(cudaMemcpyAsync(raw, dw.p, 4 * sizeof(float) * n, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaMemcpyAsync(&hflag, flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
-  } else if (precision == 2) {
-    // the train-path tile forward (fp32 GEMM, FMA)
+  } else if (precision == 2 || precision == PRENOM_MLP_BF16) {
+    // the train-path tile forward: fp32 smem GEMMs (2) or bf16 tcgen05 (1)
+    if (precision == PRENOM_MLP_BF16 && !tc_supported(fd)) return fail(PRENOM_USAGE, "arch not supported by the bf16 path");
     PointBatch pb;
     STATUS_TRY(pb.init(fd, P, n, params, xyz, st));
-    CUDA_TRY(launch_field_fwd_train(fd, pb.params.p, n, 1, pb.sb, pb.feat_t.p, pb.out.p, pb.flag.p, st));
+    if (precision == PRENOM_MLP_BF16)
+      CUDA_TRY(launch_fwd_tc(fd, pb.params.p, n, 1, pb.count.p, pb.pos.p, pb.feat_tc.p, pb.out.p, pb.flag.p, st));
+    else
+      CUDA_TRY(launch_field_fwd_train(fd, pb.params.p, n, 1, pb.sb, pb.feat_t.p, pb.out.p, pb.flag.p, st));
     ctx->launches += 1;
     std::vector<float4> h(n);
     CUDA_TRY(cudaMemcpyAsync(h.data(), pb.out.p, sizeof(float4) * n, cudaMemcpyDeviceToHost, st));
@@ -1037,7 +1067,6 @@ prenom_status prenom_debug_field_eval(prenom_ctx_t ctx, const prenom_field_arch*
 prenom_status prenom_debug_field_backward(prenom_ctx_t ctx, const prenom_field_arch* arch, const float* params,
                                           int n, const float* xyz, const float* d_sigma, const float* d_rgb,
                                           float* grad, int precision) {
-  (void)precision;
   if (!ctx || !params || !xyz || !d_sigma || !d_rgb || !grad || n < 0) return fail(PRENOM_USAGE, "bad arguments");
   STATUS_TRY(validate_arch(arch));
   const FieldDesc fd = make_desc(*arch);
@@ -1055,10 +1084,16 @@ prenom_status prenom_debug_field_backward(prenom_ctx_t ctx, const prenom_field_a
   std::vector<float4> hd(n);
   for (int i = 0; i < n; ++i) hd[i] = make_float4(d_sigma[i], d_rgb[3 * i], d_rgb[3 * i + 1], d_rgb[3 * i + 2]);
   CUDA_TRY(cudaMemcpyAsync(pb.dout.p, hd.data(), sizeof(float4) * n, cudaMemcpyHostToDevice, st));
-  CUDA_TRY(launch_field_fwd_train(fd, pb.params.p, n, 1, pb.sb, pb.feat_t.p, pb.out.p, pb.flag.p, st));
-  CUDA_TRY(launch_mlp_bwd_train(fd, pb.params.p, pb.grad.p, n, 1, pb.count.p, pb.feat_t.p, pb.dout.p, pb.dfeat_t.p,
-                                st));
-  CUDA_TRY(launch_encode_bwd(fd, pb.params.p, pb.grad.p, n, 1, pb.count.p, pb.pos.p, pb.dfeat_t.p, st));
+  if (precision == PRENOM_MLP_BF16) {
+    if (!tc_supported(fd)) return fail(PRENOM_USAGE, "arch not supported by the bf16 path");
+    CUDA_TRY(launch_fwd_tc(fd, pb.params.p, n, 1, pb.count.p, pb.pos.p, pb.feat_tc.p, pb.out.p, pb.flag.p, st));
+    CUDA_TRY(launch_bwd_tc(fd, pb.params.p, pb.grad.p, n, 1, pb.count.p, pb.pos.p, pb.feat_tc.p, pb.dout.p, st));
+  } else {
+    CUDA_TRY(launch_field_fwd_train(fd, pb.params.p, n, 1, pb.sb, pb.feat_t.p, pb.out.p, pb.flag.p, st));
+    CUDA_TRY(launch_mlp_bwd_train(fd, pb.params.p, pb.grad.p, n, 1, pb.count.p, pb.feat_t.p, pb.dout.p,
+                                  pb.dfeat_t.p, st));
+    CUDA_TRY(launch_encode_bwd(fd, pb.params.p, pb.grad.p, n, 1, pb.count.p, pb.pos.p, pb.dfeat_t.p, st));
+  }
   ctx->launches += 3;
   CUDA_TRY(cudaMemcpyAsync(grad, pb.grad.p, P * sizeof(float), cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));

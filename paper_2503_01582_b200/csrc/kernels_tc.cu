@@ -1,0 +1,560 @@
+// kernels_tc.cu -- the density+colour MLP on 5th-gen tensor cores (tcgen05,
+// bf16 operands, fp32 accumulation in TMEM), fused with the hash-grid encode
+// (forward) and the table-gradient scatter (backward).
+//
+// Replaces field_eval's MLP (field.cpp:181-211) and field_backward
+// (field.cpp:227-293) for the bf16-MLP mode of BASELINE config 2 (parity
+// tolerance 1e-2 vs the fp32 oracle; the encode itself stays fp32 and
+// bit-exact, features are rounded to bf16 only as MMA operands).
+//
+// One CTA = 256 threads works on 128-sample tiles (UMMA M = 128; the samples
+// of a ray are contiguous). Thread 0 issues every tcgen05.mma; completion is
+// signalled through tcgen05.commit -> mbarrier. Epilogues: warp w reads TMEM
+// lane quadrant w%4 (row = sample), warps w and w+4 split the columns.
+// Operand tiles use the core-matrix layout of umma.cuh, so the backward pass
+// feeds forward activations/weights to the tensor core as MN-major
+// (transposed) operands with no data movement:
+//   fwd  H_l  = relu(H_{l-1} W_l^T + b_l)          A K-major,  B K-major
+//   bwd  dH_l = D_{l+1} W_{l+1}                    A K-major,  B MN-major
+//        dW_l += D_l^T [H_{l-1} | 1]               A MN-major, B MN-major (M=64)
+// The appended ones column makes the bias gradient column `in` of dW_l. The
+// weight-gradient accumulators live in TMEM for the whole persistent CTA and
+// are flushed with one atomicAdd per weight per CTA at the end.
+#include <algorithm>
+
+#include "prenom_device.cuh"
+#include "umma.cuh"
+
+namespace prenom {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kSlack = 1024;  // bytes after each tile: MN-major M=64 views of narrow tiles over-read
+
+// bf16 copies of the MLP weights in core-matrix layouts + fp32 biases.
+template <int INP, int W, int H>
+struct WeightTiles {
+  static constexpr int kW0 = W * INP * 2;
+  static constexpr int kWl = W * W * 2;
+  static constexpr int kWo = 16 * W * 2;
+  static constexpr int kBytes = kW0 + (H - 1) * kWl + kWo + kSlack;
+  unsigned char* w0;
+  unsigned char* wl[2];
+  unsigned char* wo;
+  float* bias;  // H*W + 4
+
+  __device__ void carve(unsigned char*& p) {
+    w0 = p;
+    p += kW0;
+    for (int l = 1; l < H; ++l) {
+      wl[l - 1] = p;
+      p += kWl;
+    }
+    wo = p;
+    p += kWo + kSlack;
+    bias = reinterpret_cast<float*>(p);
+    p += ((H * W + 4) * 4 + 15) / 16 * 16;
+  }
+
+  __device__ void load(const FieldDesc& fd, const float* __restrict__ mlp) {
+    const int IN = fd.in_dim;
+    for (int i = threadIdx.x; i < W * INP; i += kThreads) {
+      const int o = i / INP, k = i % INP;
+      const float v = k < IN ? __ldg(mlp + fd.w_off[0] + o * IN + k) : 0.f;
+      *reinterpret_cast<__nv_bfloat16*>(w0 + umma::cm_offset(o, k, INP)) = __float2bfloat16_rn(v);
+    }
+    for (int l = 1; l < H; ++l)
+      for (int i = threadIdx.x; i < W * W; i += kThreads) {
+        const int o = i / W, k = i % W;
+        *reinterpret_cast<__nv_bfloat16*>(wl[l - 1] + umma::cm_offset(o, k, W)) =
+            __float2bfloat16_rn(__ldg(mlp + fd.w_off[l] + o * W + k));
+      }
+    for (int i = threadIdx.x; i < 16 * W + kSlack / 2; i += kThreads) {
+      if (i < 16 * W) {
+        const int o = i / W, k = i % W;
+        const float v = o < 4 ? __ldg(mlp + fd.w_off[H] + o * W + k) : 0.f;
+        *reinterpret_cast<__nv_bfloat16*>(wo + umma::cm_offset(o, k, W)) = __float2bfloat16_rn(v);
+      } else {
+        reinterpret_cast<__nv_bfloat16*>(wo + 16 * W * 2)[i - 16 * W] = __float2bfloat16_rn(0.f);
+      }
+    }
+    for (int i = threadIdx.x; i < H * W + 4; i += kThreads) {
+      const int l = i / W;
+      bias[i] = l < H ? __ldg(mlp + fd.b_off[l] + (i % W)) : __ldg(mlp + fd.b_off[H] + (i - H * W));
+    }
+  }
+};
+
+__device__ __forceinline__ void sync_for_mma() {
+  umma::fence_proxy_async();
+  umma::fence_before_sync();
+  __syncthreads();
+  umma::fence_after_sync();
+}
+
+__device__ __forceinline__ void wait_mma(uint64_t* bar, uint32_t& phase) {
+  umma::mbar_wait(bar, phase);
+  phase ^= 1u;
+  umma::fence_after_sync();
+}
+
+// Epilogue: TMEM [128 x N] fp32 (cols c0..) -> +bias, ReLU -> bf16 tile [128][C].
+template <int N>
+__device__ __forceinline__ void epi_relu(uint32_t tm, int col0, const float* bias, unsigned char* tile, int C) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int q = warp & 3, half = warp >> 2;
+  const int row = 32 * q + lane;
+  constexpr int NH = N / 2;
+#pragma unroll
+  for (int c = 0; c < NH; c += 8) {
+    const int col = half * NH + c;
+    float v[8];
+    umma::tmem_ld8(umma::taddr(tm, 32 * q, col0 + col), v);
+    umma::tmem_wait_ld();
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = fmaxf(v[j] + bias[col + j], 0.f);
+    umma::st_row8(tile, row, col, C, v);
+  }
+}
+
+// ------------------------------------------------------------------ fwd
+template <int INP, int W, int H>
+__global__ void __launch_bounds__(kThreads) k_fwd_tc(FieldDesc fd, const float* __restrict__ params, long long n_total,
+                                                     int S, const int* __restrict__ count,
+                                                     const float4* __restrict__ pos, uint4* __restrict__ feat_tiles,
+                                                     float4* __restrict__ out, int* flag) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase;
+  WeightTiles<INP, W, H> wt;
+  unsigned char* p = smem;
+  wt.carve(p);
+  unsigned char* X = p;
+  p += 128 * INP * 2;
+  unsigned char* Hb[2];
+  Hb[0] = p;
+  p += 128 * W * 2;
+  Hb[1] = p;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  wt.load(fd, params + fd.hash_params);
+  for (int i = tid; i < 128 * INP; i += kThreads) reinterpret_cast<__nv_bfloat16*>(X)[i] = __float2bfloat16_rn(0.f);
+  if (warp == 0) umma::tmem_alloc(&tbase, 256);
+  if (tid == 0) {
+    umma::mbar_init(&bar, 1);
+    umma::fence_mbar_init();
+  }
+  umma::fence_before_sync();
+  __syncthreads();
+  umma::fence_after_sync();
+  const uint32_t tm = tbase;
+  uint32_t phase = 0;
+  constexpr uint32_t id_l0 = umma::idesc_bf16(128, W, false, false);
+  constexpr uint32_t id_out = umma::idesc_bf16(128, 16, false, false);
+  const long long ntiles = (n_total + kTile - 1) / kTile;
+  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const long long tile0 = t * kTile;
+    // ---- encode (fp32, bit-exact) -> bf16 X tile; 2 threads per sample
+    {
+      const int s = tid & (kTile - 1), half = tid >> 7;
+      const long long gs = tile0 + s;
+      bool valid = gs < n_total && __ldg(count + gs / S) > 0;
+      float4 pp = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (valid) pp = pos[gs];
+      const float px = clamp01(pp.x), py = clamp01(pp.y), pz = clamp01(pp.z);
+      for (int l = half; l < fd.L; l += 2) {
+        float f[2] = {0.f, 0.f};
+        if (valid) encode_level<2>(fd, params, l, px, py, pz, f);
+        *reinterpret_cast<__nv_bfloat162*>(X + umma::cm_offset(s, 2 * l, INP)) = __floats2bfloat162_rn(f[0], f[1]);
+      }
+    }
+    sync_for_mma();
+    if (tid == 0) {
+      for (int ks = 0; ks < INP / 16; ++ks)
+        umma::mma_bf16(tm, umma::desc_kmajor(X, INP, ks), umma::desc_kmajor(wt.w0, INP, ks), id_l0, ks > 0);
+      umma::commit(&bar);
+    }
+    // stored features for the backward pass (tile-major, same core-matrix layout)
+    {
+      const uint4* src = reinterpret_cast<const uint4*>(X);
+      uint4* dst = feat_tiles + t * (128 * INP * 2 / 16);
+      for (int i = tid; i < 128 * INP * 2 / 16; i += kThreads) dst[i] = src[i];
+    }
+    wait_mma(&bar, phase);
+    epi_relu<W>(tm, 0, wt.bias, Hb[0], W);
+    for (int l = 1; l < H; ++l) {
+      sync_for_mma();
+      if (tid == 0) {
+        for (int ks = 0; ks < W / 16; ++ks)
+          umma::mma_bf16(tm + l * W, umma::desc_kmajor(Hb[(l - 1) & 1], W, ks), umma::desc_kmajor(wt.wl[l - 1], W, ks),
+                         umma::idesc_bf16(128, W, false, false), ks > 0);
+        umma::commit(&bar);
+      }
+      wait_mma(&bar, phase);
+      epi_relu<W>(tm, l * W, wt.bias + l * W, Hb[l & 1], W);
+    }
+    sync_for_mma();
+    if (tid == 0) {
+      for (int ks = 0; ks < W / 16; ++ks)
+        umma::mma_bf16(tm + H * W, umma::desc_kmajor(Hb[(H - 1) & 1], W, ks), umma::desc_kmajor(wt.wo, W, ks), id_out,
+                       ks > 0);
+      umma::commit(&bar);
+    }
+    wait_mma(&bar, phase);
+    if (warp < 4) {
+      const int row = 32 * warp + lane;
+      float v[8];
+      umma::tmem_ld8(umma::taddr(tm, 32 * warp, H * W), v);
+      umma::tmem_wait_ld();
+      const long long gs = tile0 + row;
+      if (gs < n_total) {
+        float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (__ldg(count + gs / S) > 0) {
+          const float* b = wt.bias + H * W;
+          o.x = density_forward(fd.act, v[0] + b[0]);
+          o.y = stable_sigmoid(v[1] + b[1]);
+          o.z = stable_sigmoid(v[2] + b[2]);
+          o.w = stable_sigmoid(v[3] + b[3]);
+          if (!all_finite4(o.x, o.y, o.z, o.w)) atomicOr(flag, 1);
+        }
+        out[gs] = o;
+      }
+    }
+    umma::fence_before_sync();
+  }
+  __syncthreads();
+  if (warp == 0) umma::tmem_dealloc(tm, 256);
+}
+
+// ------------------------------------------------------------------ bwd
+template <int INP, int W, int H>
+struct BwdCols {
+  // TMEM column map (fp32 columns; dW regions use the M=64 lane layout)
+  static constexpr int kDWo = 0;                                  // [64 x (W+8)]
+  static constexpr int kDWl = ((W + 8 + 15) / 16) * 16;           // layer H-1 .. 1: each (W+8)
+  static constexpr int kDW0 = kDWl + (H - 1) * (((W + 8 + 15) / 16) * 16);  // [64 x (INP+8)]
+  static constexpr int kR = kDW0 + ((INP + 8 + 15) / 16) * 16;     // per-layer fwd/bwd regions, W each
+  static constexpr int kOut = kR + H * W;                         // 16
+  static constexpr int kDX = kOut + 16;                           // INP
+  static constexpr int kTotal = kDX + INP;
+  static_assert(kTotal <= 512, "TMEM budget");
+};
+
+template <int INP, int W, int H>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_bwd_tc(FieldDesc fd, const float* __restrict__ params, float* __restrict__ grad, long long n_total, int S,
+             const int* __restrict__ count, const float4* __restrict__ pos, const uint4* __restrict__ feat_tiles,
+             const float4* __restrict__ dout) {
+  using CM = BwdCols<INP, W, H>;
+  constexpr int XC = INP + 8, HC = W + 8;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase;
+  WeightTiles<INP, W, H> wt;
+  unsigned char* p = smem;
+  wt.carve(p);
+  unsigned char* X = p;  // [128][INP+8]
+  p += 128 * XC * 2 + kSlack;
+  unsigned char* Ht[2];  // [128][W+8] per hidden layer
+  for (int l = 0; l < H; ++l) {
+    Ht[l] = p;
+    p += 128 * HC * 2 + kSlack;
+  }
+  unsigned char* G = p;  // [128][16]
+  p += 128 * 16 * 2 + kSlack;
+  unsigned char* D = p;  // [128][W]
+  p += 128 * W * 2 + kSlack;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  wt.load(fd, params + fd.hash_params);
+  // zero every activation tile (+slack) once; then set the ones columns
+  {
+    uint4* z = reinterpret_cast<uint4*>(X);
+    const int n16 = (int)((p - X) / 16);
+    for (int i = tid; i < n16; i += kThreads) z[i] = make_uint4(0u, 0u, 0u, 0u);
+  }
+  __syncthreads();
+  const __nv_bfloat16 one = __float2bfloat16_rn(1.f);
+  for (int r = tid; r < 128; r += kThreads) {
+    *reinterpret_cast<__nv_bfloat16*>(X + umma::cm_offset(r, INP, XC)) = one;
+    for (int l = 0; l < H; ++l) *reinterpret_cast<__nv_bfloat16*>(Ht[l] + umma::cm_offset(r, W, HC)) = one;
+  }
+  if (warp == 0) umma::tmem_alloc(&tbase, 512);
+  if (tid == 0) {
+    umma::mbar_init(&bar, 1);
+    umma::fence_mbar_init();
+  }
+  umma::fence_before_sync();
+  __syncthreads();
+  umma::fence_after_sync();
+  const uint32_t tm = tbase;
+  uint32_t phase = 0;
+  const long long ntiles = (n_total + kTile - 1) / kTile;
+  int iter = 0;
+  const int q = warp & 3, half = warp >> 2, row = 32 * q + lane;
+  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x, ++iter) {
+    const long long tile0 = t * kTile;
+    const long long gs = tile0 + row;
+    const bool valid = gs < n_total && __ldg(count + gs / S) > 0;
+    // ---- stored bf16 features -> X (row-group stride differs: copy per 16 B)
+    {
+      const uint4* src = feat_tiles + t * (128 * INP * 2 / 16);
+      for (int i = tid; i < 128 * INP * 2 / 16; i += kThreads) {
+        const int rg = i / (INP / 8 * 8), rem = i % (INP / 8 * 8);  // 16 B units inside a row group
+        const int chunk = rem / 8, r8 = rem % 8;
+        *reinterpret_cast<uint4*>(X + rg * (XC / 8) * 128 + chunk * 128 + r8 * 16) = src[i];
+      }
+    }
+    sync_for_mma();
+    // ---- forward recompute
+    if (tid == 0) {
+      for (int ks = 0; ks < INP / 16; ++ks)
+        umma::mma_bf16(tm + CM::kR, umma::desc_kmajor(X, XC, ks), umma::desc_kmajor(wt.w0, INP, ks),
+                       umma::idesc_bf16(128, W, false, false), ks > 0);
+      umma::commit(&bar);
+    }
+    wait_mma(&bar, phase);
+    epi_relu<W>(tm, CM::kR, wt.bias, Ht[0], HC);
+    for (int l = 1; l < H; ++l) {
+      sync_for_mma();
+      if (tid == 0) {
+        for (int ks = 0; ks < W / 16; ++ks)
+          umma::mma_bf16(tm + CM::kR + l * W, umma::desc_kmajor(Ht[l - 1], HC, ks),
+                         umma::desc_kmajor(wt.wl[l - 1], W, ks), umma::idesc_bf16(128, W, false, false), ks > 0);
+        umma::commit(&bar);
+      }
+      wait_mma(&bar, phase);
+      epi_relu<W>(tm, CM::kR + l * W, wt.bias + l * W, Ht[l], HC);
+    }
+    sync_for_mma();
+    if (tid == 0) {
+      for (int ks = 0; ks < W / 16; ++ks)
+        umma::mma_bf16(tm + CM::kOut, umma::desc_kmajor(Ht[H - 1], HC, ks), umma::desc_kmajor(wt.wo, W, ks),
+                       umma::idesc_bf16(128, 16, false, false), ks > 0);
+      umma::commit(&bar);
+    }
+    wait_mma(&bar, phase);
+    // ---- g_raw (field.cpp:233-238) -> G tile
+    if (warp < 4) {
+      float v[8];
+      umma::tmem_ld8(umma::taddr(tm, 32 * q, CM::kOut), v);
+      umma::tmem_wait_ld();
+      float g[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      if (valid) {
+        const float4 d = dout[gs];
+        const float* b = wt.bias + H * W;
+        const float r0 = v[0] + b[0];
+        const float sg = density_forward(fd.act, r0);
+        g[0] = d.x * density_derivative(fd.act, r0, sg);
+        const float s1 = stable_sigmoid(v[1] + b[1]), s2 = stable_sigmoid(v[2] + b[2]), s3 = stable_sigmoid(v[3] + b[3]);
+        g[1] = d.y * s1 * (1.f - s1);
+        g[2] = d.z * s2 * (1.f - s2);
+        g[3] = d.w * s3 * (1.f - s3);
+      }
+      umma::st_row8(G, row, 0, 16, g);
+    }
+    sync_for_mma();
+    // ---- output layer: dW_out += G^T [H_{H-1} | 1];  dH_{H-1} = G W_out
+    if (tid == 0) {
+      for (int ks = 0; ks < 8; ++ks)
+        umma::mma_bf16(tm + CM::kDWo, umma::desc_mnmajor(G, 16, ks), umma::desc_mnmajor(Ht[H - 1], HC, ks),
+                       umma::idesc_bf16(64, HC, true, true), (iter > 0 || ks > 0));
+      umma::mma_bf16(tm + CM::kR + (H - 1) * W, umma::desc_kmajor(G, 16, 0), umma::desc_mnmajor(wt.wo, W, 0),
+                     umma::idesc_bf16(128, W, false, true), 0u);
+      umma::commit(&bar);
+    }
+    wait_mma(&bar, phase);
+    for (int l = H - 1; l >= 0; --l) {
+      // D_l = dH_l * relu'(H_l) -> D tile
+      {
+        constexpr int NH = W / 2;
+#pragma unroll
+        for (int c = 0; c < NH; c += 8) {
+          const int col = half * NH + c;
+          float v[8];
+          umma::tmem_ld8(umma::taddr(tm, 32 * q, CM::kR + l * W + col), v);
+          umma::tmem_wait_ld();
+          const uint4 hv = *reinterpret_cast<const uint4*>(Ht[l] + umma::cm_offset(row, col, HC));
+          const __nv_bfloat16* hb = reinterpret_cast<const __nv_bfloat16*>(&hv);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v[j] = __bfloat162float(hb[j]) > 0.f ? v[j] : 0.f;
+          umma::st_row8(D, row, col, W, v);
+        }
+      }
+      sync_for_mma();
+      if (tid == 0) {
+        const int dwc = l == 0 ? CM::kDW0 : CM::kDWl + (H - 1 - l) * (((W + 8 + 15) / 16) * 16);
+        const unsigned char* prev = l == 0 ? X : Ht[l - 1];
+        const int pc = l == 0 ? XC : HC;
+        for (int ks = 0; ks < 8; ++ks)
+          umma::mma_bf16(tm + dwc, umma::desc_mnmajor(D, W, ks), umma::desc_mnmajor(prev, pc, ks),
+                         umma::idesc_bf16(64, pc, true, true), (iter > 0 || ks > 0));
+        if (l > 0) {
+          for (int ks = 0; ks < W / 16; ++ks)
+            umma::mma_bf16(tm + CM::kR + (l - 1) * W, umma::desc_kmajor(D, W, ks), umma::desc_mnmajor(wt.wl[l - 1], W, ks),
+                           umma::idesc_bf16(128, W, false, true), ks > 0);
+        } else {
+          for (int ks = 0; ks < W / 16; ++ks)
+            umma::mma_bf16(tm + CM::kDX, umma::desc_kmajor(D, W, ks), umma::desc_mnmajor(wt.w0, INP, ks),
+                           umma::idesc_bf16(128, INP, false, true), ks > 0);
+        }
+        umma::commit(&bar);
+      }
+      wait_mma(&bar, phase);
+    }
+    // ---- d_features -> table-gradient scatter (field.cpp:279-292), fused
+    {
+      constexpr int NH = INP / 2;  // columns of this thread's half
+      float v[NH];
+#pragma unroll
+      for (int c = 0; c < NH; c += 8) umma::tmem_ld8(umma::taddr(tm, 32 * q, CM::kDX + half * NH + c), v + c);
+      umma::tmem_wait_ld();  // (warp-collective loads stay outside the per-sample branch)
+      if (valid) {
+        const float4 pp = pos[gs];
+        const float px = clamp01(pp.x), py = clamp01(pp.y), pz = clamp01(pp.z);
+#pragma unroll
+        for (int j = 0; j < NH; j += 2) {
+          const int l = (half * NH + j) >> 1;
+          if (l >= fd.L) continue;
+          if (v[j] == 0.f && v[j + 1] == 0.f) continue;
+          const LevelCell cell = level_cell(fd.res[l], px, py, pz);
+          float* gl = grad + (long long)l * 2 * fd.rows;
+#pragma unroll
+          for (int corner = 0; corner < 8; ++corner) {
+            const float w = corner_weight(cell, corner);
+            if (w == 0.f) continue;
+            const uint32_t r = table_row(fd, l, (uint32_t)(cell.cx + (corner & 1)),
+                                         (uint32_t)(cell.cy + ((corner >> 1) & 1)),
+                                         (uint32_t)(cell.cz + ((corner >> 2) & 1)));
+            atomicAdd(reinterpret_cast<float2*>(gl + (size_t)r * 2), make_float2(w * v[j], w * v[j + 1]));
+          }
+        }
+      }
+    }
+    umma::fence_before_sync();
+  }
+  // ---- flush the TMEM weight-gradient accumulators (one atomic per weight per CTA)
+  __syncthreads();
+  umma::fence_after_sync();
+  if (iter > 0 && warp < 4) {
+    float* gm = grad + fd.hash_params;
+    const int r = 16 * warp + lane;  // M=64 layout: rows 16q..16q+15 in lanes 32q..32q+15
+    auto flush = [&](int col0, int rows, int in, int w_off, int b_off) {
+      for (int c = 0; c < in + 8; c += 8) {
+        float v[8];
+        umma::tmem_ld8(umma::taddr(tm, 32 * warp, col0 + c), v);
+        umma::tmem_wait_ld();
+        if (lane < 16 && r < rows)
+          for (int j = 0; j < 8; ++j) {
+            const int k = c + j;
+            if (k < in) atomicAdd(gm + w_off + r * in + k, v[j]);
+            else if (k == in) atomicAdd(gm + b_off + r, v[j]);
+          }
+      }
+    };
+    flush(CM::kDWo, 4, W, fd.w_off[H], fd.b_off[H]);
+    for (int l = H - 1; l >= 1; --l)
+      flush(CM::kDWl + (H - 1 - l) * (((W + 8 + 15) / 16) * 16), W, W, fd.w_off[l], fd.b_off[l]);
+    // layer 0: columns >= in_dim (zero padding up to INP) are skipped; bias sits at column INP
+    for (int c = 0; c < INP + 8; c += 8) {
+      float v[8];
+      umma::tmem_ld8(umma::taddr(tm, 32 * warp, CM::kDW0 + c), v);
+      umma::tmem_wait_ld();
+      if (lane < 16 && r < W)
+        for (int j = 0; j < 8; ++j) {
+          const int k = c + j;
+          if (k < fd.in_dim) atomicAdd(gm + fd.w_off[0] + r * fd.in_dim + k, v[j]);
+          else if (k == INP) atomicAdd(gm + fd.b_off[0] + r, v[j]);
+        }
+    }
+  }
+  umma::fence_before_sync();
+  __syncthreads();
+  if (warp == 0) umma::tmem_dealloc(tm, 512);
+}
+
+int g_sms = 0;
+int sms() {
+  if (!g_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return g_sms;
+}
+
+template <int INP, int W, int H>
+size_t fwd_smem() {
+  return WeightTiles<INP, W, H>::kBytes + ((H * W + 4) * 4 + 15) / 16 * 16 + 128 * INP * 2 + 2 * 128 * W * 2 + 1024;
+}
+
+template <int INP, int W, int H>
+size_t bwd_smem() {
+  return WeightTiles<INP, W, H>::kBytes + ((H * W + 4) * 4 + 15) / 16 * 16 + (128 * (INP + 8) * 2 + kSlack) +
+         H * (128 * (W + 8) * 2 + kSlack) + (128 * 16 * 2 + kSlack) + (128 * W * 2 + kSlack) + 1024;
+}
+
+template <int INP, int W, int H>
+cudaError_t run_fwd(const FieldDesc& fd, const float* params, long long n, int S, const int* count, const float4* pos,
+                    void* feat_tiles, float4* out, int* flag, cudaStream_t st) {
+  // >= 80 KB so at most two CTAs (2 x 256 TMEM columns) share an SM
+  const size_t smem = std::max<size_t>(fwd_smem<INP, W, H>(), 80 * 1024);
+  cudaError_t e = cudaFuncSetAttribute(k_fwd_tc<INP, W, H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const long long ntiles = (n + kTile - 1) / kTile;
+  const long long grid = std::min<long long>(ntiles, 2LL * sms());
+  k_fwd_tc<INP, W, H><<<(unsigned)grid, kThreads, smem, st>>>(fd, params, n, S, count, pos,
+                                                              reinterpret_cast<uint4*>(feat_tiles), out, flag);
+  return cudaGetLastError();
+}
+
+template <int INP, int W, int H>
+cudaError_t run_bwd(const FieldDesc& fd, const float* params, float* grad, long long n, int S, const int* count,
+                    const float4* pos, const void* feat_tiles, const float4* dout, cudaStream_t st) {
+  const size_t smem = std::max<size_t>(bwd_smem<INP, W, H>(), 120 * 1024);  // one CTA (512 TMEM cols) per SM
+  cudaError_t e = cudaFuncSetAttribute(k_bwd_tc<INP, W, H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const long long ntiles = (n + kTile - 1) / kTile;
+  const long long grid = std::min<long long>(ntiles, (long long)sms());
+  k_bwd_tc<INP, W, H><<<(unsigned)grid, kThreads, smem, st>>>(fd, params, grad, n, S, count, pos,
+                                                              reinterpret_cast<const uint4*>(feat_tiles), dout);
+  return cudaGetLastError();
+}
+
+#define PRENOM_TC_DISPATCH(FN, ...)                                                          \
+  do {                                                                                       \
+    const int inp = fd.in_dim <= 16 ? 16 : 32;                                               \
+    if (inp == 16 && fd.W == 32 && fd.H == 1) return FN<16, 32, 1>(__VA_ARGS__);             \
+    if (inp == 16 && fd.W == 32 && fd.H == 2) return FN<16, 32, 2>(__VA_ARGS__);             \
+    if (inp == 16 && fd.W == 64 && fd.H == 1) return FN<16, 64, 1>(__VA_ARGS__);             \
+    if (inp == 16 && fd.W == 64 && fd.H == 2) return FN<16, 64, 2>(__VA_ARGS__);             \
+    if (inp == 32 && fd.W == 32 && fd.H == 1) return FN<32, 32, 1>(__VA_ARGS__);             \
+    if (inp == 32 && fd.W == 32 && fd.H == 2) return FN<32, 32, 2>(__VA_ARGS__);             \
+    if (inp == 32 && fd.W == 64 && fd.H == 1) return FN<32, 64, 1>(__VA_ARGS__);             \
+    if (inp == 32 && fd.W == 64 && fd.H == 2) return FN<32, 64, 2>(__VA_ARGS__);             \
+    return cudaErrorInvalidValue;                                                            \
+  } while (0)
+
+}  // namespace
+
+bool tc_supported(const FieldDesc& fd) {
+  return fd.F == 2 && fd.in_dim <= 32 && (fd.W == 32 || fd.W == 64) && (fd.H == 1 || fd.H == 2);
+}
+
+size_t tc_feature_bytes(const FieldDesc& fd, long long n) {
+  const int inp = fd.in_dim <= 16 ? 16 : 32;
+  return (size_t)((n + kTile - 1) / kTile) * kTile * inp * 2;
+}
+
+cudaError_t launch_fwd_tc(const FieldDesc& fd, const float* params, long long n, int S, const int* count,
+                          const float4* pos, void* feat_tiles, float4* out, int* flag, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  PRENOM_TC_DISPATCH(run_fwd, fd, params, n, S, count, pos, feat_tiles, out, flag, st);
+}
+
+cudaError_t launch_bwd_tc(const FieldDesc& fd, const float* params, float* grad, long long n, int S,
+                          const int* count, const float4* pos, const void* feat_tiles, const float4* dout,
+                          cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  PRENOM_TC_DISPATCH(run_bwd, fd, params, grad, n, S, count, pos, feat_tiles, dout, st);
+}
+
+}  // namespace prenom

@@ -302,3 +302,52 @@ def test_tcgen05_tile_gemm(ctx, rng, M, N, K, a_mn, b_mn):
 
     ref = (torch.from_numpy(A).bfloat16().float() @ torch.from_numpy(B).bfloat16().float().T).numpy()
     np.testing.assert_allclose(D, ref, rtol=1e-3, atol=1e-3)
+
+
+def tc_archs():
+    return [scenes.cfg1_arch(),
+            FieldArch(hash_levels=16, features_per_level=2, log2_table_size=14, base_resolution=16,
+                      per_level_scale=scenes.cfg2_arch().per_level_scale, hidden_width=64, hidden_layers=2),
+            FieldArch(hash_levels=12, features_per_level=2, log2_table_size=13, base_resolution=8,
+                      per_level_scale=1.4, hidden_width=32, hidden_layers=1, density_activation=1),
+            FieldArch(hash_levels=8, features_per_level=2, log2_table_size=12, base_resolution=8,
+                      per_level_scale=1.4, hidden_width=64, hidden_layers=1)]
+
+
+def test_bf16_tensor_core_forward_within_1e2(ctx, oracle, rng):
+    """north_star: MLP outputs within 1e-2 where the MLP runs in bf16 (fp32 accumulate)."""
+    for a in tc_archs():
+        params = grad_params(a, rng) * 0.5
+        xyz = rng.uniform(0, 1, (1000, 3)).astype(np.float32)
+        s, c, _ = T.debug_field_eval(ctx, a, params, xyz, precision=1)
+        so, co = oracle.field_eval(a, params, xyz)
+        np.testing.assert_allclose(np.log(s), np.log(so), atol=2e-2)  # sigma = exp(raw): 1e-2-ish on raw
+        np.testing.assert_allclose(c, co, atol=1e-2)
+
+
+def test_bf16_tensor_core_backward(ctx, oracle, rng):
+    for a in tc_archs():
+        params = grad_params(a, rng) * 0.5
+        n = 700
+        xyz = rng.uniform(0, 1, (n, 3)).astype(np.float32)
+        ds = rng.standard_normal(n).astype(np.float32) * 0.1
+        dr = rng.standard_normal((n, 3)).astype(np.float32)
+        g = T.debug_field_backward(ctx, a, params, xyz, ds, dr, precision=1)
+        go = oracle.field_backward(a, params, xyz, ds, dr)
+        nh = a.hash_param_count()
+        for part in (slice(0, nh), slice(nh, None)):
+            num = np.linalg.norm(g[part] - go[part])
+            den = np.linalg.norm(go[part])
+            assert num <= 2e-2 * den, (a, part, num / den)
+
+
+def test_bf16_train_loss_tracks_fp32_oracle(ctx, oracle):
+    sc, grid = small_scene(res=40, views=5)
+    arch = FieldArch(hash_levels=8, features_per_level=2, log2_table_size=11, base_resolution=6,
+                     per_level_scale=1.5, hidden_width=32, hidden_layers=2)
+    cfg = TrainConfig(rays_per_iter=256, samples_per_ray=32, prior_sampling=1, grid_refresh_every=50, mlp_precision=1)
+    gpu, ob = make_pair(ctx, oracle, arch, cfg, sc, grid, seed=4)
+    lg = np.array([s["total"] for s in gpu.train_step(200)])
+    lo = np.array([s["total"] for s in ob.train_step(200)])
+    assert lo[-20:].mean() < 0.8 * lo[:5].mean()
+    assert abs(lg[-20:].mean() / lo[-20:].mean() - 1) < 0.03, (lg[-20:].mean(), lo[-20:].mean())
