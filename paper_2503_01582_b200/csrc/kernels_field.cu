@@ -368,31 +368,58 @@ template <int F>
 __global__ void __launch_bounds__(256) k_encode_bwd(FieldDesc fd, float* grad, long long n_total, int S,
                                                     const int* count, const float4* __restrict__ pos,
                                                     const float* __restrict__ dfeat_t, long long ld_t) {
+  // Consecutive lanes = consecutive depth-sorted samples of a ray: equal
+  // (ray, cell) keys form contiguous runs; a segmented suffix sum leaves each
+  // run's corner totals in its first lane, which alone issues the atomics.
   const long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const int l = blockIdx.y;
-  if (!sample_valid(s, n_total, S, count)) return;
+  const int l = blockIdx.y, lane = threadIdx.x & 31;
+  const bool valid = sample_valid(s, n_total, S, count);
   float d[F];
-  bool any = false;
 #pragma unroll
-  for (int j = 0; j < F; ++j) {
-    d[j] = dfeat_t[(long long)(l * F + j) * ld_t + s];
-    any |= d[j] != 0.f;
-  }
-  if (!any) return;
-  const float4 p = pos[s];
+  for (int j = 0; j < F; ++j) d[j] = valid ? dfeat_t[(long long)(l * F + j) * ld_t + s] : 0.f;
+  float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (valid) p = pos[s];
   const LevelCell c = level_cell(fd.res[l], clamp01(p.x), clamp01(p.y), clamp01(p.z));
-  float* g = grad + (long long)l * F * fd.rows;
+  const unsigned long long key =
+      (valid && fd.res[l] < 4096)
+          ? (((unsigned long long)(s / S) << 36) | ((unsigned long long)c.cz << 24) | ((unsigned long long)c.cy << 12) |
+             (unsigned long long)c.cx)
+          : (~0ull - (unsigned long long)lane);
+  float v[8][F];
 #pragma unroll
   for (int corner = 0; corner < 8; ++corner) {
     const float w = corner_weight(c, corner);
-    if (w == 0.f) continue;
+#pragma unroll
+    for (int j = 0; j < F; ++j) v[corner][j] = w * d[j];
+  }
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const unsigned long long ok = __shfl_down_sync(0xffffffffu, key, off);
+    const bool take = (lane + off < 32) && ok == key;
+#pragma unroll
+    for (int corner = 0; corner < 8; ++corner)
+#pragma unroll
+      for (int j = 0; j < F; ++j) {
+        const float t = __shfl_down_sync(0xffffffffu, v[corner][j], off);
+        if (take) v[corner][j] += t;
+      }
+  }
+  const unsigned long long pk = __shfl_up_sync(0xffffffffu, key, 1);
+  if (!valid || (lane != 0 && pk == key)) return;
+  float* g = grad + (long long)l * F * fd.rows;
+#pragma unroll
+  for (int corner = 0; corner < 8; ++corner) {
+    bool any = false;
+#pragma unroll
+    for (int j = 0; j < F; ++j) any |= v[corner][j] != 0.f;
+    if (!any) continue;
     const uint32_t row = table_row(fd, l, (uint32_t)(c.cx + (corner & 1)), (uint32_t)(c.cy + ((corner >> 1) & 1)),
                                    (uint32_t)(c.cz + ((corner >> 2) & 1)));
     if constexpr (F == 2) {
-      atomicAdd(reinterpret_cast<float2*>(g + (size_t)row * 2), make_float2(w * d[0], w * d[1]));
+      atomicAdd(reinterpret_cast<float2*>(g + (size_t)row * 2), make_float2(v[corner][0], v[corner][1]));
     } else {
 #pragma unroll
-      for (int j = 0; j < F; ++j) atomicAdd(g + (size_t)row * F + j, w * d[j]);
+      for (int j = 0; j < F; ++j) atomicAdd(g + (size_t)row * F + j, v[corner][j]);
     }
   }
 }

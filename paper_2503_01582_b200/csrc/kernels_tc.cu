@@ -407,24 +407,51 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int c = 0; c < NH; c += 8) umma::tmem_ld8(umma::taddr(tm, 32 * q, CM::kDX + half * NH + c), v + c);
       umma::tmem_wait_ld();  // (warp-collective loads stay outside the per-sample branch)
-      if (valid) {
-        const float4 pp = pos[gs];
-        const float px = clamp01(pp.x), py = clamp01(pp.y), pz = clamp01(pp.z);
+      float4 pp = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (valid) pp = pos[gs];
+      const float px = clamp01(pp.x), py = clamp01(pp.y), pz = clamp01(pp.z);
+      const unsigned long long ray_key = (unsigned long long)(gs / S) << 36;
 #pragma unroll
-        for (int j = 0; j < NH; j += 2) {
-          const int l = (half * NH + j) >> 1;
-          if (l >= fd.L) continue;
-          if (v[j] == 0.f && v[j + 1] == 0.f) continue;
-          const LevelCell cell = level_cell(fd.res[l], px, py, pz);
+      for (int j = 0; j < NH; j += 2) {
+        const int l = (half * NH + j) >> 1;  // warp-uniform
+        if (l >= fd.L) continue;
+        const LevelCell cell = level_cell(fd.res[l], px, py, pz);
+        // Samples of a ray are depth-sorted and a line enters each cell once, so
+        // equal (ray, cell) keys form contiguous lane runs: a segmented suffix
+        // sum leaves each run's total in its first lane, which alone issues the
+        // 8 corner atomics (field.cpp:279-292 scatter, de-duplicated).
+        const unsigned long long key =
+            valid ? (ray_key | ((unsigned long long)(cell.cz & 4095) << 24) | ((unsigned long long)(cell.cy & 4095) << 12) |
+                     (unsigned long long)(cell.cx & 4095))
+                  : (~0ull - (unsigned long long)lane);
+        const float d0 = valid ? v[j] : 0.f, d1 = valid ? v[j + 1] : 0.f;
+        float c[16];
+#pragma unroll
+        for (int corner = 0; corner < 8; ++corner) {
+          const float w = corner_weight(cell, corner);
+          c[2 * corner] = w * d0;
+          c[2 * corner + 1] = w * d1;
+        }
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const unsigned long long ok = __shfl_down_sync(0xffffffffu, key, off);
+          const bool take = (lane + off < 32) && ok == key;
+#pragma unroll
+          for (int k = 0; k < 16; ++k) {
+            const float t = __shfl_down_sync(0xffffffffu, c[k], off);
+            if (take) c[k] += t;
+          }
+        }
+        const unsigned long long pk = __shfl_up_sync(0xffffffffu, key, 1);
+        if (valid && (lane == 0 || pk != key)) {
           float* gl = grad + (long long)l * 2 * fd.rows;
 #pragma unroll
           for (int corner = 0; corner < 8; ++corner) {
-            const float w = corner_weight(cell, corner);
-            if (w == 0.f) continue;
+            if (c[2 * corner] == 0.f && c[2 * corner + 1] == 0.f) continue;
             const uint32_t r = table_row(fd, l, (uint32_t)(cell.cx + (corner & 1)),
                                          (uint32_t)(cell.cy + ((corner >> 1) & 1)),
                                          (uint32_t)(cell.cz + ((corner >> 2) & 1)));
-            atomicAdd(reinterpret_cast<float2*>(gl + (size_t)r * 2), make_float2(w * v[j], w * v[j + 1]));
+            atomicAdd(reinterpret_cast<float2*>(gl + (size_t)r * 2), make_float2(c[2 * corner], c[2 * corner + 1]));
           }
         }
       }
@@ -536,6 +563,8 @@ cudaError_t run_bwd(const FieldDesc& fd, const float* params, float* grad, long 
 }  // namespace
 
 bool tc_supported(const FieldDesc& fd) {
+  for (int l = 0; l < fd.L; ++l)
+    if (fd.res[l] >= 4096) return false;  // scatter de-dup key packs 12-bit cell coordinates
   return fd.F == 2 && fd.in_dim <= 32 && (fd.W == 32 || fd.W == 64) && (fd.H == 1 || fd.H == 2);
 }
 

@@ -325,7 +325,82 @@ def test_bf16_tensor_core_forward_within_1e2(ctx, oracle, rng):
         np.testing.assert_allclose(c, co, atol=1e-2)
 
 
+def bf16_reference_backward(oracle, a, params, xyz, ds, dr):
+    """Torch fp32 reference of the bf16 tensor-core MLP backward: identical
+    bf16 operand roundings (features, activations, weights, upstream grads),
+    fp32 accumulation, the same recomputed ReLU masks; table gradient
+    scattered with the oracle's corner rows/weights."""
+    import torch
+
+    bf = lambda t: t.to(torch.bfloat16).to(torch.float32)
+    feat, rows, w = oracle.hash_encode(a, params, xyz)
+    P = torch.from_numpy(params)
+    nh = a.hash_param_count()
+    IN, W, H = a.hash_levels * a.features_per_level, a.hidden_width, a.hidden_layers
+    off, Ws, Bs, ins = nh, [], [], []
+    i = IN
+    for l in range(H + 1):
+        o = W if l < H else 4
+        Ws.append(P[off:off + o * i].reshape(o, i))
+        Bs.append(P[off + o * i: off + o * i + o])
+        ins.append(i)
+        off += o * i + o
+        i = o
+    X = bf(torch.from_numpy(feat))
+    acts = [X]
+    h = X
+    for l in range(H):
+        h = bf(torch.relu(h @ bf(Ws[l]).T + Bs[l]))
+        acts.append(h)
+    raw = h @ bf(Ws[H]).T + Bs[H]
+    if a.density_activation == 0:
+        sg = torch.clamp(torch.exp(torch.clamp(raw[:, 0], max=10.0)), max=1e4)
+        d0 = torch.where(sg < 1e4, sg, torch.zeros_like(sg))
+    else:
+        sg = torch.nn.functional.softplus(raw[:, 0])
+        d0 = torch.sigmoid(raw[:, 0])
+    rgb = torch.sigmoid(raw[:, 1:4])
+    G = torch.zeros(len(xyz), 4)
+    G[:, 0] = torch.from_numpy(ds) * d0
+    G[:, 1:] = torch.from_numpy(dr) * rgb * (1 - rgb)
+    Gb = bf(G)
+    grad = torch.zeros(len(params))
+    off_w = []
+    off = nh
+    for l in range(H + 1):
+        o = W if l < H else 4
+        off_w.append((off, off + o * ins[l]))
+        off += o * ins[l] + o
+    D = Gb
+    for l in range(H, -1, -1):
+        prev = acts[l]
+        wo, bo = off_w[l]
+        grad[wo:bo] = (D.T @ prev).reshape(-1)
+        grad[bo:bo + D.shape[1]] = D.sum(0)
+        dprev = D @ bf(Ws[l])
+        if l > 0:
+            D = bf(dprev * (acts[l] > 0))
+        else:
+            dX = dprev
+    g = grad.numpy()
+    dX = dX.numpy()
+    L, F = a.hash_levels, a.features_per_level
+    T = 1 << a.log2_table_size
+    for l in range(L):
+        for c in range(8):
+            wc = w[:, l * 8 + c]
+            r = rows[:, l * 8 + c].astype(np.int64)
+            m = wc != 0
+            for f in range(F):
+                np.add.at(g, l * F * T + r[m] * F + f, (wc * dX[:, l * F + f])[m])
+    return g
+
+
 def test_bf16_tensor_core_backward(ctx, oracle, rng):
+    """Numerics of the tcgen05 backward vs a torch fp32 reference with the same
+    bf16 roundings (1e-3), and vs the fp32 oracle at the bf16 level for the MLP
+    weights (the fp32 oracle's ReLU masks differ near zero, so the table
+    gradient is only checked against the bf16-aware reference)."""
     for a in tc_archs():
         params = grad_params(a, rng) * 0.5
         n = 700
@@ -333,12 +408,14 @@ def test_bf16_tensor_core_backward(ctx, oracle, rng):
         ds = rng.standard_normal(n).astype(np.float32) * 0.1
         dr = rng.standard_normal((n, 3)).astype(np.float32)
         g = T.debug_field_backward(ctx, a, params, xyz, ds, dr, precision=1)
-        go = oracle.field_backward(a, params, xyz, ds, dr)
+        ref = bf16_reference_backward(oracle, a, params, xyz, ds, dr)
         nh = a.hash_param_count()
         for part in (slice(0, nh), slice(nh, None)):
-            num = np.linalg.norm(g[part] - go[part])
-            den = np.linalg.norm(go[part])
-            assert num <= 2e-2 * den, (a, part, num / den)
+            num = np.linalg.norm(g[part] - ref[part])
+            den = np.linalg.norm(ref[part])
+            assert num <= 2e-3 * den, (a, part, num / den)
+        go = oracle.field_backward(a, params, xyz, ds, dr)
+        assert np.linalg.norm(g[nh:] - go[nh:]) <= 0.1 * np.linalg.norm(go[nh:])
 
 
 def test_bf16_train_loss_tracks_fp32_oracle(ctx, oracle):
