@@ -396,6 +396,7 @@ __global__ void __launch_bounds__(256) k_encode_bwd(FieldDesc fd, float* grad, l
   for (int off = 1; off < 32; off <<= 1) {
     const unsigned long long ok = __shfl_down_sync(0xffffffffu, key, off);
     const bool take = (lane + off < 32) && ok == key;
+    if (!__any_sync(0xffffffffu, take)) break;  // no run longer than off
 #pragma unroll
     for (int corner = 0; corner < 8; ++corner)
 #pragma unroll

@@ -29,7 +29,7 @@ namespace prenom {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kSlack = 1024;  // bytes after each tile: MN-major M=64 views of narrow tiles over-read
+constexpr int kSlack = 2048;  // bytes after each tile: M=128 MN-major views of narrow tiles over-read (finite garbage rows)
 
 // bf16 copies of the MLP weights in core-matrix layouts + fp32 biases.
 template <int INP, int W, int H>
@@ -138,7 +138,9 @@ __global__ void __launch_bounds__(kThreads) k_fwd_tc(FieldDesc fd, const float* 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   wt.load(fd, params + fd.hash_params);
   for (int i = tid; i < 128 * INP; i += kThreads) reinterpret_cast<__nv_bfloat16*>(X)[i] = __float2bfloat16_rn(0.f);
-  if (warp == 0) umma::tmem_alloc(&tbase, 256);
+  // One 64-column TMEM region serves every layer: each MMA is issued only
+  // after the previous epilogue drained it (sync_for_mma), so up to 8 CTAs fit.
+  if (warp == 0) umma::tmem_alloc(&tbase, 64);
   if (tid == 0) {
     umma::mbar_init(&bar, 1);
     umma::fence_mbar_init();
@@ -185,17 +187,17 @@ __global__ void __launch_bounds__(kThreads) k_fwd_tc(FieldDesc fd, const float* 
       sync_for_mma();
       if (tid == 0) {
         for (int ks = 0; ks < W / 16; ++ks)
-          umma::mma_bf16(tm + l * W, umma::desc_kmajor(Hb[(l - 1) & 1], W, ks), umma::desc_kmajor(wt.wl[l - 1], W, ks),
+          umma::mma_bf16(tm, umma::desc_kmajor(Hb[(l - 1) & 1], W, ks), umma::desc_kmajor(wt.wl[l - 1], W, ks),
                          umma::idesc_bf16(128, W, false, false), ks > 0);
         umma::commit(&bar);
       }
       wait_mma(&bar, phase);
-      epi_relu<W>(tm, l * W, wt.bias + l * W, Hb[l & 1], W);
+      epi_relu<W>(tm, 0, wt.bias + l * W, Hb[l & 1], W);
     }
     sync_for_mma();
     if (tid == 0) {
       for (int ks = 0; ks < W / 16; ++ks)
-        umma::mma_bf16(tm + H * W, umma::desc_kmajor(Hb[(H - 1) & 1], W, ks), umma::desc_kmajor(wt.wo, W, ks), id_out,
+        umma::mma_bf16(tm, umma::desc_kmajor(Hb[(H - 1) & 1], W, ks), umma::desc_kmajor(wt.wo, W, ks), id_out,
                        ks > 0);
       umma::commit(&bar);
     }
@@ -203,7 +205,7 @@ __global__ void __launch_bounds__(kThreads) k_fwd_tc(FieldDesc fd, const float* 
     if (warp < 4) {
       const int row = 32 * warp + lane;
       float v[8];
-      umma::tmem_ld8(umma::taddr(tm, 32 * warp, H * W), v);
+      umma::tmem_ld8(umma::taddr(tm, 32 * warp, 0), v);
       umma::tmem_wait_ld();
       const long long gs = tile0 + row;
       if (gs < n_total) {
@@ -222,21 +224,22 @@ __global__ void __launch_bounds__(kThreads) k_fwd_tc(FieldDesc fd, const float* 
     umma::fence_before_sync();
   }
   __syncthreads();
-  if (warp == 0) umma::tmem_dealloc(tm, 256);
+  if (warp == 0) umma::tmem_dealloc(tm, 64);
 }
 
 // ------------------------------------------------------------------ bwd
+// TMEM column map (fp32, M=128 lane layout everywhere; 256 columns per CTA so
+// two CTAs share an SM). Weight gradients are accumulated transposed,
+// dW_l^T = [H_{l-1} | 1]^T D_l (rows = input units + the ones row = bias),
+// so every accumulator is an M=128 tile: the output layer needs 16 columns.
 template <int INP, int W, int H>
 struct BwdCols {
-  // TMEM column map (fp32 columns; dW regions use the M=64 lane layout)
-  static constexpr int kDWo = 0;                                  // [64 x (W+8)]
-  static constexpr int kDWl = ((W + 8 + 15) / 16) * 16;           // layer H-1 .. 1: each (W+8)
-  static constexpr int kDW0 = kDWl + (H - 1) * (((W + 8 + 15) / 16) * 16);  // [64 x (INP+8)]
-  static constexpr int kR = kDW0 + ((INP + 8 + 15) / 16) * 16;     // per-layer fwd/bwd regions, W each
-  static constexpr int kOut = kR + H * W;                         // 16
-  static constexpr int kDX = kOut + 16;                           // INP
-  static constexpr int kTotal = kDX + INP;
-  static_assert(kTotal <= 512, "TMEM budget");
+  static constexpr int kDWo = 0;                 // [128 x 16]  (h | 1) x o
+  static constexpr int kDWl = 16;                // layers H-1..1: [128 x W] each
+  static constexpr int kDW0 = kDWl + (H - 1) * W;  // [128 x W]  (in | 1) x out
+  static constexpr int kR = kDW0 + W;            // working region, 64 columns
+  static constexpr int kTotal = kR + 64;
+  static_assert(kTotal <= 256, "TMEM budget");
 };
 
 template <int INP, int W, int H>
@@ -252,20 +255,19 @@ __global__ void __launch_bounds__(kThreads, 1)
   WeightTiles<INP, W, H> wt;
   unsigned char* p = smem;
   wt.carve(p);
-  unsigned char* X = p;  // [128][INP+8]
+  unsigned char* X = p;  // [128][INP+8]: features | ones
   p += 128 * XC * 2 + kSlack;
-  unsigned char* Ht[2];  // [128][W+8] per hidden layer
+  unsigned char* Ht[2];  // [128][W+8] per hidden layer: activations | ones
   for (int l = 0; l < H; ++l) {
     Ht[l] = p;
     p += 128 * HC * 2 + kSlack;
   }
-  unsigned char* G = p;  // [128][16]
+  unsigned char* G = p;  // [128][16] g_raw (4 used)
   p += 128 * 16 * 2 + kSlack;
   unsigned char* D = p;  // [128][W]
   p += 128 * W * 2 + kSlack;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   wt.load(fd, params + fd.hash_params);
-  // zero every activation tile (+slack) once; then set the ones columns
   {
     uint4* z = reinterpret_cast<uint4*>(X);
     const int n16 = (int)((p - X) / 16);
@@ -277,7 +279,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     *reinterpret_cast<__nv_bfloat16*>(X + umma::cm_offset(r, INP, XC)) = one;
     for (int l = 0; l < H; ++l) *reinterpret_cast<__nv_bfloat16*>(Ht[l] + umma::cm_offset(r, W, HC)) = one;
   }
-  if (warp == 0) umma::tmem_alloc(&tbase, 512);
+  if (warp == 0) umma::tmem_alloc(&tbase, 256);
   if (tid == 0) {
     umma::mbar_init(&bar, 1);
     umma::fence_mbar_init();
@@ -286,6 +288,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   umma::fence_after_sync();
   const uint32_t tm = tbase;
+  const uint32_t tr = tm + CM::kR;
   uint32_t phase = 0;
   const long long ntiles = (n_total + kTile - 1) / kTile;
   int iter = 0;
@@ -298,36 +301,35 @@ __global__ void __launch_bounds__(kThreads, 1)
     {
       const uint4* src = feat_tiles + t * (128 * INP * 2 / 16);
       for (int i = tid; i < 128 * INP * 2 / 16; i += kThreads) {
-        const int rg = i / (INP / 8 * 8), rem = i % (INP / 8 * 8);  // 16 B units inside a row group
-        const int chunk = rem / 8, r8 = rem % 8;
-        *reinterpret_cast<uint4*>(X + rg * (XC / 8) * 128 + chunk * 128 + r8 * 16) = src[i];
+        const int rg = i / INP, rem = i % INP;  // INP uint4 per row group
+        *reinterpret_cast<uint4*>(X + rg * (XC / 8) * 128 + (rem >> 3) * 128 + (rem & 7) * 16) = src[i];
       }
     }
     sync_for_mma();
-    // ---- forward recompute
+    // ---- forward recompute (field.cpp:181-211), one TMEM region reused per layer
     if (tid == 0) {
       for (int ks = 0; ks < INP / 16; ++ks)
-        umma::mma_bf16(tm + CM::kR, umma::desc_kmajor(X, XC, ks), umma::desc_kmajor(wt.w0, INP, ks),
+        umma::mma_bf16(tr, umma::desc_kmajor(X, XC, ks), umma::desc_kmajor(wt.w0, INP, ks),
                        umma::idesc_bf16(128, W, false, false), ks > 0);
       umma::commit(&bar);
     }
     wait_mma(&bar, phase);
-    epi_relu<W>(tm, CM::kR, wt.bias, Ht[0], HC);
+    epi_relu<W>(tr, 0, wt.bias, Ht[0], HC);
     for (int l = 1; l < H; ++l) {
       sync_for_mma();
       if (tid == 0) {
         for (int ks = 0; ks < W / 16; ++ks)
-          umma::mma_bf16(tm + CM::kR + l * W, umma::desc_kmajor(Ht[l - 1], HC, ks),
-                         umma::desc_kmajor(wt.wl[l - 1], W, ks), umma::idesc_bf16(128, W, false, false), ks > 0);
+          umma::mma_bf16(tr, umma::desc_kmajor(Ht[l - 1], HC, ks), umma::desc_kmajor(wt.wl[l - 1], W, ks),
+                         umma::idesc_bf16(128, W, false, false), ks > 0);
         umma::commit(&bar);
       }
       wait_mma(&bar, phase);
-      epi_relu<W>(tm, CM::kR + l * W, wt.bias + l * W, Ht[l], HC);
+      epi_relu<W>(tr, 0, wt.bias + l * W, Ht[l], HC);
     }
     sync_for_mma();
     if (tid == 0) {
       for (int ks = 0; ks < W / 16; ++ks)
-        umma::mma_bf16(tm + CM::kOut, umma::desc_kmajor(Ht[H - 1], HC, ks), umma::desc_kmajor(wt.wo, W, ks),
+        umma::mma_bf16(tr, umma::desc_kmajor(Ht[H - 1], HC, ks), umma::desc_kmajor(wt.wo, W, ks),
                        umma::idesc_bf16(128, 16, false, false), ks > 0);
       umma::commit(&bar);
     }
@@ -335,7 +337,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---- g_raw (field.cpp:233-238) -> G tile
     if (warp < 4) {
       float v[8];
-      umma::tmem_ld8(umma::taddr(tm, 32 * q, CM::kOut), v);
+      umma::tmem_ld8(umma::taddr(tr, 32 * q, 0), v);
       umma::tmem_wait_ld();
       float g[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
       if (valid) {
@@ -352,12 +354,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       umma::st_row8(G, row, 0, 16, g);
     }
     sync_for_mma();
-    // ---- output layer: dW_out += G^T [H_{H-1} | 1];  dH_{H-1} = G W_out
+    // ---- output layer: dW_out^T += [H_{H-1}|1]^T G;  dH_{H-1} = G W_out
     if (tid == 0) {
       for (int ks = 0; ks < 8; ++ks)
-        umma::mma_bf16(tm + CM::kDWo, umma::desc_mnmajor(G, 16, ks), umma::desc_mnmajor(Ht[H - 1], HC, ks),
-                       umma::idesc_bf16(64, HC, true, true), (iter > 0 || ks > 0));
-      umma::mma_bf16(tm + CM::kR + (H - 1) * W, umma::desc_kmajor(G, 16, 0), umma::desc_mnmajor(wt.wo, W, 0),
+        umma::mma_bf16(tm + CM::kDWo, umma::desc_mnmajor(Ht[H - 1], HC, ks), umma::desc_mnmajor(G, 16, ks),
+                       umma::idesc_bf16(128, 16, true, true), (iter > 0 || ks > 0));
+      umma::mma_bf16(tr, umma::desc_kmajor(G, 16, 0), umma::desc_mnmajor(wt.wo, W, 0),
                      umma::idesc_bf16(128, W, false, true), 0u);
       umma::commit(&bar);
     }
@@ -370,7 +372,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int c = 0; c < NH; c += 8) {
           const int col = half * NH + c;
           float v[8];
-          umma::tmem_ld8(umma::taddr(tm, 32 * q, CM::kR + l * W + col), v);
+          umma::tmem_ld8(umma::taddr(tr, 32 * q, col), v);
           umma::tmem_wait_ld();
           const uint4 hv = *reinterpret_cast<const uint4*>(Ht[l] + umma::cm_offset(row, col, HC));
           const __nv_bfloat16* hb = reinterpret_cast<const __nv_bfloat16*>(&hv);
@@ -381,19 +383,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       sync_for_mma();
       if (tid == 0) {
-        const int dwc = l == 0 ? CM::kDW0 : CM::kDWl + (H - 1 - l) * (((W + 8 + 15) / 16) * 16);
+        const int dwc = l == 0 ? CM::kDW0 : CM::kDWl + (H - 1 - l) * W;
         const unsigned char* prev = l == 0 ? X : Ht[l - 1];
         const int pc = l == 0 ? XC : HC;
         for (int ks = 0; ks < 8; ++ks)
-          umma::mma_bf16(tm + dwc, umma::desc_mnmajor(D, W, ks), umma::desc_mnmajor(prev, pc, ks),
-                         umma::idesc_bf16(64, pc, true, true), (iter > 0 || ks > 0));
+          umma::mma_bf16(tm + dwc, umma::desc_mnmajor(prev, pc, ks), umma::desc_mnmajor(D, W, ks),
+                         umma::idesc_bf16(128, W, true, true), (iter > 0 || ks > 0));
         if (l > 0) {
           for (int ks = 0; ks < W / 16; ++ks)
-            umma::mma_bf16(tm + CM::kR + (l - 1) * W, umma::desc_kmajor(D, W, ks), umma::desc_mnmajor(wt.wl[l - 1], W, ks),
+            umma::mma_bf16(tr, umma::desc_kmajor(D, W, ks), umma::desc_mnmajor(wt.wl[l - 1], W, ks),
                            umma::idesc_bf16(128, W, false, true), ks > 0);
         } else {
           for (int ks = 0; ks < W / 16; ++ks)
-            umma::mma_bf16(tm + CM::kDX, umma::desc_kmajor(D, W, ks), umma::desc_mnmajor(wt.w0, INP, ks),
+            umma::mma_bf16(tr, umma::desc_kmajor(D, W, ks), umma::desc_mnmajor(wt.w0, INP, ks),
                            umma::idesc_bf16(128, INP, false, true), ks > 0);
         }
         umma::commit(&bar);
@@ -405,7 +407,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr int NH = INP / 2;  // columns of this thread's half
       float v[NH];
 #pragma unroll
-      for (int c = 0; c < NH; c += 8) umma::tmem_ld8(umma::taddr(tm, 32 * q, CM::kDX + half * NH + c), v + c);
+      for (int c = 0; c < NH; c += 8) umma::tmem_ld8(umma::taddr(tr, 32 * q, half * NH + c), v + c);
       umma::tmem_wait_ld();  // (warp-collective loads stay outside the per-sample branch)
       float4 pp = make_float4(0.f, 0.f, 0.f, 0.f);
       if (valid) pp = pos[gs];
@@ -432,10 +434,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           c[2 * corner] = w * d0;
           c[2 * corner + 1] = w * d1;
         }
-#pragma unroll
+        // runs are contiguous: once no run is longer than `off`, no larger
+        // offset can match either, so fine levels (runs of 1) skip all value shuffles
         for (int off = 1; off < 32; off <<= 1) {
           const unsigned long long ok = __shfl_down_sync(0xffffffffu, key, off);
           const bool take = (lane + off < 32) && ok == key;
+          if (!__any_sync(0xffffffffu, take)) break;
 #pragma unroll
           for (int k = 0; k < 16; ++k) {
             const float t = __shfl_down_sync(0xffffffffu, c[k], off);
@@ -458,44 +462,33 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     umma::fence_before_sync();
   }
-  // ---- flush the TMEM weight-gradient accumulators (one atomic per weight per CTA)
+  // ---- flush the TMEM weight-gradient accumulators: row = input unit (or the
+  // ones row = bias), column = output unit; one atomicAdd per weight per CTA
   __syncthreads();
   umma::fence_after_sync();
   if (iter > 0 && warp < 4) {
     float* gm = grad + fd.hash_params;
-    const int r = 16 * warp + lane;  // M=64 layout: rows 16q..16q+15 in lanes 32q..32q+15
-    auto flush = [&](int col0, int rows, int in, int w_off, int b_off) {
-      for (int c = 0; c < in + 8; c += 8) {
+    auto flush = [&](int col0, int ncol, int n_out, int in, int bias_row, int w_off, int b_off) {
+      for (int c = 0; c < ncol; c += 8) {
         float v[8];
         umma::tmem_ld8(umma::taddr(tm, 32 * warp, col0 + c), v);
         umma::tmem_wait_ld();
-        if (lane < 16 && r < rows)
-          for (int j = 0; j < 8; ++j) {
-            const int k = c + j;
-            if (k < in) atomicAdd(gm + w_off + r * in + k, v[j]);
-            else if (k == in) atomicAdd(gm + b_off + r, v[j]);
-          }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int o = c + j;
+          if (o >= n_out) continue;
+          if (row < in) atomicAdd(gm + w_off + o * in + row, v[j]);
+          else if (row == bias_row) atomicAdd(gm + b_off + o, v[j]);
+        }
       }
     };
-    flush(CM::kDWo, 4, W, fd.w_off[H], fd.b_off[H]);
-    for (int l = H - 1; l >= 1; --l)
-      flush(CM::kDWl + (H - 1 - l) * (((W + 8 + 15) / 16) * 16), W, W, fd.w_off[l], fd.b_off[l]);
-    // layer 0: columns >= in_dim (zero padding up to INP) are skipped; bias sits at column INP
-    for (int c = 0; c < INP + 8; c += 8) {
-      float v[8];
-      umma::tmem_ld8(umma::taddr(tm, 32 * warp, CM::kDW0 + c), v);
-      umma::tmem_wait_ld();
-      if (lane < 16 && r < W)
-        for (int j = 0; j < 8; ++j) {
-          const int k = c + j;
-          if (k < fd.in_dim) atomicAdd(gm + fd.w_off[0] + r * fd.in_dim + k, v[j]);
-          else if (k == INP) atomicAdd(gm + fd.b_off[0] + r, v[j]);
-        }
-    }
+    flush(CM::kDWo, 16, 4, W, W, fd.w_off[H], fd.b_off[H]);
+    for (int l = H - 1; l >= 1; --l) flush(CM::kDWl + (H - 1 - l) * W, W, W, W, W, fd.w_off[l], fd.b_off[l]);
+    flush(CM::kDW0, W, W, fd.in_dim, INP, fd.w_off[0], fd.b_off[0]);
   }
   umma::fence_before_sync();
   __syncthreads();
-  if (warp == 0) umma::tmem_dealloc(tm, 512);
+  if (warp == 0) umma::tmem_dealloc(tm, 256);
 }
 
 int g_sms = 0;
@@ -522,12 +515,12 @@ size_t bwd_smem() {
 template <int INP, int W, int H>
 cudaError_t run_fwd(const FieldDesc& fd, const float* params, long long n, int S, const int* count, const float4* pos,
                     void* feat_tiles, float4* out, int* flag, cudaStream_t st) {
-  // >= 80 KB so at most two CTAs (2 x 256 TMEM columns) share an SM
-  const size_t smem = std::max<size_t>(fwd_smem<INP, W, H>(), 80 * 1024);
+  // >= 46 KB: at most four CTAs (8 warps each) share an SM's 228 KB
+  const size_t smem = std::max<size_t>(fwd_smem<INP, W, H>(), 46 * 1024);
   cudaError_t e = cudaFuncSetAttribute(k_fwd_tc<INP, W, H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const long long ntiles = (n + kTile - 1) / kTile;
-  const long long grid = std::min<long long>(ntiles, 2LL * sms());
+  const long long grid = std::min<long long>(ntiles, 4LL * sms());
   k_fwd_tc<INP, W, H><<<(unsigned)grid, kThreads, smem, st>>>(fd, params, n, S, count, pos,
                                                               reinterpret_cast<uint4*>(feat_tiles), out, flag);
   return cudaGetLastError();
@@ -536,11 +529,11 @@ cudaError_t run_fwd(const FieldDesc& fd, const float* params, long long n, int S
 template <int INP, int W, int H>
 cudaError_t run_bwd(const FieldDesc& fd, const float* params, float* grad, long long n, int S, const int* count,
                     const float4* pos, const void* feat_tiles, const float4* dout, cudaStream_t st) {
-  const size_t smem = std::max<size_t>(bwd_smem<INP, W, H>(), 120 * 1024);  // one CTA (512 TMEM cols) per SM
+  const size_t smem = std::max<size_t>(bwd_smem<INP, W, H>(), 80 * 1024);  // two CTAs (2 x 256 TMEM cols) per SM
   cudaError_t e = cudaFuncSetAttribute(k_bwd_tc<INP, W, H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const long long ntiles = (n + kTile - 1) / kTile;
-  const long long grid = std::min<long long>(ntiles, (long long)sms());
+  const long long grid = std::min<long long>(ntiles, 2LL * sms());
   k_bwd_tc<INP, W, H><<<(unsigned)grid, kThreads, smem, st>>>(fd, params, grad, n, S, count, pos,
                                                               reinterpret_cast<const uint4*>(feat_tiles), dout);
   return cudaGetLastError();
