@@ -131,10 +131,9 @@ __global__ void __launch_bounds__(kThreads) k_fwd_tc(FieldDesc fd, const float* 
   wt.carve(p);
   unsigned char* X = p;
   p += 128 * INP * 2;
-  unsigned char* Hb[2];
-  Hb[0] = p;
-  p += 128 * W * 2;
-  Hb[1] = p;
+  // one activation tile: layer l+1's MMA completes (mbarrier) before layer
+  // l+1's epilogue overwrites the tile it read
+  unsigned char* Hb = p;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   wt.load(fd, params + fd.hash_params);
   for (int i = tid; i < 128 * INP; i += kThreads) reinterpret_cast<__nv_bfloat16*>(X)[i] = __float2bfloat16_rn(0.f);
@@ -163,10 +162,19 @@ __global__ void __launch_bounds__(kThreads) k_fwd_tc(FieldDesc fd, const float* 
       float4 pp = make_float4(0.f, 0.f, 0.f, 0.f);
       if (valid) pp = pos[gs];
       const float px = clamp01(pp.x), py = clamp01(pp.y), pz = clamp01(pp.z);
-      for (int l = half; l < fd.L; l += 2) {
-        float f[2] = {0.f, 0.f};
-        if (valid) encode_level<2>(fd, params, l, px, py, pz, f);
+      // this thread's levels: half, half+2, ...; two levels' 16 corner gathers in flight at once
+      for (int l = half; l < fd.L; l += 4) {
+        const int l2 = l + 2;
+        float f[2] = {0.f, 0.f}, g[2] = {0.f, 0.f};
+        if (valid) {
+          if (l2 < fd.L)
+            encode_level_pair<2>(fd, params, l, l2, px, py, pz, f, g);
+          else
+            encode_level<2>(fd, params, l, px, py, pz, f);
+        }
         *reinterpret_cast<__nv_bfloat162*>(X + umma::cm_offset(s, 2 * l, INP)) = __floats2bfloat162_rn(f[0], f[1]);
+        if (l2 < fd.L)
+          *reinterpret_cast<__nv_bfloat162*>(X + umma::cm_offset(s, 2 * l2, INP)) = __floats2bfloat162_rn(g[0], g[1]);
       }
     }
     sync_for_mma();
@@ -182,22 +190,22 @@ __global__ void __launch_bounds__(kThreads) k_fwd_tc(FieldDesc fd, const float* 
       for (int i = tid; i < 128 * INP * 2 / 16; i += kThreads) dst[i] = src[i];
     }
     wait_mma(&bar, phase);
-    epi_relu<W>(tm, 0, wt.bias, Hb[0], W);
+    epi_relu<W>(tm, 0, wt.bias, Hb, W);
     for (int l = 1; l < H; ++l) {
       sync_for_mma();
       if (tid == 0) {
         for (int ks = 0; ks < W / 16; ++ks)
-          umma::mma_bf16(tm, umma::desc_kmajor(Hb[(l - 1) & 1], W, ks), umma::desc_kmajor(wt.wl[l - 1], W, ks),
+          umma::mma_bf16(tm, umma::desc_kmajor(Hb, W, ks), umma::desc_kmajor(wt.wl[l - 1], W, ks),
                          umma::idesc_bf16(128, W, false, false), ks > 0);
         umma::commit(&bar);
       }
       wait_mma(&bar, phase);
-      epi_relu<W>(tm, 0, wt.bias + l * W, Hb[l & 1], W);
+      epi_relu<W>(tm, 0, wt.bias + l * W, Hb, W);
     }
     sync_for_mma();
     if (tid == 0) {
       for (int ks = 0; ks < W / 16; ++ks)
-        umma::mma_bf16(tm, umma::desc_kmajor(Hb[(H - 1) & 1], W, ks), umma::desc_kmajor(wt.wo, W, ks), id_out,
+        umma::mma_bf16(tm, umma::desc_kmajor(Hb, W, ks), umma::desc_kmajor(wt.wo, W, ks), id_out,
                        ks > 0);
       umma::commit(&bar);
     }
@@ -503,7 +511,7 @@ int sms() {
 
 template <int INP, int W, int H>
 size_t fwd_smem() {
-  return WeightTiles<INP, W, H>::kBytes + ((H * W + 4) * 4 + 15) / 16 * 16 + 128 * INP * 2 + 2 * 128 * W * 2 + 1024;
+  return WeightTiles<INP, W, H>::kBytes + ((H * W + 4) * 4 + 15) / 16 * 16 + 128 * INP * 2 + 128 * W * 2 + 1024;
 }
 
 template <int INP, int W, int H>
@@ -515,12 +523,12 @@ size_t bwd_smem() {
 template <int INP, int W, int H>
 cudaError_t run_fwd(const FieldDesc& fd, const float* params, long long n, int S, const int* count, const float4* pos,
                     void* feat_tiles, float4* out, int* flag, cudaStream_t st) {
-  // >= 46 KB: at most four CTAs (8 warps each) share an SM's 228 KB
-  const size_t smem = std::max<size_t>(fwd_smem<INP, W, H>(), 46 * 1024);
+  // at most five CTAs (8 warps each; 5 x 64 TMEM columns) share an SM
+  const size_t smem = std::max<size_t>(fwd_smem<INP, W, H>(), 38 * 1024);  // <= 5 CTAs/SM
   cudaError_t e = cudaFuncSetAttribute(k_fwd_tc<INP, W, H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const long long ntiles = (n + kTile - 1) / kTile;
-  const long long grid = std::min<long long>(ntiles, 4LL * sms());
+  const long long grid = std::min<long long>(ntiles, 5LL * sms());
   k_fwd_tc<INP, W, H><<<(unsigned)grid, kThreads, smem, st>>>(fd, params, n, S, count, pos,
                                                               reinterpret_cast<uint4*>(feat_tiles), out, flag);
   return cudaGetLastError();

@@ -169,6 +169,52 @@ __device__ __forceinline__ void encode_level(const FieldDesc& fd, const float* _
     }
 }
 
+// Two levels at once (16 independent corner gathers in flight), same
+// per-level arithmetic and accumulation order as encode_level.
+template <int F>
+__device__ __forceinline__ void encode_level_pair(const FieldDesc& fd, const float* __restrict__ params, int la,
+                                                  int lb, float px, float py, float pz, float* fa, float* fb) {
+  const LevelCell ca = level_cell(fd.res[la], px, py, pz);
+  const LevelCell cb = level_cell(fd.res[lb], px, py, pz);
+  const float* ta = params + (long long)la * F * fd.rows;
+  const float* tb = params + (long long)lb * F * fd.rows;
+  float ea[8][F], eb[8][F], wa[8], wb[8];
+#pragma unroll
+  for (int corner = 0; corner < 8; ++corner) {
+    const uint32_t ra = table_row(fd, la, (uint32_t)(ca.cx + (corner & 1)), (uint32_t)(ca.cy + ((corner >> 1) & 1)),
+                                  (uint32_t)(ca.cz + ((corner >> 2) & 1)));
+    const uint32_t rb = table_row(fd, lb, (uint32_t)(cb.cx + (corner & 1)), (uint32_t)(cb.cy + ((corner >> 1) & 1)),
+                                  (uint32_t)(cb.cz + ((corner >> 2) & 1)));
+    wa[corner] = corner_weight(ca, corner);
+    wb[corner] = corner_weight(cb, corner);
+    if constexpr (F == 2) {
+      const float2 va = __ldg(reinterpret_cast<const float2*>(ta + (size_t)ra * 2));
+      const float2 vb = __ldg(reinterpret_cast<const float2*>(tb + (size_t)rb * 2));
+      ea[corner][0] = va.x;
+      ea[corner][1] = va.y;
+      eb[corner][0] = vb.x;
+      eb[corner][1] = vb.y;
+    } else {
+#pragma unroll
+      for (int f = 0; f < F; ++f) {
+        ea[corner][f] = __ldg(ta + (size_t)ra * F + f);
+        eb[corner][f] = __ldg(tb + (size_t)rb * F + f);
+      }
+    }
+  }
+#pragma unroll
+  for (int f = 0; f < F; ++f) fa[f] = fb[f] = 0.f;
+#pragma unroll
+  for (int corner = 0; corner < 8; ++corner) {
+    if (wa[corner] != 0.f)
+#pragma unroll
+      for (int f = 0; f < F; ++f) fa[f] = __fadd_rn(fa[f], __fmul_rn(wa[corner], ea[corner][f]));
+    if (wb[corner] != 0.f)
+#pragma unroll
+      for (int f = 0; f < F; ++f) fb[f] = __fadd_rn(fb[f], __fmul_rn(wb[corner], eb[corner][f]));
+  }
+}
+
 // Runtime-F variant (tiny test archs).
 __device__ __forceinline__ void encode_level_rt(const FieldDesc& fd, const float* __restrict__ params,
                                                 int l, float px, float py, float pz, float* feat) {
