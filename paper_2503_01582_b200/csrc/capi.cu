@@ -232,6 +232,7 @@ struct prenom_object_s {
   DevBuf<float4> pos_depth, target, out, dout;
   DevBuf<float> delta, feat_t, dfeat_t, t_entry, t_exit;
   DevBuf<unsigned char> feat_tc;  // bf16 feature tiles (tensor-core path)
+  DevBuf<int> tile_ctr;           // dynamic tile-scheduler counters (fwd, bwd)
   DevBuf<int> kind, count;
   DevBuf<StepStatsDev> stats;
   int last_n_steps = 0;
@@ -252,6 +253,7 @@ prenom_status ensure_scratch(prenom_object_s* o, int B, int S) {
   CUDA_TRY(o->dout.ensure(Npad));
   if (o->cfg.mlp_precision == PRENOM_MLP_BF16) {
     CUDA_TRY(o->feat_tc.ensure(tc_feature_bytes(o->fd, (long long)N)));
+    CUDA_TRY(o->tile_ctr.ensure(2));
   } else {
     CUDA_TRY(o->feat_t.ensure(Npad * o->fd.in_dim));
     CUDA_TRY(o->dfeat_t.ensure(Npad * o->fd.in_dim));
@@ -351,7 +353,7 @@ prenom_status enqueue_step(prenom_object_s* o, StepStatsDev* stats) {
     ProfScope ps(o->ctx, PRENOM_K_FIELD_FWD);
     if (tc)
       CUDA_TRY(launch_fwd_tc(o->fd, o->params.p, (long long)B * S, S, sb.count, sb.pos_depth, o->feat_tc.p, o->out.p,
-                             o->flag.p, st));
+                             o->flag.p, o->tile_ctr.p, st));
     else
       CUDA_TRY(launch_field_fwd_train(o->fd, o->params.p, B, S, sb, o->feat_t.p, o->out.p, o->flag.p, st));
   }
@@ -381,7 +383,7 @@ prenom_status enqueue_step(prenom_object_s* o, StepStatsDev* stats) {
   if (tc) {
     ProfScope ps(o->ctx, PRENOM_K_MLP_BWD);  // MLP backward + fused table-gradient scatter
     CUDA_TRY(launch_bwd_tc(o->fd, o->params.p, o->grad.p, (long long)B * S, S, sb.count, sb.pos_depth,
-                           o->feat_tc.p, o->dout.p, st));
+                           o->feat_tc.p, o->dout.p, o->tile_ctr.p + 1, st));
   } else {
     {
       ProfScope ps(o->ctx, PRENOM_K_MLP_BWD);
@@ -755,7 +757,7 @@ prenom_status prenom_render(prenom_object_t o, int n_rays, const float* origins,
                                           (uint32_t)o->render_calls++), sb, nullptr, st));
   if (o->cfg.mlp_precision == PRENOM_MLP_BF16)
     CUDA_TRY(launch_fwd_tc(o->fd, o->params.p, (long long)n_rays * S, S, sb.count, sb.pos_depth, o->feat_tc.p,
-                           o->out.p, o->flag.p, st));
+                           o->out.p, o->flag.p, o->tile_ctr.p, st));
   else
     CUDA_TRY(launch_field_fwd_train(o->fd, o->params.p, n_rays, S, sb, o->feat_t.p, o->out.p, o->flag.p, st));
   CompositeArgs ca;
@@ -975,7 +977,7 @@ struct PointBatch {
   DevBuf<float> params, feat_t, dfeat_t, grad;
   DevBuf<unsigned char> feat_tc;
   DevBuf<float4> pos, out, dout;
-  DevBuf<int> count, flag;
+  DevBuf<int> count, flag, ctr;
   SampleBufs sb;
   prenom_status init(const FieldDesc& fd, size_t P, int n, const float* h_params, const float* xyz,
                      cudaStream_t st) {
@@ -989,6 +991,7 @@ struct PointBatch {
     CUDA_TRY(dout.ensure(npad));
     CUDA_TRY(count.ensure(n));
     CUDA_TRY(flag.ensure(1));
+    CUDA_TRY(ctr.ensure(2));
     CUDA_TRY(cudaMemsetAsync(flag.p, 0, sizeof(int), st));
     CUDA_TRY(cudaMemcpyAsync(params.p, h_params, P * sizeof(float), cudaMemcpyHostToDevice, st));
     std::vector<float4> hp(n);
@@ -1040,7 +1043,8 @@ prenom_status prenom_debug_field_eval(prenom_ctx_t ctx, const prenom_field_arch*
     PointBatch pb;
     STATUS_TRY(pb.init(fd, P, n, params, xyz, st));
     if (precision == PRENOM_MLP_BF16)
-      CUDA_TRY(launch_fwd_tc(fd, pb.params.p, n, 1, pb.count.p, pb.pos.p, pb.feat_tc.p, pb.out.p, pb.flag.p, st));
+      CUDA_TRY(launch_fwd_tc(fd, pb.params.p, n, 1, pb.count.p, pb.pos.p, pb.feat_tc.p, pb.out.p, pb.flag.p, pb.ctr.p,
+                             st));
     else
       CUDA_TRY(launch_field_fwd_train(fd, pb.params.p, n, 1, pb.sb, pb.feat_t.p, pb.out.p, pb.flag.p, st));
     ctx->launches += 1;
@@ -1086,8 +1090,10 @@ prenom_status prenom_debug_field_backward(prenom_ctx_t ctx, const prenom_field_a
   CUDA_TRY(cudaMemcpyAsync(pb.dout.p, hd.data(), sizeof(float4) * n, cudaMemcpyHostToDevice, st));
   if (precision == PRENOM_MLP_BF16) {
     if (!tc_supported(fd)) return fail(PRENOM_USAGE, "arch not supported by the bf16 path");
-    CUDA_TRY(launch_fwd_tc(fd, pb.params.p, n, 1, pb.count.p, pb.pos.p, pb.feat_tc.p, pb.out.p, pb.flag.p, st));
-    CUDA_TRY(launch_bwd_tc(fd, pb.params.p, pb.grad.p, n, 1, pb.count.p, pb.pos.p, pb.feat_tc.p, pb.dout.p, st));
+    CUDA_TRY(launch_fwd_tc(fd, pb.params.p, n, 1, pb.count.p, pb.pos.p, pb.feat_tc.p, pb.out.p, pb.flag.p, pb.ctr.p,
+                           st));
+    CUDA_TRY(launch_bwd_tc(fd, pb.params.p, pb.grad.p, n, 1, pb.count.p, pb.pos.p, pb.feat_tc.p, pb.dout.p,
+                           pb.ctr.p + 1, st));
   } else {
     CUDA_TRY(launch_field_fwd_train(fd, pb.params.p, n, 1, pb.sb, pb.feat_t.p, pb.out.p, pb.flag.p, st));
     CUDA_TRY(launch_mlp_bwd_train(fd, pb.params.p, pb.grad.p, n, 1, pb.count.p, pb.feat_t.p, pb.dout.p,

@@ -21,6 +21,7 @@
 // weight-gradient accumulators live in TMEM for the whole persistent CTA and
 // are flushed with one atomicAdd per weight per CTA at the end.
 #include <algorithm>
+#include <cstdlib>
 
 #include "prenom_device.cuh"
 #include "umma.cuh"
@@ -85,6 +86,15 @@ struct WeightTiles {
   }
 };
 
+// Dynamic tile scheduler: CTAs pull 128-sample tiles from a global counter,
+// so the tile load balances whatever number of CTAs the hardware co-locates
+// on an SM (static striding left SMs with more resident CTAs as stragglers).
+__device__ __forceinline__ long long next_tile(int* ctr, int* s_tile) {
+  if (threadIdx.x == 0) *s_tile = atomicAdd(ctr, 1);
+  __syncthreads();
+  return *s_tile;
+}
+
 __device__ __forceinline__ void sync_for_mma() {
   umma::fence_proxy_async();
   umma::fence_before_sync();
@@ -122,7 +132,7 @@ template <int INP, int W, int H>
 __global__ void __launch_bounds__(kThreads) k_fwd_tc(FieldDesc fd, const float* __restrict__ params, long long n_total,
                                                      int S, const int* __restrict__ count,
                                                      const float4* __restrict__ pos, uint4* __restrict__ feat_tiles,
-                                                     float4* __restrict__ out, int* flag) {
+                                                     float4* __restrict__ out, int* flag, int* tile_ctr) {
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ uint64_t bar;
   __shared__ uint32_t tbase;
@@ -152,7 +162,8 @@ __global__ void __launch_bounds__(kThreads) k_fwd_tc(FieldDesc fd, const float* 
   constexpr uint32_t id_l0 = umma::idesc_bf16(128, W, false, false);
   constexpr uint32_t id_out = umma::idesc_bf16(128, 16, false, false);
   const long long ntiles = (n_total + kTile - 1) / kTile;
-  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
+  __shared__ int s_tile;
+  for (long long t = next_tile(tile_ctr, &s_tile); t < ntiles; t = next_tile(tile_ctr, &s_tile)) {
     const long long tile0 = t * kTile;
     // ---- encode (fp32, bit-exact) -> bf16 X tile; 2 threads per sample
     {
@@ -162,19 +173,12 @@ __global__ void __launch_bounds__(kThreads) k_fwd_tc(FieldDesc fd, const float* 
       float4 pp = make_float4(0.f, 0.f, 0.f, 0.f);
       if (valid) pp = pos[gs];
       const float px = clamp01(pp.x), py = clamp01(pp.y), pz = clamp01(pp.z);
-      // this thread's levels: half, half+2, ...; two levels' 16 corner gathers in flight at once
-      for (int l = half; l < fd.L; l += 4) {
-        const int l2 = l + 2;
-        float f[2] = {0.f, 0.f}, g[2] = {0.f, 0.f};
-        if (valid) {
-          if (l2 < fd.L)
-            encode_level_pair<2>(fd, params, l, l2, px, py, pz, f, g);
-          else
-            encode_level<2>(fd, params, l, px, py, pz, f);
-        }
+      // (batching two levels' gathers per thread measured slower: more distinct
+      // lines in flight thrash L1, which serves the coarse levels)
+      for (int l = half; l < fd.L; l += 2) {
+        float f[2] = {0.f, 0.f};
+        if (valid) encode_level<2>(fd, params, l, px, py, pz, f);
         *reinterpret_cast<__nv_bfloat162*>(X + umma::cm_offset(s, 2 * l, INP)) = __floats2bfloat162_rn(f[0], f[1]);
-        if (l2 < fd.L)
-          *reinterpret_cast<__nv_bfloat162*>(X + umma::cm_offset(s, 2 * l2, INP)) = __floats2bfloat162_rn(g[0], g[1]);
       }
     }
     sync_for_mma();
@@ -254,7 +258,7 @@ template <int INP, int W, int H>
 __global__ void __launch_bounds__(kThreads, 2)
     k_bwd_tc(FieldDesc fd, const float* __restrict__ params, float* __restrict__ grad, long long n_total, int S,
              const int* __restrict__ count, const float4* __restrict__ pos, const uint4* __restrict__ feat_tiles,
-             const float4* __restrict__ dout) {
+             const float4* __restrict__ dout, int* tile_ctr) {
   using CM = BwdCols<INP, W, H>;
   constexpr int XC = INP + 8, HC = W + 8;
   extern __shared__ __align__(1024) unsigned char smem[];
@@ -301,7 +305,8 @@ __global__ void __launch_bounds__(kThreads, 2)
   const long long ntiles = (n_total + kTile - 1) / kTile;
   int iter = 0;
   const int q = warp & 3, half = warp >> 2, row = 32 * q + lane;
-  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x, ++iter) {
+  __shared__ int s_tile;
+  for (long long t = next_tile(tile_ctr, &s_tile); t < ntiles; t = next_tile(tile_ctr, &s_tile), ++iter) {
     const long long tile0 = t * kTile;
     const long long gs = tile0 + row;
     const bool valid = gs < n_total && __ldg(count + gs / S) > 0;
@@ -522,28 +527,43 @@ size_t bwd_smem() {
 
 template <int INP, int W, int H>
 cudaError_t run_fwd(const FieldDesc& fd, const float* params, long long n, int S, const int* count, const float4* pos,
-                    void* feat_tiles, float4* out, int* flag, cudaStream_t st) {
+                    void* feat_tiles, float4* out, int* flag, int* tile_ctr, cudaStream_t st) {
   // at most five CTAs (8 warps each; 5 x 64 TMEM columns) share an SM
-  const size_t smem = std::max<size_t>(fwd_smem<INP, W, H>(), 38 * 1024);  // <= 5 CTAs/SM
+  // CTAs per SM trade gather latency hiding against L1 capacity (L1 = 228 KB -
+  // shared memory); PRENOM_FWD_CTAS overrides the default for tuning.
+  static const int ctas = [] {
+    const char* e = getenv("PRENOM_FWD_CTAS");
+    const int v = e ? atoi(e) : 3;
+    return v < 1 ? 1 : (v > 8 ? 8 : v);
+  }();
+  static const size_t min_smem = [] {
+    const char* e = getenv("PRENOM_FWD_SMEM_KB");
+    return (size_t)(e ? atoi(e) : 0) * 1024;
+  }();
+  const size_t smem = std::max<size_t>(fwd_smem<INP, W, H>(), min_smem);
   cudaError_t e = cudaFuncSetAttribute(k_fwd_tc<INP, W, H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const long long ntiles = (n + kTile - 1) / kTile;
-  const long long grid = std::min<long long>(ntiles, 5LL * sms());
+  const long long grid = std::min<long long>(ntiles, (long long)ctas * sms());
+  e = cudaMemsetAsync(tile_ctr, 0, sizeof(int), st);
+  if (e != cudaSuccess) return e;
   k_fwd_tc<INP, W, H><<<(unsigned)grid, kThreads, smem, st>>>(fd, params, n, S, count, pos,
-                                                              reinterpret_cast<uint4*>(feat_tiles), out, flag);
+                                                              reinterpret_cast<uint4*>(feat_tiles), out, flag, tile_ctr);
   return cudaGetLastError();
 }
 
 template <int INP, int W, int H>
 cudaError_t run_bwd(const FieldDesc& fd, const float* params, float* grad, long long n, int S, const int* count,
-                    const float4* pos, const void* feat_tiles, const float4* dout, cudaStream_t st) {
+                    const float4* pos, const void* feat_tiles, const float4* dout, int* tile_ctr, cudaStream_t st) {
   const size_t smem = std::max<size_t>(bwd_smem<INP, W, H>(), 80 * 1024);  // two CTAs (2 x 256 TMEM cols) per SM
   cudaError_t e = cudaFuncSetAttribute(k_bwd_tc<INP, W, H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const long long ntiles = (n + kTile - 1) / kTile;
   const long long grid = std::min<long long>(ntiles, 2LL * sms());
+  e = cudaMemsetAsync(tile_ctr, 0, sizeof(int), st);
+  if (e != cudaSuccess) return e;
   k_bwd_tc<INP, W, H><<<(unsigned)grid, kThreads, smem, st>>>(fd, params, grad, n, S, count, pos,
-                                                              reinterpret_cast<const uint4*>(feat_tiles), dout);
+                                                              reinterpret_cast<const uint4*>(feat_tiles), dout, tile_ctr);
   return cudaGetLastError();
 }
 
@@ -575,16 +595,16 @@ size_t tc_feature_bytes(const FieldDesc& fd, long long n) {
 }
 
 cudaError_t launch_fwd_tc(const FieldDesc& fd, const float* params, long long n, int S, const int* count,
-                          const float4* pos, void* feat_tiles, float4* out, int* flag, cudaStream_t st) {
+                          const float4* pos, void* feat_tiles, float4* out, int* flag, int* tile_ctr, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
-  PRENOM_TC_DISPATCH(run_fwd, fd, params, n, S, count, pos, feat_tiles, out, flag, st);
+  PRENOM_TC_DISPATCH(run_fwd, fd, params, n, S, count, pos, feat_tiles, out, flag, tile_ctr, st);
 }
 
 cudaError_t launch_bwd_tc(const FieldDesc& fd, const float* params, float* grad, long long n, int S,
                           const int* count, const float4* pos, const void* feat_tiles, const float4* dout,
-                          cudaStream_t st) {
+                          int* tile_ctr, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
-  PRENOM_TC_DISPATCH(run_bwd, fd, params, grad, n, S, count, pos, feat_tiles, dout, st);
+  PRENOM_TC_DISPATCH(run_bwd, fd, params, grad, n, S, count, pos, feat_tiles, dout, tile_ctr, st);
 }
 
 }  // namespace prenom

@@ -303,11 +303,13 @@ cudaError_t launch_reptile_apply(size_t n, float* meta, const float* delta, floa
 // bf16 tensor-core MLP path (kernels_tc.cu)
 bool tc_supported(const FieldDesc& fd);
 size_t tc_feature_bytes(const FieldDesc& fd, long long n);
+// tile_ctr: one device int per launch, zeroed by the launcher (dynamic tile scheduler)
 cudaError_t launch_fwd_tc(const FieldDesc& fd, const float* params, long long n, int S, const int* count,
-                          const float4* pos, void* feat_tiles, float4* out, int* flag, cudaStream_t st);
+                          const float4* pos, void* feat_tiles, float4* out, int* flag, int* tile_ctr,
+                          cudaStream_t st);
 cudaError_t launch_bwd_tc(const FieldDesc& fd, const float* params, float* grad, long long n, int S,
                           const int* count, const float4* pos, const void* feat_tiles, const float4* dout,
-                          cudaStream_t st);
+                          int* tile_ctr, cudaStream_t st);
 cudaError_t launch_umma_gemm(int M, int N, int K, int a_mn, int b_mn, const float* A, const float* B,
                              float* D, cudaStream_t st);
 
