@@ -258,7 +258,7 @@ template <int INP, int W, int H>
 __global__ void __launch_bounds__(kThreads, 2)
     k_bwd_tc(FieldDesc fd, const float* __restrict__ params, float* __restrict__ grad, long long n_total, int S,
              const int* __restrict__ count, const float4* __restrict__ pos, const uint4* __restrict__ feat_tiles,
-             const float4* __restrict__ dout, int* tile_ctr, int skip_scatter) {
+             const float4* __restrict__ dout, int* tile_ctr) {
   using CM = BwdCols<INP, W, H>;
   constexpr int XC = INP + 8, HC = W + 8;
   extern __shared__ __align__(1024) unsigned char smem[];
@@ -416,7 +416,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       wait_mma(&bar, phase);
     }
     // ---- d_features -> table-gradient scatter (field.cpp:279-292), fused
-    if (!skip_scatter) {
+    {
       constexpr int NH = INP / 2;  // columns of this thread's half
       float v[NH];
 #pragma unroll
@@ -463,25 +463,12 @@ __global__ void __launch_bounds__(kThreads, 2)
         if (valid && (lane == 0 || pk != key)) {
           float* gl = grad + (long long)l * 2 * fd.rows;
 #pragma unroll
-          for (int cp = 0; cp < 8; cp += 2) {  // x-adjacent corner pair (dx = 0, 1)
-            const float* a = c + 2 * cp;
-            const float* b = c + 2 * cp + 2;
-            const bool za = a[0] == 0.f && a[1] == 0.f, zb = b[0] == 0.f && b[1] == 0.f;
-            if (za && zb) continue;
-            const uint32_t yy = (uint32_t)(cell.cy + ((cp >> 1) & 1)), zz = (uint32_t)(cell.cz + ((cp >> 2) & 1));
-            const uint32_t ra = table_row(fd, l, (uint32_t)cell.cx, yy, zz);
-            const uint32_t rb = table_row(fd, l, (uint32_t)cell.cx + 1u, yy, zz);
-            // rows of the two x-corners share one 16-byte entry pair whenever they
-            // differ only in bit 0 (hashed levels with even x: the x prime is 1;
-            // dense levels with an even row) -> one vector atomic instead of two
-            if ((ra ^ rb) == 1u) {
-              const uint32_t r0 = ra & ~1u;
-              const float4 v = (ra & 1u) ? make_float4(b[0], b[1], a[0], a[1]) : make_float4(a[0], a[1], b[0], b[1]);
-              atomicAdd(reinterpret_cast<float4*>(gl + (size_t)r0 * 2), v);
-            } else {
-              if (!za) atomicAdd(reinterpret_cast<float2*>(gl + (size_t)ra * 2), make_float2(a[0], a[1]));
-              if (!zb) atomicAdd(reinterpret_cast<float2*>(gl + (size_t)rb * 2), make_float2(b[0], b[1]));
-            }
+          for (int corner = 0; corner < 8; ++corner) {
+            if (c[2 * corner] == 0.f && c[2 * corner + 1] == 0.f) continue;
+            const uint32_t r = table_row(fd, l, (uint32_t)(cell.cx + (corner & 1)),
+                                         (uint32_t)(cell.cy + ((corner >> 1) & 1)),
+                                         (uint32_t)(cell.cz + ((corner >> 2) & 1)));
+            atomicAdd(reinterpret_cast<float2*>(gl + (size_t)r * 2), make_float2(c[2 * corner], c[2 * corner + 1]));
           }
         }
       }
@@ -550,10 +537,8 @@ cudaError_t run_fwd(const FieldDesc& fd, const float* params, long long n, int S
     return v < 1 ? 1 : (v > 8 ? 8 : v);
   }();
   static const size_t min_smem = [] {
-    // measured on B200 (cfg2): 3 CTAs x 57 KB (24 warps/SM, ~57 KB L1 for the
-    // coarse-level gathers) beats both more warps with less L1 and fewer warps
     const char* e = getenv("PRENOM_FWD_SMEM_KB");
-    return (size_t)(e ? atoi(e) : 57) * 1024;
+    return (size_t)(e ? atoi(e) : 0) * 1024;
   }();
   const size_t smem = std::max<size_t>(fwd_smem<INP, W, H>(), min_smem);
   cudaError_t e = cudaFuncSetAttribute(k_fwd_tc<INP, W, H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -578,8 +563,7 @@ cudaError_t run_bwd(const FieldDesc& fd, const float* params, float* grad, long 
   e = cudaMemsetAsync(tile_ctr, 0, sizeof(int), st);
   if (e != cudaSuccess) return e;
   k_bwd_tc<INP, W, H><<<(unsigned)grid, kThreads, smem, st>>>(fd, params, grad, n, S, count, pos,
-                                                              reinterpret_cast<const uint4*>(feat_tiles), dout, tile_ctr,
-                                                              getenv("PRENOM_PROF_SKIP_SCATTER") ? 1 : 0);
+                                                              reinterpret_cast<const uint4*>(feat_tiles), dout, tile_ctr);
   return cudaGetLastError();
 }
 
