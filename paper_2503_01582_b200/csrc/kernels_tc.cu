@@ -30,7 +30,11 @@ namespace prenom {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kSlack = 2048;  // bytes after each tile: M=128 MN-major views of narrow tiles over-read (finite garbage rows)
+constexpr int kSlack = 0;       // weight tiles are never over-read
+// M=128 MN-major views of the (features|1) and (activations|1) tiles read
+// past the tile end (finite garbage rows that are never flushed)
+constexpr int kSlackX = 2048;
+constexpr int kSlackH = 1024;
 
 // bf16 copies of the MLP weights in core-matrix layouts + fp32 biases.
 template <int INP, int W, int H>
@@ -254,192 +258,117 @@ struct BwdCols {
   static_assert(kTotal <= 256, "TMEM budget");
 };
 
+// Warp-specialized: warps 0-7 ("MLP warps", named barrier 1) run the
+// tensor-core chain of a tile and hand its fp32 d_features to warps 8-11
+// ("scatter warps", named barrier 2) through one shared-memory slot guarded
+// by full/empty mbarriers; the scatter of tile t overlaps the MMA chain of
+// tile t+1.
+constexpr int kMlpThreads = 256;
+constexpr int kScatThreads = 128;
+constexpr int kBwdThreads = kMlpThreads + kScatThreads;
+
+__device__ __forceinline__ void named_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+__device__ __forceinline__ void mlp_sync_for_mma() {
+  umma::fence_proxy_async();
+  umma::fence_before_sync();
+  named_sync(1, kMlpThreads);
+  umma::fence_after_sync();
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(umma::smem_u32(bar)) : "memory");
+}
+
+template <int INP>
+struct ScatterSlot {
+  static constexpr int kLd = INP + 4;  // floats per row (float4 rows, bank-spread)
+  static constexpr int kBytes = 128 * kLd * 4;
+};
+
 template <int INP, int W, int H>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kBwdThreads, 2)
     k_bwd_tc(FieldDesc fd, const float* __restrict__ params, float* __restrict__ grad, long long n_total, int S,
              const int* __restrict__ count, const float4* __restrict__ pos, const uint4* __restrict__ feat_tiles,
-             const float4* __restrict__ dout, int* tile_ctr) {
+             const float4* __restrict__ dout, int* tile_ctr, int skip_scatter) {
   using CM = BwdCols<INP, W, H>;
   constexpr int XC = INP + 8, HC = W + 8;
+  constexpr int SLD = ScatterSlot<INP>::kLd;
   extern __shared__ __align__(1024) unsigned char smem[];
-  __shared__ uint64_t bar;
+  __shared__ uint64_t bar, full_bar, empty_bar;
   __shared__ uint32_t tbase;
+  __shared__ int s_tile;
+  __shared__ long long slot_tile;
   WeightTiles<INP, W, H> wt;
   unsigned char* p = smem;
   wt.carve(p);
   unsigned char* X = p;  // [128][INP+8]: features | ones
-  p += 128 * XC * 2 + kSlack;
+  p += 128 * XC * 2 + kSlackX;
   unsigned char* Ht[2];  // [128][W+8] per hidden layer: activations | ones
   for (int l = 0; l < H; ++l) {
     Ht[l] = p;
-    p += 128 * HC * 2 + kSlack;
+    p += 128 * HC * 2 + kSlackH;
   }
   unsigned char* G = p;  // [128][16] g_raw (4 used)
-  p += 128 * 16 * 2 + kSlack;
+  p += 128 * 16 * 2;
   unsigned char* D = p;  // [128][W]
-  p += 128 * W * 2 + kSlack;
+  p += 128 * W * 2;
+  unsigned char* zero_end = p;
+  float* slot = reinterpret_cast<float*>(p);  // [128][SLD] d_features of one tile
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  wt.load(fd, params + fd.hash_params);
+  if (tid < kMlpThreads) wt.load(fd, params + fd.hash_params);
   {
     uint4* z = reinterpret_cast<uint4*>(X);
-    const int n16 = (int)((p - X) / 16);
-    for (int i = tid; i < n16; i += kThreads) z[i] = make_uint4(0u, 0u, 0u, 0u);
+    const int n16 = (int)((zero_end - X) / 16);
+    for (int i = tid; i < n16; i += kBwdThreads) z[i] = make_uint4(0u, 0u, 0u, 0u);
   }
   __syncthreads();
   const __nv_bfloat16 one = __float2bfloat16_rn(1.f);
-  for (int r = tid; r < 128; r += kThreads) {
+  for (int r = tid; r < 128; r += kBwdThreads) {
     *reinterpret_cast<__nv_bfloat16*>(X + umma::cm_offset(r, INP, XC)) = one;
     for (int l = 0; l < H; ++l) *reinterpret_cast<__nv_bfloat16*>(Ht[l] + umma::cm_offset(r, W, HC)) = one;
   }
   if (warp == 0) umma::tmem_alloc(&tbase, 256);
   if (tid == 0) {
     umma::mbar_init(&bar, 1);
+    umma::mbar_init(&full_bar, 1);
+    umma::mbar_init(&empty_bar, 1);
     umma::fence_mbar_init();
   }
   umma::fence_before_sync();
   __syncthreads();
   umma::fence_after_sync();
   const uint32_t tm = tbase;
-  const uint32_t tr = tm + CM::kR;
-  uint32_t phase = 0;
   const long long ntiles = (n_total + kTile - 1) / kTile;
-  int iter = 0;
-  const int q = warp & 3, half = warp >> 2, row = 32 * q + lane;
-  __shared__ int s_tile;
-  for (long long t = next_tile(tile_ctr, &s_tile); t < ntiles; t = next_tile(tile_ctr, &s_tile), ++iter) {
-    const long long tile0 = t * kTile;
-    const long long gs = tile0 + row;
-    const bool valid = gs < n_total && __ldg(count + gs / S) > 0;
-    // ---- stored bf16 features -> X (row-group stride differs: copy per 16 B)
-    {
-      const uint4* src = feat_tiles + t * (128 * INP * 2 / 16);
-      for (int i = tid; i < 128 * INP * 2 / 16; i += kThreads) {
-        const int rg = i / INP, rem = i % INP;  // INP uint4 per row group
-        *reinterpret_cast<uint4*>(X + rg * (XC / 8) * 128 + (rem >> 3) * 128 + (rem & 7) * 16) = src[i];
-      }
-    }
-    sync_for_mma();
-    // ---- forward recompute (field.cpp:181-211), one TMEM region reused per layer
-    if (tid == 0) {
-      for (int ks = 0; ks < INP / 16; ++ks)
-        umma::mma_bf16(tr, umma::desc_kmajor(X, XC, ks), umma::desc_kmajor(wt.w0, INP, ks),
-                       umma::idesc_bf16(128, W, false, false), ks > 0);
-      umma::commit(&bar);
-    }
-    wait_mma(&bar, phase);
-    epi_relu<W>(tr, 0, wt.bias, Ht[0], HC);
-    for (int l = 1; l < H; ++l) {
-      sync_for_mma();
-      if (tid == 0) {
-        for (int ks = 0; ks < W / 16; ++ks)
-          umma::mma_bf16(tr, umma::desc_kmajor(Ht[l - 1], HC, ks), umma::desc_kmajor(wt.wl[l - 1], W, ks),
-                         umma::idesc_bf16(128, W, false, false), ks > 0);
-        umma::commit(&bar);
-      }
-      wait_mma(&bar, phase);
-      epi_relu<W>(tr, 0, wt.bias + l * W, Ht[l], HC);
-    }
-    sync_for_mma();
-    if (tid == 0) {
-      for (int ks = 0; ks < W / 16; ++ks)
-        umma::mma_bf16(tr, umma::desc_kmajor(Ht[H - 1], HC, ks), umma::desc_kmajor(wt.wo, W, ks),
-                       umma::idesc_bf16(128, 16, false, false), ks > 0);
-      umma::commit(&bar);
-    }
-    wait_mma(&bar, phase);
-    // ---- g_raw (field.cpp:233-238) -> G tile
-    if (warp < 4) {
-      float v[8];
-      umma::tmem_ld8(umma::taddr(tr, 32 * q, 0), v);
-      umma::tmem_wait_ld();
-      float g[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-      if (valid) {
-        const float4 d = dout[gs];
-        const float* b = wt.bias + H * W;
-        const float r0 = v[0] + b[0];
-        const float sg = density_forward(fd.act, r0);
-        g[0] = d.x * density_derivative(fd.act, r0, sg);
-        const float s1 = stable_sigmoid(v[1] + b[1]), s2 = stable_sigmoid(v[2] + b[2]), s3 = stable_sigmoid(v[3] + b[3]);
-        g[1] = d.y * s1 * (1.f - s1);
-        g[2] = d.z * s2 * (1.f - s2);
-        g[3] = d.w * s3 * (1.f - s3);
-      }
-      umma::st_row8(G, row, 0, 16, g);
-    }
-    sync_for_mma();
-    // ---- output layer: dW_out^T += [H_{H-1}|1]^T G;  dH_{H-1} = G W_out
-    if (tid == 0) {
-      for (int ks = 0; ks < 8; ++ks)
-        umma::mma_bf16(tm + CM::kDWo, umma::desc_mnmajor(Ht[H - 1], HC, ks), umma::desc_mnmajor(G, 16, ks),
-                       umma::idesc_bf16(128, 16, true, true), (iter > 0 || ks > 0));
-      umma::mma_bf16(tr, umma::desc_kmajor(G, 16, 0), umma::desc_mnmajor(wt.wo, W, 0),
-                     umma::idesc_bf16(128, W, false, true), 0u);
-      umma::commit(&bar);
-    }
-    wait_mma(&bar, phase);
-    for (int l = H - 1; l >= 0; --l) {
-      // D_l = dH_l * relu'(H_l) -> D tile
-      {
-        constexpr int NH = W / 2;
-#pragma unroll
-        for (int c = 0; c < NH; c += 8) {
-          const int col = half * NH + c;
-          float v[8];
-          umma::tmem_ld8(umma::taddr(tr, 32 * q, col), v);
-          umma::tmem_wait_ld();
-          const uint4 hv = *reinterpret_cast<const uint4*>(Ht[l] + umma::cm_offset(row, col, HC));
-          const __nv_bfloat16* hb = reinterpret_cast<const __nv_bfloat16*>(&hv);
-#pragma unroll
-          for (int j = 0; j < 8; ++j) v[j] = __bfloat162float(hb[j]) > 0.f ? v[j] : 0.f;
-          umma::st_row8(D, row, col, W, v);
-        }
-      }
-      sync_for_mma();
-      if (tid == 0) {
-        const int dwc = l == 0 ? CM::kDW0 : CM::kDWl + (H - 1 - l) * W;
-        const unsigned char* prev = l == 0 ? X : Ht[l - 1];
-        const int pc = l == 0 ? XC : HC;
-        for (int ks = 0; ks < 8; ++ks)
-          umma::mma_bf16(tm + dwc, umma::desc_mnmajor(prev, pc, ks), umma::desc_mnmajor(D, W, ks),
-                         umma::idesc_bf16(128, W, true, true), (iter > 0 || ks > 0));
-        if (l > 0) {
-          for (int ks = 0; ks < W / 16; ++ks)
-            umma::mma_bf16(tr, umma::desc_kmajor(D, W, ks), umma::desc_mnmajor(wt.wl[l - 1], W, ks),
-                           umma::idesc_bf16(128, W, false, true), ks > 0);
-        } else {
-          for (int ks = 0; ks < W / 16; ++ks)
-            umma::mma_bf16(tr, umma::desc_kmajor(D, W, ks), umma::desc_mnmajor(wt.w0, INP, ks),
-                           umma::idesc_bf16(128, INP, false, true), ks > 0);
-        }
-        umma::commit(&bar);
-      }
-      wait_mma(&bar, phase);
-    }
-    // ---- d_features -> table-gradient scatter (field.cpp:279-292), fused
-    {
-      constexpr int NH = INP / 2;  // columns of this thread's half
-      float v[NH];
-#pragma unroll
-      for (int c = 0; c < NH; c += 8) umma::tmem_ld8(umma::taddr(tr, 32 * q, half * NH + c), v + c);
-      umma::tmem_wait_ld();  // (warp-collective loads stay outside the per-sample branch)
+
+  if (warp >= kMlpThreads / 32) {
+    // ================= scatter warps: d_features -> table gradient
+    const int r = tid - kMlpThreads;  // sample row in the tile; warp = 32 consecutive samples
+    for (uint32_t k = 0;; ++k) {
+      umma::mbar_wait(&full_bar, k & 1u);
+      const long long t = slot_tile;
+      if (t < 0) break;
+      const long long gs = t * kTile + r;
+      const bool valid = gs < n_total && __ldg(count + gs / S) > 0;
       float4 pp = make_float4(0.f, 0.f, 0.f, 0.f);
       if (valid) pp = pos[gs];
       const float px = clamp01(pp.x), py = clamp01(pp.y), pz = clamp01(pp.z);
       const unsigned long long ray_key = (unsigned long long)(gs / S) << 36;
-#pragma unroll
-      for (int j = 0; j < NH; j += 2) {
-        const int l = (half * NH + j) >> 1;  // warp-uniform
-        if (l >= fd.L) continue;
+      const float* drow = slot + r * SLD;
+      for (int l = 0; l < fd.L; ++l) {  // warp-uniform
+        const float2 dv = *reinterpret_cast<const float2*>(drow + 2 * l);
         const LevelCell cell = level_cell(fd.res[l], px, py, pz);
         // Samples of a ray are depth-sorted and a line enters each cell once, so
         // equal (ray, cell) keys form contiguous lane runs: a segmented suffix
         // sum leaves each run's total in its first lane, which alone issues the
         // 8 corner atomics (field.cpp:279-292 scatter, de-duplicated).
         const unsigned long long key =
-            valid ? (ray_key | ((unsigned long long)(cell.cz & 4095) << 24) | ((unsigned long long)(cell.cy & 4095) << 12) |
-                     (unsigned long long)(cell.cx & 4095))
+            valid ? (ray_key | ((unsigned long long)(cell.cz & 4095) << 24) |
+                     ((unsigned long long)(cell.cy & 4095) << 12) | (unsigned long long)(cell.cx & 4095))
                   : (~0ull - (unsigned long long)lane);
-        const float d0 = valid ? v[j] : 0.f, d1 = valid ? v[j + 1] : 0.f;
+        const float d0 = valid ? dv.x : 0.f, d1 = valid ? dv.y : 0.f;
         float c[16];
 #pragma unroll
         for (int corner = 0; corner < 8; ++corner) {
@@ -448,56 +377,200 @@ __global__ void __launch_bounds__(kThreads, 2)
           c[2 * corner + 1] = w * d1;
         }
         // runs are contiguous: once no run is longer than `off`, no larger
-        // offset can match either, so fine levels (runs of 1) skip all value shuffles
+        // offset can match, so fine levels (runs of 1) skip all value shuffles
         for (int off = 1; off < 32; off <<= 1) {
           const unsigned long long ok = __shfl_down_sync(0xffffffffu, key, off);
           const bool take = (lane + off < 32) && ok == key;
           if (!__any_sync(0xffffffffu, take)) break;
 #pragma unroll
-          for (int k = 0; k < 16; ++k) {
-            const float t = __shfl_down_sync(0xffffffffu, c[k], off);
-            if (take) c[k] += t;
+          for (int kk = 0; kk < 16; ++kk) {
+            const float tv = __shfl_down_sync(0xffffffffu, c[kk], off);
+            if (take) c[kk] += tv;
           }
         }
         const unsigned long long pk = __shfl_up_sync(0xffffffffu, key, 1);
-        if (valid && (lane == 0 || pk != key)) {
+        if (!skip_scatter && valid && (lane == 0 || pk != key)) {
           float* gl = grad + (long long)l * 2 * fd.rows;
 #pragma unroll
           for (int corner = 0; corner < 8; ++corner) {
             if (c[2 * corner] == 0.f && c[2 * corner + 1] == 0.f) continue;
-            const uint32_t r = table_row(fd, l, (uint32_t)(cell.cx + (corner & 1)),
-                                         (uint32_t)(cell.cy + ((corner >> 1) & 1)),
-                                         (uint32_t)(cell.cz + ((corner >> 2) & 1)));
-            atomicAdd(reinterpret_cast<float2*>(gl + (size_t)r * 2), make_float2(c[2 * corner], c[2 * corner + 1]));
+            const uint32_t rr = table_row(fd, l, (uint32_t)(cell.cx + (corner & 1)),
+                                          (uint32_t)(cell.cy + ((corner >> 1) & 1)),
+                                          (uint32_t)(cell.cz + ((corner >> 2) & 1)));
+            atomicAdd(reinterpret_cast<float2*>(gl + (size_t)rr * 2), make_float2(c[2 * corner], c[2 * corner + 1]));
           }
         }
       }
+      named_sync(2, kScatThreads);  // every scatter thread is done with the slot
+      if (r == 0) mbar_arrive(&empty_bar);
     }
-    umma::fence_before_sync();
-  }
-  // ---- flush the TMEM weight-gradient accumulators: row = input unit (or the
-  // ones row = bias), column = output unit; one atomicAdd per weight per CTA
-  __syncthreads();
-  umma::fence_after_sync();
-  if (iter > 0 && warp < 4) {
-    float* gm = grad + fd.hash_params;
-    auto flush = [&](int col0, int ncol, int n_out, int in, int bias_row, int w_off, int b_off) {
-      for (int c = 0; c < ncol; c += 8) {
-        float v[8];
-        umma::tmem_ld8(umma::taddr(tm, 32 * warp, col0 + c), v);
-        umma::tmem_wait_ld();
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int o = c + j;
-          if (o >= n_out) continue;
-          if (row < in) atomicAdd(gm + w_off + o * in + row, v[j]);
-          else if (row == bias_row) atomicAdd(gm + b_off + o, v[j]);
+  } else {
+    // ================= MLP warps: tensor-core backward chain
+    const uint32_t tr = tm + CM::kR;
+    uint32_t phase = 0;
+    int iter = 0;
+    const int q = warp & 3, half = warp >> 2, row = 32 * q + lane;
+    auto fetch = [&]() -> long long {
+      if (tid == 0) s_tile = atomicAdd(tile_ctr, 1);
+      named_sync(1, kMlpThreads);
+      return s_tile;
+    };
+    for (long long t = fetch(); t < ntiles; t = fetch(), ++iter) {
+      const long long tile0 = t * kTile;
+      const long long gs = tile0 + row;
+      const bool valid = gs < n_total && __ldg(count + gs / S) > 0;
+      // ---- stored bf16 features -> X (row-group stride differs: copy per 16 B)
+      {
+        const uint4* src = feat_tiles + t * (128 * INP * 2 / 16);
+        for (int i = tid; i < 128 * INP * 2 / 16; i += kMlpThreads) {
+          const int rg = i / INP, rem = i % INP;  // INP uint4 per row group
+          *reinterpret_cast<uint4*>(X + rg * (XC / 8) * 128 + (rem >> 3) * 128 + (rem & 7) * 16) = src[i];
         }
       }
-    };
-    flush(CM::kDWo, 16, 4, W, W, fd.w_off[H], fd.b_off[H]);
-    for (int l = H - 1; l >= 1; --l) flush(CM::kDWl + (H - 1 - l) * W, W, W, W, W, fd.w_off[l], fd.b_off[l]);
-    flush(CM::kDW0, W, W, fd.in_dim, INP, fd.w_off[0], fd.b_off[0]);
+      mlp_sync_for_mma();
+      // ---- forward recompute (field.cpp:181-211), one TMEM region reused per layer
+      if (tid == 0) {
+        for (int ks = 0; ks < INP / 16; ++ks)
+          umma::mma_bf16(tr, umma::desc_kmajor(X, XC, ks), umma::desc_kmajor(wt.w0, INP, ks),
+                         umma::idesc_bf16(128, W, false, false), ks > 0);
+        umma::commit(&bar);
+      }
+      wait_mma(&bar, phase);
+      epi_relu<W>(tr, 0, wt.bias, Ht[0], HC);
+      for (int l = 1; l < H; ++l) {
+        mlp_sync_for_mma();
+        if (tid == 0) {
+          for (int ks = 0; ks < W / 16; ++ks)
+            umma::mma_bf16(tr, umma::desc_kmajor(Ht[l - 1], HC, ks), umma::desc_kmajor(wt.wl[l - 1], W, ks),
+                           umma::idesc_bf16(128, W, false, false), ks > 0);
+          umma::commit(&bar);
+        }
+        wait_mma(&bar, phase);
+        epi_relu<W>(tr, 0, wt.bias + l * W, Ht[l], HC);
+      }
+      mlp_sync_for_mma();
+      if (tid == 0) {
+        for (int ks = 0; ks < W / 16; ++ks)
+          umma::mma_bf16(tr, umma::desc_kmajor(Ht[H - 1], HC, ks), umma::desc_kmajor(wt.wo, W, ks),
+                         umma::idesc_bf16(128, 16, false, false), ks > 0);
+        umma::commit(&bar);
+      }
+      wait_mma(&bar, phase);
+      // ---- g_raw (field.cpp:233-238) -> G tile
+      if (warp < 4) {
+        float v[8];
+        umma::tmem_ld8(umma::taddr(tr, 32 * q, 0), v);
+        umma::tmem_wait_ld();
+        float g[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        if (valid) {
+          const float4 d = dout[gs];
+          const float* b = wt.bias + H * W;
+          const float r0 = v[0] + b[0];
+          const float sg = density_forward(fd.act, r0);
+          g[0] = d.x * density_derivative(fd.act, r0, sg);
+          const float s1 = stable_sigmoid(v[1] + b[1]), s2 = stable_sigmoid(v[2] + b[2]),
+                      s3 = stable_sigmoid(v[3] + b[3]);
+          g[1] = d.y * s1 * (1.f - s1);
+          g[2] = d.z * s2 * (1.f - s2);
+          g[3] = d.w * s3 * (1.f - s3);
+        }
+        umma::st_row8(G, row, 0, 16, g);
+      }
+      mlp_sync_for_mma();
+      // ---- output layer: dW_out^T += [H_{H-1}|1]^T G;  dH_{H-1} = G W_out
+      if (tid == 0) {
+        for (int ks = 0; ks < 8; ++ks)
+          umma::mma_bf16(tm + CM::kDWo, umma::desc_mnmajor(Ht[H - 1], HC, ks), umma::desc_mnmajor(G, 16, ks),
+                         umma::idesc_bf16(128, 16, true, true), (iter > 0 || ks > 0));
+        umma::mma_bf16(tr, umma::desc_kmajor(G, 16, 0), umma::desc_mnmajor(wt.wo, W, 0),
+                       umma::idesc_bf16(128, W, false, true), 0u);
+        umma::commit(&bar);
+      }
+      wait_mma(&bar, phase);
+      for (int l = H - 1; l >= 0; --l) {
+        // D_l = dH_l * relu'(H_l) -> D tile
+        {
+          constexpr int NH = W / 2;
+#pragma unroll
+          for (int c = 0; c < NH; c += 8) {
+            const int col = half * NH + c;
+            float v[8];
+            umma::tmem_ld8(umma::taddr(tr, 32 * q, col), v);
+            umma::tmem_wait_ld();
+            const uint4 hv = *reinterpret_cast<const uint4*>(Ht[l] + umma::cm_offset(row, col, HC));
+            const __nv_bfloat16* hb = reinterpret_cast<const __nv_bfloat16*>(&hv);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v[j] = __bfloat162float(hb[j]) > 0.f ? v[j] : 0.f;
+            umma::st_row8(D, row, col, W, v);
+          }
+        }
+        mlp_sync_for_mma();
+        if (tid == 0) {
+          const int dwc = l == 0 ? CM::kDW0 : CM::kDWl + (H - 1 - l) * W;
+          const unsigned char* prev = l == 0 ? X : Ht[l - 1];
+          const int pc = l == 0 ? XC : HC;
+          for (int ks = 0; ks < 8; ++ks)
+            umma::mma_bf16(tm + dwc, umma::desc_mnmajor(prev, pc, ks), umma::desc_mnmajor(D, W, ks),
+                           umma::idesc_bf16(128, W, true, true), (iter > 0 || ks > 0));
+          if (l > 0) {
+            for (int ks = 0; ks < W / 16; ++ks)
+              umma::mma_bf16(tr, umma::desc_kmajor(D, W, ks), umma::desc_mnmajor(wt.wl[l - 1], W, ks),
+                             umma::idesc_bf16(128, W, false, true), ks > 0);
+          } else {
+            for (int ks = 0; ks < W / 16; ++ks)
+              umma::mma_bf16(tr, umma::desc_kmajor(D, W, ks), umma::desc_mnmajor(wt.w0, INP, ks),
+                             umma::idesc_bf16(128, INP, false, true), ks > 0);
+          }
+          umma::commit(&bar);
+        }
+        wait_mma(&bar, phase);
+      }
+      // ---- hand d_features to the scatter warps (slot free once they drained it)
+      {
+        constexpr int NH = INP / 2;
+        float v[NH];
+#pragma unroll
+        for (int c = 0; c < NH; c += 8) umma::tmem_ld8(umma::taddr(tr, 32 * q, half * NH + c), v + c);
+        umma::tmem_wait_ld();
+        umma::mbar_wait(&empty_bar, ((uint32_t)iter & 1u) ^ 1u);
+        float* dst = slot + row * SLD + half * NH;
+#pragma unroll
+        for (int c = 0; c < NH; c += 4) *reinterpret_cast<float4*>(dst + c) = make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]);
+        if (tid == 0) slot_tile = t;
+        umma::fence_before_sync();
+        named_sync(1, kMlpThreads);
+        if (tid == 0) mbar_arrive(&full_bar);
+      }
+    }
+    // sentinel: stop the scatter warps
+    if (tid == 0) {
+      umma::mbar_wait(&empty_bar, ((uint32_t)iter & 1u) ^ 1u);
+      slot_tile = -1;
+      mbar_arrive(&full_bar);
+    }
+    // ---- flush the TMEM weight-gradient accumulators: row = input unit (or the
+    // ones row = bias), column = output unit; one atomicAdd per weight per CTA
+    umma::fence_after_sync();
+    if (iter > 0 && warp < 4) {
+      float* gm = grad + fd.hash_params;
+      auto flush = [&](int col0, int ncol, int n_out, int in, int bias_row, int w_off, int b_off) {
+        for (int c = 0; c < ncol; c += 8) {
+          float v[8];
+          umma::tmem_ld8(umma::taddr(tm, 32 * warp, col0 + c), v);
+          umma::tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int o = c + j;
+            if (o >= n_out) continue;
+            if (row < in) atomicAdd(gm + w_off + o * in + row, v[j]);
+            else if (row == bias_row) atomicAdd(gm + b_off + o, v[j]);
+          }
+        }
+      };
+      flush(CM::kDWo, 16, 4, W, W, fd.w_off[H], fd.b_off[H]);
+      for (int l = H - 1; l >= 1; --l) flush(CM::kDWl + (H - 1 - l) * W, W, W, W, W, fd.w_off[l], fd.b_off[l]);
+      flush(CM::kDW0, W, W, fd.in_dim, INP, fd.w_off[0], fd.b_off[0]);
+    }
   }
   umma::fence_before_sync();
   __syncthreads();
@@ -521,8 +594,8 @@ size_t fwd_smem() {
 
 template <int INP, int W, int H>
 size_t bwd_smem() {
-  return WeightTiles<INP, W, H>::kBytes + ((H * W + 4) * 4 + 15) / 16 * 16 + (128 * (INP + 8) * 2 + kSlack) +
-         H * (128 * (W + 8) * 2 + kSlack) + (128 * 16 * 2 + kSlack) + (128 * W * 2 + kSlack) + 1024;
+  return WeightTiles<INP, W, H>::kBytes + ((H * W + 4) * 4 + 15) / 16 * 16 + (128 * (INP + 8) * 2 + kSlackX) +
+         H * (128 * (W + 8) * 2 + kSlackH) + 128 * 16 * 2 + 128 * W * 2 + ScatterSlot<INP>::kBytes + 1024;
 }
 
 template <int INP, int W, int H>
@@ -562,8 +635,9 @@ cudaError_t run_bwd(const FieldDesc& fd, const float* params, float* grad, long 
   const long long grid = std::min<long long>(ntiles, 2LL * sms());
   e = cudaMemsetAsync(tile_ctr, 0, sizeof(int), st);
   if (e != cudaSuccess) return e;
-  k_bwd_tc<INP, W, H><<<(unsigned)grid, kThreads, smem, st>>>(fd, params, grad, n, S, count, pos,
-                                                              reinterpret_cast<const uint4*>(feat_tiles), dout, tile_ctr);
+  k_bwd_tc<INP, W, H><<<(unsigned)grid, kBwdThreads, smem, st>>>(fd, params, grad, n, S, count, pos,
+                                                              reinterpret_cast<const uint4*>(feat_tiles), dout, tile_ctr,
+                                                              getenv("PRENOM_PROF_SKIP_SCATTER") ? 1 : 0);
   return cudaGetLastError();
 }
 
