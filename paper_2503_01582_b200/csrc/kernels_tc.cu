@@ -610,8 +610,10 @@ cudaError_t run_fwd(const FieldDesc& fd, const float* params, long long n, int S
     return v < 1 ? 1 : (v > 8 ? 8 : v);
   }();
   static const size_t min_smem = [] {
+    // measured on B200 (cfg2): 3 CTAs x 57 KB (24 warps/SM, ~57 KB L1 for the
+    // coarse-level gathers) beats both more warps with less L1 and fewer warps
     const char* e = getenv("PRENOM_FWD_SMEM_KB");
-    return (size_t)(e ? atoi(e) : 0) * 1024;
+    return (size_t)(e ? atoi(e) : 57) * 1024;
   }();
   const size_t smem = std::max<size_t>(fwd_smem<INP, W, H>(), min_smem);
   cudaError_t e = cudaFuncSetAttribute(k_fwd_tc<INP, W, H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
