@@ -50,7 +50,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--width", type=int, default=64)
-    ap.add_argument("--mlp", default="fp32", choices=["fp32", "bf16"])
+    ap.add_argument("--mlp", default="bf16", choices=["fp32", "bf16"])
     ap.add_argument("--rays", type=int, default=8192)
     ap.add_argument("--samples", type=int, default=96)
     ap.add_argument("--e2e-steps", type=int, default=20)

@@ -264,7 +264,7 @@ struct BwdCols {
 // by full/empty mbarriers; the scatter of tile t overlaps the MMA chain of
 // tile t+1.
 constexpr int kMlpThreads = 256;
-constexpr int kScatThreads = 128;
+constexpr int kScatThreads = 256;  // two warps per 32-sample group: level halves
 constexpr int kBwdThreads = kMlpThreads + kScatThreads;
 
 __device__ __forceinline__ void named_sync(int id, int n) {
@@ -345,7 +345,8 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
 
   if (warp >= kMlpThreads / 32) {
     // ================= scatter warps: d_features -> table gradient
-    const int r = tid - kMlpThreads;  // sample row in the tile; warp = 32 consecutive samples
+    const int r = (tid - kMlpThreads) & 127;  // sample row in the tile; warp = 32 consecutive samples
+    const int lhalf = (tid - kMlpThreads) >> 7;  // levels [lhalf*L/2, ...)
     for (uint32_t k = 0;; ++k) {
       umma::mbar_wait(&full_bar, k & 1u);
       const long long t = slot_tile;
@@ -357,7 +358,8 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
       const float px = clamp01(pp.x), py = clamp01(pp.y), pz = clamp01(pp.z);
       const unsigned long long ray_key = (unsigned long long)(gs / S) << 36;
       const float* drow = slot + r * SLD;
-      for (int l = 0; l < fd.L; ++l) {  // warp-uniform
+      const int l_lo = lhalf ? (fd.L + 1) / 2 : 0, l_hi = lhalf ? fd.L : (fd.L + 1) / 2;
+      for (int l = l_lo; l < l_hi; ++l) {  // warp-uniform
         const float2 dv = *reinterpret_cast<const float2*>(drow + 2 * l);
         const LevelCell cell = level_cell(fd.res[l], px, py, pz);
         // Samples of a ray are depth-sorted and a line enters each cell once, so
@@ -402,7 +404,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
         }
       }
       named_sync(2, kScatThreads);  // every scatter thread is done with the slot
-      if (r == 0) mbar_arrive(&empty_bar);
+      if (tid == kMlpThreads) mbar_arrive(&empty_bar);
     }
   } else {
     // ================= MLP warps: tensor-core backward chain
