@@ -145,8 +145,13 @@ def peaks():
     return p
 
 
-def algorithmic_costs(arch, B, S, n_coarse, P):
-    """SURVEY.md §8(d) per-launch algorithmic bytes / flops (N = B*S samples)."""
+def algorithmic_costs(arch, B, S, n_coarse, P, mlp="bf16"):
+    """SURVEY.md §8(d) per-launch algorithmic bytes / flops (N = B*S samples).
+
+    bf16 mode: k_bwd_tc fuses the MLP backward (tensor cores) with the
+    table-gradient scatter; its dominant work is the scatter's read-modify-
+    write of 2*8*L*F*4 B/sample, so it is rated against HBM bandwidth (its
+    tensor-pipe use is reported separately as `tensor`)."""
     N = B * S
     L, F, W, H, IN = arch.hash_levels, arch.features_per_level, arch.hidden_width, arch.hidden_layers, \
         arch.hash_levels * arch.features_per_level
@@ -157,10 +162,10 @@ def algorithmic_costs(arch, B, S, n_coarse, P):
         # encode gathers 8*L*F*4 B/sample (the MLP forward rides in the same kernel, fused)
         "field_fwd": ("hbm", 8 * L * F * 4 * N),
         "composite": ("hbm", 40 * N),
-        # MLP backward: recompute fwd + 2x fwd for the backward
-        "mlp_bwd": ("tensor", 3 * mlp_fwd_flops * N),
+        # bf16: fused MLP bwd + scatter RMW (2*8*L*F*4 B/sample); fp32: SIMT MLP backward flops
+        "mlp_bwd": ("hbm", 2 * 8 * L * F * 4 * N) if mlp == "bf16" else ("tensor", 3 * mlp_fwd_flops * N),
         # table-gradient RMW: 2 * 8*L*F*4 B/sample
-        "encode_bwd": ("hbm", 2 * 8 * L * F * 4 * N),
+        "encode_bwd": ("hbm", 2 * 8 * L * F * 4 * N),  # fp32 path: standalone k_encode_bwd
         # dense Adam: p,m,v read+write, g read + zero = 32 B/param
         "adam": ("hbm", 32 * P),
         "refresh": ("hbm", 0),
@@ -280,7 +285,10 @@ def run_ours(args):
     # roofline of the dominant kernel (largest share of the step), live events
     pk = peaks()
     costs = algorithmic_costs(arch, cfg.rays_per_iter, cfg.samples_per_ray, cfg.coarse_samples,
-                              arch.param_count())
+                              arch.param_count(), args.mlp)
+    mlp_flops = 3 * 2 * (arch.hash_levels * arch.features_per_level * arch.hidden_width
+                         + (arch.hidden_layers - 1) * arch.hidden_width ** 2 + 4 * arch.hidden_width) \
+        * cfg.rays_per_iter * cfg.samples_per_ray
     traffic = load_traffic()
     kernels = {}
     total_k = sum(kms[i] for i in range(7)) or 1.0
@@ -311,7 +319,13 @@ def run_ours(args):
     enc_t = (kernels.get("field_fwd", {}).get("ms_per_launch", 0) + kernels.get("encode_bwd", {}).get(
         "ms_per_launch", 0)) / 1e3
     encode_roofline = {"achieved": round(enc_bytes / enc_t / 1e9, 2) if enc_t else None, "unit": "GB/s",
-                       "peak": pk["hbm_gbs"], "frac": round(enc_bytes / enc_t / 1e9 / pk["hbm_gbs"], 4) if enc_t else None}
+                       "peak": pk["hbm_gbs"], "frac": round(enc_bytes / enc_t / 1e9 / pk["hbm_gbs"], 4) if enc_t else None,
+                       "bytes_per_sample": 96 * arch.hash_levels * arch.features_per_level,
+                       "kernels": ["field_fwd", "encode_bwd" if "encode_bwd" in kernels else "mlp_bwd"]}
+    if "mlp_bwd" in kernels and args.mlp == "bf16":
+        t_bwd = kernels["mlp_bwd"]["ms_per_launch"] / 1e3
+        kernels["mlp_bwd"]["tensor"] = {"flops_per_launch": mlp_flops, "achieved_tflops": round(mlp_flops / t_bwd / 1e12, 2),
+                                        "frac_of_bf16_sustained": round(mlp_flops / t_bwd / 1e12 / pk["bf16_tflops_sustained"], 4)}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:

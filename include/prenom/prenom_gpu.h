@@ -258,6 +258,11 @@ prenom_status prenom_reptile_apply(prenom_object_t meta, const float* delta_dev,
 /* Copy parameters device-to-device (fresh inner-loop copy: inner_adapt's
  * `ParamVector params = theta`, meta.cpp:31) and reset Adam (meta.cpp:32). */
 prenom_status prenom_object_copy_params(prenom_object_t dst, prenom_object_t src);
+/* meta <- (1 - beta) * meta + beta * adapted, exactly meta.cpp:83-92 (one task). */
+prenom_status prenom_reptile_update(prenom_object_t meta, prenom_object_t adapted, float beta);
+/* Philox key of the object's draws (inner_adapt uses mt19937(derive_seed(seed,
+ * step)) per meta-step, meta.cpp:111; here: set_seed(derive_seed(...))). */
+prenom_status prenom_object_set_seed(prenom_object_t obj, uint64_t seed);
 
 /* ---- single-stage debug / parity entry points ---------------------------
  * Run one stage on caller (host) buffers so unit parity does not depend on

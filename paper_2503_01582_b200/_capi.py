@@ -137,7 +137,8 @@ EXPORTED = [
     "prenom_render", "prenom_density_query", "prenom_field_eval",
     "prenom_get_params", "prenom_set_params", "prenom_get_grid", "prenom_set_grid",
     "prenom_get_adam", "prenom_reset_adam", "prenom_train_step_many",
-    "prenom_reptile_delta", "prenom_reptile_apply", "prenom_object_copy_params",
+    "prenom_reptile_delta", "prenom_reptile_apply", "prenom_object_copy_params", "prenom_reptile_update",
+    "prenom_object_set_seed",
     "prenom_debug_philox", "prenom_debug_hash_encode", "prenom_debug_field_eval",
     "prenom_debug_field_backward", "prenom_debug_adam", "prenom_debug_sample_rays",
     "prenom_debug_batch_loss", "prenom_debug_generate_rays", "prenom_debug_umma_gemm",
@@ -207,6 +208,8 @@ def _declare(lib):
         "prenom_reptile_delta": (i32, [P, P, C.c_void_p]),
         "prenom_reptile_apply": (i32, [P, C.c_void_p, i32, C.c_float]),
         "prenom_object_copy_params": (i32, [P, P]),
+        "prenom_reptile_update": (i32, [P, P, C.c_float]),
+        "prenom_object_set_seed": (i32, [P, u64]),
         "prenom_debug_philox": (i32, [P, i32, u32p, u32p]),
         "prenom_debug_hash_encode": (i32, [P, archp, f32p, i32, f32p, f32p]),
         "prenom_debug_field_eval": (i32, [P, archp, f32p, i32, f32p, f32p, f32p, f32p, i32]),

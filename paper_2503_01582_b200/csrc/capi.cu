@@ -922,6 +922,22 @@ prenom_status prenom_reptile_apply(prenom_object_t meta, const float* delta_dev,
   return PRENOM_OK;
 }
 
+prenom_status prenom_reptile_update(prenom_object_t meta, prenom_object_t adapted, float beta) {
+  if (!meta || !adapted) return fail(PRENOM_USAGE, "NULL argument");
+  if (meta->P != adapted->P) return fail(PRENOM_DATA, "reptile_update: parameter vectors differ in length");
+  CUDA_TRY(cudaSetDevice(meta->ctx->device));
+  CUDA_TRY(cudaStreamSynchronize(adapted->ctx->stream));
+  CUDA_TRY(launch_reptile_update(meta->P, meta->params.p, adapted->params.p, beta, meta->ctx->stream));
+  meta->ctx->launches += 1;
+  return PRENOM_OK;
+}
+
+prenom_status prenom_object_set_seed(prenom_object_t o, uint64_t seed) {
+  if (!o) return fail(PRENOM_USAGE, "NULL object");
+  o->seed = seed;
+  return PRENOM_OK;
+}
+
 prenom_status prenom_object_copy_params(prenom_object_t dst, prenom_object_t src) {
   if (!dst || !src) return fail(PRENOM_USAGE, "NULL argument");
   if (dst->P != src->P) return fail(PRENOM_DATA, "parameter vectors differ in length");

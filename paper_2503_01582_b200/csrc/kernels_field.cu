@@ -605,6 +605,13 @@ __global__ void k_reptile_apply(size_t n, float* meta, const float* delta, float
   }
 }
 
+// meta.cpp:83-92: out = keep * meta + beta * adapted (keep = 1 - beta), in place.
+__global__ void k_reptile_update(size_t n, float* meta, const float* adapted, float beta) {
+  const float keep = __fsub_rn(1.f, beta);
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    meta[i] = __fadd_rn(__fmul_rn(keep, meta[i]), __fmul_rn(beta, adapted[i]));
+}
+
 int g_num_sms = 0;
 int num_sms() {
   if (!g_num_sms) {
@@ -713,6 +720,11 @@ cudaError_t launch_philox(int n, const uint32_t* ck, uint32_t* out, cudaStream_t
 
 cudaError_t launch_reptile_delta(size_t n, const float* meta, const float* adapted, float* delta, cudaStream_t st) {
   k_reptile_delta<<<num_sms() * 4, 256, 0, st>>>(n, meta, adapted, delta);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reptile_update(size_t n, float* meta, const float* adapted, float beta, cudaStream_t st) {
+  k_reptile_update<<<num_sms() * 4, 256, 0, st>>>(n, meta, adapted, beta);
   return cudaGetLastError();
 }
 

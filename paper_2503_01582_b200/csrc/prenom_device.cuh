@@ -300,6 +300,7 @@ cudaError_t launch_reptile_delta(size_t n, const float* meta, const float* adapt
                                  cudaStream_t st);
 cudaError_t launch_reptile_apply(size_t n, float* meta, const float* delta, float inv_n,
                                  float beta, cudaStream_t st);
+cudaError_t launch_reptile_update(size_t n, float* meta, const float* adapted, float beta, cudaStream_t st);
 // bf16 tensor-core MLP path (kernels_tc.cu)
 bool tc_supported(const FieldDesc& fd);
 size_t tc_feature_bytes(const FieldDesc& fd, long long n);

@@ -352,7 +352,15 @@ class ObjectTrainer:
         _check(self.lib.prenom_reset_adam(self.h))
 
     def copy_params_from(self, other: "ObjectTrainer"):
+        """params <- other's params (device to device) and a fresh Adam (meta.cpp:31-34)."""
         _check(self.lib.prenom_object_copy_params(self.h, other.h))
+
+    def set_seed(self, seed: int):
+        _check(self.lib.prenom_object_set_seed(self.h, seed))
+
+    def reptile_update(self, adapted: "ObjectTrainer", beta: float):
+        """self <- (1-beta)*self + beta*adapted (meta.cpp:83-92), on the device."""
+        _check(self.lib.prenom_reptile_update(self.h, adapted.h, beta))
 
     def debug_generate_rays(self, frame: int, step: int):
         n = self.cfg.rays_per_iter

@@ -1,0 +1,84 @@
+"""GPU: Reptile meta-training (CudaEngine) and multi-object training vs the oracle."""
+import numpy as np
+import pytest
+import torch
+
+from paper_2503_01582_b200 import FieldArch, ObjectTrainer, TrainConfig, scenes
+from paper_2503_01582_b200 import trainer as T
+from paper_2503_01582_b200.meta import CudaEngine, MetaConfig, meta_train
+
+from test_meta_parallel import OracleEngine
+
+pytestmark = pytest.mark.gpu
+
+ARCH = FieldArch(hash_levels=6, features_per_level=2, log2_table_size=11, base_resolution=6, per_level_scale=1.5,
+                 hidden_width=16, hidden_layers=2)
+CFG = TrainConfig(rays_per_iter=64, samples_per_ray=16, prior_sampling=0, grid_refresh_every=0)
+
+
+def tasks():
+    return [scenes.box_union_scene(n_views=4, res=32, seed=200 + i) for i in range(3)]
+
+
+@pytest.mark.parametrize("tps", [1, 3])
+def test_reptile_cuda_engine_matches_oracle_engine(ctx, oracle, tps):
+    ts = tasks()
+    theta = (np.random.default_rng(1).standard_normal(ARCH.param_count()) * 0.05).astype(np.float32)
+    meta = ObjectTrainer.create(ctx, ARCH, theta=theta, grid_res=8, cfg=CFG)
+    workers = []
+    for sc in ts:
+        w = ObjectTrainer.create(ctx, ARCH, theta=theta, grid_res=8, cfg=CFG, box_min=sc.box_min, box_max=sc.box_max)
+        w.set_frames(sc.cams, sc.rgb, sc.depth, sc.mask, 1, sc.obj_pose)
+        workers.append(w)
+    mc = MetaConfig(N=3, q=4, beta=0.2, seed=7, tasks_per_step=tps)
+    meta_train(CudaEngine(meta, workers), len(ts), mc)
+    ref = OracleEngine(oracle, ARCH, theta, ts, CFG)
+    meta_train(ref, len(ts), mc)
+    got = meta.get_params()
+    # Same draws (bit-exact samples); parameters differ only by gradient summation order.
+    moved = np.abs(ref.theta - theta) > 1e-6
+    assert moved.mean() > 0.01
+    err = np.abs(got - ref.theta)
+    assert np.quantile(err, 0.999) < 2e-3, np.quantile(err, 0.999)
+
+
+def test_train_many_equals_individual_training(ctx):
+    """prenom_train_step_many (objects back to back on one stream) == training each alone."""
+    ts = tasks()
+    objs_a, objs_b = [], []
+    for i, sc in enumerate(ts):
+        for lst in (objs_a, objs_b):
+            o = ObjectTrainer.create(ctx, ARCH, grid_res=8, seed=10 + i, cfg=CFG, box_min=sc.box_min, box_max=sc.box_max)
+            o.set_frames(sc.cams, sc.rgb, sc.depth, sc.mask, 1, sc.obj_pose)
+            lst.append(o)
+    T.train_many(objs_a, 5)
+    for o in objs_b:
+        o.train_step(5, stats=False)
+    for a, b in zip(objs_a, objs_b):
+        la, lb = a.last_stats(5), b.last_stats(5)
+        for x, y in zip(la, lb):
+            assert x["n_samples"] == y["n_samples"] and x["frame"] == y["frame"]
+            assert abs(x["total"] - y["total"]) <= 1e-4 * abs(y["total"])
+
+
+def test_reptile_delta_apply_linearity(ctx, rng):
+    """prenom_reptile_delta + NCCL-style sum + prenom_reptile_apply == reptile_update(theta, mean)."""
+    P = ARCH.param_count()
+    th = rng.standard_normal(P).astype(np.float32)
+    meta = ObjectTrainer.create(ctx, ARCH, theta=th, grid_res=8, cfg=CFG)
+    ads = [rng.standard_normal(P).astype(np.float32) for _ in range(3)]
+    objs = [ObjectTrainer.create(ctx, ARCH, theta=a, grid_res=8, cfg=CFG) for a in ads]
+    acc = torch.zeros(P, device="cuda")
+    tmp = torch.empty(P, device="cuda")
+    for o in objs:
+        T.reptile_delta(meta, o, tmp.data_ptr())
+        acc += tmp
+    torch.cuda.synchronize()
+    T.reptile_apply(meta, acc.data_ptr(), 3, 0.1)
+    mean = np.mean(ads, axis=0)
+    want = (np.float32(0.9) * th + np.float32(0.1) * mean).astype(np.float32)
+    np.testing.assert_allclose(meta.get_params(), want, rtol=1e-5, atol=1e-6)
+    # exact single-task update (meta.cpp:83-92)
+    meta.set_params(th)
+    meta.reptile_update(objs[0], 0.1)
+    assert np.array_equal(meta.get_params(), (np.float32(0.9) * th + np.float32(0.1) * ads[0]).astype(np.float32))
