@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg3", "cfg4"])
     ap.add_argument("--width", type=int, default=64)
     ap.add_argument("--mlp", default="bf16", choices=["fp32", "bf16"])
     ap.add_argument("--rays", type=int, default=8192)
@@ -183,34 +184,215 @@ def load_traffic():
 
 
 # --------------------------------------------------------------- our arm
+class Workload:
+    """One bench workload: objects on this rank, how to run K steps, how to count."""
+
+    name = ""
+    e2e_capable = False
+
+    def step(self, k):
+        raise NotImplementedError
+
+    def samples(self, k):
+        raise NotImplementedError
+
+    def work_items(self):
+        """[(arch, cfg, steps_factor)] whose per-step algorithmic costs add up."""
+        raise NotImplementedError
+
+
+class Cfg2(Workload):
+    """BASELINE config 2: one object with a 32^3 prior (the headline)."""
+
+    name = "cfg2"
+    e2e_capable = True
+
+    def __init__(self, args, ctx, rank, ws):
+        from paper_2503_01582_b200 import ObjectTrainer
+
+        self.sc, grid, self.arch, self.cfg = make_workload(args, rank)
+        self.obj = ObjectTrainer.create(ctx, self.arch, theta=None, grid=grid, seed=7 + rank, cfg=self.cfg,
+                                        box_min=self.sc.box_min, box_max=self.sc.box_max)
+        self.obj.set_frames(self.sc.cams, self.sc.rgb, self.sc.depth, self.sc.mask, 1, self.sc.obj_pose)
+        self.objs = [self.obj]
+        self.n_objects_total = ws
+        self.desc = ("cfg2: single object with 32^3 prior, L16 F2 T19 max-res 1024, MLP "
+                     f"W{self.arch.hidden_width} H{self.arch.hidden_layers}, {self.cfg.rays_per_iter} rays x "
+                     f"{self.cfg.samples_per_ray} MLP samples (32 coarse grid lookups), 50 views 256^2, "
+                     "Adam lr 1e-2, grid refresh every 50")
+        self.extra = {"rays_per_step": self.cfg.rays_per_iter, "mlp_samples_per_ray": self.cfg.samples_per_ray,
+                      "coarse_samples": self.cfg.coarse_samples, "params": self.arch.param_count(),
+                      "objects_per_gpu": 1,
+                      "l2": "inputs larger than L2 (params+grad+Adam m,v = 256 MiB streamed every step); no flush"}
+
+    def step(self, k):
+        self.obj.train_step(k, stats=False)
+
+    def samples(self, k):
+        st = self.obj.last_stats(k)
+        self.loss = {"first": st[0]["total"], "last": st[-1]["total"]}
+        return sum(s["n_samples"] for s in st)
+
+    def work_items(self):
+        return [(self.arch, self.cfg, 1)]
+
+
+class Cfg3(Workload):
+    """BASELINE config 3: 32 objects in 4 categories (seeded GA-style arch draw),
+    each a box union with a 64^3 prior, 2048 rays x 96 samples, 40 views 256^2;
+    objects LPT-sharded over the ranks (no collective)."""
+
+    name = "cfg3"
+
+    def __init__(self, args, ctx, rank, ws):
+        from paper_2503_01582_b200 import FieldArch, ObjectTrainer, TrainConfig, scenes
+        from paper_2503_01582_b200._capi import MLP_BF16, MLP_FP32
+        from paper_2503_01582_b200.parallel import shard_lpt, step_cost
+
+        rng = np.random.default_rng(31)
+        cats = []
+        for _ in range(4):
+            L = int(rng.choice([8, 12, 16]))
+            cats.append(FieldArch(hash_levels=L, features_per_level=2, log2_table_size=int(rng.integers(14, 20)),
+                                  base_resolution=16, per_level_scale=FieldArch.scale_for(16, 1024, L),
+                                  hidden_width=int(rng.choice([32, 64])), hidden_layers=int(rng.choice([1, 2]))))
+        n_obj = 32
+        archs = [cats[i % 4] for i in range(n_obj)]
+        self.cfg = TrainConfig(rays_per_iter=2048, samples_per_ray=96, coarse_samples=32, prior_sampling=1,
+                               grid_refresh_every=50, mlp_precision=MLP_BF16 if args.mlp == "bf16" else MLP_FP32)
+        shards = shard_lpt([step_cost(a, 2048, 96) for a in archs], ws)
+        self.mine = shards[rank]
+        self.objs, self.archs = [], []
+        for i in self.mine:
+            sc = scenes.box_union_scene(n_views=40, res=256, seed=5000 + i)
+            grid = scenes.occupancy_prior(sc.boxes, R=64)
+            o = ObjectTrainer.create(ctx, archs[i], theta=None, grid=grid, seed=900 + i, cfg=self.cfg,
+                                     box_min=sc.box_min, box_max=sc.box_max)
+            o.set_frames(sc.cams, sc.rgb, sc.depth, sc.mask, 1, sc.obj_pose)
+            self.objs.append(o)
+            self.archs.append(archs[i])
+        self.n_objects_total = n_obj
+        self.desc = ("cfg3: 32 objects (4 categories, archs L{8,12,16} T2^14..2^19 W{32,64} H{1,2}), "
+                     "64^3 priors, 2048 rays x 96 samples per object-step, 40 views 256^2, LPT-sharded")
+        self.extra = {"objects_total": n_obj, "objects_on_rank0": len(self.mine),
+                      "category_archs": [dict(L=a.hash_levels, T=a.log2_table_size, W=a.hidden_width,
+                                              H=a.hidden_layers) for a in cats],
+                      "l2": "inputs larger than L2 (all objects' params+Adam state); no flush"}
+
+    def step(self, k):
+        from paper_2503_01582_b200.trainer import train_many
+
+        train_many(self.objs, k)
+
+    def samples(self, k):
+        n, first, last = 0, 0.0, 0.0
+        for o in self.objs:
+            st = o.last_stats(k)
+            n += sum(s["n_samples"] for s in st)
+            first += st[0]["total"]
+            last += st[-1]["total"]
+        self.loss = {"first_sum": first, "last_sum": last}
+        return n
+
+    def work_items(self):
+        return [(a, self.cfg, 1) for a in self.archs]
+
+
+class Cfg4(Workload):
+    """BASELINE config 4: Reptile meta-learning of a category prior. One
+    meta-step = every rank adapts one task (32 inner Adam steps of 4096 rays
+    x 64 midpoint samples, fresh Adam), then the task deltas are all-reduced
+    over NCCL and theta <- theta + eps * mean(delta) (eps = 0.1). Arch L16 F2
+    T2^18 W64 H2; tasks are seeded box unions with 20 views at 128^2 (a pool
+    of 4 tasks per rank stands in for BASELINE's 512 x 4 shapes: the per-step
+    work does not depend on the pool size)."""
+
+    name = "cfg4"
+
+    def __init__(self, args, ctx, rank, ws):
+        from paper_2503_01582_b200 import ObjectTrainer, TrainConfig, scenes
+        from paper_2503_01582_b200._capi import MLP_BF16, MLP_FP32
+        from paper_2503_01582_b200.meta import CudaEngine
+
+        self.ws, self.rank = ws, rank
+        self.arch = scenes.cfg4_arch()
+        self.cfg = TrainConfig(rays_per_iter=4096, samples_per_ray=64, prior_sampling=0, grid_refresh_every=0,
+                               mlp_precision=MLP_BF16 if args.mlp == "bf16" else MLP_FP32)
+        self.q = 32
+        self.meta = ObjectTrainer.create(ctx, self.arch, theta=None, grid_res=8, seed=4242, cfg=self.cfg)
+        self.workers = []
+        for i in range(4):
+            sc = scenes.box_union_scene(n_views=20, res=128, seed=7000 + 4 * rank + i)
+            w = ObjectTrainer.create(ctx, self.arch, theta=None, grid_res=8, seed=1, cfg=self.cfg,
+                                     box_min=sc.box_min, box_max=sc.box_max)
+            w.set_frames(sc.cams, sc.rgb, sc.depth, sc.mask, 1, sc.obj_pose)
+            self.workers.append(w)
+        self.objs = self.workers
+        self.engine = CudaEngine(self.meta, self.workers)
+        self.n_objects_total = ws
+        self.k = 0
+        self.n = 0
+        self.desc = ("cfg4: Reptile meta-step = per rank one task x 32 inner Adam steps of 4096 rays x 64 samples "
+                     "(L16 F2 T18 W64 H2), NCCL all-reduce of task deltas, eps 0.1")
+        self.extra = {"inner_steps": self.q, "rays_per_inner_step": 4096, "mlp_samples_per_ray": 64,
+                      "tasks_per_meta_step": ws, "params": self.arch.param_count(),
+                      "l2": "inputs larger than L2 (params+Adam state 128 MiB per task + meta); no flush"}
+
+    def step(self, k):
+        import torch
+
+        from paper_2503_01582_b200.trainer import derive_seed
+
+        for _ in range(k):
+            t = self.k % len(self.workers)
+            self.engine.adapt(t, self.q, derive_seed(0, self.k * self.ws + self.rank))
+            st = self.workers[t].last_stats(self.q)
+            self.n += sum(s["n_samples"] for s in st)
+            if self.ws == 1:
+                self.engine.update_exact(t, 0.1)
+            else:
+                buf = self.engine.delta_sum([t])
+                torch.distributed.all_reduce(buf)
+                self.engine.apply(buf, self.ws, 0.1)
+            self.k += 1
+
+    def samples(self, k):
+        n, self.n = self.n, 0
+        self.loss = {}
+        return n
+
+    def work_items(self):
+        return [(self.arch, self.cfg, self.q)]
+
+
+WORKLOADS = {"cfg2": Cfg2, "cfg3": Cfg3, "cfg4": Cfg4}
+
+
 def run_ours(args):
+    import ctypes as C
+
     import torch
 
     ws, rank, local = dist_info()
+    torch.cuda.set_device(local)
     if ws > 1:
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:
-        torch.cuda.set_device(local)
-    from paper_2503_01582_b200 import Context, ObjectTrainer
+    from paper_2503_01582_b200 import Context
     from paper_2503_01582_b200._capi import KERNEL_CLASSES
 
-    sc, grid, arch, cfg = make_workload(args, rank)
     ctx = Context(local)
-    obj = ObjectTrainer.create(ctx, arch, theta=None, grid=grid, seed=7 + rank, cfg=cfg, box_min=sc.box_min,
-                               box_max=sc.box_max)
-    obj.set_frames(sc.cams, sc.rgb, sc.depth, sc.mask, 1, sc.obj_pose)
+    wl = WORKLOADS[args.workload](args, ctx, rank, ws)
     stream = torch.cuda.ExternalStream(ctx.stream)
     lib = ctx.lib
-    import ctypes as C
 
     # warm-up (untimed)
-    obj.train_step(args.warmup, stats=False)
+    wl.step(args.warmup)
     ctx.synchronize()
+    wl.samples(args.warmup)
 
-    # timed region: K steps, one C call, per-kernel events on
+    # timed region: K steps, per-kernel events on
     launches0 = ctx.launch_count()
     lib.prenom_ctx_profile(ctx.h, 1)
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -220,7 +402,7 @@ def run_ours(args):
     ctx.synchronize()
     with ClockSampler(local) as clk:
         t_start.record(stream)
-        obj.train_step(args.steps, stats=False)
+        wl.step(args.steps)
         t_end.record(stream)
         ctx.synchronize()
         torch.cuda.synchronize()
@@ -232,13 +414,12 @@ def run_ours(args):
     kn = (C.c_int64 * 7)()
     lib.prenom_ctx_kernel_times(ctx.h, kms, kn)
     lib.prenom_ctx_profile(ctx.h, 0)
-    stats = obj.last_stats(args.steps)
-    n_samples = sum(s["n_samples"] for s in stats)
-    loss_first, loss_last = stats[0]["total"], stats[-1]["total"]
+    n_samples = wl.samples(args.steps)
 
     # e2e through the C-ABI with host buffers (pinned), loss read back every step
     e2e = None
-    if args.e2e_steps > 0:
+    if args.e2e_steps > 0 and wl.e2e_capable:
+        sc, obj = wl.sc, wl.obj
         rgb_h = torch.from_numpy(np.ascontiguousarray(sc.rgb)).pin_memory()
         dep_h = torch.from_numpy(np.ascontiguousarray(sc.depth)).pin_memory()
         npx = sc.rgb.shape[1] * sc.rgb.shape[2]
@@ -261,8 +442,7 @@ def run_ours(args):
             e_samples += st["n_samples"]
         e_end.record(stream)
         ctx.synchronize()
-        e_ms = e_start.elapsed_time(e_end)
-        e2e = dict(ms=e_ms, samples=e_samples, h2d=h2d // args.e2e_steps, d2h=48)
+        e2e = dict(ms=e_start.elapsed_time(e_end), samples=e_samples, h2d=h2d // args.e2e_steps, d2h=48)
 
     # aggregate over ranks: max time, summed samples
     t_dev = ms / 1e3
@@ -280,55 +460,62 @@ def run_ours(args):
         if e2e:
             e2e["ms"], e2e["samples"] = e_t * 1e3, e_tot
     value = tot_samples / t_dev
-    per_gpu = value / ws
 
-    # roofline of the dominant kernel (largest share of the step), live events
+    # roofline of the dominant kernel class, from live events: total algorithmic work
+    # of the timed region (summed over the rank's objects) / total kernel time
     pk = peaks()
-    costs = algorithmic_costs(arch, cfg.rays_per_iter, cfg.samples_per_ray, cfg.coarse_samples,
+    work = {}
+    tensor_flops = 0.0
+    for arch, cfg, fac in wl.work_items():
+        c = algorithmic_costs(arch, cfg.rays_per_iter, cfg.samples_per_ray, cfg.coarse_samples,
                               arch.param_count(), args.mlp)
-    mlp_flops = 3 * 2 * (arch.hash_levels * arch.features_per_level * arch.hidden_width
-                         + (arch.hidden_layers - 1) * arch.hidden_width ** 2 + 4 * arch.hidden_width) \
-        * cfg.rays_per_iter * cfg.samples_per_ray
+        for name, (bound, w) in c.items():
+            work.setdefault(name, [bound, 0.0])[1] += w * fac * args.steps
+        tensor_flops += 3 * 2 * (arch.hash_levels * arch.features_per_level * arch.hidden_width
+                                 + (arch.hidden_layers - 1) * arch.hidden_width ** 2 + 4 * arch.hidden_width) \
+            * cfg.rays_per_iter * cfg.samples_per_ray * fac * args.steps
     traffic = load_traffic()
     kernels = {}
     total_k = sum(kms[i] for i in range(7)) or 1.0
     for i, name in enumerate(KERNEL_CLASSES):
         if kn[i] == 0:
             continue
-        avg_s = kms[i] / kn[i] / 1e3
-        bound, work = costs[name]
+        t_tot = kms[i] / 1e3
+        bound, w = work[name]
         if bound == "hbm":
-            ach = work / avg_s / 1e9
-            peak, unit = pk["hbm_gbs"], "GB/s"
+            ach, peak, unit = w / t_tot / 1e9, pk["hbm_gbs"], "GB/s"
         else:
-            ach = work / avg_s / 1e12
-            peak, unit = pk["bf16_tflops_sustained"], "TFLOP/s"
+            ach, peak, unit = w / t_tot / 1e12, pk["bf16_tflops_sustained"], "TFLOP/s"
         kernels[name] = {"ms_per_launch": round(kms[i] / kn[i], 4), "launches": int(kn[i]),
                          "share": round(kms[i] / total_k, 4), "bound": bound, "achieved": round(ach, 2),
-                         "unit": unit, "frac": round(ach / peak, 4) if work else None,
-                         "work_per_launch": work}
+                         "unit": unit, "frac": round(ach / peak, 4) if w else None,
+                         "work_per_launch": w / kn[i]}
     dom = max((k for k in kernels if k != "refresh"), key=lambda k: kernels[k]["share"])
     d = kernels[dom]
     roofline = {"kernel": dom, "bound": d["bound"], "achieved": d["achieved"],
                 "peak": pk["hbm_gbs"] if d["bound"] == "hbm" else pk["bf16_tflops_sustained"],
                 "unit": d["unit"], "frac": d["frac"],
-                "traffic": traffic.get(dom, {}).get("dram_bytes_per_launch"),
+                "traffic": traffic.get(dom, {}).get("dram_bytes_per_launch") if args.workload == "cfg2" else None,
                 "peak_source": pk["source"] + (" hbm_gbs" if d["bound"] == "hbm" else " bf16_tflops_sustained")}
-    # encode kernels (north_star: >= 50% of the memory roofline)
-    enc_bytes = costs["field_fwd"][1] + costs["encode_bwd"][1]
-    enc_t = (kernels.get("field_fwd", {}).get("ms_per_launch", 0) + kernels.get("encode_bwd", {}).get(
-        "ms_per_launch", 0)) / 1e3
+    # encode kernels (north_star: >= 50% of the memory roofline for the encoding kernels):
+    # gathers (fwd) + scatter RMW (bwd) over the time of the kernels that contain them
+    # (bf16: k_fwd_tc + k_bwd_tc, which also run the MLP -> a lower bound)
+    bwd_name = "encode_bwd" if "encode_bwd" in kernels else "mlp_bwd"
+    enc_bytes = work["field_fwd"][1] + work["encode_bwd"][1]
+    enc_t = (kms[KERNEL_CLASSES.index("field_fwd")] + kms[KERNEL_CLASSES.index(bwd_name)]) / 1e3
     encode_roofline = {"achieved": round(enc_bytes / enc_t / 1e9, 2) if enc_t else None, "unit": "GB/s",
-                       "peak": pk["hbm_gbs"], "frac": round(enc_bytes / enc_t / 1e9 / pk["hbm_gbs"], 4) if enc_t else None,
-                       "bytes_per_sample": 96 * arch.hash_levels * arch.features_per_level,
-                       "kernels": ["field_fwd", "encode_bwd" if "encode_bwd" in kernels else "mlp_bwd"]}
+                       "peak": pk["hbm_gbs"],
+                       "frac": round(enc_bytes / enc_t / 1e9 / pk["hbm_gbs"], 4) if enc_t else None,
+                       "bytes_per_sample": "96*L*F (8 corners x L*F x (4 B gather + 8 B RMW))",
+                       "kernels": ["field_fwd", bwd_name]}
     if "mlp_bwd" in kernels and args.mlp == "bf16":
-        t_bwd = kernels["mlp_bwd"]["ms_per_launch"] / 1e3
-        kernels["mlp_bwd"]["tensor"] = {"flops_per_launch": mlp_flops, "achieved_tflops": round(mlp_flops / t_bwd / 1e12, 2),
-                                        "frac_of_bf16_sustained": round(mlp_flops / t_bwd / 1e12 / pk["bf16_tflops_sustained"], 4)}
+        t_bwd = kms[KERNEL_CLASSES.index("mlp_bwd")] / 1e3
+        kernels["mlp_bwd"]["tensor"] = {
+            "flops": tensor_flops, "achieved_tflops": round(tensor_flops / t_bwd / 1e12, 2),
+            "frac_of_bf16_sustained": round(tensor_flops / t_bwd / 1e12 / pk["bf16_tflops_sustained"], 4)}
 
     cpu = None
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline and args.workload == "cfg2":
         try:
             cpu = cpu_baseline(args, budget_s=args.cpu_seconds)
         except Exception as e:  # reported, never fatal
@@ -339,17 +526,11 @@ def run_ours(args):
             "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(t_dev * 1e3 / args.steps, 4), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32" if args.mlp == "fp32" else "f32+bf16-mlp",
-            "data": "synthetic (seeded box-union RGB-D scenes, BASELINE cfg2 shapes)",
-            "config": {"workload": "cfg2: single object with 32^3 prior, L16 F2 T19 max-res 1024, MLP "
-                                   f"W{arch.hidden_width} H{arch.hidden_layers}, {cfg.rays_per_iter} rays x "
-                                   f"{cfg.samples_per_ray} MLP samples (32 coarse grid lookups), 50 views 256^2, "
-                                   "Adam lr 1e-2, grid refresh every 50",
-                       "rays_per_step": cfg.rays_per_iter, "mlp_samples_per_ray": cfg.samples_per_ray,
-                       "coarse_samples": cfg.coarse_samples, "params": arch.param_count(),
-                       "mlp_precision": args.mlp, "objects_per_gpu": 1,
-                       "l2": "inputs larger than L2 (params+grad+Adam m,v = 256 MiB streamed every step); no flush"},
-            "per_gpu": round(per_gpu, 1),
-            "objects_steps_per_s": round(ws * args.steps / t_dev, 2),
+            "data": "synthetic (seeded box-union RGB-D scenes, BASELINE shapes)",
+            "config": dict({"workload": wl.desc, "mlp_precision": args.mlp, "parallelism": f"objects x{ws}"},
+                           **wl.extra),
+            "per_gpu": round(value / ws, 1),
+            "objects_steps_per_s": round(wl.n_objects_total * args.steps / t_dev, 2),
             "e2e": None if not e2e else {"value": round(e2e["samples"] / (e2e["ms"] / 1e3), 1), "unit": UNIT,
                                          "h2d_bytes_per_step": int(e2e["h2d"]), "d2h_bytes_per_step": e2e["d2h"],
                                          "steps": args.e2e_steps},
@@ -359,10 +540,11 @@ def run_ours(args):
             "kernels": kernels,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
-            "loss": {"first": loss_first, "last": loss_last},
+            "loss": getattr(wl, "loss", None),
         }
         print(json.dumps(line), flush=True)
-    obj.close()
+    for o in wl.objs:
+        o.close()
     ctx.close()
     if ws > 1:
         torch.distributed.destroy_process_group()
