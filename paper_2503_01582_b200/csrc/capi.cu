@@ -163,6 +163,8 @@ uint32_t philox_first(uint64_t seed, uint32_t tag, uint32_t step, uint32_t ray, 
 struct prenom_ctx_s {
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t side = nullptr;  // ray sampling of step t+1 overlaps Adam of step t
+  bool overlap = true;          // PRENOM_NO_OVERLAP=1 disables (A/B measurement)
   int64_t launches = 0;
   // optional per-kernel event timing
   bool prof = false;
@@ -184,17 +186,18 @@ namespace {
 struct ProfScope {
   prenom_ctx_s* c;
   int k;
+  cudaStream_t s;
   cudaEvent_t b = nullptr, e = nullptr;
-  ProfScope(prenom_ctx_s* ctx, int kind) : c(ctx), k(kind) {
+  ProfScope(prenom_ctx_s* ctx, int kind, cudaStream_t st = nullptr) : c(ctx), k(kind), s(st ? st : ctx->stream) {
     if (c->prof) {
       b = c->get_event();
       e = c->get_event();
-      cudaEventRecord(b, c->stream);
+      cudaEventRecord(b, s);
     }
   }
   ~ProfScope() {
     if (c->prof) {
-      cudaEventRecord(e, c->stream);
+      cudaEventRecord(e, s);
       c->ev_used.push_back({k, {b, e}});
     }
   }
@@ -236,9 +239,14 @@ struct prenom_object_s {
   DevBuf<int> kind, count;
   DevBuf<StepStatsDev> stats;
   int last_n_steps = 0;
+  // sample-ahead pipelining (k_sample(t+1) on ctx->side while k_adam(t) runs)
+  cudaEvent_t ev_bwd = nullptr, ev_sample = nullptr;
+  bool sample_ready = false;
   DevBuf<int> flag;
   ~prenom_object_s() {
     for (auto* f : frames) delete f;
+    if (ev_bwd) cudaEventDestroy(ev_bwd);
+    if (ev_sample) cudaEventDestroy(ev_sample);
   }
 };
 
@@ -333,20 +341,37 @@ SamplerCfg sampler_cfg(prenom_object_s* o, int B, int prior, uint32_t tag, uint3
   return c;
 }
 
-// One iteration of train_track's loop body (mapper.cpp:150-184).
-prenom_status enqueue_step(prenom_object_s* o, StepStatsDev* stats) {
+int frame_of_step(const prenom_object_s* o, int64_t step) {  // keyframe pick (mapper.cpp:151)
+  return (int)pdm_pick(philox_first(o->seed, PRENOM_TAG_FRAME, (uint32_t)step, 0, 0), (uint32_t)o->frames.size());
+}
+
+// generate_rays + sample_ray for `step` (render.cpp:47-102, density_grid.cpp:110-117)
+prenom_status enqueue_sample(prenom_object_s* o, int64_t step, cudaStream_t st) {
+  const RaySource src = frame_source(o, frame_of_step(o, step));
+  if (src.n_obj_px == 0) return fail(PRENOM_DATA, "generate_rays: no object pixels");
+  ProfScope ps(o->ctx, PRENOM_K_SAMPLE, st);
+  CUDA_TRY(launch_sample(src, sampler_cfg(o, o->cfg.rays_per_iter, o->cfg.prior_sampling, PRENOM_TAG_FINE,
+                                          (uint32_t)step), bufs(o), nullptr, st));
+  return PRENOM_OK;
+}
+
+// One iteration of train_track's loop body (mapper.cpp:150-184). With
+// has_next, the next step's ray sampling is issued on the side stream as
+// soon as this step's backward has consumed the sample buffers, so it runs
+// concurrently with this step's Adam (it only reads frames and the grid;
+// steps that refresh the grid keep the serial order).
+prenom_status enqueue_step(prenom_object_s* o, StepStatsDev* stats, bool has_next = false) {
   cudaStream_t st = o->ctx->stream;
   const prenom_train_cfg& c = o->cfg;
   const int B = c.rays_per_iter, S = c.samples_per_ray;
   const uint32_t step = (uint32_t)o->step;
-  // keyframe pick (mapper.cpp:151)
-  const int fi = (int)pdm_pick(philox_first(o->seed, PRENOM_TAG_FRAME, step, 0, 0), (uint32_t)o->frames.size());
-  const RaySource src = frame_source(o, fi);
-  if (src.n_obj_px == 0) return fail(PRENOM_DATA, "generate_rays: no object pixels");
+  const int fi = frame_of_step(o, o->step);
   const SampleBufs sb = bufs(o);
-  {
-    ProfScope ps(o->ctx, PRENOM_K_SAMPLE);
-    CUDA_TRY(launch_sample(src, sampler_cfg(o, B, c.prior_sampling, PRENOM_TAG_FINE, step), sb, nullptr, st));
+  if (o->sample_ready) {
+    CUDA_TRY(cudaStreamWaitEvent(st, o->ev_sample, 0));
+    o->sample_ready = false;
+  } else {
+    STATUS_TRY(enqueue_sample(o, o->step, st));
   }
   const bool tc = c.mlp_precision == PRENOM_MLP_BF16;
   {
@@ -394,6 +419,18 @@ prenom_status enqueue_step(prenom_object_s* o, StepStatsDev* stats) {
       ProfScope ps(o->ctx, PRENOM_K_ENCODE_BWD);
       CUDA_TRY(launch_encode_bwd(o->fd, o->params.p, o->grad.p, B, S, sb.count, sb.pos_depth, o->dfeat_t.p, st));
     }
+  }
+  const bool refresh_now = c.grid_refresh_every > 0 && (o->step + 1) % c.grid_refresh_every == 0;
+  if (has_next && !refresh_now && o->ctx->overlap) {
+    if (!o->ev_bwd) {
+      CUDA_TRY(cudaEventCreateWithFlags(&o->ev_bwd, cudaEventDisableTiming));
+      CUDA_TRY(cudaEventCreateWithFlags(&o->ev_sample, cudaEventDisableTiming));
+    }
+    CUDA_TRY(cudaEventRecord(o->ev_bwd, st));
+    CUDA_TRY(cudaStreamWaitEvent(o->ctx->side, o->ev_bwd, 0));
+    STATUS_TRY(enqueue_sample(o, o->step + 1, o->ctx->side));
+    CUDA_TRY(cudaEventRecord(o->ev_sample, o->ctx->side));
+    o->sample_ready = true;
   }
   // adam_step (field.cpp:295-310); grad zeroed in the same pass (mapper.cpp:175)
   const float stepf = (float)(o->step + 1);
@@ -504,6 +541,8 @@ prenom_status prenom_ctx_create(int device, prenom_ctx_t* out) {
   auto* c = new prenom_ctx_s;
   c->device = device;
   cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
+  c->overlap = getenv("PRENOM_NO_OVERLAP") == nullptr;
   if (e != cudaSuccess) {
     delete c;
     return fail(PRENOM_CUDA, cudaGetErrorString(e));
@@ -521,6 +560,8 @@ prenom_status prenom_ctx_destroy(prenom_ctx_t ctx) {
     cudaEventDestroy(u.second.first);
     cudaEventDestroy(u.second.second);
   }
+  cudaStreamSynchronize(ctx->side);
+  cudaStreamDestroy(ctx->side);
   cudaStreamDestroy(ctx->stream);
   delete ctx;
   return PRENOM_OK;
@@ -698,7 +739,7 @@ prenom_status prenom_train_step(prenom_object_t o, int n_steps, prenom_step_stat
   CUDA_TRY(o->stats.ensure((size_t)n_steps));
   cudaStream_t st = o->ctx->stream;
   CUDA_TRY(cudaMemsetAsync(o->stats.p, 0, sizeof(StepStatsDev) * n_steps, st));
-  for (int it = 0; it < n_steps; ++it) STATUS_TRY(enqueue_step(o, o->stats.p + it));
+  for (int it = 0; it < n_steps; ++it) STATUS_TRY(enqueue_step(o, o->stats.p + it, it + 1 < n_steps));
   o->last_n_steps = n_steps;
   if (stats) {
     std::vector<StepStatsDev> h(n_steps);
@@ -897,7 +938,7 @@ prenom_status prenom_train_step_many(prenom_object_t* objs, int n_objs, int n_st
     o->last_n_steps = n_steps;
   }
   for (int it = 0; it < n_steps; ++it)
-    for (int i = 0; i < n_objs; ++i) STATUS_TRY(enqueue_step(objs[i], objs[i]->stats.p + it));
+    for (int i = 0; i < n_objs; ++i) STATUS_TRY(enqueue_step(objs[i], objs[i]->stats.p + it, it + 1 < n_steps));
   return PRENOM_OK;
 }
 
