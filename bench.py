@@ -68,6 +68,12 @@ def dist_info():
     return ws, rank, local
 
 
+def launched_distributed() -> bool:
+    """True under torchrun (even with one rank): the process group, barriers,
+    max-over-ranks timing and NCCL all-reduces then run for real."""
+    return "TORCHELASTIC_RUN_ID" in os.environ or int(os.environ.get("WORLD_SIZE", "1")) > 1
+
+
 def make_workload(args, rank):
     from paper_2503_01582_b200 import TrainConfig, scenes
     from paper_2503_01582_b200._capi import MLP_BF16, MLP_FP32
@@ -315,6 +321,7 @@ class Cfg4(Workload):
         from paper_2503_01582_b200.meta import CudaEngine
 
         self.ws, self.rank = ws, rank
+        self.dist = launched_distributed()
         self.arch = scenes.cfg4_arch()
         self.cfg = TrainConfig(rays_per_iter=4096, samples_per_ray=64, prior_sampling=0, grid_refresh_every=0,
                                mlp_precision=MLP_BF16 if args.mlp == "bf16" else MLP_FP32)
@@ -348,7 +355,7 @@ class Cfg4(Workload):
             self.engine.adapt(t, self.q, derive_seed(0, self.k * self.ws + self.rank))
             st = self.workers[t].last_stats(self.q)
             self.n += sum(s["n_samples"] for s in st)
-            if self.ws == 1:
+            if not self.dist:
                 self.engine.update_exact(t, 0.1)
             else:
                 buf = self.engine.delta_sum([t])
@@ -375,7 +382,8 @@ def run_ours(args):
 
     ws, rank, local = dist_info()
     torch.cuda.set_device(local)
-    if ws > 1:
+    dist_on = launched_distributed()
+    if dist_on:
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -396,7 +404,7 @@ def run_ours(args):
     launches0 = ctx.launch_count()
     lib.prenom_ctx_profile(ctx.h, 1)
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if ws > 1:
+    if dist_on:
         torch.distributed.barrier()
     torch.cuda.synchronize()
     ctx.synchronize()
@@ -406,7 +414,7 @@ def run_ours(args):
         t_end.record(stream)
         ctx.synchronize()
         torch.cuda.synchronize()
-    if ws > 1:
+    if dist_on:
         torch.distributed.barrier()
     ms = t_start.elapsed_time(t_end)
     launches = ctx.launch_count() - launches0
@@ -428,7 +436,7 @@ def run_ours(args):
         e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e_samples = 0
         h2d = 0
-        if ws > 1:
+        if dist_on:
             torch.distributed.barrier()
         ctx.synchronize()
         e_start.record(stream)
@@ -447,7 +455,7 @@ def run_ours(args):
     # aggregate over ranks: max time, summed samples
     t_dev = ms / 1e3
     tot_samples = n_samples
-    if ws > 1:
+    if dist_on:
         import torch.distributed as dist
 
         t = torch.tensor([t_dev, e2e["ms"] / 1e3 if e2e else 0.0], device="cuda", dtype=torch.float64)
@@ -546,7 +554,7 @@ def run_ours(args):
     for o in wl.objs:
         o.close()
     ctx.close()
-    if ws > 1:
+    if dist_on:
         torch.distributed.destroy_process_group()
 
 
