@@ -359,7 +359,8 @@ class Cfg4(Workload):
                 self.engine.update_exact(t, 0.1)
             else:
                 buf = self.engine.delta_sum([t])
-                torch.distributed.all_reduce(buf)
+                with torch.cuda.stream(self.engine.stream):  # NCCL on the library stream
+                    torch.distributed.all_reduce(buf)
                 self.engine.apply(buf, self.ws, 0.1)
             self.k += 1
 

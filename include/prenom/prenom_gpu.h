@@ -248,7 +248,9 @@ prenom_status prenom_train_step_many(prenom_object_t* objs, int n_objs, int n_st
 
 /* ---- Reptile (meta.cpp:83-92) -------------------------------------------
  * delta_dev[i] = theta_adapted[i] - theta_meta[i] (device buffer of P floats,
- * e.g. a torch tensor to be all-reduced over NCCL by the caller).
+ * e.g. a torch tensor to be all-reduced over NCCL by the caller). Both calls
+ * are asynchronous and ordered on the meta object's context stream
+ * (prenom_ctx_stream): run the all-reduce on that stream, or synchronize.
  * prenom_reptile_apply: theta_meta <- keep*theta_meta + beta*(theta_meta + delta/n)
  * with keep = 1 - beta, i.e. reptile_update(meta, mean adapted, beta). */
 prenom_status prenom_reptile_delta(prenom_object_t meta, prenom_object_t adapted,

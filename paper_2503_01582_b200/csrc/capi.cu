@@ -946,11 +946,10 @@ prenom_status prenom_reptile_delta(prenom_object_t meta, prenom_object_t adapted
   if (!meta || !adapted || !delta_dev) return fail(PRENOM_USAGE, "NULL argument");
   if (meta->P != adapted->P) return fail(PRENOM_DATA, "reptile_update: parameter vectors differ in length");
   CUDA_TRY(cudaSetDevice(meta->ctx->device));
-  CUDA_TRY(cudaStreamSynchronize(adapted->ctx->stream));
+  if (adapted->ctx != meta->ctx) CUDA_TRY(cudaStreamSynchronize(adapted->ctx->stream));
   CUDA_TRY(launch_reptile_delta(meta->P, meta->params.p, adapted->params.p, delta_dev, meta->ctx->stream));
   meta->ctx->launches += 1;
-  CUDA_TRY(cudaStreamSynchronize(meta->ctx->stream));
-  return PRENOM_OK;
+  return PRENOM_OK;  // stream-ordered on the meta context's stream
 }
 
 prenom_status prenom_reptile_apply(prenom_object_t meta, const float* delta_dev, int n_tasks, float beta) {
@@ -959,8 +958,7 @@ prenom_status prenom_reptile_apply(prenom_object_t meta, const float* delta_dev,
   CUDA_TRY(cudaSetDevice(meta->ctx->device));
   CUDA_TRY(launch_reptile_apply(meta->P, meta->params.p, delta_dev, 1.f / (float)n_tasks, beta, meta->ctx->stream));
   meta->ctx->launches += 1;
-  CUDA_TRY(cudaStreamSynchronize(meta->ctx->stream));
-  return PRENOM_OK;
+  return PRENOM_OK;  // stream-ordered on the meta context's stream
 }
 
 prenom_status prenom_reptile_update(prenom_object_t meta, prenom_object_t adapted, float beta) {

@@ -93,21 +93,33 @@ def meta_train(engine: Engine, n_tasks: int, cfg: MetaConfig, world: int = 1, ra
             continue
         buf = engine.delta_sum(mine)
         if allreduce is not None:
-            allreduce(buf)
+            stream = getattr(engine, "stream", None)
+            if stream is not None:
+                import torch
+
+                with torch.cuda.stream(stream):
+                    allreduce(buf)
+            else:
+                allreduce(buf)
         engine.apply(buf, len(batch), cfg.beta)
 
 
 class CudaEngine(Engine):
     """Product engine: tasks are ObjectTrainers (views on the device), the
     meta parameters a frames-less ObjectTrainer; deltas are device buffers
-    (torch tensors) all-reduced with NCCL by the caller."""
+    (torch tensors). Every torch op -- and the caller's NCCL all-reduce, run
+    inside `with torch.cuda.stream(engine.stream)` -- is ordered on the
+    library's own stream, so a meta-step needs no host synchronization."""
 
     def __init__(self, meta, workers):
         import torch
 
         self.meta, self.workers = meta, workers
         self.P = meta.arch.param_count()
-        self.tmp = torch.empty(self.P, dtype=torch.float32, device=f"cuda:{meta.ctx.device}")
+        dev = f"cuda:{meta.ctx.device}"
+        self.stream = torch.cuda.ExternalStream(meta.ctx.stream, device=dev)
+        self.buf = torch.empty(self.P, dtype=torch.float32, device=dev)
+        self.tmp = torch.empty(self.P, dtype=torch.float32, device=dev)
 
     def adapt(self, task, q, seed):
         w = self.workers[task]
@@ -120,22 +132,20 @@ class CudaEngine(Engine):
 
         from .trainer import reptile_delta
 
-        acc = torch.zeros(self.P, dtype=torch.float32, device=self.tmp.device)
-        for t in tasks:
-            self.workers[t].ctx.synchronize()
-            reptile_delta(self.meta, self.workers[t], self.tmp.data_ptr())
-            acc += self.tmp
-        torch.cuda.synchronize(self.tmp.device)
-        return acc
+        with torch.cuda.stream(self.stream):
+            if len(tasks) == 1:
+                reptile_delta(self.meta, self.workers[tasks[0]], self.buf.data_ptr())
+            else:
+                self.buf.zero_()
+                for t in tasks:
+                    reptile_delta(self.meta, self.workers[t], self.tmp.data_ptr())
+                    self.buf += self.tmp
+        return self.buf
 
     def apply(self, delta_sum, n_tasks, beta):
-        import torch
-
         from .trainer import reptile_apply
 
-        torch.cuda.synchronize(delta_sum.device)
         reptile_apply(self.meta, delta_sum.data_ptr(), n_tasks, beta)
 
     def update_exact(self, task, beta):
-        self.workers[task].ctx.synchronize()
         self.meta.reptile_update(self.workers[task], beta)

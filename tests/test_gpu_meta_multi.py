@@ -72,6 +72,7 @@ def test_reptile_delta_apply_linearity(ctx, rng):
     tmp = torch.empty(P, device="cuda")
     for o in objs:
         T.reptile_delta(meta, o, tmp.data_ptr())
+        ctx.synchronize()  # stream-ordered on the library stream; torch reads it next
         acc += tmp
     torch.cuda.synchronize()
     T.reptile_apply(meta, acc.data_ptr(), 3, 0.1)
