@@ -358,7 +358,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
       const float px = clamp01(pp.x), py = clamp01(pp.y), pz = clamp01(pp.z);
       const unsigned long long ray_key = (unsigned long long)(gs / S) << 36;
       const float* drow = slot + r * SLD;
-      const int l_lo = lhalf ? (fd.L + 1) / 2 : 0, l_hi = lhalf ? fd.L : (fd.L + 1) / 2;
+      const int l_lo = lhalf ? (fd.L + 1) / 2 : 0, l_hi = skip_scatter == 2 ? l_lo : (lhalf ? fd.L : (fd.L + 1) / 2);
       for (int l = l_lo; l < l_hi; ++l) {  // warp-uniform
         const float2 dv = *reinterpret_cast<const float2*>(drow + 2 * l);
         const LevelCell cell = level_cell(fd.res[l], px, py, pz);
@@ -641,7 +641,7 @@ cudaError_t run_bwd(const FieldDesc& fd, const float* params, float* grad, long 
   if (e != cudaSuccess) return e;
   k_bwd_tc<INP, W, H><<<(unsigned)grid, kBwdThreads, smem, st>>>(fd, params, grad, n, S, count, pos,
                                                               reinterpret_cast<const uint4*>(feat_tiles), dout, tile_ctr,
-                                                              getenv("PRENOM_PROF_SKIP_SCATTER") ? 1 : 0);
+                                                              getenv("PRENOM_PROF_SKIP_SCATTER") ? atoi(getenv("PRENOM_PROF_SKIP_SCATTER")) : 0);
   return cudaGetLastError();
 }
 
