@@ -243,6 +243,52 @@ __global__ void __launch_bounds__(kThreads) k_fwd_tc(FieldDesc fd, const float* 
   if (warp == 0) umma::tmem_dealloc(tm, 64);
 }
 
+// One level of the table-gradient scatter for the 32 consecutive samples of a
+// warp (field.cpp:279-292). Samples of a ray are depth-sorted and a line
+// enters each cell once, so equal (ray, cell) keys form contiguous lane runs:
+// a segmented suffix sum leaves each run's total in its first lane, which
+// alone issues the 8 corner atomics (de-duplicated scatter).
+__device__ __forceinline__ void scatter_level(const FieldDesc& fd, float* __restrict__ grad, int l, bool valid,
+                                              float px, float py, float pz, unsigned long long ray_key, float dx,
+                                              float dy, int lane, int skip) {
+  const LevelCell cell = level_cell(fd.res[l], px, py, pz);
+  const unsigned long long key =
+      valid ? (ray_key | ((unsigned long long)(cell.cz & 4095) << 24) | ((unsigned long long)(cell.cy & 4095) << 12) |
+               (unsigned long long)(cell.cx & 4095))
+            : (~0ull - (unsigned long long)lane);
+  const float d0 = valid ? dx : 0.f, d1 = valid ? dy : 0.f;
+  float w[8], c[16];
+  corner_weights(cell, w);
+#pragma unroll
+  for (int corner = 0; corner < 8; ++corner) {
+    c[2 * corner] = w[corner] * d0;
+    c[2 * corner + 1] = w[corner] * d1;
+  }
+  // runs are contiguous: once no run is longer than `off`, no larger offset
+  // can match, so fine levels (runs of 1) skip all value shuffles
+  for (int off = 1; off < 32; off <<= 1) {
+    const unsigned long long ok = __shfl_down_sync(0xffffffffu, key, off);
+    const bool take = (lane + off < 32) && ok == key;
+    if (!__any_sync(0xffffffffu, take)) break;
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      const float tv = __shfl_down_sync(0xffffffffu, c[kk], off);
+      if (take) c[kk] += tv;
+    }
+  }
+  const unsigned long long pk = __shfl_up_sync(0xffffffffu, key, 1);
+  if (!skip && valid && (lane == 0 || pk != key)) {
+    float* gl = grad + (long long)l * 2 * fd.rows;
+    uint32_t rows[8];
+    corner_rows(fd, l, cell, rows);
+#pragma unroll
+    for (int corner = 0; corner < 8; ++corner) {
+      if (c[2 * corner] == 0.f && c[2 * corner + 1] == 0.f) continue;
+      atomicAdd(reinterpret_cast<float2*>(gl + (size_t)rows[corner] * 2), make_float2(c[2 * corner], c[2 * corner + 1]));
+    }
+  }
+}
+
 // ------------------------------------------------------------------ bwd
 // TMEM column map (fp32, M=128 lane layout everywhere; 256 columns per CTA so
 // two CTAs share an SM). Weight gradients are accumulated transposed,
@@ -265,6 +311,7 @@ struct BwdCols {
 // tile t+1.
 constexpr int kMlpThreads = 256;
 constexpr int kScatThreads = 256;  // two warps per 32-sample group: level halves
+constexpr int kBwdMlpLevels = 1;   // per half, scattered by the MLP warps (measured on cfg2)
 constexpr int kBwdThreads = kMlpThreads + kScatThreads;
 
 __device__ __forceinline__ void named_sync(int id, int n) {
@@ -292,10 +339,11 @@ template <int INP, int W, int H>
 __global__ void __launch_bounds__(kBwdThreads, 2)
     k_bwd_tc(FieldDesc fd, const float* __restrict__ params, float* __restrict__ grad, long long n_total, int S,
              const int* __restrict__ count, const float4* __restrict__ pos, const uint4* __restrict__ feat_tiles,
-             const float4* __restrict__ dout, int* tile_ctr, int skip_scatter) {
+             const float4* __restrict__ dout, int* tile_ctr, int skip_scatter, int mlp_levels) {
   using CM = BwdCols<INP, W, H>;
   constexpr int XC = INP + 8, HC = W + 8;
   constexpr int SLD = ScatterSlot<INP>::kLd;
+  constexpr int LH = INP / 4;  // levels per half (d_feature columns [h*INP/2, (h+1)*INP/2))
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ uint64_t bar, full_bar, empty_bar;
   __shared__ uint32_t tbase;
@@ -358,50 +406,13 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
       const float px = clamp01(pp.x), py = clamp01(pp.y), pz = clamp01(pp.z);
       const unsigned long long ray_key = (unsigned long long)(gs / S) << 36;
       const float* drow = slot + r * SLD;
-      const int l_lo = lhalf ? (fd.L + 1) / 2 : 0, l_hi = skip_scatter == 2 ? l_lo : (lhalf ? fd.L : (fd.L + 1) / 2);
+      // levels [lhalf*LH, (lhalf+1)*LH) belong to this half; the MLP warps
+      // scatter the first mlp_levels of them straight from registers
+      const int l_lo = lhalf * LH + mlp_levels;
+      const int l_hi = skip_scatter == 2 ? l_lo : min(fd.L, (lhalf + 1) * LH);
       for (int l = l_lo; l < l_hi; ++l) {  // warp-uniform
         const float2 dv = *reinterpret_cast<const float2*>(drow + 2 * l);
-        const LevelCell cell = level_cell(fd.res[l], px, py, pz);
-        // Samples of a ray are depth-sorted and a line enters each cell once, so
-        // equal (ray, cell) keys form contiguous lane runs: a segmented suffix
-        // sum leaves each run's total in its first lane, which alone issues the
-        // 8 corner atomics (field.cpp:279-292 scatter, de-duplicated).
-        const unsigned long long key =
-            valid ? (ray_key | ((unsigned long long)(cell.cz & 4095) << 24) |
-                     ((unsigned long long)(cell.cy & 4095) << 12) | (unsigned long long)(cell.cx & 4095))
-                  : (~0ull - (unsigned long long)lane);
-        const float d0 = valid ? dv.x : 0.f, d1 = valid ? dv.y : 0.f;
-        float c[16];
-#pragma unroll
-        for (int corner = 0; corner < 8; ++corner) {
-          const float w = corner_weight(cell, corner);
-          c[2 * corner] = w * d0;
-          c[2 * corner + 1] = w * d1;
-        }
-        // runs are contiguous: once no run is longer than `off`, no larger
-        // offset can match, so fine levels (runs of 1) skip all value shuffles
-        for (int off = 1; off < 32; off <<= 1) {
-          const unsigned long long ok = __shfl_down_sync(0xffffffffu, key, off);
-          const bool take = (lane + off < 32) && ok == key;
-          if (!__any_sync(0xffffffffu, take)) break;
-#pragma unroll
-          for (int kk = 0; kk < 16; ++kk) {
-            const float tv = __shfl_down_sync(0xffffffffu, c[kk], off);
-            if (take) c[kk] += tv;
-          }
-        }
-        const unsigned long long pk = __shfl_up_sync(0xffffffffu, key, 1);
-        if (!skip_scatter && valid && (lane == 0 || pk != key)) {
-          float* gl = grad + (long long)l * 2 * fd.rows;
-#pragma unroll
-          for (int corner = 0; corner < 8; ++corner) {
-            if (c[2 * corner] == 0.f && c[2 * corner + 1] == 0.f) continue;
-            const uint32_t rr = table_row(fd, l, (uint32_t)(cell.cx + (corner & 1)),
-                                          (uint32_t)(cell.cy + ((corner >> 1) & 1)),
-                                          (uint32_t)(cell.cz + ((corner >> 2) & 1)));
-            atomicAdd(reinterpret_cast<float2*>(gl + (size_t)rr * 2), make_float2(c[2 * corner], c[2 * corner + 1]));
-          }
-        }
+        scatter_level(fd, grad, l, valid, px, py, pz, ray_key, dv.x, dv.y, lane, skip_scatter);
       }
       named_sync(2, kScatThreads);  // every scatter thread is done with the slot
       if (tid == kMlpThreads) mbar_arrive(&empty_bar);
@@ -542,6 +553,19 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
         umma::fence_before_sync();
         named_sync(1, kMlpThreads);
         if (tid == 0) mbar_arrive(&full_bar);
+        // this half's first mlp_levels levels: scattered here, overlapping the
+        // scatter warps' share of the same tile
+        if (mlp_levels > 0 && skip_scatter != 2) {
+          float4 pp = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (valid) pp = pos[gs];
+          const float px = clamp01(pp.x), py = clamp01(pp.y), pz = clamp01(pp.z);
+          const unsigned long long ray_key = (unsigned long long)(gs / S) << 36;
+          const int l0 = half * LH;
+#pragma unroll
+          for (int j = 0; j < NH / 2; ++j)
+            if (j < mlp_levels && l0 + j < fd.L)  // warp-uniform
+              scatter_level(fd, grad, l0 + j, valid, px, py, pz, ray_key, v[2 * j], v[2 * j + 1], lane, skip_scatter);
+        }
       }
     }
     // sentinel: stop the scatter warps
@@ -637,11 +661,19 @@ cudaError_t run_bwd(const FieldDesc& fd, const float* params, float* grad, long 
   if (e != cudaSuccess) return e;
   const long long ntiles = (n + kTile - 1) / kTile;
   const long long grid = std::min<long long>(ntiles, 2LL * sms());
+  // levels per half the MLP warps scatter themselves (they would otherwise
+  // wait on the scatter warps); PRENOM_BWD_MLP_LEVELS overrides for tuning
+  static const int mlp_env = [] {
+    const char* v = getenv("PRENOM_BWD_MLP_LEVELS");
+    return v ? atoi(v) : -1;
+  }();
+  const int mlp_levels = std::max(0, std::min(INP / 4, mlp_env >= 0 ? mlp_env : kBwdMlpLevels));
   e = cudaMemsetAsync(tile_ctr, 0, sizeof(int), st);
   if (e != cudaSuccess) return e;
   k_bwd_tc<INP, W, H><<<(unsigned)grid, kBwdThreads, smem, st>>>(fd, params, grad, n, S, count, pos,
                                                               reinterpret_cast<const uint4*>(feat_tiles), dout, tile_ctr,
-                                                              getenv("PRENOM_PROF_SKIP_SCATTER") ? atoi(getenv("PRENOM_PROF_SKIP_SCATTER")) : 0);
+                                                              getenv("PRENOM_PROF_SKIP_SCATTER") ? atoi(getenv("PRENOM_PROF_SKIP_SCATTER")) : 0,
+                                                              mlp_levels);
   return cudaGetLastError();
 }
 

@@ -127,6 +127,35 @@ __device__ __forceinline__ LevelCell level_cell(int res, float px, float py, flo
   return c;
 }
 
+// The 8 corner rows of a level cell, factored: identical values to
+// table_row(fd, l, cx + (k & 1), cy + (k >> 1 & 1), cz + (k >> 2 & 1)) (the
+// dense index is affine mod 2^32; the hash XORs per-axis terms).
+__device__ __forceinline__ void corner_rows(const FieldDesc& fd, int l, const LevelCell& c, uint32_t rows[8]) {
+  const uint32_t V = fd.dense_verts[l];
+  const uint32_t x = (uint32_t)c.cx, y = (uint32_t)c.cy, z = (uint32_t)c.cz;
+  if (V) {
+    const uint32_t b = x + V * (y + V * z), VV = V * V;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) rows[k] = b + (k & 1 ? 1u : 0u) + (k & 2 ? V : 0u) + (k & 4 ? VV : 0u);
+  } else {
+    const uint32_t hy0 = y * kPrime1, hy1 = hy0 + kPrime1, hz0 = z * kPrime2, hz1 = hz0 + kPrime2;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      rows[k] = ((x + (k & 1 ? 1u : 0u)) ^ (k & 2 ? hy1 : hy0) ^ (k & 4 ? hz1 : hz0)) & fd.row_mask;
+  }
+}
+
+// All 8 trilinear weights, same product order as corner_weight.
+__device__ __forceinline__ void corner_weights(const LevelCell& c, float w[8]) {
+  const float wx[2] = {__fsub_rn(1.f, c.fx), c.fx}, wy[2] = {__fsub_rn(1.f, c.fy), c.fy},
+              wz[2] = {__fsub_rn(1.f, c.fz), c.fz};
+  float wxy[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) wxy[k] = __fmul_rn(wx[k & 1], wy[k >> 1]);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) w[k] = __fmul_rn(wxy[k & 3], wz[k >> 2]);
+}
+
 // Trilinear corner weight, same product order as field.cpp:88.
 __device__ __forceinline__ float corner_weight(const LevelCell& c, int corner) {
   const float wx = (corner & 1) ? c.fx : __fsub_rn(1.f, c.fx);

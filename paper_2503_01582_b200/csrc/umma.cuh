@@ -98,6 +98,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t phase) {
         : "memory");
   }
 }
+// Same, but the waiting warp is suspended in hardware (up to `ns`) instead of
+// re-polling: for waits that are long compared with the issue slots a spin
+// would take from co-resident warps.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* mbar, uint32_t phase, uint32_t ns = 1000000u) {
+  const uint32_t a = smem_u32(mbar);
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(done)
+        : "r"(a), "r"(phase), "r"(ns)
+        : "memory");
+  }
+}
 
 __device__ __forceinline__ void fence_before_sync() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
