@@ -30,6 +30,10 @@ namespace prenom {
 namespace {
 
 constexpr int kThreads = 256;
+// forward launch shape (measured on B200, cfg2): see run_fwd
+constexpr int kFwdThreadsDefault = 256;
+constexpr int kFwdCtasDefault = 3;
+constexpr int kFwdSmemKbDefault = 57;
 constexpr int kSlack = 0;       // weight tiles are never over-read
 // M=128 MN-major views of the (features|1) and (activations|1) tiles read
 // past the tile end (finite garbage rows that are never flushed)
@@ -61,20 +65,21 @@ struct WeightTiles {
     p += ((H * W + 4) * 4 + 15) / 16 * 16;
   }
 
-  __device__ void load(const FieldDesc& fd, const float* __restrict__ mlp) {
+  // threads [0, nt) cooperate
+  __device__ void load(const FieldDesc& fd, const float* __restrict__ mlp, int nt) {
     const int IN = fd.in_dim;
-    for (int i = threadIdx.x; i < W * INP; i += kThreads) {
+    for (int i = threadIdx.x; i < W * INP; i += nt) {
       const int o = i / INP, k = i % INP;
       const float v = k < IN ? __ldg(mlp + fd.w_off[0] + o * IN + k) : 0.f;
       *reinterpret_cast<__nv_bfloat16*>(w0 + umma::cm_offset(o, k, INP)) = __float2bfloat16_rn(v);
     }
     for (int l = 1; l < H; ++l)
-      for (int i = threadIdx.x; i < W * W; i += kThreads) {
+      for (int i = threadIdx.x; i < W * W; i += nt) {
         const int o = i / W, k = i % W;
         *reinterpret_cast<__nv_bfloat16*>(wl[l - 1] + umma::cm_offset(o, k, W)) =
             __float2bfloat16_rn(__ldg(mlp + fd.w_off[l] + o * W + k));
       }
-    for (int i = threadIdx.x; i < 16 * W + kSlack / 2; i += kThreads) {
+    for (int i = threadIdx.x; i < 16 * W + kSlack / 2; i += nt) {
       if (i < 16 * W) {
         const int o = i / W, k = i % W;
         const float v = o < 4 ? __ldg(mlp + fd.w_off[H] + o * W + k) : 0.f;
@@ -83,7 +88,7 @@ struct WeightTiles {
         reinterpret_cast<__nv_bfloat16*>(wo + 16 * W * 2)[i - 16 * W] = __float2bfloat16_rn(0.f);
       }
     }
-    for (int i = threadIdx.x; i < H * W + 4; i += kThreads) {
+    for (int i = threadIdx.x; i < H * W + 4; i += nt) {
       const int l = i / W;
       bias[i] = l < H ? __ldg(mlp + fd.b_off[l] + (i % W)) : __ldg(mlp + fd.b_off[H] + (i - H * W));
     }
@@ -113,12 +118,14 @@ __device__ __forceinline__ void wait_mma(uint64_t* bar, uint32_t& phase) {
 }
 
 // Epilogue: TMEM [128 x N] fp32 (cols c0..) -> +bias, ReLU -> bf16 tile [128][C].
-template <int N>
+// G column groups: warp w reads lane quadrant w%4, columns [(w/4)*N/G, ...).
+template <int N, int G = 2>
 __device__ __forceinline__ void epi_relu(uint32_t tm, int col0, const float* bias, unsigned char* tile, int C) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q = warp & 3, half = warp >> 2;
   const int row = 32 * q + lane;
-  constexpr int NH = N / 2;
+  constexpr int NH = N / G;
+  static_assert(NH % 8 == 0, "8-column TMEM loads");
 #pragma unroll
   for (int c = 0; c < NH; c += 8) {
     const int col = half * NH + c;
@@ -132,8 +139,10 @@ __device__ __forceinline__ void epi_relu(uint32_t tm, int col0, const float* bia
 }
 
 // ------------------------------------------------------------------ fwd
-template <int INP, int W, int H>
-__global__ void __launch_bounds__(kThreads) k_fwd_tc(FieldDesc fd, const float* __restrict__ params, long long n_total,
+// NT threads: NT/128 threads per sample share the levels in the encode and
+// the columns in the epilogues.
+template <int INP, int W, int H, int NT>
+__global__ void __launch_bounds__(NT) k_fwd_tc(FieldDesc fd, const float* __restrict__ params, long long n_total,
                                                      int S, const int* __restrict__ count,
                                                      const float4* __restrict__ pos, uint4* __restrict__ feat_tiles,
                                                      float4* __restrict__ out, int* flag, int* tile_ctr) {
@@ -149,8 +158,9 @@ __global__ void __launch_bounds__(kThreads) k_fwd_tc(FieldDesc fd, const float* 
   // l+1's epilogue overwrites the tile it read
   unsigned char* Hb = p;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  wt.load(fd, params + fd.hash_params);
-  for (int i = tid; i < 128 * INP; i += kThreads) reinterpret_cast<__nv_bfloat16*>(X)[i] = __float2bfloat16_rn(0.f);
+  wt.load(fd, params + fd.hash_params, NT);
+  constexpr int TPS = NT / 128;  // threads per sample
+  for (int i = tid; i < 128 * INP; i += NT) reinterpret_cast<__nv_bfloat16*>(X)[i] = __float2bfloat16_rn(0.f);
   // One 64-column TMEM region serves every layer: each MMA is issued only
   // after the previous epilogue drained it (sync_for_mma), so up to 8 CTAs fit.
   if (warp == 0) umma::tmem_alloc(&tbase, 64);
@@ -169,9 +179,9 @@ __global__ void __launch_bounds__(kThreads) k_fwd_tc(FieldDesc fd, const float* 
   __shared__ int s_tile;
   for (long long t = next_tile(tile_ctr, &s_tile); t < ntiles; t = next_tile(tile_ctr, &s_tile)) {
     const long long tile0 = t * kTile;
-    // ---- encode (fp32, bit-exact) -> bf16 X tile; 2 threads per sample
+    // ---- encode (fp32, bit-exact) -> bf16 X tile; TPS threads per sample
     {
-      const int s = tid & (kTile - 1), half = tid >> 7;
+      const int s = tid & (kTile - 1), part = tid >> 7;
       const long long gs = tile0 + s;
       bool valid = gs < n_total && __ldg(count + gs / S) > 0;
       float4 pp = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -179,7 +189,7 @@ __global__ void __launch_bounds__(kThreads) k_fwd_tc(FieldDesc fd, const float* 
       const float px = clamp01(pp.x), py = clamp01(pp.y), pz = clamp01(pp.z);
       // (batching two levels' gathers per thread measured slower: more distinct
       // lines in flight thrash L1, which serves the coarse levels)
-      for (int l = half; l < fd.L; l += 2) {
+      for (int l = part; l < fd.L; l += TPS) {
         float f[2] = {0.f, 0.f};
         if (valid) encode_level<2>(fd, params, l, px, py, pz, f);
         *reinterpret_cast<__nv_bfloat162*>(X + umma::cm_offset(s, 2 * l, INP)) = __floats2bfloat162_rn(f[0], f[1]);
@@ -195,10 +205,10 @@ __global__ void __launch_bounds__(kThreads) k_fwd_tc(FieldDesc fd, const float* 
     {
       const uint4* src = reinterpret_cast<const uint4*>(X);
       uint4* dst = feat_tiles + t * (128 * INP * 2 / 16);
-      for (int i = tid; i < 128 * INP * 2 / 16; i += kThreads) dst[i] = src[i];
+      for (int i = tid; i < 128 * INP * 2 / 16; i += NT) dst[i] = src[i];
     }
     wait_mma(&bar, phase);
-    epi_relu<W>(tm, 0, wt.bias, Hb, W);
+    epi_relu<W, TPS>(tm, 0, wt.bias, Hb, W);
     for (int l = 1; l < H; ++l) {
       sync_for_mma();
       if (tid == 0) {
@@ -208,7 +218,7 @@ __global__ void __launch_bounds__(kThreads) k_fwd_tc(FieldDesc fd, const float* 
         umma::commit(&bar);
       }
       wait_mma(&bar, phase);
-      epi_relu<W>(tm, 0, wt.bias + l * W, Hb, W);
+      epi_relu<W, TPS>(tm, 0, wt.bias + l * W, Hb, W);
     }
     sync_for_mma();
     if (tid == 0) {
@@ -366,7 +376,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
   unsigned char* zero_end = p;
   float* slot = reinterpret_cast<float*>(p);  // [128][SLD] d_features of one tile
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (tid < kMlpThreads) wt.load(fd, params + fd.hash_params);
+  if (tid < kMlpThreads) wt.load(fd, params + fd.hash_params, kMlpThreads);
   {
     uint4* z = reinterpret_cast<uint4*>(X);
     const int n16 = (int)((zero_end - X) / 16);
@@ -624,33 +634,44 @@ size_t bwd_smem() {
          H * (128 * (W + 8) * 2 + kSlackH) + 128 * 16 * 2 + 128 * W * 2 + ScatterSlot<INP>::kBytes + 1024;
 }
 
-template <int INP, int W, int H>
-cudaError_t run_fwd(const FieldDesc& fd, const float* params, long long n, int S, const int* count, const float4* pos,
-                    void* feat_tiles, float4* out, int* flag, int* tile_ctr, cudaStream_t st) {
-  // at most five CTAs (8 warps each; 5 x 64 TMEM columns) share an SM
-  // CTAs per SM trade gather latency hiding against L1 capacity (L1 = 228 KB -
-  // shared memory); PRENOM_FWD_CTAS overrides the default for tuning.
-  static const int ctas = [] {
-    const char* e = getenv("PRENOM_FWD_CTAS");
-    const int v = e ? atoi(e) : 3;
-    return v < 1 ? 1 : (v > 8 ? 8 : v);
-  }();
-  static const size_t min_smem = [] {
-    // measured on B200 (cfg2): 3 CTAs x 57 KB (24 warps/SM, ~57 KB L1 for the
-    // coarse-level gathers) beats both more warps with less L1 and fewer warps
-    const char* e = getenv("PRENOM_FWD_SMEM_KB");
-    return (size_t)(e ? atoi(e) : 57) * 1024;
-  }();
+template <int INP, int W, int H, int NT>
+cudaError_t run_fwd_nt(const FieldDesc& fd, const float* params, long long n, int S, const int* count,
+                       const float4* pos, void* feat_tiles, float4* out, int* flag, int* tile_ctr, int ctas,
+                       size_t min_smem, cudaStream_t st) {
   const size_t smem = std::max<size_t>(fwd_smem<INP, W, H>(), min_smem);
-  cudaError_t e = cudaFuncSetAttribute(k_fwd_tc<INP, W, H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(k_fwd_tc<INP, W, H, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const long long ntiles = (n + kTile - 1) / kTile;
   const long long grid = std::min<long long>(ntiles, (long long)ctas * sms());
   e = cudaMemsetAsync(tile_ctr, 0, sizeof(int), st);
   if (e != cudaSuccess) return e;
-  k_fwd_tc<INP, W, H><<<(unsigned)grid, kThreads, smem, st>>>(fd, params, n, S, count, pos,
-                                                              reinterpret_cast<uint4*>(feat_tiles), out, flag, tile_ctr);
+  k_fwd_tc<INP, W, H, NT><<<(unsigned)grid, NT, smem, st>>>(fd, params, n, S, count, pos,
+                                                            reinterpret_cast<uint4*>(feat_tiles), out, flag, tile_ctr);
   return cudaGetLastError();
+}
+
+template <int INP, int W, int H>
+cudaError_t run_fwd(const FieldDesc& fd, const float* params, long long n, int S, const int* count, const float4* pos,
+                    void* feat_tiles, float4* out, int* flag, int* tile_ctr, cudaStream_t st) {
+  // CTAs per SM x threads per CTA trade gather latency hiding against L1
+  // capacity (L1 = 228 KB - shared memory); PRENOM_FWD_{CTAS,SMEM_KB,THREADS}
+  // override the measured defaults for tuning.
+  static const int nt = [] {
+    const char* e = getenv("PRENOM_FWD_THREADS");
+    return e ? (atoi(e) == 512 ? 512 : 256) : kFwdThreadsDefault;
+  }();
+  static const int ctas = [] {
+    const char* e = getenv("PRENOM_FWD_CTAS");
+    const int v = e ? atoi(e) : kFwdCtasDefault;
+    return v < 1 ? 1 : (v > 8 ? 8 : v);
+  }();
+  static const size_t min_smem = [] {
+    const char* e = getenv("PRENOM_FWD_SMEM_KB");
+    return (size_t)(e ? atoi(e) : kFwdSmemKbDefault) * 1024;
+  }();
+  if (nt == 512)
+    return run_fwd_nt<INP, W, H, 512>(fd, params, n, S, count, pos, feat_tiles, out, flag, tile_ctr, ctas, min_smem, st);
+  return run_fwd_nt<INP, W, H, 256>(fd, params, n, S, count, pos, feat_tiles, out, flag, tile_ctr, ctas, min_smem, st);
 }
 
 template <int INP, int W, int H>

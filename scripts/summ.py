@@ -9,4 +9,4 @@ for line in sys.stdin:
         continue
     d = json.loads(line)
     ks = " ".join(f"{k}={v['ms_per_launch']:.4f}" for k, v in d.get("kernels", {}).items())
-    print(f"{tag} value={d['value']:.4g} ms/step={d['ms_per_step']} {ks}")
+    print(f"{tag} value={d['value']:.4g} ms/step={d['ms_per_step']} prof_pass={d.get('kernels_pass_ms_per_step')} {ks}")
