@@ -228,6 +228,17 @@ prenom_status prenom_render(prenom_object_t obj, int n_rays, const float* origin
  * result as the object's sampling grid (train_track's refresh). */
 prenom_status prenom_density_query(prenom_object_t obj, int R, float* out,
                                    int update_sampling_grid);
+/* Mesh extraction, train_track's tail (mapper.cpp:186-187) on the device:
+ * density query at R, iso = choose_iso(grid, iso_floor) = max(0.5 max, floor)
+ * (density_grid.cpp:134-136) when iso is NaN, then marching_cubes
+ * (marching_cubes.cpp:125-180) -- the reference's Mesh exactly: unit-cube
+ * vertices, triangles in cell order, vertices numbered by first use after
+ * cleanup_mesh (mesh.cpp:30-54). The mesh stays in the object; sizes are
+ * returned, prenom_get_mesh copies it out. */
+prenom_status prenom_extract_mesh(prenom_object_t obj, int R, float iso, float iso_floor, float* iso_used,
+                                  int64_t* n_vertices, int64_t* n_triangles);
+/* vertices [n_vertices][3] float, triangles [n_triangles][3] int32 (either may be NULL). */
+prenom_status prenom_get_mesh(prenom_object_t obj, float* vertices, int32_t* triangles);
 /* Batched noma::field_eval (field.cpp:219-225): n points in [0,1]^3. */
 prenom_status prenom_field_eval(prenom_object_t obj, int n, const float* xyz, float* sigma,
                                 float* rgb);
@@ -324,6 +335,17 @@ prenom_status prenom_debug_generate_rays(prenom_object_t obj, int frame, int64_t
  * N % 8 == 0 (16 for M=128), K % 16 == 0. */
 prenom_status prenom_debug_umma_gemm(prenom_ctx_t ctx, int M, int N, int K, int a_mn, int b_mn,
                                      const float* A, const float* B, float* D);
+
+/* marching_cubes (marching_cubes.cpp:125-180) of a caller grid (R^3 floats,
+ * x-fastest, host memory) on the device; the result is kept in the context
+ * until the next call and copied out by prenom_debug_mesh_get. */
+prenom_status prenom_debug_marching_cubes(prenom_ctx_t ctx, int R, const float* grid, float iso,
+                                          int64_t* n_vertices, int64_t* n_triangles);
+prenom_status prenom_debug_mesh_get(prenom_ctx_t ctx, float* vertices, int32_t* triangles);
+/* Host only: the cube-edge triangles of one of the 256 corner configurations
+ * (cube_case_triangles, marching_cubes.cpp:115-117) into edges[3 * count];
+ * returns count (<= 16), or -1 for a bad config. */
+int prenom_mc_case_triangles(int config, int* edges);
 
 #ifdef __cplusplus
 }

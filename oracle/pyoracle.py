@@ -404,6 +404,10 @@ class Ref(_Lib):
                                             C.c_uint32, C.c_int, f32p, f32p, i32p, f32p, f32p, i32p]),
             "ref_refresh_grid": (C.c_int, [rarch, f32p, C.c_int, f32p]),
             "ref_reptile_update": (C.c_int, [sz, f32p, f32p, C.c_float, f32p]),
+            "ref_marching_cubes": (C.c_int, [C.c_int, f32p, C.c_float, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+            "ref_mesh_get": (None, [f32p, i32p]),
+            "ref_cube_case_triangles": (C.c_int, [C.c_int, i32p]),
+            "ref_choose_iso": (C.c_float, [C.c_int, f32p, C.c_float]),
             "ref_train_object": (C.c_int, [rarch, f32p, C.c_int, f32p, C.c_int, rcam, f32p, f32p, u8p, C.c_uint8,
                                            f32p, f32p, f32p, f32p, C.POINTER(RefTrainCfg), C.c_uint32, C.c_int,
                                            f64p, f64p]),
@@ -576,6 +580,25 @@ class Ref(_Lib):
         out = zeros(R, R, R)
         self._check(self.lib.ref_refresh_grid(C.byref(self._a(arch)), fptr(f32(params)), R, fptr(out.reshape(-1))))
         return out
+
+    def marching_cubes(self, grid, iso):
+        """marching_cubes.cpp:125-180 on a [R][R][R] (z, y, x) grid: (vertices [V,3], triangles [T,3])."""
+        g = f32(grid)
+        nv, nt = C.c_int64(), C.c_int64()
+        self._check(self.lib.ref_marching_cubes(g.shape[0], fptr(g.reshape(-1)), iso, C.byref(nv), C.byref(nt)))
+        v = zeros(nv.value, 3)
+        t = np.zeros((nt.value, 3), np.int32)
+        self.lib.ref_mesh_get(fptr(v), iptr(t))
+        return v, t
+
+    def cube_case_triangles(self, config):
+        out = np.zeros(16 * 3, np.int32)
+        n = self.lib.ref_cube_case_triangles(config, iptr(out))
+        return out[:3 * n].reshape(-1, 3)
+
+    def choose_iso(self, grid, floor_value=5.0):
+        g = f32(grid)
+        return float(self.lib.ref_choose_iso(g.shape[0], fptr(g.reshape(-1)), floor_value))
 
     def reptile_update(self, meta, adapted, beta):
         meta, adapted = f32(meta), f32(adapted)

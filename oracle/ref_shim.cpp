@@ -27,6 +27,8 @@
 #include "noma/density_grid.hpp"
 #include "noma/errors.hpp"
 #include "noma/field.hpp"
+#include "noma/marching_cubes.hpp"
+#include "noma/mesh.hpp"
 #include "noma/meta.hpp"
 #include "noma/render.hpp"
 #include "noma/task.hpp"
@@ -480,6 +482,44 @@ int ref_refresh_grid(const RefArch* a, const float* params, int R, float* out) {
   std::memcpy(out, g.values.data(), g.values.size() * sizeof(float));
   return 0;
   REF_GUARD_END
+}
+
+// marching_cubes.cpp:125-180 (+ cleanup_mesh). The mesh is kept here until
+// ref_mesh_get copies it out (two-call pattern: sizes first).
+static thread_local Mesh g_ref_mesh;
+
+int ref_marching_cubes(int R, const float* vals, float iso, std::int64_t* nv, std::int64_t* nt) {
+  REF_GUARD_BEGIN
+  DensityGrid g(R);
+  std::memcpy(g.values.data(), vals, sizeof(float) * g.values.size());
+  g_ref_mesh = marching_cubes(g, iso);
+  *nv = (std::int64_t)g_ref_mesh.vertices.size();
+  *nt = (std::int64_t)g_ref_mesh.triangles.size();
+  return 0;
+  REF_GUARD_END
+}
+
+void ref_mesh_get(float* verts, int* tris) {
+  for (std::size_t i = 0; i < g_ref_mesh.vertices.size(); ++i) {
+    verts[3 * i] = g_ref_mesh.vertices[i].x;
+    verts[3 * i + 1] = g_ref_mesh.vertices[i].y;
+    verts[3 * i + 2] = g_ref_mesh.vertices[i].z;
+  }
+  for (std::size_t i = 0; i < g_ref_mesh.triangles.size(); ++i)
+    for (int k = 0; k < 3; ++k) tris[3 * i + k] = g_ref_mesh.triangles[i][k];
+}
+
+int ref_cube_case_triangles(int config, int* edges) {
+  const auto& t = cube_case_triangles(config);
+  for (std::size_t i = 0; i < t.size(); ++i)
+    for (int k = 0; k < 3; ++k) edges[3 * i + k] = t[i][k];
+  return (int)t.size();
+}
+
+float ref_choose_iso(int R, const float* vals, float floor_value) {
+  DensityGrid g(R);
+  std::memcpy(g.values.data(), vals, sizeof(float) * g.values.size());
+  return choose_iso(g, floor_value);
 }
 
 // meta.cpp:83-92.

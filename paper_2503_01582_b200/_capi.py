@@ -134,7 +134,7 @@ EXPORTED = [
     "prenom_object_create", "prenom_object_destroy", "prenom_object_set_frames",
     "prenom_object_upload_frame", "prenom_train_step", "prenom_object_last_stats",
     "prenom_object_step", "prenom_object_check",
-    "prenom_render", "prenom_density_query", "prenom_field_eval",
+    "prenom_render", "prenom_density_query", "prenom_extract_mesh", "prenom_get_mesh", "prenom_field_eval",
     "prenom_get_params", "prenom_set_params", "prenom_get_grid", "prenom_set_grid",
     "prenom_get_adam", "prenom_reset_adam", "prenom_train_step_many",
     "prenom_reptile_delta", "prenom_reptile_apply", "prenom_object_copy_params", "prenom_reptile_update",
@@ -142,6 +142,7 @@ EXPORTED = [
     "prenom_debug_philox", "prenom_debug_hash_encode", "prenom_debug_field_eval",
     "prenom_debug_field_backward", "prenom_debug_adam", "prenom_debug_sample_rays",
     "prenom_debug_batch_loss", "prenom_debug_generate_rays", "prenom_debug_umma_gemm",
+    "prenom_debug_marching_cubes", "prenom_debug_mesh_get", "prenom_mc_case_triangles",
 ]
 
 _lib = None
@@ -197,6 +198,8 @@ def _declare(lib):
         "prenom_object_check": (i32, [P]),
         "prenom_render": (i32, [P, i32, f32p, f32p, f32p, f32p]),
         "prenom_density_query": (i32, [P, i32, f32p, i32]),
+        "prenom_extract_mesh": (i32, [P, i32, C.c_float, C.c_float, f32p, i64p, i64p]),
+        "prenom_get_mesh": (i32, [P, f32p, i32p]),
         "prenom_field_eval": (i32, [P, i32, f32p, f32p, f32p]),
         "prenom_get_params": (i32, [P, f32p]),
         "prenom_set_params": (i32, [P, f32p]),
@@ -224,6 +227,9 @@ def _declare(lib):
                                           f32p, f32p]),
         "prenom_debug_generate_rays": (i32, [P, i32, i64, f32p, f32p, i32p, f32p, f32p, i32p]),
         "prenom_debug_umma_gemm": (i32, [P, i32, i32, i32, i32, i32, f32p, f32p, f32p]),
+        "prenom_debug_marching_cubes": (i32, [P, i32, f32p, C.c_float, i64p, i64p]),
+        "prenom_debug_mesh_get": (i32, [P, f32p, i32p]),
+        "prenom_mc_case_triangles": (i32, [i32, i32p]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(lib, name)

@@ -166,6 +166,7 @@ struct prenom_ctx_s {
   cudaStream_t side = nullptr;  // ray sampling of step t+1 overlaps Adam of step t
   bool overlap = true;          // PRENOM_NO_OVERLAP=1 disables (A/B measurement)
   int64_t launches = 0;
+  McMesh mc_dbg;  // prenom_debug_marching_cubes result
   // optional per-kernel event timing
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -243,6 +244,7 @@ struct prenom_object_s {
   cudaEvent_t ev_bwd = nullptr, ev_sample = nullptr;
   bool sample_ready = false;
   DevBuf<int> flag;
+  McMesh mesh;  // prenom_extract_mesh result (device)
   ~prenom_object_s() {
     for (auto* f : frames) delete f;
     if (ev_bwd) cudaEventDestroy(ev_bwd);
@@ -840,6 +842,90 @@ prenom_status prenom_density_query(prenom_object_t o, int R, float* out, int upd
     o->R = R;
   }
   return check_flag(o);
+}
+
+// train_track's tail (mapper.cpp:186-187): refresh_grid at R, choose_iso
+// (density_grid.cpp:134-136) unless iso is given, marching_cubes
+// (marching_cubes.cpp:125-180) -- all on the device; the mesh stays in the
+// object until prenom_get_mesh copies it out.
+prenom_status prenom_extract_mesh(prenom_object_t o, int R, float iso, float iso_floor, float* iso_used,
+                                  int64_t* n_vertices, int64_t* n_triangles) {
+  if (!o) return fail(PRENOM_USAGE, "NULL object");
+  if (R < 2 || R > 1024) return fail(PRENOM_DATA, "grid resolution out of range");
+  CUDA_TRY(cudaSetDevice(o->ctx->device));
+  cudaStream_t st = o->ctx->stream;
+  const size_t n = (size_t)R * R * R;
+  McMesh& m = o->mesh;
+  CUDA_TRY(m.grid.ensure(n));
+  CUDA_TRY(launch_refresh_grid(o->fd, o->params.p, R, m.grid.p, o->flag.p, st));
+  o->ctx->launches += 1;
+  STATUS_TRY(check_flag(o));
+  float level = iso;
+  if (std::isnan(iso)) {
+    CUDA_TRY(m.gmax.ensure(1));
+    CUDA_TRY(launch_grid_max(m.grid.p, (long long)n, m.gmax.p, st));
+    o->ctx->launches += 1;
+    float mx = 0.f;
+    CUDA_TRY(cudaMemcpyAsync(&mx, m.gmax.p, sizeof(float), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    level = std::fmax(0.5f * mx, iso_floor);
+  }
+  int launches = 0;
+  CUDA_TRY(run_marching_cubes(m.grid.p, R, level, m, st, &launches));
+  o->ctx->launches += launches;
+  if (iso_used) *iso_used = level;
+  if (n_vertices) *n_vertices = m.n_vertices;
+  if (n_triangles) *n_triangles = m.n_triangles;
+  return PRENOM_OK;
+}
+
+prenom_status prenom_get_mesh(prenom_object_t o, float* vertices, int32_t* triangles) {
+  if (!o) return fail(PRENOM_USAGE, "NULL object");
+  CUDA_TRY(cudaSetDevice(o->ctx->device));
+  cudaStream_t st = o->ctx->stream;
+  const McMesh& m = o->mesh;
+  if (vertices && m.n_vertices)
+    CUDA_TRY(cudaMemcpyAsync(vertices, m.verts.p, 3 * sizeof(float) * m.n_vertices, cudaMemcpyDeviceToHost, st));
+  if (triangles && m.n_triangles)
+    CUDA_TRY(cudaMemcpyAsync(triangles, m.tris.p, 3 * sizeof(int32_t) * m.n_triangles, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return PRENOM_OK;
+}
+
+prenom_status prenom_debug_marching_cubes(prenom_ctx_t c, int R, const float* grid, float iso, int64_t* n_vertices,
+                                          int64_t* n_triangles) {
+  if (!c || !grid) return fail(PRENOM_USAGE, "NULL argument");
+  if (R < 1 || R > 1024) return fail(PRENOM_DATA, "grid resolution out of range");
+  CUDA_TRY(cudaSetDevice(c->device));
+  McMesh& m = c->mc_dbg;
+  const size_t n = (size_t)R * R * R;
+  CUDA_TRY(m.grid.ensure(n));
+  CUDA_TRY(cudaMemcpyAsync(m.grid.p, grid, n * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+  int launches = 0;
+  CUDA_TRY(run_marching_cubes(m.grid.p, R, iso, m, c->stream, &launches));
+  c->launches += launches;
+  if (n_vertices) *n_vertices = m.n_vertices;
+  if (n_triangles) *n_triangles = m.n_triangles;
+  return PRENOM_OK;
+}
+
+prenom_status prenom_debug_mesh_get(prenom_ctx_t c, float* vertices, int32_t* triangles) {
+  if (!c) return fail(PRENOM_USAGE, "NULL context");
+  CUDA_TRY(cudaSetDevice(c->device));
+  const McMesh& m = c->mc_dbg;
+  if (vertices && m.n_vertices)
+    CUDA_TRY(cudaMemcpyAsync(vertices, m.verts.p, 3 * sizeof(float) * m.n_vertices, cudaMemcpyDeviceToHost,
+                             c->stream));
+  if (triangles && m.n_triangles)
+    CUDA_TRY(cudaMemcpyAsync(triangles, m.tris.p, 3 * sizeof(int32_t) * m.n_triangles, cudaMemcpyDeviceToHost,
+                             c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return PRENOM_OK;
+}
+
+int prenom_mc_case_triangles(int config, int* edges) {
+  if (!edges) return -1;
+  return mc_case_triangles(config, edges);
 }
 
 prenom_status prenom_field_eval(prenom_object_t o, int n, const float* xyz, float* sigma, float* rgb) {

@@ -330,6 +330,41 @@ cudaError_t launch_reptile_delta(size_t n, const float* meta, const float* adapt
 cudaError_t launch_reptile_apply(size_t n, float* meta, const float* delta, float inv_n,
                                  float beta, cudaStream_t st);
 cudaError_t launch_reptile_update(size_t n, float* meta, const float* adapted, float beta, cudaStream_t st);
+// ---- isosurface (mesh.cu)
+template <typename T>
+struct MeshBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  MeshBuf() = default;
+  MeshBuf(const MeshBuf&) = delete;
+  MeshBuf& operator=(const MeshBuf&) = delete;
+  ~MeshBuf() {
+    if (p) cudaFree(p);
+  }
+  cudaError_t ensure(size_t want) {
+    if (want <= n && p) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    cudaError_t e = cudaMalloc(&p, (want ? want : 1) * sizeof(T));
+    if (e == cudaSuccess) n = want ? want : 1;
+    return e;
+  }
+};
+// A mesh in the reference layout (mesh.hpp:12-17) on the device, plus the
+// extraction scratch (kept for re-use across calls on the same object).
+struct McMesh {
+  MeshBuf<float> verts;  // [n_vertices][3]
+  MeshBuf<int> tris;     // [n_triangles][3]
+  int64_t n_vertices = 0, n_triangles = 0;
+  MeshBuf<uint32_t> block, tmp, keep, keep_off, first_use, mark, vid, total;
+  MeshBuf<uint4> tri_keys, kept;
+  MeshBuf<float> grid, gmax;
+};
+int mc_case_triangles(int config, int* edges);  // host table (marching_cubes.cpp:24-107)
+cudaError_t launch_grid_max(const float* grid, long long n, float* d_out, cudaStream_t st);
+cudaError_t run_marching_cubes(const float* d_grid, int R, float iso, McMesh& m, cudaStream_t st, int* launches);
+
 // bf16 tensor-core MLP path (kernels_tc.cu)
 bool tc_supported(const FieldDesc& fd);
 size_t tc_feature_bytes(const FieldDesc& fd, long long n);

@@ -315,6 +315,18 @@ class ObjectTrainer:
         _check(self.lib.prenom_density_query(self.h, R, fptr(out.reshape(-1)), int(update_sampling_grid)))
         return out
 
+    def extract_mesh(self, R: int, iso: float | None = None, iso_floor: float = 5.0):
+        """train_track's tail on the device (mapper.cpp:186-187): density query at R,
+        choose_iso unless `iso` is given, marching_cubes. Returns (vertices [V,3] in the
+        unit cube, triangles [T,3] int32, iso used)."""
+        nv, nt, used = C.c_int64(), C.c_int64(), C.c_float()
+        _check(self.lib.prenom_extract_mesh(self.h, R, float("nan") if iso is None else iso, iso_floor,
+                                            C.byref(used), C.byref(nv), C.byref(nt)))
+        v = np.zeros((nv.value, 3), np.float32)
+        t = np.zeros((nt.value, 3), np.int32)
+        _check(self.lib.prenom_get_mesh(self.h, fptr(v), iptr(t)))
+        return v, t, used.value
+
     def field_eval(self, xyz):
         x = _f32(xyz).reshape(-1, 3)
         n = len(x)
@@ -478,3 +490,24 @@ def debug_umma_gemm(ctx: Context, A, B, a_mn: bool = False, b_mn: bool = False):
     D = np.zeros((M, N), np.float32)
     _check(ctx.lib.prenom_debug_umma_gemm(ctx.h, M, N, K, int(a_mn), int(b_mn), fptr(A), fptr(B), fptr(D)))
     return D
+
+
+def debug_marching_cubes(ctx: Context, grid, iso: float):
+    """marching_cubes (marching_cubes.cpp:125-180) of a host grid [R][R][R] (z, y, x) on the device."""
+    g = _f32(grid)
+    R = g.shape[0]
+    nv, nt = C.c_int64(), C.c_int64()
+    _check(ctx.lib.prenom_debug_marching_cubes(ctx.h, R, fptr(g.reshape(-1)), iso, C.byref(nv), C.byref(nt)))
+    v = np.zeros((nv.value, 3), np.float32)
+    t = np.zeros((nt.value, 3), np.int32)
+    _check(ctx.lib.prenom_debug_mesh_get(ctx.h, fptr(v), iptr(t)))
+    return v, t
+
+
+def mc_case_triangles(config: int):
+    """The host case table (cube_case_triangles, marching_cubes.cpp:115-117) as edge triples."""
+    out = np.zeros(16 * 3, np.int32)
+    n = _capi.load().prenom_mc_case_triangles(config, iptr(out))
+    if n < 0:
+        raise ValueError("config out of range")
+    return out[:3 * n].reshape(-1, 3)
