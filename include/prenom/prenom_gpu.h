@@ -40,6 +40,7 @@
  *   TAG_BG     c0=0 c1=ray   out[0..2]         -> background target colour
  *   TAG_RENDER c0=s/2 c1=ray (c2 = render call) -> fine draws for prenom_render
  *   TAG_INIT   c0=i/4 c1=0 c2=0                 -> device-side init_params draws
+ *   TAG_SYNTH  c0=pixel c1=view c2=0 out[0..1] -> depth noise (Box-Muller), out[2] -> missing depth
  * The CPU oracle (oracle/prenom_oracle.c) restates the reference math with
  * exactly these draws, which is what makes bit-exact sample parity possible.
  */
@@ -69,7 +70,8 @@ enum {
   PRENOM_TAG_FINE = 3,
   PRENOM_TAG_BG = 4,
   PRENOM_TAG_RENDER = 5,
-  PRENOM_TAG_INIT = 6
+  PRENOM_TAG_INIT = 6,
+  PRENOM_TAG_SYNTH = 7
 };
 
 enum { PRENOM_ACT_EXP_CLAMPED = 0, PRENOM_ACT_SOFTPLUS = 1 };
@@ -200,6 +202,23 @@ prenom_status prenom_object_set_frames(prenom_object_t obj, int n_frames,
  * copied on the context stream. Used by streaming callers (and bench e2e). */
 prenom_status prenom_object_upload_frame(prenom_object_t obj, int frame, const float* rgb,
                                          const float* depth, const uint8_t* mask);
+/* Synthetic RGB-D views rendered on the device straight into the object's
+ * frames (the device twin of scenes.box_union_scene; stands in for the
+ * reference's sdf_render.cpp at cfg5 scale): a union of n_boxes (<= 16)
+ * axis-aligned boxes in the scene frame, n views through cams (pixel rays as
+ * Camera::pixel_direction, render.hpp:20-22), depth = hit distance +
+ * N(0, depth_noise), missing (0) with probability missing_frac (TAG_SYNTH
+ * draws), mask instance 1. Band masks and pixel lists are built on the device. */
+typedef struct {
+  float lo[3], hi[3], albedo[3];
+} prenom_box;
+prenom_status prenom_object_synth_frames(prenom_object_t obj, int n, const prenom_camera* cams, int n_boxes,
+                                         const prenom_box* boxes, float depth_noise, float missing_frac,
+                                         uint64_t seed, const prenom_pose* obj_pose);
+/* Copy one frame back (any pointer may be NULL): rgb [H][W][3], depth [H][W],
+ * and the object / band pixel lists generate_rays draws from (render.cpp:57-66). */
+prenom_status prenom_object_get_frame(prenom_object_t obj, int frame, float* rgb, float* depth, int* n_obj_px,
+                                      int* n_bg_px, int* obj_px, int* bg_px);
 
 /* ---- train step --------------------------------------------------------
  * n_steps iterations of train_track's loop body (mapper.cpp:150-184):

@@ -15,7 +15,7 @@ PKG_DIR = Path(__file__).resolve().parent
 LIB_PATH = PKG_DIR / "_lib" / "libprenom_b200.so"
 
 PRENOM_OK, PRENOM_USAGE, PRENOM_DATA, PRENOM_NUMERIC, PRENOM_CUDA = range(5)
-TAG_FRAME, TAG_PIXEL, TAG_FINE, TAG_BG, TAG_RENDER, TAG_INIT = 1, 2, 3, 4, 5, 6
+TAG_FRAME, TAG_PIXEL, TAG_FINE, TAG_BG, TAG_RENDER, TAG_INIT, TAG_SYNTH = 1, 2, 3, 4, 5, 6, 7
 ACT_EXP_CLAMPED, ACT_SOFTPLUS = 0, 1
 MLP_FP32, MLP_BF16 = 0, 1
 KERNEL_CLASSES = ["sample", "field_fwd", "composite", "mlp_bwd", "encode_bwd", "adam", "refresh"]
@@ -34,6 +34,12 @@ class FieldArchC(C.Structure):
         ("hidden_layers", C.c_int32),
         ("density_activation", C.c_int32),
     ]
+
+
+class BoxC(C.Structure):
+    """prenom_box: an axis-aligned box of a synthetic scene with its albedo."""
+
+    _fields_ = [("lo", C.c_float * 3), ("hi", C.c_float * 3), ("albedo", C.c_float * 3)]
 
 
 class CameraC(C.Structure):
@@ -132,7 +138,7 @@ EXPORTED = [
     "prenom_ctx_create", "prenom_ctx_destroy", "prenom_ctx_stream", "prenom_ctx_synchronize",
     "prenom_ctx_launch_count", "prenom_ctx_profile", "prenom_ctx_kernel_times", "prenom_object_next_frame",
     "prenom_object_create", "prenom_object_destroy", "prenom_object_set_frames",
-    "prenom_object_upload_frame", "prenom_train_step", "prenom_object_last_stats",
+    "prenom_object_upload_frame", "prenom_object_synth_frames", "prenom_object_get_frame", "prenom_train_step", "prenom_object_last_stats",
     "prenom_object_step", "prenom_object_check",
     "prenom_render", "prenom_density_query", "prenom_extract_mesh", "prenom_get_mesh", "prenom_field_eval",
     "prenom_get_params", "prenom_set_params", "prenom_get_grid", "prenom_set_grid",
@@ -192,6 +198,9 @@ def _declare(lib):
         "prenom_object_set_frames": (i32, [P, i32, C.POINTER(CameraC), f32p, f32p, u8p,
                                            C.c_uint8, C.POINTER(PoseC)]),
         "prenom_object_upload_frame": (i32, [P, i32, f32p, f32p, u8p]),
+        "prenom_object_synth_frames": (i32, [P, i32, C.POINTER(CameraC), i32, C.POINTER(BoxC), C.c_float,
+                                             C.c_float, u64, C.POINTER(PoseC)]),
+        "prenom_object_get_frame": (i32, [P, i32, f32p, f32p, i32p, i32p, i32p, i32p]),
         "prenom_train_step": (i32, [P, i32, C.POINTER(StepStatsC)]),
         "prenom_object_last_stats": (i32, [P, i32, C.POINTER(StepStatsC)]),
         "prenom_object_step": (i32, [P, i64p]),

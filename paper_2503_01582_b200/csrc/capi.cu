@@ -116,35 +116,6 @@ size_t param_count_host(const prenom_field_arch& a) {
   return (size_t)d.hash_params + (size_t)d.mlp_params;
 }
 
-// render.cpp:17-45 (8-connected BFS = Chebyshev band), per frame at upload.
-void dilation_band(int W, int H, const uint8_t* mask, uint8_t value, int band_px, std::vector<uint8_t>& band) {
-  const size_t n = (size_t)W * H;
-  band.assign(n, 0);
-  std::vector<int> dist(n, -1);
-  std::deque<int> q;
-  for (size_t i = 0; i < n; ++i)
-    if (mask[i] == value) {
-      dist[i] = 0;
-      q.push_back((int)i);
-    }
-  while (!q.empty()) {
-    const int idx = q.front();
-    q.pop_front();
-    const int x = idx % W, y = idx / W, d = dist[idx];
-    if (d >= band_px) continue;
-    for (int dy = -1; dy <= 1; ++dy)
-      for (int dx = -1; dx <= 1; ++dx) {
-        const int nx = x + dx, ny = y + dy;
-        if (nx < 0 || ny < 0 || nx >= W || ny >= H) continue;
-        const size_t ni = (size_t)ny * W + nx;
-        if (dist[ni] >= 0) continue;
-        dist[ni] = d + 1;
-        band[ni] = 1;
-        q.push_back((int)ni);
-      }
-  }
-}
-
 void mat_vec(const float* M, const float* v, float* out) {
   out[0] = M[0] * v[0] + M[1] * v[1] + M[2] * v[2];
   out[1] = M[3] * v[0] + M[4] * v[1] + M[5] * v[2];
@@ -207,7 +178,7 @@ struct ProfScope {
 
 struct FrameDev {
   DevBuf<float> rgb, depth;
-  DevBuf<int> obj_px, bg_px;
+  MeshBuf<int> obj_px, bg_px;  // dilation_band / pixel lists, built on the device (kernels_data.cu)
   int n_obj_px = 0, n_bg_px = 0;
   prenom_camera cam;
   float origin[3];  // world_to_obj.apply(camera.t)
@@ -245,6 +216,7 @@ struct prenom_object_s {
   bool sample_ready = false;
   DevBuf<int> flag;
   McMesh mesh;  // prenom_extract_mesh result (device)
+  FrameScratch fscratch;  // band / pixel-list construction
   ~prenom_object_s() {
     for (auto* f : frames) delete f;
     if (ev_bwd) cudaEventDestroy(ev_bwd);
@@ -473,24 +445,38 @@ prenom_status set_frame_pixels(prenom_object_s* o, FrameDev* f, const float* rgb
   CUDA_TRY(cudaMemcpyAsync(f->rgb.p, rgb, npx * 3 * sizeof(float), cudaMemcpyHostToDevice, st));
   CUDA_TRY(cudaMemcpyAsync(f->depth.p, depth, npx * sizeof(float), cudaMemcpyHostToDevice, st));
   if (mask) {
-    std::vector<int> obj, bg;
-    std::vector<uint8_t> band;
-    dilation_band(o->W, o->H, mask, o->inst, o->cfg.band_px, band);
-    for (size_t i = 0; i < npx; ++i) {
-      if (mask[i] == o->inst) obj.push_back((int)i);
-      if (band[i]) bg.push_back((int)i);
-    }
-    f->n_obj_px = (int)obj.size();
-    f->n_bg_px = (int)bg.size();
-    CUDA_TRY(f->obj_px.ensure(obj.size()));
-    CUDA_TRY(f->bg_px.ensure(bg.size()));
-    if (!obj.empty())
-      CUDA_TRY(cudaMemcpyAsync(f->obj_px.p, obj.data(), obj.size() * sizeof(int), cudaMemcpyHostToDevice, st));
-    if (!bg.empty())
-      CUDA_TRY(cudaMemcpyAsync(f->bg_px.p, bg.data(), bg.size() * sizeof(int), cudaMemcpyHostToDevice, st));
-    CUDA_TRY(cudaStreamSynchronize(st));  // host vectors go out of scope
+    CUDA_TRY(o->fscratch.mask.ensure(npx));
+    CUDA_TRY(cudaMemcpyAsync(o->fscratch.mask.p, mask, npx, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(build_pixel_lists(o->fscratch.mask.p, o->W, o->H, o->inst, o->cfg.band_px, o->fscratch, f->obj_px,
+                               f->bg_px, &f->n_obj_px, &f->n_bg_px, st));
+    o->ctx->launches += 9;
   }
   return PRENOM_OK;
+}
+
+// Frame records (camera, object-frame ray origin) for n views; pixel data
+// is filled by set_frame_pixels or the device renderer.
+void init_frames(prenom_object_s* o, int n, const prenom_camera* cams, uint8_t inst, const prenom_pose* pose) {
+  for (auto* f : o->frames) delete f;
+  o->frames.clear();
+  o->W = cams[0].width;
+  o->H = cams[0].height;
+  o->inst = inst;
+  o->pose = *pose;
+  // Pose::inverse (geom.hpp:127-130)
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) o->Rt[i * 3 + j] = pose->R[j * 3 + i];
+  float tt[3];
+  mat_vec(o->Rt, pose->t, tt);
+  const float tinv[3] = {-tt[0], -tt[1], -tt[2]};
+  for (int i = 0; i < n; ++i) {
+    auto* f = new FrameDev;
+    o->frames.push_back(f);
+    f->cam = cams[i];
+    float wt[3];
+    mat_vec(o->Rt, cams[i].t, wt);
+    for (int k = 0; k < 3; ++k) f->origin[k] = wt[k] + tinv[k];
+  }
 }
 
 }  // namespace
@@ -699,28 +685,72 @@ prenom_status prenom_object_set_frames(prenom_object_t o, int n, const prenom_ca
     if (cams[i].width != W || cams[i].height != H)
       return fail(PRENOM_DATA, "generate_rays: mask does not match camera dimensions");
   CUDA_TRY(cudaSetDevice(o->ctx->device));
-  for (auto* f : o->frames) delete f;
-  o->frames.clear();
-  o->W = W;
-  o->H = H;
-  o->inst = inst;
-  o->pose = *pose;
-  // Pose::inverse (geom.hpp:127-130)
-  for (int i = 0; i < 3; ++i)
-    for (int j = 0; j < 3; ++j) o->Rt[i * 3 + j] = pose->R[j * 3 + i];
-  float tt[3];
-  mat_vec(o->Rt, pose->t, tt);
-  const float tinv[3] = {-tt[0], -tt[1], -tt[2]};
+  init_frames(o, n, cams, inst, pose);
   const size_t npx = (size_t)W * H;
+  for (int i = 0; i < n; ++i)
+    STATUS_TRY(set_frame_pixels(o, o->frames[i], rgb + 3 * npx * i, depth + npx * i, mask + npx * i));
+  return PRENOM_OK;
+}
+
+prenom_status prenom_object_synth_frames(prenom_object_t o, int n, const prenom_camera* cams, int n_boxes,
+                                         const prenom_box* boxes, float depth_noise, float missing_frac,
+                                         uint64_t seed, const prenom_pose* pose) {
+  if (!o || !cams || !boxes || !pose) return fail(PRENOM_USAGE, "NULL argument");
+  if (n < 1) return fail(PRENOM_DATA, "no frames");
+  if (n_boxes < 1 || n_boxes > kMaxSynthBoxes) return fail(PRENOM_USAGE, "n_boxes out of range [1, 16]");
+  if (depth_noise < 0.f || missing_frac < 0.f || missing_frac > 1.f) return fail(PRENOM_USAGE, "bad noise");
+  const int W = cams[0].width, H = cams[0].height;
+  if (W < 1 || H < 1) return fail(PRENOM_DATA, "bad frame size");
+  for (int i = 0; i < n; ++i)
+    if (cams[i].width != W || cams[i].height != H) return fail(PRENOM_DATA, "views differ in size");
+  CUDA_TRY(cudaSetDevice(o->ctx->device));
+  init_frames(o, n, cams, 1, pose);
+  cudaStream_t st = o->ctx->stream;
+  const size_t npx = (size_t)W * H;
+  SynthView v;
+  std::memset(&v, 0, sizeof v);
+  v.n_boxes = n_boxes;
+  for (int b = 0; b < n_boxes; ++b)
+    for (int a = 0; a < 3; ++a) {
+      v.boxes[b].lo[a] = boxes[b].lo[a];
+      v.boxes[b].hi[a] = boxes[b].hi[a];
+      v.boxes[b].albedo[a] = boxes[b].albedo[a];
+    }
+  v.depth_noise = depth_noise;
+  v.missing_frac = missing_frac;
+  v.seed = seed;
+  CUDA_TRY(o->fscratch.mask.ensure(npx));
   for (int i = 0; i < n; ++i) {
-    auto* f = new FrameDev;
-    o->frames.push_back(f);
-    f->cam = cams[i];
-    float wt[3];
-    mat_vec(o->Rt, cams[i].t, wt);
-    for (int k = 0; k < 3; ++k) f->origin[k] = wt[k] + tinv[k];
-    STATUS_TRY(set_frame_pixels(o, f, rgb + 3 * npx * i, depth + npx * i, mask + npx * i));
+    FrameDev* f = o->frames[i];
+    CUDA_TRY(f->rgb.ensure(npx * 3));
+    CUDA_TRY(f->depth.ensure(npx));
+    v.cam = cams[i];
+    v.view = i;
+    CUDA_TRY(launch_synth_view(v, f->rgb.p, f->depth.p, o->fscratch.mask.p, st));
+    CUDA_TRY(build_pixel_lists(o->fscratch.mask.p, W, H, 1, o->cfg.band_px, o->fscratch, f->obj_px, f->bg_px,
+                               &f->n_obj_px, &f->n_bg_px, st));
+    o->ctx->launches += 10;
   }
+  return PRENOM_OK;
+}
+
+prenom_status prenom_object_get_frame(prenom_object_t o, int frame, float* rgb, float* depth, int* n_obj_px,
+                                      int* n_bg_px, int* obj_px, int* bg_px) {
+  if (!o) return fail(PRENOM_USAGE, "NULL object");
+  if (frame < 0 || frame >= (int)o->frames.size()) return fail(PRENOM_USAGE, "frame index out of range");
+  CUDA_TRY(cudaSetDevice(o->ctx->device));
+  cudaStream_t st = o->ctx->stream;
+  const FrameDev* f = o->frames[frame];
+  const size_t npx = (size_t)o->W * o->H;
+  if (rgb) CUDA_TRY(cudaMemcpyAsync(rgb, f->rgb.p, 3 * sizeof(float) * npx, cudaMemcpyDeviceToHost, st));
+  if (depth) CUDA_TRY(cudaMemcpyAsync(depth, f->depth.p, sizeof(float) * npx, cudaMemcpyDeviceToHost, st));
+  if (obj_px && f->n_obj_px)
+    CUDA_TRY(cudaMemcpyAsync(obj_px, f->obj_px.p, sizeof(int) * f->n_obj_px, cudaMemcpyDeviceToHost, st));
+  if (bg_px && f->n_bg_px)
+    CUDA_TRY(cudaMemcpyAsync(bg_px, f->bg_px.p, sizeof(int) * f->n_bg_px, cudaMemcpyDeviceToHost, st));
+  if (n_obj_px) *n_obj_px = f->n_obj_px;
+  if (n_bg_px) *n_bg_px = f->n_bg_px;
+  CUDA_TRY(cudaStreamSynchronize(st));
   return PRENOM_OK;
 }
 

@@ -417,8 +417,10 @@ cudaError_t upload_tables(cudaStream_t st) {
   return e;
 }
 
+}  // namespace
+
 // exclusive scan of n u32 -> out; returns the total through a host read
-cudaError_t scan_u32(const uint32_t* in, long long n, uint32_t* out, MeshBuf<uint32_t>& tmp, uint32_t* d_total,
+cudaError_t scan_exclusive_u32(const uint32_t* in, long long n, uint32_t* out, MeshBuf<uint32_t>& tmp, uint32_t* d_total,
                      uint32_t* h_total, cudaStream_t st) {
   const long long nb = (n + kScanTile - 1) / kScanTile;
   cudaError_t e = tmp.ensure((size_t)std::max<long long>(nb, 1));
@@ -436,7 +438,6 @@ cudaError_t scan_u32(const uint32_t* in, long long n, uint32_t* out, MeshBuf<uin
   return e == cudaSuccess ? cudaGetLastError() : e;
 }
 
-}  // namespace
 
 int mc_case_triangles(int config, int* edges) {
   if (config < 0 || config > 255) return -1;
@@ -483,7 +484,7 @@ cudaError_t run_marching_cubes(const float* d_grid, int R, float iso, McMesh& m,
       (e = keep_off.ensure(ntri)) != cudaSuccess)
     return e;
   k_mc_emit<<<(unsigned)nb, kScanThreads, 0, st>>>(a, block.p, tris.p, keep.p);
-  if ((e = scan_u32(keep.p, ntri, keep_off.p, tmp, total.p, &nkept, st)) != cudaSuccess) return e;
+  if ((e = scan_exclusive_u32(keep.p, ntri, keep_off.p, tmp, total.p, &nkept, st)) != cudaSuccess) return e;
   *launches += 4;
   if (nkept == 0) return cudaSuccess;
   const size_t nkeys = (size_t)3 * R * R * R;
@@ -496,7 +497,7 @@ cudaError_t run_marching_cubes(const float* d_grid, int R, float iso, McMesh& m,
   const long long nslot = 3LL * nkept;
   const unsigned gs = (unsigned)std::min<long long>((nslot + 255) / 256, 148 * 16);
   k_mc_mark<<<gs, 256, 0, st>>>(kept.p, nslot, first_use.p, mark.p);
-  if ((e = scan_u32(mark.p, nslot, vid.p, tmp, total.p, &nvert, st)) != cudaSuccess) return e;
+  if ((e = scan_exclusive_u32(mark.p, nslot, vid.p, tmp, total.p, &nvert, st)) != cudaSuccess) return e;
   if ((e = m.verts.ensure(3 * (size_t)nvert)) != cudaSuccess || (e = m.tris.ensure(nslot)) != cudaSuccess) return e;
   k_mc_write<<<gs, 256, 0, st>>>(a, kept.p, nkept, first_use.p, mark.p, vid.p, m.verts.p, m.tris.p);
   *launches += 6;

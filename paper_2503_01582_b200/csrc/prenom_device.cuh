@@ -361,7 +361,32 @@ struct McMesh {
   MeshBuf<uint4> tri_keys, kept;
   MeshBuf<float> grid, gmax;
 };
+// ---- device-side data path (kernels_data.cu)
+struct SynthBox {
+  float lo[3], hi[3], albedo[3];
+};
+constexpr int kMaxSynthBoxes = 16;
+struct SynthView {
+  prenom_camera cam;  // camera -> world (scene frame)
+  int view;
+  int n_boxes;
+  SynthBox boxes[kMaxSynthBoxes];
+  float depth_noise, missing_frac;
+  uint64_t seed;
+};
+struct FrameScratch {
+  MeshBuf<uint8_t> mask, obj, rowdil;
+  MeshBuf<uint32_t> f_obj, f_bg, o_obj, o_bg, tmp, total;
+};
+cudaError_t launch_synth_view(const SynthView& v, float* rgb, float* depth, uint8_t* mask, cudaStream_t st);
+// dilation_band + object/band pixel lists (render.cpp:17-45, 57-66) of one
+// device mask; synchronizes st (list sizes are read back)
+cudaError_t build_pixel_lists(const uint8_t* d_mask, int W, int H, uint8_t inst, int band_px, FrameScratch& s,
+                              MeshBuf<int>& obj_px, MeshBuf<int>& bg_px, int* n_obj, int* n_bg, cudaStream_t st);
 int mc_case_triangles(int config, int* edges);  // host table (marching_cubes.cpp:24-107)
+// exclusive scan of n u32 into out; *h_total = sum (host read, synchronizes st)
+cudaError_t scan_exclusive_u32(const uint32_t* in, long long n, uint32_t* out, MeshBuf<uint32_t>& tmp,
+                               uint32_t* d_total, uint32_t* h_total, cudaStream_t st);
 cudaError_t launch_grid_max(const float* grid, long long n, float* d_out, cudaStream_t st);
 cudaError_t run_marching_cubes(const float* d_grid, int R, float iso, McMesh& m, cudaStream_t st, int* launches);
 

@@ -27,7 +27,7 @@ from dataclasses import dataclass, field, fields
 import numpy as np
 
 from . import _capi
-from ._capi import CameraC, FieldArchC, PoseC, StepStatsC, TrainCfgC, fptr, iptr, u8ptr, u32ptr
+from ._capi import BoxC, CameraC, FieldArchC, PoseC, StepStatsC, TrainCfgC, fptr, iptr, u8ptr, u32ptr
 
 
 # --------------------------------------------------------------- errors
@@ -277,6 +277,33 @@ class ObjectTrainer:
         _check(self.lib.prenom_object_set_frames(self.h, len(cams), arr, fptr(_f32(rgb)), fptr(_f32(depth)),
                                                  u8ptr(np.ascontiguousarray(mask, np.uint8)), instance_value,
                                                  C.byref(pose)))
+        self._frame_hw = (arr[0].height, arr[0].width)
+
+    def synth_frames(self, cams, boxes, depth_noise: float = 0.0, missing_frac: float = 0.0, seed: int = 0,
+                     obj_pose: Pose | None = None):
+        """Render a box-union scene's views on the device into this object's frames
+        (prenom_object_synth_frames). boxes: [(lo[3], hi[3], albedo[3])]."""
+        cc = (CameraC * len(cams))(*[c.to_c() for c in cams])
+        bb = (BoxC * len(boxes))()
+        for i, (lo, hi, alb) in enumerate(boxes):
+            bb[i].lo[:] = [float(x) for x in lo]
+            bb[i].hi[:] = [float(x) for x in hi]
+            bb[i].albedo[:] = [float(x) for x in alb]
+        pose = (obj_pose or Pose()).to_c()
+        _check(self.lib.prenom_object_synth_frames(self.h, len(cams), cc, len(boxes), bb, depth_noise, missing_frac,
+                                                   seed, C.byref(pose)))
+        self._frame_hw = (cams[0].height, cams[0].width)
+
+    def get_frame(self, frame: int):
+        """(rgb [H,W,3], depth [H,W], object pixel list, band pixel list) of one frame."""
+        H, W = self._frame_hw
+        rgb, dep = np.zeros((H, W, 3), np.float32), np.zeros((H, W), np.float32)
+        no, nb = C.c_int32(), C.c_int32()
+        _check(self.lib.prenom_object_get_frame(self.h, frame, None, None, C.byref(no), C.byref(nb), None, None))
+        op, bp = np.zeros(no.value, np.int32), np.zeros(nb.value, np.int32)
+        _check(self.lib.prenom_object_get_frame(self.h, frame, fptr(rgb), fptr(dep), C.byref(no), C.byref(nb),
+                                                iptr(op), iptr(bp)))
+        return rgb, dep, op, bp
 
     def upload_frame(self, frame: int, rgb, depth, mask):
         _check(self.lib.prenom_object_upload_frame(self.h, frame, fptr(rgb), fptr(depth), u8ptr(mask)))
