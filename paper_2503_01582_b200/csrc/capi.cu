@@ -131,11 +131,19 @@ uint32_t philox_first(uint64_t seed, uint32_t tag, uint32_t step, uint32_t ray, 
 
 }  // namespace
 
+constexpr int kDefaultLanes = 4;  // cfg3 on B200: 1 lane 1.00e9, 2: 1.15e9, 4: 1.235e9, 8: 1.21e9 samples/s
+constexpr int kMaxLanes = 16;
+
 struct prenom_ctx_s {
   int device = 0;
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;  // ray sampling of step t+1 overlaps Adam of step t
   bool overlap = true;          // PRENOM_NO_OVERLAP=1 disables (A/B measurement)
+  // multi-object scheduler: independent objects' steps run on these streams
+  // concurrently (prenom_train_step_many), forked from and joined back to `stream`
+  std::vector<cudaStream_t> lanes;
+  std::vector<cudaEvent_t> lane_ev;
+  cudaEvent_t fork_ev = nullptr;
   int64_t launches = 0;
   McMesh mc_dbg;  // prenom_debug_marching_cubes result
   // optional per-kernel event timing
@@ -214,6 +222,7 @@ struct prenom_object_s {
   // sample-ahead pipelining (k_sample(t+1) on ctx->side while k_adam(t) runs)
   cudaEvent_t ev_bwd = nullptr, ev_sample = nullptr;
   bool sample_ready = false;
+  cudaStream_t lane = nullptr;  // set while prenom_train_step_many runs this object on a lane stream
   DevBuf<int> flag;
   McMesh mesh;  // prenom_extract_mesh result (device)
   FrameScratch fscratch;  // band / pixel-list construction
@@ -335,7 +344,7 @@ prenom_status enqueue_sample(prenom_object_s* o, int64_t step, cudaStream_t st) 
 // concurrently with this step's Adam (it only reads frames and the grid;
 // steps that refresh the grid keep the serial order).
 prenom_status enqueue_step(prenom_object_s* o, StepStatsDev* stats, bool has_next = false) {
-  cudaStream_t st = o->ctx->stream;
+  cudaStream_t st = o->lane ? o->lane : o->ctx->stream;
   const prenom_train_cfg& c = o->cfg;
   const int B = c.rays_per_iter, S = c.samples_per_ray;
   const uint32_t step = (uint32_t)o->step;
@@ -349,7 +358,7 @@ prenom_status enqueue_step(prenom_object_s* o, StepStatsDev* stats, bool has_nex
   }
   const bool tc = c.mlp_precision == PRENOM_MLP_BF16;
   {
-    ProfScope ps(o->ctx, PRENOM_K_FIELD_FWD);
+    ProfScope ps(o->ctx, PRENOM_K_FIELD_FWD, st);
     if (tc)
       CUDA_TRY(launch_fwd_tc(o->fd, o->params.p, (long long)B * S, S, sb.count, sb.pos_depth, o->feat_tc.p, o->out.p,
                              o->flag.p, o->tile_ctr.p, st));
@@ -376,21 +385,21 @@ prenom_status enqueue_step(prenom_object_s* o, StepStatsDev* stats, bool has_nex
   ca.flag = o->flag.p;
   ca.frame = fi;
   {
-    ProfScope ps(o->ctx, PRENOM_K_COMPOSITE);
+    ProfScope ps(o->ctx, PRENOM_K_COMPOSITE, st);
     CUDA_TRY(launch_composite(ca, st));
   }
   if (tc) {
-    ProfScope ps(o->ctx, PRENOM_K_MLP_BWD);  // MLP backward + fused table-gradient scatter
+    ProfScope ps(o->ctx, PRENOM_K_MLP_BWD, st);  // MLP backward + fused table-gradient scatter
     CUDA_TRY(launch_bwd_tc(o->fd, o->params.p, o->grad.p, (long long)B * S, S, sb.count, sb.pos_depth,
                            o->feat_tc.p, o->dout.p, o->tile_ctr.p + 1, st));
   } else {
     {
-      ProfScope ps(o->ctx, PRENOM_K_MLP_BWD);
+      ProfScope ps(o->ctx, PRENOM_K_MLP_BWD, st);
       CUDA_TRY(launch_mlp_bwd_train(o->fd, o->params.p, o->grad.p, B, S, sb.count, o->feat_t.p, o->dout.p,
                                     o->dfeat_t.p, st));
     }
     {
-      ProfScope ps(o->ctx, PRENOM_K_ENCODE_BWD);
+      ProfScope ps(o->ctx, PRENOM_K_ENCODE_BWD, st);
       CUDA_TRY(launch_encode_bwd(o->fd, o->params.p, o->grad.p, B, S, sb.count, sb.pos_depth, o->dfeat_t.p, st));
     }
   }
@@ -411,7 +420,7 @@ prenom_status enqueue_step(prenom_object_s* o, StepStatsDev* stats, bool has_nex
   const float c1 = 1.f - std::pow(c.adam_beta1, stepf);
   const float c2 = 1.f - std::pow(c.adam_beta2, stepf);
   {
-    ProfScope ps(o->ctx, PRENOM_K_ADAM);
+    ProfScope ps(o->ctx, PRENOM_K_ADAM, st);
     CUDA_TRY(launch_adam(o->P, o->params.p, o->grad.p, o->m.p, o->v.p, c.eta, c.adam_beta1, c.adam_beta2,
                          c.adam_eps, c1, c2, 1, st));
   }
@@ -419,7 +428,7 @@ prenom_status enqueue_step(prenom_object_s* o, StepStatsDev* stats, bool has_nex
   o->step += 1;
   // grid refresh every m iterations (mapper.cpp:182-183)
   if (c.grid_refresh_every > 0 && o->step % c.grid_refresh_every == 0) {
-    ProfScope ps(o->ctx, PRENOM_K_REFRESH);
+    ProfScope ps(o->ctx, PRENOM_K_REFRESH, st);
     CUDA_TRY(launch_refresh_grid(o->fd, o->params.p, o->R, o->grid.p, o->flag.p, st));
     o->ctx->launches += 1;
   }
@@ -550,6 +559,12 @@ prenom_status prenom_ctx_destroy(prenom_ctx_t ctx) {
   }
   cudaStreamSynchronize(ctx->side);
   cudaStreamDestroy(ctx->side);
+  for (auto l : ctx->lanes) {
+    cudaStreamSynchronize(l);
+    cudaStreamDestroy(l);
+  }
+  for (auto e : ctx->lane_ev) cudaEventDestroy(e);
+  if (ctx->fork_ev) cudaEventDestroy(ctx->fork_ev);
   cudaStreamDestroy(ctx->stream);
   delete ctx;
   return PRENOM_OK;
@@ -1053,9 +1068,45 @@ prenom_status prenom_train_step_many(prenom_object_t* objs, int n_objs, int n_st
     CUDA_TRY(cudaMemsetAsync(o->stats.p, 0, sizeof(StepStatsDev) * n_steps, o->ctx->stream));
     o->last_n_steps = n_steps;
   }
-  for (int it = 0; it < n_steps; ++it)
-    for (int i = 0; i < n_objs; ++i) STATUS_TRY(enqueue_step(objs[i], objs[i]->stats.p + it, it + 1 < n_steps));
-  return PRENOM_OK;
+  // Multi-object scheduler: objects are independent (own θ, Adam, grid, rng;
+  // mapper.cpp:572-585), so their steps go round-robin onto K lane streams and
+  // the kernels of different objects overlap (filling each other's ramp and
+  // tail waves). The lanes fork from and join back to the context stream, so
+  // callers still see one ordered stream. PRENOM_LANES overrides K (1 = serial).
+  prenom_ctx_s* c = objs[0]->ctx;
+  static const int lanes_env = [] {
+    const char* v = getenv("PRENOM_LANES");
+    return v ? atoi(v) : kDefaultLanes;
+  }();
+  // per-kernel event timing (prenom_ctx_profile) needs serial kernels: one lane
+  const int K = c->prof ? 1 : std::max(1, std::min(n_objs, std::min(lanes_env, kMaxLanes)));
+  if (K == 1) {
+    for (int it = 0; it < n_steps; ++it)
+      for (int i = 0; i < n_objs; ++i) STATUS_TRY(enqueue_step(objs[i], objs[i]->stats.p + it, it + 1 < n_steps));
+    return PRENOM_OK;
+  }
+  while ((int)c->lanes.size() < K) {
+    cudaStream_t l;
+    cudaEvent_t e;
+    CUDA_TRY(cudaStreamCreateWithFlags(&l, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c->lanes.push_back(l);
+    c->lane_ev.push_back(e);
+  }
+  if (!c->fork_ev) CUDA_TRY(cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventRecord(c->fork_ev, c->stream));
+  for (int k = 0; k < K; ++k) CUDA_TRY(cudaStreamWaitEvent(c->lanes[k], c->fork_ev, 0));
+  for (int i = 0; i < n_objs; ++i) objs[i]->lane = c->lanes[i % K];
+  prenom_status st = PRENOM_OK;
+  for (int it = 0; it < n_steps && st == PRENOM_OK; ++it)
+    for (int i = 0; i < n_objs && st == PRENOM_OK; ++i)
+      st = enqueue_step(objs[i], objs[i]->stats.p + it, false);  // concurrency replaces the sample-ahead
+  for (int i = 0; i < n_objs; ++i) objs[i]->lane = nullptr;
+  for (int k = 0; k < K; ++k) {
+    CUDA_TRY(cudaEventRecord(c->lane_ev[k], c->lanes[k]));
+    CUDA_TRY(cudaStreamWaitEvent(c->stream, c->lane_ev[k], 0));
+  }
+  return st;
 }
 
 prenom_status prenom_reptile_delta(prenom_object_t meta, prenom_object_t adapted, float* delta_dev) {

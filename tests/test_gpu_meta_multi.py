@@ -43,7 +43,7 @@ def test_reptile_cuda_engine_matches_oracle_engine(ctx, oracle, tps):
 
 
 def test_train_many_equals_individual_training(ctx):
-    """prenom_train_step_many (objects back to back on one stream) == training each alone."""
+    """prenom_train_step_many (objects concurrently on lane streams) == training each alone."""
     ts = tasks()
     objs_a, objs_b = [], []
     for i, sc in enumerate(ts):
