@@ -49,7 +49,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg3", "cfg4"])
+    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg3", "cfg4", "cfg5"])
     ap.add_argument("--width", type=int, default=64)
     ap.add_argument("--mlp", default="bf16", choices=["fp32", "bf16"])
     ap.add_argument("--rays", type=int, default=8192)
@@ -255,13 +255,7 @@ class Cfg3(Workload):
         from paper_2503_01582_b200._capi import MLP_BF16, MLP_FP32
         from paper_2503_01582_b200.parallel import shard_lpt, step_cost
 
-        rng = np.random.default_rng(31)
-        cats = []
-        for _ in range(4):
-            L = int(rng.choice([8, 12, 16]))
-            cats.append(FieldArch(hash_levels=L, features_per_level=2, log2_table_size=int(rng.integers(14, 20)),
-                                  base_resolution=16, per_level_scale=FieldArch.scale_for(16, 1024, L),
-                                  hidden_width=int(rng.choice([32, 64])), hidden_layers=int(rng.choice([1, 2]))))
+        cats = mixed_category_archs()
         n_obj = 32
         archs = [cats[i % 4] for i in range(n_obj)]
         self.cfg = TrainConfig(rays_per_iter=2048, samples_per_ray=96, coarse_samples=32, prior_sampling=1,
@@ -373,7 +367,100 @@ class Cfg4(Workload):
         return [(self.arch, self.cfg, self.q)]
 
 
-WORKLOADS = {"cfg2": Cfg2, "cfg3": Cfg3, "cfg4": Cfg4}
+def mixed_category_archs(seed=31, n=4):
+    """The seeded GA-style category architectures of BASELINE configs 3 and 5."""
+    from paper_2503_01582_b200 import FieldArch
+
+    rng = np.random.default_rng(seed)
+    cats = []
+    for _ in range(n):
+        L = int(rng.choice([8, 12, 16]))
+        cats.append(FieldArch(hash_levels=L, features_per_level=2, log2_table_size=int(rng.integers(14, 20)),
+                              base_resolution=16, per_level_scale=FieldArch.scale_for(16, 1024, L),
+                              hidden_width=int(rng.choice([32, 64])), hidden_layers=int(rng.choice([1, 2]))))
+    return cats
+
+
+class Cfg5(Workload):
+    """BASELINE config 5 (scale): 256 objects of mixed architectures over 8 GPUs,
+    i.e. 32 objects per GPU (weak scaling: 32*N objects at N GPUs), each with 100
+    RGB-D views at 512^2 rendered on the device (depth noise 0.01, 5% missing
+    depth), a 128^3 occupancy prior for the prior-CDF sampler, and ~2^22 ray-samples
+    per GPU per step (32 objects x 1366 rays x 96 samples). After the timed steps
+    every object runs the 256^3 density query + marching cubes (mapper.cpp:186-187),
+    timed separately (`tail`)."""
+
+    name = "cfg5"
+
+    def __init__(self, args, ctx, rank, ws):
+        from paper_2503_01582_b200 import ObjectTrainer, TrainConfig, scenes
+        from paper_2503_01582_b200._capi import MLP_BF16, MLP_FP32
+
+        cats = mixed_category_archs()
+        per_gpu = 32
+        rays = (1 << 22) // (per_gpu * 96) + 1  # 1366: 32 x 1366 x 96 >= 2^22
+        self.cfg = TrainConfig(rays_per_iter=rays, samples_per_ray=96, coarse_samples=32, prior_sampling=1,
+                               grid_refresh_every=50, mlp_precision=MLP_BF16 if args.mlp == "bf16" else MLP_FP32)
+        self.mine = [rank * per_gpu + j for j in range(per_gpu)]  # objects are independent: block-sharded
+        self.objs, self.archs = [], []
+        res, views = 512, 100
+        cams = scenes.fibonacci_cameras(views, 1.5, res, res, float(res))
+        for i in self.mine:
+            rng = np.random.default_rng(90000 + i)
+            boxes = scenes.random_boxes(rng)
+            arch = cats[i % len(cats)]
+            o = ObjectTrainer.create(ctx, arch, theta=None, grid=scenes.occupancy_prior(boxes, R=128),
+                                     seed=7000 + i, cfg=self.cfg, box_min=np.full(3, -0.5, np.float32),
+                                     box_max=np.full(3, 0.5, np.float32))
+            o.synth_frames(cams, boxes, depth_noise=0.01, missing_frac=0.05, seed=13 + i)
+            self.objs.append(o)
+            self.archs.append(arch)
+        self.n_objects_total = per_gpu * ws
+        self.desc = ("cfg5: 256 mixed-arch objects over 8 GPUs = 32 objects/GPU (archs as cfg3), 100 RGB-D views "
+                     "512^2 per object rendered on the device (depth noise 0.01, 5% missing), 128^3 priors, "
+                     f"32 x {rays} rays x 96 samples (~2^22) per GPU per step; final 256^3 density query + mesh "
+                     "per object timed separately")
+        self.extra = {"objects_per_gpu": per_gpu, "objects_total": per_gpu * ws, "rays_per_object_step": rays,
+                      "samples_per_gpu_step": per_gpu * rays * 96,
+                      "frame_bytes_per_gpu": per_gpu * views * res * res * 16,
+                      "l2": "inputs larger than L2 (32 objects' params+Adam state, 13 GB of frames); no flush"}
+
+    def step(self, k):
+        from paper_2503_01582_b200.trainer import train_many
+
+        train_many(self.objs, k)
+
+    def samples(self, k):
+        n = 0
+        for o in self.objs:
+            n += sum(s["n_samples"] for s in o.last_stats(k))
+        self.loss = {}
+        return n
+
+    def work_items(self):
+        return [(a, self.cfg, 1) for a in self.archs]
+
+    def tail(self, ctx):
+        """256^3 density query + marching cubes per object (device-timed)."""
+        import torch
+
+        stream = torch.cuda.ExternalStream(ctx.stream)
+        ctx.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        tris = []
+        a.record(stream)
+        for o in self.objs:
+            tris.append(o.extract_mesh_counts(256))
+        b.record(stream)
+        ctx.synchronize()
+        ms = a.elapsed_time(b)
+        return {"what": "per object: 256^3 density query (refresh_grid) + choose_iso + marching cubes + cleanup",
+                "ms_total": round(ms, 2), "ms_per_object": round(ms / len(self.objs), 3),
+                "points_per_s": round(len(self.objs) * 256 ** 3 / (ms / 1e3), 1),
+                "triangles_mean": float(np.mean(tris))}
+
+
+WORKLOADS = {"cfg2": Cfg2, "cfg3": Cfg3, "cfg4": Cfg4, "cfg5": Cfg5}
 
 
 def run_ours(args):
@@ -531,6 +618,8 @@ def run_ours(args):
             "flops": tensor_flops, "achieved_tflops": round(tensor_flops / t_bwd / 1e12, 2),
             "frac_of_bf16_sustained": round(tensor_flops / t_bwd / 1e12 / pk["bf16_tflops_sustained"], 4)}
 
+    tail = wl.tail(ctx) if hasattr(wl, "tail") else None
+
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline and args.workload == "cfg2":
         try:
@@ -560,6 +649,8 @@ def run_ours(args):
             "clocks": clk.summary(),
             "loss": getattr(wl, "loss", None),
         }
+        if tail:
+            line["tail"] = tail
         print(json.dumps(line), flush=True)
     for o in wl.objs:
         o.close()

@@ -354,6 +354,14 @@ class ObjectTrainer:
         _check(self.lib.prenom_get_mesh(self.h, fptr(v), iptr(t)))
         return v, t, used.value
 
+    def extract_mesh_counts(self, R: int, iso: float | None = None, iso_floor: float = 5.0) -> int:
+        """extract_mesh without the host copy (the mesh stays on the device); returns
+        the triangle count."""
+        nv, nt, used = C.c_int64(), C.c_int64(), C.c_float()
+        _check(self.lib.prenom_extract_mesh(self.h, R, float("nan") if iso is None else iso, iso_floor,
+                                            C.byref(used), C.byref(nv), C.byref(nt)))
+        return nt.value
+
     def field_eval(self, xyz):
         x = _f32(xyz).reshape(-1, 3)
         n = len(x)
