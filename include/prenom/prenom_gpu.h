@@ -258,6 +258,10 @@ prenom_status prenom_extract_mesh(prenom_object_t obj, int R, float iso, float i
                                   int64_t* n_vertices, int64_t* n_triangles);
 /* vertices [n_vertices][3] float, triangles [n_triangles][3] int32 (either may be NULL). */
 prenom_status prenom_get_mesh(prenom_object_t obj, float* vertices, int32_t* triangles);
+/* The R^3 density lattice the last prenom_extract_mesh ran on (x-fastest), i.e.
+ * bake_prior's grid (density_grid.cpp:138-143: refresh_grid then marching_cubes
+ * of that grid). res receives R; grid may be NULL. */
+prenom_status prenom_get_mesh_grid(prenom_object_t obj, int* res, float* grid);
 /* Batched noma::field_eval (field.cpp:219-225): n points in [0,1]^3. */
 prenom_status prenom_field_eval(prenom_object_t obj, int n, const float* xyz, float* sigma,
                                 float* rgb);

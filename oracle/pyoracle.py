@@ -33,6 +33,10 @@ REF_DIR = Path("/root/reference/proj")
 
 f32p, f64p = C.POINTER(C.c_float), C.POINTER(C.c_double)
 i32p, i64p = C.POINTER(C.c_int32), C.POINTER(C.c_int64)
+
+
+def i64ptr(a):
+    return a.ctypes.data_as(i64p)
 u8p, u32p = C.POINTER(C.c_uint8), C.POINTER(C.c_uint32)
 archp = C.POINTER(FieldArchC)
 
@@ -408,6 +412,12 @@ class Ref(_Lib):
             "ref_mesh_get": (None, [f32p, i32p]),
             "ref_cube_case_triangles": (C.c_int, [C.c_int, i32p]),
             "ref_choose_iso": (C.c_float, [C.c_int, f32p, C.c_float]),
+            "ref_save_prior": (C.c_int, [C.c_char_p, C.c_char_p, rarch, f32p, C.c_int, f32p, C.c_int64, f32p,
+                                         C.c_int64, i32p, C.c_uint64, C.c_int, C.c_int, i32p, f32p]),
+            "ref_prior_summary": (C.c_int, [C.c_char_p, C.c_char_p, C.c_int]),
+            "ref_load_prior": (C.c_int, [C.c_char_p, rarch, i64p, f32p, f32p, f32p, i32p]),
+            "ref_bake_prior": (C.c_int, [rarch, f32p, C.c_int, C.c_float, f32p, C.POINTER(C.c_int64),
+                                         C.POINTER(C.c_int64)]),
             "ref_train_object": (C.c_int, [rarch, f32p, C.c_int, f32p, C.c_int, rcam, f32p, f32p, u8p, C.c_uint8,
                                            f32p, f32p, f32p, f32p, C.POINTER(RefTrainCfg), C.c_uint32, C.c_int,
                                            f64p, f64p]),
@@ -599,6 +609,50 @@ class Ref(_Lib):
     def choose_iso(self, grid, floor_value=5.0):
         g = f32(grid)
         return float(self.lib.ref_choose_iso(g.shape[0], fptr(g.reshape(-1)), floor_value))
+
+    # -- prior bundles (prior_bundle.cpp; bake_prior density_grid.cpp:138-143)
+    def save_prior(self, path, category, arch, theta, grid, vertices, triangles, search_seed=0, population=0,
+                   generations=0, genome_ints=(8, 14, 2, 32, 2, 60, 15, 0),
+                   genome_floats=(1e-2, 0.1, 1.45, 0.1, 1e-4)):
+        g = f32(grid)
+        v = f32(vertices).reshape(-1, 3)
+        t = np.ascontiguousarray(triangles, np.int32).reshape(-1, 3)
+        gi = np.asarray(genome_ints, np.int32)
+        gf = np.asarray(genome_floats, np.float32)
+        self._check(self.lib.ref_save_prior(str(path).encode(), category.encode(), C.byref(self._a(arch)),
+                                            fptr(f32(theta)), g.shape[0], fptr(g.reshape(-1)), len(v), fptr(v),
+                                            len(t), iptr(t), search_seed, population, generations, iptr(gi),
+                                            fptr(gf)))
+
+    def prior_summary(self, path):
+        """(status, text or error message): the reference's load_prior + prior_summary."""
+        buf = C.create_string_buffer(1 << 16)
+        st = self.lib.ref_prior_summary(str(path).encode(), buf, len(buf))
+        return st, (buf.value.decode() if st == 0 else self.lib.ref_last_error().decode())
+
+    def load_prior(self, path):
+        a = RefArch()
+        sz = np.zeros(4, np.int64)
+        self._check(self.lib.ref_load_prior(str(path).encode(), C.byref(a), i64ptr(sz), None, None, None, None))
+        P, R, nv, nt = (int(x) for x in sz)
+        th, g, v, t = zeros(P), zeros(R, R, R), zeros(nv, 3), np.zeros((nt, 3), np.int32)
+        self._check(self.lib.ref_load_prior(str(path).encode(), C.byref(a), i64ptr(sz), fptr(th),
+                                            fptr(g.reshape(-1)), fptr(v), iptr(t)))
+        arch = dict(hash_levels=a.hash_levels, features_per_level=a.features_per_level,
+                    log2_table_size=a.log2_table_size, base_resolution=a.base_resolution,
+                    per_level_scale=a.per_level_scale, hidden_width=a.hidden_width, hidden_layers=a.hidden_layers,
+                    density_activation=a.density_activation)
+        return arch, th, g, v, t
+
+    def bake_prior(self, arch, params, R, iso):
+        g = zeros(R, R, R)
+        nv, nt = C.c_int64(), C.c_int64()
+        self._check(self.lib.ref_bake_prior(C.byref(self._a(arch)), fptr(f32(params)), R, iso, fptr(g.reshape(-1)),
+                                            C.byref(nv), C.byref(nt)))
+        v = zeros(nv.value, 3)
+        t = np.zeros((nt.value, 3), np.int32)
+        self.lib.ref_mesh_get(fptr(v), iptr(t))
+        return g, v, t
 
     def reptile_update(self, meta, adapted, beta):
         meta, adapted = f32(meta), f32(adapted)

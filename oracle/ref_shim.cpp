@@ -17,6 +17,8 @@
 // and returns the drawn values, so the oracle can be fed identical draws.
 
 #include <chrono>
+#include <cstdio>
+#include <string>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -30,6 +32,8 @@
 #include "noma/marching_cubes.hpp"
 #include "noma/mesh.hpp"
 #include "noma/meta.hpp"
+#include "noma/prior_bundle.hpp"
+#include "noma/shapes.hpp"
 #include "noma/render.hpp"
 #include "noma/task.hpp"
 
@@ -520,6 +524,88 @@ float ref_choose_iso(int R, const float* vals, float floor_value) {
   DensityGrid g(R);
   std::memcpy(g.values.data(), vals, sizeof(float) * g.values.size());
   return choose_iso(g, floor_value);
+}
+
+// ---- prior bundles (prior_bundle.cpp:103-220; bake_prior density_grid.cpp:138-143)
+// Genome fields as two arrays: gi = {hash_levels, log2_table_size,
+// features_per_level, hidden_width, hidden_layers, meta_steps, inner_iters,
+// density_activation}, gf = {eta, beta, per_level_scale, lambda_d, lambda_sigma}.
+int ref_save_prior(const char* path, const char* category, const RefArch* a, const float* theta, int R,
+                   const float* grid, std::int64_t nv, const float* verts, std::int64_t nt, const int* tris,
+                   std::uint64_t search_seed, int population, int generations, const int* gi, const float* gf) {
+  REF_GUARD_BEGIN
+  PriorBundle b;
+  b.category = category_from_string(category);
+  b.arch = to_arch(a);
+  b.theta.assign(theta, theta + param_count(b.arch));
+  b.grid = DensityGrid(R);
+  std::memcpy(b.grid.values.data(), grid, sizeof(float) * b.grid.values.size());
+  b.mesh.vertices.resize((std::size_t)nv);
+  for (std::int64_t i = 0; i < nv; ++i) b.mesh.vertices[i] = {verts[3 * i], verts[3 * i + 1], verts[3 * i + 2]};
+  b.mesh.triangles.resize((std::size_t)nt);
+  for (std::int64_t i = 0; i < nt; ++i) b.mesh.triangles[i] = {tris[3 * i], tris[3 * i + 1], tris[3 * i + 2]};
+  b.provenance.search_seed = search_seed;
+  b.provenance.population = population;
+  b.provenance.generations = generations;
+  Genome& g = b.provenance.genome;
+  g.hash_levels = gi[0], g.log2_table_size = gi[1], g.features_per_level = gi[2], g.hidden_width = gi[3];
+  g.hidden_layers = gi[4], g.meta_steps = gi[5], g.inner_iters = gi[6];
+  g.density_activation = gi[7] ? DensityActivation::kSoftplus : DensityActivation::kExpClamped;
+  g.eta = gf[0], g.beta = gf[1], g.per_level_scale = gf[2], g.lambda_d = gf[3], g.lambda_sigma = gf[4];
+  save_prior(b, path);
+  return 0;
+  REF_GUARD_END
+}
+
+// load_prior then prior_summary text (0 = ok; else the error class, message
+// in ref_last_error). out receives the summary (truncated to cap).
+int ref_prior_summary(const char* path, char* out, int cap) {
+  REF_GUARD_BEGIN
+  const std::string s = prior_summary(path);
+  std::snprintf(out, (std::size_t)cap, "%s", s.c_str());
+  return 0;
+  REF_GUARD_END
+}
+
+// load_prior: sizes first (theta count, R, nv, nt), arrays when the pointers are non-NULL.
+int ref_load_prior(const char* path, RefArch* a, std::int64_t* sizes, float* theta, float* grid, float* verts,
+                   int* tris) {
+  REF_GUARD_BEGIN
+  const PriorBundle b = load_prior(path);
+  a->hash_levels = b.arch.hash_levels, a->features_per_level = b.arch.features_per_level;
+  a->log2_table_size = b.arch.log2_table_size, a->base_resolution = b.arch.base_resolution;
+  a->per_level_scale = b.arch.per_level_scale, a->hidden_width = b.arch.hidden_width;
+  a->hidden_layers = b.arch.hidden_layers;
+  a->density_activation = b.arch.density_activation == DensityActivation::kSoftplus ? 1 : 0;
+  sizes[0] = (std::int64_t)b.theta.size(), sizes[1] = b.grid.resolution;
+  sizes[2] = (std::int64_t)b.mesh.vertices.size(), sizes[3] = (std::int64_t)b.mesh.triangles.size();
+  if (theta) std::memcpy(theta, b.theta.data(), b.theta.size() * sizeof(float));
+  if (grid) std::memcpy(grid, b.grid.values.data(), b.grid.values.size() * sizeof(float));
+  if (verts)
+    for (std::size_t i = 0; i < b.mesh.vertices.size(); ++i) {
+      verts[3 * i] = b.mesh.vertices[i].x, verts[3 * i + 1] = b.mesh.vertices[i].y;
+      verts[3 * i + 2] = b.mesh.vertices[i].z;
+    }
+  if (tris)
+    for (std::size_t i = 0; i < b.mesh.triangles.size(); ++i)
+      for (int k = 0; k < 3; ++k) tris[3 * i + k] = b.mesh.triangles[i][k];
+  return 0;
+  REF_GUARD_END
+}
+
+// bake_prior (density_grid.cpp:138-143): grid -> out_grid, mesh kept for ref_mesh_get.
+int ref_bake_prior(const RefArch* a, const float* params, int R, float iso, float* out_grid, std::int64_t* nv,
+                   std::int64_t* nt) {
+  REF_GUARD_BEGIN
+  const FieldArch arch = to_arch(a);
+  const ParamVector p(params, params + param_count(arch));
+  BakedPrior baked = bake_prior(arch, p, R, iso);
+  std::memcpy(out_grid, baked.grid.values.data(), baked.grid.values.size() * sizeof(float));
+  g_ref_mesh = std::move(baked.mesh);
+  *nv = (std::int64_t)g_ref_mesh.vertices.size();
+  *nt = (std::int64_t)g_ref_mesh.triangles.size();
+  return 0;
+  REF_GUARD_END
 }
 
 // meta.cpp:83-92.

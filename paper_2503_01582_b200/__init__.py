@@ -13,6 +13,7 @@ from .trainer import (  # noqa: F401
     NumericError,
     ObjectTrainer,
     Pose,
+    PrenomError,
     TrainConfig,
     UsageError,
     derive_seed,

@@ -140,7 +140,7 @@ EXPORTED = [
     "prenom_object_create", "prenom_object_destroy", "prenom_object_set_frames",
     "prenom_object_upload_frame", "prenom_object_synth_frames", "prenom_object_get_frame", "prenom_train_step", "prenom_object_last_stats",
     "prenom_object_step", "prenom_object_check",
-    "prenom_render", "prenom_density_query", "prenom_extract_mesh", "prenom_get_mesh", "prenom_field_eval",
+    "prenom_render", "prenom_density_query", "prenom_extract_mesh", "prenom_get_mesh", "prenom_get_mesh_grid", "prenom_field_eval",
     "prenom_get_params", "prenom_set_params", "prenom_get_grid", "prenom_set_grid",
     "prenom_get_adam", "prenom_reset_adam", "prenom_train_step_many",
     "prenom_reptile_delta", "prenom_reptile_apply", "prenom_object_copy_params", "prenom_reptile_update",
@@ -209,6 +209,7 @@ def _declare(lib):
         "prenom_density_query": (i32, [P, i32, f32p, i32]),
         "prenom_extract_mesh": (i32, [P, i32, C.c_float, C.c_float, f32p, i64p, i64p]),
         "prenom_get_mesh": (i32, [P, f32p, i32p]),
+        "prenom_get_mesh_grid": (i32, [P, i32p, f32p]),
         "prenom_field_eval": (i32, [P, i32, f32p, f32p, f32p]),
         "prenom_get_params": (i32, [P, f32p]),
         "prenom_set_params": (i32, [P, f32p]),

@@ -916,11 +916,25 @@ prenom_status prenom_extract_mesh(prenom_object_t o, int R, float iso, float iso
     level = std::fmax(0.5f * mx, iso_floor);
   }
   int launches = 0;
+  m.R = R;
   CUDA_TRY(run_marching_cubes(m.grid.p, R, level, m, st, &launches));
   o->ctx->launches += launches;
   if (iso_used) *iso_used = level;
   if (n_vertices) *n_vertices = m.n_vertices;
   if (n_triangles) *n_triangles = m.n_triangles;
+  return PRENOM_OK;
+}
+
+prenom_status prenom_get_mesh_grid(prenom_object_t o, int* res, float* grid) {
+  if (!o || !res) return fail(PRENOM_USAGE, "NULL argument");
+  if (o->mesh.R < 2) return fail(PRENOM_USAGE, "prenom_get_mesh_grid: no mesh extracted yet");
+  CUDA_TRY(cudaSetDevice(o->ctx->device));
+  *res = o->mesh.R;
+  if (grid) {
+    const size_t n = (size_t)o->mesh.R * o->mesh.R * o->mesh.R;
+    CUDA_TRY(cudaMemcpyAsync(grid, o->mesh.grid.p, n * sizeof(float), cudaMemcpyDeviceToHost, o->ctx->stream));
+    CUDA_TRY(cudaStreamSynchronize(o->ctx->stream));
+  }
   return PRENOM_OK;
 }
 

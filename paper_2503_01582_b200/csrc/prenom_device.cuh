@@ -357,6 +357,7 @@ struct McMesh {
   MeshBuf<float> verts;  // [n_vertices][3]
   MeshBuf<int> tris;     // [n_triangles][3]
   int64_t n_vertices = 0, n_triangles = 0;
+  int R = 0;  // lattice resolution of `grid` (prenom_extract_mesh)
   MeshBuf<uint32_t> block, tmp, keep, keep_off, first_use, mark, vid, total;
   MeshBuf<uint4> tri_keys, kept;
   MeshBuf<float> grid, gmax;

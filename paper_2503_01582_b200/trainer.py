@@ -258,6 +258,14 @@ class ObjectTrainer:
                                             C.byref(c), fptr(_f32(box_min)), fptr(_f32(box_max)), C.byref(h)))
         return cls(ctx, h, arch, cfg, grid_res)
 
+    @classmethod
+    def from_prior(cls, ctx: Context, prior, seed: int = 0, cfg: TrainConfig | None = None,
+                   box_min=(-0.5, -0.5, -0.5), box_max=(0.5, 0.5, 0.5)) -> "ObjectTrainer":
+        """Create from a category prior (a prior.PriorBundle, e.g. from load_prior):
+        arch, θ and the density grid come from the bundle (mapper.cpp:133-137)."""
+        return cls.create(ctx, prior.arch, theta=prior.theta, grid=prior.grid, seed=seed, cfg=cfg,
+                          box_min=box_min, box_max=box_max)
+
     def close(self):
         if getattr(self, "h", None):
             self.lib.prenom_object_destroy(self.h)
@@ -353,6 +361,14 @@ class ObjectTrainer:
         t = np.zeros((nt.value, 3), np.int32)
         _check(self.lib.prenom_get_mesh(self.h, fptr(v), iptr(t)))
         return v, t, used.value
+
+    def get_mesh_grid(self):
+        """The R^3 σ lattice the last extract_mesh ran on (bake_prior's grid)."""
+        R = C.c_int32()
+        _check(self.lib.prenom_get_mesh_grid(self.h, C.byref(R), None))
+        g = np.zeros((R.value,) * 3, np.float32)
+        _check(self.lib.prenom_get_mesh_grid(self.h, C.byref(R), fptr(g.reshape(-1))))
+        return g
 
     def extract_mesh_counts(self, R: int, iso: float | None = None, iso_floor: float = 5.0) -> int:
         """extract_mesh without the host copy (the mesh stays on the device); returns
