@@ -199,7 +199,10 @@ prenom_status prenom_object_set_frames(prenom_object_t obj, int n_frames,
                                        const float* depth, const uint8_t* mask,
                                        uint8_t instance_value, const prenom_pose* obj_pose);
 /* Replace the pixels of one existing frame (same camera/size); host buffers
- * copied on the context stream. Used by streaming callers (and bench e2e). */
+ * (pinned for an asynchronous copy) are copied on the sampling stream, after
+ * the work already enqueued and before any sampling enqueued later, so a
+ * streaming caller's upload of step t+1's keyframe overlaps step t. Used by
+ * streaming callers (and bench e2e). */
 prenom_status prenom_object_upload_frame(prenom_object_t obj, int frame, const float* rgb,
                                          const float* depth, const uint8_t* mask);
 /* Synthetic RGB-D views rendered on the device straight into the object's
@@ -229,6 +232,17 @@ prenom_status prenom_object_get_frame(prenom_object_t obj, int frame, float* rgb
  * stats stay on the device (prenom_object_last_stats reads them). */
 prenom_status prenom_train_step(prenom_object_t obj, int n_steps, prenom_step_stats* stats);
 prenom_status prenom_object_last_stats(prenom_object_t obj, int n, prenom_step_stats* stats);
+/* Streaming train step (same steps as prenom_train_step, nothing synchronizes):
+ * the steps' stats and the numeric flag are copied to pinned host memory
+ * behind them; *ticket names the call. prefetch_next = 1 also issues the next
+ * step's ray sampling after this call's last backward (its keyframe must be
+ * resident: upload it first, prenom_object_frame_at tells which). */
+prenom_status prenom_train_step_async(prenom_object_t obj, int n_steps, int prefetch_next, uint64_t* ticket);
+/* Wait for one async call's stats (the last 4 calls are kept); stats receives
+ * its n_steps entries (may be NULL). Returns NUMERIC like train_track's throw. */
+prenom_status prenom_wait_stats(prenom_object_t obj, uint64_t ticket, prenom_step_stats* stats);
+/* Keyframe index step `step` of this object draws from (TAG_FRAME, mapper.cpp:151). */
+prenom_status prenom_object_frame_at(prenom_object_t obj, int64_t step, int* frame);
 /* Steps taken so far (AdamState::step). */
 prenom_status prenom_object_step(prenom_object_t obj, int64_t* step);
 /* Keyframe index the next train step will draw its rays from (TAG_FRAME). */

@@ -139,6 +139,7 @@ EXPORTED = [
     "prenom_ctx_launch_count", "prenom_ctx_profile", "prenom_ctx_kernel_times", "prenom_object_next_frame",
     "prenom_object_create", "prenom_object_destroy", "prenom_object_set_frames",
     "prenom_object_upload_frame", "prenom_object_synth_frames", "prenom_object_get_frame", "prenom_train_step", "prenom_object_last_stats",
+    "prenom_train_step_async", "prenom_wait_stats", "prenom_object_frame_at",
     "prenom_object_step", "prenom_object_check",
     "prenom_render", "prenom_density_query", "prenom_extract_mesh", "prenom_get_mesh", "prenom_get_mesh_grid", "prenom_field_eval",
     "prenom_get_params", "prenom_set_params", "prenom_get_grid", "prenom_set_grid",
@@ -203,6 +204,9 @@ def _declare(lib):
         "prenom_object_get_frame": (i32, [P, i32, f32p, f32p, i32p, i32p, i32p, i32p]),
         "prenom_train_step": (i32, [P, i32, C.POINTER(StepStatsC)]),
         "prenom_object_last_stats": (i32, [P, i32, C.POINTER(StepStatsC)]),
+        "prenom_train_step_async": (i32, [P, i32, i32, C.POINTER(C.c_uint64)]),
+        "prenom_wait_stats": (i32, [P, C.c_uint64, C.POINTER(StepStatsC)]),
+        "prenom_object_frame_at": (i32, [P, C.c_int64, i32p]),
         "prenom_object_step": (i32, [P, i64p]),
         "prenom_object_check": (i32, [P]),
         "prenom_render": (i32, [P, i32, f32p, f32p, f32p, f32p]),

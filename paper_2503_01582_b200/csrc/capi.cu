@@ -223,6 +223,21 @@ struct prenom_object_s {
   cudaEvent_t ev_bwd = nullptr, ev_sample = nullptr;
   bool sample_ready = false;
   cudaStream_t lane = nullptr;  // set while prenom_train_step_many runs this object on a lane stream
+  // streaming: frame uploads go on ctx->side (the sampling stream); a step
+  // whose sampling runs on the main stream waits for ev_upload first
+  cudaEvent_t ev_upload = nullptr, ev_main = nullptr;
+  bool upload_pending = false;
+  // prenom_train_step_async: ring of pinned host stat slots
+  struct AsyncSlot {
+    uint64_t ticket = 0;
+    int n = 0;
+    StepStatsDev* host = nullptr;  // pinned
+    int* flag = nullptr;           // pinned
+    int cap = 0;
+    cudaEvent_t ev = nullptr;
+  };
+  AsyncSlot slots[4];
+  uint64_t next_ticket = 1;
   DevBuf<int> flag;
   McMesh mesh;  // prenom_extract_mesh result (device)
   FrameScratch fscratch;  // band / pixel-list construction
@@ -230,6 +245,13 @@ struct prenom_object_s {
     for (auto* f : frames) delete f;
     if (ev_bwd) cudaEventDestroy(ev_bwd);
     if (ev_sample) cudaEventDestroy(ev_sample);
+    if (ev_upload) cudaEventDestroy(ev_upload);
+    if (ev_main) cudaEventDestroy(ev_main);
+    for (auto& sl : slots) {
+      if (sl.ev) cudaEventDestroy(sl.ev);
+      if (sl.host) cudaFreeHost(sl.host);
+      if (sl.flag) cudaFreeHost(sl.flag);
+    }
   }
 };
 
@@ -354,8 +376,10 @@ prenom_status enqueue_step(prenom_object_s* o, StepStatsDev* stats, bool has_nex
     CUDA_TRY(cudaStreamWaitEvent(st, o->ev_sample, 0));
     o->sample_ready = false;
   } else {
+    if (o->upload_pending) CUDA_TRY(cudaStreamWaitEvent(st, o->ev_upload, 0));
     STATUS_TRY(enqueue_sample(o, o->step, st));
   }
+  o->upload_pending = false;  // any later sampling is ordered after this step's
   const bool tc = c.mlp_precision == PRENOM_MLP_BF16;
   {
     ProfScope ps(o->ctx, PRENOM_K_FIELD_FWD, st);
@@ -446,9 +470,9 @@ void to_host_stats(const StepStatsDev& d, prenom_step_stats* s) {
 }
 
 prenom_status set_frame_pixels(prenom_object_s* o, FrameDev* f, const float* rgb, const float* depth,
-                               const uint8_t* mask) {
+                               const uint8_t* mask, cudaStream_t st = nullptr) {
   const size_t npx = (size_t)o->W * o->H;
-  cudaStream_t st = o->ctx->stream;
+  if (!st) st = o->ctx->stream;
   CUDA_TRY(f->rgb.ensure(npx * 3));
   CUDA_TRY(f->depth.ensure(npx));
   CUDA_TRY(cudaMemcpyAsync(f->rgb.p, rgb, npx * 3 * sizeof(float), cudaMemcpyHostToDevice, st));
@@ -774,7 +798,24 @@ prenom_status prenom_object_upload_frame(prenom_object_t o, int frame, const flo
   if (!o || !rgb || !depth) return fail(PRENOM_USAGE, "NULL argument");
   if (frame < 0 || frame >= (int)o->frames.size()) return fail(PRENOM_USAGE, "frame index out of range");
   CUDA_TRY(cudaSetDevice(o->ctx->device));
-  return set_frame_pixels(o, o->frames[frame], rgb, depth, mask);
+  // On the sampling stream: ordered after any sampling already issued (which
+  // may still read this frame) and before the next one; the main stream only
+  // waits for it when it samples itself (enqueue_step).
+  // It also waits for the work already on the main stream (whose sampling may
+  // read the frame), but not for steps enqueued after it.
+  cudaStream_t side = o->ctx->overlap ? o->ctx->side : o->ctx->stream;
+  if (!o->ev_upload) {
+    CUDA_TRY(cudaEventCreateWithFlags(&o->ev_upload, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&o->ev_main, cudaEventDisableTiming));
+  }
+  if (side != o->ctx->stream) {
+    CUDA_TRY(cudaEventRecord(o->ev_main, o->ctx->stream));
+    CUDA_TRY(cudaStreamWaitEvent(side, o->ev_main, 0));
+  }
+  STATUS_TRY(set_frame_pixels(o, o->frames[frame], rgb, depth, mask, side));
+  CUDA_TRY(cudaEventRecord(o->ev_upload, side));
+  o->upload_pending = true;
+  return PRENOM_OK;
 }
 
 prenom_status prenom_train_step(prenom_object_t o, int n_steps, prenom_step_stats* stats) {
@@ -794,6 +835,64 @@ prenom_status prenom_train_step(prenom_object_t o, int n_steps, prenom_step_stat
     STATUS_TRY(check_flag(o));
     for (int i = 0; i < n_steps; ++i) to_host_stats(h[i], &stats[i]);
   }
+  return PRENOM_OK;
+}
+
+// Streaming variant: nothing on this call synchronizes. The stats of the
+// call's steps (and the numeric flag) are copied device->host into a pinned
+// slot behind the steps; prenom_wait_stats(ticket) waits for that copy only.
+// prefetch_next issues the next step's ray sampling on the side stream right
+// after this call's last backward (as consecutive steps of one call do), so a
+// caller stepping one call per keyframe keeps the sampling overlapped with Adam.
+prenom_status prenom_train_step_async(prenom_object_t o, int n_steps, int prefetch_next, uint64_t* ticket) {
+  if (!o || !ticket) return fail(PRENOM_USAGE, "NULL argument");
+  if (n_steps < 1) return fail(PRENOM_USAGE, "n_steps must be >= 1");
+  if (o->frames.empty()) return fail(PRENOM_DATA, "train_step: object has no frames");
+  CUDA_TRY(cudaSetDevice(o->ctx->device));
+  STATUS_TRY(ensure_scratch(o, o->cfg.rays_per_iter, o->cfg.samples_per_ray));
+  CUDA_TRY(o->stats.ensure((size_t)n_steps));
+  cudaStream_t st = o->ctx->stream;
+  auto& sl = o->slots[o->next_ticket % 4];
+  if (sl.ev) CUDA_TRY(cudaEventSynchronize(sl.ev));  // the slot's previous copy (4 calls ago) has landed
+  if (sl.cap < n_steps) {
+    if (sl.host) CUDA_TRY(cudaFreeHost(sl.host));
+    CUDA_TRY(cudaMallocHost(&sl.host, sizeof(StepStatsDev) * n_steps));
+    sl.cap = n_steps;
+  }
+  if (!sl.flag) CUDA_TRY(cudaMallocHost(&sl.flag, sizeof(int)));
+  if (!sl.ev) CUDA_TRY(cudaEventCreateWithFlags(&sl.ev, cudaEventDisableTiming));
+  CUDA_TRY(cudaMemsetAsync(o->stats.p, 0, sizeof(StepStatsDev) * n_steps, st));
+  for (int it = 0; it < n_steps; ++it)
+    STATUS_TRY(enqueue_step(o, o->stats.p + it, it + 1 < n_steps || prefetch_next != 0));
+  o->last_n_steps = n_steps;
+  CUDA_TRY(cudaMemcpyAsync(sl.host, o->stats.p, sizeof(StepStatsDev) * n_steps, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(sl.flag, o->flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaEventRecord(sl.ev, st));
+  sl.n = n_steps;
+  sl.ticket = o->next_ticket++;
+  *ticket = sl.ticket;
+  return PRENOM_OK;
+}
+
+prenom_status prenom_wait_stats(prenom_object_t o, uint64_t ticket, prenom_step_stats* stats) {
+  if (!o) return fail(PRENOM_USAGE, "NULL object");
+  for (auto& sl : o->slots) {
+    if (sl.ticket != ticket || ticket == 0) continue;
+    CUDA_TRY(cudaEventSynchronize(sl.ev));
+    if (*sl.flag & 1) return fail(PRENOM_NUMERIC, "field_eval produced a non-finite output");
+    if (*sl.flag & 2) return fail(PRENOM_NUMERIC, "batch_loss: non-finite loss");
+    if (stats)
+      for (int i = 0; i < sl.n; ++i) to_host_stats(sl.host[i], &stats[i]);
+    return PRENOM_OK;
+  }
+  return fail(PRENOM_USAGE, "prenom_wait_stats: unknown or expired ticket (4 calls are kept)");
+}
+
+prenom_status prenom_object_frame_at(prenom_object_t o, int64_t step, int* frame) {
+  if (!o || !frame) return fail(PRENOM_USAGE, "NULL argument");
+  if (o->frames.empty()) return fail(PRENOM_DATA, "object has no frames");
+  if (step < 0) return fail(PRENOM_USAGE, "negative step");
+  *frame = frame_of_step(o, step);
   return PRENOM_OK;
 }
 

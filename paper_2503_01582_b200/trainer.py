@@ -325,6 +325,26 @@ class ObjectTrainer:
         _check(self.lib.prenom_train_step(self.h, n_steps, out))
         return [_stats(s) for s in out]
 
+    def train_step_async(self, n_steps: int = 1, prefetch_next: bool = True) -> int:
+        """Streaming step (prenom_train_step_async): returns a ticket for wait_stats."""
+        t = C.c_uint64()
+        _check(self.lib.prenom_train_step_async(self.h, n_steps, int(prefetch_next), C.byref(t)))
+        self._async_n = getattr(self, "_async_n", {})
+        self._async_n[t.value] = n_steps
+        return t.value
+
+    def wait_stats(self, ticket: int):
+        """Per-step loss dicts of one train_step_async call (waits for that call only)."""
+        n = self._async_n.pop(ticket, 1)
+        out = (StepStatsC * n)()
+        _check(self.lib.prenom_wait_stats(self.h, ticket, out))
+        return [_stats(s) for s in out]
+
+    def frame_at(self, step: int) -> int:
+        f = C.c_int32()
+        _check(self.lib.prenom_object_frame_at(self.h, step, C.byref(f)))
+        return f.value
+
     def last_stats(self, n: int = 1):
         out = (StepStatsC * n)()
         _check(self.lib.prenom_object_last_stats(self.h, n, out))

@@ -83,3 +83,33 @@ def test_reptile_delta_apply_linearity(ctx, rng):
     meta.set_params(th)
     meta.reptile_update(objs[0], 0.1)
     assert np.array_equal(meta.get_params(), (np.float32(0.9) * th + np.float32(0.1) * ads[0]).astype(np.float32))
+
+
+def test_streaming_async_steps_equal_train_step(ctx):
+    """prenom_train_step_async + prenom_wait_stats with a keyframe upload before every
+    step (the e2e streaming loop of bench.py) == prenom_train_step on a twin object."""
+    import torch
+
+    sc = tasks()[0]
+    a = ObjectTrainer.create(ctx, ARCH, grid_res=8, seed=21, cfg=CFG, box_min=sc.box_min, box_max=sc.box_max)
+    b = ObjectTrainer.create(ctx, ARCH, grid_res=8, seed=21, cfg=CFG, box_min=sc.box_min, box_max=sc.box_max)
+    for o in (a, b):
+        o.set_frames(sc.cams, sc.rgb, sc.depth, sc.mask, 1, sc.obj_pose)
+    want = a.train_step(6)
+    rgb = torch.from_numpy(np.ascontiguousarray(sc.rgb)).pin_memory()
+    dep = torch.from_numpy(np.ascontiguousarray(sc.depth)).pin_memory()
+    got, prev = [], None
+    for i in range(6):
+        f = b.frame_at(i)
+        assert f == want[i]["frame"]
+        b.upload_frame(f, rgb[f].numpy(), dep[f].numpy(), None)
+        tk = b.train_step_async(1, prefetch_next=i < 5)
+        if prev is not None:
+            got += b.wait_stats(prev)
+        prev = tk
+    got += b.wait_stats(prev)
+    for x, y in zip(got, want):
+        assert x["n_samples"] == y["n_samples"] and x["frame"] == y["frame"]
+        assert abs(x["total"] - y["total"]) <= 1e-4 * abs(y["total"])
+    with pytest.raises(Exception, match="ticket"):
+        b.wait_stats(12345)
