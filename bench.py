@@ -328,7 +328,9 @@ class Cfg4(Workload):
                                      box_min=sc.box_min, box_max=sc.box_max)
             w.set_frames(sc.cams, sc.rgb, sc.depth, sc.mask, 1, sc.obj_pose)
             self.workers.append(w)
-        self.objs = self.workers
+        for w in self.workers:  # first-use allocations outside the timed region (adapt resets Adam + step)
+            w.train_step(1, stats=False)
+        self.objs = self.workers + [self.meta]
         self.engine = CudaEngine(self.meta, self.workers)
         self.n_objects_total = ws
         self.k = 0

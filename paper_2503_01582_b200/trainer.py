@@ -22,6 +22,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import weakref
 from dataclasses import dataclass, field, fields
 
 import numpy as np
@@ -201,9 +202,12 @@ class Context:
         _check(self.lib.prenom_ctx_create(device, C.byref(h)))
         self.h = h
         self.device = device
+        self._objects = weakref.WeakSet()  # live ObjectTrainers: destroyed before the context
 
     def close(self):
         if getattr(self, "h", None):
+            for o in list(self._objects):
+                o.close()
             self.lib.prenom_ctx_destroy(self.h)
             self.h = None
 
@@ -239,6 +243,7 @@ class ObjectTrainer:
     def __init__(self, ctx: Context, handle, arch: FieldArch, cfg: TrainConfig, grid_res: int):
         self.ctx, self.h, self.arch, self.cfg, self.grid_res = ctx, handle, arch, cfg, grid_res
         self.lib = ctx.lib
+        ctx._objects.add(self)
 
     @classmethod
     def create(cls, ctx: Context, arch: FieldArch, theta=None, grid=None, grid_res: int = 48,
