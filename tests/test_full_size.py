@@ -1,0 +1,174 @@
+"""Parity at BASELINE.json's full sizes (GPU), where the oracle still finishes
+in seconds: one cfg2 step's whole batch through each stage, bit-exact where the
+north star demands it, plus size-independent properties for what the oracle
+cannot afford (the 256^3 density query, cfg5's 128^3-prior sampler batch).
+
+cfg2: 8192 rays x (32 coarse -> 96 fine) samples = 786,432 samples, hash grid
+L16 F2 T2^19 (16.78 M parameters), 256^2 views, 32^3 prior.
+"""
+import numpy as np
+import pytest
+
+from paper_2503_01582_b200 import ObjectTrainer, TrainConfig, scenes
+from paper_2503_01582_b200 import trainer as T
+
+pytestmark = pytest.mark.gpu
+
+B, S, NC = 8192, 96, 32
+N = B * S
+
+
+@pytest.fixture(scope="module")
+def cfg2_theta():
+    arch = scenes.cfg2_arch(64)
+    rng = np.random.default_rng(22)
+    P, nh = arch.param_count(), arch.hash_param_count()
+    theta = np.empty(P, np.float32)
+    theta[:nh] = rng.uniform(-0.5, 0.5, nh)
+    theta[nh:] = 0.3 * rng.standard_normal(P - nh)
+    return arch, theta
+
+
+@pytest.fixture(scope="module")
+def cfg2_scene():
+    sc = scenes.box_union_scene(n_views=4, res=256, seed=1000)
+    return sc, scenes.occupancy_prior(sc.boxes, R=32)
+
+
+def test_cfg2_encode_full_batch_bit_exact(ctx, oracle, cfg2_theta):
+    """hash_encode of one step's 786,432 samples at L16 T2^19 (every level, dense and hashed)."""
+    arch, theta = cfg2_theta
+    xyz = np.random.default_rng(1).uniform(0, 1, (N, 3)).astype(np.float32)
+    ours = T.debug_hash_encode(ctx, arch, theta, xyz)
+    ref, _, _ = oracle.hash_encode(arch, theta, xyz)
+    assert ours.shape == (N, 32)
+    assert np.array_equal(ours, ref)
+
+
+def test_cfg2_adam_full_parameter_vector_bit_exact(ctx, oracle, cfg2_theta):
+    """adam_step over all 16,783,748 parameters, 3 steps, sparse-ish gradients."""
+    arch, theta = cfg2_theta
+    rng = np.random.default_rng(2)
+    P = arch.param_count()
+    p1 = p2 = theta
+    m1 = m2 = v1 = v2 = np.zeros(P, np.float32)
+    s1 = s2 = 0
+    for _ in range(3):
+        g = rng.standard_normal(P).astype(np.float32)
+        g[rng.random(P) < 0.6] = 0.0
+        p1, m1, v1, s1 = T.debug_adam(ctx, p1, g, m1, v1, s1)
+        p2, m2, v2, s2 = oracle.adam_step(p2, g, m2, v2, s2)
+    assert np.array_equal(p1, p2) and np.array_equal(m1, m2) and np.array_equal(v1, v2)
+
+
+def test_cfg2_step_rays_and_samples_full_batch_bit_exact(ctx, oracle, cfg2_theta, cfg2_scene):
+    """One cfg2 step's 8192 rays (generate_rays: 25% band) and their 786,432 prior-CDF
+    samples: pixel picks, rays, depths, deltas, positions all bit-exact."""
+    arch, theta = cfg2_theta
+    sc, grid = cfg2_scene
+    cfg = TrainConfig(rays_per_iter=B, samples_per_ray=S, coarse_samples=NC, prior_sampling=1)
+    ob = ObjectTrainer.create(ctx, arch, theta=theta, grid=grid, seed=7, cfg=cfg, box_min=sc.box_min,
+                              box_max=sc.box_max)
+    ob.set_frames(sc.cams, sc.rgb, sc.depth, sc.mask, 1, sc.obj_pose)
+    f, step = 2, 13
+    g = ob.debug_generate_rays(f, step=step)
+    o = oracle.generate_rays(sc.cams[f], sc.rgb[f], sc.depth[f], sc.mask[f], 1, sc.obj_pose, B, 0.25, 8, seed=7,
+                             step=step)
+    for k in ("origins", "dirs", "kinds", "target_rgb", "target_depth", "pick_px"):
+        assert np.array_equal(g[k], o[k]), k
+    assert np.sum(g["kinds"] != g["kinds"][0]) == round(B * 0.25)
+    s = T.debug_sample_rays(ctx, g["origins"], g["dirs"], sc.box_min, sc.box_max, True, grid, NC, S, 1e-4,
+                            seed=7, step=step)
+    n_live = 0
+    for r in range(B):
+        ref = oracle.sample_ray(grid, g["origins"][r], g["dirs"][r], sc.box_min, sc.box_max, NC, S, 1e-4, seed=7,
+                                tag=3, step=step, ray=r)
+        assert (s["count"][r] == 0) == ref["escaped"], r
+        if ref["escaped"]:
+            continue
+        n_live += 1
+        assert np.array_equal(s["depths"][r], ref["depths"]), r
+        assert np.array_equal(s["deltas"][r], ref["deltas"]), r
+        assert np.array_equal(s["positions"][r], ref["positions"]), r
+    assert n_live > B // 2
+    ob.close()
+
+
+def test_cfg2_field_backward_full_batch(ctx, oracle, cfg2_theta):
+    """field_backward summed over 786,432 samples into the 16.78 M gradient (fp32 path):
+    within 1e-4 of the oracle (atomics reorder the sums), untouched rows exactly zero."""
+    arch, theta = cfg2_theta
+    rng = np.random.default_rng(3)
+    xyz = rng.uniform(0.2, 0.8, (N, 3)).astype(np.float32)
+    ds = rng.standard_normal(N).astype(np.float32) * 1e-2
+    dr = rng.standard_normal((N, 3)).astype(np.float32) * 1e-2
+    g = T.debug_field_backward(ctx, arch, theta, xyz, ds, dr)
+    go = oracle.field_backward(arch, theta, xyz, ds, dr)
+    scale = np.abs(go).max()
+    np.testing.assert_allclose(g, go, rtol=1e-4, atol=1e-5 * scale)
+    assert np.mean((g == 0) != (go == 0)) < 1e-4
+
+
+def test_density_query_256_cube(ctx, oracle, cfg2_theta):
+    """cfg5's final 256^3 density query (refresh_grid, density_grid.cpp:119-132) at cfg2's arch:
+    20,000 random lattice vertices vs the oracle's field_eval at (i,j,k)*(1/(R-1)) (1e-6), and the
+    lattice layout (x fastest) checked through the corners."""
+    arch, theta = cfg2_theta
+    ob = ObjectTrainer.create(ctx, arch, theta=theta, grid_res=8)
+    R = 256
+    grid = ob.density_query(R)
+    rng = np.random.default_rng(4)
+    idx = rng.integers(0, R, (20000, 3))
+    idx[:8] = [[i * (R - 1), j * (R - 1), k * (R - 1)] for i in (0, 1) for j in (0, 1) for k in (0, 1)]
+    scale = np.float32(1.0) / np.float32(R - 1)  # density_grid.cpp:121-127: p = float(i) * scale
+    pts = (idx.astype(np.float32) * scale).astype(np.float32)
+    so, _ = oracle.field_eval(arch, theta, pts)
+    got = grid[idx[:, 2], idx[:, 1], idx[:, 0]]
+    np.testing.assert_allclose(got, so, rtol=1e-6, atol=1e-30)
+    assert np.all(np.isfinite(grid)) and np.all(grid >= 0)
+    ob.close()
+
+
+def test_cfg5_sampler_128_prior_batch(ctx, oracle):
+    """cfg5 shapes: a 128^3 prior and one object's 1366-ray batch at 96 fine samples, bit-exact."""
+    rng = np.random.default_rng(5)
+    boxes = scenes.random_boxes(rng)
+    grid = scenes.occupancy_prior(boxes, R=128)
+    cams = scenes.fibonacci_cameras(3, 1.5, 512, 512, 512.0)
+    o_w, d_w = scenes._pixel_rays(cams[1])
+    pick = rng.integers(0, 512 * 512, 1366)
+    d = d_w.reshape(-1, 3)[pick].astype(np.float32)
+    o = np.repeat(o_w[None], 1366, 0).astype(np.float32)
+    lo, hi = np.full(3, -0.5, np.float32), np.full(3, 0.5, np.float32)
+    s = T.debug_sample_rays(ctx, o, d, lo, hi, True, grid, NC, S, 1e-4, seed=11, step=40)
+    n_live = 0
+    for r in range(len(o)):
+        ref = oracle.sample_ray(grid, o[r], d[r], lo, hi, NC, S, 1e-4, seed=11, tag=3, step=40, ray=r)
+        assert (s["count"][r] == 0) == ref["escaped"], r
+        if not ref["escaped"]:
+            n_live += 1
+            assert np.array_equal(s["depths"][r], ref["depths"]), r
+            assert np.array_equal(s["positions"][r], ref["positions"]), r
+    assert n_live > 100
+
+
+def test_cfg2_train_step_batch_properties(ctx, cfg2_scene):
+    """A full cfg2 bf16 train step: every live ray carries 96 samples, stats count them,
+    losses finite; two objects with the same seed draw the same frames and sample counts."""
+    sc, grid = cfg2_scene
+    arch = scenes.cfg2_arch(64)
+    cfg = TrainConfig(rays_per_iter=B, samples_per_ray=S, coarse_samples=NC, prior_sampling=1, grid_refresh_every=50,
+                      mlp_precision=1)
+    a, b = (ObjectTrainer.create(ctx, arch, grid=grid, seed=9, cfg=cfg, box_min=sc.box_min, box_max=sc.box_max)
+            for _ in range(2))
+    for o in (a, b):
+        o.set_frames(sc.cams, sc.rgb, sc.depth, sc.mask, 1, sc.obj_pose)
+    sa, sb = a.train_step(3), b.train_step(3)
+    for x, y in zip(sa, sb):
+        assert x["frame"] == y["frame"] and x["n_samples"] == y["n_samples"]
+        assert x["n_samples"] % S == 0 and 0 < x["n_samples"] <= N
+        assert x["n_samples"] // S + x["escaped"] == B
+        assert np.isfinite(x["total"]) and x["total"] > 0
+        assert abs(x["total"] - y["total"]) <= 1e-3 * abs(y["total"])
+    a.close()
+    b.close()
