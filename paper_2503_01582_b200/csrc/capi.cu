@@ -201,6 +201,7 @@ struct prenom_object_s {
   DevBuf<float> params, grad, m, v;
   int R = 0;
   DevBuf<float> grid;
+  DevBuf<float> query;  // prenom_density_query output (swapped with grid on update)
   uint64_t seed = 0;
   float bmin[3], bmax[3];
   int64_t step = 0;
@@ -974,7 +975,7 @@ prenom_status prenom_density_query(prenom_object_t o, int R, float* out, int upd
   CUDA_TRY(cudaSetDevice(o->ctx->device));
   cudaStream_t st = o->ctx->stream;
   const size_t n = (size_t)R * R * R;
-  DevBuf<float> d;
+  DevBuf<float>& d = o->query;  // kept across calls (no per-query cudaMalloc/cudaFree)
   CUDA_TRY(d.ensure(n));
   CUDA_TRY(launch_refresh_grid(o->fd, o->params.p, R, d.p, o->flag.p, st));
   o->ctx->launches += 1;

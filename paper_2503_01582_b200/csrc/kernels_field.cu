@@ -15,6 +15,8 @@
 //   k_encode_bwd: d_features x trilinear weights scattered into the table
 //                 gradient (float2 vector atomics in L2)
 //   k_adam      : dense, fused grad-zero, float4 vectorised
+#include <cstdlib>
+
 #include "prenom_device.cuh"
 
 namespace prenom {
@@ -508,6 +510,152 @@ __global__ void __launch_bounds__(128) k_field_points(FieldDesc fd, const float*
     for (int o = 0; o < 4; ++o) raw_out[4 * (size_t)i + o] = raw[o];
 }
 
+// Specialised exact field for the BASELINE family (F = 2, L*F = INP, hidden
+// width W, H hidden layers): identical per-point arithmetic to
+// k_field_points (same *_rn sums, each output's terms added in the same
+// ascending k order, so the same bits), laid out for throughput:
+//   * the MLP is staged once per CTA in shared memory TRANSPOSED ([in][out]),
+//     read as warp-broadcast float4 over outputs;
+//   * a layer walks k in a rolled loop and updates all W accumulators
+//     (registers) per step -- W independent add chains, small code;
+//   * activations live in a per-thread shared-memory column act[k][tid]
+//     (conflict-free), so the loop index stays dynamic without local memory.
+// (The generic kernel keeps runtime-sized x[]/h[] in local memory and
+// re-reads each weight through L1 per multiply.) Used for refresh_grid,
+// density queries and field_eval (cfg5: 128^3 refreshes, the 256^3 query).
+constexpr int kFpThreads = 128;
+template <int INP, int W, int H>
+struct FpSmem {
+  static constexpr int kW0 = 0, kB0 = INP * W, kL1 = kB0 + W;
+  static constexpr int kWo = kL1 + (H - 1) * (W * W + W), kBo = kWo + 4 * W;
+  static constexpr int kWeights = (kBo + 4 + 3) / 4 * 4;
+  static constexpr int kAct = (INP > W ? INP : W) * kFpThreads;  // act[k][tid]
+  static constexpr size_t kBytes = (size_t)(kWeights + kAct) * sizeof(float);
+};
+
+// out[o] = b[o] + sum_k W[o][k] act[k], k ascending (field.cpp:181-211)
+template <int NIN, int NOUT>
+__device__ __forceinline__ void fp_layer(const float* WT, const float* b, const float* act, float* out) {
+#pragma unroll
+  for (int o = 0; o < NOUT; ++o) out[o] = b[o];
+#pragma unroll 2
+  for (int k = 0; k < NIN; ++k) {
+    const float xk = act[k * kFpThreads];
+    const float4* wr = reinterpret_cast<const float4*>(WT + k * NOUT);
+#pragma unroll
+    for (int o4 = 0; o4 < NOUT / 4; ++o4) {
+      const float4 w = wr[o4];
+      out[4 * o4] = __fadd_rn(out[4 * o4], __fmul_rn(w.x, xk));
+      out[4 * o4 + 1] = __fadd_rn(out[4 * o4 + 1], __fmul_rn(w.y, xk));
+      out[4 * o4 + 2] = __fadd_rn(out[4 * o4 + 2], __fmul_rn(w.z, xk));
+      out[4 * o4 + 3] = __fadd_rn(out[4 * o4 + 3], __fmul_rn(w.w, xk));
+    }
+  }
+}
+
+template <int INP, int W, int H>
+__global__ void __launch_bounds__(kFpThreads) k_field_points_t(FieldDesc fd, const float* __restrict__ params, int n,
+                                                               const float* __restrict__ xyz, int grid_R, float* sigma,
+                                                               float* rgb, float* raw_out, float* feat_out, int* flag) {
+  using SM = FpSmem<INP, W, H>;
+  extern __shared__ __align__(16) float wsm[];
+  {
+    const float* mlp = params + fd.hash_params;  // reference layout: W[out][in], b[out] per layer
+    for (int j = threadIdx.x; j < INP * W; j += blockDim.x) wsm[SM::kW0 + j] = __ldg(mlp + (j % W) * INP + j / W);
+    for (int j = threadIdx.x; j < W; j += blockDim.x) wsm[SM::kB0 + j] = __ldg(mlp + W * INP + j);
+    if constexpr (H == 2) {
+      const float* m1 = mlp + W * INP + W;
+      for (int j = threadIdx.x; j < W * W; j += blockDim.x) wsm[SM::kL1 + j] = __ldg(m1 + (j % W) * W + j / W);
+      for (int j = threadIdx.x; j < W; j += blockDim.x) wsm[SM::kL1 + W * W + j] = __ldg(m1 + W * W + j);
+    }
+    const float* mo = mlp + W * INP + W + (H - 1) * (W * W + W);
+    for (int j = threadIdx.x; j < 4 * W; j += blockDim.x) wsm[SM::kWo + j] = __ldg(mo + (j % 4) * W + j / 4);
+    if (threadIdx.x < 4) wsm[SM::kBo + threadIdx.x] = __ldg(mo + 4 * W + threadIdx.x);
+  }
+  __syncthreads();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float* act = wsm + SM::kWeights + threadIdx.x;  // act[k * kFpThreads]
+  float px, py, pz;
+  if (grid_R > 0) {  // refresh_grid lattice point (density_grid.cpp:121-128)
+    const float scale = __fdiv_rn(1.f, (float)(grid_R - 1));
+    const int ix = i % grid_R, iy = (i / grid_R) % grid_R, iz = i / (grid_R * grid_R);
+    px = __fmul_rn((float)ix, scale);
+    py = __fmul_rn((float)iy, scale);
+    pz = __fmul_rn((float)iz, scale);
+  } else {
+    px = xyz[3 * i];
+    py = xyz[3 * i + 1];
+    pz = xyz[3 * i + 2];
+  }
+  px = clamp01(px);
+  py = clamp01(py);
+  pz = clamp01(pz);
+  for (int l = 0; l < INP / 2; ++l) {
+    float f2[2];
+    encode_level<2>(fd, params, l, px, py, pz, f2);
+    act[(2 * l) * kFpThreads] = f2[0];
+    act[(2 * l + 1) * kFpThreads] = f2[1];
+    if (feat_out) {
+      feat_out[(size_t)i * INP + 2 * l] = f2[0];
+      feat_out[(size_t)i * INP + 2 * l + 1] = f2[1];
+    }
+  }
+  float h[W];
+  fp_layer<INP, W>(wsm + SM::kW0, wsm + SM::kB0, act, h);
+#pragma unroll
+  for (int o = 0; o < W; ++o) act[o * kFpThreads] = h[o] > 0.f ? h[o] : 0.f;
+  if constexpr (H == 2) {
+    fp_layer<W, W>(wsm + SM::kL1, wsm + SM::kL1 + W * W, act, h);
+#pragma unroll
+    for (int o = 0; o < W; ++o) act[o * kFpThreads] = h[o] > 0.f ? h[o] : 0.f;
+  }
+  float raw[4];
+  fp_layer<W, 4>(wsm + SM::kWo, wsm + SM::kBo, act, raw);
+  const float sg = density_forward(fd.act, raw[0]);
+  const float c0 = stable_sigmoid(raw[1]), c1 = stable_sigmoid(raw[2]), c2 = stable_sigmoid(raw[3]);
+  if (!all_finite4(sg, c0, c1, c2) && flag) atomicOr(flag, 1);
+  if (sigma) sigma[i] = sg;
+  if (rgb) {
+    rgb[3 * i] = c0;
+    rgb[3 * i + 1] = c1;
+    rgb[3 * i + 2] = c2;
+  }
+  if (raw_out)
+#pragma unroll
+    for (int o = 0; o < 4; ++o) raw_out[4 * (size_t)i + o] = raw[o];
+}
+
+template <int INP, int W, int H>
+cudaError_t run_field_points_t(const FieldDesc& fd, const float* params, int n, const float* xyz, int R, float* sigma,
+                               float* rgb, float* raw, float* features, int* flag, cudaStream_t st) {
+  const size_t smem = FpSmem<INP, W, H>::kBytes;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k_field_points_t<INP, W, H>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  k_field_points_t<INP, W, H><<<(unsigned)((n + kFpThreads - 1) / kFpThreads), kFpThreads, smem, st>>>(
+      fd, params, n, xyz, R, sigma, rgb, raw, features, flag);
+  return cudaGetLastError();
+}
+
+// true (and launched) when the arch has a specialised exact kernel
+bool field_points_fast(const FieldDesc& fd, const float* params, int n, const float* xyz, int R, float* sigma,
+                       float* rgb, float* raw, float* features, int* flag, cudaStream_t st, cudaError_t* err) {
+  if (fd.F != 2 || fd.mlp_params != fd.b_off[fd.H] + 4) return false;
+#define PRENOM_FP_CASE(L_, W_, H_)                                                                       \
+  if (fd.L == L_ && fd.W == W_ && fd.H == H_) {                                                        \
+    *err = run_field_points_t<2 * L_, W_, H_>(fd, params, n, xyz, R, sigma, rgb, raw, features, flag, st); \
+    return true;                                                                                       \
+  }
+  PRENOM_FP_CASE(8, 32, 1) PRENOM_FP_CASE(8, 32, 2) PRENOM_FP_CASE(8, 64, 1) PRENOM_FP_CASE(8, 64, 2)
+  PRENOM_FP_CASE(12, 32, 1) PRENOM_FP_CASE(12, 32, 2) PRENOM_FP_CASE(12, 64, 1) PRENOM_FP_CASE(12, 64, 2)
+  PRENOM_FP_CASE(16, 32, 1) PRENOM_FP_CASE(16, 32, 2) PRENOM_FP_CASE(16, 64, 1) PRENOM_FP_CASE(16, 64, 2)
+#undef PRENOM_FP_CASE
+  return false;
+}
+
 // ------------------------------------------------------------------ Adam
 // field.cpp:295-310, dense, same operation order with *_rn intrinsics;
 // grad zeroed in the same pass (train_track zeroes it before each backward,
@@ -687,6 +835,9 @@ cudaError_t launch_encode_bwd(const FieldDesc& fd, const float* /*params*/, floa
 cudaError_t launch_field_points(const FieldDesc& fd, const float* params, int n, const float* xyz, float* sigma,
                                 float* rgb, float* raw, float* features, int* flag, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
+  cudaError_t e = cudaSuccess;
+  if (!getenv("PRENOM_GENERIC_FIELD") && field_points_fast(fd, params, n, xyz, 0, sigma, rgb, raw, features, flag, st, &e))
+    return e;
   k_field_points<<<(n + 127) / 128, 128, 0, st>>>(fd, params, n, xyz, 0, sigma, rgb, raw, features, flag);
   return cudaGetLastError();
 }
@@ -694,6 +845,10 @@ cudaError_t launch_field_points(const FieldDesc& fd, const float* params, int n,
 cudaError_t launch_refresh_grid(const FieldDesc& fd, const float* params, int R, float* out, int* flag,
                                 cudaStream_t st) {
   const long long n = (long long)R * R * R;
+  cudaError_t e = cudaSuccess;
+  if (!getenv("PRENOM_GENERIC_FIELD") &&
+      field_points_fast(fd, params, (int)n, nullptr, R, out, nullptr, nullptr, nullptr, flag, st, &e))
+    return e;
   k_field_points<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(fd, params, (int)n, nullptr, R, out, nullptr, nullptr,
                                                               nullptr, flag);
   return cudaGetLastError();
