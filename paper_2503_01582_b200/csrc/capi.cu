@@ -146,6 +146,8 @@ struct prenom_ctx_s {
   cudaEvent_t fork_ev = nullptr;
   int64_t launches = 0;
   McMesh mc_dbg;  // prenom_debug_marching_cubes result
+  McScratch mc;   // extraction scratch shared by the context's objects
+  const void* mc_grid_owner = nullptr;  // object whose lattice mc.grid holds
   // optional per-kernel event timing
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -710,6 +712,7 @@ prenom_status prenom_object_destroy(prenom_object_t obj) {
   if (!obj) return PRENOM_OK;
   cudaSetDevice(obj->ctx->device);
   cudaStreamSynchronize(obj->ctx->stream);
+  if (obj->ctx->mc_grid_owner == obj) obj->ctx->mc_grid_owner = nullptr;
   delete obj;
   return PRENOM_OK;
 }
@@ -1000,8 +1003,9 @@ prenom_status prenom_extract_mesh(prenom_object_t o, int R, float iso, float iso
   CUDA_TRY(cudaSetDevice(o->ctx->device));
   cudaStream_t st = o->ctx->stream;
   const size_t n = (size_t)R * R * R;
-  McMesh& m = o->mesh;
+  McScratch& m = o->ctx->mc;
   CUDA_TRY(m.grid.ensure(n));
+  o->ctx->mc_grid_owner = nullptr;
   CUDA_TRY(launch_refresh_grid(o->fd, o->params.p, R, m.grid.p, o->flag.p, st));
   o->ctx->launches += 1;
   STATUS_TRY(check_flag(o));
@@ -1016,23 +1020,26 @@ prenom_status prenom_extract_mesh(prenom_object_t o, int R, float iso, float iso
     level = std::fmax(0.5f * mx, iso_floor);
   }
   int launches = 0;
-  m.R = R;
-  CUDA_TRY(run_marching_cubes(m.grid.p, R, level, m, st, &launches));
+  o->mesh.R = R;
+  o->ctx->mc_grid_owner = o;
+  CUDA_TRY(run_marching_cubes(m.grid.p, R, level, m, o->mesh, st, &launches));
   o->ctx->launches += launches;
   if (iso_used) *iso_used = level;
-  if (n_vertices) *n_vertices = m.n_vertices;
-  if (n_triangles) *n_triangles = m.n_triangles;
+  if (n_vertices) *n_vertices = o->mesh.n_vertices;
+  if (n_triangles) *n_triangles = o->mesh.n_triangles;
   return PRENOM_OK;
 }
 
 prenom_status prenom_get_mesh_grid(prenom_object_t o, int* res, float* grid) {
   if (!o || !res) return fail(PRENOM_USAGE, "NULL argument");
   if (o->mesh.R < 2) return fail(PRENOM_USAGE, "prenom_get_mesh_grid: no mesh extracted yet");
+  if (o->ctx->mc_grid_owner != o)
+    return fail(PRENOM_USAGE, "prenom_get_mesh_grid: the lattice was replaced by a later extraction on this context");
   CUDA_TRY(cudaSetDevice(o->ctx->device));
   *res = o->mesh.R;
   if (grid) {
     const size_t n = (size_t)o->mesh.R * o->mesh.R * o->mesh.R;
-    CUDA_TRY(cudaMemcpyAsync(grid, o->mesh.grid.p, n * sizeof(float), cudaMemcpyDeviceToHost, o->ctx->stream));
+    CUDA_TRY(cudaMemcpyAsync(grid, o->ctx->mc.grid.p, n * sizeof(float), cudaMemcpyDeviceToHost, o->ctx->stream));
     CUDA_TRY(cudaStreamSynchronize(o->ctx->stream));
   }
   return PRENOM_OK;
@@ -1056,15 +1063,16 @@ prenom_status prenom_debug_marching_cubes(prenom_ctx_t c, int R, const float* gr
   if (!c || !grid) return fail(PRENOM_USAGE, "NULL argument");
   if (R < 1 || R > 1024) return fail(PRENOM_DATA, "grid resolution out of range");
   CUDA_TRY(cudaSetDevice(c->device));
-  McMesh& m = c->mc_dbg;
+  McScratch& m = c->mc;
+  c->mc_grid_owner = nullptr;
   const size_t n = (size_t)R * R * R;
   CUDA_TRY(m.grid.ensure(n));
   CUDA_TRY(cudaMemcpyAsync(m.grid.p, grid, n * sizeof(float), cudaMemcpyHostToDevice, c->stream));
   int launches = 0;
-  CUDA_TRY(run_marching_cubes(m.grid.p, R, iso, m, c->stream, &launches));
+  CUDA_TRY(run_marching_cubes(m.grid.p, R, iso, m, c->mc_dbg, c->stream, &launches));
   c->launches += launches;
-  if (n_vertices) *n_vertices = m.n_vertices;
-  if (n_triangles) *n_triangles = m.n_triangles;
+  if (n_vertices) *n_vertices = c->mc_dbg.n_vertices;
+  if (n_triangles) *n_triangles = c->mc_dbg.n_triangles;
   return PRENOM_OK;
 }
 

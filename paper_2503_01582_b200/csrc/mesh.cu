@@ -454,9 +454,10 @@ cudaError_t launch_grid_max(const float* grid, long long n, float* d_out, cudaSt
   return cudaGetLastError();
 }
 
-// Marching cubes of an R^3 device grid into device buffers owned by `m`.
-cudaError_t run_marching_cubes(const float* d_grid, int R, float iso, McMesh& m, cudaStream_t st, int* launches) {
-  m.n_vertices = m.n_triangles = 0;
+// Marching cubes of an R^3 device grid (scratch `m`) into the mesh `out`.
+cudaError_t run_marching_cubes(const float* d_grid, int R, float iso, McScratch& m, McMesh& out, cudaStream_t st,
+                               int* launches) {
+  out.n_vertices = out.n_triangles = 0;
   if (R < 2) return cudaSuccess;
   cudaError_t e = upload_tables(st);
   if (e != cudaSuccess) return e;
@@ -498,11 +499,11 @@ cudaError_t run_marching_cubes(const float* d_grid, int R, float iso, McMesh& m,
   const unsigned gs = (unsigned)std::min<long long>((nslot + 255) / 256, 148 * 16);
   k_mc_mark<<<gs, 256, 0, st>>>(kept.p, nslot, first_use.p, mark.p);
   if ((e = scan_exclusive_u32(mark.p, nslot, vid.p, tmp, total.p, &nvert, st)) != cudaSuccess) return e;
-  if ((e = m.verts.ensure(3 * (size_t)nvert)) != cudaSuccess || (e = m.tris.ensure(nslot)) != cudaSuccess) return e;
-  k_mc_write<<<gs, 256, 0, st>>>(a, kept.p, nkept, first_use.p, mark.p, vid.p, m.verts.p, m.tris.p);
+  if ((e = out.verts.ensure(3 * (size_t)nvert)) != cudaSuccess || (e = out.tris.ensure(nslot)) != cudaSuccess) return e;
+  k_mc_write<<<gs, 256, 0, st>>>(a, kept.p, nkept, first_use.p, mark.p, vid.p, out.verts.p, out.tris.p);
   *launches += 6;
-  m.n_vertices = nvert;
-  m.n_triangles = nkept;
+  out.n_vertices = nvert;
+  out.n_triangles = nkept;
   return cudaGetLastError();
 }
 

@@ -351,13 +351,17 @@ struct MeshBuf {
     return e;
   }
 };
-// A mesh in the reference layout (mesh.hpp:12-17) on the device, plus the
-// extraction scratch (kept for re-use across calls on the same object).
+// A mesh in the reference layout (mesh.hpp:12-17) on the device (per object).
 struct McMesh {
   MeshBuf<float> verts;  // [n_vertices][3]
   MeshBuf<int> tris;     // [n_triangles][3]
   int64_t n_vertices = 0, n_triangles = 0;
-  int R = 0;  // lattice resolution of `grid` (prenom_extract_mesh)
+  int R = 0;  // lattice resolution of the last extraction
+};
+// Extraction scratch, one per context (extractions are stream-ordered):
+// the R^3 lattice, its max, and the count/emit/weld buffers (first_use is
+// 3 R^3 keys, 200 MB at R = 256 -- allocated once, not per object).
+struct McScratch {
   MeshBuf<uint32_t> block, tmp, keep, keep_off, first_use, mark, vid, total;
   MeshBuf<uint4> tri_keys, kept;
   MeshBuf<float> grid, gmax;
@@ -389,7 +393,8 @@ int mc_case_triangles(int config, int* edges);  // host table (marching_cubes.cp
 cudaError_t scan_exclusive_u32(const uint32_t* in, long long n, uint32_t* out, MeshBuf<uint32_t>& tmp,
                                uint32_t* d_total, uint32_t* h_total, cudaStream_t st);
 cudaError_t launch_grid_max(const float* grid, long long n, float* d_out, cudaStream_t st);
-cudaError_t run_marching_cubes(const float* d_grid, int R, float iso, McMesh& m, cudaStream_t st, int* launches);
+cudaError_t run_marching_cubes(const float* d_grid, int R, float iso, McScratch& m, McMesh& out, cudaStream_t st,
+                               int* launches);
 
 // bf16 tensor-core MLP path (kernels_tc.cu)
 bool tc_supported(const FieldDesc& fd);
