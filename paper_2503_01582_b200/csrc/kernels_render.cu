@@ -15,7 +15,7 @@ namespace prenom {
 namespace {
 
 constexpr int kWarps = 8;
-constexpr int kMaxChunk = 8;  // S <= 256
+constexpr int kMaxChunk = 8;  // S <= 256; a lane holds K = ceil(S/32) <= kMaxChunk samples
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -23,6 +23,9 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// K (samples per lane) is a template parameter so the per-lane arrays are
+// sized to the batch (S = 96 -> 3): registers, and so occupancy, follow S.
+template <int K>
 __global__ void __launch_bounds__(kWarps * 32) k_composite(CompositeArgs a, int frame) {
   __shared__ double red[kWarps][4];
   __shared__ unsigned long long red_n[kWarps];
@@ -34,13 +37,13 @@ __global__ void __launch_bounds__(kWarps * 32) k_composite(CompositeArgs a, int 
   if (r < a.B) {
     cnt = a.count[r];
     const size_t base = (size_t)r * a.S;
-    const int k = (a.S + 31) >> 5;
+    const int k = (a.S + 31) >> 5;  // <= K
     const int i0 = lane * k;
-    float sg[kMaxChunk], dl[kMaxChunk], dp[kMaxChunk], cr[kMaxChunk], cg[kMaxChunk], cb[kMaxChunk];
-    double av[kMaxChunk], tb[kMaxChunk], rho[kMaxChunk];
+    float sg[K], dl[K], dp[K], cr[K], cg[K], cb[K];
+    double av[K], tb[K], rho[K];
     double prod = 1.0;
 #pragma unroll
-    for (int j = 0; j < kMaxChunk; ++j) {
+    for (int j = 0; j < K; ++j) {
       const int i = i0 + j;
       sg[j] = dl[j] = dp[j] = cr[j] = cg[j] = cb[j] = 0.f;
       av[j] = 0.0;
@@ -67,7 +70,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_composite(CompositeArgs a, int 
     if (lane == 0) T = 1.0;
     double pc_r = 0.0, pc_g = 0.0, pc_b = 0.0, pd = 0.0;
 #pragma unroll
-    for (int j = 0; j < kMaxChunk; ++j) {
+    for (int j = 0; j < K; ++j) {
       tb[j] = T;
       rho[j] = av[j] * T;
       pc_r += rho[j] * cr[j];
@@ -122,15 +125,15 @@ __global__ void __launch_bounds__(kWarps * 32) k_composite(CompositeArgs a, int 
       if (bg) {
         double sd = 0.0;
 #pragma unroll
-        for (int j = 0; j < kMaxChunk; ++j) sd += (double)sg[j];
+        for (int j = 0; j < K; ++j) sd += (double)sg[j];
         t_sigma = warp_sum(sd);
       }
       if (a.dout) {
         // composite_backward (render.cpp:171-184)
-        double sv[kMaxChunk];
+        double sv[K];
         double q = 0.0;
 #pragma unroll
-        for (int j = 0; j < kMaxChunk; ++j) {
+        for (int j = 0; j < K; ++j) {
           sv[j] = (double)dc0 * cr[j] + (double)dc1 * cg[j] + (double)dc2 * cb[j] + (double)dd * dp[j];
           q += sv[j] * rho[j];
         }
@@ -143,7 +146,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_composite(CompositeArgs a, int 
         }
         double suffix = incl_s - q;
 #pragma unroll
-        for (int j = kMaxChunk - 1; j >= 0; --j) {
+        for (int j = K - 1; j >= 0; --j) {
           const int i = i0 + j;
           if (j < k && i < cnt) {
             const double denom = fmax(1.0 - av[j], 1e-300);
@@ -202,7 +205,17 @@ cudaError_t launch_composite(const CompositeArgs& a, cudaStream_t st) {
   if (a.B <= 0) return cudaSuccess;
   if (a.S > 32 * kMaxChunk) return cudaErrorInvalidValue;
   const int blocks = (a.B + kWarps - 1) / kWarps;
-  k_composite<<<blocks, kWarps * 32, 0, st>>>(a, a.frame);
+  const int k = (a.S + 31) >> 5;
+  if (k <= 1)
+    k_composite<1><<<blocks, kWarps * 32, 0, st>>>(a, a.frame);
+  else if (k <= 2)
+    k_composite<2><<<blocks, kWarps * 32, 0, st>>>(a, a.frame);
+  else if (k <= 3)
+    k_composite<3><<<blocks, kWarps * 32, 0, st>>>(a, a.frame);
+  else if (k <= 4)
+    k_composite<4><<<blocks, kWarps * 32, 0, st>>>(a, a.frame);
+  else
+    k_composite<kMaxChunk><<<blocks, kWarps * 32, 0, st>>>(a, a.frame);
   if (a.stats) k_finish_stats<<<1, 1, 0, st>>>(a.stats, a.lambda_d, a.lambda_sigma, a.flag);
   return cudaGetLastError();
 }
