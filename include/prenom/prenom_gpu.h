@@ -276,6 +276,12 @@ prenom_status prenom_get_mesh(prenom_object_t obj, float* vertices, int32_t* tri
  * bake_prior's grid (density_grid.cpp:138-143: refresh_grid then marching_cubes
  * of that grid). res receives R; grid may be NULL. */
 prenom_status prenom_get_mesh_grid(prenom_object_t obj, int* res, float* grid);
+/* Nearest-neighbour step of noma::chamfer (metrics.cpp:14-22; kd-tree
+ * nearest_distance, kdtree.cpp:64-92): min_sq[i] = min_j squared_norm(points[j]
+ * - queries[i]) in the reference's float arithmetic (exact minimum). The caller
+ * takes sqrt and the two sequential double means (paper_2503_01582_b200.metrics). */
+prenom_status prenom_nearest_sq(prenom_ctx_t ctx, int n_queries, const float* queries, int n_points,
+                                const float* points, float* min_sq);
 /* Batched noma::field_eval (field.cpp:219-225): n points in [0,1]^3. */
 prenom_status prenom_field_eval(prenom_object_t obj, int n, const float* xyz, float* sigma,
                                 float* rgb);

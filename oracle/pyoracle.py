@@ -415,6 +415,10 @@ class Ref(_Lib):
             "ref_save_prior": (C.c_int, [C.c_char_p, C.c_char_p, rarch, f32p, C.c_int, f32p, C.c_int64, f32p,
                                          C.c_int64, i32p, C.c_uint64, C.c_int, C.c_int, i32p, f32p]),
             "ref_prior_summary": (C.c_int, [C.c_char_p, C.c_char_p, C.c_int]),
+            "ref_iter_cost_model": (C.c_double, [rarch, C.c_int, C.c_int]),
+            "ref_sample_surface": (C.c_int, [C.c_int64, f32p, C.c_int64, i32p, C.c_int, C.c_uint64, f32p]),
+            "ref_transformed": (C.c_int, [C.c_int64, f32p, f32p, f32p, f32p]),
+            "ref_chamfer": (C.c_int, [C.c_int64, f32p, C.c_int64, f32p, f64p]),
             "ref_load_prior": (C.c_int, [C.c_char_p, rarch, i64p, f32p, f32p, f32p, i32p]),
             "ref_bake_prior": (C.c_int, [rarch, f32p, C.c_int, C.c_float, f32p, C.POINTER(C.c_int64),
                                          C.POINTER(C.c_int64)]),
@@ -643,6 +647,29 @@ class Ref(_Lib):
                     per_level_scale=a.per_level_scale, hidden_width=a.hidden_width, hidden_layers=a.hidden_layers,
                     density_activation=a.density_activation)
         return arch, th, g, v, t
+
+    # -- genome evaluation pieces (search.cpp:214-228, mesh.cpp:56-104, metrics.cpp:14-22)
+    def iter_cost_model(self, arch, rays_per_iter, samples_per_ray):
+        return float(self.lib.ref_iter_cost_model(C.byref(self._a(arch)), rays_per_iter, samples_per_ray))
+
+    def sample_surface(self, vertices, triangles, n, seed):
+        v = f32(vertices).reshape(-1, 3)
+        t = np.ascontiguousarray(triangles, np.int32).reshape(-1, 3)
+        out = zeros(n, 3)
+        self._check(self.lib.ref_sample_surface(len(v), fptr(v), len(t), iptr(t), n, seed, fptr(out)))
+        return out
+
+    def transformed(self, vertices, scale, t):
+        v = f32(vertices).reshape(-1, 3)
+        out = np.zeros_like(v)
+        self._check(self.lib.ref_transformed(len(v), fptr(v), fptr(f32(scale)), fptr(f32(t)), fptr(out)))
+        return out
+
+    def chamfer(self, a, b):
+        a, b = f32(a).reshape(-1, 3), f32(b).reshape(-1, 3)
+        out = np.zeros(1, np.float64)
+        self._check(self.lib.ref_chamfer(len(a), fptr(a), len(b), fptr(b), dptr(out)))
+        return float(out[0])
 
     def bake_prior(self, arch, params, R, iso):
         g = zeros(R, R, R)

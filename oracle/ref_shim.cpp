@@ -32,6 +32,8 @@
 #include "noma/marching_cubes.hpp"
 #include "noma/mesh.hpp"
 #include "noma/meta.hpp"
+#include "noma/metrics.hpp"
+#include "noma/search.hpp"
 #include "noma/prior_bundle.hpp"
 #include "noma/shapes.hpp"
 #include "noma/render.hpp"
@@ -604,6 +606,57 @@ int ref_bake_prior(const RefArch* a, const float* params, int R, float iso, floa
   g_ref_mesh = std::move(baked.mesh);
   *nv = (std::int64_t)g_ref_mesh.vertices.size();
   *nt = (std::int64_t)g_ref_mesh.triangles.size();
+  return 0;
+  REF_GUARD_END
+}
+
+// ---- genome evaluation pieces (search.cpp:214-228; mesh.cpp:70-104; metrics.cpp:14-22)
+double ref_iter_cost_model(const RefArch* a, int rays_per_iter, int samples_per_ray) {
+  InnerOptions inner;
+  inner.rays_per_iter = rays_per_iter;
+  inner.samples_per_ray = samples_per_ray;
+  return iter_cost_model(to_arch(a), inner);
+}
+
+static Mesh make_mesh(std::int64_t nv, const float* verts, std::int64_t nt, const int* tris) {
+  Mesh m;
+  m.vertices.resize((std::size_t)nv);
+  for (std::int64_t i = 0; i < nv; ++i) m.vertices[i] = {verts[3 * i], verts[3 * i + 1], verts[3 * i + 2]};
+  m.triangles.resize((std::size_t)nt);
+  for (std::int64_t i = 0; i < nt; ++i) m.triangles[i] = {tris[3 * i], tris[3 * i + 1], tris[3 * i + 2]};
+  return m;
+}
+
+int ref_sample_surface(std::int64_t nv, const float* verts, std::int64_t nt, const int* tris, int n,
+                       std::uint64_t seed, float* out) {
+  REF_GUARD_BEGIN
+  const auto pts = sample_surface(make_mesh(nv, verts, nt, tris), n, seed);
+  for (std::size_t i = 0; i < pts.size(); ++i) {
+    out[3 * i] = pts[i].x, out[3 * i + 1] = pts[i].y, out[3 * i + 2] = pts[i].z;
+  }
+  return 0;
+  REF_GUARD_END
+}
+
+int ref_transformed(std::int64_t nv, const float* verts, const float* scale, const float* t, float* out) {
+  REF_GUARD_BEGIN
+  Mesh m = make_mesh(nv, verts, 0, nullptr);
+  Pose pose{};
+  pose.t = {t[0], t[1], t[2]};
+  const Mesh r = transformed(m, {scale[0], scale[1], scale[2]}, pose);
+  for (std::size_t i = 0; i < r.vertices.size(); ++i) {
+    out[3 * i] = r.vertices[i].x, out[3 * i + 1] = r.vertices[i].y, out[3 * i + 2] = r.vertices[i].z;
+  }
+  return 0;
+  REF_GUARD_END
+}
+
+int ref_chamfer(std::int64_t na, const float* a, std::int64_t nb, const float* b, double* out) {
+  REF_GUARD_BEGIN
+  std::vector<Vec3> pa((std::size_t)na), pb((std::size_t)nb);
+  for (std::int64_t i = 0; i < na; ++i) pa[i] = {a[3 * i], a[3 * i + 1], a[3 * i + 2]};
+  for (std::int64_t i = 0; i < nb; ++i) pb[i] = {b[3 * i], b[3 * i + 1], b[3 * i + 2]};
+  *out = chamfer(pa, pb);
   return 0;
   REF_GUARD_END
 }

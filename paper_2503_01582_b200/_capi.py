@@ -141,7 +141,7 @@ EXPORTED = [
     "prenom_object_upload_frame", "prenom_object_synth_frames", "prenom_object_get_frame", "prenom_train_step", "prenom_object_last_stats",
     "prenom_train_step_async", "prenom_wait_stats", "prenom_object_frame_at",
     "prenom_object_step", "prenom_object_check",
-    "prenom_render", "prenom_density_query", "prenom_extract_mesh", "prenom_get_mesh", "prenom_get_mesh_grid", "prenom_field_eval",
+    "prenom_render", "prenom_density_query", "prenom_extract_mesh", "prenom_get_mesh", "prenom_get_mesh_grid", "prenom_nearest_sq", "prenom_field_eval",
     "prenom_get_params", "prenom_set_params", "prenom_get_grid", "prenom_set_grid",
     "prenom_get_adam", "prenom_reset_adam", "prenom_train_step_many",
     "prenom_reptile_delta", "prenom_reptile_apply", "prenom_object_copy_params", "prenom_reptile_update",
@@ -214,6 +214,7 @@ def _declare(lib):
         "prenom_extract_mesh": (i32, [P, i32, C.c_float, C.c_float, f32p, i64p, i64p]),
         "prenom_get_mesh": (i32, [P, f32p, i32p]),
         "prenom_get_mesh_grid": (i32, [P, i32p, f32p]),
+        "prenom_nearest_sq": (i32, [P, i32, f32p, i32, f32p, f32p]),
         "prenom_field_eval": (i32, [P, i32, f32p, f32p, f32p]),
         "prenom_get_params": (i32, [P, f32p]),
         "prenom_set_params": (i32, [P, f32p]),

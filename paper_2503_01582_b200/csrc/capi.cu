@@ -1095,6 +1095,27 @@ int prenom_mc_case_triangles(int config, int* edges) {
   return mc_case_triangles(config, edges);
 }
 
+// metrics.cpp:14-22's nearest-neighbour step (kernels_metrics.cu): per query,
+// the exact minimum squared distance to the cloud.
+prenom_status prenom_nearest_sq(prenom_ctx_t c, int n_queries, const float* queries, int n_points,
+                                const float* points, float* min_sq) {
+  if (!c || (n_queries > 0 && (!queries || !min_sq)) || (n_points > 0 && !points))
+    return fail(PRENOM_USAGE, "NULL argument");
+  if (n_queries < 0 || n_points < 1) return fail(PRENOM_DATA, "nearest_sq: empty cloud");
+  CUDA_TRY(cudaSetDevice(c->device));
+  DevBuf<float> dq, dp, dout;
+  CUDA_TRY(dq.ensure(3 * (size_t)n_queries));
+  CUDA_TRY(dp.ensure(3 * (size_t)n_points));
+  CUDA_TRY(dout.ensure((size_t)n_queries));
+  CUDA_TRY(cudaMemcpyAsync(dq.p, queries, 12 * (size_t)n_queries, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(dp.p, points, 12 * (size_t)n_points, cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(launch_nearest_sq(n_queries, dq.p, n_points, dp.p, dout.p, c->stream));
+  c->launches += 1;
+  CUDA_TRY(cudaMemcpyAsync(min_sq, dout.p, 4 * (size_t)n_queries, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return PRENOM_OK;
+}
+
 prenom_status prenom_field_eval(prenom_object_t o, int n, const float* xyz, float* sigma, float* rgb) {
   if (!o || !xyz) return fail(PRENOM_USAGE, "NULL argument");
   if (n < 0) return fail(PRENOM_USAGE, "n < 0");

@@ -393,6 +393,7 @@ int mc_case_triangles(int config, int* edges);  // host table (marching_cubes.cp
 cudaError_t scan_exclusive_u32(const uint32_t* in, long long n, uint32_t* out, MeshBuf<uint32_t>& tmp,
                                uint32_t* d_total, uint32_t* h_total, cudaStream_t st);
 cudaError_t launch_grid_max(const float* grid, long long n, float* d_out, cudaStream_t st);
+cudaError_t launch_nearest_sq(int nq, const float* q, int np, const float* p, float* out, cudaStream_t st);
 cudaError_t run_marching_cubes(const float* d_grid, int R, float iso, McScratch& m, McMesh& out, cudaStream_t st,
                                int* launches);
 

@@ -137,6 +137,22 @@ def box_union_scene(n_views=50, res=256, cam_radius=1.5, fx=None, depth_noise=0.
                  np.full(3, -0.5, np.float32), np.full(3, 0.5, np.float32), Pose(), boxes)
 
 
+def box_union_mesh(boxes):
+    """Ground-truth surface of a box union for the genome evaluation's Chamfer metric:
+    every box's 12 outward triangles (faces inside other boxes are kept -- a
+    surface-sampling target, not a watertight union). Returns (vertices [8n,3], triangles [12n,3])."""
+    verts, tris = [], []
+    quads = [(0, 2, 3, 1), (4, 5, 7, 6), (0, 1, 5, 4), (2, 6, 7, 3), (0, 4, 6, 2), (1, 3, 7, 5)]
+    for b, (lo, hi, _) in enumerate(boxes):
+        base = 8 * b
+        for k in range(8):
+            verts.append([hi[0] if k & 1 else lo[0], hi[1] if k & 2 else lo[1], hi[2] if k & 4 else lo[2]])
+        for a, c, d, e in quads:
+            tris.append([base + a, base + c, base + d])
+            tris.append([base + a, base + d, base + e])
+    return np.asarray(verts, np.float32), np.asarray(tris, np.int32)
+
+
 def occupancy_prior(boxes, R=32, box_min=-0.5, box_max=0.5, dilate=1, blur=1, k=SIGMA_PRIOR_SCALE):
     """sigma-valued R^3 prior grid = k * blur(dilate(occupancy)) at vertices
     (i,j,k)/(R-1) of the normalised box, x-fastest (density_grid.hpp:15-35)."""
