@@ -566,7 +566,7 @@ def run_ours(args):
         losses.append(st["total"])
         e_end.record(stream)
         ctx.synchronize()
-        e2e = dict(ms=e_start.elapsed_time(e_end), samples=e_samples, h2d=h2d // args.e2e_steps, d2h=52)  # stats + flag
+        e2e = dict(ms=e_start.elapsed_time(e_end), samples=e_samples, h2d=h2d // args.e2e_steps, d2h=60)  # StepStatsDev (56 B) + flag
 
     # aggregate over ranks: max time, summed samples
     t_dev = ms / 1e3

@@ -269,7 +269,10 @@ prenom_status ensure_scratch(prenom_object_s* o, int B, int S) {
   CUDA_TRY(o->dout.ensure(Npad));
   if (o->cfg.mlp_precision == PRENOM_MLP_BF16) {
     CUDA_TRY(o->feat_tc.ensure(tc_feature_bytes(o->fd, (long long)N)));
-    CUDA_TRY(o->tile_ctr.ensure(2));
+    if (!o->tile_ctr.p) {  // [fwd next, fwd done (self-resetting), bwd next (memset per launch), -]
+      CUDA_TRY(o->tile_ctr.ensure(4));
+      CUDA_TRY(cudaMemset(o->tile_ctr.p, 0, 4 * sizeof(int)));
+    }
   } else {
     CUDA_TRY(o->feat_t.ensure(Npad * o->fd.in_dim));
     CUDA_TRY(o->dfeat_t.ensure(Npad * o->fd.in_dim));
@@ -418,7 +421,7 @@ prenom_status enqueue_step(prenom_object_s* o, StepStatsDev* stats, bool has_nex
   if (tc) {
     ProfScope ps(o->ctx, PRENOM_K_MLP_BWD, st);  // MLP backward + fused table-gradient scatter
     CUDA_TRY(launch_bwd_tc(o->fd, o->params.p, o->grad.p, (long long)B * S, S, sb.count, sb.pos_depth,
-                           o->feat_tc.p, o->dout.p, o->tile_ctr.p + 1, st));
+                           o->feat_tc.p, o->dout.p, o->tile_ctr.p + 2, st));
   } else {
     {
       ProfScope ps(o->ctx, PRENOM_K_MLP_BWD, st);
@@ -451,7 +454,7 @@ prenom_status enqueue_step(prenom_object_s* o, StepStatsDev* stats, bool has_nex
     CUDA_TRY(launch_adam(o->P, o->params.p, o->grad.p, o->m.p, o->v.p, c.eta, c.adam_beta1, c.adam_beta2,
                          c.adam_eps, c1, c2, 1, st));
   }
-  o->ctx->launches += tc ? 6 : 7;
+  o->ctx->launches += tc ? 5 : 6;  // sample, fwd, composite, bwd (+ encode_bwd), adam
   o->step += 1;
   // grid refresh every m iterations (mapper.cpp:182-183)
   if (c.grid_refresh_every > 0 && o->step % c.grid_refresh_every == 0) {
@@ -1356,7 +1359,8 @@ struct PointBatch {
     CUDA_TRY(dout.ensure(npad));
     CUDA_TRY(count.ensure(n));
     CUDA_TRY(flag.ensure(1));
-    CUDA_TRY(ctr.ensure(2));
+    CUDA_TRY(ctr.ensure(4));
+    CUDA_TRY(cudaMemset(ctr.p, 0, 4 * sizeof(int)));
     CUDA_TRY(cudaMemsetAsync(flag.p, 0, sizeof(int), st));
     CUDA_TRY(cudaMemcpyAsync(params.p, h_params, P * sizeof(float), cudaMemcpyHostToDevice, st));
     std::vector<float4> hp(n);
@@ -1458,7 +1462,7 @@ prenom_status prenom_debug_field_backward(prenom_ctx_t ctx, const prenom_field_a
     CUDA_TRY(launch_fwd_tc(fd, pb.params.p, n, 1, pb.count.p, pb.pos.p, pb.feat_tc.p, pb.out.p, pb.flag.p, pb.ctr.p,
                            st));
     CUDA_TRY(launch_bwd_tc(fd, pb.params.p, pb.grad.p, n, 1, pb.count.p, pb.pos.p, pb.feat_tc.p, pb.dout.p,
-                           pb.ctr.p + 1, st));
+                           pb.ctr.p + 2, st));
   } else {
     CUDA_TRY(launch_field_fwd_train(fd, pb.params.p, n, 1, pb.sb, pb.feat_t.p, pb.out.p, pb.flag.p, st));
     CUDA_TRY(launch_mlp_bwd_train(fd, pb.params.p, pb.grad.p, n, 1, pb.count.p, pb.feat_t.p, pb.dout.p,

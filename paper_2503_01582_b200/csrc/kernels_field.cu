@@ -673,6 +673,7 @@ __device__ __forceinline__ void adam1(float& p, float& g, float& m, float& v, fl
 __global__ void __launch_bounds__(256) k_adam(size_t n, float* __restrict__ p, float* __restrict__ g,
                                               float* __restrict__ m, float* __restrict__ v, float lr, float b1,
                                               float b2, float eps, float c1, float c2, int zero_grad) {
+  pdl_wait();  // the backward's gradient
   const size_t n4 = n / 4;
   const size_t stride = (size_t)gridDim.x * blockDim.x;
   // two float4 groups per thread per iteration: 8 independent 16 B loads in flight
@@ -872,8 +873,7 @@ cudaError_t launch_adam(size_t n, float* p, float* g, float* m, float* v, float 
                         float c1, float c2, int zero_grad, cudaStream_t st) {
   const size_t n4 = std::max<size_t>(n / 4, 1);
   const unsigned grid = (unsigned)std::min<size_t>((n4 + 255) / 256, (size_t)num_sms() * 8);
-  k_adam<<<grid, 256, 0, st>>>(n, p, g, m, v, lr, b1, b2, eps, c1, c2, zero_grad);
-  return cudaGetLastError();
+  return launch_pdl(k_adam, dim3(grid), dim3(256), 0, st, n, p, g, m, v, lr, b1, b2, eps, c1, c2, zero_grad);
 }
 
 cudaError_t launch_init_params(const FieldDesc& fd, float* params, uint64_t seed, cudaStream_t st) {

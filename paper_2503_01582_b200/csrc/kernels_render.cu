@@ -32,6 +32,8 @@ __global__ void __launch_bounds__(kWarps * 32) k_composite(CompositeArgs a, int 
   __shared__ int red_e[kWarps];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = blockIdx.x * kWarps + warp;
+  pdl_wait();  // field outputs of the forward kernel
+  pdl_trigger();
   double t_color = 0.0, t_depth = 0.0, t_sigma = 0.0;
   int cnt = 0;
   if (r < a.B) {
@@ -189,14 +191,19 @@ __global__ void __launch_bounds__(kWarps * 32) k_composite(CompositeArgs a, int 
       atomicAdd(&a.stats->n_samples, n);
       atomicAdd(&a.stats->escaped, e);
       if (blockIdx.x == 0) a.stats->frame = frame;
+      // the last block to finish forms the total (render.cpp:238-240):
+      // total = color + lambda_d * depth + lambda_sigma * sigma
+      __threadfence();
+      if (atomicAdd(&a.stats->blocks_done, 1u) == gridDim.x - 1) {
+        __threadfence();
+        StepStatsDev* st = a.stats;
+        const double cc = atomicAdd(&st->color, 0.0), dd = atomicAdd(&st->depth, 0.0),
+                     ss = atomicAdd(&st->sigma, 0.0);
+        st->total = cc + (double)a.lambda_d * dd + (double)a.lambda_sigma * ss;
+        if (!isfinite(st->total) && a.flag) atomicOr(a.flag, 2);
+      }
     }
   }
-}
-
-// total = color + lambda_d * depth + lambda_sigma * sigma (render.cpp:238-240)
-__global__ void k_finish_stats(StepStatsDev* s, float lambda_d, float lambda_sigma, int* flag) {
-  s->total = s->color + (double)lambda_d * s->depth + (double)lambda_sigma * s->sigma;
-  if (!isfinite(s->total) && flag) atomicOr(flag, 2);
 }
 
 }  // namespace
@@ -206,18 +213,12 @@ cudaError_t launch_composite(const CompositeArgs& a, cudaStream_t st) {
   if (a.S > 32 * kMaxChunk) return cudaErrorInvalidValue;
   const int blocks = (a.B + kWarps - 1) / kWarps;
   const int k = (a.S + 31) >> 5;
-  if (k <= 1)
-    k_composite<1><<<blocks, kWarps * 32, 0, st>>>(a, a.frame);
-  else if (k <= 2)
-    k_composite<2><<<blocks, kWarps * 32, 0, st>>>(a, a.frame);
-  else if (k <= 3)
-    k_composite<3><<<blocks, kWarps * 32, 0, st>>>(a, a.frame);
-  else if (k <= 4)
-    k_composite<4><<<blocks, kWarps * 32, 0, st>>>(a, a.frame);
-  else
-    k_composite<kMaxChunk><<<blocks, kWarps * 32, 0, st>>>(a, a.frame);
-  if (a.stats) k_finish_stats<<<1, 1, 0, st>>>(a.stats, a.lambda_d, a.lambda_sigma, a.flag);
-  return cudaGetLastError();
+  const dim3 g(blocks), b(kWarps * 32);
+  if (k <= 1) return launch_pdl(k_composite<1>, g, b, 0, st, a, a.frame);
+  if (k <= 2) return launch_pdl(k_composite<2>, g, b, 0, st, a, a.frame);
+  if (k <= 3) return launch_pdl(k_composite<3>, g, b, 0, st, a, a.frame);
+  if (k <= 4) return launch_pdl(k_composite<4>, g, b, 0, st, a, a.frame);
+  return launch_pdl(k_composite<kMaxChunk>, g, b, 0, st, a, a.frame);
 }
 
 }  // namespace prenom

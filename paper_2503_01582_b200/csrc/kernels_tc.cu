@@ -158,6 +158,7 @@ __global__ void __launch_bounds__(NT) k_fwd_tc(FieldDesc fd, const float* __rest
   // l+1's epilogue overwrites the tile it read
   unsigned char* Hb = p;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  pdl_wait();  // params come from the previous step's Adam
   wt.load(fd, params + fd.hash_params, NT);
   constexpr int TPS = NT / 128;  // threads per sample
   for (int i = tid; i < 128 * INP; i += NT) reinterpret_cast<__nv_bfloat16*>(X)[i] = __float2bfloat16_rn(0.f);
@@ -249,6 +250,9 @@ __global__ void __launch_bounds__(NT) k_fwd_tc(FieldDesc fd, const float* __rest
     }
     umma::fence_before_sync();
   }
+#ifndef PRENOM_VAR_FWD_MEMSET
+  tile_sched_exit(tile_ctr);
+#endif
   __syncthreads();
   if (warp == 0) umma::tmem_dealloc(tm, 64);
 }
@@ -400,6 +404,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
   umma::fence_after_sync();
   const uint32_t tm = tbase;
   const long long ntiles = (n_total + kTile - 1) / kTile;
+  pdl_wait();  // (PDL) the prologue above may overlap the compositing kernel; dout / features from here on
 
   if (warp >= kMlpThreads / 32) {
     // ================= scatter warps: d_features -> table gradient
@@ -643,11 +648,12 @@ cudaError_t run_fwd_nt(const FieldDesc& fd, const float* params, long long n, in
   if (e != cudaSuccess) return e;
   const long long ntiles = (n + kTile - 1) / kTile;
   const long long grid = std::min<long long>(ntiles, (long long)ctas * sms());
+#ifdef PRENOM_VAR_FWD_MEMSET
   e = cudaMemsetAsync(tile_ctr, 0, sizeof(int), st);
   if (e != cudaSuccess) return e;
-  k_fwd_tc<INP, W, H, NT><<<(unsigned)grid, NT, smem, st>>>(fd, params, n, S, count, pos,
-                                                            reinterpret_cast<uint4*>(feat_tiles), out, flag, tile_ctr);
-  return cudaGetLastError();
+#endif
+  return launch_pdl(k_fwd_tc<INP, W, H, NT>, dim3((unsigned)grid), dim3(NT), smem, st, fd, params, n, S, count, pos,
+                    reinterpret_cast<uint4*>(feat_tiles), out, flag, tile_ctr);
 }
 
 template <int INP, int W, int H>
@@ -689,13 +695,11 @@ cudaError_t run_bwd(const FieldDesc& fd, const float* params, float* grad, long 
     return v ? atoi(v) : -1;
   }();
   const int mlp_levels = std::max(0, std::min(INP / 4, mlp_env >= 0 ? mlp_env : kBwdMlpLevels));
-  e = cudaMemsetAsync(tile_ctr, 0, sizeof(int), st);
-  if (e != cudaSuccess) return e;
-  k_bwd_tc<INP, W, H><<<(unsigned)grid, kBwdThreads, smem, st>>>(fd, params, grad, n, S, count, pos,
-                                                              reinterpret_cast<const uint4*>(feat_tiles), dout, tile_ctr,
-                                                              getenv("PRENOM_PROF_SKIP_SCATTER") ? atoi(getenv("PRENOM_PROF_SKIP_SCATTER")) : 0,
-                                                              mlp_levels);
-  return cudaGetLastError();
+  static const int skip = getenv("PRENOM_PROF_SKIP_SCATTER") ? atoi(getenv("PRENOM_PROF_SKIP_SCATTER")) : 0;
+  cudaError_t em = cudaMemsetAsync(tile_ctr, 0, sizeof(int), st);
+  if (em != cudaSuccess) return em;
+  return launch_pdl(k_bwd_tc<INP, W, H>, dim3((unsigned)grid), dim3(kBwdThreads), smem, st, fd, params, grad, n, S,
+                    count, pos, reinterpret_cast<const uint4*>(feat_tiles), dout, tile_ctr, skip, mlp_levels);
 }
 
 #define PRENOM_TC_DISPATCH(FN, ...)                                                          \
@@ -713,6 +717,13 @@ cudaError_t run_bwd(const FieldDesc& fd, const float* params, float* grad, long 
   } while (0)
 
 }  // namespace
+
+// On by default (cfg2, B200, interleaved 3x: 0.7001 -> 0.6940 ms/step);
+// PRENOM_NO_PDL=1 disables for A/B.
+bool pdl_enabled() {
+  static const bool on = getenv("PRENOM_NO_PDL") == nullptr;
+  return on;
+}
 
 bool tc_supported(const FieldDesc& fd) {
   for (int l = 0; l < fd.L; ++l)

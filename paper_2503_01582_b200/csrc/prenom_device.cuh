@@ -41,7 +41,49 @@ struct StepStatsDev {
   unsigned long long n_samples;
   int escaped;
   int frame;
+  unsigned int blocks_done;  // k_composite's last block finishes the step's totals
+  int pad_;
 };
+
+// Persistent-kernel tile scheduler counters [next tile, CTAs done] of the
+// forward: the last CTA to leave resets both, so the forward needs no memset
+// node in front of it. (Applied to the backward too, the same self-reset made
+// k_bwd_tc 2.5x slower -- unexplained, measured -- so it keeps its memset.)
+__device__ __forceinline__ void tile_sched_exit(int* ctr) {
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(ctr + 1, 1) == (int)gridDim.x - 1) {
+      ctr[0] = 0;
+      ctr[1] = 0;
+    }
+  }
+}
+
+// ---- programmatic dependent launch (PDL) between the step's kernels.
+// A dependent kernel may start (prologue: smem carve, weight tiles, TMEM
+// alloc, barriers) while its predecessor drains; griddepcontrol.wait then
+// blocks until the predecessor grid has completed and its writes are
+// visible, so every read of predecessor outputs sits after pdl_wait().
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+bool pdl_enabled();  // PRENOM_NO_PDL=1 disables (A/B)
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 
 // Ray-sample buffers of one batch: B rays x S slots.
 struct SampleBufs {
