@@ -172,3 +172,48 @@ def test_cfg2_train_step_batch_properties(ctx, cfg2_scene):
         assert abs(x["total"] - y["total"]) <= 1e-3 * abs(y["total"])
     a.close()
     b.close()
+
+
+def _pair(ctx, oracle, arch, cfg, sc, grid, seed):
+    rng = np.random.default_rng(seed)
+    P, nh = arch.param_count(), arch.hash_param_count()
+    theta = np.empty(P, np.float32)
+    theta[:nh] = rng.uniform(-1e-4, 1e-4, nh)  # BASELINE: tables U(-1e-4, 1e-4)
+    theta[nh:] = (rng.standard_normal(P - nh) * 0.2).astype(np.float32)
+    R = grid.shape[0] if grid is not None else 8
+    gpu = ObjectTrainer.create(ctx, arch, theta=theta, grid=grid, grid_res=R, seed=seed, cfg=cfg,
+                               box_min=sc.box_min, box_max=sc.box_max)
+    gpu.set_frames(sc.cams, sc.rgb, sc.depth, sc.mask, 1, sc.obj_pose)
+    g = grid if grid is not None else np.zeros((R, R, R), np.float32)
+    ob = oracle.object_create(arch, theta, g, R, seed, cfg.to_c(), sc.box_min, sc.box_max)
+    ob.set_frames(sc.cams, sc.rgb, sc.depth, sc.mask, 1, sc.obj_pose)
+    return gpu, ob
+
+
+def test_cfg1_full_size_first_steps_loss(ctx, oracle):
+    """BASELINE cfg1 at full size (sphere, 24 views 128^2, L8 T2^15 W32 H2, 4096 rays x 64
+    midpoints, fp32 MLP): the first three steps' loss terms vs the oracle (same Philox draws)."""
+    sc = scenes.sphere_scene()
+    arch = scenes.cfg1_arch()
+    cfg = TrainConfig(rays_per_iter=4096, samples_per_ray=64, prior_sampling=0, grid_refresh_every=0)
+    gpu, ob = _pair(ctx, oracle, arch, cfg, sc, None, seed=0)
+    sg, so = gpu.train_step(3), ob.train_step(3)
+    for i, (x, y) in enumerate(zip(sg, so)):
+        assert x["frame"] == y["frame"] and x["n_samples"] == y["n_samples"] and x["escaped"] == y["escaped"]
+        tol = 1e-5 if i == 0 else 1e-4  # later steps follow Adam updates of atomically summed gradients
+        for k in ("total", "color", "depth", "sigma"):
+            assert abs(x[k] - y[k]) <= tol * abs(y[k]) + 1e-9, (i, k, x, y)
+
+
+def test_cfg2_full_size_first_step_loss_fp32(ctx, oracle, cfg2_scene):
+    """BASELINE cfg2 at full size in the fp32 MLP mode (8192 rays, 32 -> 96 prior samples,
+    L16 T2^19 W64 H2): first-step loss terms within 1e-5 of the oracle."""
+    sc, grid = cfg2_scene
+    arch = scenes.cfg2_arch(64)
+    cfg = TrainConfig(rays_per_iter=B, samples_per_ray=S, coarse_samples=NC, prior_sampling=1, grid_refresh_every=0)
+    gpu, ob = _pair(ctx, oracle, arch, cfg, sc, grid, seed=1)
+    x, y = gpu.train_step(1)[0], ob.train_step(1)[0]
+    assert x["frame"] == y["frame"] and x["n_samples"] == y["n_samples"] and x["escaped"] == y["escaped"]
+    assert x["n_samples"] > N // 2
+    for k in ("total", "color", "depth", "sigma"):
+        assert abs(x[k] - y[k]) <= 1e-5 * abs(y[k]) + 1e-9, (k, x, y)
