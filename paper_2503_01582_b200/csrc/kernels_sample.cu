@@ -90,6 +90,55 @@ __device__ __forceinline__ float uniform_depth(float t0, float step, int i) {
   return __fadd_rn(t0, __fmul_rn(__fadd_rn((float)i, 0.5f), step));
 }
 
+// Bitonic sort (ascending) of the warp's p2 = 32*E slots held in registers,
+// slot i = lane*E + e: partners j < E are in the same lane, j >= E one
+// shuffle away (lane ^ j/E). The sorted multiset is unique, so the result is
+// the one std::sort gives (density_grid.cpp:96).
+template <int E>
+__device__ __forceinline__ void warp_bitonic_sort(float (&v)[E], int lane) {
+  constexpr int n = 32 * E;
+#pragma unroll
+  for (int k = 2; k <= n; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j < E) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int f = e ^ j;
+          if (f > e) {
+            const bool up = ((lane * E + e) & k) == 0;
+            const float a = v[e], b = v[f];
+            if ((a > b) == up) {
+              v[e] = b;
+              v[f] = a;
+            }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int i = lane * E + e;
+          const float p = __shfl_xor_sync(0xffffffffu, v[e], j / E);
+          const bool want_min = ((i & j) == 0) == ((i & k) == 0);
+          v[e] = want_min ? fminf(v[e], p) : fmaxf(v[e], p);
+        }
+      }
+    }
+  }
+}
+
+template <int E>
+__device__ __forceinline__ void sort_slots(float* SORT, int lane) {
+  float v[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) v[e] = SORT[lane * E + e];
+  __syncwarp();
+  warp_bitonic_sort<E>(v, lane);
+#pragma unroll
+  for (int e = 0; e < E; ++e) SORT[lane * E + e] = v[e];
+  __syncwarp();
+}
+
 __global__ void __launch_bounds__(kWarpsPerBlock * 32)
     k_sample(RaySource src, SamplerCfg cfg, SampleBufs out, int nc_cap, int p2) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -257,21 +306,32 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
   }
   for (int s = S + lane; s < p2; s += 32) SORT[s] = INFINITY;
   __syncwarp();
-  // std::sort: bitonic network over p2 slots (the sorted multiset is unique).
-  for (int k = 2; k <= p2; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = lane; i < p2; i += 32) {
-        const int ixj = i ^ j;
-        if (ixj > i) {
-          const float a = SORT[i], b = SORT[ixj];
-          const bool up = (i & k) == 0;
-          if ((a > b) == up) {
-            SORT[i] = b;
-            SORT[ixj] = a;
+  // std::sort: bitonic network over p2 slots (the sorted multiset is unique),
+  // in registers + shuffles for p2 <= 256, else through shared memory.
+  if (p2 == 32) {
+    sort_slots<1>(SORT, lane);
+  } else if (p2 == 64) {
+    sort_slots<2>(SORT, lane);
+  } else if (p2 == 128) {
+    sort_slots<4>(SORT, lane);
+  } else if (p2 == 256) {
+    sort_slots<8>(SORT, lane);
+  } else {
+    for (int k = 2; k <= p2; k <<= 1) {
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int i = lane; i < p2; i += 32) {
+          const int ixj = i ^ j;
+          if (ixj > i) {
+            const float a = SORT[i], b = SORT[ixj];
+            const bool up = (i & k) == 0;
+            if ((a > b) == up) {
+              SORT[i] = b;
+              SORT[ixj] = a;
+            }
           }
         }
+        __syncwarp();
       }
-      __syncwarp();
     }
   }
   // strictly increasing fix-up (density_grid.cpp:97-98), sequential when needed
