@@ -259,18 +259,31 @@ __global__ void __launch_bounds__(NT) k_fwd_tc(FieldDesc fd, const float* __rest
 
 // One level of the table-gradient scatter for the 32 consecutive samples of a
 // warp (field.cpp:279-292). Samples of a ray are depth-sorted and a line
-// enters each cell once, so equal (ray, cell) keys form contiguous lane runs:
-// a segmented suffix sum leaves each run's total in its first lane, which
-// alone issues the 8 corner atomics (de-duplicated scatter).
+// enters each cell once, so equal cells form contiguous lane runs; each run's
+// total is formed in its first lane, which alone issues the 8 corner atomics
+// (de-duplicated scatter). Equal consecutive cells of different rays merge
+// too (same rows, same sum), so the key is the cell alone.
+// Two ways to form the run totals, chosen per level from the longest run R:
+//  * R <= pull_max: the head pulls each later member's (fx, fy, fz, d0, d1)
+//    -- 5 shuffles per member -- and accumulates w * d itself (ALU work);
+//  * else a segmented tree over the 16 corner products, 16 shuffles per
+//    round, log2(R) rounds.
+// Shuffles share the LSU pipe with the atomics, which bounds this kernel, so
+// the short runs of the fine levels go the pull way.
 __device__ __forceinline__ void scatter_level(const FieldDesc& fd, float* __restrict__ grad, int l, bool valid,
-                                              float px, float py, float pz, unsigned long long ray_key, float dx,
-                                              float dy, int lane, int skip) {
-  const LevelCell cell = level_cell(fd.res[l], px, py, pz);
-  const unsigned long long key =
-      valid ? (ray_key | ((unsigned long long)(cell.cz & 4095) << 24) | ((unsigned long long)(cell.cy & 4095) << 12) |
-               (unsigned long long)(cell.cx & 4095))
-            : (~0ull - (unsigned long long)lane);
+                                              float px, float py, float pz, float dx, float dy, int lane, int skip,
+                                              int pull_max) {
+  const int res = fd.res[l];
+  const LevelCell cell = level_cell(res, px, py, pz);
+  const uint32_t key = valid ? ((uint32_t)cell.cz * (uint32_t)res + (uint32_t)cell.cy) * (uint32_t)res + (uint32_t)cell.cx
+                             : 0xFFFFFFFFu - (uint32_t)lane;
   const float d0 = valid ? dx : 0.f, d1 = valid ? dy : 0.f;
+  const uint32_t pk = __shfl_up_sync(0xffffffffu, key, 1);
+  const bool head = lane == 0 || pk != key;
+  const uint32_t heads = __ballot_sync(0xffffffffu, head);
+  const uint32_t above = heads & ~((2u << lane) - 1u);  // heads strictly above this lane
+  const int rlen = head ? (above ? __ffs(above) - 1 : 32) - lane : 0;
+  const int rmax = __reduce_max_sync(0xffffffffu, (unsigned)rlen);
   float w[8], c[16];
   corner_weights(cell, w);
 #pragma unroll
@@ -278,20 +291,38 @@ __device__ __forceinline__ void scatter_level(const FieldDesc& fd, float* __rest
     c[2 * corner] = w[corner] * d0;
     c[2 * corner + 1] = w[corner] * d1;
   }
-  // runs are contiguous: once no run is longer than `off`, no larger offset
-  // can match, so fine levels (runs of 1) skip all value shuffles
-  for (int off = 1; off < 32; off <<= 1) {
-    const unsigned long long ok = __shfl_down_sync(0xffffffffu, key, off);
-    const bool take = (lane + off < 32) && ok == key;
-    if (!__any_sync(0xffffffffu, take)) break;
+  if (rmax <= pull_max) {
+    for (int j = 1; j < rmax; ++j) {  // warp-uniform
+      const float fx = __shfl_down_sync(0xffffffffu, cell.fx, j), fy = __shfl_down_sync(0xffffffffu, cell.fy, j),
+                  fz = __shfl_down_sync(0xffffffffu, cell.fz, j);
+      const float e0 = __shfl_down_sync(0xffffffffu, d0, j), e1 = __shfl_down_sync(0xffffffffu, d1, j);
+      if (j < rlen) {
+        LevelCell m;
+        m.fx = fx;
+        m.fy = fy;
+        m.fz = fz;
+        float wm[8];
+        corner_weights(m, wm);
 #pragma unroll
-    for (int kk = 0; kk < 16; ++kk) {
-      const float tv = __shfl_down_sync(0xffffffffu, c[kk], off);
-      if (take) c[kk] += tv;
+        for (int corner = 0; corner < 8; ++corner) {
+          c[2 * corner] = fmaf(wm[corner], e0, c[2 * corner]);
+          c[2 * corner + 1] = fmaf(wm[corner], e1, c[2 * corner + 1]);
+        }
+      }
+    }
+  } else {
+    // segmented suffix sums: once no run is longer than `off`, larger offsets cannot match
+    for (int off = 1; off < rmax; off <<= 1) {
+      const uint32_t ok = __shfl_down_sync(0xffffffffu, key, off);
+      const bool take = (lane + off < 32) && ok == key;
+#pragma unroll
+      for (int kk = 0; kk < 16; ++kk) {
+        const float tv = __shfl_down_sync(0xffffffffu, c[kk], off);
+        if (take) c[kk] += tv;
+      }
     }
   }
-  const unsigned long long pk = __shfl_up_sync(0xffffffffu, key, 1);
-  if (!skip && valid && (lane == 0 || pk != key)) {
+  if (!skip && valid && head) {
     float* gl = grad + (long long)l * 2 * fd.rows;
     uint32_t rows[8];
     corner_rows(fd, l, cell, rows);
@@ -326,6 +357,7 @@ struct BwdCols {
 constexpr int kMlpThreads = 256;
 constexpr int kScatThreads = 256;  // two warps per 32-sample group: level halves
 constexpr int kBwdMlpLevels = 1;   // per half, scattered by the MLP warps (measured on cfg2)
+constexpr int kBwdPullMax = 4;     // scatter_level: pull-reduce runs up to this length (cfg2 sweep 1/4/8/12/16: 4 best)
 constexpr int kBwdThreads = kMlpThreads + kScatThreads;
 
 __device__ __forceinline__ void named_sync(int id, int n) {
@@ -353,7 +385,8 @@ template <int INP, int W, int H>
 __global__ void __launch_bounds__(kBwdThreads, 2)
     k_bwd_tc(FieldDesc fd, const float* __restrict__ params, float* __restrict__ grad, long long n_total, int S,
              const int* __restrict__ count, const float4* __restrict__ pos, const uint4* __restrict__ feat_tiles,
-             const float4* __restrict__ dout, int* tile_ctr, int skip_scatter, int mlp_levels) {
+             const float4* __restrict__ dout, int* tile_ctr, int skip_scatter, int mlp_levels,
+             int pull_max) {
   using CM = BwdCols<INP, W, H>;
   constexpr int XC = INP + 8, HC = W + 8;
   constexpr int SLD = ScatterSlot<INP>::kLd;
@@ -419,7 +452,6 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
       float4 pp = make_float4(0.f, 0.f, 0.f, 0.f);
       if (valid) pp = pos[gs];
       const float px = clamp01(pp.x), py = clamp01(pp.y), pz = clamp01(pp.z);
-      const unsigned long long ray_key = (unsigned long long)(gs / S) << 36;
       const float* drow = slot + r * SLD;
       // levels [lhalf*LH, (lhalf+1)*LH) belong to this half; the MLP warps
       // scatter the first mlp_levels of them straight from registers
@@ -427,7 +459,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
       const int l_hi = skip_scatter == 2 ? l_lo : min(fd.L, (lhalf + 1) * LH);
       for (int l = l_lo; l < l_hi; ++l) {  // warp-uniform
         const float2 dv = *reinterpret_cast<const float2*>(drow + 2 * l);
-        scatter_level(fd, grad, l, valid, px, py, pz, ray_key, dv.x, dv.y, lane, skip_scatter);
+        scatter_level(fd, grad, l, valid, px, py, pz, dv.x, dv.y, lane, skip_scatter, pull_max);
       }
       named_sync(2, kScatThreads);  // every scatter thread is done with the slot
       if (tid == kMlpThreads) mbar_arrive(&empty_bar);
@@ -574,12 +606,11 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
           float4 pp = make_float4(0.f, 0.f, 0.f, 0.f);
           if (valid) pp = pos[gs];
           const float px = clamp01(pp.x), py = clamp01(pp.y), pz = clamp01(pp.z);
-          const unsigned long long ray_key = (unsigned long long)(gs / S) << 36;
-          const int l0 = half * LH;
+              const int l0 = half * LH;
 #pragma unroll
           for (int j = 0; j < NH / 2; ++j)
             if (j < mlp_levels && l0 + j < fd.L)  // warp-uniform
-              scatter_level(fd, grad, l0 + j, valid, px, py, pz, ray_key, v[2 * j], v[2 * j + 1], lane, skip_scatter);
+              scatter_level(fd, grad, l0 + j, valid, px, py, pz, v[2 * j], v[2 * j + 1], lane, skip_scatter, pull_max);
         }
       }
     }
@@ -696,10 +727,13 @@ cudaError_t run_bwd(const FieldDesc& fd, const float* params, float* grad, long 
   }();
   const int mlp_levels = std::max(0, std::min(INP / 4, mlp_env >= 0 ? mlp_env : kBwdMlpLevels));
   static const int skip = getenv("PRENOM_PROF_SKIP_SCATTER") ? atoi(getenv("PRENOM_PROF_SKIP_SCATTER")) : 0;
+  // longest run reduced by pulls (else by the shuffle tree); PRENOM_BWD_PULL_MAX overrides
+  static const int pull_max = getenv("PRENOM_BWD_PULL_MAX") ? atoi(getenv("PRENOM_BWD_PULL_MAX")) : kBwdPullMax;
   cudaError_t em = cudaMemsetAsync(tile_ctr, 0, sizeof(int), st);
   if (em != cudaSuccess) return em;
   return launch_pdl(k_bwd_tc<INP, W, H>, dim3((unsigned)grid), dim3(kBwdThreads), smem, st, fd, params, grad, n, S,
-                    count, pos, reinterpret_cast<const uint4*>(feat_tiles), dout, tile_ctr, skip, mlp_levels);
+                    count, pos, reinterpret_cast<const uint4*>(feat_tiles), dout, tile_ctr, skip, mlp_levels,
+                    pull_max);
 }
 
 #define PRENOM_TC_DISPATCH(FN, ...)                                                          \
@@ -727,7 +761,7 @@ bool pdl_enabled() {
 
 bool tc_supported(const FieldDesc& fd) {
   for (int l = 0; l < fd.L; ++l)
-    if (fd.res[l] >= 4096) return false;  // scatter de-dup key packs 12-bit cell coordinates
+    if (fd.res[l] > 1625) return false;  // scatter de-dup key: the cell index fits 32 bits (1625^3 < 2^32)
   return fd.F == 2 && fd.in_dim <= 32 && (fd.W == 32 || fd.W == 64) && (fd.H == 1 || fd.H == 2);
 }
 
