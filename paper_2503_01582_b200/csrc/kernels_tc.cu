@@ -95,6 +95,10 @@ struct WeightTiles {
   }
 };
 
+// Ray of a sample slot: 32-bit division (batches stay far below 2^31 slots;
+// launch_*_tc check), not the ~70-instruction 64-bit one.
+__device__ __forceinline__ uint32_t ray_of(long long gs, int S) { return (uint32_t)gs / (uint32_t)S; }
+
 // Dynamic tile scheduler: CTAs pull 128-sample tiles from a global counter,
 // so the tile load balances whatever number of CTAs the hardware co-locates
 // on an SM (static striding left SMs with more resident CTAs as stragglers).
@@ -184,7 +188,7 @@ __global__ void __launch_bounds__(NT) k_fwd_tc(FieldDesc fd, const float* __rest
     {
       const int s = tid & (kTile - 1), part = tid >> 7;
       const long long gs = tile0 + s;
-      bool valid = gs < n_total && __ldg(count + gs / S) > 0;
+      bool valid = gs < n_total && __ldg(count + ray_of(gs, S)) > 0;
       float4 pp = make_float4(0.f, 0.f, 0.f, 0.f);
       if (valid) pp = pos[gs];
       const float px = clamp01(pp.x), py = clamp01(pp.y), pz = clamp01(pp.z);
@@ -237,7 +241,7 @@ __global__ void __launch_bounds__(NT) k_fwd_tc(FieldDesc fd, const float* __rest
       const long long gs = tile0 + row;
       if (gs < n_total) {
         float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (__ldg(count + gs / S) > 0) {
+        if (__ldg(count + ray_of(gs, S)) > 0) {
           const float* b = wt.bias + H * W;
           o.x = density_forward(fd.act, v[0] + b[0]);
           o.y = stable_sigmoid(v[1] + b[1]);
@@ -448,7 +452,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
       const long long t = slot_tile;
       if (t < 0) break;
       const long long gs = t * kTile + r;
-      const bool valid = gs < n_total && __ldg(count + gs / S) > 0;
+      const bool valid = gs < n_total && __ldg(count + ray_of(gs, S)) > 0;
       float4 pp = make_float4(0.f, 0.f, 0.f, 0.f);
       if (valid) pp = pos[gs];
       const float px = clamp01(pp.x), py = clamp01(pp.y), pz = clamp01(pp.z);
@@ -478,7 +482,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
     for (long long t = fetch(); t < ntiles; t = fetch(), ++iter) {
       const long long tile0 = t * kTile;
       const long long gs = tile0 + row;
-      const bool valid = gs < n_total && __ldg(count + gs / S) > 0;
+      const bool valid = gs < n_total && __ldg(count + ray_of(gs, S)) > 0;
       // ---- stored bf16 features -> X (row-group stride differs: copy per 16 B)
       {
         const uint4* src = feat_tiles + t * (128 * INP * 2 / 16);
@@ -773,6 +777,7 @@ size_t tc_feature_bytes(const FieldDesc& fd, long long n) {
 cudaError_t launch_fwd_tc(const FieldDesc& fd, const float* params, long long n, int S, const int* count,
                           const float4* pos, void* feat_tiles, float4* out, int* flag, int* tile_ctr, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
+  if (n + kTile >= (1LL << 31)) return cudaErrorInvalidValue;  // ray_of's 32-bit slot index
   PRENOM_TC_DISPATCH(run_fwd, fd, params, n, S, count, pos, feat_tiles, out, flag, tile_ctr, st);
 }
 
@@ -780,6 +785,7 @@ cudaError_t launch_bwd_tc(const FieldDesc& fd, const float* params, float* grad,
                           const int* count, const float4* pos, const void* feat_tiles, const float4* dout,
                           int* tile_ctr, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
+  if (n + kTile >= (1LL << 31)) return cudaErrorInvalidValue;  // ray_of's 32-bit slot index
   PRENOM_TC_DISPATCH(run_bwd, fd, params, grad, n, S, count, pos, feat_tiles, dout, tile_ctr, st);
 }
 
