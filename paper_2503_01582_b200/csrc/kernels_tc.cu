@@ -285,8 +285,12 @@ __device__ __forceinline__ void scatter_level(const FieldDesc& fd, float* __rest
   const uint32_t pk = __shfl_up_sync(0xffffffffu, key, 1);
   const bool head = lane == 0 || pk != key;
   const uint32_t heads = __ballot_sync(0xffffffffu, head);
+  // a run = maximal block of consecutive lanes with one key; it ends at the
+  // next head (equal keys need not be contiguous: rays can revisit a cell
+  // another ray left, so run membership is positional, never key equality)
   const uint32_t above = heads & ~((2u << lane) - 1u);  // heads strictly above this lane
-  const int rlen = head ? (above ? __ffs(above) - 1 : 32) - lane : 0;
+  const int run_end = above ? __ffs(above) - 1 : 32;
+  const int rlen = head ? run_end - lane : 0;
   const int rmax = __reduce_max_sync(0xffffffffu, (unsigned)rlen);
   float w[8], c[16];
   corner_weights(cell, w);
@@ -317,8 +321,7 @@ __device__ __forceinline__ void scatter_level(const FieldDesc& fd, float* __rest
   } else {
     // segmented suffix sums: once no run is longer than `off`, larger offsets cannot match
     for (int off = 1; off < rmax; off <<= 1) {
-      const uint32_t ok = __shfl_down_sync(0xffffffffu, key, off);
-      const bool take = (lane + off < 32) && ok == key;
+      const bool take = lane + off < run_end;
 #pragma unroll
       for (int kk = 0; kk < 16; ++kk) {
         const float tv = __shfl_down_sync(0xffffffffu, c[kk], off);
