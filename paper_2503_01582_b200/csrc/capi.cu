@@ -610,6 +610,8 @@ prenom_status prenom_ctx_synchronize(prenom_ctx_t ctx) {
   if (!ctx) return fail(PRENOM_USAGE, "NULL ctx");
   CUDA_TRY(cudaSetDevice(ctx->device));
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(ctx->side));  // a trailing sample-ahead / keyframe upload
+  for (auto l : ctx->lanes) CUDA_TRY(cudaStreamSynchronize(l));
   return PRENOM_OK;
 }
 
@@ -714,7 +716,11 @@ prenom_status prenom_object_create(prenom_ctx_t ctx, const prenom_field_arch* ar
 prenom_status prenom_object_destroy(prenom_object_t obj) {
   if (!obj) return PRENOM_OK;
   cudaSetDevice(obj->ctx->device);
+  // its work may sit on the main stream, the sampling stream (sample-ahead,
+  // keyframe uploads) or a lane stream
   cudaStreamSynchronize(obj->ctx->stream);
+  cudaStreamSynchronize(obj->ctx->side);
+  for (auto l : obj->ctx->lanes) cudaStreamSynchronize(l);
   if (obj->ctx->mc_grid_owner == obj) obj->ctx->mc_grid_owner = nullptr;
   delete obj;
   return PRENOM_OK;
