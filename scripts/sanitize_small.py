@@ -27,4 +27,27 @@ for prec, arch in ((1, scenes.cfg1_arch()), (0, FieldArch(hash_levels=6, log2_ta
     g = T.debug_field_backward(ctx, arch, p, xyz, rng.standard_normal(130).astype(np.float32),
                                rng.standard_normal((130, 3)).astype(np.float32), precision=prec)
     print(np.abs(g).sum())
+# multi-object lanes, streaming API with keyframe uploads, device frames, mesh, metric NN
+from paper_2503_01582_b200 import metrics as M  # noqa: E402
+
+cfg = TrainConfig(rays_per_iter=200, samples_per_ray=24, prior_sampling=1, grid_refresh_every=0, mlp_precision=1)
+objs = []
+for i in range(3):
+    o = ObjectTrainer.create(ctx, scenes.cfg1_arch(), grid=grid, seed=10 + i, cfg=cfg, box_min=sc.box_min,
+                             box_max=sc.box_max)
+    o.set_frames(sc.cams, sc.rgb, sc.depth, sc.mask, 1, sc.obj_pose)
+    objs.append(o)
+T.train_many(objs, 2)
+o = objs[0]
+for i in range(3):
+    f = o.frame_at(o.step())
+    o.upload_frame(f, np.ascontiguousarray(sc.rgb[f]), np.ascontiguousarray(sc.depth[f]), None)
+    print(o.wait_stats(o.train_step_async(1, prefetch_next=True))[0]["total"])
+o.synth_frames(sc.cams, sc.boxes, depth_noise=0.01, missing_frac=0.05, seed=2)
+o.train_step(2)
+v, t, iso = o.extract_mesh(24, iso=0.5)
+print("mesh", len(v), len(t), o.get_mesh_grid().shape)
+a = np.random.default_rng(1).uniform(0, 1, (300, 3)).astype(np.float32)
+print("chamfer", M.chamfer(ctx, a, a[::-1] + 0.01))
+ctx.synchronize()
 print("sanitize run ok")
