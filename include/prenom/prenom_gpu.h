@@ -294,6 +294,9 @@ prenom_status prenom_set_grid(prenom_object_t obj, int res, const float* grid);
 /* Adam moments (not saved by the reference; for checkpoint/resume). */
 prenom_status prenom_get_adam(prenom_object_t obj, float* m, float* v, int64_t* step);
 prenom_status prenom_reset_adam(prenom_object_t obj);
+/* Restore a checkpointed Adam state (m, v: P floats) and step (resume; the
+ * step also keys the Philox draws). Pair with prenom_get_adam / get_params. */
+prenom_status prenom_set_adam(prenom_object_t obj, const float* m, const float* v, int64_t step);
 
 /* ---- multi-object ----------------------------------------------------- */
 /* Train several objects of one context for n_steps each, launching their

@@ -1194,6 +1194,20 @@ prenom_status prenom_get_adam(prenom_object_t o, float* m, float* v, int64_t* st
   return PRENOM_OK;
 }
 
+// Resume: restore a checkpointed Adam state (the reference never saves it,
+// SURVEY §5; this makes train_track resumable: the step also keys the
+// Philox draws, so a resumed object continues the same sample stream).
+prenom_status prenom_set_adam(prenom_object_t o, const float* m, const float* v, int64_t step) {
+  if (!o || !m || !v) return fail(PRENOM_USAGE, "NULL argument");
+  if (step < 0) return fail(PRENOM_USAGE, "negative step");
+  CUDA_TRY(cudaSetDevice(o->ctx->device));
+  CUDA_TRY(cudaMemcpyAsync(o->m.p, m, o->P * sizeof(float), cudaMemcpyHostToDevice, o->ctx->stream));
+  CUDA_TRY(cudaMemcpyAsync(o->v.p, v, o->P * sizeof(float), cudaMemcpyHostToDevice, o->ctx->stream));
+  CUDA_TRY(cudaStreamSynchronize(o->ctx->stream));
+  o->step = step;
+  return PRENOM_OK;
+}
+
 prenom_status prenom_reset_adam(prenom_object_t o) {
   if (!o) return fail(PRENOM_USAGE, "NULL object");
   CUDA_TRY(cudaSetDevice(o->ctx->device));

@@ -436,6 +436,20 @@ class ObjectTrainer:
         _check(self.lib.prenom_get_adam(self.h, fptr(m), fptr(v), C.byref(s)))
         return m, v, s.value
 
+    def set_adam(self, m, v, step: int):
+        """Restore a checkpointed Adam state (resume; see checkpoint()/restore())."""
+        _check(self.lib.prenom_set_adam(self.h, fptr(_f32(m)), fptr(_f32(v)), int(step)))
+
+    def checkpoint(self) -> dict:
+        """Everything a resumed object needs: θ, Adam (m, v, step), the sampling grid."""
+        m, v, step = self.get_adam()
+        return dict(theta=self.get_params(), m=m, v=v, step=step, grid=self.get_grid())
+
+    def restore(self, ck: dict):
+        self.set_params(ck["theta"])
+        self.set_grid(ck["grid"])
+        self.set_adam(ck["m"], ck["v"], ck["step"])
+
     def reset_adam(self):
         _check(self.lib.prenom_reset_adam(self.h))
 

@@ -113,3 +113,34 @@ def test_streaming_async_steps_equal_train_step(ctx):
         assert abs(x["total"] - y["total"]) <= 1e-4 * abs(y["total"])
     with pytest.raises(Exception, match="ticket"):
         b.wait_stats(12345)
+
+
+@pytest.mark.parametrize("mlp", [0, 1])
+def test_checkpoint_resume_continues_the_same_run(ctx, mlp):
+    """Checkpoint after 7 steps (θ, Adam m/v/step, sampling grid), restore into a fresh
+    object, train 5 more: the same frames, sample counts and losses as the uninterrupted
+    run (the step keys the Philox draws; sums differ only by atomic order)."""
+    sc = tasks()[1]
+    grid = scenes.occupancy_prior(sc.boxes, R=16)
+    cfg = TrainConfig(rays_per_iter=128, samples_per_ray=32, prior_sampling=1, grid_refresh_every=4,
+                      mlp_precision=mlp)
+
+    arch = FieldArch(hash_levels=6, features_per_level=2, log2_table_size=11, base_resolution=6, per_level_scale=1.5,
+                     hidden_width=32, hidden_layers=2)  # tensor-core-eligible for the bf16 case
+
+    def make():
+        o = ObjectTrainer.create(ctx, arch, grid=grid, seed=77, cfg=cfg, box_min=sc.box_min, box_max=sc.box_max)
+        o.set_frames(sc.cams, sc.rgb, sc.depth, sc.mask, 1, sc.obj_pose)
+        return o
+
+    a = make()
+    a.train_step(7, stats=False)
+    ck = a.checkpoint()
+    want = a.train_step(5)
+    b = make()
+    b.restore(ck)
+    assert b.step() == 7
+    got = b.train_step(5)
+    for x, y in zip(got, want):
+        assert x["frame"] == y["frame"] and x["n_samples"] == y["n_samples"]
+        assert abs(x["total"] - y["total"]) <= 1e-3 * abs(y["total"])
