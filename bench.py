@@ -57,6 +57,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=100)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0, help="budget of the cpu_baseline sample")
+    ap.add_argument("--log-jsonl", default=None, help="per-step JSONL of the timed steps (loss terms, samples)")
     return ap.parse_args()
 
 
@@ -237,6 +238,7 @@ class Cfg2(Workload):
     def samples(self, k):
         st = self.obj.last_stats(k)
         self.loss = {"first": st[0]["total"], "last": st[-1]["total"]}
+        self.step_stats = st
         return sum(s["n_samples"] for s in st)
 
     def work_items(self):
@@ -508,6 +510,13 @@ def run_ours(args):
     ms = t_start.elapsed_time(t_end)
     launches = ctx.launch_count() - launches0
     n_samples = wl.samples(args.steps)
+    if args.log_jsonl and rank == 0 and getattr(wl, "step_stats", None):
+        # SURVEY §5 metrics/logging: one JSON line per timed step
+        per_step_ms = ms / args.steps
+        with open(args.log_jsonl, "w") as f:
+            for i, st in enumerate(wl.step_stats):
+                f.write(json.dumps(dict(step=i, ms_avg=round(per_step_ms, 4),
+                                        samples_per_s_avg=round(n_samples / (ms / 1e3), 1), **st)) + "\n")
     # the same K steps again with per-kernel CUDA events (on the launching
     # streams) for the per-kernel breakdown and the roofline
     lib.prenom_ctx_profile(ctx.h, 1)

@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "prenom_device.cuh"
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: host ranges for nsys/ncu timelines
 
 using namespace prenom;
 
@@ -165,6 +166,12 @@ struct prenom_ctx_s {
 };
 
 namespace {
+// NVTX range over a host API call; free when no tool is attached.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
 struct ProfScope {
   prenom_ctx_s* c;
   int k;
@@ -372,6 +379,7 @@ prenom_status enqueue_sample(prenom_object_s* o, int64_t step, cudaStream_t st) 
 // concurrently with this step's Adam (it only reads frames and the grid;
 // steps that refresh the grid keep the serial order).
 prenom_status enqueue_step(prenom_object_s* o, StepStatsDev* stats, bool has_next = false) {
+  NvtxRange nvtx_("prenom.step");
   cudaStream_t st = o->lane ? o->lane : o->ctx->stream;
   const prenom_train_cfg& c = o->cfg;
   const int B = c.rays_per_iter, S = c.samples_per_ray;
@@ -808,6 +816,7 @@ prenom_status prenom_object_get_frame(prenom_object_t o, int frame, float* rgb, 
 
 prenom_status prenom_object_upload_frame(prenom_object_t o, int frame, const float* rgb, const float* depth,
                                          const uint8_t* mask) {
+  NvtxRange nvtx_("prenom.upload_frame");
   if (!o || !rgb || !depth) return fail(PRENOM_USAGE, "NULL argument");
   if (frame < 0 || frame >= (int)o->frames.size()) return fail(PRENOM_USAGE, "frame index out of range");
   CUDA_TRY(cudaSetDevice(o->ctx->device));
@@ -832,6 +841,7 @@ prenom_status prenom_object_upload_frame(prenom_object_t o, int frame, const flo
 }
 
 prenom_status prenom_train_step(prenom_object_t o, int n_steps, prenom_step_stats* stats) {
+  NvtxRange nvtx_("prenom.train_step");
   if (!o) return fail(PRENOM_USAGE, "NULL object");
   if (n_steps < 1) return fail(PRENOM_USAGE, "n_steps must be >= 1");
   if (o->frames.empty()) return fail(PRENOM_DATA, "train_step: object has no frames");
@@ -858,6 +868,7 @@ prenom_status prenom_train_step(prenom_object_t o, int n_steps, prenom_step_stat
 // after this call's last backward (as consecutive steps of one call do), so a
 // caller stepping one call per keyframe keeps the sampling overlapped with Adam.
 prenom_status prenom_train_step_async(prenom_object_t o, int n_steps, int prefetch_next, uint64_t* ticket) {
+  NvtxRange nvtx_("prenom.train_step_async");
   if (!o || !ticket) return fail(PRENOM_USAGE, "NULL argument");
   if (n_steps < 1) return fail(PRENOM_USAGE, "n_steps must be >= 1");
   if (o->frames.empty()) return fail(PRENOM_DATA, "train_step: object has no frames");
@@ -934,6 +945,7 @@ prenom_status prenom_object_check(prenom_object_t o) {
 
 prenom_status prenom_render(prenom_object_t o, int n_rays, const float* origins, const float* dirs,
                             float* rgb_out, float* depth_out) {
+  NvtxRange nvtx_("prenom.render");
   if (!o || !origins || !dirs) return fail(PRENOM_USAGE, "NULL argument");
   if (n_rays < 1) return fail(PRENOM_USAGE, "n_rays must be >= 1");
   CUDA_TRY(cudaSetDevice(o->ctx->device));
@@ -982,6 +994,7 @@ prenom_status prenom_render(prenom_object_t o, int n_rays, const float* origins,
 }
 
 prenom_status prenom_density_query(prenom_object_t o, int R, float* out, int update) {
+  NvtxRange nvtx_("prenom.density_query");
   if (!o) return fail(PRENOM_USAGE, "NULL object");
   if (R < 2 || R > 1024) return fail(PRENOM_DATA, "grid resolution out of range");
   CUDA_TRY(cudaSetDevice(o->ctx->device));
@@ -1007,6 +1020,7 @@ prenom_status prenom_density_query(prenom_object_t o, int R, float* out, int upd
 // object until prenom_get_mesh copies it out.
 prenom_status prenom_extract_mesh(prenom_object_t o, int R, float iso, float iso_floor, float* iso_used,
                                   int64_t* n_vertices, int64_t* n_triangles) {
+  NvtxRange nvtx_("prenom.extract_mesh");
   if (!o) return fail(PRENOM_USAGE, "NULL object");
   if (R < 2 || R > 1024) return fail(PRENOM_DATA, "grid resolution out of range");
   CUDA_TRY(cudaSetDevice(o->ctx->device));
@@ -1220,6 +1234,7 @@ prenom_status prenom_reset_adam(prenom_object_t o) {
 }
 
 prenom_status prenom_train_step_many(prenom_object_t* objs, int n_objs, int n_steps) {
+  NvtxRange nvtx_("prenom.train_step_many");
   if (!objs || n_objs < 1 || n_steps < 1) return fail(PRENOM_USAGE, "bad arguments");
   for (int i = 0; i < n_objs; ++i) {
     if (!objs[i]) return fail(PRENOM_USAGE, "NULL object");
