@@ -49,7 +49,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg3", "cfg4", "cfg5"])
+    ap.add_argument("--workload", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
     ap.add_argument("--width", type=int, default=64)
     ap.add_argument("--mlp", default="bf16", choices=["fp32", "bf16"])
     ap.add_argument("--rays", type=int, default=8192)
@@ -206,6 +206,47 @@ class Workload:
     def work_items(self):
         """[(arch, cfg, steps_factor)] whose per-step algorithmic costs add up."""
         raise NotImplementedError
+
+
+class Cfg1(Workload):
+    """BASELINE config 1 (the reference's own CPU-runnable case): sphere r=0.35 with
+    albedo sin(7 xyz)*0.5+0.5, 24 views 128^2 at radius 1.5 (Fibonacci), depth noise
+    0.005; L8 F2 T2^15 base 16 -> 256, MLP W32 H2; 4096 rays x 64 midpoint samples,
+    L2 RGB + 0.1 L1 depth, Adam 1e-2, fp32 MLP (the BASELINE precision); seed 0."""
+
+    name = "cfg1"
+    e2e_capable = False
+
+    def __init__(self, args, ctx, rank, ws):
+        from paper_2503_01582_b200 import ObjectTrainer, TrainConfig, scenes
+        from paper_2503_01582_b200._capi import MLP_BF16, MLP_FP32
+
+        self.sc = scenes.sphere_scene(seed=rank)
+        self.arch = scenes.cfg1_arch()
+        self.cfg = TrainConfig(rays_per_iter=4096, samples_per_ray=64, prior_sampling=0, grid_refresh_every=0,
+                               eta=1e-2, bg_fraction=0.25,
+                               mlp_precision=MLP_BF16 if args.mlp == "bf16" else MLP_FP32)
+        self.obj = ObjectTrainer.create(ctx, self.arch, theta=None, grid_res=8, seed=rank, cfg=self.cfg,
+                                        box_min=self.sc.box_min, box_max=self.sc.box_max)
+        self.obj.set_frames(self.sc.cams, self.sc.rgb, self.sc.depth, self.sc.mask, 1, self.sc.obj_pose)
+        self.objs = [self.obj]
+        self.n_objects_total = ws
+        self.desc = ("cfg1: sphere r0.35, 24 views 128^2, L8 F2 T15 max-res 256, MLP W32 H2, 4096 rays x 64 "
+                     f"midpoints, {args.mlp} MLP")
+        self.extra = {"rays_per_step": 4096, "mlp_samples_per_ray": 64, "params": self.arch.param_count(),
+                      "l2": "params+Adam state 8 MiB are L2-resident; no flush (the reference config is small)"}
+
+    def step(self, k):
+        self.obj.train_step(k, stats=False)
+
+    def samples(self, k):
+        st = self.obj.last_stats(k)
+        self.loss = {"first": st[0]["total"], "last": st[-1]["total"]}
+        self.step_stats = st
+        return sum(s["n_samples"] for s in st)
+
+    def work_items(self):
+        return [(self.arch, self.cfg, 1)]
 
 
 class Cfg2(Workload):
@@ -464,7 +505,7 @@ class Cfg5(Workload):
                 "triangles_mean": float(np.mean(tris))}
 
 
-WORKLOADS = {"cfg2": Cfg2, "cfg3": Cfg3, "cfg4": Cfg4, "cfg5": Cfg5}
+WORKLOADS = {"cfg1": Cfg1, "cfg2": Cfg2, "cfg3": Cfg3, "cfg4": Cfg4, "cfg5": Cfg5}
 
 
 def run_ours(args):
