@@ -81,6 +81,102 @@ __device__ __forceinline__ void tile_gemm(const float* __restrict__ Wsm, int rs,
   }
 }
 
+// Register-blocked variant for the wide layers: Y[m][s] = epi(bias[m] +
+// sum_k Wk[k*ldt + m] X[k][s]) with the weights k-major (a transposed copy
+// for the forward, the reference layout W[o][i] itself for the backward
+// data products). Warp w owns rows [w*MR, w*MR+MR) (M = 8*MR), lane owns
+// samples 4*lane..4*lane+3: per k one conflict-free LDS.128 of X and MR/4
+// broadcast LDS.128 of weights feed 4*MR FMAs (tile_gemm: 2 loads per 8).
+template <int MR>
+__device__ __forceinline__ void tile_gemm_rb(const float* Wk, int ldt, const float* bias, int K, const float* X,
+                                             float* Y, int ldy, int epi) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int m0 = warp * MR;
+  float4 acc[MR];
+#pragma unroll
+  for (int j = 0; j < MR; ++j) {
+    const float b = bias ? bias[m0 + j] : 0.f;
+    acc[j] = make_float4(b, b, b, b);
+  }
+#pragma unroll 4
+  for (int k = 0; k < K; ++k) {
+    const float4 x = *reinterpret_cast<const float4*>(X + k * kLd + 4 * lane);
+    float w[MR];
+    if constexpr (MR % 4 == 0) {
+#pragma unroll
+      for (int q = 0; q < MR / 4; ++q) {
+        const float4 v = *reinterpret_cast<const float4*>(Wk + k * ldt + m0 + 4 * q);
+        w[4 * q] = v.x;
+        w[4 * q + 1] = v.y;
+        w[4 * q + 2] = v.z;
+        w[4 * q + 3] = v.w;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < MR; ++j) w[j] = Wk[k * ldt + m0 + j];
+    }
+#pragma unroll
+    for (int j = 0; j < MR; ++j) {
+      acc[j].x = fmaf(w[j], x.x, acc[j].x);
+      acc[j].y = fmaf(w[j], x.y, acc[j].y);
+      acc[j].z = fmaf(w[j], x.z, acc[j].z);
+      acc[j].w = fmaf(w[j], x.w, acc[j].w);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < MR; ++j) {
+    float4* y = reinterpret_cast<float4*>(Y + (size_t)(m0 + j) * ldy + 4 * lane);
+    float4 v = acc[j];
+    if (epi == 1) {
+      v.x = fmaxf(v.x, 0.f);
+      v.y = fmaxf(v.y, 0.f);
+      v.z = fmaxf(v.z, 0.f);
+      v.w = fmaxf(v.w, 0.f);
+    } else if (epi == 2) {
+      const float4 g = *y;
+      v.x = g.x > 0.f ? v.x : 0.f;
+      v.y = g.y > 0.f ? v.y : 0.f;
+      v.z = g.z > 0.f ? v.z : 0.f;
+      v.w = g.w > 0.f ? v.w : 0.f;
+    }
+    *y = v;
+  }
+}
+
+// Y = epi(bias + W·X) for M output rows with k-major weights Wk[k*ldt + m]:
+// the register-blocked kernel when 8 warps split M evenly (M = 16..64),
+// else tile_gemm on the same layout (rs = 1, cs = ldt).
+template <int NT>
+__device__ __forceinline__ void gemm_kmajor(const float* Wk, int ldt, const float* bias, int M, int K,
+                                            const float* X, float* Y, int ldy, int epi) {
+  static_assert(NT == 256, "8 warps");
+  switch (M) {
+    case 64: tile_gemm_rb<8>(Wk, ldt, bias, K, X, Y, ldy, epi); return;
+    case 32: tile_gemm_rb<4>(Wk, ldt, bias, K, X, Y, ldy, epi); return;
+    case 24: tile_gemm_rb<3>(Wk, ldt, bias, K, X, Y, ldy, epi); return;
+    case 16: tile_gemm_rb<2>(Wk, ldt, bias, K, X, Y, ldy, epi); return;
+    default: tile_gemm<NT, 1>(Wk, 1, ldt, bias, M, K, X, Y, ldy, epi);
+  }
+}
+
+// Stage the MLP block transposed (per layer W[o][i] -> Wt[i][o] at the same
+// offset; biases as they are) for gemm_kmajor's forward products.
+__device__ __forceinline__ void stage_mlp_transposed(const FieldDesc& fd, const float* __restrict__ mlp, float* Wt,
+                                                     int nt) {
+  int in = fd.in_dim;
+  for (int l = 0; l <= fd.H; ++l) {
+    const int out = l < fd.H ? fd.W : 4;
+    const float* W = mlp + fd.w_off[l];
+    float* T = Wt + fd.w_off[l];
+    for (int i = threadIdx.x; i < out * in; i += nt) {
+      const int o = i / in, k = i % in;
+      T[k * out + o] = __ldg(W + i);
+    }
+    for (int i = threadIdx.x; i < out; i += nt) Wt[fd.b_off[l] + i] = __ldg(mlp + fd.b_off[l] + i);
+    in = out;
+  }
+}
+
 // acc[m*ldw + k] += sum_s A[m][s] * B[k][s] over the tile (weight gradient).
 // Warp tile 16(m) x 32(k): lane (tm = lane>>3, tk = lane&7) owns rows
 // tm + 4i and columns tk + 8j (i, j < 4), so the 8 lanes of an LDS.128
@@ -201,20 +297,21 @@ __device__ __forceinline__ void encode_tile_rt(const FieldDesc& fd, const float*
   }
 }
 
-// Forward MLP over the tile: X (in) -> hidden buffers Hb[l] -> RAW[4][kLd].
+// Forward MLP over the tile: X (in) -> hidden buffers Hb[l] -> RAW[4][kLd];
+// Wt = the MLP block staged by stage_mlp_transposed.
 template <int NT>
-__device__ __forceinline__ void mlp_forward_tile(const FieldDesc& fd, const float* Wsm, const float* X,
+__device__ __forceinline__ void mlp_forward_tile(const FieldDesc& fd, const float* Wt, const float* X,
                                                  float* Hb, float* RAW) {
   const float* in = X;
   int in_dim = fd.in_dim;
   for (int l = 0; l < fd.H; ++l) {
     float* out = Hb + (size_t)l * fd.W * kLd;
-    tile_gemm<NT, 2>(Wsm + fd.w_off[l], in_dim, 1, Wsm + fd.b_off[l], fd.W, in_dim, in, out, kLd, 1);
+    gemm_kmajor<NT>(Wt + fd.w_off[l], fd.W, Wt + fd.b_off[l], fd.W, in_dim, in, out, kLd, 1);
     __syncthreads();
     in = out;
     in_dim = fd.W;
   }
-  tile_gemm<NT, 1>(Wsm + fd.w_off[fd.H], in_dim, 1, Wsm + fd.b_off[fd.H], 4, in_dim, in, RAW, kLd, 0);
+  gemm_kmajor<NT>(Wt + fd.w_off[fd.H], 4, Wt + fd.b_off[fd.H], 4, in_dim, in, RAW, kLd, 0);
   __syncthreads();
 }
 
@@ -228,8 +325,7 @@ __global__ void __launch_bounds__(kFwdThreads) k_fwd_tile(FieldDesc fd, const fl
   float* Hb = X + (size_t)fd.in_dim * kLd;
   float* RAW = Hb + (size_t)fd.H * fd.W * kLd;
   float* Wsm = RAW + 4 * kLd;
-  const float* mlp = params + fd.hash_params;
-  for (int i = threadIdx.x; i < fd.mlp_params; i += kFwdThreads) Wsm[i] = __ldg(mlp + i);
+  stage_mlp_transposed(fd, params + fd.hash_params, Wsm, kFwdThreads);
   const long long ntiles = (n_total + kTile - 1) / kTile;
   for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const long long tile0 = t * kTile;
@@ -238,7 +334,7 @@ __global__ void __launch_bounds__(kFwdThreads) k_fwd_tile(FieldDesc fd, const fl
     else
       encode_tile_rt(fd, params, tile0, n_total, S, count, pos, X, feat_t, ld_t);
     __syncthreads();
-    mlp_forward_tile<kFwdThreads>(fd, Wsm, X, Hb, RAW);
+    mlp_forward_tile<kFwdThreads>(fd, Wsm, X, Hb, RAW);  // Wsm holds the transposed block
     if (threadIdx.x < kTile) {
       const int s = threadIdx.x;
       const long long gs = tile0 + s;
@@ -269,13 +365,15 @@ __global__ void __launch_bounds__(kBwdThreads) k_bwd_tile(FieldDesc fd, const fl
   float* Hb = X + (size_t)fd.in_dim * kLd;
   float* RAW = Hb + (size_t)fd.H * fd.W * kLd;
   float* G = RAW + 4 * kLd;
-  float* Wsm = G + 4 * kLd;
+  float* Wsm = G + 4 * kLd;                            // reference layout (backward products)
   float* Acc = Wsm + ((fd.mlp_params + 3) & ~3);
+  float* Wt = Acc + ((fd.mlp_params + 3) & ~3);         // transposed (forward recompute)
   const float* mlp = params + fd.hash_params;
   for (int i = threadIdx.x; i < fd.mlp_params; i += kBwdThreads) {
     Wsm[i] = __ldg(mlp + i);
     Acc[i] = 0.f;
   }
+  stage_mlp_transposed(fd, mlp, Wt, kBwdThreads);
   __syncthreads();
   const long long ntiles = (n_total + kTile - 1) / kTile;
   for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
@@ -296,7 +394,7 @@ __global__ void __launch_bounds__(kBwdThreads) k_bwd_tile(FieldDesc fd, const fl
       *reinterpret_cast<float4*>(X + row * kLd + 4 * q) = v;
     }
     __syncthreads();
-    mlp_forward_tile<kBwdThreads>(fd, Wsm, X, Hb, RAW);
+    mlp_forward_tile<kBwdThreads>(fd, Wt, X, Hb, RAW);
     // g_raw (field.cpp:233-238)
     if (threadIdx.x < kTile) {
       const int s = threadIdx.x;
@@ -328,8 +426,8 @@ __global__ void __launch_bounds__(kBwdThreads) k_bwd_tile(FieldDesc fd, const fl
     tile_bgrad<kBwdThreads>(G, 4, Acc + fd.b_off[H]);
     __syncthreads();
     // D_{H-1} = gate(H_{H-1}) * (W_out^T G), in place
-    tile_gemm<kBwdThreads, 2>(Wsm + fd.w_off[H], 1, last_dim, nullptr, last_dim, 4, G,
-                              Hb + (size_t)(H - 1) * fd.W * kLd, kLd, 2);
+    gemm_kmajor<kBwdThreads>(Wsm + fd.w_off[H], last_dim, nullptr, last_dim, 4, G,
+                             Hb + (size_t)(H - 1) * fd.W * kLd, kLd, 2);
     __syncthreads();
     for (int l = H - 1; l >= 0; --l) {
       float* D = Hb + (size_t)l * fd.W * kLd;
@@ -339,15 +437,15 @@ __global__ void __launch_bounds__(kBwdThreads) k_bwd_tile(FieldDesc fd, const fl
       tile_bgrad<kBwdThreads>(D, fd.W, Acc + fd.b_off[l]);
       __syncthreads();
       if (l > 0) {
-        tile_gemm<kBwdThreads, 2>(Wsm + fd.w_off[l], 1, prev_dim, nullptr, prev_dim, fd.W, D,
-                                  Hb + (size_t)(l - 1) * fd.W * kLd, kLd, 2);
+        gemm_kmajor<kBwdThreads>(Wsm + fd.w_off[l], prev_dim, nullptr, prev_dim, fd.W, D,
+                                 Hb + (size_t)(l - 1) * fd.W * kLd, kLd, 2);
       } else {
         // d_features straight to global SoA (no gate)
         if (tile0 + kTile <= n_total) {
-          tile_gemm<kBwdThreads, 2>(Wsm + fd.w_off[0], 1, fd.in_dim, nullptr, fd.in_dim, fd.W, D,
-                                    dfeat_t + tile0, (int)ld_t, 0);
+          gemm_kmajor<kBwdThreads>(Wsm + fd.w_off[0], fd.in_dim, nullptr, fd.in_dim, fd.W, D, dfeat_t + tile0,
+                                   (int)ld_t, 0);
         } else {
-          tile_gemm<kBwdThreads, 2>(Wsm + fd.w_off[0], 1, fd.in_dim, nullptr, fd.in_dim, fd.W, D, X, kLd, 0);
+          gemm_kmajor<kBwdThreads>(Wsm + fd.w_off[0], fd.in_dim, nullptr, fd.in_dim, fd.W, D, X, kLd, 0);
           __syncthreads();
           for (int i = threadIdx.x; i < fd.in_dim * kTile; i += kBwdThreads) {
             const int row = i / kTile, s = i % kTile;
@@ -795,7 +893,7 @@ static size_t fwd_smem_bytes(const FieldDesc& fd) {
 
 static size_t bwd_smem_bytes(const FieldDesc& fd) {
   return sizeof(float) * ((size_t)fd.in_dim * kLd + (size_t)fd.H * fd.W * kLd + 8 * kLd +
-                          2 * ((fd.mlp_params + 3) & ~3));
+                          3 * ((fd.mlp_params + 3) & ~3));
 }
 
 cudaError_t launch_field_fwd_train(const FieldDesc& fd, const float* params, int B, int S,
