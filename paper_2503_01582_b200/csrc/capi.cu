@@ -132,8 +132,10 @@ uint32_t philox_first(uint64_t seed, uint32_t tag, uint32_t step, uint32_t ray, 
 
 }  // namespace
 
-constexpr int kDefaultLanes = 4;  // cfg3 on B200: 1 lane 1.00e9, 2: 1.15e9, 4: 1.235e9, 8: 1.21e9 samples/s
+constexpr int kDefaultLanes = 8;  // B200, with >= 8 tiles per persistent CTA: cfg3 4 lanes 1.35e9, 8 lanes 1.41e9;
+                                  // cfg5 4: 1.10e9, 8: 1.12e9 (1 lane: cfg3 1.00e9)
 constexpr int kMaxLanes = 16;
+constexpr int kLaneMinTilesPerCta = 8;
 
 struct prenom_ctx_s {
   int device = 0;
@@ -1279,6 +1281,10 @@ prenom_status prenom_train_step_many(prenom_object_t* objs, int n_objs, int n_st
   for (int k = 0; k < K; ++k) CUDA_TRY(cudaStreamWaitEvent(c->lanes[k], c->fork_ev, 0));
   for (int i = 0; i < n_objs; ++i) objs[i]->lane = c->lanes[i % K];
   prenom_status st = PRENOM_OK;
+  struct MinTiles {  // small per-object batches: fewer, fuller persistent CTAs (kernels_tc.cu)
+    MinTiles() { tc_set_min_tiles_per_cta(kLaneMinTilesPerCta); }
+    ~MinTiles() { tc_set_min_tiles_per_cta(1); }
+  } min_tiles_;
   for (int it = 0; it < n_steps && st == PRENOM_OK; ++it)
     for (int i = 0; i < n_objs && st == PRENOM_OK; ++i)
       st = enqueue_step(objs[i], objs[i]->stats.p + it, false);  // concurrency replaces the sample-ahead

@@ -656,6 +656,22 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
   if (warp == 0) umma::tmem_dealloc(tm, 256);
 }
 
+// Persistent-grid sizing hint: under the multi-object scheduler (concurrent
+// lane streams, ~1k tiles per object) each CTA takes at least 8 tiles, so the
+// per-CTA prologue (weight tiles, TMEM alloc) is amortised and the lanes keep
+// SMs for each other's kernels (cfg5 9.9e8 -> 1.12e9, cfg3 1.34e9 -> 1.41e9);
+// a single object keeps the full grid (cfg4's 2k-tile steps lose 3% at 8).
+// Set per host thread by prenom_train_step_many; PRENOM_MIN_TILES_PER_CTA overrides.
+thread_local int t_min_tiles = 1;
+
+int min_tiles_per_cta() {
+  static const int env = [] {
+    const char* e = getenv("PRENOM_MIN_TILES_PER_CTA");
+    return e ? std::max(1, atoi(e)) : 0;
+  }();
+  return env ? env : t_min_tiles;
+}
+
 int g_sms = 0;
 int sms() {
   if (!g_sms) {
@@ -685,7 +701,7 @@ cudaError_t run_fwd_nt(const FieldDesc& fd, const float* params, long long n, in
   cudaError_t e = cudaFuncSetAttribute(k_fwd_tc<INP, W, H, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const long long ntiles = (n + kTile - 1) / kTile;
-  const long long grid = std::min<long long>(ntiles, (long long)ctas * sms());
+  const long long grid = std::min<long long>((ntiles + min_tiles_per_cta() - 1) / min_tiles_per_cta(), (long long)ctas * sms());
 #ifdef PRENOM_VAR_FWD_MEMSET
   e = cudaMemsetAsync(tile_ctr, 0, sizeof(int), st);
   if (e != cudaSuccess) return e;
@@ -725,7 +741,7 @@ cudaError_t run_bwd(const FieldDesc& fd, const float* params, float* grad, long 
   cudaError_t e = cudaFuncSetAttribute(k_bwd_tc<INP, W, H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const long long ntiles = (n + kTile - 1) / kTile;
-  const long long grid = std::min<long long>(ntiles, 2LL * sms());
+  const long long grid = std::min<long long>((ntiles + min_tiles_per_cta() - 1) / min_tiles_per_cta(), 2LL * sms());
   // levels per half the MLP warps scatter themselves (they would otherwise
   // wait on the scatter warps); PRENOM_BWD_MLP_LEVELS overrides for tuning
   static const int mlp_env = [] {
@@ -761,6 +777,8 @@ cudaError_t run_bwd(const FieldDesc& fd, const float* params, float* grad, long 
 
 // On by default (cfg2, B200, interleaved 3x: 0.7001 -> 0.6940 ms/step);
 // PRENOM_NO_PDL=1 disables for A/B.
+void tc_set_min_tiles_per_cta(int v) { t_min_tiles = v < 1 ? 1 : v; }
+
 bool pdl_enabled() {
   static const bool on = getenv("PRENOM_NO_PDL") == nullptr;
   return on;
