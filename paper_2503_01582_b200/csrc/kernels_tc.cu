@@ -329,7 +329,7 @@ __device__ __forceinline__ void scatter_level(const FieldDesc& fd, float* __rest
       }
     }
   }
-  if (!skip && valid && head) {
+  if (skip != 1 && valid && head) {  // (skip == 1: profiling, no atomics)
     float* gl = grad + (long long)l * 2 * fd.rows;
     uint32_t rows[8];
     corner_rows(fd, l, cell, rows);
@@ -495,6 +495,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
         }
       }
       mlp_sync_for_mma();
+      if (skip_scatter != 3) {  // (profiling knob 3: scatter-only timing -- the MLP chain is skipped)
       // ---- forward recompute (field.cpp:181-211), one TMEM region reused per layer
       if (tid == 0) {
         for (int ks = 0; ks < INP / 16; ++ks)
@@ -592,6 +593,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
         }
         wait_mma(&bar, phase);
       }
+      }  // skip_scatter != 3
       // ---- hand d_features to the scatter warps (slot free once they drained it)
       {
         constexpr int NH = INP / 2;
