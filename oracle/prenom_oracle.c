@@ -8,6 +8,7 @@
 #include "prenom_oracle.h"
 
 #include <math.h>
+#include <pthread.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -847,6 +848,86 @@ int po_object_set_frames(po_object* o, int n, const prenom_camera* cams, const f
 }
 
 /* mapper.cpp:150-184, one iteration per step, Philox draws with c2 = step. */
+/* ---- optional threading of the oracle's train step (env PO_THREADS, default
+ * 1 = the sequential restatement every parity test uses). Only long
+ * full-size evidence runs set it: field evaluations are independent; the
+ * backward gives each thread a contiguous sample block and a private gradient,
+ * summed in thread order -- deterministic for a given thread count, not the
+ * sequential summation order. */
+static int po_threads(void) {
+  const char* e = getenv("PO_THREADS");
+  const int n = e ? atoi(e) : 1;
+  return n < 1 ? 1 : (n > 64 ? 64 : n);
+}
+
+typedef struct {
+  const prenom_field_arch* a;
+  const float* params;
+  const float* pos;
+  float* sg;
+  float* rgb;
+  const float* dsg;
+  const float* drgb;
+  float* grad;
+  size_t P;
+  int n;
+  int nt;
+  int status;
+} po_par_job;
+
+typedef struct {
+  po_par_job* job;
+  int t;
+  float* priv;
+  int status;
+} po_par_arg;
+
+static void* po_eval_block(void* p) {
+  po_par_arg* w = (po_par_arg*)p;
+  po_par_job* j = w->job;
+  const int lo = (int)((long long)j->n * w->t / j->nt), hi = (int)((long long)j->n * (w->t + 1) / j->nt);
+  for (int i = lo; i < hi && w->status == 0; ++i)
+    w->status = po_field_eval(j->a, j->params, j->pos + 3 * (size_t)i, j->sg + i, j->rgb + 3 * (size_t)i, NULL,
+                              NULL, NULL, NULL, NULL, NULL);
+  return NULL;
+}
+
+static void* po_backward_block(void* p) {
+  po_par_arg* w = (po_par_arg*)p;
+  po_par_job* j = w->job;
+  const int lo = (int)((long long)j->n * w->t / j->nt), hi = (int)((long long)j->n * (w->t + 1) / j->nt);
+  for (int i = lo; i < hi; ++i)
+    po_field_backward(j->a, j->params, j->pos + 3 * (size_t)i, j->dsg[i], j->drgb + 3 * (size_t)i, w->priv);
+  return NULL;
+}
+
+static void po_run_parallel(po_par_job* job, void* (*fn)(void*)) {
+  const int nt = po_threads();
+  job->nt = nt;
+  job->status = 0;
+  po_par_arg args[64];
+  pthread_t th[64];
+  const int backward = fn == po_backward_block;
+  for (int t = 0; t < nt; ++t) {
+    args[t].job = job;
+    args[t].t = t;
+    args[t].status = 0;
+    args[t].priv = backward ? (float*)calloc(job->P, sizeof(float)) : NULL;
+  }
+  for (int t = 1; t < nt; ++t) pthread_create(&th[t], NULL, fn, &args[t]);
+  fn(&args[0]);
+  for (int t = 1; t < nt; ++t) pthread_join(th[t], NULL);
+  for (int t = 0; t < nt; ++t) job->status |= args[t].status;
+  if (backward) {
+    for (size_t k = 0; k < job->P; ++k) {
+      float acc = 0.f;
+      for (int t = 0; t < nt; ++t) acc += args[t].priv[k];
+      job->grad[k] = acc;
+    }
+    for (int t = 0; t < nt; ++t) free(args[t].priv);
+  }
+}
+
 int po_object_train_step(po_object* o, int n_steps, prenom_step_stats* stats) {
   const prenom_train_cfg* c = &o->cfg;
   const prenom_field_arch* a = &o->arch;
@@ -901,17 +982,24 @@ int po_object_train_step(po_object* o, int n_steps, prenom_step_stats* stats) {
       bg[3 * r + 2] = po_u01(r4[2]);
     }
     n_samples = off[B];
-    for (int i = 0; i < n_samples && status == 0; ++i)
-      status = po_field_eval(a, o->params, pos + 3 * i, sg + i, rgb + 3 * i, NULL, NULL, NULL,
-                             NULL, NULL, NULL);
+    {
+      po_par_job job = {a, o->params, pos, sg, rgb, dsg, drgb, NULL, o->P, n_samples, 0, 0};
+      po_run_parallel(&job, po_eval_block);
+      status = job.status;
+    }
     if (status) break;
     double terms[4];
     status = po_batch_loss(B, kind, trgb, tdep, esc, off, dlt, dep, sg, rgb, bg, c->lambda_d,
                            c->lambda_sigma, terms, dsg, drgb, NULL, NULL);
     if (status) break;
     memset(o->grad, 0, sizeof(float) * o->P);
-    for (int i = 0; i < n_samples; ++i)
-      po_field_backward(a, o->params, pos + 3 * i, dsg[i], drgb + 3 * i, o->grad);
+    if (po_threads() <= 1) {
+      for (int i = 0; i < n_samples; ++i)
+        po_field_backward(a, o->params, pos + 3 * i, dsg[i], drgb + 3 * i, o->grad);
+    } else {
+      po_par_job job = {a, o->params, pos, sg, rgb, dsg, drgb, o->grad, o->P, n_samples, 0, 0};
+      po_run_parallel(&job, po_backward_block);
+    }
     po_adam_step(o->P, o->params, o->grad, o->m, o->v, &o->step, c->eta, c->adam_beta1,
                  c->adam_beta2, c->adam_eps);
     if (stats) {
