@@ -1,0 +1,182 @@
+// kernels_optim.cu -- the dense parameter passes of the step and of Reptile:
+//   k_adam            adam_step (field.cpp:295-310), bit-exact, fused grad zeroing
+//   k_init_params     init_params' distributions from Philox (field.cpp:150-166)
+//   k_reptile_*       reptile_update (meta.cpp:83-92), its delta/apply split for NCCL
+//   k_philox          Philox4x32-10 known-answer entry point
+#include <algorithm>
+
+#include "prenom_device.cuh"
+
+namespace prenom {
+namespace {
+// ------------------------------------------------------------------ Adam
+// field.cpp:295-310, dense, same operation order with *_rn intrinsics;
+// grad zeroed in the same pass (train_track zeroes it before each backward,
+// mapper.cpp:175). c1 = 1 - b1^step, c2 = 1 - b2^step come from the host
+// (glibc powf, like the reference).
+__device__ __forceinline__ void adam1(float& p, float& g, float& m, float& v, float lr, float b1, float b2,
+                                      float eps, float c1, float c2) {
+  m = __fadd_rn(__fmul_rn(b1, m), __fmul_rn(__fsub_rn(1.f, b1), g));
+  v = __fadd_rn(__fmul_rn(b2, v), __fmul_rn(__fmul_rn(__fsub_rn(1.f, b2), g), g));
+  const float mhat = __fdiv_rn(m, c1);
+  const float vhat = __fdiv_rn(v, c2);
+  p = __fsub_rn(p, __fdiv_rn(__fmul_rn(lr, mhat), __fadd_rn(__fsqrt_rn(vhat), eps)));
+}
+
+__global__ void __launch_bounds__(256) k_adam(size_t n, float* __restrict__ p, float* __restrict__ g,
+                                              float* __restrict__ m, float* __restrict__ v, float lr, float b1,
+                                              float b2, float eps, float c1, float c2, int zero_grad) {
+  pdl_wait();  // the backward's gradient
+  const size_t n4 = n / 4;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  // two float4 groups per thread per iteration: 8 independent 16 B loads in flight
+  for (size_t i0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n4; i0 += 2 * stride) {
+    float4 pp[2], gg[2], mm[2], vv[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const size_t i = i0 + u * stride;
+      if (i < n4) {
+        pp[u] = __ldcs(reinterpret_cast<float4*>(p) + i);
+        gg[u] = __ldcs(reinterpret_cast<float4*>(g) + i);
+        mm[u] = __ldcs(reinterpret_cast<float4*>(m) + i);
+        vv[u] = __ldcs(reinterpret_cast<float4*>(v) + i);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const size_t i = i0 + u * stride;
+      if (i < n4) {
+        adam1(pp[u].x, gg[u].x, mm[u].x, vv[u].x, lr, b1, b2, eps, c1, c2);
+        adam1(pp[u].y, gg[u].y, mm[u].y, vv[u].y, lr, b1, b2, eps, c1, c2);
+        adam1(pp[u].z, gg[u].z, mm[u].z, vv[u].z, lr, b1, b2, eps, c1, c2);
+        adam1(pp[u].w, gg[u].w, mm[u].w, vv[u].w, lr, b1, b2, eps, c1, c2);
+        reinterpret_cast<float4*>(p)[i] = pp[u];
+        __stcs(reinterpret_cast<float4*>(m) + i, mm[u]);
+        __stcs(reinterpret_cast<float4*>(v) + i, vv[u]);
+        if (zero_grad) reinterpret_cast<float4*>(g)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x < n - n4 * 4) {
+    const size_t i = n4 * 4 + threadIdx.x;
+    float gi = g[i];
+    adam1(p[i], gi, m[i], v[i], lr, b1, b2, eps, c1, c2);
+    if (zero_grad) g[i] = 0.f;
+  }
+}
+
+// --------------------------------------------------------- device init
+// Same distributions as init_params (field.cpp:150-166): tables
+// U(-1e-4, 1e-4), weights N(0,1)*sqrt(2/fan_in) (Box-Muller on Philox
+// TAG_INIT draws), biases 0. Not the reference's mt19937 bits.
+__global__ void k_init_params(FieldDesc fd, float* params, uint64_t seed) {
+  const long long n = fd.hash_params + fd.mlp_params;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    float val;
+    if (i < fd.hash_params) {
+      uint32_t x4[4];
+      philox_draw(seed, PRENOM_TAG_INIT, 0u, 0u, (uint32_t)(i >> 2), x4);
+      val = -1e-4f + 2e-4f * pdm_u01(x4[i & 3]);
+    } else {
+      const int j = (int)(i - fd.hash_params);
+      int layer = 0;
+      for (int l = 0; l <= fd.H; ++l)
+        if (j >= fd.w_off[l]) layer = l;
+      const int in = layer == 0 ? fd.in_dim : fd.W;
+      if (j >= fd.b_off[layer]) {
+        val = 0.f;
+      } else {
+        uint32_t x4[4];
+        philox_draw(seed, PRENOM_TAG_INIT, 1u, 0u, (uint32_t)(j >> 1), x4);
+        const int q = (j & 1) * 2;
+        const float u1 = fmaxf(pdm_u01(x4[q]), 1e-7f), u2 = pdm_u01(x4[q + 1]);
+        const float nrm = sqrtf(-2.f * logf(u1)) * cospif(2.f * u2);
+        val = sqrtf(2.f / (float)in) * nrm;
+      }
+    }
+    params[i] = val;
+  }
+}
+
+__global__ void k_philox(int n, const uint32_t* ck, uint32_t* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t ctr[4] = {ck[6 * i], ck[6 * i + 1], ck[6 * i + 2], ck[6 * i + 3]};
+  uint32_t o[4];
+  pdm_philox4x32_10(ctr, ck[6 * i + 4], ck[6 * i + 5], o);
+  for (int j = 0; j < 4; ++j) out[4 * i + j] = o[j];
+}
+
+__global__ void k_reptile_delta(size_t n, const float* meta, const float* adapted, float* delta) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    delta[i] = __fsub_rn(adapted[i], meta[i]);
+}
+
+// meta.cpp:83-92 with adapted = meta + delta_sum / n_tasks.
+__global__ void k_reptile_apply(size_t n, float* meta, const float* delta, float inv_n, float beta) {
+  const float keep = __fsub_rn(1.f, beta);
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const float adapted = __fadd_rn(meta[i], __fmul_rn(delta[i], inv_n));
+    meta[i] = __fadd_rn(__fmul_rn(keep, meta[i]), __fmul_rn(beta, adapted));
+  }
+}
+
+// meta.cpp:83-92: out = keep * meta + beta * adapted (keep = 1 - beta), in place.
+__global__ void k_reptile_update(size_t n, float* meta, const float* adapted, float beta) {
+  const float keep = __fsub_rn(1.f, beta);
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    meta[i] = __fadd_rn(__fmul_rn(keep, meta[i]), __fmul_rn(beta, adapted[i]));
+}
+
+
+
+
+}  // namespace
+
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+cudaError_t launch_adam(size_t n, float* p, float* g, float* m, float* v, float lr, float b1, float b2, float eps,
+                        float c1, float c2, int zero_grad, cudaStream_t st) {
+  const size_t n4 = std::max<size_t>(n / 4, 1);
+  const unsigned grid = (unsigned)std::min<size_t>((n4 + 255) / 256, (size_t)num_sms() * 8);
+  return launch_pdl(k_adam, dim3(grid), dim3(256), 0, st, n, p, g, m, v, lr, b1, b2, eps, c1, c2, zero_grad);
+}
+
+cudaError_t launch_init_params(const FieldDesc& fd, float* params, uint64_t seed, cudaStream_t st) {
+  k_init_params<<<num_sms() * 4, 256, 0, st>>>(fd, params, seed);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_philox(int n, const uint32_t* ck, uint32_t* out, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  k_philox<<<(n + 127) / 128, 128, 0, st>>>(n, ck, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reptile_delta(size_t n, const float* meta, const float* adapted, float* delta, cudaStream_t st) {
+  k_reptile_delta<<<num_sms() * 4, 256, 0, st>>>(n, meta, adapted, delta);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reptile_update(size_t n, float* meta, const float* adapted, float beta, cudaStream_t st) {
+  k_reptile_update<<<num_sms() * 4, 256, 0, st>>>(n, meta, adapted, beta);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reptile_apply(size_t n, float* meta, const float* delta, float inv_n, float beta,
+                                 cudaStream_t st) {
+  k_reptile_apply<<<num_sms() * 4, 256, 0, st>>>(n, meta, delta, inv_n, beta);
+  return cudaGetLastError();
+}
+
+
+}  // namespace prenom

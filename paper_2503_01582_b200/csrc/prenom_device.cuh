@@ -66,6 +66,7 @@ __device__ __forceinline__ void tile_sched_exit(int* ctr) {
 // visible, so every read of predecessor outputs sits after pdl_wait().
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+int num_sms();  // SMs of the current device (kernels_optim.cu)
 bool pdl_enabled();  // PRENOM_NO_PDL=1 disables (A/B)
 
 template <typename... KArgs, typename... Args>
