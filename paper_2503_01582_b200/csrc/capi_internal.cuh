@@ -143,6 +143,8 @@ constexpr int kDefaultLanes = 8;  // B200, with >= 8 tiles per persistent CTA: c
                                   // cfg5 4: 1.10e9, 8: 1.12e9 (1 lane: cfg3 1.00e9)
 constexpr int kMaxLanes = 16;
 constexpr int kLaneMinTilesPerCta = 8;
+constexpr int kL2PersistDefault = 0;  // off: measured on cfg2, persisting the table (1) or its gradient (2)
+                                       // slows the step 0.657 -> 0.745 / 0.772 ms (Adam 0.10 -> 0.17 ms)
 
 struct prenom_ctx_s {
   int device = 0;
@@ -387,9 +389,51 @@ inline prenom_status enqueue_sample(prenom_object_s* o, int64_t step, cudaStream
 // soon as this step's backward has consumed the sample buffers, so it runs
 // concurrently with this step's Adam (it only reads frames and the grid;
 // steps that refresh the grid keep the serial order).
+// L2 residency (SURVEY §7 hard part 4): an access-policy window over one of
+// the object's 64 MiB-class arrays marks its lines persisting in L2, so
+// Adam's 256 MiB stream does not evict them between steps. Mode from
+// PRENOM_L2_PERSIST: 0 off, 1 the hash table (gathers), 2 the table
+// gradient (scatter RMW).
+inline int l2_persist_mode() {
+  static const int m = [] {
+    const char* e = getenv("PRENOM_L2_PERSIST");
+    return e ? atoi(e) : kL2PersistDefault;
+  }();
+  return m;
+}
+
+inline cudaError_t set_l2_window(prenom_object_s* o, cudaStream_t st) {
+  const int mode = l2_persist_mode();
+  if (mode == 0) return cudaSuccess;
+  static size_t max_persist = [] {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxPersistingL2CacheSize, dev);
+    if (v > 0) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)v);
+    return (size_t)(v > 0 ? v : 0);
+  }();
+  static size_t max_window = [] {
+    int dev = 0, v = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+    return (size_t)(v > 0 ? v : 0);
+  }();
+  if (!max_persist || !max_window) return cudaSuccess;
+  const size_t bytes = std::min<size_t>((size_t)o->fd.hash_params * sizeof(float), max_window);
+  cudaStreamAttrValue a;
+  std::memset(&a, 0, sizeof a);
+  a.accessPolicyWindow.base_ptr = mode == 2 ? (void*)o->grad.p : (void*)o->params.p;
+  a.accessPolicyWindow.num_bytes = bytes;
+  a.accessPolicyWindow.hitRatio = std::min(1.f, (float)max_persist / (float)bytes);
+  a.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  a.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  return cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &a);
+}
+
 inline prenom_status enqueue_step(prenom_object_s* o, StepStatsDev* stats, bool has_next = false) {
   NvtxRange nvtx_("prenom.step");
   cudaStream_t st = o->lane ? o->lane : o->ctx->stream;
+  CUDA_TRY(set_l2_window(o, st));
   const prenom_train_cfg& c = o->cfg;
   const int B = c.rays_per_iter, S = c.samples_per_ray;
   const uint32_t step = (uint32_t)o->step;
