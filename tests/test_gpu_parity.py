@@ -466,3 +466,25 @@ def test_bf16_train_loss_tracks_fp32_oracle(ctx, oracle):
     # (atomic-order nondeterminism compounds over 200 steps); the fp32 path is
     # held to the north-star 1% in test_train_200_steps_loss_within_1pct.
     assert abs(lg[-20:].mean() / lo[-20:].mean() - 1) < 0.05, (lg[-20:].mean(), lo[-20:].mean())
+
+
+@pytest.mark.parametrize("B,S,prior,mlp", [(1, 1, 0, 0), (5, 17, 1, 0), (333, 33, 1, 0), (64, 256, 1, 0),
+                                           (7, 24, 1, 1), (333, 33, 0, 1), (64, 256, 1, 1), (130, 96, 1, 1)])
+def test_ragged_batches_first_step(ctx, oracle, B, S, prior, mlp):
+    """Ragged shapes through the whole step (one ray, S not a multiple of 32, the 256-sample
+    maximum, batches not a multiple of a tile or warp), both MLP modes: the first step's
+    samples/frame/escapes equal the oracle's, loss terms within 1e-5 (fp32) / 1e-2 (bf16)."""
+    sc, grid = small_scene()
+    arch = FieldArch(hash_levels=8, features_per_level=2, log2_table_size=12, base_resolution=8,
+                     per_level_scale=1.4, hidden_width=32, hidden_layers=2)
+    cfg = TrainConfig(rays_per_iter=B, samples_per_ray=S, coarse_samples=16, prior_sampling=prior,
+                      grid_refresh_every=0, mlp_precision=mlp)
+    gpu, ob = make_pair(ctx, oracle, arch, cfg, sc, grid)
+    sg, so = gpu.train_step(2), ob.train_step(2)
+    tol = 1e-5 if mlp == 0 else 1e-2
+    for x, y in zip(sg, so):
+        assert x["frame"] == y["frame"] and x["n_samples"] == y["n_samples"] and x["escaped"] == y["escaped"]
+    x, y = sg[0], so[0]
+    for k in ("total", "color", "depth", "sigma"):
+        assert abs(x[k] - y[k]) <= tol * abs(y[k]) + 1e-9, (k, x, y)
+    assert np.isfinite(sg[1]["total"])
