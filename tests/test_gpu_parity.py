@@ -488,3 +488,32 @@ def test_ragged_batches_first_step(ctx, oracle, B, S, prior, mlp):
     for k in ("total", "color", "depth", "sigma"):
         assert abs(x[k] - y[k]) <= tol * abs(y[k]) + 1e-9, (k, x, y)
     assert np.isfinite(sg[1]["total"])
+
+
+def test_empty_and_degenerate_inputs(ctx, oracle):
+    """Edge cases the reference defines: a keyframe without object pixels is a DataError with the
+    reference's message (render.cpp:60); an object filling the whole frame has no band, so every
+    ray is an object ray (render.cpp:66-68); an empty point batch evaluates to nothing; rays that
+    miss the box render colour 0 / depth 0."""
+    from paper_2503_01582_b200 import DataError
+
+    sc, grid = small_scene()
+    arch = FieldArch(hash_levels=4, log2_table_size=10, hidden_width=16, hidden_layers=1)
+    cfg = TrainConfig(rays_per_iter=64, samples_per_ray=8, prior_sampling=0, grid_refresh_every=0)
+    empty = np.zeros_like(sc.mask)
+    ob = ObjectTrainer.create(ctx, arch, grid=grid, seed=1, cfg=cfg, box_min=sc.box_min, box_max=sc.box_max)
+    ob.set_frames(sc.cams, sc.rgb, sc.depth, empty, 1, sc.obj_pose)
+    with pytest.raises(DataError, match="generate_rays: no object pixels"):
+        ob.train_step(1)
+    full = np.ones_like(sc.mask)
+    ob2 = ObjectTrainer.create(ctx, arch, grid=grid, seed=1, cfg=cfg, box_min=sc.box_min, box_max=sc.box_max)
+    ob2.set_frames(sc.cams, sc.rgb, sc.depth, full, 1, sc.obj_pose)
+    g = ob2.debug_generate_rays(0, step=0)
+    o = oracle.generate_rays(sc.cams[0], sc.rgb[0], sc.depth[0], full[0], 1, sc.obj_pose, 64, 0.25, 8, seed=1, step=0)
+    assert np.all(g["kinds"] == g["kinds"][0]) and np.array_equal(g["pick_px"], o["pick_px"])
+    s, c = ob2.field_eval(np.zeros((0, 3), np.float32))
+    assert s.shape == (0,) and c.shape == (0, 3)
+    orig = np.array([[5.0, 5.0, 5.0], [0.0, 0.0, -3.0]], np.float32)
+    dirs = np.array([[1.0, 0.0, 0.0], [0.0, 0.0, 1.0]], np.float32)
+    rgb, dep = ob2.render(orig, dirs)
+    assert np.all(rgb[0] == 0) and dep[0] == 0 and dep[1] > 0
