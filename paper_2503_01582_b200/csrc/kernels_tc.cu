@@ -399,10 +399,10 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
   constexpr int SLD = ScatterSlot<INP>::kLd;
   constexpr int LH = INP / 4;  // levels per half (d_feature columns [h*INP/2, (h+1)*INP/2))
   extern __shared__ __align__(1024) unsigned char smem[];
-  __shared__ uint64_t bar, full_bar, empty_bar;
+  __shared__ uint64_t bar, full_bar[2], empty_bar[2];
   __shared__ uint32_t tbase;
   __shared__ int s_tile;
-  __shared__ long long slot_tile;
+  __shared__ long long slot_tile[2];
   WeightTiles<INP, W, H> wt;
   unsigned char* p = smem;
   wt.carve(p);
@@ -415,10 +415,12 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
   }
   unsigned char* G = p;  // [128][16] g_raw (4 used)
   p += 128 * 16 * 2;
-  unsigned char* D = p;  // [128][W]
-  p += 128 * W * 2;
+  // D_l = dH_l * relu'(H_l) is written over H_l itself (H_l is dead once its
+  // mask is applied), which frees the room for a second d_features slot: the
+  // MLP warps fill slot (t+1)&1 while the scatter warps drain slot t&1.
   unsigned char* zero_end = p;
-  float* slot = reinterpret_cast<float*>(p);  // [128][SLD] d_features of one tile
+  float* const slot0 = reinterpret_cast<float*>(p);  // [2][128][SLD]
+  constexpr int kSlotFloats = ScatterSlot<INP>::kBytes / 4;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid < kMlpThreads) wt.load(fd, params + fd.hash_params, kMlpThreads);
   {
@@ -435,8 +437,10 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
   if (warp == 0) umma::tmem_alloc(&tbase, 256);
   if (tid == 0) {
     umma::mbar_init(&bar, 1);
-    umma::mbar_init(&full_bar, 1);
-    umma::mbar_init(&empty_bar, 1);
+    for (int sidx = 0; sidx < 2; ++sidx) {
+      umma::mbar_init(&full_bar[sidx], 1);
+      umma::mbar_init(&empty_bar[sidx], 1);
+    }
     umma::fence_mbar_init();
   }
   umma::fence_before_sync();
@@ -451,15 +455,16 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
     const int r = (tid - kMlpThreads) & 127;  // sample row in the tile; warp = 32 consecutive samples
     const int lhalf = (tid - kMlpThreads) >> 7;  // levels [lhalf*L/2, ...)
     for (uint32_t k = 0;; ++k) {
-      umma::mbar_wait(&full_bar, k & 1u);
-      const long long t = slot_tile;
+      const int sidx = k & 1u;
+      umma::mbar_wait(&full_bar[sidx], (k >> 1) & 1u);
+      const long long t = slot_tile[sidx];
       if (t < 0) break;
       const long long gs = t * kTile + r;
       const bool valid = gs < n_total && __ldg(count + ray_of(gs, S)) > 0;
       float4 pp = make_float4(0.f, 0.f, 0.f, 0.f);
       if (valid) pp = pos[gs];
       const float px = clamp01(pp.x), py = clamp01(pp.y), pz = clamp01(pp.z);
-      const float* drow = slot + r * SLD;
+      const float* drow = slot0 + sidx * kSlotFloats + r * SLD;
       // levels [lhalf*LH, (lhalf+1)*LH) belong to this half; the MLP warps
       // scatter the first mlp_levels of them straight from registers
       const int l_lo = lhalf * LH + mlp_levels;
@@ -469,7 +474,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
         scatter_level(fd, grad, l, valid, px, py, pz, dv.x, dv.y, lane, skip_scatter, pull_max);
       }
       named_sync(2, kScatThreads);  // every scatter thread is done with the slot
-      if (tid == kMlpThreads) mbar_arrive(&empty_bar);
+      if (tid == kMlpThreads) mbar_arrive(&empty_bar[sidx]);
     }
   } else {
     // ================= MLP warps: tensor-core backward chain
@@ -569,7 +574,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
             const __nv_bfloat16* hb = reinterpret_cast<const __nv_bfloat16*>(&hv);
 #pragma unroll
             for (int j = 0; j < 8; ++j) v[j] = __bfloat162float(hb[j]) > 0.f ? v[j] : 0.f;
-            umma::st_row8(D, row, col, W, v);
+            umma::st_row8(Ht[l], row, col, HC, v);  // D_l in place of H_l
           }
         }
         mlp_sync_for_mma();
@@ -578,15 +583,15 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
           const unsigned char* prev = l == 0 ? X : Ht[l - 1];
           const int pc = l == 0 ? XC : HC;
           for (int ks = 0; ks < 8; ++ks)
-            umma::mma_bf16(tm + dwc, umma::desc_mnmajor(prev, pc, ks), umma::desc_mnmajor(D, W, ks),
+            umma::mma_bf16(tm + dwc, umma::desc_mnmajor(prev, pc, ks), umma::desc_mnmajor(Ht[l], HC, ks),
                            umma::idesc_bf16(128, W, true, true), (iter > 0 || ks > 0));
           if (l > 0) {
             for (int ks = 0; ks < W / 16; ++ks)
-              umma::mma_bf16(tr, umma::desc_kmajor(D, W, ks), umma::desc_mnmajor(wt.wl[l - 1], W, ks),
+              umma::mma_bf16(tr, umma::desc_kmajor(Ht[l], HC, ks), umma::desc_mnmajor(wt.wl[l - 1], W, ks),
                              umma::idesc_bf16(128, W, false, true), ks > 0);
           } else {
             for (int ks = 0; ks < W / 16; ++ks)
-              umma::mma_bf16(tr, umma::desc_kmajor(D, W, ks), umma::desc_mnmajor(wt.w0, INP, ks),
+              umma::mma_bf16(tr, umma::desc_kmajor(Ht[l], HC, ks), umma::desc_mnmajor(wt.w0, INP, ks),
                              umma::idesc_bf16(128, INP, false, true), ks > 0);
           }
           umma::commit(&bar);
@@ -601,14 +606,15 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
 #pragma unroll
         for (int c = 0; c < NH; c += 8) umma::tmem_ld8(umma::taddr(tr, 32 * q, half * NH + c), v + c);
         umma::tmem_wait_ld();
-        umma::mbar_wait(&empty_bar, ((uint32_t)iter & 1u) ^ 1u);
-        float* dst = slot + row * SLD + half * NH;
+        const int sidx = iter & 1;
+        umma::mbar_wait(&empty_bar[sidx], (((uint32_t)iter >> 1) & 1u) ^ 1u);
+        float* dst = slot0 + sidx * kSlotFloats + row * SLD + half * NH;
 #pragma unroll
         for (int c = 0; c < NH; c += 4) *reinterpret_cast<float4*>(dst + c) = make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]);
-        if (tid == 0) slot_tile = t;
+        if (tid == 0) slot_tile[sidx] = t;
         umma::fence_before_sync();
         named_sync(1, kMlpThreads);
-        if (tid == 0) mbar_arrive(&full_bar);
+        if (tid == 0) mbar_arrive(&full_bar[sidx]);
         // this half's first mlp_levels levels: scattered here, overlapping the
         // scatter warps' share of the same tile
         if (mlp_levels > 0 && skip_scatter != 2) {
@@ -625,9 +631,10 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
     }
     // sentinel: stop the scatter warps
     if (tid == 0) {
-      umma::mbar_wait(&empty_bar, ((uint32_t)iter & 1u) ^ 1u);
-      slot_tile = -1;
-      mbar_arrive(&full_bar);
+      const int sidx = iter & 1;
+      umma::mbar_wait(&empty_bar[sidx], (((uint32_t)iter >> 1) & 1u) ^ 1u);
+      slot_tile[sidx] = -1;
+      mbar_arrive(&full_bar[sidx]);
     }
     // ---- flush the TMEM weight-gradient accumulators: row = input unit (or the
     // ones row = bias), column = output unit; one atomicAdd per weight per CTA
@@ -692,7 +699,7 @@ size_t fwd_smem() {
 template <int INP, int W, int H>
 size_t bwd_smem() {
   return WeightTiles<INP, W, H>::kBytes + ((H * W + 4) * 4 + 15) / 16 * 16 + (128 * (INP + 8) * 2 + kSlackX) +
-         H * (128 * (W + 8) * 2 + kSlackH) + 128 * 16 * 2 + 128 * W * 2 + ScatterSlot<INP>::kBytes + 1024;
+         H * (128 * (W + 8) * 2 + kSlackH) + 128 * 16 * 2 + 2 * ScatterSlot<INP>::kBytes + 1024;
 }
 
 template <int INP, int W, int H, int NT>
