@@ -142,6 +142,37 @@ __device__ __forceinline__ void epi_relu(uint32_t tm, int col0, const float* bia
   }
 }
 
+// epi_relu for the backward's forward recompute (G = 2); also returns this
+// thread's ReLU gate, bit c = (bf16 H[row][half*N/2 + c] > 0), so the D_l
+// epilogue needs no shared-memory read of H_l.
+template <int N>
+__device__ __forceinline__ uint32_t epi_relu_gate(uint32_t tm, const float* bias, unsigned char* tile, int C) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int q = warp & 3, half = warp >> 2;
+  const int row = 32 * q + lane;
+  constexpr int NH = N / 2;
+  static_assert(NH % 8 == 0 && NH <= 32, "8-column TMEM loads, 32-bit gate");
+  uint32_t gate = 0;
+#pragma unroll
+  for (int c = 0; c < NH; c += 8) {
+    const int col = half * NH + c;
+    float v[8];
+    umma::tmem_ld8(umma::taddr(tm, 32 * q, col), v);
+    umma::tmem_wait_ld();
+    uint32_t pk[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const __nv_bfloat162 b = __floats2bfloat162_rn(fmaxf(v[2 * i] + bias[col + 2 * i], 0.f),
+                                                     fmaxf(v[2 * i + 1] + bias[col + 2 * i + 1], 0.f));
+      pk[i] = *reinterpret_cast<const uint32_t*>(&b);
+      gate |= ((pk[i] & 0x7FFFu) ? 1u : 0u) << (c + 2 * i);
+      gate |= ((pk[i] & 0x7FFF0000u) ? 1u : 0u) << (c + 2 * i + 1);
+    }
+    *reinterpret_cast<uint4*>(tile + umma::cm_offset(row, col, C)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+  }
+  return gate;
+}
+
 // ------------------------------------------------------------------ fwd
 // NT threads: NT/128 threads per sample share the levels in the encode and
 // the columns in the epilogues.
@@ -509,7 +540,8 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
         umma::commit(&bar);
       }
       wait_mma(&bar, phase);
-      epi_relu<W>(tr, 0, wt.bias, Ht[0], HC);
+      uint32_t gate[2];
+      gate[0] = epi_relu_gate<W>(tr, wt.bias, Ht[0], HC);
       for (int l = 1; l < H; ++l) {
         mlp_sync_for_mma();
         if (tid == 0) {
@@ -519,7 +551,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
           umma::commit(&bar);
         }
         wait_mma(&bar, phase);
-        epi_relu<W>(tr, 0, wt.bias + l * W, Ht[l], HC);
+        gate[l] = epi_relu_gate<W>(tr, wt.bias + l * W, Ht[l], HC);
       }
       mlp_sync_for_mma();
       if (tid == 0) {
@@ -570,10 +602,8 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
             float v[8];
             umma::tmem_ld8(umma::taddr(tr, 32 * q, col), v);
             umma::tmem_wait_ld();
-            const uint4 hv = *reinterpret_cast<const uint4*>(Ht[l] + umma::cm_offset(row, col, HC));
-            const __nv_bfloat16* hb = reinterpret_cast<const __nv_bfloat16*>(&hv);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) v[j] = __bfloat162float(hb[j]) > 0.f ? v[j] : 0.f;
+            for (int j = 0; j < 8; ++j) v[j] = (gate[l] >> (c + j)) & 1u ? v[j] : 0.f;
             umma::st_row8(Ht[l], row, col, HC, v);  // D_l in place of H_l
           }
         }
