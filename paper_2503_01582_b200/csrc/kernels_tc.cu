@@ -430,7 +430,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
   constexpr int SLD = ScatterSlot<INP>::kLd;
   constexpr int LH = INP / 4;  // levels per half (d_feature columns [h*INP/2, (h+1)*INP/2))
   extern __shared__ __align__(1024) unsigned char smem[];
-  __shared__ uint64_t bar, full_bar[2], empty_bar[2];
+  __shared__ uint64_t bar, xbar, full_bar[2], empty_bar[2];
   __shared__ uint32_t tbase;
   __shared__ int s_tile;
   __shared__ long long slot_tile[2];
@@ -468,6 +468,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
   if (warp == 0) umma::tmem_alloc(&tbase, 256);
   if (tid == 0) {
     umma::mbar_init(&bar, 1);
+    umma::mbar_init(&xbar, 1);
     for (int sidx = 0; sidx < 2; ++sidx) {
       umma::mbar_init(&full_bar[sidx], 1);
       umma::mbar_init(&empty_bar[sidx], 1);
@@ -510,7 +511,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
   } else {
     // ================= MLP warps: tensor-core backward chain
     const uint32_t tr = tm + CM::kR;
-    uint32_t phase = 0;
+    uint32_t phase = 0, xphase = 0;
     int iter = 0;
     const int q = warp & 3, half = warp >> 2, row = 32 * q + lane;
     auto fetch = [&]() -> long long {
@@ -522,14 +523,16 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
       const long long tile0 = t * kTile;
       const long long gs = tile0 + row;
       const bool valid = gs < n_total && __ldg(count + ray_of(gs, S)) > 0;
-      // ---- stored bf16 features -> X (row-group stride differs: copy per 16 B)
-      {
-        const uint4* src = feat_tiles + t * (128 * INP * 2 / 16);
-        for (int i = tid; i < 128 * INP * 2 / 16; i += kMlpThreads) {
-          const int rg = i / INP, rem = i % INP;  // INP uint4 per row group
-          *reinterpret_cast<uint4*>(X + rg * (XC / 8) * 128 + (rem >> 3) * 128 + (rem & 7) * 16) = src[i];
-        }
+      // ---- stored bf16 features -> X by the TMA engine (no LSU work): one
+      // bulk copy per 8-row group (the X row-group stride is longer: ones column)
+      if (tid == 0) {
+        const unsigned char* src = reinterpret_cast<const unsigned char*>(feat_tiles + t * (128 * INP * 2 / 16));
+        umma::mbar_arrive_expect_tx(&xbar, 128 * INP * 2);
+        for (int rg = 0; rg < 16; ++rg)
+          umma::bulk_g2s(X + rg * (XC / 8) * 128, src + rg * INP * 16, INP * 16, &xbar);
       }
+      umma::mbar_wait(&xbar, xphase);
+      xphase ^= 1u;
       mlp_sync_for_mma();
       if (skip_scatter != 3) {  // (profiling knob 3: scatter-only timing -- the MLP chain is skipped)
       // ---- forward recompute (field.cpp:181-211), one TMEM region reused per layer

@@ -166,6 +166,19 @@ __device__ __forceinline__ uint32_t taddr(uint32_t base, int lane, int col) {
   return base + ((uint32_t)lane << 16) + (uint32_t)col;
 }
 
+// TMA bulk copy global -> shared (no tensor map: 1-D, 16 B aligned, size % 16
+// == 0), completing `bytes` of transaction count on the mbarrier.
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* mbar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mbar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(mbar))
+               : "memory");
+}
+
 // Store 8 consecutive bf16 of row r, columns [c0, c0+8) (c0 % 8 == 0) as one
 // 16-byte vector into a core-matrix tile with C columns.
 __device__ __forceinline__ void st_row8(unsigned char* tile, int r, int c0, int C, const float* v) {
