@@ -383,15 +383,18 @@ struct BwdCols {
   static constexpr int kDWl = 16;                // layers H-1..1: [128 x W] each
   static constexpr int kDW0 = kDWl + (H - 1) * W;  // [128 x W]  (in | 1) x out
   static constexpr int kR = kDW0 + W;            // working region, 64 columns
-  static constexpr int kTotal = kR + 64;
+  static constexpr int kDF = kR + 64;            // d_features of the tile being handed over
+  static constexpr int kTotal = kDF + INP;
   static_assert(kTotal <= 256, "TMEM budget");
 };
 
 // Warp-specialized: warps 0-7 ("MLP warps", named barrier 1) run the
-// tensor-core chain of a tile and hand its fp32 d_features to warps 8-11
-// ("scatter warps", named barrier 2) through one shared-memory slot guarded
-// by full/empty mbarriers; the scatter of tile t overlaps the MMA chain of
-// tile t+1.
+// tensor-core chain of a tile; its last MMA writes the fp32 d_features into a
+// TMEM slot that warps 8-15 ("scatter warps") load straight into registers
+// (TMEM lane quadrant = warp % 4 = their sample rows), guarded by full/empty
+// mbarriers. A consumer releases the slot as soon as it holds the values, so
+// the scatter of tile t overlaps the MMA chain of tile t+1 and no d_features
+// pass through shared memory.
 constexpr int kMlpThreads = 256;
 constexpr int kScatThreads = 256;  // two warps per 32-sample group: level halves
 constexpr int kBwdMlpLevels = 1;   // per half, scattered by the MLP warps (measured on cfg2)
@@ -413,11 +416,9 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(umma::smem_u32(bar)) : "memory");
 }
 
-template <int INP>
-struct ScatterSlot {
-  static constexpr int kLd = INP + 4;  // floats per row (float4 rows, bank-spread)
-  static constexpr int kBytes = 128 * kLd * 4;
-};
+__device__ __forceinline__ void mbar_arrive2(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], 2;" ::"r"(umma::smem_u32(bar)) : "memory");
+}
 
 template <int INP, int W, int H>
 __global__ void __launch_bounds__(kBwdThreads, 2)
@@ -427,13 +428,13 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
              int pull_max) {
   using CM = BwdCols<INP, W, H>;
   constexpr int XC = INP + 8, HC = W + 8;
-  constexpr int SLD = ScatterSlot<INP>::kLd;
-  constexpr int LH = INP / 4;  // levels per half (d_feature columns [h*INP/2, (h+1)*INP/2))
+  constexpr int NH = INP / 2;  // d_feature columns per half: [h*NH, (h+1)*NH)
+  constexpr int LH = INP / 4;  // levels per half
   extern __shared__ __align__(1024) unsigned char smem[];
-  __shared__ uint64_t bar, xbar, full_bar[2], empty_bar[2];
+  __shared__ uint64_t bar, xbar, full_bar, empty_bar;
   __shared__ uint32_t tbase;
   __shared__ int s_tile;
-  __shared__ long long slot_tile[2];
+  __shared__ long long slot_tile;
   WeightTiles<INP, W, H> wt;
   unsigned char* p = smem;
   wt.carve(p);
@@ -447,11 +448,8 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
   unsigned char* G = p;  // [128][16] g_raw (4 used)
   p += 128 * 16 * 2;
   // D_l = dH_l * relu'(H_l) is written over H_l itself (H_l is dead once its
-  // mask is applied), which frees the room for a second d_features slot: the
-  // MLP warps fill slot (t+1)&1 while the scatter warps drain slot t&1.
+  // ReLU gate is taken)
   unsigned char* zero_end = p;
-  float* const slot0 = reinterpret_cast<float*>(p);  // [2][128][SLD]
-  constexpr int kSlotFloats = ScatterSlot<INP>::kBytes / 4;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid < kMlpThreads) wt.load(fd, params + fd.hash_params, kMlpThreads);
   {
@@ -469,10 +467,10 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
   if (tid == 0) {
     umma::mbar_init(&bar, 1);
     umma::mbar_init(&xbar, 1);
-    for (int sidx = 0; sidx < 2; ++sidx) {
-      umma::mbar_init(&full_bar[sidx], 1);
-      umma::mbar_init(&empty_bar[sidx], 1);
-    }
+    umma::mbar_init(&full_bar, 2);  // the MMA commit + the issuing thread (slot_tile written)
+    // one arrival per consumer warp: the scatter warps, and the MLP warps when
+    // they scatter levels themselves
+    umma::mbar_init(&empty_bar, kScatThreads / 32 + (mlp_levels > 0 ? kMlpThreads / 32 : 0));
     umma::fence_mbar_init();
   }
   umma::fence_before_sync();
@@ -487,26 +485,36 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
     const int r = (tid - kMlpThreads) & 127;  // sample row in the tile; warp = 32 consecutive samples
     const int lhalf = (tid - kMlpThreads) >> 7;  // levels [lhalf*L/2, ...)
     for (uint32_t k = 0;; ++k) {
-      const int sidx = k & 1u;
-      umma::mbar_wait(&full_bar[sidx], (k >> 1) & 1u);
-      const long long t = slot_tile[sidx];
+      umma::mbar_wait(&full_bar, k & 1u);
+      const long long t = slot_tile;
       if (t < 0) break;
+      umma::fence_after_sync();
+      // this half's d_features: TMEM -> registers, then the slot is released
+      float d[NH];
+#pragma unroll
+      for (int c = 0; c < NH; c += 8) umma::tmem_ld8(umma::taddr(tm + CM::kDF, 32 * (warp & 3), lhalf * NH + c), d + c);
+      umma::tmem_wait_ld();
+      umma::fence_before_sync();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_bar);
       const long long gs = t * kTile + r;
       const bool valid = gs < n_total && __ldg(count + ray_of(gs, S)) > 0;
       float4 pp = make_float4(0.f, 0.f, 0.f, 0.f);
       if (valid) pp = pos[gs];
       const float px = clamp01(pp.x), py = clamp01(pp.y), pz = clamp01(pp.z);
-      const float* drow = slot0 + sidx * kSlotFloats + r * SLD;
       // levels [lhalf*LH, (lhalf+1)*LH) belong to this half; the MLP warps
-      // scatter the first mlp_levels of them straight from registers
-      const int l_lo = lhalf * LH + mlp_levels;
+      // scatter the first mlp_levels of them. The level's pair is always
+      // d[0], d[1] (the array shifts down), so the loop stays rolled without
+      // indexing registers dynamically.
+      const int l_lo = lhalf * LH;
       const int l_hi = skip_scatter == 2 ? l_lo : min(fd.L, (lhalf + 1) * LH);
+#pragma unroll 1
       for (int l = l_lo; l < l_hi; ++l) {  // warp-uniform
-        const float2 dv = *reinterpret_cast<const float2*>(drow + 2 * l);
-        scatter_level(fd, grad, l, valid, px, py, pz, dv.x, dv.y, lane, skip_scatter, pull_max);
+        if (l >= l_lo + mlp_levels)
+          scatter_level(fd, grad, l, valid, px, py, pz, d[0], d[1], lane, skip_scatter, pull_max);
+#pragma unroll
+        for (int i = 0; i + 2 < NH; ++i) d[i] = d[i + 2];
       }
-      named_sync(2, kScatThreads);  // every scatter thread is done with the slot
-      if (tid == kMlpThreads) mbar_arrive(&empty_bar[sidx]);
     }
   } else {
     // ================= MLP warps: tensor-core backward chain
@@ -623,51 +631,54 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
               umma::mma_bf16(tr, umma::desc_kmajor(Ht[l], HC, ks), umma::desc_mnmajor(wt.wl[l - 1], W, ks),
                              umma::idesc_bf16(128, W, false, true), ks > 0);
           } else {
+            // d_features -> the TMEM slot, once every consumer holds the previous tile's
+            umma::mbar_wait(&empty_bar, ((uint32_t)iter & 1u) ^ 1u);
+            slot_tile = t;
             for (int ks = 0; ks < W / 16; ++ks)
-              umma::mma_bf16(tr, umma::desc_kmajor(Ht[l], HC, ks), umma::desc_mnmajor(wt.w0, INP, ks),
+              umma::mma_bf16(tm + CM::kDF, umma::desc_kmajor(Ht[l], HC, ks), umma::desc_mnmajor(wt.w0, INP, ks),
                              umma::idesc_bf16(128, INP, false, true), ks > 0);
           }
           umma::commit(&bar);
+          if (l == 0) {
+            umma::commit(&full_bar);
+            mbar_arrive(&full_bar);
+          }
         }
         wait_mma(&bar, phase);
       }
-      }  // skip_scatter != 3
-      // ---- hand d_features to the scatter warps (slot free once they drained it)
-      {
-        constexpr int NH = INP / 2;
-        float v[NH];
-#pragma unroll
-        for (int c = 0; c < NH; c += 8) umma::tmem_ld8(umma::taddr(tr, 32 * q, half * NH + c), v + c);
+      } else if (tid == 0) {  // (knob 3: no chain; hand over the stale slot)
+        umma::mbar_wait(&empty_bar, ((uint32_t)iter & 1u) ^ 1u);
+        slot_tile = t;
+        mbar_arrive2(&full_bar);
+      }
+      // ---- this half's first mlp_levels levels, scattered by the MLP warps
+      // straight from the slot, overlapping the scatter warps' share
+      if (mlp_levels > 0) {
+        float v[8];
+        umma::tmem_ld8(umma::taddr(tm + CM::kDF, 32 * q, half * NH), v);
         umma::tmem_wait_ld();
-        const int sidx = iter & 1;
-        umma::mbar_wait(&empty_bar[sidx], (((uint32_t)iter >> 1) & 1u) ^ 1u);
-        float* dst = slot0 + sidx * kSlotFloats + row * SLD + half * NH;
-#pragma unroll
-        for (int c = 0; c < NH; c += 4) *reinterpret_cast<float4*>(dst + c) = make_float4(v[c], v[c + 1], v[c + 2], v[c + 3]);
-        if (tid == 0) slot_tile[sidx] = t;
         umma::fence_before_sync();
-        named_sync(1, kMlpThreads);
-        if (tid == 0) mbar_arrive(&full_bar[sidx]);
-        // this half's first mlp_levels levels: scattered here, overlapping the
-        // scatter warps' share of the same tile
-        if (mlp_levels > 0 && skip_scatter != 2) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty_bar);
+        if (skip_scatter != 2) {
           float4 pp = make_float4(0.f, 0.f, 0.f, 0.f);
           if (valid) pp = pos[gs];
           const float px = clamp01(pp.x), py = clamp01(pp.y), pz = clamp01(pp.z);
-              const int l0 = half * LH;
+          const int l0 = half * LH;
+#pragma unroll 1
+          for (int j = 0; j < mlp_levels && l0 + j < fd.L; ++j) {  // warp-uniform
+            scatter_level(fd, grad, l0 + j, valid, px, py, pz, v[0], v[1], lane, skip_scatter, pull_max);
 #pragma unroll
-          for (int j = 0; j < NH / 2; ++j)
-            if (j < mlp_levels && l0 + j < fd.L)  // warp-uniform
-              scatter_level(fd, grad, l0 + j, valid, px, py, pz, v[2 * j], v[2 * j + 1], lane, skip_scatter, pull_max);
+            for (int i = 0; i < 6; ++i) v[i] = v[i + 2];
+          }
         }
       }
     }
     // sentinel: stop the scatter warps
     if (tid == 0) {
-      const int sidx = iter & 1;
-      umma::mbar_wait(&empty_bar[sidx], (((uint32_t)iter >> 1) & 1u) ^ 1u);
-      slot_tile[sidx] = -1;
-      mbar_arrive(&full_bar[sidx]);
+      umma::mbar_wait(&empty_bar, ((uint32_t)iter & 1u) ^ 1u);
+      slot_tile = -1;
+      mbar_arrive2(&full_bar);
     }
     // ---- flush the TMEM weight-gradient accumulators: row = input unit (or the
     // ones row = bias), column = output unit; one atomicAdd per weight per CTA
@@ -732,7 +743,7 @@ size_t fwd_smem() {
 template <int INP, int W, int H>
 size_t bwd_smem() {
   return WeightTiles<INP, W, H>::kBytes + ((H * W + 4) * 4 + 15) / 16 * 16 + (128 * (INP + 8) * 2 + kSlackX) +
-         H * (128 * (W + 8) * 2 + kSlackH) + 128 * 16 * 2 + 2 * ScatterSlot<INP>::kBytes + 1024;
+         H * (128 * (W + 8) * 2 + kSlackH) + 128 * 16 * 2 + 1024;
 }
 
 template <int INP, int W, int H, int NT>
@@ -790,7 +801,8 @@ cudaError_t run_bwd(const FieldDesc& fd, const float* params, float* grad, long 
     const char* v = getenv("PRENOM_BWD_MLP_LEVELS");
     return v ? atoi(v) : -1;
   }();
-  const int mlp_levels = std::max(0, std::min(INP / 4, mlp_env >= 0 ? mlp_env : kBwdMlpLevels));
+  // the MLP warps load 8 slot columns: at most 4 levels per half
+  const int mlp_levels = std::max(0, std::min(std::min(4, INP / 4), mlp_env >= 0 ? mlp_env : kBwdMlpLevels));
   static const int skip = getenv("PRENOM_PROF_SKIP_SCATTER") ? atoi(getenv("PRENOM_PROF_SKIP_SCATTER")) : 0;
   // longest run reduced by pulls (else by the shuffle tree); PRENOM_BWD_PULL_MAX overrides
   static const int pull_max = getenv("PRENOM_BWD_PULL_MAX") ? atoi(getenv("PRENOM_BWD_PULL_MAX")) : kBwdPullMax;
