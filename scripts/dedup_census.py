@@ -73,3 +73,31 @@ nv = int(valid.sum())
 print(f"total per valid sample: run {tot['run'] / nv:.2f}  pair {tot['pair'] / nv:.2f}  ideal {tot['ideal'] / nv:.2f}"
       f"  -> pair saves {1 - tot['pair'] / tot['run']:.1%}, ideal {1 - tot['ideal'] / tot['run']:.1%}, "
       f"one-hop {1 - tot['hop'] / tot['run']:.1%}")
+
+# ---- shuffle census of the run reduction (warp-uniform strategy per level-warp)
+print("\nshuffles per warp-level: current (pull<=4 else tree) vs best of {pull, tree, per-cell butterfly}")
+cur_tot = best_tot = 0
+nwl = 0
+for l in range(arch.hash_levels):
+    res = arch.level_resolution(l)
+    c = np.minimum((pos * np.float32(res)).astype(np.int64), res - 1)
+    key = (c[:, 2] * res + c[:, 1]) * res + c[:, 0]
+    key = np.where(valid, key, -1 - np.arange(n) % 32)
+    kw = key.reshape(-1, 32)
+    head = np.ones_like(kw, bool)
+    head[:, 1:] = kw[:, 1:] != kw[:, :-1]
+    cur = best = 0
+    for w in range(len(kw)):
+        hs = np.nonzero(head[w])[0]
+        ends = np.append(hs[1:], 32)
+        rmax = int((ends - hs).max())
+        pull = 5 * (rmax - 1)
+        tree = 16 * int(np.ceil(np.log2(rmax))) if rmax > 1 else 0
+        bfly = 18 * len(hs)
+        cur += pull if rmax <= 4 else tree
+        best += min(pull, tree, bfly)
+    cur_tot += cur
+    best_tot += best
+    nwl += len(kw)
+    print(f"{l:5d} cur {cur / len(kw):6.1f}  best {best / len(kw):6.1f}")
+print(f"all levels: cur {cur_tot / nwl:.1f} best {best_tot / nwl:.1f} per warp-level")
