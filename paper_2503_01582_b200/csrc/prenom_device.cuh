@@ -209,22 +209,6 @@ __device__ __forceinline__ float corner_weight(const LevelCell& c, int corner) {
 
 // One level of encode_point (field.cpp:75-98); feat[F] accumulated in
 // corner order with separate mul/add roundings (no FMA), skipping w == 0.
-#ifndef PRENOM_FINE_L1
-#define PRENOM_FINE_L1 0
-#endif
-// gathers of a hashed (fine) level: their rows are random in a 2^T table, so
-// L1 allocation only evicts the coarse levels' reusable lines
-__device__ __forceinline__ float2 ldg_f2_fine(const float2* p) {
-  float2 v;
-  if (PRENOM_FINE_L1 == 1)
-    asm volatile("ld.global.nc.L1::no_allocate.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
-  else if (PRENOM_FINE_L1 == 2)
-    asm volatile("ld.global.nc.L1::evict_first.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
-  else
-    v = __ldg(p);
-  return v;
-}
-
 template <int F>
 __device__ __forceinline__ void encode_level(const FieldDesc& fd, const float* __restrict__ params,
                                              int l, float px, float py, float pz, float* feat) {
@@ -239,8 +223,7 @@ __device__ __forceinline__ void encode_level(const FieldDesc& fd, const float* _
                                    (uint32_t)(c.cz + ((corner >> 2) & 1)));
     w[corner] = corner_weight(c, corner);
     if constexpr (F == 2) {
-      const float2* a = reinterpret_cast<const float2*>(tab + (size_t)row * 2);
-      const float2 v = fd.dense_verts[l] ? __ldg(a) : ldg_f2_fine(a);
+      const float2 v = __ldg(reinterpret_cast<const float2*>(tab + (size_t)row * 2));
       e[corner][0] = v.x;
       e[corner][1] = v.y;
     } else {
