@@ -33,7 +33,11 @@ constexpr int kThreads = 256;
 // forward launch shape (measured on B200, cfg2): see run_fwd
 constexpr int kFwdThreadsDefault = 256;
 constexpr int kFwdCtasDefault = 3;
-constexpr int kFwdSmemKbDefault = 57;
+constexpr int kFwdSmemKbDefault = 40;
+// 3 CTAs x (40 + 1) KB fit a 132 KB carve-out, leaving 124 KB of L1 for the
+// encode's gathers (was 57 KB/CTA padding, 196 KB carve-out, 60 KB of L1:
+// k_fwd_tc 0.195 -> 0.186 ms on cfg2)
+constexpr int kFwdCarveoutDefault = 58;
 constexpr int kSlack = 0;       // weight tiles are never over-read
 // M=128 MN-major views of the (features|1) and (activations|1) tiles read
 // past the tile end (finite garbage rows that are never flushed)
@@ -753,6 +757,16 @@ cudaError_t run_fwd_nt(const FieldDesc& fd, const float* params, long long n, in
   const size_t smem = std::max<size_t>(fwd_smem<INP, W, H>(), min_smem);
   cudaError_t e = cudaFuncSetAttribute(k_fwd_tc<INP, W, H, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
+  // shared-memory carve-out (percent of the maximum): the rest of the 256 KB
+  // array is L1, which serves the encode's gathers; PRENOM_FWD_CARVEOUT for tuning
+  static const int carveout = [] {
+    const char* v = getenv("PRENOM_FWD_CARVEOUT");
+    return v ? atoi(v) : kFwdCarveoutDefault;
+  }();
+  if (carveout >= 0) {
+    e = cudaFuncSetAttribute(k_fwd_tc<INP, W, H, NT>, cudaFuncAttributePreferredSharedMemoryCarveout, carveout);
+    if (e != cudaSuccess) return e;
+  }
   const long long ntiles = (n + kTile - 1) / kTile;
   const long long grid = std::min<long long>((ntiles + min_tiles_per_cta() - 1) / min_tiles_per_cta(), (long long)ctas * sms());
 #ifdef PRENOM_VAR_FWD_MEMSET
