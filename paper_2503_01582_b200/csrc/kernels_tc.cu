@@ -804,9 +804,23 @@ cudaError_t run_fwd(const FieldDesc& fd, const float* params, long long n, int S
 template <int INP, int W, int H>
 cudaError_t run_bwd(const FieldDesc& fd, const float* params, float* grad, long long n, int S, const int* count,
                     const float4* pos, const void* feat_tiles, const float4* dout, int* tile_ctr, cudaStream_t st) {
-  const size_t smem = std::max<size_t>(bwd_smem<INP, W, H>(), 80 * 1024);  // two CTAs (2 x 256 TMEM cols) per SM
+  // two CTAs (2 x 256 TMEM columns) per SM: the shared-memory floor keeps a
+  // third CTA out; PRENOM_BWD_SMEM_KB / PRENOM_BWD_CARVEOUT for tuning
+  static const size_t min_smem = [] {
+    const char* v = getenv("PRENOM_BWD_SMEM_KB");
+    return (size_t)(v ? atoi(v) : 80) * 1024;
+  }();
+  static const int carveout = [] {
+    const char* v = getenv("PRENOM_BWD_CARVEOUT");
+    return v ? atoi(v) : -1;
+  }();
+  const size_t smem = std::max<size_t>(bwd_smem<INP, W, H>(), min_smem);
   cudaError_t e = cudaFuncSetAttribute(k_bwd_tc<INP, W, H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
+  if (carveout >= 0) {
+    e = cudaFuncSetAttribute(k_bwd_tc<INP, W, H>, cudaFuncAttributePreferredSharedMemoryCarveout, carveout);
+    if (e != cudaSuccess) return e;
+  }
   const long long ntiles = (n + kTile - 1) / kTile;
   const long long grid = std::min<long long>((ntiles + min_tiles_per_cta() - 1) / min_tiles_per_cta(), 2LL * sms());
   // levels per half the MLP warps scatter themselves (they would otherwise
