@@ -149,14 +149,14 @@ __device__ __forceinline__ void epi_relu(uint32_t tm, int col0, const float* bia
 // epi_relu for the backward's forward recompute (G = 2); also returns this
 // thread's ReLU gate, bit c = (bf16 H[row][half*N/2 + c] > 0), so the D_l
 // epilogue needs no shared-memory read of H_l.
-template <int N>
-__device__ __forceinline__ uint32_t epi_relu_gate(uint32_t tm, const float* bias, unsigned char* tile, int C) {
+template <int N, int MG>
+__device__ __forceinline__ uint64_t epi_relu_gate(uint32_t tm, const float* bias, unsigned char* tile, int C) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q = warp & 3, half = warp >> 2;
   const int row = 32 * q + lane;
-  constexpr int NH = N / 2;
-  static_assert(NH % 8 == 0 && NH <= 32, "8-column TMEM loads, 32-bit gate");
-  uint32_t gate = 0;
+  constexpr int NH = N / MG;
+  static_assert(NH % 8 == 0 && NH <= 64, "8-column TMEM loads, 64-bit gate");
+  uint64_t gate = 0;
 #pragma unroll
   for (int c = 0; c < NH; c += 8) {
     const int col = half * NH + c;
@@ -169,8 +169,8 @@ __device__ __forceinline__ uint32_t epi_relu_gate(uint32_t tm, const float* bias
       const __nv_bfloat162 b = __floats2bfloat162_rn(fmaxf(v[2 * i] + bias[col + 2 * i], 0.f),
                                                      fmaxf(v[2 * i + 1] + bias[col + 2 * i + 1], 0.f));
       pk[i] = *reinterpret_cast<const uint32_t*>(&b);
-      gate |= ((pk[i] & 0x7FFFu) ? 1u : 0u) << (c + 2 * i);
-      gate |= ((pk[i] & 0x7FFF0000u) ? 1u : 0u) << (c + 2 * i + 1);
+      gate |= ((pk[i] & 0x7FFFu) ? 1ull : 0ull) << (c + 2 * i);
+      gate |= ((pk[i] & 0x7FFF0000u) ? 1ull : 0ull) << (c + 2 * i + 1);
     }
     *reinterpret_cast<uint4*>(tile + umma::cm_offset(row, col, C)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
   }
@@ -399,7 +399,12 @@ struct BwdCols {
 // mbarriers. A consumer releases the slot as soon as it holds the values, so
 // the scatter of tile t overlaps the MMA chain of tile t+1 and no d_features
 // pass through shared memory.
-constexpr int kMlpThreads = 256;
+#ifndef PRENOM_BWD_MLP_WARPS
+#define PRENOM_BWD_MLP_WARPS 8
+#endif
+constexpr int kMlpWarps = PRENOM_BWD_MLP_WARPS;  // 8: two column groups per row quadrant; 4: one
+constexpr int kMG = kMlpWarps / 4;
+constexpr int kMlpThreads = 32 * kMlpWarps;
 constexpr int kScatThreads = 256;  // two warps per 32-sample group: level halves
 constexpr int kBwdMlpLevels = 1;   // per half, scattered by the MLP warps (measured on cfg2)
 constexpr int kBwdPullMax = 4;     // scatter_level: pull-reduce runs up to this length (cfg2 sweep 1/4/8/12/16: 4 best)
@@ -555,8 +560,8 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
         umma::commit(&bar);
       }
       wait_mma(&bar, phase);
-      uint32_t gate[2];
-      gate[0] = epi_relu_gate<W>(tr, wt.bias, Ht[0], HC);
+      uint64_t gate[2];
+      gate[0] = epi_relu_gate<W, kMG>(tr, wt.bias, Ht[0], HC);
       for (int l = 1; l < H; ++l) {
         mlp_sync_for_mma();
         if (tid == 0) {
@@ -566,7 +571,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
           umma::commit(&bar);
         }
         wait_mma(&bar, phase);
-        gate[l] = epi_relu_gate<W>(tr, wt.bias + l * W, Ht[l], HC);
+        gate[l] = epi_relu_gate<W, kMG>(tr, wt.bias + l * W, Ht[l], HC);
       }
       mlp_sync_for_mma();
       if (tid == 0) {
@@ -610,15 +615,15 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
       for (int l = H - 1; l >= 0; --l) {
         // D_l = dH_l * relu'(H_l) -> D tile
         {
-          constexpr int NH = W / 2;
+          constexpr int NHD = W / kMG;
 #pragma unroll
-          for (int c = 0; c < NH; c += 8) {
-            const int col = half * NH + c;
+          for (int c = 0; c < NHD; c += 8) {
+            const int col = half * NHD + c;
             float v[8];
             umma::tmem_ld8(umma::taddr(tr, 32 * q, col), v);
             umma::tmem_wait_ld();
 #pragma unroll
-            for (int j = 0; j < 8; ++j) v[j] = (gate[l] >> (c + j)) & 1u ? v[j] : 0.f;
+            for (int j = 0; j < 8; ++j) v[j] = (gate[l] >> (c + j)) & 1ull ? v[j] : 0.f;
             umma::st_row8(Ht[l], row, col, HC, v);  // D_l in place of H_l
           }
         }
@@ -658,8 +663,11 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
       // ---- this half's first mlp_levels levels, scattered by the MLP warps
       // straight from the slot, overlapping the scatter warps' share
       if (mlp_levels > 0) {
-        float v[8];
-        umma::tmem_ld8(umma::taddr(tm + CM::kDF, 32 * q, half * NH), v);
+        // (knob 3 has no MMA to order this load after the slot's hand-over)
+        if (skip_scatter == 3) umma::mbar_wait(&full_bar, (uint32_t)iter & 1u);
+        float v[2 / kMG][8];
+#pragma unroll
+        for (int k = 0; k < 2 / kMG; ++k) umma::tmem_ld8(umma::taddr(tm + CM::kDF, 32 * q, (half + k) * NH), v[k]);
         umma::tmem_wait_ld();
         umma::fence_before_sync();
         __syncwarp();
@@ -668,12 +676,15 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
           float4 pp = make_float4(0.f, 0.f, 0.f, 0.f);
           if (valid) pp = pos[gs];
           const float px = clamp01(pp.x), py = clamp01(pp.y), pz = clamp01(pp.z);
-          const int l0 = half * LH;
-#pragma unroll 1
-          for (int j = 0; j < mlp_levels && l0 + j < fd.L; ++j) {  // warp-uniform
-            scatter_level(fd, grad, l0 + j, valid, px, py, pz, v[0], v[1], lane, skip_scatter, pull_max);
 #pragma unroll
-            for (int i = 0; i < 6; ++i) v[i] = v[i + 2];
+          for (int k = 0; k < 2 / kMG; ++k) {
+            const int l0 = (half + k) * LH;
+#pragma unroll 1
+            for (int j = 0; j < mlp_levels && l0 + j < fd.L; ++j) {  // warp-uniform
+              scatter_level(fd, grad, l0 + j, valid, px, py, pz, v[k][0], v[k][1], lane, skip_scatter, pull_max);
+#pragma unroll
+              for (int i2 = 0; i2 < 6; ++i2) v[k][i2] = v[k][i2 + 2];
+            }
           }
         }
       }
