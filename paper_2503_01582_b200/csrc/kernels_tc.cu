@@ -240,12 +240,9 @@ __global__ void __launch_bounds__(NT) k_fwd_tc(FieldDesc fd, const float* __rest
       for (int ks = 0; ks < INP / 16; ++ks)
         umma::mma_bf16(tm, umma::desc_kmajor(X, INP, ks), umma::desc_kmajor(wt.w0, INP, ks), id_l0, ks > 0);
       umma::commit(&bar);
-    }
-    // stored features for the backward pass (tile-major, same core-matrix layout)
-    {
-      const uint4* src = reinterpret_cast<const uint4*>(X);
-      uint4* dst = feat_tiles + t * (128 * INP * 2 / 16);
-      for (int i = tid; i < 128 * INP * 2 / 16; i += NT) dst[i] = src[i];
+      // stored features for the backward pass (tile-major, same core-matrix
+      // layout), written by the TMA engine: no LSU work next to the gathers
+      umma::bulk_s2g(feat_tiles + t * (128 * INP * 2 / 16), X, 128 * INP * 2);
     }
     wait_mma(&bar, phase);
     epi_relu<W, TPS>(tm, 0, wt.bias, Hb, W);
@@ -287,8 +284,10 @@ __global__ void __launch_bounds__(NT) k_fwd_tc(FieldDesc fd, const float* __rest
         out[gs] = o;
       }
     }
+    if (tid == 0) umma::bulk_wait_read();  // X is rewritten by the next tile's encode
     umma::fence_before_sync();
   }
+  if (tid == 0) umma::bulk_wait_all();
 #ifndef PRENOM_VAR_FWD_MEMSET
   tile_sched_exit(tile_ctr);
 #endif
