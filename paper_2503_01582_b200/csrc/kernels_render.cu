@@ -26,7 +26,10 @@ __device__ __forceinline__ double warp_sum(double v) {
 // K (samples per lane) is a template parameter so the per-lane arrays are
 // sized to the batch (S = 96 -> 3): registers, and so occupancy, follow S.
 template <int K>
-__global__ void __launch_bounds__(kWarps * 32) k_composite(CompositeArgs a, int frame) {
+// 4 blocks/SM caps it at 64 registers (94 unbounded; a 32-byte spill):
+// 32 resident warps hide the fp64 scans' latency (cfg2 0.0285 -> 0.0241 ms;
+// 5 blocks/SM, 48 registers, spills more and is slower)
+__global__ void __launch_bounds__(kWarps * 32, 4) k_composite(CompositeArgs a, int frame) {
   __shared__ double red[kWarps][4];
   __shared__ unsigned long long red_n[kWarps];
   __shared__ int red_e[kWarps];
