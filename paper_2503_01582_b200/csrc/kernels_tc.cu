@@ -406,7 +406,8 @@ constexpr int kMG = kMlpWarps / 4;
 constexpr int kMlpThreads = 32 * kMlpWarps;
 constexpr int kScatThreads = 256;  // two warps per 32-sample group: level halves
 constexpr int kBwdMlpLevels = 1;   // per half, scattered by the MLP warps (measured on cfg2)
-constexpr int kBwdPullMax = 4;     // scatter_level: pull-reduce runs up to this length (cfg2 sweep 1/4/8/12/16: 4 best)
+constexpr int kBwdPullMax = 4;     // scatter_level: pull-reduce runs up to this length (cfg2 sweeps:
+                                   // 2-4 equal, 6 / 8 / 12 slower by 0.3 / 1 / 3.5%: pulls cost ALU, the tree shuffles)
 constexpr int kBwdThreads = kMlpThreads + kScatThreads;
 
 __device__ __forceinline__ void named_sync(int id, int n) {
