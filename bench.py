@@ -51,7 +51,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
     ap.add_argument("--width", type=int, default=64)
-    ap.add_argument("--mlp", default="bf16", choices=["fp32", "bf16"])
+    ap.add_argument("--mlp", default="bf16", choices=["fp32", "bf16", "bf16x3"])
     ap.add_argument("--rays", type=int, default=8192)
     ap.add_argument("--samples", type=int, default=96)
     ap.add_argument("--e2e-steps", type=int, default=100)
@@ -62,6 +62,12 @@ def parse():
 
 
 # ------------------------------------------------------------------ setup
+def mlp_id(name):
+    from paper_2503_01582_b200 import _capi
+
+    return {"fp32": _capi.MLP_FP32, "bf16": _capi.MLP_BF16, "bf16x3": _capi.MLP_BF16X3}[name]
+
+
 def dist_info():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -77,14 +83,13 @@ def launched_distributed() -> bool:
 
 def make_workload(args, rank):
     from paper_2503_01582_b200 import TrainConfig, scenes
-    from paper_2503_01582_b200._capi import MLP_BF16, MLP_FP32
 
     sc = scenes.box_union_scene(n_views=50, res=256, seed=1000 + rank)
     grid = scenes.occupancy_prior(sc.boxes, R=32)
     arch = scenes.cfg2_arch(args.width)
     cfg = TrainConfig(rays_per_iter=args.rays, samples_per_ray=args.samples, coarse_samples=32, prior_sampling=1,
                       grid_refresh_every=50, eta=1e-2, bg_fraction=0.25,
-                      mlp_precision=MLP_BF16 if args.mlp == "bf16" else MLP_FP32)
+                      mlp_precision=mlp_id(args.mlp))
     return sc, grid, arch, cfg
 
 
@@ -219,13 +224,12 @@ class Cfg1(Workload):
 
     def __init__(self, args, ctx, rank, ws):
         from paper_2503_01582_b200 import ObjectTrainer, TrainConfig, scenes
-        from paper_2503_01582_b200._capi import MLP_BF16, MLP_FP32
 
         self.sc = scenes.sphere_scene(seed=rank)
         self.arch = scenes.cfg1_arch()
         self.cfg = TrainConfig(rays_per_iter=4096, samples_per_ray=64, prior_sampling=0, grid_refresh_every=0,
                                eta=1e-2, bg_fraction=0.25,
-                               mlp_precision=MLP_BF16 if args.mlp == "bf16" else MLP_FP32)
+                               mlp_precision=mlp_id(args.mlp))
         self.obj = ObjectTrainer.create(ctx, self.arch, theta=None, grid_res=8, seed=rank, cfg=self.cfg,
                                         box_min=self.sc.box_min, box_max=self.sc.box_max)
         self.obj.set_frames(self.sc.cams, self.sc.rgb, self.sc.depth, self.sc.mask, 1, self.sc.obj_pose)
@@ -295,14 +299,13 @@ class Cfg3(Workload):
 
     def __init__(self, args, ctx, rank, ws):
         from paper_2503_01582_b200 import FieldArch, ObjectTrainer, TrainConfig, scenes
-        from paper_2503_01582_b200._capi import MLP_BF16, MLP_FP32
         from paper_2503_01582_b200.parallel import shard_lpt, step_cost
 
         cats = mixed_category_archs()
         n_obj = 32
         archs = [cats[i % 4] for i in range(n_obj)]
         self.cfg = TrainConfig(rays_per_iter=2048, samples_per_ray=96, coarse_samples=32, prior_sampling=1,
-                               grid_refresh_every=50, mlp_precision=MLP_BF16 if args.mlp == "bf16" else MLP_FP32)
+                               grid_refresh_every=50, mlp_precision=mlp_id(args.mlp))
         shards = shard_lpt([step_cost(a, 2048, 96) for a in archs], ws)
         self.mine = shards[rank]
         self.objs, self.archs = [], []
@@ -354,14 +357,13 @@ class Cfg4(Workload):
 
     def __init__(self, args, ctx, rank, ws):
         from paper_2503_01582_b200 import ObjectTrainer, TrainConfig, scenes
-        from paper_2503_01582_b200._capi import MLP_BF16, MLP_FP32
         from paper_2503_01582_b200.meta import CudaEngine
 
         self.ws, self.rank = ws, rank
         self.dist = launched_distributed()
         self.arch = scenes.cfg4_arch()
         self.cfg = TrainConfig(rays_per_iter=4096, samples_per_ray=64, prior_sampling=0, grid_refresh_every=0,
-                               mlp_precision=MLP_BF16 if args.mlp == "bf16" else MLP_FP32)
+                               mlp_precision=mlp_id(args.mlp))
         self.q = 32
         self.meta = ObjectTrainer.create(ctx, self.arch, theta=None, grid_res=8, seed=4242, cfg=self.cfg)
         self.workers = []
@@ -375,6 +377,16 @@ class Cfg4(Workload):
             w.train_step(1, stats=False)
         self.objs = self.workers + [self.meta]
         self.engine = CudaEngine(self.meta, self.workers)
+        if self.dist:
+            # the Reptile all-reduce runs inside the C ABI (prenom_reptile_step) on an NCCL
+            # communicator bound to the context; torch.distributed only ships the unique id
+            import torch.distributed as dist
+
+            from paper_2503_01582_b200.trainer import comm_unique_id
+
+            uid = [comm_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0)
+            ctx.init_comm(ws, rank, uid[0])
         self.n_objects_total = ws
         self.k = 0
         self.n = 0
@@ -385,8 +397,6 @@ class Cfg4(Workload):
                       "l2": "inputs larger than L2 (params+Adam state 128 MiB per task + meta); no flush"}
 
     def step(self, k):
-        import torch
-
         from paper_2503_01582_b200.trainer import derive_seed
 
         for _ in range(k):
@@ -396,11 +406,8 @@ class Cfg4(Workload):
             self.n += sum(s["n_samples"] for s in st)
             if not self.dist:
                 self.engine.update_exact(t, 0.1)
-            else:
-                buf = self.engine.delta_sum([t])
-                with torch.cuda.stream(self.engine.stream):  # NCCL on the library stream
-                    torch.distributed.all_reduce(buf)
-                self.engine.apply(buf, self.ws, 0.1)
+            else:  # delta sum -> ncclAllReduce -> interpolation, one C call on the library stream
+                self.engine.reptile_step([t], self.ws, 0.1)
             self.k += 1
 
     def samples(self, k):
@@ -439,13 +446,12 @@ class Cfg5(Workload):
 
     def __init__(self, args, ctx, rank, ws):
         from paper_2503_01582_b200 import ObjectTrainer, TrainConfig, scenes
-        from paper_2503_01582_b200._capi import MLP_BF16, MLP_FP32
 
         cats = mixed_category_archs()
         per_gpu = 32
         rays = (1 << 22) // (per_gpu * 96) + 1  # 1366: 32 x 1366 x 96 >= 2^22
         self.cfg = TrainConfig(rays_per_iter=rays, samples_per_ray=96, coarse_samples=32, prior_sampling=1,
-                               grid_refresh_every=50, mlp_precision=MLP_BF16 if args.mlp == "bf16" else MLP_FP32)
+                               grid_refresh_every=50, mlp_precision=mlp_id(args.mlp))
         self.mine = [rank * per_gpu + j for j in range(per_gpu)]  # objects are independent: block-sharded
         self.objs, self.archs = [], []
         res, views = 512, 100
@@ -843,8 +849,33 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def free_port() -> int:
+    import socket
+
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def respawn_distributed(args) -> int:
+    """`bench.py --gpus N` outside torchrun: re-exec this command under
+    torch.distributed.run with N ranks (one per GPU, rendezvous on 127.0.0.1)."""
+    import subprocess
+
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if args.gpus < 1:
+        raise SystemExit("--gpus must be >= 1")
+    if args.gpus > 1 and not launched_distributed():
+        sys.exit(respawn_distributed(args))
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws} ranks were launched")
     if args.impl == "reference":
         run_reference(args)
     else:

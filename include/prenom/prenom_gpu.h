@@ -75,7 +75,13 @@ enum {
 };
 
 enum { PRENOM_ACT_EXP_CLAMPED = 0, PRENOM_ACT_SOFTPLUS = 1 };
-enum { PRENOM_MLP_FP32 = 0, PRENOM_MLP_BF16 = 1 };
+/* MLP arithmetic of the train step:
+ *   FP32      fp32 SIMT GEMMs (1e-4 parity path, no tensor cores);
+ *   BF16      tcgen05 kind::f16, bf16 operands, fp32 accumulation (1e-2);
+ *   BF16X3    tcgen05 kind::f16 on split operands x = hi + lo (both bf16):
+ *             hi*hi + hi*lo + lo*hi, fp32 accumulation -- ~16 significand
+ *             bits per product, fp32-class results (1e-4) on tensor cores. */
+enum { PRENOM_MLP_FP32 = 0, PRENOM_MLP_BF16 = 1, PRENOM_MLP_BF16X3 = 2 };
 enum { PRENOM_KIND_OBJECT = 0, PRENOM_KIND_BACKGROUND = 1 };
 
 /* Mirrors noma::FieldArch (core/include/noma/field.hpp:20-31). */
@@ -319,6 +325,29 @@ prenom_status prenom_reptile_apply(prenom_object_t meta, const float* delta_dev,
 prenom_status prenom_object_copy_params(prenom_object_t dst, prenom_object_t src);
 /* meta <- (1 - beta) * meta + beta * adapted, exactly meta.cpp:83-92 (one task). */
 prenom_status prenom_reptile_update(prenom_object_t meta, prenom_object_t adapted, float beta);
+
+/* ---- multi-GPU Reptile: the path's one collective ---------
+ * One process per GPU. Rank 0 makes an NCCL unique id, the caller ships its
+ * PRENOM_COMM_ID_BYTES bytes to every rank (any transport), and each rank
+ * binds a communicator to its context. NCCL is loaded at run time
+ * (libnccl.so.2 or $PRENOM_NCCL_LIB); without it these calls fail with
+ * PRENOM_CUDA and everything else works. */
+#define PRENOM_COMM_ID_BYTES 128
+prenom_status prenom_comm_unique_id(uint8_t* id /* PRENOM_COMM_ID_BYTES */);
+prenom_status prenom_ctx_init_comm(prenom_ctx_t ctx, int nranks, int rank, const uint8_t* id);
+/* nranks = 0 when no communicator is bound; nccl_version as ncclGetVersion. */
+prenom_status prenom_ctx_comm_info(prenom_ctx_t ctx, int* nranks, int* rank, int* nccl_version);
+/* One Reptile outer step over a meta-batch of n_tasks tasks, n_adapted of
+ * them adapted on this rank (meta.cpp:94-120 batched across GPUs):
+ *   s = sum over this rank's tasks of (theta_i - theta)       (one kernel)
+ *   s = ncclAllReduce(s, sum) over the context's communicator  (if one is bound)
+ *   theta <- (1 - beta) theta + beta (theta + s / n_tasks)    = reptile_update
+ *                                                (meta, mean adapted, beta)
+ * With one task and no communicator it is exactly reptile_update(meta,
+ * adapted, beta) (meta.cpp:83-92). Asynchronous on the meta context stream;
+ * every rank of the communicator must call it (n_adapted may be 0). */
+prenom_status prenom_reptile_step(prenom_object_t meta, const prenom_object_t* adapted,
+                                  int n_adapted, int n_tasks, float beta);
 /* Philox key of the object's draws (inner_adapt uses mt19937(derive_seed(seed,
  * step)) per meta-step, meta.cpp:111; here: set_seed(derive_seed(...))). */
 prenom_status prenom_object_set_seed(prenom_object_t obj, uint64_t seed);
@@ -336,6 +365,8 @@ prenom_status prenom_debug_hash_encode(prenom_ctx_t ctx, const prenom_field_arch
 prenom_status prenom_debug_field_eval(prenom_ctx_t ctx, const prenom_field_arch* arch,
                                       const float* params, int n, const float* xyz,
                                       float* sigma, float* rgb, float* raw, int mlp_precision);
+/* (mlp_precision 0: exact per-point kernel; 1 / 2: the tcgen05 train-path tile
+ * forward in bf16 / split bf16; 3: the fp32 SIMT train-path tile forward.) */
 /* Sum over points of field_backward (field.cpp:227-293) into grad (P floats,
  * overwritten). */
 prenom_status prenom_debug_field_backward(prenom_ctx_t ctx, const prenom_field_arch* arch,

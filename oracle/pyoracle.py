@@ -408,6 +408,7 @@ class Ref(_Lib):
                                             C.c_uint32, C.c_int, f32p, f32p, i32p, f32p, f32p, i32p]),
             "ref_refresh_grid": (C.c_int, [rarch, f32p, C.c_int, f32p]),
             "ref_reptile_update": (C.c_int, [sz, f32p, f32p, C.c_float, f32p]),
+            "ref_meta_task_order": (C.c_int, [sz, C.c_uint64, C.c_int, C.POINTER(C.c_int64)]),
             "ref_marching_cubes": (C.c_int, [C.c_int, f32p, C.c_float, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
             "ref_mesh_get": (None, [f32p, i32p]),
             "ref_cube_case_triangles": (C.c_int, [C.c_int, i32p]),
@@ -686,6 +687,13 @@ class Ref(_Lib):
         out = np.zeros_like(meta)
         self._check(self.lib.ref_reptile_update(len(meta), fptr(meta), fptr(adapted), beta, fptr(out)))
         return out
+
+    def meta_task_order(self, n_tasks, seed, n_epochs):
+        """meta_train's per-epoch task order (meta.cpp:104-110), epochs x tasks."""
+        out = np.zeros(n_tasks * n_epochs, np.int64)
+        self._check(self.lib.ref_meta_task_order(n_tasks, seed, n_epochs,
+                                                 out.ctypes.data_as(C.POINTER(C.c_int64))))
+        return out.reshape(n_epochs, n_tasks)
 
     def trainer(self, arch, params, grid, grid_R, cams, rgb, depth, mask, inst, pose, bmin, bmax, cfg, seed):
         """Persistent reference train_track state (frames converted once)."""

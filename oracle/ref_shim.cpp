@@ -672,6 +672,32 @@ int ref_reptile_update(std::size_t n, const float* meta, const float* adapted, f
   REF_GUARD_END
 }
 
+// meta_train's task order (meta.cpp:101-110): `order` starts as iota and is
+// reshuffled in place at every epoch by std::shuffle over
+// std::mt19937(derive_seed(seed, 0xE9C6 + epoch)) -- this toolchain's
+// libstdc++, as the reference binary would run it. derive_seed lives in
+// meta.cpp's anonymous namespace (meta.cpp:14-20) and is restated here.
+// out: n_epochs x n_tasks indices, epoch-major.
+int ref_meta_task_order(std::size_t n_tasks, std::uint64_t seed, int n_epochs, std::int64_t* out) {
+  REF_GUARD_BEGIN
+  auto derive = [](std::uint64_t base, std::uint64_t salt) {
+    std::uint64_t s = base * 0x9E3779B97F4A7C15ULL + salt * 0xBF58476D1CE4E5B9ULL + 1;
+    s ^= s >> 31;
+    s *= 0x94D049BB133111EBULL;
+    s ^= s >> 29;
+    return static_cast<std::uint32_t>(s ^ (s >> 32));
+  };
+  std::vector<std::size_t> order(n_tasks);
+  for (std::size_t i = 0; i < n_tasks; ++i) order[i] = i;
+  for (int e = 0; e < n_epochs; ++e) {
+    std::mt19937 shuffle_rng(derive(seed, 0xE9C6ULL + static_cast<std::size_t>(e)));
+    std::shuffle(order.begin(), order.end(), shuffle_rng);
+    for (std::size_t i = 0; i < n_tasks; ++i) out[(std::size_t)e * n_tasks + i] = (std::int64_t)order[i];
+  }
+  return 0;
+  REF_GUARD_END
+}
+
 }  // extern "C"
 
 // Restatement of train_track (mapper.cpp:130-184) on the public API with

@@ -17,7 +17,9 @@ LIB_PATH = PKG_DIR / "_lib" / "libprenom_b200.so"
 PRENOM_OK, PRENOM_USAGE, PRENOM_DATA, PRENOM_NUMERIC, PRENOM_CUDA = range(5)
 TAG_FRAME, TAG_PIXEL, TAG_FINE, TAG_BG, TAG_RENDER, TAG_INIT, TAG_SYNTH = 1, 2, 3, 4, 5, 6, 7
 ACT_EXP_CLAMPED, ACT_SOFTPLUS = 0, 1
-MLP_FP32, MLP_BF16 = 0, 1
+MLP_FP32, MLP_BF16, MLP_BF16X3 = 0, 1, 2
+DEBUG_TILE_FP32 = 3
+COMM_ID_BYTES = 128  # prenom_debug_field_eval: the fp32 SIMT train-path tile forward
 KERNEL_CLASSES = ["sample", "field_fwd", "composite", "mlp_bwd", "encode_bwd", "adam", "refresh"]
 
 
@@ -146,6 +148,7 @@ EXPORTED = [
     "prenom_get_adam", "prenom_reset_adam", "prenom_set_adam", "prenom_train_step_many",
     "prenom_reptile_delta", "prenom_reptile_apply", "prenom_object_copy_params", "prenom_reptile_update",
     "prenom_object_set_seed",
+    "prenom_comm_unique_id", "prenom_ctx_init_comm", "prenom_ctx_comm_info", "prenom_reptile_step",
     "prenom_debug_philox", "prenom_debug_hash_encode", "prenom_debug_field_eval",
     "prenom_debug_field_backward", "prenom_debug_adam", "prenom_debug_sample_rays",
     "prenom_debug_batch_loss", "prenom_debug_generate_rays", "prenom_debug_umma_gemm",
@@ -229,6 +232,10 @@ def _declare(lib):
         "prenom_object_copy_params": (i32, [P, P]),
         "prenom_reptile_update": (i32, [P, P, C.c_float]),
         "prenom_object_set_seed": (i32, [P, u64]),
+        "prenom_comm_unique_id": (i32, [u8p]),
+        "prenom_ctx_init_comm": (i32, [P, i32, i32, u8p]),
+        "prenom_ctx_comm_info": (i32, [P, i32p, i32p, i32p]),
+        "prenom_reptile_step": (i32, [P, C.POINTER(P), i32, i32, C.c_float]),
         "prenom_debug_philox": (i32, [P, i32, u32p, u32p]),
         "prenom_debug_hash_encode": (i32, [P, archp, f32p, i32, f32p, f32p]),
         "prenom_debug_field_eval": (i32, [P, archp, f32p, i32, f32p, f32p, f32p, f32p, i32]),

@@ -71,6 +71,7 @@ prenom_status prenom_ctx_destroy(prenom_ctx_t ctx) {
   }
   cudaStreamSynchronize(ctx->side);
   cudaStreamDestroy(ctx->side);
+  comm_destroy(ctx);
   for (auto l : ctx->lanes) {
     cudaStreamSynchronize(l);
     cudaStreamDestroy(l);
@@ -148,10 +149,11 @@ prenom_status prenom_object_create(prenom_ctx_t ctx, const prenom_field_arch* ar
     return fail(PRENOM_USAGE, "coarse_samples must be in [1, 1024]");
   for (int a = 0; a < 3; ++a)
     if (!(box_max[a] > box_min[a])) return fail(PRENOM_DATA, "degenerate object box");
-  if (cfg->mlp_precision == PRENOM_MLP_BF16 && !tc_supported(make_desc(*arch)))
-    return fail(PRENOM_USAGE, "bf16 tensor-core MLP needs F=2, L*F<=32, W in {32,64}, H in {1,2}");
-  if (cfg->mlp_precision != PRENOM_MLP_FP32 && cfg->mlp_precision != PRENOM_MLP_BF16)
+  if (cfg->mlp_precision != PRENOM_MLP_FP32 && cfg->mlp_precision != PRENOM_MLP_BF16 &&
+      cfg->mlp_precision != PRENOM_MLP_BF16X3)
     return fail(PRENOM_USAGE, "unknown mlp_precision");
+  if (cfg->mlp_precision != PRENOM_MLP_FP32 && !tc_supported(make_desc(*arch)))
+    return fail(PRENOM_USAGE, "tensor-core MLP needs F=2, L*F<=32, W in {32,64}, H in {1,2}");
   CUDA_TRY(cudaSetDevice(ctx->device));
   auto* o = new prenom_object_s;
   o->ctx = ctx;

@@ -46,6 +46,9 @@ prenom_status prenom_debug_hash_encode(prenom_ctx_t ctx, const prenom_field_arch
 }
 
 namespace {
+// prenom_debug_field_eval precision selecting the fp32 SIMT tile forward
+constexpr int kDebugTileFp32 = 3;
+
 // Points as B = n one-sample "rays" through the train-path tile kernels.
 struct PointBatch {
   DevBuf<float> params, feat_t, dfeat_t, grad;
@@ -59,7 +62,7 @@ struct PointBatch {
     CUDA_TRY(params.ensure(P));
     CUDA_TRY(feat_t.ensure(npad * fd.in_dim));
     CUDA_TRY(dfeat_t.ensure(npad * fd.in_dim));
-    if (tc_supported(fd)) CUDA_TRY(feat_tc.ensure(tc_feature_bytes(fd, n)));
+    if (tc_supported(fd)) CUDA_TRY(feat_tc.ensure(tc_feature_bytes(fd, n, 1)));
     CUDA_TRY(pos.ensure(npad));
     CUDA_TRY(out.ensure(npad));
     CUDA_TRY(dout.ensure(npad));
@@ -112,14 +115,16 @@ prenom_status prenom_debug_field_eval(prenom_ctx_t ctx, const prenom_field_arch*
     if (raw) CUDA_TRY(cudaMemcpyAsync(raw, dw.p, 4 * sizeof(float) * n, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaMemcpyAsync(&hflag, flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
-  } else if (precision == 2 || precision == PRENOM_MLP_BF16) {
-    // the train-path tile forward: fp32 smem GEMMs (2) or bf16 tcgen05 (1)
-    if (precision == PRENOM_MLP_BF16 && !tc_supported(fd)) return fail(PRENOM_USAGE, "arch not supported by the bf16 path");
+  } else if (precision == kDebugTileFp32 || precision == PRENOM_MLP_BF16 || precision == PRENOM_MLP_BF16X3) {
+    // the train-path tile forward: fp32 smem GEMMs (kDebugTileFp32) or tcgen05
+    // (bf16 / split bf16)
+    const bool tc = precision != kDebugTileFp32;
+    if (tc && !tc_supported(fd)) return fail(PRENOM_USAGE, "arch not supported by the tensor-core path");
     PointBatch pb;
     STATUS_TRY(pb.init(fd, P, n, params, xyz, st));
-    if (precision == PRENOM_MLP_BF16)
+    if (tc)
       CUDA_TRY(launch_fwd_tc(fd, pb.params.p, n, 1, pb.count.p, pb.pos.p, pb.feat_tc.p, pb.out.p, pb.flag.p, pb.ctr.p,
-                             st));
+                             precision == PRENOM_MLP_BF16X3, st));
     else
       CUDA_TRY(launch_field_fwd_train(fd, pb.params.p, n, 1, pb.sb, pb.feat_t.p, pb.out.p, pb.flag.p, st));
     ctx->launches += 1;
@@ -163,12 +168,13 @@ prenom_status prenom_debug_field_backward(prenom_ctx_t ctx, const prenom_field_a
   std::vector<float4> hd(n);
   for (int i = 0; i < n; ++i) hd[i] = make_float4(d_sigma[i], d_rgb[3 * i], d_rgb[3 * i + 1], d_rgb[3 * i + 2]);
   CUDA_TRY(cudaMemcpyAsync(pb.dout.p, hd.data(), sizeof(float4) * n, cudaMemcpyHostToDevice, st));
-  if (precision == PRENOM_MLP_BF16) {
-    if (!tc_supported(fd)) return fail(PRENOM_USAGE, "arch not supported by the bf16 path");
+  if (precision == PRENOM_MLP_BF16 || precision == PRENOM_MLP_BF16X3) {
+    if (!tc_supported(fd)) return fail(PRENOM_USAGE, "arch not supported by the tensor-core path");
+    const int split = precision == PRENOM_MLP_BF16X3;
     CUDA_TRY(launch_fwd_tc(fd, pb.params.p, n, 1, pb.count.p, pb.pos.p, pb.feat_tc.p, pb.out.p, pb.flag.p, pb.ctr.p,
-                           st));
+                           split, st));
     CUDA_TRY(launch_bwd_tc(fd, pb.params.p, pb.grad.p, n, 1, pb.count.p, pb.pos.p, pb.feat_tc.p, pb.dout.p,
-                           pb.ctr.p + 2, st));
+                           pb.ctr.p + 2, split, st));
   } else {
     CUDA_TRY(launch_field_fwd_train(fd, pb.params.p, n, 1, pb.sb, pb.feat_t.p, pb.out.p, pb.flag.p, st));
     CUDA_TRY(launch_mlp_bwd_train(fd, pb.params.p, pb.grad.p, n, 1, pb.count.p, pb.feat_t.p, pb.dout.p,

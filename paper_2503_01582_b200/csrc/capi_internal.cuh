@@ -32,6 +32,8 @@ namespace prenom_capi {
 
 inline thread_local std::string g_err;
 
+void comm_destroy(prenom_ctx_t ctx);  // capi_comm.cu
+
 inline prenom_status fail(prenom_status s, const std::string& msg) {
   g_err = msg;
   return s;
@@ -157,6 +159,12 @@ struct prenom_ctx_s {
   std::vector<cudaEvent_t> lane_ev;
   cudaEvent_t fork_ev = nullptr;
   int64_t launches = 0;
+  // NCCL communicator of the Reptile all-reduce (prenom_ctx_init_comm; an
+  // opaque ncclComm_t, NCCL is loaded at run time) and its buffers
+  void* comm = nullptr;
+  int comm_size = 1, comm_rank = 0;
+  DevBuf<float> reptile_sum;          // this rank's sum of task deltas, all-reduced in place
+  DevBuf<const float*> reptile_ptrs;  // adapted parameter vectors of one reptile step
   McMesh mc_dbg;  // prenom_debug_marching_cubes result
   McScratch mc;   // extraction scratch shared by the context's objects
   const void* mc_grid_owner = nullptr;  // object whose lattice mc.grid holds
@@ -278,6 +286,10 @@ struct prenom_object_s {
 
 namespace prenom_capi {
 
+// tensor-core MLP modes (bf16 / split bf16) and their split flag
+inline bool uses_tc(const prenom_object_s* o) { return o->cfg.mlp_precision != PRENOM_MLP_FP32; }
+inline int tc_split(const prenom_object_s* o) { return o->cfg.mlp_precision == PRENOM_MLP_BF16X3 ? 1 : 0; }
+
 inline prenom_status ensure_scratch(prenom_object_s* o, int B, int S) {
   const size_t N = (size_t)B * S;
   const size_t Npad = ((N + kTile - 1) / kTile) * kTile;
@@ -285,8 +297,8 @@ inline prenom_status ensure_scratch(prenom_object_s* o, int B, int S) {
   CUDA_TRY(o->delta.ensure(Npad));
   CUDA_TRY(o->out.ensure(Npad));
   CUDA_TRY(o->dout.ensure(Npad));
-  if (o->cfg.mlp_precision == PRENOM_MLP_BF16) {
-    CUDA_TRY(o->feat_tc.ensure(tc_feature_bytes(o->fd, (long long)N)));
+  if (uses_tc(o)) {
+    CUDA_TRY(o->feat_tc.ensure(tc_feature_bytes(o->fd, (long long)N, tc_split(o))));
     if (!o->tile_ctr.p) {  // [fwd next, fwd done (self-resetting), bwd next (memset per launch), -]
       CUDA_TRY(o->tile_ctr.ensure(4));
       CUDA_TRY(cudaMemset(o->tile_ctr.p, 0, 4 * sizeof(int)));
@@ -447,12 +459,12 @@ inline prenom_status enqueue_step(prenom_object_s* o, StepStatsDev* stats, bool 
     STATUS_TRY(enqueue_sample(o, o->step, st));
   }
   o->upload_pending = false;  // any later sampling is ordered after this step's
-  const bool tc = c.mlp_precision == PRENOM_MLP_BF16;
+  const bool tc = uses_tc(o);
   {
     ProfScope ps(o->ctx, PRENOM_K_FIELD_FWD, st);
     if (tc)
       CUDA_TRY(launch_fwd_tc(o->fd, o->params.p, (long long)B * S, S, sb.count, sb.pos_depth, o->feat_tc.p, o->out.p,
-                             o->flag.p, o->tile_ctr.p, st));
+                             o->flag.p, o->tile_ctr.p, tc_split(o), st));
     else
       CUDA_TRY(launch_field_fwd_train(o->fd, o->params.p, B, S, sb, o->feat_t.p, o->out.p, o->flag.p, st));
   }
@@ -482,7 +494,7 @@ inline prenom_status enqueue_step(prenom_object_s* o, StepStatsDev* stats, bool 
   if (tc) {
     ProfScope ps(o->ctx, PRENOM_K_MLP_BWD, st);  // MLP backward + fused table-gradient scatter
     CUDA_TRY(launch_bwd_tc(o->fd, o->params.p, o->grad.p, (long long)B * S, S, sb.count, sb.pos_depth,
-                           o->feat_tc.p, o->dout.p, o->tile_ctr.p + 2, st));
+                           o->feat_tc.p, o->dout.p, o->tile_ctr.p + 2, tc_split(o), st));
   } else {
     {
       ProfScope ps(o->ctx, PRENOM_K_MLP_BWD, st);

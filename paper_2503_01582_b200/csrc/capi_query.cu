@@ -29,9 +29,9 @@ prenom_status prenom_render(prenom_object_t o, int n_rays, const float* origins,
   const SampleBufs sb = bufs(o);
   CUDA_TRY(launch_sample(src, sampler_cfg(o, n_rays, o->cfg.prior_sampling, PRENOM_TAG_RENDER,
                                           (uint32_t)o->render_calls++), sb, nullptr, st));
-  if (o->cfg.mlp_precision == PRENOM_MLP_BF16)
+  if (uses_tc(o))
     CUDA_TRY(launch_fwd_tc(o->fd, o->params.p, (long long)n_rays * S, S, sb.count, sb.pos_depth, o->feat_tc.p,
-                           o->out.p, o->flag.p, o->tile_ctr.p, st));
+                           o->out.p, o->flag.p, o->tile_ctr.p, tc_split(o), st));
   else
     CUDA_TRY(launch_field_fwd_train(o->fd, o->params.p, n_rays, S, sb, o->feat_t.p, o->out.p, o->flag.p, st));
   CompositeArgs ca;

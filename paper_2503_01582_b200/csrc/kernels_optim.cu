@@ -112,6 +112,32 @@ __global__ void k_reptile_delta(size_t n, const float* meta, const float* adapte
     delta[i] = __fsub_rn(adapted[i], meta[i]);
 }
 
+// Sum over a rank's adapted tasks of (theta_j - theta_meta), j in order, in one
+// pass (k + 1 streams in, one out) -- the buffer the NCCL all-reduce sums
+// across ranks. float4 main body, scalar tail.
+__global__ void k_reptile_delta_sum(size_t n, const float* __restrict__ meta, const float* const* __restrict__ adapted,
+                                    int k, float* __restrict__ out) {
+  const size_t n4 = n / 4;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+    const float4 m = reinterpret_cast<const float4*>(meta)[i];
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int j = 0; j < k; ++j) {
+      const float4 a = __ldg(reinterpret_cast<const float4*>(adapted[j]) + i);
+      acc.x = __fadd_rn(acc.x, __fsub_rn(a.x, m.x));
+      acc.y = __fadd_rn(acc.y, __fsub_rn(a.y, m.y));
+      acc.z = __fadd_rn(acc.z, __fsub_rn(a.z, m.z));
+      acc.w = __fadd_rn(acc.w, __fsub_rn(a.w, m.w));
+    }
+    reinterpret_cast<float4*>(out)[i] = acc;
+  }
+  for (size_t i = 4 * n4 + (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    float acc = 0.f;
+    for (int j = 0; j < k; ++j) acc = __fadd_rn(acc, __fsub_rn(adapted[j][i], meta[i]));
+    out[i] = acc;
+  }
+}
+
 // meta.cpp:83-92 with adapted = meta + delta_sum / n_tasks.
 __global__ void k_reptile_apply(size_t n, float* meta, const float* delta, float inv_n, float beta) {
   const float keep = __fsub_rn(1.f, beta);
@@ -164,6 +190,12 @@ cudaError_t launch_philox(int n, const uint32_t* ck, uint32_t* out, cudaStream_t
 
 cudaError_t launch_reptile_delta(size_t n, const float* meta, const float* adapted, float* delta, cudaStream_t st) {
   k_reptile_delta<<<num_sms() * 4, 256, 0, st>>>(n, meta, adapted, delta);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reptile_delta_sum(size_t n, const float* meta, const float* const* adapted_dev, int k, float* out,
+                                     cudaStream_t st) {
+  k_reptile_delta_sum<<<num_sms() * 4, 256, 0, st>>>(n, meta, adapted_dev, k, out);
   return cudaGetLastError();
 }
 

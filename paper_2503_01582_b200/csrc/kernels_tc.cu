@@ -38,35 +38,55 @@ constexpr int kFwdSmemKbDefault = 40;
 // encode's gathers (was 57 KB/CTA padding, 196 KB carve-out, 60 KB of L1:
 // k_fwd_tc 0.195 -> 0.186 ms on cfg2)
 constexpr int kFwdCarveoutDefault = 58;
+// split-bf16 forward (~77 KB of operand tiles per CTA): two CTAs per SM
+constexpr int kFwdSThreadsDefault = 256;
+constexpr int kFwdSCtasDefault = 2;
+constexpr int kFwdSCarveoutDefault = -1;
+constexpr size_t kSmemPerSm = 228 * 1024;
 constexpr int kSlack = 0;       // weight tiles are never over-read
 // M=128 MN-major views of the (features|1) and (activations|1) tiles read
 // past the tile end (finite garbage rows that are never flushed)
 constexpr int kSlackX = 2048;
 constexpr int kSlackH = 1024;
 
-// bf16 copies of the MLP weights in core-matrix layouts + fp32 biases.
-template <int INP, int W, int H>
+// bf16 copies of the MLP weights in core-matrix layouts + fp32 biases. With
+// SPL (split-bf16 mode) a lo copy of every weight tile follows the hi copies
+// at kLo bytes (umma.cuh split_bf16).
+template <int INP, int W, int H, int SPL = 0>
 struct WeightTiles {
   static constexpr int kW0 = W * INP * 2;
   static constexpr int kWl = W * W * 2;
   static constexpr int kWo = 16 * W * 2;
-  static constexpr int kBytes = kW0 + (H - 1) * kWl + kWo + kSlack;
+  static constexpr int kLo = kW0 + (H - 1) * kWl + kWo + kSlack;  // hi block bytes = lo offset
+  static constexpr int kBytes = kLo * (SPL ? 2 : 1);
   unsigned char* w0;
   unsigned char* wl[2];
   unsigned char* wo;
   float* bias;  // H*W + 4
 
   __device__ void carve(unsigned char*& p) {
-    w0 = p;
-    p += kW0;
+    unsigned char* q = p;
+    w0 = q;
+    q += kW0;
     for (int l = 1; l < H; ++l) {
-      wl[l - 1] = p;
-      p += kWl;
+      wl[l - 1] = q;
+      q += kWl;
     }
-    wo = p;
-    p += kWo + kSlack;
+    wo = q;
+    p += kBytes;
     bias = reinterpret_cast<float*>(p);
     p += ((H * W + 4) * 4 + 15) / 16 * 16;
+  }
+
+  __device__ __forceinline__ static void put(unsigned char* t, uint32_t off, float v) {
+    if (SPL) {
+      __nv_bfloat16 hi, lo;
+      umma::split_bf16(v, hi, lo);
+      *reinterpret_cast<__nv_bfloat16*>(t + off) = hi;
+      *reinterpret_cast<__nv_bfloat16*>(t + kLo + off) = lo;
+    } else {
+      *reinterpret_cast<__nv_bfloat16*>(t + off) = __float2bfloat16_rn(v);
+    }
   }
 
   // threads [0, nt) cooperate
@@ -75,22 +95,17 @@ struct WeightTiles {
     for (int i = threadIdx.x; i < W * INP; i += nt) {
       const int o = i / INP, k = i % INP;
       const float v = k < IN ? __ldg(mlp + fd.w_off[0] + o * IN + k) : 0.f;
-      *reinterpret_cast<__nv_bfloat16*>(w0 + umma::cm_offset(o, k, INP)) = __float2bfloat16_rn(v);
+      put(w0, umma::cm_offset(o, k, INP), v);
     }
     for (int l = 1; l < H; ++l)
       for (int i = threadIdx.x; i < W * W; i += nt) {
         const int o = i / W, k = i % W;
-        *reinterpret_cast<__nv_bfloat16*>(wl[l - 1] + umma::cm_offset(o, k, W)) =
-            __float2bfloat16_rn(__ldg(mlp + fd.w_off[l] + o * W + k));
+        put(wl[l - 1], umma::cm_offset(o, k, W), __ldg(mlp + fd.w_off[l] + o * W + k));
       }
-    for (int i = threadIdx.x; i < 16 * W + kSlack / 2; i += nt) {
-      if (i < 16 * W) {
-        const int o = i / W, k = i % W;
-        const float v = o < 4 ? __ldg(mlp + fd.w_off[H] + o * W + k) : 0.f;
-        *reinterpret_cast<__nv_bfloat16*>(wo + umma::cm_offset(o, k, W)) = __float2bfloat16_rn(v);
-      } else {
-        reinterpret_cast<__nv_bfloat16*>(wo + 16 * W * 2)[i - 16 * W] = __float2bfloat16_rn(0.f);
-      }
+    for (int i = threadIdx.x; i < 16 * W; i += nt) {
+      const int o = i / W, k = i % W;
+      const float v = o < 4 ? __ldg(mlp + fd.w_off[H] + o * W + k) : 0.f;
+      put(wo, umma::cm_offset(o, k, W), v);
     }
     for (int i = threadIdx.x; i < H * W + 4; i += nt) {
       const int l = i / W;
@@ -127,7 +142,7 @@ __device__ __forceinline__ void wait_mma(uint64_t* bar, uint32_t& phase) {
 
 // Epilogue: TMEM [128 x N] fp32 (cols c0..) -> +bias, ReLU -> bf16 tile [128][C].
 // G column groups: warp w reads lane quadrant w%4, columns [(w/4)*N/G, ...).
-template <int N, int G = 2>
+template <int N, int G = 2, uint32_t LO = 0>
 __device__ __forceinline__ void epi_relu(uint32_t tm, int col0, const float* bias, unsigned char* tile, int C) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q = warp & 3, half = warp >> 2;
@@ -142,14 +157,14 @@ __device__ __forceinline__ void epi_relu(uint32_t tm, int col0, const float* bia
     umma::tmem_wait_ld();
 #pragma unroll
     for (int j = 0; j < 8; ++j) v[j] = fmaxf(v[j] + bias[col + j], 0.f);
-    umma::st_row8(tile, row, col, C, v);
+    umma::st_row8_split(tile, row, col, C, v, LO);
   }
 }
 
 // epi_relu for the backward's forward recompute (G = 2); also returns this
 // thread's ReLU gate, bit c = (bf16 H[row][half*N/2 + c] > 0), so the D_l
 // epilogue needs no shared-memory read of H_l.
-template <int N, int MG>
+template <int N, int MG, uint32_t LO = 0>
 __device__ __forceinline__ uint64_t epi_relu_gate(uint32_t tm, const float* bias, unsigned char* tile, int C) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q = warp & 3, half = warp >> 2;
@@ -163,16 +178,21 @@ __device__ __forceinline__ uint64_t epi_relu_gate(uint32_t tm, const float* bias
     float v[8];
     umma::tmem_ld8(umma::taddr(tm, 32 * q, col), v);
     umma::tmem_wait_ld();
-    uint32_t pk[4];
+    uint32_t pk[4], pl[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      const __nv_bfloat162 b = __floats2bfloat162_rn(fmaxf(v[2 * i] + bias[col + 2 * i], 0.f),
-                                                     fmaxf(v[2 * i + 1] + bias[col + 2 * i + 1], 0.f));
+      const float a0 = fmaxf(v[2 * i] + bias[col + 2 * i], 0.f), a1 = fmaxf(v[2 * i + 1] + bias[col + 2 * i + 1], 0.f);
+      const __nv_bfloat162 b = __floats2bfloat162_rn(a0, a1);
       pk[i] = *reinterpret_cast<const uint32_t*>(&b);
+      if (LO) {
+        const __nv_bfloat162 lo = __floats2bfloat162_rn(a0 - __low2float(b), a1 - __high2float(b));
+        pl[i] = *reinterpret_cast<const uint32_t*>(&lo);
+      }
       gate |= ((pk[i] & 0x7FFFu) ? 1ull : 0ull) << (c + 2 * i);
       gate |= ((pk[i] & 0x7FFF0000u) ? 1ull : 0ull) << (c + 2 * i + 1);
     }
     *reinterpret_cast<uint4*>(tile + umma::cm_offset(row, col, C)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+    if (LO) *reinterpret_cast<uint4*>(tile + LO + umma::cm_offset(row, col, C)) = make_uint4(pl[0], pl[1], pl[2], pl[3]);
   }
   return gate;
 }
@@ -180,19 +200,26 @@ __device__ __forceinline__ uint64_t epi_relu_gate(uint32_t tm, const float* bias
 // ------------------------------------------------------------------ fwd
 // NT threads: NT/128 threads per sample share the levels in the encode and
 // the columns in the epilogues.
-template <int INP, int W, int H, int NT>
+// SPL: split-bf16 operands (umma.cuh split_bf16); bit 0 of `split` turns the
+// cross products on (the lo tiles are written either way).
+template <int INP, int W, int H, int NT, int SPL>
 __global__ void __launch_bounds__(NT) k_fwd_tc(FieldDesc fd, const float* __restrict__ params, long long n_total,
                                                      int S, const int* __restrict__ count,
                                                      const float4* __restrict__ pos, uint4* __restrict__ feat_tiles,
-                                                     float4* __restrict__ out, int* flag, int* tile_ctr) {
+                                                     float4* __restrict__ out, int* flag, int* tile_ctr, int split) {
+  using WT = WeightTiles<INP, W, H, SPL>;
+  constexpr uint32_t XLO = SPL ? 128 * INP * 2 : 0;  // lo copies follow the hi tiles
+  constexpr uint32_t HLO = SPL ? 128 * W * 2 : 0;
+  constexpr uint32_t kXBytes = 128 * INP * 2 * (SPL ? 2 : 1);
+  const bool sp = SPL && (split & 1);
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ uint64_t bar;
   __shared__ uint32_t tbase;
-  WeightTiles<INP, W, H> wt;
+  WT wt;
   unsigned char* p = smem;
   wt.carve(p);
   unsigned char* X = p;
-  p += 128 * INP * 2;
+  p += kXBytes;
   // one activation tile: layer l+1's MMA completes (mbarrier) before layer
   // l+1's epilogue overwrites the tile it read
   unsigned char* Hb = p;
@@ -200,7 +227,7 @@ __global__ void __launch_bounds__(NT) k_fwd_tc(FieldDesc fd, const float* __rest
   pdl_wait();  // params come from the previous step's Adam
   wt.load(fd, params + fd.hash_params, NT);
   constexpr int TPS = NT / 128;  // threads per sample
-  for (int i = tid; i < 128 * INP; i += NT) reinterpret_cast<__nv_bfloat16*>(X)[i] = __float2bfloat16_rn(0.f);
+  for (int i = tid; i < (int)kXBytes / 2; i += NT) reinterpret_cast<__nv_bfloat16*>(X)[i] = __float2bfloat16_rn(0.f);
   // One 64-column TMEM region serves every layer: each MMA is issued only
   // after the previous epilogue drained it (sync_for_mma), so up to 8 CTAs fit.
   if (warp == 0) umma::tmem_alloc(&tbase, 64);
@@ -232,36 +259,42 @@ __global__ void __launch_bounds__(NT) k_fwd_tc(FieldDesc fd, const float* __rest
       for (int l = part; l < fd.L; l += TPS) {
         float f[2] = {0.f, 0.f};
         if (valid) encode_level<2>(fd, params, l, px, py, pz, f);
-        *reinterpret_cast<__nv_bfloat162*>(X + umma::cm_offset(s, 2 * l, INP)) = __floats2bfloat162_rn(f[0], f[1]);
+        const __nv_bfloat162 hi = __floats2bfloat162_rn(f[0], f[1]);
+        *reinterpret_cast<__nv_bfloat162*>(X + umma::cm_offset(s, 2 * l, INP)) = hi;
+        if (SPL)
+          *reinterpret_cast<__nv_bfloat162*>(X + XLO + umma::cm_offset(s, 2 * l, INP)) =
+              __floats2bfloat162_rn(f[0] - __low2float(hi), f[1] - __high2float(hi));
       }
     }
     sync_for_mma();
     if (tid == 0) {
       for (int ks = 0; ks < INP / 16; ++ks)
-        umma::mma_bf16(tm, umma::desc_kmajor(X, INP, ks), umma::desc_kmajor(wt.w0, INP, ks), id_l0, ks > 0);
+        umma::mma_split(tm, umma::desc_kmajor(X, INP, ks), umma::desc_kmajor(wt.w0, INP, ks), id_l0, ks > 0, sp, XLO,
+                        WT::kLo);
       umma::commit(&bar);
       // stored features for the backward pass (tile-major, same core-matrix
-      // layout), written by the TMA engine: no LSU work next to the gathers
-      umma::bulk_s2g(feat_tiles + t * (128 * INP * 2 / 16), X, 128 * INP * 2);
+      // layout; split mode: hi tile then lo tile), written by the TMA engine:
+      // no LSU work next to the gathers
+      umma::bulk_s2g(feat_tiles + t * (kXBytes / 16), X, kXBytes);
     }
     wait_mma(&bar, phase);
-    epi_relu<W, TPS>(tm, 0, wt.bias, Hb, W);
+    epi_relu<W, TPS, HLO>(tm, 0, wt.bias, Hb, W);
     for (int l = 1; l < H; ++l) {
       sync_for_mma();
       if (tid == 0) {
         for (int ks = 0; ks < W / 16; ++ks)
-          umma::mma_bf16(tm, umma::desc_kmajor(Hb, W, ks), umma::desc_kmajor(wt.wl[l - 1], W, ks),
-                         umma::idesc_bf16(128, W, false, false), ks > 0);
+          umma::mma_split(tm, umma::desc_kmajor(Hb, W, ks), umma::desc_kmajor(wt.wl[l - 1], W, ks),
+                          umma::idesc_bf16(128, W, false, false), ks > 0, sp, HLO, WT::kLo);
         umma::commit(&bar);
       }
       wait_mma(&bar, phase);
-      epi_relu<W, TPS>(tm, 0, wt.bias + l * W, Hb, W);
+      epi_relu<W, TPS, HLO>(tm, 0, wt.bias + l * W, Hb, W);
     }
     sync_for_mma();
     if (tid == 0) {
       for (int ks = 0; ks < W / 16; ++ks)
-        umma::mma_bf16(tm, umma::desc_kmajor(Hb, W, ks), umma::desc_kmajor(wt.wo, W, ks), id_out,
-                       ks > 0);
+        umma::mma_split(tm, umma::desc_kmajor(Hb, W, ks), umma::desc_kmajor(wt.wo, W, ks), id_out, ks > 0, sp, HLO,
+                        WT::kLo);
       umma::commit(&bar);
     }
     wait_mma(&bar, phase);
@@ -429,14 +462,23 @@ __device__ __forceinline__ void mbar_arrive2(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], 2;" ::"r"(umma::smem_u32(bar)) : "memory");
 }
 
-template <int INP, int W, int H>
-__global__ void __launch_bounds__(kBwdThreads, 2)
+// SPL: split-bf16 operands; `split` bits: 0 forward recompute, 1 the data
+// products (dH, dX), 2 the weight gradients.
+template <int INP, int W, int H, int SPL>
+__global__ void __launch_bounds__(kBwdThreads, SPL ? 1 : 2)
     k_bwd_tc(FieldDesc fd, const float* __restrict__ params, float* __restrict__ grad, long long n_total, int S,
              const int* __restrict__ count, const float4* __restrict__ pos, const uint4* __restrict__ feat_tiles,
              const float4* __restrict__ dout, int* tile_ctr, int skip_scatter, int mlp_levels,
-             int pull_max) {
+             int pull_max, int split) {
   using CM = BwdCols<INP, W, H>;
+  using WT = WeightTiles<INP, W, H, SPL>;
   constexpr int XC = INP + 8, HC = W + 8;
+  // lo copies sit one (tile + slack) after the hi copies
+  constexpr uint32_t XLO = SPL ? 128 * XC * 2 + kSlackX : 0;
+  constexpr uint32_t HLO = SPL ? 128 * HC * 2 + kSlackH : 0;
+  constexpr uint32_t GLO = SPL ? 128 * 16 * 2 : 0;
+  constexpr uint32_t kFeatBytes = 128 * INP * 2 * (SPL ? 2 : 1);
+  const bool sp_f = SPL && (split & 1), sp_d = SPL && (split & 2), sp_w = SPL && (split & 4);
   constexpr int NH = INP / 2;  // d_feature columns per half: [h*NH, (h+1)*NH)
   constexpr int LH = INP / 4;  // levels per half
   extern __shared__ __align__(1024) unsigned char smem[];
@@ -444,18 +486,18 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
   __shared__ uint32_t tbase;
   __shared__ int s_tile;
   __shared__ long long slot_tile;
-  WeightTiles<INP, W, H> wt;
+  WT wt;
   unsigned char* p = smem;
   wt.carve(p);
   unsigned char* X = p;  // [128][INP+8]: features | ones
-  p += 128 * XC * 2 + kSlackX;
+  p += (128 * XC * 2 + kSlackX) * (SPL ? 2 : 1);
   unsigned char* Ht[2];  // [128][W+8] per hidden layer: activations | ones
   for (int l = 0; l < H; ++l) {
     Ht[l] = p;
-    p += 128 * HC * 2 + kSlackH;
+    p += (128 * HC * 2 + kSlackH) * (SPL ? 2 : 1);
   }
   unsigned char* G = p;  // [128][16] g_raw (4 used)
-  p += 128 * 16 * 2;
+  p += 128 * 16 * 2 * (SPL ? 2 : 1);
   // D_l = dH_l * relu'(H_l) is written over H_l itself (H_l is dead once its
   // ReLU gate is taken)
   unsigned char* zero_end = p;
@@ -543,10 +585,13 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
       // ---- stored bf16 features -> X by the TMA engine (no LSU work): one
       // bulk copy per 8-row group (the X row-group stride is longer: ones column)
       if (tid == 0) {
-        const unsigned char* src = reinterpret_cast<const unsigned char*>(feat_tiles + t * (128 * INP * 2 / 16));
-        umma::mbar_arrive_expect_tx(&xbar, 128 * INP * 2);
+        const unsigned char* src = reinterpret_cast<const unsigned char*>(feat_tiles + t * (kFeatBytes / 16));
+        umma::mbar_arrive_expect_tx(&xbar, kFeatBytes);
         for (int rg = 0; rg < 16; ++rg)
           umma::bulk_g2s(X + rg * (XC / 8) * 128, src + rg * INP * 16, INP * 16, &xbar);
+        if (SPL)
+          for (int rg = 0; rg < 16; ++rg)
+            umma::bulk_g2s(X + XLO + rg * (XC / 8) * 128, src + 128 * INP * 2 + rg * INP * 16, INP * 16, &xbar);
       }
       umma::mbar_wait(&xbar, xphase);
       xphase ^= 1u;
@@ -555,29 +600,29 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
       // ---- forward recompute (field.cpp:181-211), one TMEM region reused per layer
       if (tid == 0) {
         for (int ks = 0; ks < INP / 16; ++ks)
-          umma::mma_bf16(tr, umma::desc_kmajor(X, XC, ks), umma::desc_kmajor(wt.w0, INP, ks),
-                         umma::idesc_bf16(128, W, false, false), ks > 0);
+          umma::mma_split(tr, umma::desc_kmajor(X, XC, ks), umma::desc_kmajor(wt.w0, INP, ks),
+                          umma::idesc_bf16(128, W, false, false), ks > 0, sp_f, XLO, WT::kLo);
         umma::commit(&bar);
       }
       wait_mma(&bar, phase);
       uint64_t gate[2];
-      gate[0] = epi_relu_gate<W, kMG>(tr, wt.bias, Ht[0], HC);
+      gate[0] = epi_relu_gate<W, kMG, HLO>(tr, wt.bias, Ht[0], HC);
       for (int l = 1; l < H; ++l) {
         mlp_sync_for_mma();
         if (tid == 0) {
           for (int ks = 0; ks < W / 16; ++ks)
-            umma::mma_bf16(tr, umma::desc_kmajor(Ht[l - 1], HC, ks), umma::desc_kmajor(wt.wl[l - 1], W, ks),
-                           umma::idesc_bf16(128, W, false, false), ks > 0);
+            umma::mma_split(tr, umma::desc_kmajor(Ht[l - 1], HC, ks), umma::desc_kmajor(wt.wl[l - 1], W, ks),
+                            umma::idesc_bf16(128, W, false, false), ks > 0, sp_f, HLO, WT::kLo);
           umma::commit(&bar);
         }
         wait_mma(&bar, phase);
-        gate[l] = epi_relu_gate<W, kMG>(tr, wt.bias + l * W, Ht[l], HC);
+        gate[l] = epi_relu_gate<W, kMG, HLO>(tr, wt.bias + l * W, Ht[l], HC);
       }
       mlp_sync_for_mma();
       if (tid == 0) {
         for (int ks = 0; ks < W / 16; ++ks)
-          umma::mma_bf16(tr, umma::desc_kmajor(Ht[H - 1], HC, ks), umma::desc_kmajor(wt.wo, W, ks),
-                         umma::idesc_bf16(128, 16, false, false), ks > 0);
+          umma::mma_split(tr, umma::desc_kmajor(Ht[H - 1], HC, ks), umma::desc_kmajor(wt.wo, W, ks),
+                          umma::idesc_bf16(128, 16, false, false), ks > 0, sp_f, HLO, WT::kLo);
         umma::commit(&bar);
       }
       wait_mma(&bar, phase);
@@ -599,16 +644,16 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
           g[2] = d.z * s2 * (1.f - s2);
           g[3] = d.w * s3 * (1.f - s3);
         }
-        umma::st_row8(G, row, 0, 16, g);
+        umma::st_row8_split(G, row, 0, 16, g, GLO);
       }
       mlp_sync_for_mma();
       // ---- output layer: dW_out^T += [H_{H-1}|1]^T G;  dH_{H-1} = G W_out
       if (tid == 0) {
         for (int ks = 0; ks < 8; ++ks)
-          umma::mma_bf16(tm + CM::kDWo, umma::desc_mnmajor(Ht[H - 1], HC, ks), umma::desc_mnmajor(G, 16, ks),
-                         umma::idesc_bf16(128, 16, true, true), (iter > 0 || ks > 0));
-        umma::mma_bf16(tr, umma::desc_kmajor(G, 16, 0), umma::desc_mnmajor(wt.wo, W, 0),
-                       umma::idesc_bf16(128, W, false, true), 0u);
+          umma::mma_split(tm + CM::kDWo, umma::desc_mnmajor(Ht[H - 1], HC, ks), umma::desc_mnmajor(G, 16, ks),
+                          umma::idesc_bf16(128, 16, true, true), (iter > 0 || ks > 0), sp_w, HLO, GLO);
+        umma::mma_split(tr, umma::desc_kmajor(G, 16, 0), umma::desc_mnmajor(wt.wo, W, 0),
+                        umma::idesc_bf16(128, W, false, true), 0u, sp_d, GLO, WT::kLo);
         umma::commit(&bar);
       }
       wait_mma(&bar, phase);
@@ -624,7 +669,7 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
             umma::tmem_wait_ld();
 #pragma unroll
             for (int j = 0; j < 8; ++j) v[j] = (gate[l] >> (c + j)) & 1ull ? v[j] : 0.f;
-            umma::st_row8(Ht[l], row, col, HC, v);  // D_l in place of H_l
+            umma::st_row8_split(Ht[l], row, col, HC, v, HLO);  // D_l in place of H_l
           }
         }
         mlp_sync_for_mma();
@@ -632,20 +677,21 @@ __global__ void __launch_bounds__(kBwdThreads, 2)
           const int dwc = l == 0 ? CM::kDW0 : CM::kDWl + (H - 1 - l) * W;
           const unsigned char* prev = l == 0 ? X : Ht[l - 1];
           const int pc = l == 0 ? XC : HC;
+          const uint32_t plo = l == 0 ? XLO : HLO;
           for (int ks = 0; ks < 8; ++ks)
-            umma::mma_bf16(tm + dwc, umma::desc_mnmajor(prev, pc, ks), umma::desc_mnmajor(Ht[l], HC, ks),
-                           umma::idesc_bf16(128, W, true, true), (iter > 0 || ks > 0));
+            umma::mma_split(tm + dwc, umma::desc_mnmajor(prev, pc, ks), umma::desc_mnmajor(Ht[l], HC, ks),
+                            umma::idesc_bf16(128, W, true, true), (iter > 0 || ks > 0), sp_w, plo, HLO);
           if (l > 0) {
             for (int ks = 0; ks < W / 16; ++ks)
-              umma::mma_bf16(tr, umma::desc_kmajor(Ht[l], HC, ks), umma::desc_mnmajor(wt.wl[l - 1], W, ks),
-                             umma::idesc_bf16(128, W, false, true), ks > 0);
+              umma::mma_split(tr, umma::desc_kmajor(Ht[l], HC, ks), umma::desc_mnmajor(wt.wl[l - 1], W, ks),
+                              umma::idesc_bf16(128, W, false, true), ks > 0, sp_d, HLO, WT::kLo);
           } else {
             // d_features -> the TMEM slot, once every consumer holds the previous tile's
             umma::mbar_wait(&empty_bar, ((uint32_t)iter & 1u) ^ 1u);
             slot_tile = t;
             for (int ks = 0; ks < W / 16; ++ks)
-              umma::mma_bf16(tm + CM::kDF, umma::desc_kmajor(Ht[l], HC, ks), umma::desc_mnmajor(wt.w0, INP, ks),
-                             umma::idesc_bf16(128, INP, false, true), ks > 0);
+              umma::mma_split(tm + CM::kDF, umma::desc_kmajor(Ht[l], HC, ks), umma::desc_mnmajor(wt.w0, INP, ks),
+                              umma::idesc_bf16(128, INP, false, true), ks > 0, sp_d, HLO, WT::kLo);
           }
           umma::commit(&bar);
           if (l == 0) {
@@ -750,32 +796,30 @@ int sms() {
   return g_sms;
 }
 
-template <int INP, int W, int H>
+template <int INP, int W, int H, int SPL>
 size_t fwd_smem() {
-  return WeightTiles<INP, W, H>::kBytes + ((H * W + 4) * 4 + 15) / 16 * 16 + 128 * INP * 2 + 128 * W * 2 + 1024;
+  return WeightTiles<INP, W, H, SPL>::kBytes + ((H * W + 4) * 4 + 15) / 16 * 16 +
+         (128 * INP * 2 + 128 * W * 2) * (SPL ? 2 : 1) + 1024;
 }
 
-template <int INP, int W, int H>
+template <int INP, int W, int H, int SPL>
 size_t bwd_smem() {
-  return WeightTiles<INP, W, H>::kBytes + ((H * W + 4) * 4 + 15) / 16 * 16 + (128 * (INP + 8) * 2 + kSlackX) +
-         H * (128 * (W + 8) * 2 + kSlackH) + 128 * 16 * 2 + 1024;
+  return WeightTiles<INP, W, H, SPL>::kBytes + ((H * W + 4) * 4 + 15) / 16 * 16 +
+         ((128 * (INP + 8) * 2 + kSlackX) + H * (128 * (W + 8) * 2 + kSlackH) + 128 * 16 * 2) * (SPL ? 2 : 1) + 1024;
 }
 
-template <int INP, int W, int H, int NT>
+template <int INP, int W, int H, int NT, int SPL>
 cudaError_t run_fwd_nt(const FieldDesc& fd, const float* params, long long n, int S, const int* count,
                        const float4* pos, void* feat_tiles, float4* out, int* flag, int* tile_ctr, int ctas,
-                       size_t min_smem, cudaStream_t st) {
-  const size_t smem = std::max<size_t>(fwd_smem<INP, W, H>(), min_smem);
-  cudaError_t e = cudaFuncSetAttribute(k_fwd_tc<INP, W, H, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                       size_t min_smem, int carveout, int split, cudaStream_t st) {
+  auto kern = k_fwd_tc<INP, W, H, NT, SPL>;
+  const size_t smem = std::max<size_t>(fwd_smem<INP, W, H, SPL>(), min_smem);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   // shared-memory carve-out (percent of the maximum): the rest of the 256 KB
-  // array is L1, which serves the encode's gathers; PRENOM_FWD_CARVEOUT for tuning
-  static const int carveout = [] {
-    const char* v = getenv("PRENOM_FWD_CARVEOUT");
-    return v ? atoi(v) : kFwdCarveoutDefault;
-  }();
+  // array is L1, which serves the encode's gathers
   if (carveout >= 0) {
-    e = cudaFuncSetAttribute(k_fwd_tc<INP, W, H, NT>, cudaFuncAttributePreferredSharedMemoryCarveout, carveout);
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carveout);
     if (e != cudaSuccess) return e;
   }
   const long long ntiles = (n + kTile - 1) / kTile;
@@ -784,72 +828,85 @@ cudaError_t run_fwd_nt(const FieldDesc& fd, const float* params, long long n, in
   e = cudaMemsetAsync(tile_ctr, 0, sizeof(int), st);
   if (e != cudaSuccess) return e;
 #endif
-  return launch_pdl(k_fwd_tc<INP, W, H, NT>, dim3((unsigned)grid), dim3(NT), smem, st, fd, params, n, S, count, pos,
-                    reinterpret_cast<uint4*>(feat_tiles), out, flag, tile_ctr);
+  return launch_pdl(kern, dim3((unsigned)grid), dim3(NT), smem, st, fd, params, n, S, count, pos,
+                    reinterpret_cast<uint4*>(feat_tiles), out, flag, tile_ctr, split);
+}
+
+int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
 }
 
 template <int INP, int W, int H>
 cudaError_t run_fwd(const FieldDesc& fd, const float* params, long long n, int S, const int* count, const float4* pos,
-                    void* feat_tiles, float4* out, int* flag, int* tile_ctr, cudaStream_t st) {
+                    void* feat_tiles, float4* out, int* flag, int* tile_ctr, int split, cudaStream_t st) {
   // CTAs per SM x threads per CTA trade gather latency hiding against L1
-  // capacity (L1 = 228 KB - shared memory); PRENOM_FWD_{CTAS,SMEM_KB,THREADS}
-  // override the measured defaults for tuning.
-  static const int nt = [] {
-    const char* e = getenv("PRENOM_FWD_THREADS");
-    return e ? (atoi(e) == 512 ? 512 : 256) : kFwdThreadsDefault;
-  }();
-  static const int ctas = [] {
-    const char* e = getenv("PRENOM_FWD_CTAS");
-    const int v = e ? atoi(e) : kFwdCtasDefault;
-    return v < 1 ? 1 : (v > 8 ? 8 : v);
-  }();
-  static const size_t min_smem = [] {
-    const char* e = getenv("PRENOM_FWD_SMEM_KB");
-    return (size_t)(e ? atoi(e) : kFwdSmemKbDefault) * 1024;
-  }();
+  // capacity (L1 = 256 KB - the shared-memory carve-out);
+  // PRENOM_FWD_{CTAS,SMEM_KB,THREADS,CARVEOUT} override the measured defaults
+  // (split mode: PRENOM_FWDS_*).
+  if (split) {
+    static const int nt = env_int("PRENOM_FWDS_THREADS", kFwdSThreadsDefault) == 512 ? 512 : 256;
+    static const int ctas = std::max(1, std::min(8, env_int("PRENOM_FWDS_CTAS", kFwdSCtasDefault)));
+    static const size_t min_smem = (size_t)env_int("PRENOM_FWDS_SMEM_KB", 0) * 1024;
+    static const int carve = env_int("PRENOM_FWDS_CARVEOUT", kFwdSCarveoutDefault);
+    if (nt == 512)
+      return run_fwd_nt<INP, W, H, 512, 1>(fd, params, n, S, count, pos, feat_tiles, out, flag, tile_ctr, ctas,
+                                           min_smem, carve, split, st);
+    return run_fwd_nt<INP, W, H, 256, 1>(fd, params, n, S, count, pos, feat_tiles, out, flag, tile_ctr, ctas, min_smem,
+                                         carve, split, st);
+  }
+  static const int nt = env_int("PRENOM_FWD_THREADS", kFwdThreadsDefault) == 512 ? 512 : 256;
+  static const int ctas = std::max(1, std::min(8, env_int("PRENOM_FWD_CTAS", kFwdCtasDefault)));
+  static const size_t min_smem = (size_t)env_int("PRENOM_FWD_SMEM_KB", kFwdSmemKbDefault) * 1024;
+  static const int carve = env_int("PRENOM_FWD_CARVEOUT", kFwdCarveoutDefault);
   if (nt == 512)
-    return run_fwd_nt<INP, W, H, 512>(fd, params, n, S, count, pos, feat_tiles, out, flag, tile_ctr, ctas, min_smem, st);
-  return run_fwd_nt<INP, W, H, 256>(fd, params, n, S, count, pos, feat_tiles, out, flag, tile_ctr, ctas, min_smem, st);
+    return run_fwd_nt<INP, W, H, 512, 0>(fd, params, n, S, count, pos, feat_tiles, out, flag, tile_ctr, ctas, min_smem,
+                                         carve, 0, st);
+  return run_fwd_nt<INP, W, H, 256, 0>(fd, params, n, S, count, pos, feat_tiles, out, flag, tile_ctr, ctas, min_smem,
+                                       carve, 0, st);
+}
+
+template <int INP, int W, int H, int SPL>
+cudaError_t run_bwd_s(const FieldDesc& fd, const float* params, float* grad, long long n, int S, const int* count,
+                      const float4* pos, const void* feat_tiles, const float4* dout, int* tile_ctr, int split,
+                      cudaStream_t st) {
+  // plain bf16: two CTAs (2 x 256 TMEM columns) per SM, the shared-memory
+  // floor keeps a third CTA out; PRENOM_BWD_SMEM_KB / PRENOM_BWD_CARVEOUT for tuning
+  static const size_t min_smem = (size_t)env_int("PRENOM_BWD_SMEM_KB", SPL ? 0 : 80) * 1024;
+  static const int carveout = env_int("PRENOM_BWD_CARVEOUT", -1);
+  auto kern = k_bwd_tc<INP, W, H, SPL>;
+  const size_t smem = std::max<size_t>(bwd_smem<INP, W, H, SPL>(), min_smem);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  if (carveout >= 0) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carveout);
+    if (e != cudaSuccess) return e;
+  }
+  const long long ntiles = (n + kTile - 1) / kTile;
+  const int per_sm = std::max(1, (int)(kSmemPerSm / (smem + 1024)));
+  const long long grid =
+      std::min<long long>((ntiles + min_tiles_per_cta() - 1) / min_tiles_per_cta(), (long long)std::min(2, per_sm) * sms());
+  // levels per half the MLP warps scatter themselves (they would otherwise
+  // wait on the scatter warps); PRENOM_BWD_MLP_LEVELS overrides for tuning
+  static const int mlp_env = env_int("PRENOM_BWD_MLP_LEVELS", -1);
+  // the MLP warps load 8 slot columns: at most 4 levels per half
+  const int mlp_levels = std::max(0, std::min(std::min(4, INP / 4), mlp_env >= 0 ? mlp_env : kBwdMlpLevels));
+  static const int skip = env_int("PRENOM_PROF_SKIP_SCATTER", 0);
+  // longest run reduced by pulls (else by the shuffle tree); PRENOM_BWD_PULL_MAX overrides
+  static const int pull_max = env_int("PRENOM_BWD_PULL_MAX", kBwdPullMax);
+  cudaError_t em = cudaMemsetAsync(tile_ctr, 0, sizeof(int), st);
+  if (em != cudaSuccess) return em;
+  return launch_pdl(kern, dim3((unsigned)grid), dim3(kBwdThreads), smem, st, fd, params, grad, n, S, count, pos,
+                    reinterpret_cast<const uint4*>(feat_tiles), dout, tile_ctr, skip, mlp_levels, pull_max, split);
 }
 
 template <int INP, int W, int H>
 cudaError_t run_bwd(const FieldDesc& fd, const float* params, float* grad, long long n, int S, const int* count,
-                    const float4* pos, const void* feat_tiles, const float4* dout, int* tile_ctr, cudaStream_t st) {
-  // two CTAs (2 x 256 TMEM columns) per SM: the shared-memory floor keeps a
-  // third CTA out; PRENOM_BWD_SMEM_KB / PRENOM_BWD_CARVEOUT for tuning
-  static const size_t min_smem = [] {
-    const char* v = getenv("PRENOM_BWD_SMEM_KB");
-    return (size_t)(v ? atoi(v) : 80) * 1024;
-  }();
-  static const int carveout = [] {
-    const char* v = getenv("PRENOM_BWD_CARVEOUT");
-    return v ? atoi(v) : -1;
-  }();
-  const size_t smem = std::max<size_t>(bwd_smem<INP, W, H>(), min_smem);
-  cudaError_t e = cudaFuncSetAttribute(k_bwd_tc<INP, W, H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  if (carveout >= 0) {
-    e = cudaFuncSetAttribute(k_bwd_tc<INP, W, H>, cudaFuncAttributePreferredSharedMemoryCarveout, carveout);
-    if (e != cudaSuccess) return e;
-  }
-  const long long ntiles = (n + kTile - 1) / kTile;
-  const long long grid = std::min<long long>((ntiles + min_tiles_per_cta() - 1) / min_tiles_per_cta(), 2LL * sms());
-  // levels per half the MLP warps scatter themselves (they would otherwise
-  // wait on the scatter warps); PRENOM_BWD_MLP_LEVELS overrides for tuning
-  static const int mlp_env = [] {
-    const char* v = getenv("PRENOM_BWD_MLP_LEVELS");
-    return v ? atoi(v) : -1;
-  }();
-  // the MLP warps load 8 slot columns: at most 4 levels per half
-  const int mlp_levels = std::max(0, std::min(std::min(4, INP / 4), mlp_env >= 0 ? mlp_env : kBwdMlpLevels));
-  static const int skip = getenv("PRENOM_PROF_SKIP_SCATTER") ? atoi(getenv("PRENOM_PROF_SKIP_SCATTER")) : 0;
-  // longest run reduced by pulls (else by the shuffle tree); PRENOM_BWD_PULL_MAX overrides
-  static const int pull_max = getenv("PRENOM_BWD_PULL_MAX") ? atoi(getenv("PRENOM_BWD_PULL_MAX")) : kBwdPullMax;
-  cudaError_t em = cudaMemsetAsync(tile_ctr, 0, sizeof(int), st);
-  if (em != cudaSuccess) return em;
-  return launch_pdl(k_bwd_tc<INP, W, H>, dim3((unsigned)grid), dim3(kBwdThreads), smem, st, fd, params, grad, n, S,
-                    count, pos, reinterpret_cast<const uint4*>(feat_tiles), dout, tile_ctr, skip, mlp_levels,
-                    pull_max);
+                    const float4* pos, const void* feat_tiles, const float4* dout, int* tile_ctr, int split,
+                    cudaStream_t st) {
+  if (split)
+    return run_bwd_s<INP, W, H, 1>(fd, params, grad, n, S, count, pos, feat_tiles, dout, tile_ctr, split, st);
+  return run_bwd_s<INP, W, H, 0>(fd, params, grad, n, S, count, pos, feat_tiles, dout, tile_ctr, 0, st);
 }
 
 #define PRENOM_TC_DISPATCH(FN, ...)                                                          \
@@ -883,24 +940,35 @@ bool tc_supported(const FieldDesc& fd) {
   return fd.F == 2 && fd.in_dim <= 32 && (fd.W == 32 || fd.W == 64) && (fd.H == 1 || fd.H == 2);
 }
 
-size_t tc_feature_bytes(const FieldDesc& fd, long long n) {
+size_t tc_feature_bytes(const FieldDesc& fd, long long n, int split) {
   const int inp = fd.in_dim <= 16 ? 16 : 32;
-  return (size_t)((n + kTile - 1) / kTile) * kTile * inp * 2;
+  return (size_t)((n + kTile - 1) / kTile) * kTile * inp * 2 * (split ? 2 : 1);
+}
+
+// split: 0 = bf16 operands; else split-bf16 with the cross products enabled
+// per bit (1 forward, 2 backward data products, 4 weight gradients).
+// PRENOM_SPLIT_MASK overrides the mask of split-mode calls (bisection).
+int split_mask(int split) {
+  static const int m = env_int("PRENOM_SPLIT_MASK", 7);
+  return split ? (m | 8) : 0;  // bit 3 keeps "split mode" set when the mask is 0
 }
 
 cudaError_t launch_fwd_tc(const FieldDesc& fd, const float* params, long long n, int S, const int* count,
-                          const float4* pos, void* feat_tiles, float4* out, int* flag, int* tile_ctr, cudaStream_t st) {
+                          const float4* pos, void* feat_tiles, float4* out, int* flag, int* tile_ctr, int split,
+                          cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   if (n + kTile >= (1LL << 31)) return cudaErrorInvalidValue;  // ray_of's 32-bit slot index
-  PRENOM_TC_DISPATCH(run_fwd, fd, params, n, S, count, pos, feat_tiles, out, flag, tile_ctr, st);
+  split = split_mask(split);
+  PRENOM_TC_DISPATCH(run_fwd, fd, params, n, S, count, pos, feat_tiles, out, flag, tile_ctr, split, st);
 }
 
 cudaError_t launch_bwd_tc(const FieldDesc& fd, const float* params, float* grad, long long n, int S,
                           const int* count, const float4* pos, const void* feat_tiles, const float4* dout,
-                          int* tile_ctr, cudaStream_t st) {
+                          int* tile_ctr, int split, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   if (n + kTile >= (1LL << 31)) return cudaErrorInvalidValue;  // ray_of's 32-bit slot index
-  PRENOM_TC_DISPATCH(run_bwd, fd, params, grad, n, S, count, pos, feat_tiles, dout, tile_ctr, st);
+  split = split_mask(split);
+  PRENOM_TC_DISPATCH(run_bwd, fd, params, grad, n, S, count, pos, feat_tiles, dout, tile_ctr, split, st);
 }
 
 }  // namespace prenom

@@ -372,6 +372,8 @@ cudaError_t launch_reptile_delta(size_t n, const float* meta, const float* adapt
                                  cudaStream_t st);
 cudaError_t launch_reptile_apply(size_t n, float* meta, const float* delta, float inv_n,
                                  float beta, cudaStream_t st);
+cudaError_t launch_reptile_delta_sum(size_t n, const float* meta, const float* const* adapted_dev, int k, float* out,
+                                     cudaStream_t st);
 cudaError_t launch_reptile_update(size_t n, float* meta, const float* adapted, float beta, cudaStream_t st);
 // ---- isosurface (mesh.cu)
 template <typename T>
@@ -443,14 +445,14 @@ cudaError_t run_marching_cubes(const float* d_grid, int R, float iso, McScratch&
 // bf16 tensor-core MLP path (kernels_tc.cu)
 bool tc_supported(const FieldDesc& fd);
 void tc_set_min_tiles_per_cta(int v);  // persistent-grid hint for the calling host thread (multi-object)
-size_t tc_feature_bytes(const FieldDesc& fd, long long n);
+size_t tc_feature_bytes(const FieldDesc& fd, long long n, int split);
 // tile_ctr: one device int per launch, zeroed by the launcher (dynamic tile scheduler)
 cudaError_t launch_fwd_tc(const FieldDesc& fd, const float* params, long long n, int S, const int* count,
-                          const float4* pos, void* feat_tiles, float4* out, int* flag, int* tile_ctr,
+                          const float4* pos, void* feat_tiles, float4* out, int* flag, int* tile_ctr, int split,
                           cudaStream_t st);
 cudaError_t launch_bwd_tc(const FieldDesc& fd, const float* params, float* grad, long long n, int S,
                           const int* count, const float4* pos, const void* feat_tiles, const float4* dout,
-                          int* tile_ctr, cudaStream_t st);
+                          int* tile_ctr, int split, cudaStream_t st);
 cudaError_t launch_umma_gemm(int M, int N, int K, int a_mn, int b_mn, const float* A, const float* B,
                              float* D, cudaStream_t st);
 

@@ -200,5 +200,42 @@ __device__ __forceinline__ void st_row8(unsigned char* tile, int r, int c0, int 
   *reinterpret_cast<uint4*>(tile + cm_offset(r, c0, C)) = *reinterpret_cast<uint4*>(p);
 }
 
+// Split-bf16 ("bf16x3") operands: x = hi + lo with hi = bf16(x) and
+// lo = bf16(x - hi), so a product a*b ~ a_hi b_hi + a_hi b_lo + a_lo b_hi keeps
+// ~16 significand bits (the dropped a_lo b_lo term is 2^-16 relative) while
+// every MMA stays kind::f16 at full bf16 tensor rate. The lo copy of a tile sits
+// `lo_off` bytes after the hi copy, so its descriptor is the hi descriptor plus
+// lo_off >> 4 in the start-address field.
+__device__ __forceinline__ void split_bf16(float x, __nv_bfloat16& hi, __nv_bfloat16& lo) {
+  hi = __float2bfloat16_rn(x);
+  lo = __float2bfloat16_rn(x - __bfloat162float(hi));
+}
+
+__device__ __forceinline__ uint64_t desc_add(uint64_t d, uint32_t byte_off) { return d + (uint64_t)(byte_off >> 4); }
+
+// st_row8 of the hi and (when lo_off != 0) lo parts.
+__device__ __forceinline__ void st_row8_split(unsigned char* tile, int r, int c0, int C, const float* v,
+                                              uint32_t lo_off) {
+  if (!lo_off) {
+    st_row8(tile, r, c0, C, v);
+    return;
+  }
+  __nv_bfloat16 h[8], l[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) split_bf16(v[i], h[i], l[i]);
+  *reinterpret_cast<uint4*>(tile + cm_offset(r, c0, C)) = *reinterpret_cast<uint4*>(h);
+  *reinterpret_cast<uint4*>(tile + lo_off + cm_offset(r, c0, C)) = *reinterpret_cast<uint4*>(l);
+}
+
+// D (+)= A*B^T with split operands: hi*hi, then the two cross terms when `split`.
+__device__ __forceinline__ void mma_split(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                          uint32_t accumulate, bool split, uint32_t a_lo, uint32_t b_lo) {
+  mma_bf16(tmem_d, a, b, idesc, accumulate);
+  if (split) {
+    mma_bf16(tmem_d, a, desc_add(b, b_lo), idesc, 1u);
+    mma_bf16(tmem_d, desc_add(a, a_lo), b, idesc, 1u);
+  }
+}
+
 }  // namespace umma
 }  // namespace prenom

@@ -231,6 +231,27 @@ class Context:
         _check(self.lib.prenom_ctx_launch_count(self.h, C.byref(n)))
         return n.value
 
+    def init_comm(self, nranks: int, rank: int, unique_id: bytes):
+        """Bind an NCCL communicator (prenom_ctx_init_comm) for prenom_reptile_step."""
+        if len(unique_id) != _capi.COMM_ID_BYTES:
+            raise UsageError("NCCL unique id must be 128 bytes")
+        buf = (C.c_uint8 * _capi.COMM_ID_BYTES).from_buffer_copy(unique_id)
+        _check(self.lib.prenom_ctx_init_comm(self.h, nranks, rank, buf))
+
+    def comm_info(self) -> tuple[int, int, int]:
+        """(nranks or 0 when unbound, rank, NCCL version code)."""
+        n, r, v = C.c_int32(), C.c_int32(), C.c_int32()
+        _check(self.lib.prenom_ctx_comm_info(self.h, C.byref(n), C.byref(r), C.byref(v)))
+        return n.value, r.value, v.value
+
+
+def comm_unique_id() -> bytes:
+    """ncclGetUniqueId on this process (rank 0), as bytes to broadcast."""
+    lib = _capi.load()
+    buf = (C.c_uint8 * _capi.COMM_ID_BYTES)()
+    _check(lib.prenom_comm_unique_id(buf))
+    return bytes(buf)
+
 
 def _f32(a):
     return np.ascontiguousarray(a, dtype=np.float32)
@@ -486,6 +507,13 @@ def reptile_delta(meta: ObjectTrainer, adapted: ObjectTrainer, delta_ptr: int):
 
 def reptile_apply(meta: ObjectTrainer, delta_ptr: int, n_tasks: int, beta: float):
     _check(meta.lib.prenom_reptile_apply(meta.h, C.c_void_p(delta_ptr), n_tasks, beta))
+
+
+def reptile_step(meta: ObjectTrainer, adapted: list, n_tasks: int, beta: float):
+    """prenom_reptile_step: this rank's task deltas summed, all-reduced over the context's
+    NCCL communicator (if bound), reptile_update(meta, mean adapted, beta) applied."""
+    arr = (C.c_void_p * max(1, len(adapted)))(*[a.h for a in adapted])
+    _check(meta.lib.prenom_reptile_step(meta.h, arr, len(adapted), n_tasks, beta))
 
 
 def _stats(s: StepStatsC) -> dict:

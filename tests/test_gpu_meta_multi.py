@@ -144,3 +144,51 @@ def test_checkpoint_resume_continues_the_same_run(ctx, mlp):
     for x, y in zip(got, want):
         assert x["frame"] == y["frame"] and x["n_samples"] == y["n_samples"]
         assert abs(x["total"] - y["total"]) <= 1e-3 * abs(y["total"])
+
+
+def test_reptile_step_nccl_one_rank(oracle):
+    """prenom_reptile_step with an NCCL communicator bound to the context (1 rank: the
+    ncclAllReduce runs for real and is the identity): delta-sum kernel -> all-reduce ->
+    interpolation equals the fp32 formula bit for bit, and reptile_update(theta, mean theta_i,
+    beta) of the reference restatement to fp32 rounding (meta.cpp:83-92)."""
+    from paper_2503_01582_b200 import Context, UsageError
+
+    c = Context(0)
+    try:
+        c.init_comm(1, 0, T.comm_unique_id())
+        n, r, ver = c.comm_info()
+        assert (n, r) == (1, 0) and ver > 0
+        rng = np.random.default_rng(5)
+        P = ARCH.param_count()
+        theta = rng.standard_normal(P).astype(np.float32)
+        thetas = [(theta + rng.standard_normal(P).astype(np.float32) * 0.1).astype(np.float32) for _ in range(3)]
+        meta = ObjectTrainer.create(c, ARCH, theta=theta, grid_res=8, cfg=CFG)
+        ws = [ObjectTrainer.create(c, ARCH, theta=t, grid_res=8, cfg=CFG) for t in thetas]
+        beta = np.float32(0.1)
+        T.reptile_step(meta, ws, 3, float(beta))
+        got = meta.get_params()
+        acc = np.zeros(P, np.float32)
+        for t in thetas:
+            acc = (acc + (t - theta)).astype(np.float32)
+        inv = np.float32(1.0) / np.float32(3.0)
+        adapted = (theta + acc * inv).astype(np.float32)
+        want = ((np.float32(1.0) - beta) * theta + beta * adapted).astype(np.float32)
+        assert np.array_equal(got, want)
+        ref = oracle.reptile_update(theta, np.mean(np.stack(thetas), 0).astype(np.float32), float(beta))
+        np.testing.assert_allclose(got, ref, rtol=1e-6, atol=1e-6)
+        # a rank with no task in this meta-step still joins the all-reduce
+        before = meta.get_params()
+        T.reptile_step(meta, [], 2, float(beta))
+        np.testing.assert_allclose(meta.get_params(), before, rtol=1e-6, atol=1e-7)
+    finally:
+        c.close()
+    # without a communicator the other ranks' tasks cannot be summed
+    c2 = Context(0)
+    try:
+        meta = ObjectTrainer.create(c2, ARCH, grid_res=8, cfg=CFG)
+        w = ObjectTrainer.create(c2, ARCH, grid_res=8, cfg=CFG)
+        with pytest.raises(UsageError):
+            T.reptile_step(meta, [w], 2, 0.1)
+        T.reptile_step(meta, [w], 1, 0.1)  # one task, no communicator: the exact reference update
+    finally:
+        c2.close()

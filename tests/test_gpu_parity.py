@@ -65,7 +65,7 @@ def test_field_eval_train_tile_path(ctx, oracle, rng):
     for a in archs(rng):
         params = grad_params(a, rng)
         xyz = rng.uniform(0, 1, (300, 3)).astype(np.float32)
-        s, c, _ = T.debug_field_eval(ctx, a, params, xyz, precision=2)
+        s, c, _ = T.debug_field_eval(ctx, a, params, xyz, precision=3)
         so, co = oracle.field_eval(a, params, xyz)
         np.testing.assert_allclose(s, so, rtol=1e-4, atol=1e-6)
         np.testing.assert_allclose(c, co, rtol=1e-4, atol=1e-6)

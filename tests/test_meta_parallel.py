@@ -6,7 +6,7 @@
   and equals reptile_update(theta, mean_i theta_i, beta) (meta.cpp:83-92,
   SPEC.md:323 linearity);
 * the meta-step task schedule (round-robin over per-epoch shuffles,
-  meta.cpp:104-110).
+  meta.cpp:104-110), equal to the compiled reference's order.
 """
 import os
 
@@ -39,6 +39,21 @@ def test_task_schedule_round_robin_epochs():
     flat = [t for b in s for t in b]
     assert sorted(flat[:5]) == list(range(5)) and sorted(flat[5:10]) == list(range(5))
     assert task_schedule(5, 7, 2, seed=3) == s
+
+
+@pytest.mark.ref
+@pytest.mark.parametrize("n_tasks", [1, 2, 7, 512, 513, 70001])
+def test_task_schedule_equals_reference_meta_train_order(ref, n_tasks):
+    """meta_train's schedule (meta.cpp:101-112: order reshuffled in place each epoch by
+    std::shuffle over mt19937(derive_seed(seed, 0xE9C6 + epoch))) is index work: the
+    restated libstdc++ shuffle reproduces the compiled reference's order exactly, for 3 epochs,
+    on both of libstdc++'s paths (paired draws while n^2 < 2^32, single draws beyond)."""
+    for seed in (0, 9, 2**40 + 5):
+        want = ref.meta_task_order(n_tasks, seed, 3)
+        steps = 3 * n_tasks if n_tasks < 1000 else n_tasks + 5
+        got = [b[0] for b in task_schedule(n_tasks, steps, 1, seed)]
+        flat = want.reshape(-1)[:steps]
+        assert got == flat.tolist()
 
 
 class OracleEngine(Engine):

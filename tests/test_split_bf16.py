@@ -1,0 +1,127 @@
+"""Split-bf16 ("bf16x3") tensor-core MLP mode vs the CPU oracle, held to the fp32 bars.
+
+PRENOM_MLP_BF16X3 runs every MLP product of field_eval / field_backward (field.cpp:174-293)
+on tcgen05 kind::f16 with operands split as x = hi + lo (both bf16; hi*hi + hi*lo + lo*hi,
+fp32 accumulation in TMEM), so the tensor-core path meets north_star's fp32 tolerances:
+MLP outputs within 1e-4 relative, the first train step's loss terms within 1e-5, and the
+loss after 200 steps within 1% of the oracle -- at BASELINE cfg1's full size and on a
+reduced-ray cfg2 (L16 T2^19 W64 H2, prior sampling).
+"""
+import os
+
+import numpy as np
+import pytest
+
+from conftest import grad_params
+from paper_2503_01582_b200 import FieldArch, ObjectTrainer, TrainConfig, scenes
+from paper_2503_01582_b200 import trainer as T
+from paper_2503_01582_b200._capi import MLP_BF16X3
+
+pytestmark = pytest.mark.gpu
+
+
+def tc_archs():
+    return [scenes.cfg1_arch(),
+            FieldArch(hash_levels=16, features_per_level=2, log2_table_size=14, base_resolution=16,
+                      per_level_scale=scenes.cfg2_arch().per_level_scale, hidden_width=64, hidden_layers=2),
+            FieldArch(hash_levels=12, features_per_level=2, log2_table_size=13, base_resolution=8,
+                      per_level_scale=1.4, hidden_width=32, hidden_layers=1, density_activation=1),
+            FieldArch(hash_levels=8, features_per_level=2, log2_table_size=12, base_resolution=8,
+                      per_level_scale=1.4, hidden_width=64, hidden_layers=1)]
+
+
+def test_split_forward_within_1e4(ctx, oracle, rng):
+    """north_star fp32 bar on the tensor-core forward: sigma and rgb within 1e-4 relative."""
+    for a in tc_archs():
+        params = grad_params(a, rng) * 0.5
+        xyz = rng.uniform(0, 1, (1000, 3)).astype(np.float32)
+        s, c, _ = T.debug_field_eval(ctx, a, params, xyz, precision=MLP_BF16X3)
+        so, co = oracle.field_eval(a, params, xyz)
+        np.testing.assert_allclose(s, so, rtol=1e-4, atol=1e-6)
+        np.testing.assert_allclose(c, co, rtol=1e-4, atol=1e-6)
+
+
+def test_split_backward_matches_oracle(ctx, oracle, rng):
+    """field_backward (MLP weights + table gradient scatter) within 1e-4 of the fp32 oracle."""
+    for a in tc_archs():
+        params = grad_params(a, rng) * 0.5
+        n = 700
+        xyz = rng.uniform(0, 1, (n, 3)).astype(np.float32)
+        ds = rng.standard_normal(n).astype(np.float32) * 0.1
+        dr = rng.standard_normal((n, 3)).astype(np.float32)
+        g = T.debug_field_backward(ctx, a, params, xyz, ds, dr, precision=MLP_BF16X3)
+        go = oracle.field_backward(a, params, xyz, ds, dr)
+        nh = a.hash_param_count()
+        for part in (slice(0, nh), slice(nh, None)):
+            num = np.linalg.norm(g[part] - go[part])
+            assert num <= 1e-4 * np.linalg.norm(go[part]), (a, part, num / np.linalg.norm(go[part]))
+        assert np.mean((g == 0) != (go == 0)) < 1e-3
+
+
+def small_scene(seed=3, res=48, views=6):
+    sc = scenes.box_union_scene(n_views=views, res=res, seed=seed)
+    return sc, scenes.occupancy_prior(sc.boxes, R=16)
+
+
+@pytest.mark.parametrize("B,S,prior", [(1, 1, 0), (7, 24, 1), (333, 33, 0), (64, 256, 1), (130, 96, 1)])
+def test_split_first_step_loss_terms_1e5(ctx, oracle, B, S, prior):
+    sc, grid = small_scene()
+    arch = FieldArch(hash_levels=8, features_per_level=2, log2_table_size=12, base_resolution=8,
+                     per_level_scale=1.4, hidden_width=32, hidden_layers=2)
+    cfg = TrainConfig(rays_per_iter=B, samples_per_ray=S, coarse_samples=16, prior_sampling=prior,
+                      grid_refresh_every=0, mlp_precision=MLP_BF16X3)
+    theta = grad_params(arch, np.random.default_rng(11)) * 0.5
+    theta[: arch.hash_param_count()] *= 1e-3
+    gpu = ObjectTrainer.create(ctx, arch, theta=theta, grid=grid, seed=11, cfg=cfg, box_min=sc.box_min,
+                               box_max=sc.box_max)
+    gpu.set_frames(sc.cams, sc.rgb, sc.depth, sc.mask, 1, sc.obj_pose)
+    ob = oracle.object_create(arch, theta, grid, grid.shape[0], 11, cfg.to_c(), sc.box_min, sc.box_max)
+    ob.set_frames(sc.cams, sc.rgb, sc.depth, sc.mask, 1, sc.obj_pose)
+    sg, so = gpu.train_step(2), ob.train_step(2)
+    for x, y in zip(sg, so):
+        assert x["frame"] == y["frame"] and x["n_samples"] == y["n_samples"] and x["escaped"] == y["escaped"]
+    for k in ("total", "color", "depth", "sigma"):
+        assert abs(sg[0][k] - so[0][k]) <= 1e-5 * abs(so[0][k]) + 1e-9, (k, sg[0], so[0])
+    assert np.isfinite(sg[1]["total"])
+
+
+def full_size_pair(ctx, oracle, which, rays=None):
+    if which == "cfg1":
+        sc = scenes.sphere_scene()
+        arch = scenes.cfg1_arch()
+        grid = np.zeros((8, 8, 8), np.float32)
+        kw = dict(rays_per_iter=4096, samples_per_ray=64, prior_sampling=0, grid_refresh_every=0)
+    else:
+        sc = scenes.box_union_scene(n_views=50, res=256, seed=1000)
+        arch = scenes.cfg2_arch(64)
+        grid = scenes.occupancy_prior(sc.boxes, R=32)
+        kw = dict(rays_per_iter=rays or 8192, samples_per_ray=96, coarse_samples=32, prior_sampling=1,
+                  grid_refresh_every=50)
+    rng = np.random.default_rng(0)
+    P, nh = arch.param_count(), arch.hash_param_count()
+    theta = np.empty(P, np.float32)
+    theta[:nh] = rng.uniform(-1e-4, 1e-4, nh)
+    theta[nh:] = (rng.standard_normal(P - nh) * np.sqrt(2.0 / arch.hidden_width)).astype(np.float32)
+    cfg = TrainConfig(mlp_precision=MLP_BF16X3, **kw)
+    gpu = ObjectTrainer.create(ctx, arch, theta=theta, grid=grid, seed=0, cfg=cfg, box_min=sc.box_min,
+                               box_max=sc.box_max)
+    gpu.set_frames(sc.cams, sc.rgb, sc.depth, sc.mask, 1, sc.obj_pose)
+    ob = oracle.object_create(arch, theta, grid, grid.shape[0], 0, TrainConfig(**kw).to_c(), sc.box_min, sc.box_max)
+    ob.set_frames(sc.cams, sc.rgb, sc.depth, sc.mask, 1, sc.obj_pose)
+    return gpu, ob
+
+
+@pytest.mark.parametrize("which,rays", [("cfg1", None), ("cfg2", 1024)])
+def test_split_200_steps_full_size_loss_within_1pct(ctx, oracle, which, rays):
+    """north_star: loss after 200 steps within 1% of the CPU reference path, on the tensor-core
+    MLP: BASELINE cfg1 at full size, and cfg2's architecture / prior sampler with 1024 rays
+    (the oracle is threaded: PO_THREADS = host cores, deterministic per thread count)."""
+    os.environ.setdefault("PO_THREADS", str(min(32, os.cpu_count() or 1)))
+    gpu, ob = full_size_pair(ctx, oracle, which, rays)
+    lg = np.array([s["total"] for s in gpu.train_step(200)])
+    lo = np.array([s["total"] for s in ob.train_step(200)])
+    assert lo[-20:].mean() < 0.8 * lo[:5].mean()  # it trains
+    assert abs(lg[0] / lo[0] - 1) < 1e-5
+    ratio = lg[-20:].mean() / lo[-20:].mean()
+    print(which, "bf16x3 / oracle final-loss ratio", ratio)
+    assert abs(ratio - 1) < 0.01, ratio
