@@ -221,6 +221,7 @@ prenom_status prenom_object_set_frames(prenom_object_t o, int n, const prenom_ca
     if (cams[i].width != W || cams[i].height != H)
       return fail(PRENOM_DATA, "generate_rays: mask does not match camera dimensions");
   CUDA_TRY(cudaSetDevice(o->ctx->device));
+  STATUS_TRY(drop_prefetch(o));
   init_frames(o, n, cams, inst, pose);
   const size_t npx = (size_t)W * H;
   for (int i = 0; i < n; ++i)
@@ -240,6 +241,7 @@ prenom_status prenom_object_synth_frames(prenom_object_t o, int n, const prenom_
   for (int i = 0; i < n; ++i)
     if (cams[i].width != W || cams[i].height != H) return fail(PRENOM_DATA, "views differ in size");
   CUDA_TRY(cudaSetDevice(o->ctx->device));
+  STATUS_TRY(drop_prefetch(o));
   init_frames(o, n, cams, 1, pose);
   cudaStream_t st = o->ctx->stream;
   const size_t npx = (size_t)W * H;
@@ -302,6 +304,8 @@ prenom_status prenom_object_upload_frame(prenom_object_t o, int frame, const flo
   // It also waits for the work already on the main stream (whose sampling may
   // read the frame), but not for steps enqueued after it.
   cudaStream_t side = o->ctx->overlap ? o->ctx->side : o->ctx->stream;
+  // samples already prefetched from this very frame would be stale: re-sample
+  if (o->sample_ready && o->prefetch_frame == frame) STATUS_TRY(drop_prefetch(o));
   if (!o->ev_upload) {
     CUDA_TRY(cudaEventCreateWithFlags(&o->ev_upload, cudaEventDisableTiming));
     CUDA_TRY(cudaEventCreateWithFlags(&o->ev_main, cudaEventDisableTiming));
@@ -350,6 +354,7 @@ prenom_status prenom_set_grid(prenom_object_t o, int R, const float* grid) {
   if (R < 2 || R > 1024) return fail(PRENOM_DATA, "grid resolution out of range");
   CUDA_TRY(cudaSetDevice(o->ctx->device));
   const size_t n = (size_t)R * R * R;
+  STATUS_TRY(drop_prefetch(o));  // (the prefetched samples read the old grid)
   CUDA_TRY(cudaStreamSynchronize(o->ctx->stream));
   CUDA_TRY(o->grid.ensure(n));
   o->R = R;
@@ -375,6 +380,7 @@ prenom_status prenom_set_adam(prenom_object_t o, const float* m, const float* v,
   if (!o || !m || !v) return fail(PRENOM_USAGE, "NULL argument");
   if (step < 0) return fail(PRENOM_USAGE, "negative step");
   CUDA_TRY(cudaSetDevice(o->ctx->device));
+  STATUS_TRY(drop_prefetch(o));  // the step keys the draws
   CUDA_TRY(cudaMemcpyAsync(o->m.p, m, o->P * sizeof(float), cudaMemcpyHostToDevice, o->ctx->stream));
   CUDA_TRY(cudaMemcpyAsync(o->v.p, v, o->P * sizeof(float), cudaMemcpyHostToDevice, o->ctx->stream));
   CUDA_TRY(cudaStreamSynchronize(o->ctx->stream));
@@ -385,6 +391,7 @@ prenom_status prenom_set_adam(prenom_object_t o, const float* m, const float* v,
 prenom_status prenom_reset_adam(prenom_object_t o) {
   if (!o) return fail(PRENOM_USAGE, "NULL object");
   CUDA_TRY(cudaSetDevice(o->ctx->device));
+  STATUS_TRY(drop_prefetch(o));  // the step keys the draws
   const size_t P4 = (o->P + 3) & ~size_t(3);
   CUDA_TRY(cudaMemsetAsync(o->m.p, 0, P4 * sizeof(float), o->ctx->stream));
   CUDA_TRY(cudaMemsetAsync(o->v.p, 0, P4 * sizeof(float), o->ctx->stream));
@@ -395,6 +402,10 @@ prenom_status prenom_reset_adam(prenom_object_t o) {
 
 prenom_status prenom_object_set_seed(prenom_object_t o, uint64_t seed) {
   if (!o) return fail(PRENOM_USAGE, "NULL object");
+  if (o->sample_ready) {
+    CUDA_TRY(cudaSetDevice(o->ctx->device));
+    STATUS_TRY(drop_prefetch(o));  // the seed keys the draws
+  }
   o->seed = seed;
   return PRENOM_OK;
 }

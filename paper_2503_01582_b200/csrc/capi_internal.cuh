@@ -251,6 +251,7 @@ struct prenom_object_s {
   // sample-ahead pipelining (k_sample(t+1) on ctx->side while k_adam(t) runs)
   cudaEvent_t ev_bwd = nullptr, ev_sample = nullptr;
   bool sample_ready = false;
+  int prefetch_frame = -1;  // keyframe the prefetched samples were drawn from
   cudaStream_t lane = nullptr;  // set while prenom_train_step_many runs this object on a lane stream
   // streaming: frame uploads go on ctx->side (the sampling stream); a step
   // whose sampling runs on the main stream waits for ev_upload first
@@ -517,6 +518,7 @@ inline prenom_status enqueue_step(prenom_object_s* o, StepStatsDev* stats, bool 
     STATUS_TRY(enqueue_sample(o, o->step + 1, o->ctx->side));
     CUDA_TRY(cudaEventRecord(o->ev_sample, o->ctx->side));
     o->sample_ready = true;
+    o->prefetch_frame = frame_of_step(o, o->step + 1);
   }
   // adam_step (field.cpp:295-310); grad zeroed in the same pass (mapper.cpp:175)
   const float stepf = (float)(o->step + 1);
@@ -535,6 +537,20 @@ inline prenom_status enqueue_step(prenom_object_s* o, StepStatsDev* stats, bool 
     CUDA_TRY(launch_refresh_grid(o->fd, o->params.p, o->R, o->grid.p, o->flag.p, st));
     o->ctx->launches += 1;
   }
+  return PRENOM_OK;
+}
+
+// A prefetched sample set (enqueue_step with has_next) was drawn for
+// (step + 1, seed, grid, frames) as they stood. Every call that changes one of
+// them drops it, after ordering the context stream behind the sampling kernel
+// (which may still be reading the grid / frame being replaced), so the next
+// step re-samples from the new state (resumed objects continue the
+// same sample stream; a new grid or keyframe is what the next step samples).
+inline prenom_status drop_prefetch(prenom_object_s* o) {
+  if (!o->sample_ready) return PRENOM_OK;
+  CUDA_TRY(cudaStreamWaitEvent(o->ctx->stream, o->ev_sample, 0));
+  o->sample_ready = false;
+  o->prefetch_frame = -1;
   return PRENOM_OK;
 }
 

@@ -63,11 +63,12 @@ prenom_status prenom_density_query(prenom_object_t o, int R, float* out, int upd
   cudaStream_t st = o->ctx->stream;
   const size_t n = (size_t)R * R * R;
   DevBuf<float>& d = o->query;  // kept across calls (no per-query cudaMalloc/cudaFree)
-  CUDA_TRY(d.ensure(n));
+  CUDA_TRY(d.ensure(n));  // (never the live sampling grid: update swaps the two)
   CUDA_TRY(launch_refresh_grid(o->fd, o->params.p, R, d.p, o->flag.p, st));
   o->ctx->launches += 1;
   if (out) CUDA_TRY(cudaMemcpyAsync(out, d.p, n * sizeof(float), cudaMemcpyDeviceToHost, st));
   if (update) {
+    STATUS_TRY(drop_prefetch(o));  // the sampling grid is replaced
     CUDA_TRY(cudaStreamSynchronize(st));
     std::swap(o->grid.p, d.p);
     std::swap(o->grid.n, d.n);

@@ -38,10 +38,10 @@ constexpr int kFwdSmemKbDefault = 40;
 // encode's gathers (was 57 KB/CTA padding, 196 KB carve-out, 60 KB of L1:
 // k_fwd_tc 0.195 -> 0.186 ms on cfg2)
 constexpr int kFwdCarveoutDefault = 58;
-// split-bf16 forward (~77 KB of operand tiles per CTA): two CTAs per SM
-constexpr int kFwdSThreadsDefault = 256;
+// split-bf16 forward (~62 KB per CTA): two CTAs of 512 threads per SM
+constexpr int kFwdSThreadsDefault = 512;
 constexpr int kFwdSCtasDefault = 2;
-constexpr int kFwdSCarveoutDefault = -1;
+constexpr int kFwdSCarveoutDefault = 58;  // 132 KB of shared memory, 124 KB of L1
 constexpr size_t kSmemPerSm = 228 * 1024;
 constexpr int kSlack = 0;       // weight tiles are never over-read
 // M=128 MN-major views of the (features|1) and (activations|1) tiles read
@@ -218,8 +218,11 @@ __global__ void __launch_bounds__(NT) k_fwd_tc(FieldDesc fd, const float* __rest
   WT wt;
   unsigned char* p = smem;
   wt.carve(p);
+  // split mode: X overlays the activation tile (it is dead once the layer-0
+  // MMA and the bulk store of the features have read it), so a CTA needs
+  // ~62 KB and two fit an SM with 124 KB of L1 left for the gathers
   unsigned char* X = p;
-  p += kXBytes;
+  if (!SPL) p += kXBytes;
   // one activation tile: layer l+1's MMA completes (mbarrier) before layer
   // l+1's epilogue overwrites the tile it read
   unsigned char* Hb = p;
@@ -278,6 +281,10 @@ __global__ void __launch_bounds__(NT) k_fwd_tc(FieldDesc fd, const float* __rest
       umma::bulk_s2g(feat_tiles + t * (kXBytes / 16), X, kXBytes);
     }
     wait_mma(&bar, phase);
+    if (SPL) {  // the bulk store must have read X before H overwrites it
+      if (tid == 0) umma::bulk_wait_read();
+      __syncthreads();
+    }
     epi_relu<W, TPS, HLO>(tm, 0, wt.bias, Hb, W);
     for (int l = 1; l < H; ++l) {
       sync_for_mma();
@@ -462,10 +469,19 @@ __device__ __forceinline__ void mbar_arrive2(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], 2;" ::"r"(umma::smem_u32(bar)) : "memory");
 }
 
+template <int INP, int W, int H, int SPL>
+struct BwdLayout {
+  static constexpr bool kOverlay = SPL && H >= 2;
+  static constexpr size_t kOperandBytes =
+      kOverlay ? (size_t)(128 * 16 * 2 * 2 + H * 128 * (W + 8) * 2 * 2 + 1024)
+               : (size_t)((128 * (INP + 8) * 2 + kSlackX) + H * (128 * (W + 8) * 2 + kSlackH) + 128 * 16 * 2) *
+                     (SPL ? 2 : 1);
+};
+
 // SPL: split-bf16 operands; `split` bits: 0 forward recompute, 1 the data
 // products (dH, dX), 2 the weight gradients.
 template <int INP, int W, int H, int SPL>
-__global__ void __launch_bounds__(kBwdThreads, SPL ? 1 : 2)
+__global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
     k_bwd_tc(FieldDesc fd, const float* __restrict__ params, float* __restrict__ grad, long long n_total, int S,
              const int* __restrict__ count, const float4* __restrict__ pos, const uint4* __restrict__ feat_tiles,
              const float4* __restrict__ dout, int* tile_ctr, int skip_scatter, int mlp_levels,
@@ -473,9 +489,15 @@ __global__ void __launch_bounds__(kBwdThreads, SPL ? 1 : 2)
   using CM = BwdCols<INP, W, H>;
   using WT = WeightTiles<INP, W, H, SPL>;
   constexpr int XC = INP + 8, HC = W + 8;
+  // Split mode with >= 2 hidden layers: the feature tile X overlays the last
+  // hidden tile H_{H-1} (X is dead from the layer-0 MMA until dW0, and is
+  // re-fetched by TMA once D_{H-1} is dead), so the operand tiles fit two CTAs
+  // per SM (~110 KB each); the MN-major over-reads land in the next buffer and
+  // one slack block at the end.
+  constexpr bool OV = BwdLayout<INP, W, H, SPL>::kOverlay;
   // lo copies sit one (tile + slack) after the hi copies
-  constexpr uint32_t XLO = SPL ? 128 * XC * 2 + kSlackX : 0;
-  constexpr uint32_t HLO = SPL ? 128 * HC * 2 + kSlackH : 0;
+  constexpr uint32_t XLO = SPL ? 128 * XC * 2 + (OV ? 0 : kSlackX) : 0;
+  constexpr uint32_t HLO = SPL ? 128 * HC * 2 + (OV ? 0 : kSlackH) : 0;
   constexpr uint32_t GLO = SPL ? 128 * 16 * 2 : 0;
   constexpr uint32_t kFeatBytes = 128 * INP * 2 * (SPL ? 2 : 1);
   const bool sp_f = SPL && (split & 1), sp_d = SPL && (split & 2), sp_w = SPL && (split & 4);
@@ -489,23 +511,38 @@ __global__ void __launch_bounds__(kBwdThreads, SPL ? 1 : 2)
   WT wt;
   unsigned char* p = smem;
   wt.carve(p);
-  unsigned char* X = p;  // [128][INP+8]: features | ones
-  p += (128 * XC * 2 + kSlackX) * (SPL ? 2 : 1);
+  unsigned char* X;      // [128][INP+8]: features | ones
   unsigned char* Ht[2];  // [128][W+8] per hidden layer: activations | ones
-  for (int l = 0; l < H; ++l) {
-    Ht[l] = p;
-    p += (128 * HC * 2 + kSlackH) * (SPL ? 2 : 1);
+  unsigned char* G;      // [128][16] g_raw (4 used)
+  unsigned char* zero_begin = p;
+  if (OV) {
+    G = p;
+    p += 128 * 16 * 2 * 2;
+#pragma unroll
+    for (int l = 0; l < H; ++l) {
+      Ht[l] = p;
+      p += 128 * HC * 2 * 2;
+    }
+    X = Ht[H - 1];
+    p += 1024;
+  } else {
+    X = p;
+    p += (128 * XC * 2 + kSlackX) * (SPL ? 2 : 1);
+    for (int l = 0; l < H; ++l) {
+      Ht[l] = p;
+      p += (128 * HC * 2 + kSlackH) * (SPL ? 2 : 1);
+    }
+    G = p;
+    p += 128 * 16 * 2 * (SPL ? 2 : 1);
   }
-  unsigned char* G = p;  // [128][16] g_raw (4 used)
-  p += 128 * 16 * 2 * (SPL ? 2 : 1);
   // D_l = dH_l * relu'(H_l) is written over H_l itself (H_l is dead once its
   // ReLU gate is taken)
   unsigned char* zero_end = p;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid < kMlpThreads) wt.load(fd, params + fd.hash_params, kMlpThreads);
   {
-    uint4* z = reinterpret_cast<uint4*>(X);
-    const int n16 = (int)((zero_end - X) / 16);
+    uint4* z = reinterpret_cast<uint4*>(zero_begin);
+    const int n16 = (int)((zero_end - zero_begin) / 16);
     for (int i = tid; i < n16; i += kBwdThreads) z[i] = make_uint4(0u, 0u, 0u, 0u);
   }
   __syncthreads();
@@ -573,6 +610,23 @@ __global__ void __launch_bounds__(kBwdThreads, SPL ? 1 : 2)
     uint32_t phase = 0, xphase = 0;
     int iter = 0;
     const int q = warp & 3, half = warp >> 2, row = 32 * q + lane;
+    // (overlay) the ones column of [X | 1] and [H_{H-1} | 1], rewritten per tile:
+    // one 16-byte core-matrix row [1, 0, ..., 0] (hi) and zeros (lo) per sample
+    const uint4 ones_row = make_uint4(0x3F80u, 0u, 0u, 0u), zero_row = make_uint4(0u, 0u, 0u, 0u);
+    auto set_ones = [&](unsigned char* tile, int col, int C, uint32_t lo) {
+      if (tid < 128) {
+        *reinterpret_cast<uint4*>(tile + umma::cm_offset(tid, col, C)) = ones_row;
+        *reinterpret_cast<uint4*>(tile + lo + umma::cm_offset(tid, col, C)) = zero_row;
+      }
+    };
+    auto fetch_x = [&](long long t) {  // stored bf16 features -> X (TMA), one bulk copy per 8-row group
+      const unsigned char* src = reinterpret_cast<const unsigned char*>(feat_tiles + t * (kFeatBytes / 16));
+      umma::mbar_arrive_expect_tx(&xbar, kFeatBytes);
+      for (int rg = 0; rg < 16; ++rg) umma::bulk_g2s(X + rg * (XC / 8) * 128, src + rg * INP * 16, INP * 16, &xbar);
+      if (SPL)
+        for (int rg = 0; rg < 16; ++rg)
+          umma::bulk_g2s(X + XLO + rg * (XC / 8) * 128, src + 128 * INP * 2 + rg * INP * 16, INP * 16, &xbar);
+    };
     auto fetch = [&]() -> long long {
       if (tid == 0) s_tile = atomicAdd(tile_ctr, 1);
       named_sync(1, kMlpThreads);
@@ -584,15 +638,8 @@ __global__ void __launch_bounds__(kBwdThreads, SPL ? 1 : 2)
       const bool valid = gs < n_total && __ldg(count + ray_of(gs, S)) > 0;
       // ---- stored bf16 features -> X by the TMA engine (no LSU work): one
       // bulk copy per 8-row group (the X row-group stride is longer: ones column)
-      if (tid == 0) {
-        const unsigned char* src = reinterpret_cast<const unsigned char*>(feat_tiles + t * (kFeatBytes / 16));
-        umma::mbar_arrive_expect_tx(&xbar, kFeatBytes);
-        for (int rg = 0; rg < 16; ++rg)
-          umma::bulk_g2s(X + rg * (XC / 8) * 128, src + rg * INP * 16, INP * 16, &xbar);
-        if (SPL)
-          for (int rg = 0; rg < 16; ++rg)
-            umma::bulk_g2s(X + XLO + rg * (XC / 8) * 128, src + 128 * INP * 2 + rg * INP * 16, INP * 16, &xbar);
-      }
+      if (tid == 0) fetch_x(t);
+      if (OV) set_ones(X, INP, XC, XLO);
       umma::mbar_wait(&xbar, xphase);
       xphase ^= 1u;
       mlp_sync_for_mma();
@@ -605,8 +652,10 @@ __global__ void __launch_bounds__(kBwdThreads, SPL ? 1 : 2)
         umma::commit(&bar);
       }
       wait_mma(&bar, phase);
+      if (OV) set_ones(Ht[H - 1], W, HC, HLO);  // X is dead until dW0
       uint64_t gate[2];
       gate[0] = epi_relu_gate<W, kMG, HLO>(tr, wt.bias, Ht[0], HC);
+#pragma unroll
       for (int l = 1; l < H; ++l) {
         mlp_sync_for_mma();
         if (tid == 0) {
@@ -657,7 +706,12 @@ __global__ void __launch_bounds__(kBwdThreads, SPL ? 1 : 2)
         umma::commit(&bar);
       }
       wait_mma(&bar, phase);
+#pragma unroll
       for (int l = H - 1; l >= 0; --l) {
+        if (OV && l == 0) {  // D_{H-1} is dead: X back into its place for dW0
+          if (tid == 0) fetch_x(t);
+          set_ones(X, INP, XC, XLO);
+        }
         // D_l = dH_l * relu'(H_l) -> D tile
         {
           constexpr int NHD = W / kMG;
@@ -671,6 +725,10 @@ __global__ void __launch_bounds__(kBwdThreads, SPL ? 1 : 2)
             for (int j = 0; j < 8; ++j) v[j] = (gate[l] >> (c + j)) & 1ull ? v[j] : 0.f;
             umma::st_row8_split(Ht[l], row, col, HC, v, HLO);  // D_l in place of H_l
           }
+        }
+        if (OV && l == 0) {
+          umma::mbar_wait(&xbar, xphase);
+          xphase ^= 1u;
         }
         mlp_sync_for_mma();
         if (tid == 0) {
@@ -798,14 +856,15 @@ int sms() {
 
 template <int INP, int W, int H, int SPL>
 size_t fwd_smem() {
+  static_assert(W >= INP, "split-mode X overlays the activation tile");
   return WeightTiles<INP, W, H, SPL>::kBytes + ((H * W + 4) * 4 + 15) / 16 * 16 +
-         (128 * INP * 2 + 128 * W * 2) * (SPL ? 2 : 1) + 1024;
+         (SPL ? 128 * W * 2 * 2 : 128 * INP * 2 + 128 * W * 2) + 1024;
 }
 
 template <int INP, int W, int H, int SPL>
 size_t bwd_smem() {
-  return WeightTiles<INP, W, H, SPL>::kBytes + ((H * W + 4) * 4 + 15) / 16 * 16 +
-         ((128 * (INP + 8) * 2 + kSlackX) + H * (128 * (W + 8) * 2 + kSlackH) + 128 * 16 * 2) * (SPL ? 2 : 1) + 1024;
+  return WeightTiles<INP, W, H, SPL>::kBytes + ((H * W + 4) * 4 + 15) / 16 * 16 + BwdLayout<INP, W, H, SPL>::kOperandBytes +
+         1024;
 }
 
 template <int INP, int W, int H, int NT, int SPL>

@@ -192,6 +192,8 @@ def derive_seed(base: int, salt: int) -> int:
     return (s ^ (s >> 32)) & 0xFFFFFFFF
 
 
+MAX_GRID_RES = 1024  # prenom_object_create / prenom_set_grid / prenom_density_query
+
 # -------------------------------------------------------------- context
 class Context:
     """One per GPU (prenom_ctx_create)."""
@@ -288,7 +290,13 @@ class ObjectTrainer:
     def from_prior(cls, ctx: Context, prior, seed: int = 0, cfg: TrainConfig | None = None,
                    box_min=(-0.5, -0.5, -0.5), box_max=(0.5, 0.5, 0.5)) -> "ObjectTrainer":
         """Create from a category prior (a prior.PriorBundle, e.g. from load_prior):
-        arch, θ and the density grid come from the bundle (mapper.cpp:133-137)."""
+        arch, θ and the density grid come from the bundle (mapper.cpp:133-137).
+        Deviation: load_prior accepts grids up to 4096^3 (prior_bundle.cpp); the device
+        sampler's grids are limited to 1024^3 (32-bit lattice indices), larger ones are a
+        DataError here rather than a silent resample."""
+        R = int(np.asarray(prior.grid).shape[0])
+        if R > MAX_GRID_RES:
+            raise DataError(f"from_prior: {R}^3 prior grid exceeds the device sampler's {MAX_GRID_RES}^3 limit")
         return cls.create(ctx, prior.arch, theta=prior.theta, grid=prior.grid, seed=seed, cfg=cfg,
                           box_min=box_min, box_max=box_max)
 

@@ -115,6 +115,48 @@ def test_streaming_async_steps_equal_train_step(ctx):
         b.wait_stats(12345)
 
 
+@pytest.mark.parametrize("mutation", ["upload_new_pixels", "set_seed", "restore", "set_grid"])
+def test_pending_prefetch_is_dropped_by_state_changes(ctx, mutation):
+    """A step enqueued with prefetch_next samples step t+1 ahead on the sampling stream. A call
+    that changes what step t+1 must sample -- new pixels for its keyframe, a new seed, a
+    checkpoint restore, a new sampling grid -- drops that prefetch, so the step equals the same
+    sequence run without any prefetch."""
+    sc = tasks()[1]
+    grid = scenes.occupancy_prior(sc.boxes, R=16)
+    cfg = TrainConfig(rays_per_iter=128, samples_per_ray=32, prior_sampling=1, grid_refresh_every=0)
+
+    def make():
+        o = ObjectTrainer.create(ctx, ARCH, grid=grid, seed=5, cfg=cfg, box_min=sc.box_min, box_max=sc.box_max)
+        o.set_frames(sc.cams, sc.rgb, sc.depth, sc.mask, 1, sc.obj_pose)
+        return o
+
+    a, b = make(), make()
+    ck = a.checkpoint()
+    f1 = a.frame_at(1)
+    new_rgb = np.ascontiguousarray(1.0 - sc.rgb[f1]).astype(np.float32)
+    new_grid = np.ascontiguousarray(grid[::-1]).astype(np.float32)
+
+    def mutate(o):
+        if mutation == "upload_new_pixels":
+            o.upload_frame(f1, new_rgb, np.ascontiguousarray(sc.depth[f1]), None)
+        elif mutation == "set_seed":
+            o.set_seed(99)
+        elif mutation == "restore":
+            o.restore(ck)
+        else:
+            o.set_grid(new_grid)
+
+    a.wait_stats(a.train_step_async(1, prefetch_next=True))  # leaves step 1's samples prefetched
+    mutate(a)
+    got = a.train_step(1)[0]
+    b.train_step(1)  # no prefetch
+    mutate(b)
+    want = b.train_step(1)[0]
+    assert got["frame"] == want["frame"] and got["n_samples"] == want["n_samples"]
+    assert got["escaped"] == want["escaped"]
+    assert abs(got["total"] - want["total"]) <= 1e-4 * abs(want["total"]), (got, want)
+
+
 @pytest.mark.parametrize("mlp", [0, 1])
 def test_checkpoint_resume_continues_the_same_run(ctx, mlp):
     """Checkpoint after 7 steps (θ, Adam m/v/step, sampling grid), restore into a fresh
