@@ -42,6 +42,11 @@ constexpr int kFwdCarveoutDefault = 58;
 constexpr int kFwdSThreadsDefault = 512;
 constexpr int kFwdSCtasDefault = 2;
 constexpr int kFwdSCarveoutDefault = 58;  // 132 KB of shared memory, 124 KB of L1
+// split forward with TMEM-resident activations (k_fwd_ts, ~47 KB per CTA)
+constexpr int kFwdSTsDefault = 1;
+constexpr int kFwdSTsThreads = 512;
+constexpr int kFwdSTsCtas = 2;
+constexpr int kFwdSTsCarveout = 44;  // 100 KB of shared memory, 156 KB of L1
 constexpr size_t kSmemPerSm = 228 * 1024;
 constexpr int kSlack = 0;       // weight tiles are never over-read
 // M=128 MN-major views of the (features|1) and (activations|1) tiles read
@@ -335,6 +340,156 @@ __global__ void __launch_bounds__(NT) k_fwd_tc(FieldDesc fd, const float* __rest
   if (warp == 0) umma::tmem_dealloc(tm, 64);
 }
 
+// ------------------------------------------------------------------ fwd, TS form
+// The same forward with the hidden activations kept in tensor memory: each
+// epilogue reads the fp32 accumulator (tcgen05.ld), applies bias + ReLU,
+// (split mode) splits hi/lo, packs bf16 pairs and writes them back with
+// tcgen05.st; the next layer's MMA reads its A operand from TMEM
+// (tcgen05.mma ... [d], [a], b_desc). Shared memory holds only the weights and
+// the feature tile (~46 KB split, ~23 KB bf16), so more CTAs -- or more L1 for
+// the encode's gathers -- fit an SM, and no epilogue touches shared memory.
+// TMEM per CTA: accumulator [0, W), H hi [W, W + W/2), H lo [W + W/2, 2W).
+template <int INP, int W, int H, int NT, int SPL>
+__global__ void __launch_bounds__(NT) k_fwd_ts(FieldDesc fd, const float* __restrict__ params, long long n_total,
+                                               int S, const int* __restrict__ count, const float4* __restrict__ pos,
+                                               uint4* __restrict__ feat_tiles, float4* __restrict__ out, int* flag,
+                                               int* tile_ctr, int split) {
+  using WT = WeightTiles<INP, W, H, SPL>;
+  constexpr uint32_t XLO = SPL ? 128 * INP * 2 : 0;
+  constexpr uint32_t kXBytes = 128 * INP * 2 * (SPL ? 2 : 1);
+  constexpr uint32_t kCols = 2 * W <= 64 ? 64 : 128;  // accumulator + H hi + H lo
+  constexpr int kHhi = W, kHlo = W + W / 2;
+  constexpr int TPS = NT / 128;  // threads per sample (encode) = column groups (epilogues)
+  static_assert(W % (8 * TPS) == 0, "epilogue column groups of 8");
+  const bool sp = SPL && (split & 1);
+  extern __shared__ __align__(1024) unsigned char smem[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase;
+  __shared__ int s_tile;
+  WT wt;
+  unsigned char* p = smem;
+  wt.carve(p);
+  unsigned char* X = p;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int q = warp & 3, g = warp >> 2, row = 32 * q + lane;
+  pdl_wait();  // params come from the previous step's Adam
+  wt.load(fd, params + fd.hash_params, NT);
+  for (int i = tid; i < (int)kXBytes / 2; i += NT) reinterpret_cast<__nv_bfloat16*>(X)[i] = __float2bfloat16_rn(0.f);
+  if (warp == 0) umma::tmem_alloc(&tbase, kCols);
+  if (tid == 0) {
+    umma::mbar_init(&bar, 1);
+    umma::fence_mbar_init();
+  }
+  umma::fence_before_sync();
+  __syncthreads();
+  umma::fence_after_sync();
+  const uint32_t tm = tbase;
+  const uint32_t lane_base = (uint32_t)(32 * q) << 16;
+  uint32_t phase = 0;
+  constexpr uint32_t id_h = umma::idesc_bf16(128, W, false, false);
+  constexpr uint32_t id_out = umma::idesc_bf16(128, 16, false, false);
+  // bias + ReLU of the accumulator -> bf16 (hi, lo) pairs in TMEM; column group g
+  auto epilogue = [&](const float* bias) {
+    constexpr int NG = W / TPS;
+#pragma unroll
+    for (int c = 0; c < NG; c += 8) {
+      const int col = g * NG + c;
+      float v[8];
+      umma::tmem_ld8(tm + lane_base + col, v);
+      umma::tmem_wait_ld();
+      uint32_t hi[4], lo[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float a0 = fmaxf(v[2 * i] + bias[col + 2 * i], 0.f), a1 = fmaxf(v[2 * i + 1] + bias[col + 2 * i + 1], 0.f);
+        const __nv_bfloat162 h = __floats2bfloat162_rn(a0, a1);
+        hi[i] = *reinterpret_cast<const uint32_t*>(&h);
+        if (SPL) {
+          const __nv_bfloat162 l = __floats2bfloat162_rn(a0 - __low2float(h), a1 - __high2float(h));
+          lo[i] = *reinterpret_cast<const uint32_t*>(&l);
+        }
+      }
+      umma::tmem_st4(tm + lane_base + kHhi + col / 2, hi);
+      if (SPL) umma::tmem_st4(tm + lane_base + kHlo + col / 2, lo);
+    }
+    umma::tmem_wait_st();
+    umma::fence_before_sync();
+    __syncthreads();
+    umma::fence_after_sync();
+  };
+  const long long ntiles = (n_total + kTile - 1) / kTile;
+  for (long long t = next_tile(tile_ctr, &s_tile); t < ntiles; t = next_tile(tile_ctr, &s_tile)) {
+    const long long tile0 = t * kTile;
+    {  // ---- encode (fp32, bit-exact) -> bf16 X tile (hi, lo)
+      const int s = tid & (kTile - 1), part = tid >> 7;
+      const long long gs = tile0 + s;
+      bool valid = gs < n_total && __ldg(count + ray_of(gs, S)) > 0;
+      float4 pp = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (valid) pp = pos[gs];
+      const float px = clamp01(pp.x), py = clamp01(pp.y), pz = clamp01(pp.z);
+      for (int l = part; l < fd.L; l += TPS) {
+        float f[2] = {0.f, 0.f};
+        if (valid) encode_level<2>(fd, params, l, px, py, pz, f);
+        const __nv_bfloat162 hi = __floats2bfloat162_rn(f[0], f[1]);
+        *reinterpret_cast<__nv_bfloat162*>(X + umma::cm_offset(s, 2 * l, INP)) = hi;
+        if (SPL)
+          *reinterpret_cast<__nv_bfloat162*>(X + XLO + umma::cm_offset(s, 2 * l, INP)) =
+              __floats2bfloat162_rn(f[0] - __low2float(hi), f[1] - __high2float(hi));
+      }
+    }
+    sync_for_mma();
+    if (tid == 0) {
+      for (int ks = 0; ks < INP / 16; ++ks)
+        umma::mma_split(tm, umma::desc_kmajor(X, INP, ks), umma::desc_kmajor(wt.w0, INP, ks), id_h, ks > 0, sp, XLO,
+                        WT::kLo);
+      umma::commit(&bar);
+      umma::bulk_s2g(feat_tiles + t * (kXBytes / 16), X, kXBytes);  // stored features for the backward
+    }
+    wait_mma(&bar, phase);
+    epilogue(wt.bias);
+    for (int l = 1; l < H; ++l) {
+      if (tid == 0) {
+        for (int ks = 0; ks < W / 16; ++ks)
+          umma::mma_split_ts(tm, tm + kHhi + ks * 8, umma::desc_kmajor(wt.wl[l - 1], W, ks), id_h, ks > 0, sp,
+                             kHlo - kHhi, WT::kLo);
+        umma::commit(&bar);
+      }
+      wait_mma(&bar, phase);
+      epilogue(wt.bias + l * W);
+    }
+    if (tid == 0) {
+      for (int ks = 0; ks < W / 16; ++ks)
+        umma::mma_split_ts(tm, tm + kHhi + ks * 8, umma::desc_kmajor(wt.wo, W, ks), id_out, ks > 0, sp, kHlo - kHhi,
+                           WT::kLo);
+      umma::commit(&bar);
+    }
+    wait_mma(&bar, phase);
+    if (warp < 4) {
+      float v[8];
+      umma::tmem_ld8(tm + lane_base, v);
+      umma::tmem_wait_ld();
+      const long long gs = tile0 + row;
+      if (gs < n_total) {
+        float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (__ldg(count + ray_of(gs, S)) > 0) {
+          const float* b = wt.bias + H * W;
+          o.x = density_forward(fd.act, v[0] + b[0]);
+          o.y = stable_sigmoid(v[1] + b[1]);
+          o.z = stable_sigmoid(v[2] + b[2]);
+          o.w = stable_sigmoid(v[3] + b[3]);
+          if (!all_finite4(o.x, o.y, o.z, o.w)) atomicOr(flag, 1);
+        }
+        out[gs] = o;
+      }
+    }
+    if (tid == 0) umma::bulk_wait_read();  // X is rewritten by the next tile's encode
+    umma::fence_before_sync();
+  }
+  if (tid == 0) umma::bulk_wait_all();
+  tile_sched_exit(tile_ctr);
+  __syncthreads();
+  if (warp == 0) umma::tmem_dealloc(tm, kCols);
+}
+
 // One level of the table-gradient scatter for the 32 consecutive samples of a
 // warp (field.cpp:279-292). Samples of a ray are depth-sorted and a line
 // enters each cell once, so equal cells form contiguous lane runs; each run's
@@ -422,10 +577,15 @@ __device__ __forceinline__ void scatter_level(const FieldDesc& fd, float* __rest
 // so every accumulator is an M=128 tile: the output layer needs 16 columns.
 template <int INP, int W, int H>
 struct BwdCols {
-  static constexpr int kDWo = 0;                 // [128 x 16]  (h | 1) x o
-  static constexpr int kDWl = 16;                // layers H-1..1: [128 x W] each
-  static constexpr int kDW0 = kDWl + (H - 1) * W;  // [128 x W]  (in | 1) x out
-  static constexpr int kR = kDW0 + W;            // working region, 64 columns
+  // Output layer: dW_out^T = [H_{H-1} | 1]^T G, M = 128 (input units + the ones
+  // row = bias), 16 columns. Hidden and input layers: dW_l = D_l^T [H_{l-1} | 1],
+  // M = 64 (output units: rows 16q..16q+15 in lanes 32q..32q+15), N = the
+  // previous tile's width incl. its ones column -- half the tensor work of the
+  // M = 128 transposed form, whose M rows beyond in+1 were padding.
+  static constexpr int kDWo = 0;                       // [128 x 16]
+  static constexpr int kDWl = 16;                      // layers H-1..1: [64 x (W+8)] each
+  static constexpr int kDW0 = kDWl + (H - 1) * (W + 8);  // [64 x (INP+8)]
+  static constexpr int kR = (kDW0 + INP + 8 + 15) / 16 * 16;  // working region, 64 columns
   static constexpr int kDF = kR + 64;            // d_features of the tile being handed over
   static constexpr int kTotal = kDF + INP;
   static_assert(kTotal <= 256, "TMEM budget");
@@ -449,6 +609,9 @@ constexpr int kBwdMlpLevels = 1;   // per half, scattered by the MLP warps (meas
 constexpr int kBwdPullMax = 4;     // scatter_level: pull-reduce runs up to this length (cfg2 sweeps:
                                    // 2-4 equal, 6 / 8 / 12 slower by 0.3 / 1 / 3.5%: pulls cost ALU, the tree shuffles)
 constexpr int kBwdThreads = kMlpThreads + kScatThreads;
+// MMA / slot waits (PRENOM_BWD_WAIT bits): 1 scatter warps sleep on the slot
+// barrier, 2 one MLP warp polls each MMA barrier
+constexpr int kBwdWaitDefault = 0;
 
 __device__ __forceinline__ void named_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
@@ -485,7 +648,7 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
     k_bwd_tc(FieldDesc fd, const float* __restrict__ params, float* __restrict__ grad, long long n_total, int S,
              const int* __restrict__ count, const float4* __restrict__ pos, const uint4* __restrict__ feat_tiles,
              const float4* __restrict__ dout, int* tile_ctr, int skip_scatter, int mlp_levels,
-             int pull_max, int split) {
+             int pull_max, int split, int wait_mode) {
   using CM = BwdCols<INP, W, H>;
   using WT = WeightTiles<INP, W, H, SPL>;
   constexpr int XC = INP + 8, HC = W + 8;
@@ -573,7 +736,10 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
     const int r = (tid - kMlpThreads) & 127;  // sample row in the tile; warp = 32 consecutive samples
     const int lhalf = (tid - kMlpThreads) >> 7;  // levels [lhalf*L/2, ...)
     for (uint32_t k = 0;; ++k) {
-      umma::mbar_wait(&full_bar, k & 1u);
+      if (wait_mode & 1)
+        umma::mbar_wait_sleep(&full_bar, k & 1u, 20000u);  // (sleeping waiters leave issue slots to the chain)
+      else
+        umma::mbar_wait(&full_bar, k & 1u);
       const long long t = slot_tile;
       if (t < 0) break;
       umma::fence_after_sync();
@@ -610,6 +776,18 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
     uint32_t phase = 0, xphase = 0;
     int iter = 0;
     const int q = warp & 3, half = warp >> 2, row = 32 * q + lane;
+    // MMA completion: every MLP warp polls the mbarrier, or (wait_mode bit 1)
+    // warp 0 polls and the others sleep on the named barrier
+    auto wait_chain = [&](uint32_t& ph) {
+      if (wait_mode & 2) {
+        if (warp == 0) umma::mbar_wait(&bar, ph);
+        named_sync(1, kMlpThreads);
+        ph ^= 1u;
+        umma::fence_after_sync();
+      } else {
+        wait_mma(&bar, ph);
+      }
+    };
     // (overlay) the ones column of [X | 1] and [H_{H-1} | 1], rewritten per tile:
     // one 16-byte core-matrix row [1, 0, ..., 0] (hi) and zeros (lo) per sample
     const uint4 ones_row = make_uint4(0x3F80u, 0u, 0u, 0u), zero_row = make_uint4(0u, 0u, 0u, 0u);
@@ -651,7 +829,7 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
                           umma::idesc_bf16(128, W, false, false), ks > 0, sp_f, XLO, WT::kLo);
         umma::commit(&bar);
       }
-      wait_mma(&bar, phase);
+      wait_chain(phase);
       if (OV) set_ones(Ht[H - 1], W, HC, HLO);  // X is dead until dW0
       uint64_t gate[2];
       gate[0] = epi_relu_gate<W, kMG, HLO>(tr, wt.bias, Ht[0], HC);
@@ -664,7 +842,7 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
                             umma::idesc_bf16(128, W, false, false), ks > 0, sp_f, HLO, WT::kLo);
           umma::commit(&bar);
         }
-        wait_mma(&bar, phase);
+        wait_chain(phase);
         gate[l] = epi_relu_gate<W, kMG, HLO>(tr, wt.bias + l * W, Ht[l], HC);
       }
       mlp_sync_for_mma();
@@ -674,7 +852,7 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
                           umma::idesc_bf16(128, 16, false, false), ks > 0, sp_f, HLO, WT::kLo);
         umma::commit(&bar);
       }
-      wait_mma(&bar, phase);
+      wait_chain(phase);
       // ---- g_raw (field.cpp:233-238) -> G tile
       if (warp < 4) {
         float v[8];
@@ -705,7 +883,7 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
                         umma::idesc_bf16(128, W, false, true), 0u, sp_d, GLO, WT::kLo);
         umma::commit(&bar);
       }
-      wait_mma(&bar, phase);
+      wait_chain(phase);
 #pragma unroll
       for (int l = H - 1; l >= 0; --l) {
         if (OV && l == 0) {  // D_{H-1} is dead: X back into its place for dW0
@@ -732,13 +910,14 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
         }
         mlp_sync_for_mma();
         if (tid == 0) {
-          const int dwc = l == 0 ? CM::kDW0 : CM::kDWl + (H - 1 - l) * W;
+          const int dwc = l == 0 ? CM::kDW0 : CM::kDWl + (H - 1 - l) * (W + 8);
           const unsigned char* prev = l == 0 ? X : Ht[l - 1];
           const int pc = l == 0 ? XC : HC;
           const uint32_t plo = l == 0 ? XLO : HLO;
+          // dW_l = D_l^T [prev | 1]: A = D_l (MN-major, M = 64 units), B = prev (MN-major, N = pc)
           for (int ks = 0; ks < 8; ++ks)
-            umma::mma_split(tm + dwc, umma::desc_mnmajor(prev, pc, ks), umma::desc_mnmajor(Ht[l], HC, ks),
-                            umma::idesc_bf16(128, W, true, true), (iter > 0 || ks > 0), sp_w, plo, HLO);
+            umma::mma_split(tm + dwc, umma::desc_mnmajor(Ht[l], HC, ks), umma::desc_mnmajor(prev, pc, ks),
+                            umma::idesc_bf16(64, pc, true, true), (iter > 0 || ks > 0), sp_w, HLO, plo);
           if (l > 0) {
             for (int ks = 0; ks < W / 16; ++ks)
               umma::mma_split(tr, umma::desc_kmajor(Ht[l], HC, ks), umma::desc_mnmajor(wt.wl[l - 1], W, ks),
@@ -757,7 +936,7 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
             mbar_arrive(&full_bar);
           }
         }
-        wait_mma(&bar, phase);
+        wait_chain(phase);
       }
       } else if (tid == 0) {  // (knob 3: no chain; hand over the stale slot)
         umma::mbar_wait(&empty_bar, ((uint32_t)iter & 1u) ^ 1u);
@@ -818,9 +997,26 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
           }
         }
       };
+      // M = 64 accumulators: output unit o = 16 * warp + lane (lanes < 16), column
+      // = input unit (or the ones column = bias)
+      auto flush64 = [&](int col0, int ncol, int in, int ones_col, int w_off, int b_off) {
+        const int o = 16 * warp + lane;
+        for (int c = 0; c < ncol; c += 8) {
+          float v[8];
+          umma::tmem_ld8(umma::taddr(tm, 32 * warp, col0 + c), v);
+          umma::tmem_wait_ld();
+          if (lane >= 16 || o >= W) continue;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int k = c + j;
+            if (k < in) atomicAdd(gm + w_off + o * in + k, v[j]);
+            else if (k == ones_col) atomicAdd(gm + b_off + o, v[j]);
+          }
+        }
+      };
       flush(CM::kDWo, 16, 4, W, W, fd.w_off[H], fd.b_off[H]);
-      for (int l = H - 1; l >= 1; --l) flush(CM::kDWl + (H - 1 - l) * W, W, W, W, W, fd.w_off[l], fd.b_off[l]);
-      flush(CM::kDW0, W, W, fd.in_dim, INP, fd.w_off[0], fd.b_off[0]);
+      for (int l = H - 1; l >= 1; --l) flush64(CM::kDWl + (H - 1 - l) * (W + 8), W + 8, W, W, fd.w_off[l], fd.b_off[l]);
+      flush64(CM::kDW0, INP + 8, fd.in_dim, INP, fd.w_off[0], fd.b_off[0]);
     }
   }
   umma::fence_before_sync();
@@ -867,12 +1063,17 @@ size_t bwd_smem() {
          1024;
 }
 
+template <int INP, int W, int H, int SPL>
+size_t fwd_ts_smem() {
+  return WeightTiles<INP, W, H, SPL>::kBytes + ((H * W + 4) * 4 + 15) / 16 * 16 + 128 * INP * 2 * (SPL ? 2 : 1) + 1024;
+}
+
 template <int INP, int W, int H, int NT, int SPL>
 cudaError_t run_fwd_nt(const FieldDesc& fd, const float* params, long long n, int S, const int* count,
                        const float4* pos, void* feat_tiles, float4* out, int* flag, int* tile_ctr, int ctas,
-                       size_t min_smem, int carveout, int split, cudaStream_t st) {
-  auto kern = k_fwd_tc<INP, W, H, NT, SPL>;
-  const size_t smem = std::max<size_t>(fwd_smem<INP, W, H, SPL>(), min_smem);
+                       size_t min_smem, int carveout, int split, bool ts, cudaStream_t st) {
+  auto kern = ts ? k_fwd_ts<INP, W, H, NT, SPL> : k_fwd_tc<INP, W, H, NT, SPL>;
+  const size_t smem = std::max<size_t>(ts ? fwd_ts_smem<INP, W, H, SPL>() : fwd_smem<INP, W, H, SPL>(), min_smem);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   // shared-memory carve-out (percent of the maximum): the rest of the 256 KB
@@ -901,28 +1102,30 @@ cudaError_t run_fwd(const FieldDesc& fd, const float* params, long long n, int S
                     void* feat_tiles, float4* out, int* flag, int* tile_ctr, int split, cudaStream_t st) {
   // CTAs per SM x threads per CTA trade gather latency hiding against L1
   // capacity (L1 = 256 KB - the shared-memory carve-out);
-  // PRENOM_FWD_{CTAS,SMEM_KB,THREADS,CARVEOUT} override the measured defaults
-  // (split mode: PRENOM_FWDS_*).
+  // PRENOM_FWD{,S}_{CTAS,SMEM_KB,THREADS,CARVEOUT,TS} override the measured
+  // defaults of the bf16 / split (S) forward; TS = activations in TMEM (k_fwd_ts)
   if (split) {
-    static const int nt = env_int("PRENOM_FWDS_THREADS", kFwdSThreadsDefault) == 512 ? 512 : 256;
-    static const int ctas = std::max(1, std::min(8, env_int("PRENOM_FWDS_CTAS", kFwdSCtasDefault)));
+    static const bool ts = env_int("PRENOM_FWDS_TS", kFwdSTsDefault) != 0;
+    static const int nt = env_int("PRENOM_FWDS_THREADS", ts ? kFwdSTsThreads : kFwdSThreadsDefault) == 512 ? 512 : 256;
+    static const int ctas = std::max(1, std::min(8, env_int("PRENOM_FWDS_CTAS", ts ? kFwdSTsCtas : kFwdSCtasDefault)));
     static const size_t min_smem = (size_t)env_int("PRENOM_FWDS_SMEM_KB", 0) * 1024;
-    static const int carve = env_int("PRENOM_FWDS_CARVEOUT", kFwdSCarveoutDefault);
+    static const int carve = env_int("PRENOM_FWDS_CARVEOUT", ts ? kFwdSTsCarveout : kFwdSCarveoutDefault);
     if (nt == 512)
       return run_fwd_nt<INP, W, H, 512, 1>(fd, params, n, S, count, pos, feat_tiles, out, flag, tile_ctr, ctas,
-                                           min_smem, carve, split, st);
+                                           min_smem, carve, split, ts, st);
     return run_fwd_nt<INP, W, H, 256, 1>(fd, params, n, S, count, pos, feat_tiles, out, flag, tile_ctr, ctas, min_smem,
-                                         carve, split, st);
+                                         carve, split, ts, st);
   }
+  static const bool ts = env_int("PRENOM_FWD_TS", 0) != 0;
   static const int nt = env_int("PRENOM_FWD_THREADS", kFwdThreadsDefault) == 512 ? 512 : 256;
   static const int ctas = std::max(1, std::min(8, env_int("PRENOM_FWD_CTAS", kFwdCtasDefault)));
-  static const size_t min_smem = (size_t)env_int("PRENOM_FWD_SMEM_KB", kFwdSmemKbDefault) * 1024;
+  static const size_t min_smem = (size_t)env_int("PRENOM_FWD_SMEM_KB", ts ? 0 : kFwdSmemKbDefault) * 1024;
   static const int carve = env_int("PRENOM_FWD_CARVEOUT", kFwdCarveoutDefault);
   if (nt == 512)
     return run_fwd_nt<INP, W, H, 512, 0>(fd, params, n, S, count, pos, feat_tiles, out, flag, tile_ctr, ctas, min_smem,
-                                         carve, 0, st);
+                                         carve, 0, ts, st);
   return run_fwd_nt<INP, W, H, 256, 0>(fd, params, n, S, count, pos, feat_tiles, out, flag, tile_ctr, ctas, min_smem,
-                                       carve, 0, st);
+                                       carve, 0, ts, st);
 }
 
 template <int INP, int W, int H, int SPL>
@@ -953,10 +1156,12 @@ cudaError_t run_bwd_s(const FieldDesc& fd, const float* params, float* grad, lon
   static const int skip = env_int("PRENOM_PROF_SKIP_SCATTER", 0);
   // longest run reduced by pulls (else by the shuffle tree); PRENOM_BWD_PULL_MAX overrides
   static const int pull_max = env_int("PRENOM_BWD_PULL_MAX", kBwdPullMax);
+  static const int wait_mode = env_int("PRENOM_BWD_WAIT", kBwdWaitDefault);
   cudaError_t em = cudaMemsetAsync(tile_ctr, 0, sizeof(int), st);
   if (em != cudaSuccess) return em;
   return launch_pdl(kern, dim3((unsigned)grid), dim3(kBwdThreads), smem, st, fd, params, grad, n, S, count, pos,
-                    reinterpret_cast<const uint4*>(feat_tiles), dout, tile_ctr, skip, mlp_levels, pull_max, split);
+                    reinterpret_cast<const uint4*>(feat_tiles), dout, tile_ctr, skip, mlp_levels, pull_max, split,
+                    wait_mode);
 }
 
 template <int INP, int W, int H>

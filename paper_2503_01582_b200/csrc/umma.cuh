@@ -71,6 +71,19 @@ __device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b
       "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
 }
 
+// D[tmem] (+)= A[tmem] * B[smem]^T: the A operand (M x K, K-major, 16-bit
+// elements packed two per 32-bit column, lower k in the low half; row = lane)
+// is read from tensor memory ("TS" form) -- activations produced by an
+// epilogue never pass through shared memory.
+__device__ __forceinline__ void mma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
 // Arrive on an mbarrier when all prior tcgen05.mma of this thread complete.
 __device__ __forceinline__ void commit(uint64_t* mbar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(mbar))
@@ -161,6 +174,15 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
 
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
+// 32 lanes x 32-bit, 4 consecutive columns per thread (the inverse of tmem_ld).
+__device__ __forceinline__ void tmem_st4(uint32_t taddr, const uint32_t* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr), "r"(v[0]), "r"(v[1]),
+               "r"(v[2]), "r"(v[3])
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
 // TMEM address of (lane, column) relative to an allocation base.
 __device__ __forceinline__ uint32_t taddr(uint32_t base, int lane, int col) {
   return base + ((uint32_t)lane << 16) + (uint32_t)col;
@@ -234,6 +256,16 @@ __device__ __forceinline__ void mma_split(uint32_t tmem_d, uint64_t a, uint64_t 
   if (split) {
     mma_bf16(tmem_d, a, desc_add(b, b_lo), idesc, 1u);
     mma_bf16(tmem_d, desc_add(a, a_lo), b, idesc, 1u);
+  }
+}
+
+// mma_split with the A operand in tensor memory: hi at tmem_a, lo at tmem_a + a_lo_cols.
+__device__ __forceinline__ void mma_split_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc,
+                                             uint32_t accumulate, bool split, uint32_t a_lo_cols, uint32_t b_lo) {
+  mma_bf16_ts(tmem_d, tmem_a, b, idesc, accumulate);
+  if (split) {
+    mma_bf16_ts(tmem_d, tmem_a, desc_add(b, b_lo), idesc, 1u);
+    mma_bf16_ts(tmem_d, tmem_a + a_lo_cols, b, idesc, 1u);
   }
 }
 
