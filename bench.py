@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--rays", type=int, default=8192)
     ap.add_argument("--samples", type=int, default=96)
     ap.add_argument("--e2e-steps", type=int, default=100)
+    ap.add_argument("--steady-steps", type=int, default=100,
+                    help="single-object workloads: also time this many steps from object step 50 on")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0, help="budget of the cpu_baseline sample")
     ap.add_argument("--log-jsonl", default=None, help="per-step JSONL of the timed steps (loss terms, samples)")
@@ -296,6 +298,7 @@ class Cfg3(Workload):
     objects LPT-sharded over the ranks (no collective)."""
 
     name = "cfg3"
+    scaling = "strong"  # 32 objects in total, sharded over the ranks
 
     def __init__(self, args, ctx, rank, ws):
         from paper_2503_01582_b200 import FieldArch, ObjectTrainer, TrainConfig, scenes
@@ -564,8 +567,42 @@ def run_ours(args):
             for i, st in enumerate(wl.step_stats):
                 f.write(json.dumps(dict(step=i, ms_avg=round(per_step_ms, 4),
                                         samples_per_s_avg=round(n_samples / (ms / 1e3), 1), **st)) + "\n")
+    # steady state (the K-step window starts right after warm-up, when
+    # samples are still spread out): time steps [max(50, current), +steady_steps)
+    steady = None
+    if args.steady_steps > 0 and getattr(wl, "obj", None) is not None and len(wl.objs) == 1:
+        cur = wl.obj.step()
+        if cur < 50:
+            wl.step(50 - cur)
+            ctx.synchronize()
+            wl.samples(50 - cur)
+        s0 = wl.obj.step()
+        a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if dist_on:
+            torch.distributed.barrier()
+        ctx.synchronize()
+        a_ev.record(stream)
+        wl.step(args.steady_steps)
+        b_ev.record(stream)
+        ctx.synchronize()
+        st_ms = a_ev.elapsed_time(b_ev)
+        st_n = wl.samples(args.steady_steps)
+        if dist_on:
+            import torch.distributed as dist
+
+            tt = torch.tensor([st_ms], device="cuda", dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            nn = torch.tensor([float(st_n)], device="cuda", dtype=torch.float64)
+            dist.all_reduce(nn, op=dist.ReduceOp.SUM)
+            st_ms, st_n = tt.item(), nn.item()
+        steady = {"value": round(st_n / (st_ms / 1e3), 1), "unit": UNIT, "object_steps": [s0, s0 + args.steady_steps],
+                  "ms_per_step": round(st_ms / args.steady_steps, 4),
+                  "note": "object steps 50+ (samples concentrated by the prior refreshes; grid refresh every 50 "
+                          "inside the window)"}
+
     # the same K steps again with per-kernel CUDA events (on the launching
-    # streams) for the per-kernel breakdown and the roofline
+    # streams; the sampler is serialised in this pass so its time is its own)
+    # for the per-kernel breakdown and the roofline
     lib.prenom_ctx_profile(ctx.h, 1)
     p_start, p_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     p_start.record(stream)
@@ -702,7 +739,7 @@ def run_ours(args):
     tail = wl.tail(ctx) if hasattr(wl, "tail") else None
 
     cpu = None
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline and args.workload == "cfg2":
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         try:
             cpu = cpu_baseline(args, budget_s=args.cpu_seconds)
         except Exception as e:  # reported, never fatal
@@ -712,7 +749,8 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(t_dev * 1e3 / args.steps, 4), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32" if args.mlp == "fp32" else "f32+bf16-mlp",
+            "scaling": getattr(wl, "scaling", "weak"), "vs_baseline": None,
+            "dtype": {"fp32": "f32", "bf16": "f32+bf16-mlp", "bf16x3": "f32+split-bf16-mlp (bf16x3)"}[args.mlp],
             "data": "synthetic (seeded box-union RGB-D scenes, BASELINE shapes)",
             "config": dict({"workload": wl.desc, "mlp_precision": args.mlp, "parallelism": f"objects x{ws}"},
                            **wl.extra),
@@ -727,6 +765,7 @@ def run_ours(args):
             "kernels": kernels,
             "kernels_pass_ms_per_step": round(prof_ms / args.steps, 4),  # 2nd pass, with per-kernel events
             "cpu_baseline": cpu,
+            "steady_state": steady,
             "clocks": clk.summary(),
             "loss": getattr(wl, "loss", None),
         }
@@ -748,6 +787,48 @@ def host_cores():
         return os.cpu_count() or 1
 
 
+REF_THREADS = {"cfg1": 1, "cfg4": 4}  # cfg1: one object, no intra-object parallelism; cfg4: meta_train is
+                                       # sequential over tasks, the 4 categories run in parallel
+
+
+def ref_threads(args):
+    cores = host_cores()
+    return max(1, min(cores, 32, REF_THREADS.get(args.workload, cores)))
+
+
+def _ref_items(args, n):
+    """Per host thread, the reference-side object of the workload: (arch, scene, grid, R, cfg).
+    Views per object are cut to a few (each step trains on one keyframe, so the per-step cost
+    does not depend on the view count); everything else is the workload's shape."""
+    from paper_2503_01582_b200 import TrainConfig, scenes
+
+    wl = args.workload
+    out = []
+    for i in range(n):
+        if wl == "cfg1":
+            sc = scenes.sphere_scene(n_views=4)
+            out.append((scenes.cfg1_arch(), sc, np.zeros((8, 8, 8), np.float32), 8,
+                        TrainConfig(rays_per_iter=4096, samples_per_ray=64, prior_sampling=0, grid_refresh_every=0)))
+        elif wl == "cfg2":
+            sc, grid, arch, cfg = make_workload(args, 0)
+            out.append((arch, sc, grid, 32, cfg))
+        elif wl in ("cfg3", "cfg5"):
+            cats = mixed_category_archs()
+            R = 64 if wl == "cfg3" else 128
+            res, rays = (256, 2048) if wl == "cfg3" else (512, 1366)
+            sc = scenes.box_union_scene(n_views=4, res=res, seed=5000 + i,
+                                        depth_noise=0.0 if wl == "cfg3" else 0.01,
+                                        missing_frac=0.0 if wl == "cfg3" else 0.05)
+            out.append((cats[i % 4], sc, scenes.occupancy_prior(sc.boxes, R=R), R,
+                        TrainConfig(rays_per_iter=rays, samples_per_ray=96, coarse_samples=32, prior_sampling=1,
+                                    grid_refresh_every=50)))
+        else:  # cfg4: inner_adapt's iteration = train_track's with midpoint samples and a fresh Adam
+            sc = scenes.box_union_scene(n_views=4, res=128, seed=7000 + i)
+            out.append((scenes.cfg4_arch(), sc, np.zeros((8, 8, 8), np.float32), 8,
+                        TrainConfig(rays_per_iter=4096, samples_per_ray=64, prior_sampling=0, grid_refresh_every=0)))
+    return out
+
+
 def _ref_trainers(args, n, rays, seed0=0):
     from oracle import pyoracle
     from paper_2503_01582_b200 import TrainConfig
@@ -755,15 +836,22 @@ def _ref_trainers(args, n, rays, seed0=0):
     if not pyoracle.REF_SO.exists():
         pyoracle.build_oracle(ref=True)
     ref = pyoracle.Ref()
-    sc, grid, arch, cfg = make_workload(args, 0)
-    rcfg = TrainConfig(rays_per_iter=rays, samples_per_ray=cfg.samples_per_ray, coarse_samples=cfg.coarse_samples,
-                       prior_sampling=1, grid_refresh_every=cfg.grid_refresh_every, eta=cfg.eta)
     out = []
-    for i in range(n):
+    for i, (arch, sc, grid, R, cfg) in enumerate(_ref_items(args, n)):
+        rcfg = TrainConfig(rays_per_iter=rays, samples_per_ray=cfg.samples_per_ray, coarse_samples=cfg.coarse_samples,
+                           prior_sampling=cfg.prior_sampling, grid_refresh_every=cfg.grid_refresh_every, eta=cfg.eta)
         theta = ref.init_params(arch, seed0 + i)  # noma::init_params (field.cpp:150-166)
-        out.append(ref.trainer(arch, theta, grid, 32, sc.cams, sc.rgb, sc.depth, sc.mask, 1, sc.obj_pose, sc.box_min,
+        out.append(ref.trainer(arch, theta, grid, R, sc.cams, sc.rgb, sc.depth, sc.mask, 1, sc.obj_pose, sc.box_min,
                                sc.box_max, rcfg, 1234 + i))
-    return out, arch
+    return out
+
+
+def _full_rays(args):
+    return {"cfg1": 4096, "cfg2": args.rays, "cfg3": 2048, "cfg4": 4096, "cfg5": 1366}[args.workload]
+
+
+def _samples_per_ray(args):
+    return {"cfg1": 64, "cfg2": args.samples, "cfg3": 96, "cfg4": 64, "cfg5": 96}[args.workload]
 
 
 def _parallel_steps(trainers, iters):
@@ -785,50 +873,55 @@ def _parallel_steps(trainers, iters):
     return sum(res), time.perf_counter() - t0
 
 
-def _calibrate(args, threads):
-    """Seconds per reference iteration at `rays` rays, per thread (1 probe)."""
-    tr, arch = _ref_trainers(args, 1, 256, seed0=99)
+def _calibrate(args):
+    """Seconds per reference iteration per ray (and fixed cost), one probe object."""
+    tr = _ref_trainers(args, 1, 256, seed0=99)
     t0 = time.perf_counter()
     tr[0].step(1)
     t_256 = time.perf_counter() - t0
-    tr2, _ = _ref_trainers(args, 1, 64, seed0=98)
+    tr2 = _ref_trainers(args, 1, 64, seed0=98)
     t0 = time.perf_counter()
     tr2[0].step(1)
     t_64 = time.perf_counter() - t0
+    for t in tr + tr2:
+        t.close()
     per_ray = max((t_256 - t_64) / 192.0, 1e-5)
     fixed = max(t_64 - 64 * per_ray, 0.0)
     return per_ray, fixed
 
 
 def cpu_baseline(args, budget_s=20.0):
-    """The reference train_track (mt19937) on the host cores: one object per
-    thread (mapper.cpp:572 parallel_for), bounded per-step ray count."""
+    """The reference's own CPU implementation of the workload's step (oracle/_ref: the unmodified
+    reference sources, mt19937 draws) on the host cores: one object per thread as
+    parallel_for does (mapper.cpp:572-585), cfg1 on one thread, cfg4 one task's inner_adapt
+    iteration per category thread; a bounded ray sample per iteration."""
     cores = host_cores()
-    threads = max(1, min(cores, 32))
-    per_ray, fixed = _calibrate(args, threads)
-    iters = 2
-    rays = int(max(64, min(args.rays // 4, (budget_s / iters - fixed) / per_ray)))
-    trainers, _ = _ref_trainers(args, threads, rays)
+    threads = ref_threads(args)
+    per_ray, fixed = _calibrate(args)
+    iters = 4
+    full = _full_rays(args)
+    rays = int(max(64, min(full, (budget_s / iters - fixed) / per_ray)))
+    trainers = _ref_trainers(args, threads, rays)
     n, dt = _parallel_steps(trainers, iters)
     for t in trainers:
         t.close()
     return {"value": round(n / dt, 1), "unit": UNIT, "cores": threads, "kind": "reference",
-            "sample": f"{threads} threads x {iters} reference train_track iterations (mt19937) of cfg2, "
-                      f"{rays} rays x {args.samples} samples per iteration (of {args.rays}), each thread its own "
-                      f"object; {n} samples in {dt:.2f} s on {cores} host cores"}
+            "sample": f"sampled: {threads} thread(s) x {iters} reference train_track iterations (mt19937) of "
+                      f"{args.workload}, {rays} of {full} rays x {_samples_per_ray(args)} samples per iteration, each "
+                      f"thread its own object; {n} samples in {dt:.2f} s on {cores} host cores"}
 
 
 def run_reference(args):
     ws, rank, local = dist_info()
     if rank != 0:
         return  # reference arm runs on rank 0 only
-    cores = host_cores()
-    threads = max(1, min(cores, 32))
-    per_ray, fixed = _calibrate(args, threads)
+    threads = ref_threads(args)
+    per_ray, fixed = _calibrate(args)
     # size each step so warmup+steps end within ~3 minutes
     budget = 180.0 / max(1, args.steps + args.warmup)
-    rays = int(max(16, min(args.rays, (budget - fixed) / per_ray)))
-    trainers, _ = _ref_trainers(args, threads, rays)
+    full = _full_rays(args)
+    rays = int(max(16, min(full, (budget - fixed) / per_ray)))
+    trainers = _ref_trainers(args, threads, rays)
     _parallel_steps(trainers, args.warmup)
     n, dt = _parallel_steps(trainers, args.steps)
     for t in trainers:
@@ -838,12 +931,13 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3 / args.steps, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic (seeded box-union RGB-D scenes, BASELINE cfg2 shapes)",
-        "config": {"workload": "cfg2 (see ours); reference CPU train_track, one object per host thread",
-                   "rays_per_step_per_thread": rays, "mlp_samples_per_ray": args.samples},
+        "data": f"synthetic (seeded RGB-D scenes, BASELINE {args.workload} shapes)",
+        "config": {"workload": f"{args.workload} (see ours); reference CPU train_track, one object per host thread",
+                   "rays_per_step_per_thread": rays, "mlp_samples_per_ray": _samples_per_ray(args)},
         "cpu_baseline": {"value": round(value, 1), "unit": UNIT, "cores": threads, "kind": "reference",
-                         "sample": f"{threads} threads x 1 iteration per step, {rays} rays x {args.samples} samples "
-                                   f"per iteration (of {args.rays}), oracle/_ref (unmodified reference sources)"},
+                         "sample": f"sampled: {threads} thread(s) x 1 iteration per step, {rays} of {full} rays x "
+                                   f"{_samples_per_ray(args)} samples per iteration, oracle/_ref (unmodified "
+                                   "reference sources)"},
         "e2e": {"value": round(value, 1), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)

@@ -373,6 +373,10 @@ prenom_status prenom_debug_field_backward(prenom_ctx_t ctx, const prenom_field_a
                                           const float* params, int n, const float* xyz,
                                           const float* d_sigma, const float* d_rgb, float* grad,
                                           int mlp_precision);
+/* Phase trace of the tensor-core backward (set PRENOM_BWD_WAIT bit 8 before the
+ * first backward launch): clock64 stamps of CTA 0's first 64 tiles, MLP issuing
+ * thread mlp[64][16] (slots 0..10) and first scatter thread scatter[64][4]. */
+prenom_status prenom_debug_bwd_trace(prenom_ctx_t ctx, int64_t* mlp, int64_t* scatter);
 /* adam_step (field.cpp:295-310) on n floats; *step in/out. */
 prenom_status prenom_debug_adam(prenom_ctx_t ctx, size_t n, float* params, const float* grads,
                                 float* m, float* v, int64_t* step, float lr, float beta1,

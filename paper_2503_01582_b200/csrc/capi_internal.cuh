@@ -508,7 +508,8 @@ inline prenom_status enqueue_step(prenom_object_s* o, StepStatsDev* stats, bool 
     }
   }
   const bool refresh_now = c.grid_refresh_every > 0 && (o->step + 1) % c.grid_refresh_every == 0;
-  if (has_next && !refresh_now && o->ctx->overlap) {
+  // (per-kernel timing serialises the sampler: its events then time the kernel alone)
+  if (has_next && !refresh_now && o->ctx->overlap && !o->ctx->prof) {
     if (!o->ev_bwd) {
       CUDA_TRY(cudaEventCreateWithFlags(&o->ev_bwd, cudaEventDisableTiming));
       CUDA_TRY(cudaEventCreateWithFlags(&o->ev_sample, cudaEventDisableTiming));

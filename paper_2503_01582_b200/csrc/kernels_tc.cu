@@ -632,6 +632,22 @@ __device__ __forceinline__ void mbar_arrive2(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], 2;" ::"r"(umma::smem_u32(bar)) : "memory");
 }
 
+// Phase trace of k_bwd_tc (PRENOM_BWD_WAIT bit 3): clock64 stamps of CTA 0's
+// first 64 tiles, MLP thread 0 (slots 0..10: tile start, X in, L0, L1, out,
+// G ready, dWo/dH1, dW1/dH0, dW0/dX, X re-fetched, slot free) and the first
+// scatter thread (0 slot full, 1 slot released, 2 scatter done); read by
+// prenom_debug_bwd_trace.
+__device__ long long g_bwd_trace[64][16];
+__device__ long long g_bwd_strace[64][4];
+#define TRACE_MLP(slot)                                                                   \
+  do {                                                                                    \
+    if ((wait_mode & 8) && blockIdx.x == 0 && tid == 0 && iter < 64) g_bwd_trace[iter][slot] = clock64(); \
+  } while (0)
+#define TRACE_SCAT(slot)                                                                            \
+  do {                                                                                              \
+    if ((wait_mode & 8) && blockIdx.x == 0 && tid == kMlpThreads && k < 64) g_bwd_strace[k][slot] = clock64(); \
+  } while (0)
+
 template <int INP, int W, int H, int SPL>
 struct BwdLayout {
   static constexpr bool kOverlay = SPL && H >= 2;
@@ -742,6 +758,7 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
         umma::mbar_wait(&full_bar, k & 1u);
       const long long t = slot_tile;
       if (t < 0) break;
+      TRACE_SCAT(0);
       umma::fence_after_sync();
       // this half's d_features: TMEM -> registers, then the slot is released
       float d[NH];
@@ -751,6 +768,7 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
       umma::fence_before_sync();
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty_bar);
+      TRACE_SCAT(1);
       const long long gs = t * kTile + r;
       const bool valid = gs < n_total && __ldg(count + ray_of(gs, S)) > 0;
       float4 pp = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -769,6 +787,7 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
 #pragma unroll
         for (int i = 0; i + 2 < NH; ++i) d[i] = d[i + 2];
       }
+      TRACE_SCAT(2);
     }
   } else {
     // ================= MLP warps: tensor-core backward chain
@@ -812,6 +831,7 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
     };
     for (long long t = fetch(); t < ntiles; t = fetch(), ++iter) {
       const long long tile0 = t * kTile;
+      TRACE_MLP(0);
       const long long gs = tile0 + row;
       const bool valid = gs < n_total && __ldg(count + ray_of(gs, S)) > 0;
       // ---- stored bf16 features -> X by the TMA engine (no LSU work): one
@@ -820,6 +840,7 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
       if (OV) set_ones(X, INP, XC, XLO);
       umma::mbar_wait(&xbar, xphase);
       xphase ^= 1u;
+      TRACE_MLP(1);
       mlp_sync_for_mma();
       if (skip_scatter != 3) {  // (profiling knob 3: scatter-only timing -- the MLP chain is skipped)
       // ---- forward recompute (field.cpp:181-211), one TMEM region reused per layer
@@ -830,6 +851,7 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
         umma::commit(&bar);
       }
       wait_chain(phase);
+      TRACE_MLP(2);
       if (OV) set_ones(Ht[H - 1], W, HC, HLO);  // X is dead until dW0
       uint64_t gate[2];
       gate[0] = epi_relu_gate<W, kMG, HLO>(tr, wt.bias, Ht[0], HC);
@@ -843,6 +865,7 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
           umma::commit(&bar);
         }
         wait_chain(phase);
+        TRACE_MLP(2 + l);
         gate[l] = epi_relu_gate<W, kMG, HLO>(tr, wt.bias + l * W, Ht[l], HC);
       }
       mlp_sync_for_mma();
@@ -853,6 +876,7 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
         umma::commit(&bar);
       }
       wait_chain(phase);
+      TRACE_MLP(4);
       // ---- g_raw (field.cpp:233-238) -> G tile
       if (warp < 4) {
         float v[8];
@@ -874,6 +898,7 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
         umma::st_row8_split(G, row, 0, 16, g, GLO);
       }
       mlp_sync_for_mma();
+      TRACE_MLP(5);
       // ---- output layer: dW_out^T += [H_{H-1}|1]^T G;  dH_{H-1} = G W_out
       if (tid == 0) {
         for (int ks = 0; ks < 8; ++ks)
@@ -884,6 +909,7 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
         umma::commit(&bar);
       }
       wait_chain(phase);
+      TRACE_MLP(6);
 #pragma unroll
       for (int l = H - 1; l >= 0; --l) {
         if (OV && l == 0) {  // D_{H-1} is dead: X back into its place for dW0
@@ -907,6 +933,7 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
         if (OV && l == 0) {
           umma::mbar_wait(&xbar, xphase);
           xphase ^= 1u;
+          TRACE_MLP(9);
         }
         mlp_sync_for_mma();
         if (tid == 0) {
@@ -925,6 +952,7 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
           } else {
             // d_features -> the TMEM slot, once every consumer holds the previous tile's
             umma::mbar_wait(&empty_bar, ((uint32_t)iter & 1u) ^ 1u);
+            TRACE_MLP(10);
             slot_tile = t;
             for (int ks = 0; ks < W / 16; ++ks)
               umma::mma_split(tm + CM::kDF, umma::desc_kmajor(Ht[l], HC, ks), umma::desc_mnmajor(wt.w0, INP, ks),
@@ -937,6 +965,7 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
           }
         }
         wait_chain(phase);
+        TRACE_MLP(7 + (H - 1 - l));
       }
       } else if (tid == 0) {  // (knob 3: no chain; hand over the stale slot)
         umma::mbar_wait(&empty_bar, ((uint32_t)iter & 1u) ^ 1u);
@@ -1196,6 +1225,12 @@ void tc_set_min_tiles_per_cta(int v) { t_min_tiles = v < 1 ? 1 : v; }
 bool pdl_enabled() {
   static const bool on = getenv("PRENOM_NO_PDL") == nullptr;
   return on;
+}
+
+cudaError_t tc_bwd_trace(long long* mlp, long long* scat) {
+  cudaError_t e = cudaMemcpyFromSymbol(mlp, g_bwd_trace, sizeof(g_bwd_trace));
+  if (e != cudaSuccess) return e;
+  return cudaMemcpyFromSymbol(scat, g_bwd_strace, sizeof(g_bwd_strace));
 }
 
 bool tc_supported(const FieldDesc& fd) {

@@ -1,0 +1,55 @@
+"""Phase timeline of the tensor-core backward (k_bwd_tc) on the cfg2 workload: clock64 stamps of
+CTA 0's first 64 tiles (MLP issuing thread and first scatter thread), via prenom_debug_bwd_trace.
+
+  PRENOM_BWD_WAIT=8 python scripts/bwd_trace.py [bf16x3|bf16] [out.json]
+"""
+import ctypes as C
+import json
+import os
+import sys
+
+import numpy as np
+
+os.environ["PRENOM_BWD_WAIT"] = str(int(os.environ.get("PRENOM_BWD_WAIT", "0")) | 8)
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import bench  # noqa: E402
+from paper_2503_01582_b200 import Context, ObjectTrainer  # noqa: E402
+
+mode = sys.argv[1] if len(sys.argv) > 1 else "bf16x3"
+sys.argv = ["bench.py", "--mlp", mode]
+args = bench.parse()
+ctx = Context(0)
+sc, grid, arch, cfg = bench.make_workload(args, 0)
+o = ObjectTrainer.create(ctx, arch, theta=None, grid=grid, seed=7, cfg=cfg, box_min=sc.box_min, box_max=sc.box_max)
+o.set_frames(sc.cams, sc.rgb, sc.depth, sc.mask, 1, sc.obj_pose)
+o.train_step(20, stats=False)
+ctx.synchronize()
+mlp = np.zeros((64, 16), np.int64)
+sca = np.zeros((64, 4), np.int64)
+ctx.lib.prenom_debug_bwd_trace(ctx.h, mlp.ctypes.data_as(C.POINTER(C.c_int64)), sca.ctypes.data_as(C.POINTER(C.c_int64)))
+GHZ = 1.965
+names = ["start", "X in", "L0", "L1", "out", "G ready", "dWo+dH1", "dW1+dH0", "dW0+dX", "X re-fetched", "slot free"]
+order = [0, 1, 2, 3, 4, 5, 6, 7, 9, 10, 8]
+n = 0
+while n < 64 and mlp[n, 0] and mlp[n, 8]:
+    n += 1
+rows = mlp[:n]
+res = {"tiles": int(n), "mode": mode, "phase_us": {}, "tile_us": None}
+prev = rows[:, 0]
+for sl in order[1:]:
+    d = (rows[:, sl] - prev) / GHZ / 1e3
+    res["phase_us"][names[sl]] = round(float(np.median(d)), 3)
+    prev = rows[:, sl]
+tile = (rows[1:, 0] - rows[:-1, 0]) / GHZ / 1e3
+res["tile_us"] = round(float(np.median(tile)), 3)
+ns = 0
+while ns < 64 and sca[ns, 0] and sca[ns, 2]:
+    ns += 1
+s = sca[:ns]
+res["scatter_us"] = {"wait_slot_to_release": round(float(np.median((s[:, 1] - s[:, 0]) / GHZ / 1e3)), 3),
+                     "scatter": round(float(np.median((s[:, 2] - s[:, 1]) / GHZ / 1e3)), 3),
+                     "idle_before_next": round(float(np.median((s[1:, 0] - s[:-1, 2]) / GHZ / 1e3)), 3)}
+line = json.dumps(res)
+print(line)
+if len(sys.argv) > 2:
+    open(sys.argv[2], "w").write(line)

@@ -29,11 +29,11 @@ for mb in (4, 8, 16, 24, 32, 48):
     res["copy"][mb] = round(2 * n * 4 * reps / (s.elapsed_time(e) / 1e3) / 1e9, 1)
     out = torch.empty(1, device="cuda")
     for _ in range(20):
-        torch.sum(a, out=out)
+        torch.sum(a)
     torch.cuda.synchronize()
     s.record()
     for _ in range(reps):
-        torch.sum(a, out=out)
+        torch.sum(a)
     e.record()
     torch.cuda.synchronize()
     res["read"][mb] = round(n * 4 * reps / (s.elapsed_time(e) / 1e3) / 1e9, 1)
