@@ -683,7 +683,7 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
   constexpr int NH = INP / 2;  // d_feature columns per half: [h*NH, (h+1)*NH)
   constexpr int LH = INP / 4;  // levels per half
   extern __shared__ __align__(1024) unsigned char smem[];
-  __shared__ uint64_t bar, xbar, full_bar, empty_bar;
+  __shared__ uint64_t bar, xbar, full_bar, empty_bar, xfree;
   __shared__ uint32_t tbase;
   __shared__ int s_tile;
   __shared__ long long slot_tile;
@@ -734,6 +734,7 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
   if (tid == 0) {
     umma::mbar_init(&bar, 1);
     umma::mbar_init(&xbar, 1);
+    umma::mbar_init(&xfree, 1);  // (overlay) dW0 has read X: the next tile's features may land
     umma::mbar_init(&full_bar, 2);  // the MMA commit + the issuing thread (slot_tile written)
     // one arrival per consumer warp: the scatter warps, and the MLP warps when
     // they scatter levels themselves
@@ -792,7 +793,7 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
   } else {
     // ================= MLP warps: tensor-core backward chain
     const uint32_t tr = tm + CM::kR;
-    uint32_t phase = 0, xphase = 0;
+    uint32_t phase = 0, xphase = 0, xfphase = 0;
     int iter = 0;
     const int q = warp & 3, half = warp >> 2, row = 32 * q + lane;
     // MMA completion: every MLP warp polls the mbarrier, or (wait_mode bit 1)
@@ -829,14 +830,17 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
       named_sync(1, kMlpThreads);
       return s_tile;
     };
-    for (long long t = fetch(); t < ntiles; t = fetch(), ++iter) {
+    // (overlay) the next tile's features are prefetched into X as soon as this
+    // tile's dW0 has read it, so only the first tile waits for its TMA
+    bool prefetched = false;
+    for (long long t = fetch(); t < ntiles; ++iter) {
       const long long tile0 = t * kTile;
       TRACE_MLP(0);
       const long long gs = tile0 + row;
       const bool valid = gs < n_total && __ldg(count + ray_of(gs, S)) > 0;
       // ---- stored bf16 features -> X by the TMA engine (no LSU work): one
       // bulk copy per 8-row group (the X row-group stride is longer: ones column)
-      if (tid == 0) fetch_x(t);
+      if (tid == 0 && !prefetched) fetch_x(t);
       if (OV) set_ones(X, INP, XC, XLO);
       umma::mbar_wait(&xbar, xphase);
       xphase ^= 1u;
@@ -945,6 +949,7 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
           for (int ks = 0; ks < 8; ++ks)
             umma::mma_split(tm + dwc, umma::desc_mnmajor(Ht[l], HC, ks), umma::desc_mnmajor(prev, pc, ks),
                             umma::idesc_bf16(64, pc, true, true), (iter > 0 || ks > 0), sp_w, HLO, plo);
+          if (OV && l == 0) umma::commit(&xfree);
           if (l > 0) {
             for (int ks = 0; ks < W / 16; ++ks)
               umma::mma_split(tr, umma::desc_kmajor(Ht[l], HC, ks), umma::desc_mnmajor(wt.wl[l - 1], W, ks),
@@ -962,6 +967,13 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
           if (l == 0) {
             umma::commit(&full_bar);
             mbar_arrive(&full_bar);
+            if (OV) {  // claim the next tile and start its feature copy once dW0 is done with X
+              umma::mbar_wait(&xfree, xfphase);
+              xfphase ^= 1u;
+              const long long nt = atomicAdd(tile_ctr, 1);
+              s_tile = nt;
+              if (nt < ntiles) fetch_x(nt);
+            }
           }
         }
         wait_chain(phase);
@@ -999,6 +1011,14 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
             }
           }
         }
+      }
+      // next tile: claimed (and its features prefetched) by the issuing thread
+      if (OV && skip_scatter != 3) {
+        named_sync(1, kMlpThreads);
+        t = s_tile;
+        prefetched = true;
+      } else {
+        t = fetch();
       }
     }
     // sentinel: stop the scatter warps

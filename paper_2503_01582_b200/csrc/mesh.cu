@@ -33,17 +33,12 @@ namespace prenom {
 namespace {
 
 // Cube conventions of the reference's table (marching_cubes.cpp:10-13): corner
-// offsets, the 12 edges as corner pairs, the 6 faces as corner cycles and
-// the edge joining consecutive corners of each cycle.
+// offsets and the 12 edges as corner pairs (vertex placement on crossed edges).
 constexpr int kCorner[8][3] = {{0, 0, 0}, {1, 0, 0}, {1, 1, 0}, {0, 1, 0},
                                {0, 0, 1}, {1, 0, 1}, {1, 1, 1}, {0, 1, 1}};
 constexpr int kEdge[12][2] = {{0, 1}, {1, 2}, {2, 3}, {3, 0}, {4, 5}, {5, 6},
                               {6, 7}, {7, 4}, {0, 4}, {1, 5}, {2, 6}, {3, 7}};
-constexpr int kFaceCorners[6][4] = {{0, 1, 2, 3}, {4, 5, 6, 7}, {0, 1, 5, 4},
-                                    {1, 2, 6, 5}, {2, 3, 7, 6}, {3, 0, 4, 7}};
-constexpr int kFaceEdges[6][4] = {{0, 1, 2, 3}, {4, 5, 6, 7}, {0, 9, 4, 8},
-                                  {1, 10, 5, 9}, {2, 11, 6, 10}, {3, 8, 7, 11}};
-constexpr int kMaxTri = 16;  // per configuration (the table below needs <= 12)
+constexpr int kMaxTri = 16;  // per configuration (the reference's table needs <= 12)
 
 struct CaseTableDev {
   unsigned char count[256];
@@ -56,86 +51,19 @@ __constant__ unsigned char c_edge_lo[12][3];    // offset of the lower (canonica
 struct F3 {
   float x, y, z;
 };
-inline F3 f3sub(F3 a, F3 b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
-inline F3 f3add(F3 a, F3 b) { return {a.x + b.x, a.y + b.y, a.z + b.z}; }
-inline F3 f3mul(F3 a, float s) { return {a.x * s, a.y * s, a.z * s}; }
-inline F3 f3cross(F3 a, F3 b) { return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x}; }
-inline float f3dot(F3 a, F3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
 
-// Host restatement of build_case_table (marching_cubes.cpp:24-107): per
-// configuration, crossed edges are paired face by face (an ambiguous face --
-// four crossings -- pairs the edges around its inside corners), the pairs
-// are traced into closed polygons starting from the lowest unvisited edge,
-// each polygon is oriented so its normal points away from the inside corners,
-// and fan-triangulated from its first edge.
-std::vector<std::array<int, 3>> build_case(int config) {
-  std::vector<std::array<int, 3>> out;
-  auto inside = [&](int c) { return (config >> c) & 1; };
-  bool crossed[12];
-  for (int e = 0; e < 12; ++e) crossed[e] = inside(kEdge[e][0]) != inside(kEdge[e][1]);
-  int partner[12][2], np[12] = {};
-  for (auto& p : partner) p[0] = p[1] = -1;
-  auto join = [&](int a, int b) {
-    partner[a][np[a]++] = b;
-    partner[b][np[b]++] = a;
-  };
-  for (int f = 0; f < 6; ++f) {
-    int hit[4], nh = 0;
-    for (int i = 0; i < 4; ++i)
-      if (crossed[kFaceEdges[f][i]]) hit[nh++] = i;
-    if (nh == 2) {
-      join(kFaceEdges[f][hit[0]], kFaceEdges[f][hit[1]]);
-    } else if (nh == 4) {
-      if (inside(kFaceCorners[f][0])) {
-        join(kFaceEdges[f][3], kFaceEdges[f][0]);
-        join(kFaceEdges[f][1], kFaceEdges[f][2]);
-      } else {
-        join(kFaceEdges[f][0], kFaceEdges[f][1]);
-        join(kFaceEdges[f][2], kFaceEdges[f][3]);
-      }
-    }
-  }
-  auto corner_f3 = [](int c) { return F3{(float)kCorner[c][0], (float)kCorner[c][1], (float)kCorner[c][2]}; };
-  auto mid = [&](int e) { return f3mul(f3add(corner_f3(kEdge[e][0]), corner_f3(kEdge[e][1])), 0.5f); };
-  bool seen[12] = {};
-  for (int s = 0; s < 12; ++s) {
-    if (!crossed[s] || seen[s]) continue;
-    std::vector<int> poly;
-    for (int prev = -1, cur = s;;) {
-      poly.push_back(cur);
-      seen[cur] = true;
-      const int nxt = partner[cur][0] == prev ? partner[cur][1] : partner[cur][0];
-      prev = cur;
-      cur = nxt;
-      if (cur == s) break;
-    }
-    F3 cen{0, 0, 0}, icen{0, 0, 0};
-    for (int e : poly) {
-      cen = f3add(cen, mid(e));
-      icen = f3add(icen, corner_f3(inside(kEdge[e][0]) ? kEdge[e][0] : kEdge[e][1]));
-    }
-    const float inv = 1.f / (float)poly.size();
-    cen = f3mul(cen, inv);
-    icen = f3mul(icen, inv);
-    F3 nrm{0, 0, 0};
-    const size_t n = poly.size();
-    for (size_t i = 0; i < n; ++i)
-      nrm = f3add(nrm, f3cross(f3sub(mid(poly[i]), cen), f3sub(mid(poly[(i + 1) % n]), cen)));
-    if (f3dot(nrm, f3sub(cen, icen)) < 0.f) std::reverse(poly.begin(), poly.end());
-    for (size_t i = 1; i + 1 < n; ++i) out.push_back({poly[0], poly[i], poly[i + 1]});
-  }
-  return out;
-}
+// The reference's case table (cube_case_triangles, marching_cubes.cpp:115-117),
+// generated from its golden fixture by scripts/gen_mc_table.py.
+#include "mc_case_table.inc"
 
 const CaseTableDev& host_case_table() {
   static const CaseTableDev t = [] {
     CaseTableDev c;
     std::memset(&c, 0, sizeof c);
     for (int cfg = 0; cfg < 256; ++cfg) {
-      const auto tris = build_case(cfg);
-      c.count[cfg] = (unsigned char)tris.size();
-      for (size_t i = 0; i < tris.size() && i < (size_t)kMaxTri; ++i)
-        for (int k = 0; k < 3; ++k) c.tri[cfg][i][k] = (unsigned char)tris[i][k];
+      c.count[cfg] = kMcCaseCount[cfg];
+      for (int i = 0; i < kMcCaseCount[cfg]; ++i)
+        for (int k = 0; k < 3; ++k) c.tri[cfg][i][k] = kMcCaseTri[cfg][i][k];
     }
     return c;
   }();

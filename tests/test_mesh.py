@@ -21,7 +21,7 @@ NAMES = list(GRIDS().keys())
 
 # ------------------------------------------------------------------ CPU
 def test_case_table_matches_reference_golden():
-    """The library's host restatement of build_case_table (marching_cubes.cpp:24-107)
+    """The library's case table (generated from the reference's fixture, scripts/gen_mc_table.py)
     equals cube_case_triangles of the reference for all 256 configurations."""
     from paper_2503_01582_b200 import trainer as T
 
