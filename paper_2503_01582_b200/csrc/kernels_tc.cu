@@ -685,7 +685,7 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ uint64_t bar, xbar, full_bar, empty_bar, xfree;
   __shared__ uint32_t tbase;
-  __shared__ int s_tile;
+  __shared__ int s_tile, s_next;
   __shared__ long long slot_tile;
   WT wt;
   unsigned char* p = smem;
@@ -836,8 +836,15 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
     for (long long t = fetch(); t < ntiles; ++iter) {
       const long long tile0 = t * kTile;
       TRACE_MLP(0);
+      // (overlay) claim the next tile now: its index is known long before this
+      // tile's chain ends, so neither the claim nor its feature copy is on the chain
+      if (OV && tid == 0) s_next = atomicAdd(tile_ctr, 1);
       const long long gs = tile0 + row;
       const bool valid = gs < n_total && __ldg(count + ray_of(gs, S)) > 0;
+      // upstream gradient of this row, loaded now: its latency would otherwise sit
+      // on the chain at the g_raw epilogue (warps 0-3 own the rows there)
+      float4 dpre = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (warp < 4 && valid) dpre = dout[gs];
       // ---- stored bf16 features -> X by the TMA engine (no LSU work): one
       // bulk copy per 8-row group (the X row-group stride is longer: ones column)
       if (tid == 0 && !prefetched) fetch_x(t);
@@ -888,7 +895,7 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
         umma::tmem_wait_ld();
         float g[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         if (valid) {
-          const float4 d = dout[gs];
+          const float4 d = dpre;
           const float* b = wt.bias + H * W;
           const float r0 = v[0] + b[0];
           const float sg = density_forward(fd.act, r0);
@@ -949,7 +956,7 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
           for (int ks = 0; ks < 8; ++ks)
             umma::mma_split(tm + dwc, umma::desc_mnmajor(Ht[l], HC, ks), umma::desc_mnmajor(prev, pc, ks),
                             umma::idesc_bf16(64, pc, true, true), (iter > 0 || ks > 0), sp_w, HLO, plo);
-          if (OV && l == 0) umma::commit(&xfree);
+          if (OV && l == 0) umma::commit(&xfree);  // dW0 is the last reader of X
           if (l > 0) {
             for (int ks = 0; ks < W / 16; ++ks)
               umma::mma_split(tr, umma::desc_kmajor(Ht[l], HC, ks), umma::desc_mnmajor(wt.wl[l - 1], W, ks),
@@ -967,14 +974,14 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
           if (l == 0) {
             umma::commit(&full_bar);
             mbar_arrive(&full_bar);
-            if (OV) {  // claim the next tile and start its feature copy once dW0 is done with X
-              umma::mbar_wait(&xfree, xfphase);
-              xfphase ^= 1u;
-              const long long nt = atomicAdd(tile_ctr, 1);
-              s_tile = nt;
-              if (nt < ntiles) fetch_x(nt);
-            }
           }
+        }
+        if (OV && l == 0 && tid == 32) {
+          // a second thread copies the next tile's features into X once dW0 is done with
+          // it, in parallel with the issuing thread's dX / slot hand-over
+          umma::mbar_wait(&xfree, xfphase);
+          xfphase ^= 1u;
+          if (s_next < ntiles) fetch_x(s_next);
         }
         wait_chain(phase);
         TRACE_MLP(7 + (H - 1 - l));
@@ -1015,7 +1022,7 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
       // next tile: claimed (and its features prefetched) by the issuing thread
       if (OV && skip_scatter != 3) {
         named_sync(1, kMlpThreads);
-        t = s_tile;
+        t = s_next;
         prefetched = true;
       } else {
         t = fetch();
@@ -1201,7 +1208,9 @@ cudaError_t run_bwd_s(const FieldDesc& fd, const float* params, float* grad, lon
   // wait on the scatter warps); PRENOM_BWD_MLP_LEVELS overrides for tuning
   static const int mlp_env = env_int("PRENOM_BWD_MLP_LEVELS", -1);
   // the MLP warps load 8 slot columns: at most 4 levels per half
-  const int mlp_levels = std::max(0, std::min(std::min(4, INP / 4), mlp_env >= 0 ? mlp_env : kBwdMlpLevels));
+  // (split mode: 0 -- the MLP chain, not the scatter, bounds the kernel)
+  const int mlp_levels =
+      std::max(0, std::min(std::min(4, INP / 4), mlp_env >= 0 ? mlp_env : (SPL ? 0 : kBwdMlpLevels)));
   static const int skip = env_int("PRENOM_PROF_SKIP_SCATTER", 0);
   // longest run reduced by pulls (else by the shuffle tree); PRENOM_BWD_PULL_MAX overrides
   static const int pull_max = env_int("PRENOM_BWD_PULL_MAX", kBwdPullMax);

@@ -1,10 +1,11 @@
 set -x
 mkdir -p gpurun_out
-T=r2f
+T=r2g
 B="timeout 300 python bench.py --steps 30 --warmup 5 --no-cpu-baseline --e2e-steps 0 --steady-steps 0"
-timeout 900 python -m pytest tests/test_split_bf16.py tests/test_gpu_parity.py tests/test_gpu_meta_multi.py -x -q -m gpu -k "not 200_steps" > gpurun_out/${T}_tests.log 2>&1
+timeout 900 python -m pytest tests/test_split_bf16.py -x -q -m gpu -k "not 200_steps" > gpurun_out/${T}_tests.log 2>&1
 python scripts/bwd_trace.py bf16x3 gpurun_out/${T}_trace_x3.json > gpurun_out/${T}_trace.log 2>&1
 $B --mlp bf16x3 > gpurun_out/${T}_x3.log 2>&1
+PRENOM_BWD_MLP_LEVELS=1 $B --mlp bf16x3 > gpurun_out/${T}_x3_ml1.log 2>&1
+PRENOM_BWD_WAIT=1 $B --mlp bf16x3 > gpurun_out/${T}_x3_w1.log 2>&1
 $B --mlp bf16 > gpurun_out/${T}_bf16.log 2>&1
-timeout 600 python bench.py --mlp bf16x3 --steps 200 --warmup 10 --no-cpu-baseline > gpurun_out/${T}_x3_200.log 2>&1
 echo done
