@@ -365,7 +365,7 @@ __global__ void __launch_bounds__(NT) k_fwd_ts(FieldDesc fd, const float* __rest
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ uint64_t bar;
   __shared__ uint32_t tbase;
-  __shared__ int s_tile;
+  __shared__ int s_tile, s_next;
   WT wt;
   unsigned char* p = smem;
   wt.carve(p);
@@ -417,8 +417,11 @@ __global__ void __launch_bounds__(NT) k_fwd_ts(FieldDesc fd, const float* __rest
     umma::fence_after_sync();
   };
   const long long ntiles = (n_total + kTile - 1) / kTile;
-  for (long long t = next_tile(tile_ctr, &s_tile); t < ntiles; t = next_tile(tile_ctr, &s_tile)) {
+  // the next tile is claimed at the start of this one (published by the first
+  // barrier), so no claim round trip sits between tiles
+  for (long long t = next_tile(tile_ctr, &s_tile); t < ntiles; t = s_next) {
     const long long tile0 = t * kTile;
+    if (tid == 0) s_next = atomicAdd(tile_ctr, 1);
     {  // ---- encode (fp32, bit-exact) -> bf16 X tile (hi, lo)
       const int s = tid & (kTile - 1), part = tid >> 7;
       const long long gs = tile0 + s;
@@ -483,6 +486,7 @@ __global__ void __launch_bounds__(NT) k_fwd_ts(FieldDesc fd, const float* __rest
     }
     if (tid == 0) umma::bulk_wait_read();  // X is rewritten by the next tile's encode
     umma::fence_before_sync();
+    __syncthreads();  // (X reuse; s_next was published by the tile's first barrier)
   }
   if (tid == 0) umma::bulk_wait_all();
   tile_sched_exit(tile_ctr);
@@ -954,8 +958,9 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
           const uint32_t plo = l == 0 ? XLO : HLO;
           // dW_l = D_l^T [prev | 1]: A = D_l (MN-major, M = 64 units), B = prev (MN-major, N = pc)
           for (int ks = 0; ks < 8; ++ks)
-            umma::mma_split(tm + dwc, umma::desc_mnmajor(Ht[l], HC, ks), umma::desc_mnmajor(prev, pc, ks),
-                            umma::idesc_bf16(64, pc, true, true), (iter > 0 || ks > 0), sp_w, HLO, plo);
+            umma::mma_split_terms(tm + dwc, umma::desc_mnmajor(Ht[l], HC, ks), umma::desc_mnmajor(prev, pc, ks),
+                                  umma::idesc_bf16(64, pc, true, true), (iter > 0 || ks > 0), sp_w && !(split & 32),
+                                  sp_w && !(split & 16), HLO, plo);
           if (OV && l == 0) umma::commit(&xfree);  // dW0 is the last reader of X
           if (l > 0) {
             for (int ks = 0; ks < W / 16; ++ks)
@@ -1274,7 +1279,9 @@ size_t tc_feature_bytes(const FieldDesc& fd, long long n, int split) {
 }
 
 // split: 0 = bf16 operands; else split-bf16 with the cross products enabled
-// per bit (1 forward, 2 backward data products, 4 weight gradients).
+// per bit (1 forward, 2 backward data products, 4 weight gradients; 16 / 32
+// drop the D_lo*prev_hi / D_hi*prev_lo term of the hidden/input weight
+// gradients -- numerics experiments).
 // PRENOM_SPLIT_MASK overrides the mask of split-mode calls (bisection).
 int split_mask(int split) {
   static const int m = env_int("PRENOM_SPLIT_MASK", 7);

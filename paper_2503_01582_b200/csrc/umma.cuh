@@ -259,6 +259,15 @@ __device__ __forceinline__ void mma_split(uint32_t tmem_d, uint64_t a, uint64_t 
   }
 }
 
+// mma_split with each cross term switchable (numerics experiments)
+__device__ __forceinline__ void mma_split_terms(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                                uint32_t accumulate, bool a_hi_b_lo, bool a_lo_b_hi, uint32_t a_lo,
+                                                uint32_t b_lo) {
+  mma_bf16(tmem_d, a, b, idesc, accumulate);
+  if (a_hi_b_lo) mma_bf16(tmem_d, a, desc_add(b, b_lo), idesc, 1u);
+  if (a_lo_b_hi) mma_bf16(tmem_d, desc_add(a, a_lo), b, idesc, 1u);
+}
+
 // mma_split with the A operand in tensor memory: hi at tmem_a, lo at tmem_a + a_lo_cols.
 __device__ __forceinline__ void mma_split_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc,
                                              uint32_t accumulate, bool split, uint32_t a_lo_cols, uint32_t b_lo) {
