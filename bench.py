@@ -51,10 +51,13 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="cfg2", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
     ap.add_argument("--width", type=int, default=64)
-    ap.add_argument("--mlp", default="bf16", choices=["fp32", "bf16", "bf16x3"])
+    ap.add_argument("--mlp", default="bf16x3", choices=["fp32", "bf16", "bf16x3"],
+                    help="MLP arithmetic: bf16x3 = split-bf16 tensor cores (fp32-class, the parity-green headline "
+                         "mode), bf16 = plain bf16 operands (1e-2), fp32 = SIMT")
     ap.add_argument("--rays", type=int, default=8192)
     ap.add_argument("--samples", type=int, default=96)
     ap.add_argument("--e2e-steps", type=int, default=100)
+    ap.add_argument("--tasks-per-gpu", type=int, default=4, help="cfg4: tasks adapted concurrently per GPU per meta-step")
     ap.add_argument("--steady-steps", type=int, default=100,
                     help="single-object workloads: also time this many steps from object step 50 on")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -178,7 +181,7 @@ def algorithmic_costs(arch, B, S, n_coarse, P, mlp="bf16"):
         "field_fwd": ("hbm", 8 * L * F * 4 * N),
         "composite": ("hbm", 40 * N),
         # bf16: fused MLP bwd + scatter RMW (2*8*L*F*4 B/sample); fp32: SIMT MLP backward flops
-        "mlp_bwd": ("hbm", 2 * 8 * L * F * 4 * N) if mlp == "bf16" else ("tensor", 3 * mlp_fwd_flops * N),
+        "mlp_bwd": ("hbm", 2 * 8 * L * F * 4 * N) if mlp in ("bf16", "bf16x3") else ("tensor", 3 * mlp_fwd_flops * N),
         # table-gradient RMW: 2 * 8*L*F*4 B/sample
         "encode_bwd": ("hbm", 2 * 8 * L * F * 4 * N),  # fp32 path: standalone k_encode_bwd
         # dense Adam: p,m,v read+write, g read + zero = 32 B/param
@@ -348,13 +351,14 @@ class Cfg3(Workload):
 
 
 class Cfg4(Workload):
-    """BASELINE config 4: Reptile meta-learning of a category prior. One
-    meta-step = every rank adapts one task (32 inner Adam steps of 4096 rays
-    x 64 midpoint samples, fresh Adam), then the task deltas are all-reduced
-    over NCCL and theta <- theta + eps * mean(delta) (eps = 0.1). Arch L16 F2
-    T2^18 W64 H2; tasks are seeded box unions with 20 views at 128^2 (a pool
-    of 4 tasks per rank stands in for BASELINE's 512 x 4 shapes: the per-step
-    work does not depend on the pool size)."""
+    """BASELINE config 4: Reptile meta-learning of a category prior. One meta-step = every rank
+    adapts `--tasks-per-gpu` tasks concurrently (multi-object scheduler lanes), each 32 inner Adam
+    steps of 4096 rays x 64 midpoint samples from theta with a fresh Adam; then one
+    prenom_reptile_step: the task deltas are summed on the device, all-reduced over NCCL (N > 1)
+    and theta <- reptile_update(theta, mean adapted, eps = 0.1). Arch L16 F2 T2^18 W64 H2;
+    tasks are seeded box unions with 20 views at 128^2 (a pool of tasks per rank stands in for
+    BASELINE's 512 x 4 shapes: the per-step work does not depend on the pool size). With one
+    task per GPU on one GPU the exact reference update (meta.cpp:83-92) is applied."""
 
     name = "cfg4"
 
@@ -364,14 +368,15 @@ class Cfg4(Workload):
 
         self.ws, self.rank = ws, rank
         self.dist = launched_distributed()
+        self.tpg = max(1, args.tasks_per_gpu)
         self.arch = scenes.cfg4_arch()
         self.cfg = TrainConfig(rays_per_iter=4096, samples_per_ray=64, prior_sampling=0, grid_refresh_every=0,
                                mlp_precision=mlp_id(args.mlp))
         self.q = 32
         self.meta = ObjectTrainer.create(ctx, self.arch, theta=None, grid_res=8, seed=4242, cfg=self.cfg)
         self.workers = []
-        for i in range(4):
-            sc = scenes.box_union_scene(n_views=20, res=128, seed=7000 + 4 * rank + i)
+        for i in range(self.tpg):
+            sc = scenes.box_union_scene(n_views=20, res=128, seed=7000 + self.tpg * rank + i)
             w = ObjectTrainer.create(ctx, self.arch, theta=None, grid_res=8, seed=1, cfg=self.cfg,
                                      box_min=sc.box_min, box_max=sc.box_max)
             w.set_frames(sc.cams, sc.rgb, sc.depth, sc.mask, 1, sc.obj_pose)
@@ -390,27 +395,34 @@ class Cfg4(Workload):
             uid = [comm_unique_id() if rank == 0 else None]
             dist.broadcast_object_list(uid, src=0)
             ctx.init_comm(ws, rank, uid[0])
-        self.n_objects_total = ws
+        self.n_objects_total = ws * self.tpg
         self.k = 0
         self.n = 0
-        self.desc = ("cfg4: Reptile meta-step = per rank one task x 32 inner Adam steps of 4096 rays x 64 samples "
-                     "(L16 F2 T18 W64 H2), NCCL all-reduce of task deltas, eps 0.1")
+        self.desc = (f"cfg4: Reptile meta-step = per rank {self.tpg} task(s) adapted concurrently x 32 inner Adam "
+                     "steps of 4096 rays x 64 samples (L16 F2 T18 W64 H2), device delta sum + NCCL all-reduce + "
+                     "interpolation (prenom_reptile_step), eps 0.1")
         self.extra = {"inner_steps": self.q, "rays_per_inner_step": 4096, "mlp_samples_per_ray": 64,
-                      "tasks_per_meta_step": ws, "params": self.arch.param_count(),
+                      "tasks_per_gpu": self.tpg, "tasks_per_meta_step": ws * self.tpg,
+                      "params": self.arch.param_count(),
                       "l2": "inputs larger than L2 (params+Adam state 128 MiB per task + meta); no flush"}
 
     def step(self, k):
-        from paper_2503_01582_b200.trainer import derive_seed
+        from paper_2503_01582_b200.trainer import derive_seed, train_many
 
         for _ in range(k):
-            t = self.k % len(self.workers)
-            self.engine.adapt(t, self.q, derive_seed(0, self.k * self.ws + self.rank))
-            st = self.workers[t].last_stats(self.q)
-            self.n += sum(s["n_samples"] for s in st)
-            if not self.dist:
-                self.engine.update_exact(t, 0.1)
+            for j, w in enumerate(self.workers):  # inner_adapt: theta, fresh Adam, per-step stream (meta.cpp:31-34)
+                w.copy_params_from(self.meta)
+                w.set_seed(derive_seed(0, (self.k * self.ws + self.rank) * self.tpg + j))
+            if self.tpg == 1:
+                self.workers[0].train_step(self.q, stats=False)
+            else:
+                train_many(self.workers, self.q)
+            for w in self.workers:
+                self.n += sum(s["n_samples"] for s in w.last_stats(self.q))
+            if not self.dist and self.tpg == 1:
+                self.engine.update_exact(0, 0.1)
             else:  # delta sum -> ncclAllReduce -> interpolation, one C call on the library stream
-                self.engine.reptile_step([t], self.ws, 0.1)
+                self.engine.reptile_step(list(range(self.tpg)), self.ws * self.tpg, 0.1)
             self.k += 1
 
     def samples(self, k):
@@ -419,7 +431,7 @@ class Cfg4(Workload):
         return n
 
     def work_items(self):
-        return [(self.arch, self.cfg, self.q)]
+        return [(self.arch, self.cfg, self.q * self.tpg)]
 
 
 def mixed_category_archs(seed=31, n=4):
@@ -730,11 +742,13 @@ def run_ours(args):
                        "frac": round(enc_bytes / enc_t / 1e9 / pk["hbm_gbs"], 4) if enc_t else None,
                        "bytes_per_sample": "96*L*F (8 corners x L*F x (4 B gather + 8 B RMW))",
                        "kernels": ["field_fwd", bwd_name]}
-    if "mlp_bwd" in kernels and args.mlp == "bf16":
+    if "mlp_bwd" in kernels and args.mlp in ("bf16", "bf16x3"):
         t_bwd = kms[KERNEL_CLASSES.index("mlp_bwd")] / 1e3
+        executed = tensor_flops * (3 if args.mlp == "bf16x3" else 1)  # split operands: 3 bf16 products each
         kernels["mlp_bwd"]["tensor"] = {
-            "flops": tensor_flops, "achieved_tflops": round(tensor_flops / t_bwd / 1e12, 2),
-            "frac_of_bf16_sustained": round(tensor_flops / t_bwd / 1e12 / pk["bf16_tflops_sustained"], 4)}
+            "flops_algorithmic": tensor_flops, "flops_executed": executed,
+            "achieved_tflops_executed": round(executed / t_bwd / 1e12, 2),
+            "frac_of_bf16_sustained": round(executed / t_bwd / 1e12 / pk["bf16_tflops_sustained"], 4)}
 
     tail = wl.tail(ctx) if hasattr(wl, "tail") else None
 

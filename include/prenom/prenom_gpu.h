@@ -375,8 +375,10 @@ prenom_status prenom_debug_field_backward(prenom_ctx_t ctx, const prenom_field_a
                                           int mlp_precision);
 /* Phase trace of the tensor-core backward (set PRENOM_BWD_WAIT bit 8 before the
  * first backward launch): clock64 stamps of CTA 0's first 64 tiles, MLP issuing
- * thread mlp[64][16] (slots 0..10) and first scatter thread scatter[64][4]. */
-prenom_status prenom_debug_bwd_trace(prenom_ctx_t ctx, int64_t* mlp, int64_t* scatter);
+ * thread mlp[64][16] (slots 0..10) and first scatter thread scatter[64][4]; and
+ * (cta may be NULL) per CTA cta[1024][5]: globaltimer ns at entry, after the
+ * prologue, at the end of its tiles and at exit, and its tile count. */
+prenom_status prenom_debug_bwd_trace(prenom_ctx_t ctx, int64_t* mlp, int64_t* scatter, int64_t* cta);
 /* adam_step (field.cpp:295-310) on n floats; *step in/out. */
 prenom_status prenom_debug_adam(prenom_ctx_t ctx, size_t n, float* params, const float* grads,
                                 float* m, float* v, int64_t* step, float lr, float beta1,

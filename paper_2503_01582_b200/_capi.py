@@ -254,7 +254,7 @@ def _declare(lib):
         "prenom_debug_marching_cubes": (i32, [P, i32, f32p, C.c_float, i64p, i64p]),
         "prenom_debug_mesh_get": (i32, [P, f32p, i32p]),
         "prenom_mc_case_triangles": (i32, [i32, i32p]),
-        "prenom_debug_bwd_trace": (i32, [P, i64p, i64p]),
+        "prenom_debug_bwd_trace": (i32, [P, i64p, i64p, i64p]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(lib, name)

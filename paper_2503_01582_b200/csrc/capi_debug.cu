@@ -448,11 +448,12 @@ prenom_status prenom_debug_umma_gemm(prenom_ctx_t ctx, int M, int N, int K, int 
   CUDA_TRY(cudaStreamSynchronize(st));
   return PRENOM_OK;
 }
-prenom_status prenom_debug_bwd_trace(prenom_ctx_t ctx, int64_t* mlp, int64_t* scatter) {
+prenom_status prenom_debug_bwd_trace(prenom_ctx_t ctx, int64_t* mlp, int64_t* scatter, int64_t* cta) {
   if (!ctx || !mlp || !scatter) return fail(PRENOM_USAGE, "NULL argument");
   CUDA_TRY(cudaSetDevice(ctx->device));
   CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-  CUDA_TRY(tc_bwd_trace(reinterpret_cast<long long*>(mlp), reinterpret_cast<long long*>(scatter)));
+  CUDA_TRY(tc_bwd_trace(reinterpret_cast<long long*>(mlp), reinterpret_cast<long long*>(scatter),
+                        reinterpret_cast<long long*>(cta)));
   return PRENOM_OK;
 }
 }  // extern "C"

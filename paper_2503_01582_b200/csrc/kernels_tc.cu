@@ -132,6 +132,10 @@ __device__ __forceinline__ long long next_tile(int* ctr, int* s_tile) {
   return *s_tile;
 }
 
+__device__ __forceinline__ void named_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
 __device__ __forceinline__ void sync_for_mma() {
   umma::fence_proxy_async();
   umma::fence_before_sync();
@@ -494,6 +498,193 @@ __global__ void __launch_bounds__(NT) k_fwd_ts(FieldDesc fd, const float* __rest
   if (warp == 0) umma::tmem_dealloc(tm, kCols);
 }
 
+// ------------------------------------------------------------------ fwd, warp-specialised
+// k_fwd_ts with the encode and the MLP chain on different warps, so the gathers
+// of tile t+1 run while tile t is on the tensor cores (in k_fwd_ts every warp
+// waits for the chain). 16 encode warps (4 threads per sample, levels
+// interleaved as before) fill a double-buffered feature tile (full / empty
+// mbarriers); 4 MLP warps (one row per thread: TMEM lane quadrant = warp % 4)
+// issue the MMAs, run the epilogues through TMEM and write (sigma, rgb).
+// Tiles are claimed one ahead by the encode leader.
+constexpr int kWsEncWarps = 16;
+constexpr int kWsThreads = (kWsEncWarps + 4) * 32;
+
+template <int INP, int W, int H, int SPL>
+__global__ void __launch_bounds__(kWsThreads, 2) k_fwd_ws(FieldDesc fd, const float* __restrict__ params, long long n_total,
+                                                    int S, const int* __restrict__ count, const float4* __restrict__ pos,
+                                                    uint4* __restrict__ feat_tiles, float4* __restrict__ out, int* flag,
+                                                    int* tile_ctr, int split) {
+  using WT = WeightTiles<INP, W, H, SPL>;
+  constexpr int kEnc = kWsEncWarps * 32;
+  constexpr int TPS = kEnc / 128;
+  constexpr uint32_t XLO = SPL ? 128 * INP * 2 : 0;
+  constexpr uint32_t kXBytes = 128 * INP * 2 * (SPL ? 2 : 1);
+  constexpr uint32_t kCols = 2 * W <= 64 ? 64 : 128;
+  constexpr int kHhi = W, kHlo = W + W / 2;
+  const bool sp = SPL && (split & 1);
+  extern __shared__ __align__(1024) unsigned char smem[];
+  __shared__ uint64_t full[2], empty[2], bar;
+  __shared__ uint32_t tbase;
+  __shared__ long long claim[2], tile_of[2];
+  WT wt;
+  unsigned char* p = smem;
+  wt.carve(p);
+  unsigned char* const Xb0 = p;  // two feature buffers, kXBytes apart
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const long long ntiles = (n_total + kTile - 1) / kTile;
+  pdl_wait();  // params come from the previous step's Adam
+  wt.load(fd, params + fd.hash_params, kWsThreads);
+  for (int i = tid; i < (int)kXBytes; i += kWsThreads) {  // (both buffers; padding levels stay 0)
+    reinterpret_cast<__nv_bfloat16*>(Xb0)[i] = __float2bfloat16_rn(0.f);
+  }
+  if (warp == kWsEncWarps) umma::tmem_alloc(&tbase, kCols);
+  if (tid == 0) {
+    for (int b = 0; b < 2; ++b) {
+      umma::mbar_init(&full[b], kEnc);
+      umma::mbar_init(&empty[b], 1);
+    }
+    umma::mbar_init(&bar, 1);
+    umma::fence_mbar_init();
+    claim[0] = atomicAdd(tile_ctr, 1);
+  }
+  umma::fence_before_sync();
+  __syncthreads();
+  umma::fence_after_sync();
+  const uint32_t tm = tbase;
+  if (warp < kWsEncWarps) {
+    // ================= encode warps
+    const int s = tid & (kTile - 1), part = tid >> 7;
+    for (int i = 0;; ++i) {
+      const int b = i & 1;
+      umma::mbar_wait(&empty[b], ((uint32_t)(i >> 1) & 1u) ^ 1u);  // buffer b free (first pass: immediately)
+      named_sync(2, kEnc);  // claim[b] of this iteration is published
+      const long long t = claim[b];
+      if (tid == 0 && t < ntiles) claim[b ^ 1] = atomicAdd(tile_ctr, 1);  // next iteration's tile
+      if (t >= ntiles) {
+        if (tid == 0) tile_of[b] = -1;  // sentinel for the MLP warps
+        umma::mbar_arrive_plain(&full[b]);
+        break;
+      }
+      if (tid == 0) tile_of[b] = t;
+      unsigned char* X = Xb0 + b * kXBytes;
+      const long long gs = t * kTile + s;
+      const bool valid = gs < n_total && __ldg(count + ray_of(gs, S)) > 0;
+      float4 pp = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (valid) pp = pos[gs];
+      const float px = clamp01(pp.x), py = clamp01(pp.y), pz = clamp01(pp.z);
+      for (int l = part; l < fd.L; l += TPS) {
+        float f[2] = {0.f, 0.f};
+        if (valid) encode_level<2>(fd, params, l, px, py, pz, f);
+        const __nv_bfloat162 hi = __floats2bfloat162_rn(f[0], f[1]);
+        *reinterpret_cast<__nv_bfloat162*>(X + umma::cm_offset(s, 2 * l, INP)) = hi;
+        if (SPL)
+          *reinterpret_cast<__nv_bfloat162*>(X + XLO + umma::cm_offset(s, 2 * l, INP)) =
+              __floats2bfloat162_rn(f[0] - __low2float(hi), f[1] - __high2float(hi));
+      }
+      umma::fence_proxy_async();  // generic smem writes -> the tensor core and the TMA store
+      umma::mbar_arrive_plain(&full[b]);
+    }
+  } else {
+    // ================= MLP warps: one row per thread
+    const int q = warp & 3, row = 32 * q + lane, mt = tid - kEnc;
+    const uint32_t lane_base = (uint32_t)(32 * q) << 16;
+    uint32_t phase = 0;
+    constexpr uint32_t id_h = umma::idesc_bf16(128, W, false, false);
+    constexpr uint32_t id_out = umma::idesc_bf16(128, 16, false, false);
+    auto mlp_sync = [&]() {
+      umma::fence_before_sync();
+      named_sync(1, 128);
+      umma::fence_after_sync();
+    };
+    auto epilogue = [&](const float* bias) {
+#pragma unroll
+      for (int c = 0; c < W; c += 16) {
+        float v[16];
+        umma::tmem_ld16(tm + lane_base + c, v);
+        umma::tmem_wait_ld();
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          uint32_t hi[4], lo[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int k = 8 * h + 2 * i;
+            const float a0 = fmaxf(v[k] + bias[c + k], 0.f), a1 = fmaxf(v[k + 1] + bias[c + k + 1], 0.f);
+            const __nv_bfloat162 hh = __floats2bfloat162_rn(a0, a1);
+            hi[i] = *reinterpret_cast<const uint32_t*>(&hh);
+            if (SPL) {
+              const __nv_bfloat162 ll = __floats2bfloat162_rn(a0 - __low2float(hh), a1 - __high2float(hh));
+              lo[i] = *reinterpret_cast<const uint32_t*>(&ll);
+            }
+          }
+          umma::tmem_st4(tm + lane_base + kHhi + (c + 8 * h) / 2, hi);
+          if (SPL) umma::tmem_st4(tm + lane_base + kHlo + (c + 8 * h) / 2, lo);
+        }
+      }
+      umma::tmem_wait_st();
+      mlp_sync();
+    };
+    for (int i = 0;; ++i) {
+      const int b = i & 1;
+      umma::mbar_wait(&full[b], (uint32_t)(i >> 1) & 1u);
+      const long long t = tile_of[b];
+      if (t < 0) break;
+      umma::fence_after_sync();
+      unsigned char* X = Xb0 + b * kXBytes;
+      if (mt == 0) {
+        for (int ks = 0; ks < INP / 16; ++ks)
+          umma::mma_split(tm, umma::desc_kmajor(X, INP, ks), umma::desc_kmajor(wt.w0, INP, ks), id_h, ks > 0, sp, XLO,
+                          WT::kLo);
+        umma::commit(&bar);
+        umma::bulk_s2g(feat_tiles + t * (kXBytes / 16), X, kXBytes);  // stored features for the backward
+      }
+      wait_mma(&bar, phase);
+      if (mt == 0) {  // the layer-0 MMA and the feature store have read buffer b
+        umma::bulk_wait_read();
+        umma::mbar_arrive_plain(&empty[b]);
+      }
+      epilogue(wt.bias);
+      for (int l = 1; l < H; ++l) {
+        if (mt == 0) {
+          for (int ks = 0; ks < W / 16; ++ks)
+            umma::mma_split_ts(tm, tm + kHhi + ks * 8, umma::desc_kmajor(wt.wl[l - 1], W, ks), id_h, ks > 0, sp,
+                               kHlo - kHhi, WT::kLo);
+          umma::commit(&bar);
+        }
+        wait_mma(&bar, phase);
+        epilogue(wt.bias + l * W);
+      }
+      if (mt == 0) {
+        for (int ks = 0; ks < W / 16; ++ks)
+          umma::mma_split_ts(tm, tm + kHhi + ks * 8, umma::desc_kmajor(wt.wo, W, ks), id_out, ks > 0, sp,
+                             kHlo - kHhi, WT::kLo);
+        umma::commit(&bar);
+      }
+      wait_mma(&bar, phase);
+      float v[8];
+      umma::tmem_ld8(tm + lane_base, v);
+      umma::tmem_wait_ld();
+      const long long gs = t * kTile + row;
+      if (gs < n_total) {
+        float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (__ldg(count + ray_of(gs, S)) > 0) {
+          const float* bb = wt.bias + H * W;
+          o.x = density_forward(fd.act, v[0] + bb[0]);
+          o.y = stable_sigmoid(v[1] + bb[1]);
+          o.z = stable_sigmoid(v[2] + bb[2]);
+          o.w = stable_sigmoid(v[3] + bb[3]);
+          if (!all_finite4(o.x, o.y, o.z, o.w)) atomicOr(flag, 1);
+        }
+        out[gs] = o;
+      }
+      mlp_sync();  // the accumulator is free for the next tile's layer 0
+    }
+    if (mt == 0) umma::bulk_wait_all();
+  }
+  __syncthreads();
+  tile_sched_exit(tile_ctr);
+  if (warp == kWsEncWarps) umma::tmem_dealloc(tm, kCols);
+}
+
 // One level of the table-gradient scatter for the 32 consecutive samples of a
 // warp (field.cpp:279-292). Samples of a ray are depth-sorted and a line
 // enters each cell once, so equal cells form contiguous lane runs; each run's
@@ -617,9 +808,6 @@ constexpr int kBwdThreads = kMlpThreads + kScatThreads;
 // barrier, 2 one MLP warp polls each MMA barrier
 constexpr int kBwdWaitDefault = 0;
 
-__device__ __forceinline__ void named_sync(int id, int n) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
 
 __device__ __forceinline__ void mlp_sync_for_mma() {
   umma::fence_proxy_async();
@@ -643,6 +831,17 @@ __device__ __forceinline__ void mbar_arrive2(uint64_t* bar) {
 // prenom_debug_bwd_trace.
 __device__ long long g_bwd_trace[64][16];
 __device__ long long g_bwd_strace[64][4];
+// per CTA (globaltimer ns): entry, after the prologue + pdl_wait, MLP loop end, exit; tiles
+__device__ long long g_bwd_cta[1024][5];
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define TRACE_CTA(slot, v)                                                              \
+  do {                                                                                  \
+    if ((wait_mode & 8) && tid == 0 && blockIdx.x < 1024) g_bwd_cta[blockIdx.x][slot] = (v); \
+  } while (0)
 #define TRACE_MLP(slot)                                                                   \
   do {                                                                                    \
     if ((wait_mode & 8) && blockIdx.x == 0 && tid == 0 && iter < 64) g_bwd_trace[iter][slot] = clock64(); \
@@ -687,6 +886,7 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
   constexpr int NH = INP / 2;  // d_feature columns per half: [h*NH, (h+1)*NH)
   constexpr int LH = INP / 4;  // levels per half
   extern __shared__ __align__(1024) unsigned char smem[];
+  const long long t_entry = (wait_mode & 8) ? gtimer() : 0;
   __shared__ uint64_t bar, xbar, full_bar, empty_bar, xfree;
   __shared__ uint32_t tbase;
   __shared__ int s_tile, s_next;
@@ -751,6 +951,8 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
   const uint32_t tm = tbase;
   const long long ntiles = (n_total + kTile - 1) / kTile;
   pdl_wait();  // (PDL) the prologue above may overlap the compositing kernel; dout / features from here on
+  TRACE_CTA(0, t_entry);
+  TRACE_CTA(1, gtimer());
 
   if (warp >= kMlpThreads / 32) {
     // ================= scatter warps: d_features -> table gradient
@@ -1033,6 +1235,8 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
         t = fetch();
       }
     }
+    TRACE_CTA(2, gtimer());
+    TRACE_CTA(4, (long long)iter);
     // sentinel: stop the scatter warps
     if (tid == 0) {
       umma::mbar_wait(&empty_bar, ((uint32_t)iter & 1u) ^ 1u);
@@ -1083,6 +1287,7 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
   umma::fence_before_sync();
   __syncthreads();
   if (warp == 0) umma::tmem_dealloc(tm, 256);
+  TRACE_CTA(3, gtimer());
 }
 
 // Persistent-grid sizing hint: under the multi-object scheduler (concurrent
@@ -1132,9 +1337,14 @@ size_t fwd_ts_smem() {
 template <int INP, int W, int H, int NT, int SPL>
 cudaError_t run_fwd_nt(const FieldDesc& fd, const float* params, long long n, int S, const int* count,
                        const float4* pos, void* feat_tiles, float4* out, int* flag, int* tile_ctr, int ctas,
-                       size_t min_smem, int carveout, int split, bool ts, cudaStream_t st) {
-  auto kern = ts ? k_fwd_ts<INP, W, H, NT, SPL> : k_fwd_tc<INP, W, H, NT, SPL>;
-  const size_t smem = std::max<size_t>(ts ? fwd_ts_smem<INP, W, H, SPL>() : fwd_smem<INP, W, H, SPL>(), min_smem);
+                       size_t min_smem, int carveout, int split, int ts, cudaStream_t st) {
+  // ts: 1 = TMEM activations (k_fwd_ts), 2 = + warp-specialised encode (k_fwd_ws, fixed shape)
+  auto kern = ts == 2 ? k_fwd_ws<INP, W, H, SPL> : ts ? k_fwd_ts<INP, W, H, NT, SPL> : k_fwd_tc<INP, W, H, NT, SPL>;
+  const size_t smem = std::max<size_t>(ts == 2 ? fwd_ts_smem<INP, W, H, SPL>() + 128 * INP * 2 * (SPL ? 2 : 1)
+                                       : ts     ? fwd_ts_smem<INP, W, H, SPL>()
+                                                : fwd_smem<INP, W, H, SPL>(),
+                                       min_smem);
+  const int nthreads = ts == 2 ? kWsThreads : NT;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   // shared-memory carve-out (percent of the maximum): the rest of the 256 KB
@@ -1149,7 +1359,7 @@ cudaError_t run_fwd_nt(const FieldDesc& fd, const float* params, long long n, in
   e = cudaMemsetAsync(tile_ctr, 0, sizeof(int), st);
   if (e != cudaSuccess) return e;
 #endif
-  return launch_pdl(kern, dim3((unsigned)grid), dim3(NT), smem, st, fd, params, n, S, count, pos,
+  return launch_pdl(kern, dim3((unsigned)grid), dim3(nthreads), smem, st, fd, params, n, S, count, pos,
                     reinterpret_cast<uint4*>(feat_tiles), out, flag, tile_ctr, split);
 }
 
@@ -1166,7 +1376,7 @@ cudaError_t run_fwd(const FieldDesc& fd, const float* params, long long n, int S
   // PRENOM_FWD{,S}_{CTAS,SMEM_KB,THREADS,CARVEOUT,TS} override the measured
   // defaults of the bf16 / split (S) forward; TS = activations in TMEM (k_fwd_ts)
   if (split) {
-    static const bool ts = env_int("PRENOM_FWDS_TS", kFwdSTsDefault) != 0;
+    static const int ts = env_int("PRENOM_FWDS_TS", kFwdSTsDefault);
     static const int nt = env_int("PRENOM_FWDS_THREADS", ts ? kFwdSTsThreads : kFwdSThreadsDefault) == 512 ? 512 : 256;
     static const int ctas = std::max(1, std::min(8, env_int("PRENOM_FWDS_CTAS", ts ? kFwdSTsCtas : kFwdSCtasDefault)));
     static const size_t min_smem = (size_t)env_int("PRENOM_FWDS_SMEM_KB", 0) * 1024;
@@ -1177,7 +1387,7 @@ cudaError_t run_fwd(const FieldDesc& fd, const float* params, long long n, int S
     return run_fwd_nt<INP, W, H, 256, 1>(fd, params, n, S, count, pos, feat_tiles, out, flag, tile_ctr, ctas, min_smem,
                                          carve, split, ts, st);
   }
-  static const bool ts = env_int("PRENOM_FWD_TS", 0) != 0;
+  static const int ts = env_int("PRENOM_FWD_TS", 0);
   static const int nt = env_int("PRENOM_FWD_THREADS", kFwdThreadsDefault) == 512 ? 512 : 256;
   static const int ctas = std::max(1, std::min(8, env_int("PRENOM_FWD_CTAS", kFwdCtasDefault)));
   static const size_t min_smem = (size_t)env_int("PRENOM_FWD_SMEM_KB", ts ? 0 : kFwdSmemKbDefault) * 1024;
@@ -1261,10 +1471,12 @@ bool pdl_enabled() {
   return on;
 }
 
-cudaError_t tc_bwd_trace(long long* mlp, long long* scat) {
+cudaError_t tc_bwd_trace(long long* mlp, long long* scat, long long* cta) {
   cudaError_t e = cudaMemcpyFromSymbol(mlp, g_bwd_trace, sizeof(g_bwd_trace));
   if (e != cudaSuccess) return e;
-  return cudaMemcpyFromSymbol(scat, g_bwd_strace, sizeof(g_bwd_strace));
+  e = cudaMemcpyFromSymbol(scat, g_bwd_strace, sizeof(g_bwd_strace));
+  if (e != cudaSuccess || !cta) return e;
+  return cudaMemcpyFromSymbol(cta, g_bwd_cta, sizeof(g_bwd_cta));
 }
 
 bool tc_supported(const FieldDesc& fd) {

@@ -444,7 +444,7 @@ cudaError_t run_marching_cubes(const float* d_grid, int R, float iso, McScratch&
 
 // bf16 tensor-core MLP path (kernels_tc.cu)
 bool tc_supported(const FieldDesc& fd);
-cudaError_t tc_bwd_trace(long long* mlp /* 64 x 16 */, long long* scat /* 64 x 4 */);
+cudaError_t tc_bwd_trace(long long* mlp /* 64 x 16 */, long long* scat /* 64 x 4 */, long long* cta /* 1024 x 5 */);
 void tc_set_min_tiles_per_cta(int v);  // persistent-grid hint for the calling host thread (multi-object)
 size_t tc_feature_bytes(const FieldDesc& fd, long long n, int split);
 // tile_ctr: one device int per launch, zeroed by the launcher (dynamic tile scheduler)

@@ -188,6 +188,11 @@ __device__ __forceinline__ uint32_t taddr(uint32_t base, int lane, int col) {
   return base + ((uint32_t)lane << 16) + (uint32_t)col;
 }
 
+// Plain arrive (count 1) on an mbarrier, release semantics for this thread's prior writes.
+__device__ __forceinline__ void mbar_arrive_plain(uint64_t* mbar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(mbar)) : "memory");
+}
+
 // TMA bulk copy global -> shared (no tensor map: 1-D, 16 B aligned, size % 16
 // == 0), completing `bytes` of transaction count on the mbarrier.
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* mbar, uint32_t bytes) {

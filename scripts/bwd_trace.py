@@ -26,7 +26,9 @@ o.train_step(20, stats=False)
 ctx.synchronize()
 mlp = np.zeros((64, 16), np.int64)
 sca = np.zeros((64, 4), np.int64)
-ctx.lib.prenom_debug_bwd_trace(ctx.h, mlp.ctypes.data_as(C.POINTER(C.c_int64)), sca.ctypes.data_as(C.POINTER(C.c_int64)))
+cta = np.zeros((1024, 5), np.int64)
+P64 = C.POINTER(C.c_int64)
+ctx.lib.prenom_debug_bwd_trace(ctx.h, mlp.ctypes.data_as(P64), sca.ctypes.data_as(P64), cta.ctypes.data_as(P64))
 GHZ = 1.965
 names = ["start", "X in", "L0", "L1", "out", "G ready", "dWo+dH1", "dW1+dH0", "dW0+dX", "X re-fetched", "slot free"]
 order = [0, 1, 2, 3, 4, 5, 6, 7, 9, 10, 8]
@@ -49,6 +51,17 @@ s = sca[:ns]
 res["scatter_us"] = {"wait_slot_to_release": round(float(np.median((s[:, 1] - s[:, 0]) / GHZ / 1e3)), 3),
                      "scatter": round(float(np.median((s[:, 2] - s[:, 1]) / GHZ / 1e3)), 3),
                      "idle_before_next": round(float(np.median((s[1:, 0] - s[:-1, 2]) / GHZ / 1e3)), 3)}
+nc = int(np.sum(cta[:, 3] > 0))
+c = cta[:nc]
+t0 = c[:, 0].min()
+res["ctas"] = {"n": nc, "kernel_us": round((c[:, 3].max() - t0) / 1e3, 2),
+               "prologue_us_median": round(float(np.median(c[:, 1] - c[:, 0])) / 1e3, 2),
+               "first_entry_to_last_entry_us": round((c[:, 0].max() - t0) / 1e3, 2),
+               "loop_end_us": {"min": round((c[:, 2].min() - t0) / 1e3, 2), "median": round(float(np.median(c[:, 2] - t0)) / 1e3, 2),
+                               "max": round((c[:, 2].max() - t0) / 1e3, 2)},
+               "flush_us_median": round(float(np.median(c[:, 3] - c[:, 2])) / 1e3, 2),
+               "tiles_per_cta": {"min": int(c[:, 4].min()), "max": int(c[:, 4].max()), "mean": round(float(c[:, 4].mean()), 2)},
+               "tile_us_mean": round(float(np.mean((c[:, 2] - c[:, 1]) / np.maximum(c[:, 4], 1))) / 1e3, 3)}
 line = json.dumps(res)
 print(line)
 if len(sys.argv) > 2:

@@ -321,8 +321,8 @@ def test_bf16_tensor_core_forward_within_1e2(ctx, oracle, rng):
         xyz = rng.uniform(0, 1, (1000, 3)).astype(np.float32)
         s, c, _ = T.debug_field_eval(ctx, a, params, xyz, precision=1)
         so, co = oracle.field_eval(a, params, xyz)
-        np.testing.assert_allclose(np.log(s), np.log(so), atol=2e-2)  # sigma = exp(raw): 1e-2-ish on raw
-        np.testing.assert_allclose(c, co, atol=1e-2)
+        np.testing.assert_allclose(s, so, rtol=1e-2, atol=1e-4)  # north_star bf16 bar: 1e-2 relative
+        np.testing.assert_allclose(c, co, rtol=1e-2, atol=1e-3)
 
 
 def bf16_reference_backward(oracle, a, params, xyz, ds, dr):
@@ -452,6 +452,10 @@ def test_bf16_backward_ray_ordered_runs(ctx, oracle, rng, S):
         assert np.mean((g[:nh] == 0) != (ref[:nh] == 0)) < 1e-3
 
 
+@pytest.mark.xfail(strict=False, reason="plain-bf16 MLP operands: the 200-step loss lands 1-2.5% from the fp32 "
+                   "oracle (measured 0.985-0.989 here; 1.022 at cfg2, 0.985 at cfg1 full size, "
+                   "profiles/loss_parity_cfg*_r2a.json). The benchmarked mode is split-bf16 (bf16x3), held to 1% "
+                   "by tests/test_split_bf16.py.")
 def test_bf16_train_loss_tracks_fp32_oracle(ctx, oracle):
     sc, grid = small_scene(res=40, views=5)
     arch = FieldArch(hash_levels=8, features_per_level=2, log2_table_size=11, base_resolution=6,
@@ -462,10 +466,7 @@ def test_bf16_train_loss_tracks_fp32_oracle(ctx, oracle):
     lo = np.array([s["total"] for s in ob.train_step(200)])
     assert lo[-20:].mean() < 0.8 * lo[:5].mean()
     print("bf16/fp32 final-loss ratio", lg[-20:].mean() / lo[-20:].mean())
-    # bf16 MLP vs the fp32 oracle: measured 0.985-0.989 over repeated runs
-    # (atomic-order nondeterminism compounds over 200 steps); the fp32 path is
-    # held to the north-star 1% in test_train_200_steps_loss_within_1pct.
-    assert abs(lg[-20:].mean() / lo[-20:].mean() - 1) < 0.05, (lg[-20:].mean(), lo[-20:].mean())
+    assert abs(lg[-20:].mean() / lo[-20:].mean() - 1) < 0.01, (lg[-20:].mean(), lo[-20:].mean())
 
 
 @pytest.mark.parametrize("B,S,prior,mlp", [(1, 1, 0, 0), (5, 17, 1, 0), (333, 33, 1, 0), (64, 256, 1, 0),
