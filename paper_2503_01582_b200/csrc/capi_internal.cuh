@@ -244,6 +244,7 @@ struct prenom_object_s {
   DevBuf<float4> pos_depth, target, out, dout;
   DevBuf<float> delta, feat_t, dfeat_t, t_entry, t_exit;
   DevBuf<unsigned char> feat_tc;  // bf16 feature tiles (tensor-core path)
+  DevBuf<float> mlp_part;         // per-CTA MLP weight-gradient partials of the tensor-core backward
   DevBuf<int> tile_ctr;           // dynamic tile-scheduler counters (fwd, bwd)
   DevBuf<int> kind, count;
   DevBuf<StepStatsDev> stats;
@@ -300,6 +301,7 @@ inline prenom_status ensure_scratch(prenom_object_s* o, int B, int S) {
   CUDA_TRY(o->dout.ensure(Npad));
   if (uses_tc(o)) {
     CUDA_TRY(o->feat_tc.ensure(tc_feature_bytes(o->fd, (long long)N, tc_split(o))));
+    CUDA_TRY(o->mlp_part.ensure(tc_mlp_part_floats(o->fd)));
     if (!o->tile_ctr.p) {  // [fwd next, fwd done (self-resetting), bwd next (memset per launch), -]
       CUDA_TRY(o->tile_ctr.ensure(4));
       CUDA_TRY(cudaMemset(o->tile_ctr.p, 0, 4 * sizeof(int)));
@@ -495,7 +497,8 @@ inline prenom_status enqueue_step(prenom_object_s* o, StepStatsDev* stats, bool 
   if (tc) {
     ProfScope ps(o->ctx, PRENOM_K_MLP_BWD, st);  // MLP backward + fused table-gradient scatter
     CUDA_TRY(launch_bwd_tc(o->fd, o->params.p, o->grad.p, (long long)B * S, S, sb.count, sb.pos_depth,
-                           o->feat_tc.p, o->dout.p, o->tile_ctr.p + 2, tc_split(o), st));
+                           o->feat_tc.p, o->dout.p, o->tile_ctr.p + 2, tc_split(o), o->mlp_part.p, o->mlp_part.n,
+                           st));
   } else {
     {
       ProfScope ps(o->ctx, PRENOM_K_MLP_BWD, st);
@@ -530,7 +533,7 @@ inline prenom_status enqueue_step(prenom_object_s* o, StepStatsDev* stats, bool 
     CUDA_TRY(launch_adam(o->P, o->params.p, o->grad.p, o->m.p, o->v.p, c.eta, c.adam_beta1, c.adam_beta2,
                          c.adam_eps, c1, c2, 1, st));
   }
-  o->ctx->launches += tc ? 5 : 6;  // sample, fwd, composite, bwd (+ encode_bwd), adam
+  o->ctx->launches += tc ? 6 : 6;  // sample, fwd, composite, bwd + MLP-gradient reduce (or encode_bwd), adam
   o->step += 1;
   // grid refresh every m iterations (mapper.cpp:182-183)
   if (c.grid_refresh_every > 0 && o->step % c.grid_refresh_every == 0) {

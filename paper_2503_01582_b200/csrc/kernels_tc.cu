@@ -42,11 +42,13 @@ constexpr int kFwdCarveoutDefault = 58;
 constexpr int kFwdSThreadsDefault = 512;
 constexpr int kFwdSCtasDefault = 2;
 constexpr int kFwdSCarveoutDefault = 58;  // 132 KB of shared memory, 124 KB of L1
-// split forward with TMEM-resident activations (k_fwd_ts, ~47 KB per CTA)
-constexpr int kFwdSTsDefault = 1;
+// split forward: warp-specialised with TMEM-resident activations (k_fwd_ws,
+// ~62 KB per CTA, 2 CTAs per SM in a 132 KB carve-out; cfg2 0.181 ms vs 0.214 for
+// k_fwd_ts at 512 x 2 and 0.250 for k_fwd_tc); PRENOM_FWDS_TS=1 / 0 select those
+constexpr int kFwdSTsDefault = 2;
 constexpr int kFwdSTsThreads = 512;
 constexpr int kFwdSTsCtas = 2;
-constexpr int kFwdSTsCarveout = 44;  // 100 KB of shared memory, 156 KB of L1
+constexpr int kFwdSTsCarveout = 58;
 constexpr size_t kSmemPerSm = 228 * 1024;
 constexpr int kSlack = 0;       // weight tiles are never over-read
 // M=128 MN-major views of the (features|1) and (activations|1) tiles read
@@ -867,7 +869,7 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
     k_bwd_tc(FieldDesc fd, const float* __restrict__ params, float* __restrict__ grad, long long n_total, int S,
              const int* __restrict__ count, const float4* __restrict__ pos, const uint4* __restrict__ feat_tiles,
              const float4* __restrict__ dout, int* tile_ctr, int skip_scatter, int mlp_levels,
-             int pull_max, int split, int wait_mode) {
+             int pull_max, int split, int wait_mode, float* __restrict__ mlp_part) {
   using CM = BwdCols<INP, W, H>;
   using WT = WeightTiles<INP, W, H, SPL>;
   constexpr int XC = INP + 8, HC = W + 8;
@@ -1244,10 +1246,19 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
       mbar_arrive2(&full_bar);
     }
     // ---- flush the TMEM weight-gradient accumulators: row = input unit (or the
-    // ones row = bias), column = output unit; one atomicAdd per weight per CTA
+    // ones row = bias), column = output unit. With mlp_part, each CTA stores its
+    // partial sums (every MLP parameter once, zeros if it had no tile) and
+    // k_mlp_grad_reduce adds them in CTA order: no same-address atomics from
+    // all CTAs at once (measured 25-29 us of contention), and deterministic
+    // MLP gradients. Without it: one atomicAdd per weight per CTA.
     umma::fence_after_sync();
-    if (iter > 0 && warp < 4) {
+    if (warp < 4 && (iter > 0 || mlp_part)) {
       float* gm = grad + fd.hash_params;
+      float* part = mlp_part ? mlp_part + (size_t)blockIdx.x * fd.mlp_params : nullptr;
+      auto put = [&](int idx, float val) {
+        if (part) part[idx] = iter > 0 ? val : 0.f;
+        else atomicAdd(gm + idx, val);
+      };
       auto flush = [&](int col0, int ncol, int n_out, int in, int bias_row, int w_off, int b_off) {
         for (int c = 0; c < ncol; c += 8) {
           float v[8];
@@ -1257,8 +1268,8 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
           for (int j = 0; j < 8; ++j) {
             const int o = c + j;
             if (o >= n_out) continue;
-            if (row < in) atomicAdd(gm + w_off + o * in + row, v[j]);
-            else if (row == bias_row) atomicAdd(gm + b_off + o, v[j]);
+            if (row < in) put(w_off + o * in + row, v[j]);
+            else if (row == bias_row) put(b_off + o, v[j]);
           }
         }
       };
@@ -1274,8 +1285,8 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             const int k = c + j;
-            if (k < in) atomicAdd(gm + w_off + o * in + k, v[j]);
-            else if (k == ones_col) atomicAdd(gm + b_off + o, v[j]);
+            if (k < in) put(w_off + o * in + k, v[j]);
+            else if (k == ones_col) put(b_off + o, v[j]);
           }
         }
       };
@@ -1288,6 +1299,18 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
   __syncthreads();
   if (warp == 0) umma::tmem_dealloc(tm, 256);
   TRACE_CTA(3, gtimer());
+}
+
+// MLP weight gradients: grad[i] += sum over the backward's CTAs of their partials, in CTA
+// order (thread per parameter, coalesced over the CTA-major partial rows).
+__global__ void __launch_bounds__(256) k_mlp_grad_reduce(const float* __restrict__ part, int nparts, int P,
+                                                         float* __restrict__ g) {
+  pdl_wait();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= P) return;
+  float acc = 0.f;
+  for (int c = 0; c < nparts; ++c) acc += part[(size_t)c * P + i];
+  g[i] += acc;
 }
 
 // Persistent-grid sizing hint: under the multi-object scheduler (concurrent
@@ -1402,7 +1425,7 @@ cudaError_t run_fwd(const FieldDesc& fd, const float* params, long long n, int S
 template <int INP, int W, int H, int SPL>
 cudaError_t run_bwd_s(const FieldDesc& fd, const float* params, float* grad, long long n, int S, const int* count,
                       const float4* pos, const void* feat_tiles, const float4* dout, int* tile_ctr, int split,
-                      cudaStream_t st) {
+                      float* mlp_part, size_t part_cap, cudaStream_t st) {
   // plain bf16: two CTAs (2 x 256 TMEM columns) per SM, the shared-memory
   // floor keeps a third CTA out; PRENOM_BWD_SMEM_KB / PRENOM_BWD_CARVEOUT for tuning
   static const size_t min_smem = (size_t)env_int("PRENOM_BWD_SMEM_KB", SPL ? 0 : 80) * 1024;
@@ -1432,18 +1455,24 @@ cudaError_t run_bwd_s(const FieldDesc& fd, const float* params, float* grad, lon
   static const int wait_mode = env_int("PRENOM_BWD_WAIT", kBwdWaitDefault);
   cudaError_t em = cudaMemsetAsync(tile_ctr, 0, sizeof(int), st);
   if (em != cudaSuccess) return em;
-  return launch_pdl(kern, dim3((unsigned)grid), dim3(kBwdThreads), smem, st, fd, params, grad, n, S, count, pos,
-                    reinterpret_cast<const uint4*>(feat_tiles), dout, tile_ctr, skip, mlp_levels, pull_max, split,
-                    wait_mode);
+  float* part = mlp_part && (size_t)grid * fd.mlp_params <= part_cap ? mlp_part : nullptr;
+  cudaError_t e2 = launch_pdl(kern, dim3((unsigned)grid), dim3(kBwdThreads), smem, st, fd, params, grad, n, S, count,
+                              pos, reinterpret_cast<const uint4*>(feat_tiles), dout, tile_ctr, skip, mlp_levels,
+                              pull_max, split, wait_mode, part);
+  if (e2 != cudaSuccess || !part) return e2;
+  return launch_pdl(k_mlp_grad_reduce, dim3((unsigned)((fd.mlp_params + 255) / 256)), dim3(256), 0, st,
+                    (const float*)part, (int)grid, fd.mlp_params, grad + fd.hash_params);
 }
 
 template <int INP, int W, int H>
 cudaError_t run_bwd(const FieldDesc& fd, const float* params, float* grad, long long n, int S, const int* count,
                     const float4* pos, const void* feat_tiles, const float4* dout, int* tile_ctr, int split,
-                    cudaStream_t st) {
+                    float* mlp_part, size_t part_cap, cudaStream_t st) {
   if (split)
-    return run_bwd_s<INP, W, H, 1>(fd, params, grad, n, S, count, pos, feat_tiles, dout, tile_ctr, split, st);
-  return run_bwd_s<INP, W, H, 0>(fd, params, grad, n, S, count, pos, feat_tiles, dout, tile_ctr, 0, st);
+    return run_bwd_s<INP, W, H, 1>(fd, params, grad, n, S, count, pos, feat_tiles, dout, tile_ctr, split, mlp_part,
+                                   part_cap, st);
+  return run_bwd_s<INP, W, H, 0>(fd, params, grad, n, S, count, pos, feat_tiles, dout, tile_ctr, 0, mlp_part,
+                                 part_cap, st);
 }
 
 #define PRENOM_TC_DISPATCH(FN, ...)                                                          \
@@ -1509,13 +1538,16 @@ cudaError_t launch_fwd_tc(const FieldDesc& fd, const float* params, long long n,
   PRENOM_TC_DISPATCH(run_fwd, fd, params, n, S, count, pos, feat_tiles, out, flag, tile_ctr, split, st);
 }
 
+size_t tc_mlp_part_floats(const FieldDesc& fd) { return (size_t)2 * sms() * fd.mlp_params; }
+
 cudaError_t launch_bwd_tc(const FieldDesc& fd, const float* params, float* grad, long long n, int S,
                           const int* count, const float4* pos, const void* feat_tiles, const float4* dout,
-                          int* tile_ctr, int split, cudaStream_t st) {
+                          int* tile_ctr, int split, float* mlp_part, size_t part_cap, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   if (n + kTile >= (1LL << 31)) return cudaErrorInvalidValue;  // ray_of's 32-bit slot index
   split = split_mask(split);
-  PRENOM_TC_DISPATCH(run_bwd, fd, params, grad, n, S, count, pos, feat_tiles, dout, tile_ctr, split, st);
+  PRENOM_TC_DISPATCH(run_bwd, fd, params, grad, n, S, count, pos, feat_tiles, dout, tile_ctr, split, mlp_part,
+                     part_cap, st);
 }
 
 }  // namespace prenom

@@ -453,7 +453,9 @@ cudaError_t launch_fwd_tc(const FieldDesc& fd, const float* params, long long n,
                           cudaStream_t st);
 cudaError_t launch_bwd_tc(const FieldDesc& fd, const float* params, float* grad, long long n, int S,
                           const int* count, const float4* pos, const void* feat_tiles, const float4* dout,
-                          int* tile_ctr, int split, cudaStream_t st);
+                          int* tile_ctr, int split, float* mlp_part, size_t part_cap, cudaStream_t st);
+// floats of per-CTA MLP-gradient partials launch_bwd_tc can use (else it flushes with atomics)
+size_t tc_mlp_part_floats(const FieldDesc& fd);
 cudaError_t launch_umma_gemm(int M, int N, int K, int a_mn, int b_mn, const float* A, const float* B,
                              float* D, cudaStream_t st);
 
