@@ -62,7 +62,7 @@ struct PointBatch {
     CUDA_TRY(params.ensure(P));
     CUDA_TRY(feat_t.ensure(npad * fd.in_dim));
     CUDA_TRY(dfeat_t.ensure(npad * fd.in_dim));
-    if (tc_supported(fd)) CUDA_TRY(feat_tc.ensure(tc_feature_bytes(fd, n, 1)));
+    if (tc_supported(fd)) CUDA_TRY(feat_tc.ensure(tc_feature_bytes(fd, n, 1)));  // (split-sized: fits both modes)
     CUDA_TRY(pos.ensure(npad));
     CUDA_TRY(out.ensure(npad));
     CUDA_TRY(dout.ensure(npad));
@@ -171,6 +171,7 @@ prenom_status prenom_debug_field_backward(prenom_ctx_t ctx, const prenom_field_a
   if (precision == PRENOM_MLP_BF16 || precision == PRENOM_MLP_BF16X3) {
     if (!tc_supported(fd)) return fail(PRENOM_USAGE, "arch not supported by the tensor-core path");
     const int split = precision == PRENOM_MLP_BF16X3;
+    CUDA_TRY(init_feature_tiles(fd, pb.feat_tc.p, tc_feature_bytes(fd, n, split), split, st));
     CUDA_TRY(launch_fwd_tc(fd, pb.params.p, n, 1, pb.count.p, pb.pos.p, pb.feat_tc.p, pb.out.p, pb.flag.p, pb.ctr.p,
                            split, st));
     CUDA_TRY(launch_bwd_tc(fd, pb.params.p, pb.grad.p, n, 1, pb.count.p, pb.pos.p, pb.feat_tc.p, pb.dout.p,

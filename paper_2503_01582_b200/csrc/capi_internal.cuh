@@ -300,7 +300,10 @@ inline prenom_status ensure_scratch(prenom_object_s* o, int B, int S) {
   CUDA_TRY(o->out.ensure(Npad));
   CUDA_TRY(o->dout.ensure(Npad));
   if (uses_tc(o)) {
+    unsigned char* before = o->feat_tc.p;
     CUDA_TRY(o->feat_tc.ensure(tc_feature_bytes(o->fd, (long long)N, tc_split(o))));
+    if (o->feat_tc.p != before)
+      CUDA_TRY(init_feature_tiles(o->fd, o->feat_tc.p, o->feat_tc.n, tc_split(o), o->ctx->stream));
     CUDA_TRY(o->mlp_part.ensure(tc_mlp_part_floats(o->fd)));
     if (!o->tile_ctr.p) {  // [fwd next, fwd done (self-resetting), bwd next (memset per launch), -]
       CUDA_TRY(o->tile_ctr.ensure(4));

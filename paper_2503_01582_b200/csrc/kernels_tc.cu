@@ -38,6 +38,10 @@ constexpr int kFwdSmemKbDefault = 40;
 // encode's gathers (was 57 KB/CTA padding, 196 KB carve-out, 60 KB of L1:
 // k_fwd_tc 0.195 -> 0.186 ms on cfg2)
 constexpr int kFwdCarveoutDefault = 58;
+// bf16 forward: the warp-specialised kernel (k_fwd_ws, ~31 KB per CTA), 2 CTAs in a
+// 64 KB carve-out -> 192 KB of L1 (cfg2 0.163 ms vs 0.177 for k_fwd_tc 3 x 256)
+constexpr int kFwdTsDefault = 2;
+constexpr int kFwdWsCarveout = 30;
 // split-bf16 forward (~62 KB per CTA): two CTAs of 512 threads per SM
 constexpr int kFwdSThreadsDefault = 512;
 constexpr int kFwdSCtasDefault = 2;
@@ -132,6 +136,42 @@ __device__ __forceinline__ long long next_tile(int* ctr, int* s_tile) {
   if (threadIdx.x == 0) *s_tile = atomicAdd(ctr, 1);
   __syncthreads();
   return *s_tile;
+}
+
+// Stored feature tiles (forward -> backward) use the backward's operand layout
+// [128][INP + 8] per hi / lo half: the features plus the core matrix holding the
+// ones column of [X | 1] (written once per buffer by init_feature_tiles), so the
+// backward fetches a tile with ONE bulk copy. The forward's smem tile is
+// [128][INP]; its 16 row groups go out as bulk copies into their slots.
+template <int INP, int SPL>
+__device__ __forceinline__ void store_features(uint4* feat_tiles, long long t, const unsigned char* X) {
+  constexpr int XC = INP + 8;
+  constexpr size_t kTileG = (size_t)128 * XC * 2 * (SPL ? 2 : 1);
+  unsigned char* dst = reinterpret_cast<unsigned char*>(feat_tiles) + (size_t)t * kTileG;
+#pragma unroll 1
+  for (int h = 0; h < (SPL ? 2 : 1); ++h)
+#pragma unroll 1
+    for (int rg = 0; rg < 16; ++rg)
+      umma::bulk_s2g_part(dst + h * 128 * XC * 2 + rg * (XC / 8) * 128, X + h * 128 * INP * 2 + rg * (INP / 8) * 128,
+                          INP * 16);
+  umma::bulk_commit();
+}
+
+// the ones / zero core matrices of every stored tile: hi [1, 0, ..., 0] per row, lo zeros
+__global__ void k_feature_ones(unsigned char* feat, long long ntiles, int INP, int split) {
+  const int XC = INP + 8;
+  const long long tile_bytes = 128LL * XC * 2 * (split ? 2 : 1);
+  const long long n = ntiles * 16 * 8 * (split ? 2 : 1);  // (tile, row group, row, half)
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    long long k = i;
+    const int h = split ? (int)(k & 1) : 0;
+    if (split) k >>= 1;
+    const int r = (int)(k & 7), rg = (int)((k >> 3) & 15);
+    const long long t = k >> 7;
+    uint4* dst = reinterpret_cast<uint4*>(feat + t * tile_bytes + (long long)h * 128 * XC * 2 +
+                                          (rg * (XC / 8) + INP / 8) * 128 + r * 16);
+    *dst = make_uint4(h == 0 ? 0x3F80u : 0u, 0u, 0u, 0u);
+  }
 }
 
 __device__ __forceinline__ void named_sync(int id, int n) {
@@ -289,7 +329,7 @@ __global__ void __launch_bounds__(NT) k_fwd_tc(FieldDesc fd, const float* __rest
       // stored features for the backward pass (tile-major, same core-matrix
       // layout; split mode: hi tile then lo tile), written by the TMA engine:
       // no LSU work next to the gathers
-      umma::bulk_s2g(feat_tiles + t * (kXBytes / 16), X, kXBytes);
+      store_features<INP, SPL>(feat_tiles, t, X);
     }
     wait_mma(&bar, phase);
     if (SPL) {  // the bulk store must have read X before H overwrites it
@@ -451,7 +491,7 @@ __global__ void __launch_bounds__(NT) k_fwd_ts(FieldDesc fd, const float* __rest
         umma::mma_split(tm, umma::desc_kmajor(X, INP, ks), umma::desc_kmajor(wt.w0, INP, ks), id_h, ks > 0, sp, XLO,
                         WT::kLo);
       umma::commit(&bar);
-      umma::bulk_s2g(feat_tiles + t * (kXBytes / 16), X, kXBytes);  // stored features for the backward
+      store_features<INP, SPL>(feat_tiles, t, X);  // stored features for the backward
     }
     wait_mma(&bar, phase);
     epilogue(wt.bias);
@@ -637,7 +677,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_fwd_ws(FieldDesc fd, const fl
           umma::mma_split(tm, umma::desc_kmajor(X, INP, ks), umma::desc_kmajor(wt.w0, INP, ks), id_h, ks > 0, sp, XLO,
                           WT::kLo);
         umma::commit(&bar);
-        umma::bulk_s2g(feat_tiles + t * (kXBytes / 16), X, kXBytes);  // stored features for the backward
+        store_features<INP, SPL>(feat_tiles, t, X);  // stored features for the backward
       }
       wait_mma(&bar, phase);
       if (mt == 0) {  // the layer-0 MMA and the feature store have read buffer b
@@ -883,7 +923,7 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
   constexpr uint32_t XLO = SPL ? 128 * XC * 2 + (OV ? 0 : kSlackX) : 0;
   constexpr uint32_t HLO = SPL ? 128 * HC * 2 + (OV ? 0 : kSlackH) : 0;
   constexpr uint32_t GLO = SPL ? 128 * 16 * 2 : 0;
-  constexpr uint32_t kFeatBytes = 128 * INP * 2 * (SPL ? 2 : 1);
+  constexpr uint32_t kFeatBytes = 128 * XC * 2 * (SPL ? 2 : 1);  // one stored tile (store_features)
   const bool sp_f = SPL && (split & 1), sp_d = SPL && (split & 2), sp_w = SPL && (split & 4);
   constexpr int NH = INP / 2;  // d_feature columns per half: [h*NH, (h+1)*NH)
   constexpr int LH = INP / 4;  // levels per half
@@ -1025,13 +1065,15 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
         *reinterpret_cast<uint4*>(tile + lo + umma::cm_offset(tid, col, C)) = zero_row;
       }
     };
-    auto fetch_x = [&](long long t) {  // stored bf16 features -> X (TMA), one bulk copy per 8-row group
-      const unsigned char* src = reinterpret_cast<const unsigned char*>(feat_tiles + t * (kFeatBytes / 16));
+    auto fetch_x = [&](long long t) {  // stored features [X | 1] (hi, lo) -> X: one bulk copy per half
+      const unsigned char* src = reinterpret_cast<const unsigned char*>(feat_tiles) + (size_t)t * kFeatBytes;
       umma::mbar_arrive_expect_tx(&xbar, kFeatBytes);
-      for (int rg = 0; rg < 16; ++rg) umma::bulk_g2s(X + rg * (XC / 8) * 128, src + rg * INP * 16, INP * 16, &xbar);
-      if (SPL)
-        for (int rg = 0; rg < 16; ++rg)
-          umma::bulk_g2s(X + XLO + rg * (XC / 8) * 128, src + 128 * INP * 2 + rg * INP * 16, INP * 16, &xbar);
+      if (!SPL || XLO == 128 * XC * 2) {
+        umma::bulk_g2s(X, src, kFeatBytes, &xbar);  // (hi | lo contiguous in smem too)
+      } else {
+        umma::bulk_g2s(X, src, 128 * XC * 2, &xbar);
+        umma::bulk_g2s(X + XLO, src + 128 * XC * 2, 128 * XC * 2, &xbar);
+      }
     };
     auto fetch = [&]() -> long long {
       if (tid == 0) s_tile = atomicAdd(tile_ctr, 1);
@@ -1055,8 +1097,7 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
       if (warp < 4 && valid) dpre = dout[gs];
       // ---- stored bf16 features -> X by the TMA engine (no LSU work): one
       // bulk copy per 8-row group (the X row-group stride is longer: ones column)
-      if (tid == 0 && !prefetched) fetch_x(t);
-      if (OV) set_ones(X, INP, XC, XLO);
+      if (tid == 0 && !prefetched) fetch_x(t);  // ([X | 1]: the ones come with the tile)
       umma::mbar_wait(&xbar, xphase);
       xphase ^= 1u;
       TRACE_MLP(1);
@@ -1133,7 +1174,6 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
       for (int l = H - 1; l >= 0; --l) {
         if (OV && l == 0) {  // D_{H-1} is dead: X back into its place for dW0
           if (tid == 0) fetch_x(t);
-          set_ones(X, INP, XC, XLO);
         }
         // D_l = dH_l * relu'(H_l) -> D tile
         {
@@ -1301,16 +1341,35 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
   TRACE_CTA(3, gtimer());
 }
 
-// MLP weight gradients: grad[i] += sum over the backward's CTAs of their partials, in CTA
-// order (thread per parameter, coalesced over the CTA-major partial rows).
+// MLP weight gradients: grad[i] += sum over the backward's CTAs of their partials.
+// Block = 32 parameters x 8 row groups: each thread sums every 8th CTA row (4
+// independent loads in flight), then the 8 group sums are added in fixed order
+// -- deterministic, and no 296-long dependent load chain per thread.
 __global__ void __launch_bounds__(256) k_mlp_grad_reduce(const float* __restrict__ part, int nparts, int P,
                                                          float* __restrict__ g) {
+  __shared__ float red[8][33];
   pdl_wait();
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= P) return;
-  float acc = 0.f;
-  for (int c = 0; c < nparts; ++c) acc += part[(size_t)c * P + i];
-  g[i] += acc;
+  const int c = threadIdx.x & 31, grp = threadIdx.x >> 5;
+  const int i = blockIdx.x * 32 + c;
+  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+  if (i < P) {
+    int r = grp;
+    for (; r + 24 < nparts; r += 32) {
+      a0 += part[(size_t)r * P + i];
+      a1 += part[(size_t)(r + 8) * P + i];
+      a2 += part[(size_t)(r + 16) * P + i];
+      a3 += part[(size_t)(r + 24) * P + i];
+    }
+    for (; r < nparts; r += 8) a0 += part[(size_t)r * P + i];
+  }
+  red[grp][c] = (a0 + a1) + (a2 + a3);
+  __syncthreads();
+  if (grp == 0 && i < P) {
+    float acc = red[0][c];
+#pragma unroll
+    for (int k = 1; k < 8; ++k) acc += red[k][c];
+    g[i] += acc;
+  }
 }
 
 // Persistent-grid sizing hint: under the multi-object scheduler (concurrent
@@ -1410,11 +1469,11 @@ cudaError_t run_fwd(const FieldDesc& fd, const float* params, long long n, int S
     return run_fwd_nt<INP, W, H, 256, 1>(fd, params, n, S, count, pos, feat_tiles, out, flag, tile_ctr, ctas, min_smem,
                                          carve, split, ts, st);
   }
-  static const int ts = env_int("PRENOM_FWD_TS", 0);
+  static const int ts = env_int("PRENOM_FWD_TS", kFwdTsDefault);
   static const int nt = env_int("PRENOM_FWD_THREADS", kFwdThreadsDefault) == 512 ? 512 : 256;
-  static const int ctas = std::max(1, std::min(8, env_int("PRENOM_FWD_CTAS", kFwdCtasDefault)));
+  static const int ctas = std::max(1, std::min(8, env_int("PRENOM_FWD_CTAS", ts == 2 ? 2 : kFwdCtasDefault)));
   static const size_t min_smem = (size_t)env_int("PRENOM_FWD_SMEM_KB", ts ? 0 : kFwdSmemKbDefault) * 1024;
-  static const int carve = env_int("PRENOM_FWD_CARVEOUT", kFwdCarveoutDefault);
+  static const int carve = env_int("PRENOM_FWD_CARVEOUT", ts == 2 ? kFwdWsCarveout : kFwdCarveoutDefault);
   if (nt == 512)
     return run_fwd_nt<INP, W, H, 512, 0>(fd, params, n, S, count, pos, feat_tiles, out, flag, tile_ctr, ctas, min_smem,
                                          carve, 0, ts, st);
@@ -1460,7 +1519,7 @@ cudaError_t run_bwd_s(const FieldDesc& fd, const float* params, float* grad, lon
                               pos, reinterpret_cast<const uint4*>(feat_tiles), dout, tile_ctr, skip, mlp_levels,
                               pull_max, split, wait_mode, part);
   if (e2 != cudaSuccess || !part) return e2;
-  return launch_pdl(k_mlp_grad_reduce, dim3((unsigned)((fd.mlp_params + 255) / 256)), dim3(256), 0, st,
+  return launch_pdl(k_mlp_grad_reduce, dim3((unsigned)((fd.mlp_params + 31) / 32)), dim3(256), 0, st,
                     (const float*)part, (int)grid, fd.mlp_params, grad + fd.hash_params);
 }
 
@@ -1516,7 +1575,16 @@ bool tc_supported(const FieldDesc& fd) {
 
 size_t tc_feature_bytes(const FieldDesc& fd, long long n, int split) {
   const int inp = fd.in_dim <= 16 ? 16 : 32;
-  return (size_t)((n + kTile - 1) / kTile) * kTile * inp * 2 * (split ? 2 : 1);
+  return (size_t)((n + kTile - 1) / kTile) * kTile * (inp + 8) * 2 * (split ? 2 : 1);
+}
+
+cudaError_t init_feature_tiles(const FieldDesc& fd, void* feat, size_t bytes, int split, cudaStream_t st) {
+  const int inp = fd.in_dim <= 16 ? 16 : 32;
+  const long long ntiles = (long long)(bytes / ((size_t)128 * (inp + 8) * 2 * (split ? 2 : 1)));
+  if (ntiles <= 0) return cudaSuccess;
+  k_feature_ones<<<std::max(1, std::min(4 * sms(), (int)((ntiles * 256 + 255) / 256))), 256, 0, st>>>(
+      reinterpret_cast<unsigned char*>(feat), ntiles, inp, split);
+  return cudaGetLastError();
 }
 
 // split: 0 = bf16 operands; else split-bf16 with the cross products enabled

@@ -447,6 +447,8 @@ bool tc_supported(const FieldDesc& fd);
 cudaError_t tc_bwd_trace(long long* mlp /* 64 x 16 */, long long* scat /* 64 x 4 */, long long* cta /* 1024 x 5 */);
 void tc_set_min_tiles_per_cta(int v);  // persistent-grid hint for the calling host thread (multi-object)
 size_t tc_feature_bytes(const FieldDesc& fd, long long n, int split);
+// writes the constant ones / zero core matrices of a stored-feature buffer (once per allocation)
+cudaError_t init_feature_tiles(const FieldDesc& fd, void* feat, size_t bytes, int split, cudaStream_t st);
 // tile_ctr: one device int per launch, zeroed by the launcher (dynamic tile scheduler)
 cudaError_t launch_fwd_tc(const FieldDesc& fd, const float* params, long long n, int S, const int* count,
                           const float4* pos, void* feat_tiles, float4* out, int* flag, int* tile_ctr, int split,

@@ -213,6 +213,14 @@ __device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t by
                : "memory");
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
+// bulk store without the commit (several copies, one bulk group: bulk_commit)
+__device__ __forceinline__ void bulk_s2g_part(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+
 // the source shared memory of every committed bulk store has been read
 __device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 // every committed bulk store has completed

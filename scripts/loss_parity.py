@@ -3,7 +3,7 @@ CPU oracle on the same seeded inputs, θ and Philox draws.
 
   python scripts/loss_parity.py cfg1 200                       (oracle single-threaded, ~4 min)
   PO_THREADS=16 python scripts/loss_parity.py cfg2 200         (oracle threaded, see prenom_oracle.c)
-  python scripts/loss_parity.py cfg2 200 --oracle-cache profiles/loss_parity_cfg2.json \
+  python scripts/loss_parity.py cfg2 200 --oracle-cache profiles/r1/loss_parity_cfg2.json \
       --modes fp32,bf16,bf16x3,x3m1,x3m2,x3m4 --repeats 2 --tag r2a
 
 Modes: fp32 (SIMT), bf16, bf16x3 (split bf16, all products split), x3m<mask> (split bf16 with
