@@ -677,12 +677,22 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_fwd_ws(FieldDesc fd, const fl
           umma::mma_split(tm, umma::desc_kmajor(X, INP, ks), umma::desc_kmajor(wt.w0, INP, ks), id_h, ks > 0, sp, XLO,
                           WT::kLo);
         umma::commit(&bar);
-        store_features<INP, SPL>(feat_tiles, t, X);  // stored features for the backward
+      }
+      // stored features for the backward: the lanes of MLP warp 0 issue one row-group
+      // copy each (into the [X | 1] slots of the stored tile), in parallel
+      constexpr int XCg = INP + 8;
+      if (mt < 32 && mt < 16 * (SPL ? 2 : 1)) {
+        const int h = mt >> 4, rg = mt & 15;
+        unsigned char* dst = reinterpret_cast<unsigned char*>(feat_tiles) + (size_t)t * (128 * XCg * 2 * (SPL ? 2 : 1)) +
+                             h * 128 * XCg * 2 + rg * (XCg / 8) * 128;
+        umma::bulk_s2g_part(dst, X + h * 128 * INP * 2 + rg * (INP / 8) * 128, INP * 16);
+        umma::bulk_commit();
       }
       wait_mma(&bar, phase);
-      if (mt == 0) {  // the layer-0 MMA and the feature store have read buffer b
+      if (mt < 32) {  // the layer-0 MMA and the feature stores have read buffer b
         umma::bulk_wait_read();
-        umma::mbar_arrive_plain(&empty[b]);
+        __syncwarp();
+        if (mt == 0) umma::mbar_arrive_plain(&empty[b]);
       }
       epilogue(wt.bias);
       for (int l = 1; l < H; ++l) {
@@ -720,7 +730,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_fwd_ws(FieldDesc fd, const fl
       }
       mlp_sync();  // the accumulator is free for the next tile's layer 0
     }
-    if (mt == 0) umma::bulk_wait_all();
+    if (mt < 32) umma::bulk_wait_all();
   }
   __syncthreads();
   tile_sched_exit(tile_ctr);
