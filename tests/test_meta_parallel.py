@@ -126,3 +126,28 @@ def test_reptile_allreduce_two_gloo_ranks(oracle, tmp_path):
     meta_train(eng1, 4, MetaConfig(N=1, q=2, beta=0.3, seed=9, tasks_per_step=4))
     mean_adapted = np.mean([eng1.adapted[t] for t in range(4)], axis=0).astype(np.float32)
     np.testing.assert_allclose(eng1.theta, oracle.reptile_update(theta, mean_adapted, 0.3), rtol=1e-5, atol=1e-7)
+
+
+def test_bench_gpus_flag_spawns_ranks(monkeypatch):
+    """`bench.py --gpus N` outside torchrun re-executes itself under torch.distributed.run with N
+    ranks on 127.0.0.1; inside a launch the rank count must equal --gpus (fails loudly)."""
+    import subprocess
+    import sys
+
+    import bench
+
+    calls = []
+    monkeypatch.setattr(subprocess, "call", lambda cmd: calls.append(cmd) or 0)
+    monkeypatch.delenv("WORLD_SIZE", raising=False)
+    monkeypatch.delenv("TORCHELASTIC_RUN_ID", raising=False)
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "4", "--workload", "cfg4", "--steps", "3"])
+    with pytest.raises(SystemExit) as e:
+        bench.main()
+    assert e.value.code == 0 and len(calls) == 1
+    cmd = calls[0]
+    assert cmd[1:3] == ["-m", "torch.distributed.run"] and "--nproc-per-node=4" in cmd
+    assert "--master-addr=127.0.0.1" in cmd and cmd[-6:] == ["--gpus", "4", "--workload", "cfg4", "--steps", "3"]
+    monkeypatch.setenv("WORLD_SIZE", "2")
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "4"])
+    with pytest.raises(SystemExit, match="WORLD_SIZE=2"):
+        bench.main()
