@@ -379,6 +379,9 @@ prenom_status prenom_debug_field_backward(prenom_ctx_t ctx, const prenom_field_a
  * (cta may be NULL) per CTA cta[1024][5]: globaltimer ns at entry, after the
  * prologue, at the end of its tiles and at exit, and its tile count. */
 prenom_status prenom_debug_bwd_trace(prenom_ctx_t ctx, int64_t* mlp, int64_t* scatter, int64_t* cta);
+/* L2 read bandwidth probe: an L2-resident buffer of mbytes MiB re-read reps times in one
+ * launch; *gbs = bytes read / time (the L2 roofline denominator, measured on the box). */
+prenom_status prenom_debug_l2_read(prenom_ctx_t ctx, int mbytes, int reps, double* gbs);
 /* adam_step (field.cpp:295-310) on n floats; *step in/out. */
 prenom_status prenom_debug_adam(prenom_ctx_t ctx, size_t n, float* params, const float* grads,
                                 float* m, float* v, int64_t* step, float lr, float beta1,

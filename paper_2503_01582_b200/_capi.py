@@ -153,7 +153,7 @@ EXPORTED = [
     "prenom_debug_field_backward", "prenom_debug_adam", "prenom_debug_sample_rays",
     "prenom_debug_batch_loss", "prenom_debug_generate_rays", "prenom_debug_umma_gemm",
     "prenom_debug_marching_cubes", "prenom_debug_mesh_get", "prenom_mc_case_triangles",
-    "prenom_debug_bwd_trace",
+    "prenom_debug_bwd_trace", "prenom_debug_l2_read",
 ]
 
 _lib = None
@@ -255,6 +255,7 @@ def _declare(lib):
         "prenom_debug_mesh_get": (i32, [P, f32p, i32p]),
         "prenom_mc_case_triangles": (i32, [i32, i32p]),
         "prenom_debug_bwd_trace": (i32, [P, i64p, i64p, i64p]),
+        "prenom_debug_l2_read": (i32, [P, i32, i32, C.POINTER(C.c_double)]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(lib, name)

@@ -457,4 +457,21 @@ prenom_status prenom_debug_bwd_trace(prenom_ctx_t ctx, int64_t* mlp, int64_t* sc
                         reinterpret_cast<long long*>(cta)));
   return PRENOM_OK;
 }
+// L2 read bandwidth probe (the L2 peak is measured on the box): one launch
+// re-reads an L2-resident buffer `reps` times (float4, grid-stride), timed with events.
+prenom_status prenom_debug_l2_read(prenom_ctx_t ctx, int mbytes, int reps, double* gbs) {
+  if (!ctx || !gbs || mbytes < 1 || reps < 1) return fail(PRENOM_USAGE, "bad arguments");
+  CUDA_TRY(cudaSetDevice(ctx->device));
+  const size_t n4 = (size_t)mbytes * (1 << 20) / 16;
+  DevBuf<float4> buf;
+  DevBuf<float> sink;
+  CUDA_TRY(buf.ensure(n4));
+  CUDA_TRY(sink.ensure(1 << 20));
+  CUDA_TRY(cudaMemsetAsync(buf.p, 0, n4 * 16, ctx->stream));
+  float ms = 0.f;
+  CUDA_TRY(launch_l2_read(buf.p, n4, 1, sink.p, ctx->stream, nullptr));  // warm: lines into L2
+  CUDA_TRY(launch_l2_read(buf.p, n4, reps, sink.p, ctx->stream, &ms));
+  *gbs = (double)n4 * 16.0 * reps / (ms * 1e-3) / 1e9;
+  return PRENOM_OK;
+}
 }  // extern "C"

@@ -199,6 +199,32 @@ cudaError_t launch_reptile_delta_sum(size_t n, const float* meta, const float* c
   return cudaGetLastError();
 }
 
+// L2 read probe: every thread sums float4s of a grid-stride walk over the buffer, reps times
+__global__ void k_l2_read(const float4* __restrict__ buf, size_t n4, int reps, float* sink) {
+  float acc = 0.f;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (int r = 0; r < reps; ++r)
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+      const float4 v = __ldcg(buf + i);
+      acc += (v.x + v.y) + (v.z + v.w);
+    }
+  sink[(blockIdx.x * blockDim.x + threadIdx.x) & ((1 << 20) - 1)] = acc;
+}
+
+cudaError_t launch_l2_read(const float4* buf, size_t n4, int reps, float* sink, cudaStream_t st, float* ms) {
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a, st);
+  k_l2_read<<<num_sms() * 8, 512, 0, st>>>(buf, n4, reps, sink);
+  cudaEventRecord(b, st);
+  cudaError_t e = cudaEventSynchronize(b);
+  if (ms) cudaEventElapsedTime(ms, a, b);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
+
 cudaError_t launch_reptile_update(size_t n, float* meta, const float* adapted, float beta, cudaStream_t st) {
   k_reptile_update<<<num_sms() * 4, 256, 0, st>>>(n, meta, adapted, beta);
   return cudaGetLastError();

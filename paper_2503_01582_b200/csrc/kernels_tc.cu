@@ -1352,32 +1352,30 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
 }
 
 // MLP weight gradients: grad[i] += sum over the backward's CTAs of their partials.
-// Block = 32 parameters x 8 row groups: each thread sums every 8th CTA row (4
-// independent loads in flight), then the 8 group sums are added in fixed order
-// -- deterministic, and no 296-long dependent load chain per thread.
-__global__ void __launch_bounds__(256) k_mlp_grad_reduce(const float* __restrict__ part, int nparts, int P,
-                                                         float* __restrict__ g) {
-  __shared__ float red[8][33];
+// Block = 32 parameters x 32 row groups: each thread sums every 32nd CTA row (a
+// short, independent load chain: the partials were just written and sit in L2),
+// then the 32 group sums are added in fixed order -- deterministic.
+__global__ void __launch_bounds__(1024) k_mlp_grad_reduce(const float* __restrict__ part, int nparts, int P,
+                                                          float* __restrict__ g) {
+  __shared__ float red[32][33];
   pdl_wait();
   const int c = threadIdx.x & 31, grp = threadIdx.x >> 5;
   const int i = blockIdx.x * 32 + c;
-  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+  float a0 = 0.f, a1 = 0.f;
   if (i < P) {
     int r = grp;
-    for (; r + 24 < nparts; r += 32) {
+    for (; r + 32 < nparts; r += 64) {
       a0 += part[(size_t)r * P + i];
-      a1 += part[(size_t)(r + 8) * P + i];
-      a2 += part[(size_t)(r + 16) * P + i];
-      a3 += part[(size_t)(r + 24) * P + i];
+      a1 += part[(size_t)(r + 32) * P + i];
     }
-    for (; r < nparts; r += 8) a0 += part[(size_t)r * P + i];
+    if (r < nparts) a0 += part[(size_t)r * P + i];
   }
-  red[grp][c] = (a0 + a1) + (a2 + a3);
+  red[grp][c] = a0 + a1;
   __syncthreads();
   if (grp == 0 && i < P) {
     float acc = red[0][c];
-#pragma unroll
-    for (int k = 1; k < 8; ++k) acc += red[k][c];
+#pragma unroll 8
+    for (int k = 1; k < 32; ++k) acc += red[k][c];
     g[i] += acc;
   }
 }
@@ -1529,7 +1527,7 @@ cudaError_t run_bwd_s(const FieldDesc& fd, const float* params, float* grad, lon
                               pos, reinterpret_cast<const uint4*>(feat_tiles), dout, tile_ctr, skip, mlp_levels,
                               pull_max, split, wait_mode, part);
   if (e2 != cudaSuccess || !part) return e2;
-  return launch_pdl(k_mlp_grad_reduce, dim3((unsigned)((fd.mlp_params + 31) / 32)), dim3(256), 0, st,
+  return launch_pdl(k_mlp_grad_reduce, dim3((unsigned)((fd.mlp_params + 31) / 32)), dim3(1024), 0, st,
                     (const float*)part, (int)grid, fd.mlp_params, grad + fd.hash_params);
 }
 

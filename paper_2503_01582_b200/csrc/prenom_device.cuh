@@ -375,6 +375,7 @@ cudaError_t launch_reptile_apply(size_t n, float* meta, const float* delta, floa
 cudaError_t launch_reptile_delta_sum(size_t n, const float* meta, const float* const* adapted_dev, int k, float* out,
                                      cudaStream_t st);
 cudaError_t launch_reptile_update(size_t n, float* meta, const float* adapted, float beta, cudaStream_t st);
+cudaError_t launch_l2_read(const float4* buf, size_t n4, int reps, float* sink, cudaStream_t st, float* ms);
 // ---- isosurface (mesh.cu)
 template <typename T>
 struct MeshBuf {

@@ -48,9 +48,23 @@ for _ in range(10):
 e.record()
 torch.cuda.synchronize()
 res["hbm_copy_1GiB"] = round(2 * big.numel() * 4 * 10 / (s.elapsed_time(e) / 1e3) / 1e9, 1)
-res["l2_peak_gbs"] = max(max(res["copy"].values()), max(res["read"].values()))
+# the library's own probe: one launch re-reading an L2-resident buffer (no launch overheads)
+import ctypes as C  # noqa: E402
+import os  # noqa: E402
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2503_01582_b200 import Context  # noqa: E402
+
+ctx = Context(0)
+res["kernel_read"] = {}
+for mb in (16, 32, 48, 64, 96):
+    g = C.c_double()
+    ctx.lib.prenom_debug_l2_read(ctx.h, mb, 50, C.byref(g))
+    res["kernel_read"][mb] = round(g.value, 1)
+res["l2_peak_gbs"] = max(max(res["copy"].values()), max(res["read"].values()), max(res["kernel_read"].values()))
 res["how"] = ("torch copy_ (read+write bytes) and sum (read bytes) of L2-resident fp32 buffers, 400 back-to-back "
-              "launches after 20 warm-up, CUDA events; l2_peak_gbs = the best of all sizes")
+              "launches after 20 warm-up; prenom_debug_l2_read: one launch re-reading an L2-resident buffer 50x "
+              "(float4 __ldcg, 8 CTAs x 512 threads per SM); CUDA events; l2_peak_gbs = the best of all")
 line = json.dumps(res)
 print(line)
 if tag:

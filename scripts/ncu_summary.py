@@ -23,7 +23,7 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
         "launch__shared_mem_per_block_dynamic", "lts__t_sectors_srcunit_tex_op_red.sum",
         "l1tex__t_sector_hit_rate.pct", "lts__t_sector_hit_rate.pct", "smsp__inst_executed.sum",
-        "lts__t_bytes.sum", "sm__pipe_tensor_op_hmma_cycles_active.avg.pct_of_peak_sustained_active"]
+        "lts__t_sectors.sum"]
 
 
 def short(name):
@@ -54,13 +54,21 @@ def raw_rows(path):
             yield dict(zip(hdr, r)), dict(zip(hdr, rows[1]))
 
 
-def raw(path, header):
+def raw(path, header, l2_peak_gbs=None):
     print(header)
     for d, u in raw_rows(path):
         print(f"\n{short(d['Kernel Name'])}")
         for k in KEYS:
             if k in d:
                 print(f"  {k:70s} {d[k]:>18s} {u.get(k, '')}")
+        if "lts__t_sectors.sum" in d:  # L2 bytes and rate (32 B sectors)
+            t = float(d["gpu__time_duration.sum"].replace(",", "")) * (1e-3 if u["gpu__time_duration.sum"] == "ns" else 1)
+            b = float(d["lts__t_sectors.sum"].replace(",", "")) * 32
+            rate = b / (t * 1e-6) / 1e9
+            line = f"  {'L2 bytes (lts__t_sectors x 32) / rate':70s} {b / 1e6:>14.1f} MB {rate:>9.1f} GB/s"
+            if l2_peak_gbs:
+                line += f"  ({rate / l2_peak_gbs:.2f} of the measured L2 peak {l2_peak_gbs:.0f} GB/s)"
+            print(line)
 
 
 def traffic(path, tag):
@@ -84,6 +92,6 @@ if __name__ == "__main__":
     if mode == "launches":
         launches(sys.argv[2], int(sys.argv[3]), sys.argv[4])
     elif mode == "raw":
-        raw(sys.argv[2], sys.argv[3])
+        raw(sys.argv[2], sys.argv[3], float(sys.argv[4]) if len(sys.argv) > 4 else None)
     else:
         traffic(sys.argv[2], sys.argv[3])
