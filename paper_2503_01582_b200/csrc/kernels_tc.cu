@@ -1090,15 +1090,17 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
       named_sync(1, kMlpThreads);
       return s_tile;
     };
-    // (overlay) the next tile's features are prefetched into X as soon as this
-    // tile's dW0 has read it, so only the first tile waits for its TMA
+    // The next tile is claimed at the start of this one (the atomic's result is
+    // only consumed mid-tile, so its latency is hidden) and its features are
+    // prefetched into X by a second thread as soon as this tile's dW0 has read X:
+    // only the first tile waits for its copy. (knob 3 keeps the plain loop.)
+    const bool pf = skip_scatter != 3;
     bool prefetched = false;
+    long long claim_reg = 0;
     for (long long t = fetch(); t < ntiles; ++iter) {
       const long long tile0 = t * kTile;
       TRACE_MLP(0);
-      // (overlay) claim the next tile now: its index is known long before this
-      // tile's chain ends, so neither the claim nor its feature copy is on the chain
-      if (OV && tid == 0) s_next = atomicAdd(tile_ctr, 1);
+      if (pf && tid == 0) claim_reg = atomicAdd(tile_ctr, 1);
       const long long gs = tile0 + row;
       const bool valid = gs < n_total && __ldg(count + ray_of(gs, S)) > 0;
       // upstream gradient of this row, loaded now: its latency would otherwise sit
@@ -1204,6 +1206,7 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
           xphase ^= 1u;
           TRACE_MLP(9);
         }
+        if (l == 0 && tid == 0) s_next = (int)claim_reg;  // published by the barrier below
         mlp_sync_for_mma();
         if (tid == 0) {
           const int dwc = l == 0 ? CM::kDW0 : CM::kDWl + (H - 1 - l) * (W + 8);
@@ -1215,7 +1218,7 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
             umma::mma_split_terms(tm + dwc, umma::desc_mnmajor(Ht[l], HC, ks), umma::desc_mnmajor(prev, pc, ks),
                                   umma::idesc_bf16(64, pc, true, true), (iter > 0 || ks > 0), sp_w && !(split & 32),
                                   sp_w && !(split & 16), HLO, plo);
-          if (OV && l == 0) umma::commit(&xfree);  // dW0 is the last reader of X
+          if (pf && l == 0) umma::commit(&xfree);  // dW0 is the last reader of X
           if (l > 0) {
             for (int ks = 0; ks < W / 16; ++ks)
               umma::mma_split(tr, umma::desc_kmajor(Ht[l], HC, ks), umma::desc_mnmajor(wt.wl[l - 1], W, ks),
@@ -1235,7 +1238,7 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
             mbar_arrive(&full_bar);
           }
         }
-        if (OV && l == 0 && tid == 32) {
+        if (pf && l == 0 && tid == 32) {
           // a second thread copies the next tile's features into X once dW0 is done with
           // it, in parallel with the issuing thread's dX / slot hand-over
           umma::mbar_wait(&xfree, xfphase);
@@ -1279,7 +1282,7 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
         }
       }
       // next tile: claimed (and its features prefetched) by the issuing thread
-      if (OV && skip_scatter != 3) {
+      if (pf) {
         named_sync(1, kMlpThreads);
         t = s_next;
         prefetched = true;

@@ -151,3 +151,48 @@ def test_bench_gpus_flag_spawns_ranks(monkeypatch):
     monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "4"])
     with pytest.raises(SystemExit, match="WORLD_SIZE=2"):
         bench.main()
+
+
+def _objects_rank_main(rank, world, port, out_path):
+    """One rank of the object-sharded path (cfg3/cfg5): LPT shard of the objects, each trained
+    independently (oracle objects stand in for the GPU ones), per-object losses gathered."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle.pyoracle import Oracle
+
+    orc = Oracle()
+    tasks = make_tasks()
+    archs = [ARCH, FieldArch(hash_levels=4, log2_table_size=9, hidden_width=8, hidden_layers=2), ARCH,
+             FieldArch(hash_levels=2, log2_table_size=7, hidden_width=4, hidden_layers=1)]
+    mine = shard_lpt([step_cost(a, CFG.rays_per_iter, CFG.samples_per_ray) for a in archs], world)[rank]
+    losses = torch.zeros(len(archs), 3, dtype=torch.float64)
+    for i in mine:
+        sc = tasks[i]
+        theta = (np.random.default_rng(40 + i).standard_normal(archs[i].param_count()) * 0.1).astype(np.float32)
+        ob = orc.object_create(archs[i], theta, None, 8, 70 + i, CFG.to_c(), sc.box_min, sc.box_max)
+        ob.set_frames(sc.cams, sc.rgb, sc.depth, sc.mask, 1, sc.obj_pose)
+        losses[i] = torch.tensor([s["total"] for s in ob.train_step(3)], dtype=torch.float64)
+    dist.all_reduce(losses)  # every object lives on exactly one rank: the sum is a gather
+    if rank == 0:
+        np.save(out_path, losses.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_object_sharding_two_gloo_ranks(oracle, tmp_path):
+    """Objects are independent (mapper.cpp:572-585): LPT-sharding them over 2 ranks and gathering
+    their losses gives exactly the single-process per-object losses -- no data-path collective."""
+    out = str(tmp_path / "losses.npy")
+    port = 30500 + os.getpid() % 1000
+    mp.spawn(_objects_rank_main, args=(2, port, out), nprocs=2, join=True)
+    got = np.load(out)
+    tasks = make_tasks()
+    archs = [ARCH, FieldArch(hash_levels=4, log2_table_size=9, hidden_width=8, hidden_layers=2), ARCH,
+             FieldArch(hash_levels=2, log2_table_size=7, hidden_width=4, hidden_layers=1)]
+    assert sorted(i for s in shard_lpt([step_cost(a, 16, 8) for a in archs], 2) for i in s) == [0, 1, 2, 3]
+    for i, sc in enumerate(tasks):
+        theta = (np.random.default_rng(40 + i).standard_normal(archs[i].param_count()) * 0.1).astype(np.float32)
+        ob = oracle.object_create(archs[i], theta, None, 8, 70 + i, CFG.to_c(), sc.box_min, sc.box_max)
+        ob.set_frames(sc.cams, sc.rgb, sc.depth, sc.mask, 1, sc.obj_pose)
+        want = [s["total"] for s in ob.train_step(3)]
+        assert np.array_equal(got[i], want), (i, got[i], want)
