@@ -396,6 +396,7 @@ prenom_status prenom_debug_generate_rays(prenom_object_t o, int frame, int64_t s
   if (frame < 0 || frame >= (int)o->frames.size()) return fail(PRENOM_USAGE, "frame index out of range");
   CUDA_TRY(cudaSetDevice(o->ctx->device));
   const int B = o->cfg.rays_per_iter;
+  STATUS_TRY(drop_prefetch(o));
   STATUS_TRY(ensure_scratch(o, B, o->cfg.samples_per_ray));
   const RaySource src = frame_source(o, frame);
   if (src.n_obj_px == 0) return fail(PRENOM_DATA, "generate_rays: no object pixels");

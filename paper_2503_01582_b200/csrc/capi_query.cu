@@ -11,6 +11,7 @@ prenom_status prenom_render(prenom_object_t o, int n_rays, const float* origins,
   if (!o || !origins || !dirs) return fail(PRENOM_USAGE, "NULL argument");
   if (n_rays < 1) return fail(PRENOM_USAGE, "n_rays must be >= 1");
   CUDA_TRY(cudaSetDevice(o->ctx->device));
+  STATUS_TRY(drop_prefetch(o));  // render reuses the sample buffers a prefetched step would read
   const int S = o->cfg.samples_per_ray;
   STATUS_TRY(ensure_scratch(o, n_rays, S));
   cudaStream_t st = o->ctx->stream;

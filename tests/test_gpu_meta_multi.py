@@ -115,12 +115,12 @@ def test_streaming_async_steps_equal_train_step(ctx):
         b.wait_stats(12345)
 
 
-@pytest.mark.parametrize("mutation", ["upload_new_pixels", "set_seed", "restore", "set_grid"])
+@pytest.mark.parametrize("mutation", ["upload_new_pixels", "set_seed", "restore", "set_grid", "render"])
 def test_pending_prefetch_is_dropped_by_state_changes(ctx, mutation):
     """A step enqueued with prefetch_next samples step t+1 ahead on the sampling stream. A call
     that changes what step t+1 must sample -- new pixels for its keyframe, a new seed, a
     checkpoint restore, a new sampling grid -- drops that prefetch, so the step equals the same
-    sequence run without any prefetch."""
+    sequence run without any prefetch; so does a render, which reuses the sample buffers."""
     sc = tasks()[1]
     grid = scenes.occupancy_prior(sc.boxes, R=16)
     cfg = TrainConfig(rays_per_iter=128, samples_per_ray=32, prior_sampling=1, grid_refresh_every=0)
@@ -143,6 +143,10 @@ def test_pending_prefetch_is_dropped_by_state_changes(ctx, mutation):
             o.set_seed(99)
         elif mutation == "restore":
             o.restore(ck)
+        elif mutation == "render":  # reuses the sample buffers; must not leave the prefetch corrupted
+            orig = np.array([[0.0, 0.0, -2.0], [0.3, -0.2, 2.0]], np.float32)
+            dirs = np.array([[0.0, 0.0, 1.0], [0.0, 0.0, -1.0]], np.float32)
+            o.render(orig, dirs)
         else:
             o.set_grid(new_grid)
 
