@@ -1,17 +1,11 @@
-# round-2 evidence session: full GPU suite, profile of the headline, other workloads, L2 peak, trace
 set -x
 mkdir -p gpurun_out
-T=${T:-r2m}
-timeout 2400 python -m pytest tests -q -m gpu > gpurun_out/${T}_gputests.log 2>&1
-python scripts/measure_l2.py ${T} > gpurun_out/${T}_l2.log 2>&1
-timeout 1500 bash scripts/profile.sh ${T} --mlp bf16x3 > gpurun_out/${T}_profile.log 2>&1
-python scripts/bwd_trace.py bf16x3 gpurun_out/${T}_trace_x3.json > gpurun_out/${T}_trace.log 2>&1
-mkdir -p gpurun_out/${T}_workloads
-for w in cfg1 cfg3 cfg4 cfg5; do
-  timeout 900 python bench.py --workload $w --steps 50 --warmup 5 > gpurun_out/${T}_workloads/$w.json 2> gpurun_out/${T}_workloads/$w.err
+T=r2n
+B="timeout 300 python bench.py --steps 30 --warmup 5 --no-cpu-baseline --e2e-steps 0 --steady-steps 0 --mlp bf16x3"
+timeout 1200 python -m pytest tests/test_split_bf16.py tests/test_gpu_meta_multi.py -x -q -m gpu > gpurun_out/${T}_tests.log 2>&1
+for i in 1 2; do
+  $B > gpurun_out/${T}_x3_pipe_$i.log 2>&1
+  PRENOM_LIB=paper_2503_01582_b200/_lib/variants/libprenom_nopipe.so $B > gpurun_out/${T}_x3_nopipe_$i.log 2>&1
 done
-timeout 600 python bench.py --mlp bf16 --steps 100 --warmup 10 --no-cpu-baseline > gpurun_out/${T}_workloads/cfg2_bf16.json 2> gpurun_out/${T}_workloads/cfg2_bf16.err
-timeout 600 python bench.py --mlp fp32 --steps 50 --warmup 5 --no-cpu-baseline --e2e-steps 0 > gpurun_out/${T}_workloads/cfg2_fp32.json 2> gpurun_out/${T}_workloads/cfg2_fp32.err
-timeout 600 python bench.py --impl reference --steps 5 --warmup 1 > gpurun_out/${T}_reference.json 2> gpurun_out/${T}_reference.err
-python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${T}_smoke.log 2>&1
+python scripts/bwd_trace.py bf16x3 gpurun_out/${T}_trace_x3.json > gpurun_out/${T}_trace.log 2>&1
 echo done
