@@ -222,27 +222,12 @@ __device__ __forceinline__ uint64_t epi_relu_gate(uint32_t tm, const float* bias
   constexpr int NH = N / MG;
   static_assert(NH % 8 == 0 && NH <= 64, "8-column TMEM loads, 64-bit gate");
   uint64_t gate = 0;
-  // TMEM loads one chunk ahead: each tcgen05.wait::ld overlaps the previous chunk's math
-  // (PRENOM_NO_EPI_PIPE: load, wait, compute per chunk -- A/B builds)
-#ifdef PRENOM_NO_EPI_PIPE
-  constexpr bool kPipe = false;
-#else
-  constexpr bool kPipe = true;
-#endif
-  float vb[2][8];
-  if (kPipe) {
-    umma::tmem_ld8(umma::taddr(tm, 32 * q, half * NH), vb[0]);
-    umma::tmem_wait_ld();
-  }
 #pragma unroll
   for (int c = 0; c < NH; c += 8) {
     const int col = half * NH + c;
-    if (kPipe && c + 8 < NH) umma::tmem_ld8(umma::taddr(tm, 32 * q, col + 8), vb[((c >> 3) + 1) & 1]);
-    if (!kPipe) {
-      umma::tmem_ld8(umma::taddr(tm, 32 * q, col), vb[(c >> 3) & 1]);
-      umma::tmem_wait_ld();
-    }
-    const float* v = vb[(c >> 3) & 1];
+    float v[8];
+    umma::tmem_ld8(umma::taddr(tm, 32 * q, col), v);
+    umma::tmem_wait_ld();
     uint32_t pk[4], pl[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -258,7 +243,6 @@ __device__ __forceinline__ uint64_t epi_relu_gate(uint32_t tm, const float* bias
     }
     *reinterpret_cast<uint4*>(tile + umma::cm_offset(row, col, C)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
     if (LO) *reinterpret_cast<uint4*>(tile + LO + umma::cm_offset(row, col, C)) = make_uint4(pl[0], pl[1], pl[2], pl[3]);
-    if (kPipe && c + 8 < NH) umma::tmem_wait_ld();
   }
   return gate;
 }
@@ -1205,29 +1189,15 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
         // D_l = dH_l * relu'(H_l) -> D tile
         {
           constexpr int NHD = W / kMG;
-#ifdef PRENOM_NO_EPI_PIPE
-          constexpr bool kPipe = false;
-#else
-          constexpr bool kPipe = true;
-#endif
-          float vb[2][8];  // TMEM loads one chunk ahead (as in epi_relu_gate)
-          if (kPipe) {
-            umma::tmem_ld8(umma::taddr(tr, 32 * q, half * NHD), vb[0]);
-            umma::tmem_wait_ld();
-          }
 #pragma unroll
           for (int c = 0; c < NHD; c += 8) {
             const int col = half * NHD + c;
-            if (kPipe && c + 8 < NHD) umma::tmem_ld8(umma::taddr(tr, 32 * q, col + 8), vb[((c >> 3) + 1) & 1]);
-            if (!kPipe) {
-              umma::tmem_ld8(umma::taddr(tr, 32 * q, col), vb[(c >> 3) & 1]);
-              umma::tmem_wait_ld();
-            }
-            float* v = vb[(c >> 3) & 1];
+            float v[8];
+            umma::tmem_ld8(umma::taddr(tr, 32 * q, col), v);
+            umma::tmem_wait_ld();
 #pragma unroll
             for (int j = 0; j < 8; ++j) v[j] = (gate[l] >> (c + j)) & 1ull ? v[j] : 0.f;
             umma::st_row8_split(Ht[l], row, col, HC, v, HLO);  // D_l in place of H_l
-            if (kPipe && c + 8 < NHD) umma::tmem_wait_ld();
           }
         }
         if (OV && l == 0) {
