@@ -1,11 +1,9 @@
+# final-state validation: the driver's commands (GPU test suite, smoke, default bench, reference arm)
 set -x
 mkdir -p gpurun_out
-T=r2n
-B="timeout 300 python bench.py --steps 30 --warmup 5 --no-cpu-baseline --e2e-steps 0 --steady-steps 0 --mlp bf16x3"
-timeout 1200 python -m pytest tests/test_split_bf16.py tests/test_gpu_meta_multi.py -x -q -m gpu > gpurun_out/${T}_tests.log 2>&1
-for i in 1 2; do
-  $B > gpurun_out/${T}_x3_pipe_$i.log 2>&1
-  PRENOM_LIB=paper_2503_01582_b200/_lib/variants/libprenom_nopipe.so $B > gpurun_out/${T}_x3_nopipe_$i.log 2>&1
-done
-python scripts/bwd_trace.py bf16x3 gpurun_out/${T}_trace_x3.json > gpurun_out/${T}_trace.log 2>&1
+T=${T:-r2o}
+timeout 2400 python -m pytest tests -q -m gpu > gpurun_out/${T}_gputests.log 2>&1
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${T}_smoke.log 2>&1
+timeout 900 python bench.py > gpurun_out/${T}_bench_default.json 2> gpurun_out/${T}_bench_default.err
+timeout 900 python bench.py --impl reference --steps 5 --warmup 1 > gpurun_out/${T}_reference.json 2> gpurun_out/${T}_reference.err
 echo done
