@@ -547,15 +547,15 @@ __global__ void __launch_bounds__(NT) k_fwd_ts(FieldDesc fd, const float* __rest
 // mbarriers); 4 MLP warps (one row per thread: TMEM lane quadrant = warp % 4)
 // issue the MMAs, run the epilogues through TMEM and write (sigma, rgb).
 // Tiles are claimed one ahead by the encode leader.
-constexpr int kWsEncWarps = 16;
-constexpr int kWsThreads = (kWsEncWarps + 4) * 32;
-
-template <int INP, int W, int H, int SPL>
-__global__ void __launch_bounds__(kWsThreads, 2) k_fwd_ws(FieldDesc fd, const float* __restrict__ params, long long n_total,
+// NE encode warps (a multiple of 4: NE/4 threads per sample), MINB CTAs per SM.
+template <int INP, int W, int H, int SPL, int NE = 16, int MINB = 2>
+__global__ void __launch_bounds__((NE + 4) * 32, MINB) k_fwd_ws(FieldDesc fd, const float* __restrict__ params, long long n_total,
                                                     int S, const int* __restrict__ count, const float4* __restrict__ pos,
                                                     uint4* __restrict__ feat_tiles, float4* __restrict__ out, int* flag,
                                                     int* tile_ctr, int split) {
   using WT = WeightTiles<INP, W, H, SPL>;
+  constexpr int kWsEncWarps = NE;
+  constexpr int kWsThreads = (NE + 4) * 32;
   constexpr int kEnc = kWsEncWarps * 32;
   constexpr int TPS = kEnc / 128;
   constexpr uint32_t XLO = SPL ? 128 * INP * 2 : 0;
@@ -1430,13 +1430,19 @@ template <int INP, int W, int H, int NT, int SPL>
 cudaError_t run_fwd_nt(const FieldDesc& fd, const float* params, long long n, int S, const int* count,
                        const float4* pos, void* feat_tiles, float4* out, int* flag, int* tile_ctr, int ctas,
                        size_t min_smem, int carveout, int split, int ts, cudaStream_t st) {
-  // ts: 1 = TMEM activations (k_fwd_ts), 2 = + warp-specialised encode (k_fwd_ws, fixed shape)
-  auto kern = ts == 2 ? k_fwd_ws<INP, W, H, SPL> : ts ? k_fwd_ts<INP, W, H, NT, SPL> : k_fwd_tc<INP, W, H, NT, SPL>;
-  const size_t smem = std::max<size_t>(ts == 2 ? fwd_ts_smem<INP, W, H, SPL>() + 128 * INP * 2 * (SPL ? 2 : 1)
+  // ts: 1 = TMEM activations (k_fwd_ts), 2 = + warp-specialised encode (k_fwd_ws: 16 encode warps,
+  // 2 CTAs/SM); 3 / 4 / 5 = k_fwd_ws with 28 x 1, 12 x 2, 24 x 1 (encode warps x CTAs/SM)
+  auto kern = ts == 2   ? k_fwd_ws<INP, W, H, SPL>
+              : ts == 3 ? k_fwd_ws<INP, W, H, SPL, 28, 1>
+              : ts == 4 ? k_fwd_ws<INP, W, H, SPL, 12, 2>
+              : ts == 5 ? k_fwd_ws<INP, W, H, SPL, 24, 1>
+              : ts      ? k_fwd_ts<INP, W, H, NT, SPL>
+                        : k_fwd_tc<INP, W, H, NT, SPL>;
+  const size_t smem = std::max<size_t>(ts >= 2 ? fwd_ts_smem<INP, W, H, SPL>() + 128 * INP * 2 * (SPL ? 2 : 1)
                                        : ts     ? fwd_ts_smem<INP, W, H, SPL>()
                                                 : fwd_smem<INP, W, H, SPL>(),
                                        min_smem);
-  const int nthreads = ts == 2 ? kWsThreads : NT;
+  const int nthreads = ts == 2 ? 20 * 32 : ts == 3 ? 32 * 32 : ts == 4 ? 16 * 32 : ts == 5 ? 28 * 32 : NT;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   // shared-memory carve-out (percent of the maximum): the rest of the 256 KB
