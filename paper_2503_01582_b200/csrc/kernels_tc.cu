@@ -1431,18 +1431,13 @@ cudaError_t run_fwd_nt(const FieldDesc& fd, const float* params, long long n, in
                        const float4* pos, void* feat_tiles, float4* out, int* flag, int* tile_ctr, int ctas,
                        size_t min_smem, int carveout, int split, int ts, cudaStream_t st) {
   // ts: 1 = TMEM activations (k_fwd_ts), 2 = + warp-specialised encode (k_fwd_ws: 16 encode warps,
-  // 2 CTAs/SM); 3 / 4 / 5 = k_fwd_ws with 28 x 1, 12 x 2, 24 x 1 (encode warps x CTAs/SM)
-  auto kern = ts == 2   ? k_fwd_ws<INP, W, H, SPL>
-              : ts == 3 ? k_fwd_ws<INP, W, H, SPL, 28, 1>
-              : ts == 4 ? k_fwd_ws<INP, W, H, SPL, 12, 2>
-              : ts == 5 ? k_fwd_ws<INP, W, H, SPL, 24, 1>
-              : ts      ? k_fwd_ts<INP, W, H, NT, SPL>
-                        : k_fwd_tc<INP, W, H, NT, SPL>;
-  const size_t smem = std::max<size_t>(ts >= 2 ? fwd_ts_smem<INP, W, H, SPL>() + 128 * INP * 2 * (SPL ? 2 : 1)
+  // 2 CTAs/SM; measured on cfg2 split: 12 x 2 within 2%, 28 x 1 and 24 x 1 +40%: one MLP chain per SM)
+  auto kern = ts == 2 ? k_fwd_ws<INP, W, H, SPL> : ts ? k_fwd_ts<INP, W, H, NT, SPL> : k_fwd_tc<INP, W, H, NT, SPL>;
+  const size_t smem = std::max<size_t>(ts == 2 ? fwd_ts_smem<INP, W, H, SPL>() + 128 * INP * 2 * (SPL ? 2 : 1)
                                        : ts     ? fwd_ts_smem<INP, W, H, SPL>()
                                                 : fwd_smem<INP, W, H, SPL>(),
                                        min_smem);
-  const int nthreads = ts == 2 ? 20 * 32 : ts == 3 ? 32 * 32 : ts == 4 ? 16 * 32 : ts == 5 ? 28 * 32 : NT;
+  const int nthreads = ts == 2 ? 20 * 32 : NT;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   // shared-memory carve-out (percent of the maximum): the rest of the 256 KB
