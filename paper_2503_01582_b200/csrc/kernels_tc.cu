@@ -22,6 +22,8 @@
 // are flushed with one atomicAdd per weight per CTA at the end.
 #include <algorithm>
 #include <cstdlib>
+#include <map>
+#include <mutex>
 
 #include "prenom_device.cuh"
 #include "umma.cuh"
@@ -1421,6 +1423,27 @@ size_t bwd_smem() {
          1024;
 }
 
+// cudaFuncSetAttribute only when a kernel's (shared memory, carve-out) changes:
+// the attributes persist, and two driver calls per launch are host time on
+// every step (the timed region enqueues ~7 launches per step).
+std::mutex g_attr_mu;
+std::map<const void*, std::pair<size_t, int>> g_attr;
+template <class K>
+cudaError_t set_attrs(K kern, size_t smem, int carveout) {
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  const void* key = reinterpret_cast<const void*>(kern);
+  auto it = g_attr.find(key);
+  if (it != g_attr.end() && it->second == std::make_pair(smem, carveout)) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  if (carveout >= 0) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carveout);
+    if (e != cudaSuccess) return e;
+  }
+  g_attr[key] = {smem, carveout};
+  return cudaSuccess;
+}
+
 template <int INP, int W, int H, int SPL>
 size_t fwd_ts_smem() {
   return WeightTiles<INP, W, H, SPL>::kBytes + ((H * W + 4) * 4 + 15) / 16 * 16 + 128 * INP * 2 * (SPL ? 2 : 1) + 1024;
@@ -1438,14 +1461,10 @@ cudaError_t run_fwd_nt(const FieldDesc& fd, const float* params, long long n, in
                                                 : fwd_smem<INP, W, H, SPL>(),
                                        min_smem);
   const int nthreads = ts == 2 ? 20 * 32 : NT;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
   // shared-memory carve-out (percent of the maximum): the rest of the 256 KB
   // array is L1, which serves the encode's gathers
-  if (carveout >= 0) {
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carveout);
-    if (e != cudaSuccess) return e;
-  }
+  cudaError_t e = set_attrs(kern, smem, carveout);
+  if (e != cudaSuccess) return e;
   const long long ntiles = (n + kTile - 1) / kTile;
   const long long grid = std::min<long long>((ntiles + min_tiles_per_cta() - 1) / min_tiles_per_cta(), (long long)ctas * sms());
 #ifdef PRENOM_VAR_FWD_MEMSET
@@ -1502,12 +1521,8 @@ cudaError_t run_bwd_s(const FieldDesc& fd, const float* params, float* grad, lon
   static const int carveout = env_int("PRENOM_BWD_CARVEOUT", -1);
   auto kern = k_bwd_tc<INP, W, H, SPL>;
   const size_t smem = std::max<size_t>(bwd_smem<INP, W, H, SPL>(), min_smem);
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = set_attrs(kern, smem, carveout);
   if (e != cudaSuccess) return e;
-  if (carveout >= 0) {
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, carveout);
-    if (e != cudaSuccess) return e;
-  }
   const long long ntiles = (n + kTile - 1) / kTile;
   const int per_sm = std::max(1, (int)(kSmemPerSm / (smem + 1024)));
   const long long grid =
