@@ -144,7 +144,7 @@ inline uint32_t philox_first(uint64_t seed, uint32_t tag, uint32_t step, uint32_
 constexpr int kDefaultLanes = 8;  // B200, with >= 8 tiles per persistent CTA: cfg3 4 lanes 1.35e9, 8 lanes 1.41e9;
                                   // cfg5 4: 1.10e9, 8: 1.12e9 (1 lane: cfg3 1.00e9)
 constexpr int kMaxLanes = 16;
-constexpr int kLaneMinTilesPerCta = 8;
+constexpr int kLaneMinTilesPerCta = 16;  // split mode, B200: cfg3 1.13 -> 1.22e9, cfg5 1.01 -> 1.06e9, cfg4 0.81 -> 0.85e9 vs 8 (32: within 1%)
 constexpr int kL2PersistDefault = 0;  // off: measured on cfg2, persisting the table (1) or its gradient (2)
                                        // slows the step 0.657 -> 0.745 / 0.772 ms (Adam 0.10 -> 0.17 ms)
 
