@@ -23,17 +23,20 @@ for wl_name in ("cfg2", "cfg3"):
     wl.step(5)
     ctx.synchronize()
     stream = torch.cuda.ExternalStream(ctx.stream)
-    k = 50
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record(stream)
-    t0 = time.perf_counter()
-    wl.step(k)
-    t_host = time.perf_counter() - t0
-    b.record(stream)
-    ctx.synchronize()
-    t_dev = a.elapsed_time(b) / 1e3
-    out[wl_name] = {"host_enqueue_us_per_step": round(t_host / k * 1e6, 1), "device_us_per_step": round(t_dev / k * 1e6, 1),
-                    "launches_per_step": round(ctx.launch_count() / (k + 5), 1)}
+    res = {}
+    for k in (2, 5, 20, 50):  # short calls: pure enqueue; long ones fill the launch queue and wait on the GPU
+        l0 = ctx.launch_count()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        t0 = time.perf_counter()
+        wl.step(k)
+        t_host = time.perf_counter() - t0
+        b.record(stream)
+        ctx.synchronize()
+        t_dev = a.elapsed_time(b) / 1e3
+        res[k] = {"host_enqueue_us_per_step": round(t_host / k * 1e6, 1), "device_us_per_step": round(t_dev / k * 1e6, 1),
+                  "launches_per_step": round((ctx.launch_count() - l0) / k, 1)}
+    out[wl_name] = res
     for o in wl.objs:
         o.close()
     ctx.close()
