@@ -212,3 +212,16 @@ def test_from_prior_round_trip_and_train(ctx, rng, tmp_path):
     obj.set_frames(sc.cams, sc.rgb, sc.depth, sc.mask, 1, sc.obj_pose)
     st = obj.train_step(5)
     assert all(np.isfinite(s["total"]) for s in st)
+
+
+def test_from_prior_rejects_grids_beyond_the_device_limit():
+    """load_prior accepts grids up to 4096^3 (prior_bundle.cpp); the device sampler's grids stop at
+    1024^3 (32-bit lattice indices) -- a DataError naming the limit, not a silent resample (CPU)."""
+    from types import SimpleNamespace
+
+    from paper_2503_01582_b200 import DataError, ObjectTrainer
+    from paper_2503_01582_b200.trainer import MAX_GRID_RES
+
+    big = SimpleNamespace(grid=np.zeros((MAX_GRID_RES + 1, 1, 1), np.float32), arch=None, theta=None)
+    with pytest.raises(DataError, match="1024"):
+        ObjectTrainer.from_prior(None, big)
