@@ -1,13 +1,15 @@
+# round-2 final evidence: headline profile, workloads, full GPU suite, smoke, reference arm
 set -x
 mkdir -p gpurun_out
-T=r2q
-B="timeout 600 python bench.py --steps 20 --warmup 3 --no-cpu-baseline --e2e-steps 0 --steady-steps 0"
-for w in cfg3 cfg5; do
-  for mt in 8 16 32; do for ln in 8 16; do
-    PRENOM_MIN_TILES_PER_CTA=$mt PRENOM_LANES=$ln $B --workload $w > gpurun_out/${T}_${w}_mt${mt}_l${ln}.log 2>&1
-  done; done
+T=${T:-r2f2}
+timeout 1500 bash scripts/profile.sh ${T} --mlp bf16x3 > gpurun_out/${T}_profile.log 2>&1
+python scripts/bwd_trace.py bf16x3 gpurun_out/${T}_trace_x3.json > gpurun_out/${T}_trace.log 2>&1
+mkdir -p gpurun_out/${T}_workloads
+for w in cfg1 cfg3 cfg4 cfg5; do
+  timeout 900 python bench.py --workload $w --steps 50 --warmup 5 > gpurun_out/${T}_workloads/$w.json 2> gpurun_out/${T}_workloads/$w.err
 done
-for tpg in 4 8; do for mt in 8 16; do
-  PRENOM_MIN_TILES_PER_CTA=$mt $B --workload cfg4 --tasks-per-gpu $tpg > gpurun_out/${T}_cfg4_t${tpg}_mt${mt}.log 2>&1
-done; done
+timeout 600 python bench.py --mlp bf16 --steps 200 --warmup 10 --no-cpu-baseline > gpurun_out/${T}_workloads/cfg2_bf16.json 2> gpurun_out/${T}_workloads/cfg2_bf16.err
+timeout 2400 python -m pytest tests -q -m gpu > gpurun_out/${T}_gputests.log 2>&1
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${T}_smoke.log 2>&1
+timeout 900 python bench.py --impl reference --steps 5 --warmup 1 > gpurun_out/${T}_reference.json 2> gpurun_out/${T}_reference.err
 echo done
