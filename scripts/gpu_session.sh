@@ -1,15 +1,10 @@
-# round-2 final evidence: headline profile, workloads, full GPU suite, smoke, reference arm
 set -x
 mkdir -p gpurun_out
-T=${T:-r2f2}
-timeout 1500 bash scripts/profile.sh ${T} --mlp bf16x3 > gpurun_out/${T}_profile.log 2>&1
-python scripts/bwd_trace.py bf16x3 gpurun_out/${T}_trace_x3.json > gpurun_out/${T}_trace.log 2>&1
-mkdir -p gpurun_out/${T}_workloads
-for w in cfg1 cfg3 cfg4 cfg5; do
-  timeout 900 python bench.py --workload $w --steps 50 --warmup 5 > gpurun_out/${T}_workloads/$w.json 2> gpurun_out/${T}_workloads/$w.err
+T=r2s
+B="timeout 300 python bench.py --steps 30 --warmup 5 --no-cpu-baseline --e2e-steps 0 --steady-steps 0 --mlp bf16x3"
+PRENOM_FWDS_TS=6 timeout 300 python -m pytest tests/test_split_bf16.py -x -q -m gpu -k "forward or first_step" > gpurun_out/${T}_tests.log 2>&1
+for i in 1 2; do
+  $B > gpurun_out/${T}_ws2_$i.log 2>&1
+  PRENOM_FWDS_TS=6 $B > gpurun_out/${T}_ws6_$i.log 2>&1
 done
-timeout 600 python bench.py --mlp bf16 --steps 200 --warmup 10 --no-cpu-baseline > gpurun_out/${T}_workloads/cfg2_bf16.json 2> gpurun_out/${T}_workloads/cfg2_bf16.err
-timeout 2400 python -m pytest tests -q -m gpu > gpurun_out/${T}_gputests.log 2>&1
-python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${T}_smoke.log 2>&1
-timeout 900 python bench.py --impl reference --steps 5 --warmup 1 > gpurun_out/${T}_reference.json 2> gpurun_out/${T}_reference.err
 echo done
