@@ -550,17 +550,14 @@ __global__ void __launch_bounds__(NT) k_fwd_ts(FieldDesc fd, const float* __rest
 // issue the MMAs, run the epilogues through TMEM and write (sigma, rgb).
 // Tiles are claimed one ahead by the encode leader.
 // NE encode warps (a multiple of 4: NE/4 threads per sample), MINB CTAs per SM.
-// NM MLP warps (4 or 8): with 8, two warps per TMEM lane quadrant split each epilogue's columns.
-template <int INP, int W, int H, int SPL, int NE = 16, int MINB = 2, int NM = 4>
-__global__ void __launch_bounds__((NE + NM) * 32, MINB) k_fwd_ws(FieldDesc fd, const float* __restrict__ params, long long n_total,
+template <int INP, int W, int H, int SPL, int NE = 16, int MINB = 2>
+__global__ void __launch_bounds__((NE + 4) * 32, MINB) k_fwd_ws(FieldDesc fd, const float* __restrict__ params, long long n_total,
                                                     int S, const int* __restrict__ count, const float4* __restrict__ pos,
                                                     uint4* __restrict__ feat_tiles, float4* __restrict__ out, int* flag,
                                                     int* tile_ctr, int split) {
   using WT = WeightTiles<INP, W, H, SPL>;
   constexpr int kWsEncWarps = NE;
-  constexpr int kWsThreads = (NE + NM) * 32;
-  constexpr int kMlp = NM * 32;
-  static_assert(NM == 4 || NM == 8, "MLP warps: one or two per TMEM lane quadrant");
+  constexpr int kWsThreads = (NE + 4) * 32;
   constexpr int kEnc = kWsEncWarps * 32;
   constexpr int TPS = kEnc / 128;
   constexpr uint32_t XLO = SPL ? 128 * INP * 2 : 0;
@@ -633,21 +630,18 @@ __global__ void __launch_bounds__((NE + NM) * 32, MINB) k_fwd_ws(FieldDesc fd, c
   } else {
     // ================= MLP warps: one row per thread
     const int q = warp & 3, row = 32 * q + lane, mt = tid - kEnc;
-    const int cg = NM == 4 ? 0 : (warp - kWsEncWarps) >> 2;  // column group of this warp (NM = 8: two per quadrant)
-    constexpr int kColsPerGroup = W / (NM / 4);
     const uint32_t lane_base = (uint32_t)(32 * q) << 16;
     uint32_t phase = 0;
     constexpr uint32_t id_h = umma::idesc_bf16(128, W, false, false);
     constexpr uint32_t id_out = umma::idesc_bf16(128, 16, false, false);
     auto mlp_sync = [&]() {
       umma::fence_before_sync();
-      named_sync(1, kMlp);
+      named_sync(1, 128);
       umma::fence_after_sync();
     };
     auto epilogue = [&](const float* bias) {
 #pragma unroll
-      for (int c0 = 0; c0 < kColsPerGroup; c0 += 16) {
-        const int c = cg * kColsPerGroup + c0;
+      for (int c = 0; c < W; c += 16) {
         float v[16];
         umma::tmem_ld16(tm + lane_base + c, v);
         umma::tmem_wait_ld();
@@ -723,7 +717,7 @@ __global__ void __launch_bounds__((NE + NM) * 32, MINB) k_fwd_ws(FieldDesc fd, c
       umma::tmem_ld8(tm + lane_base, v);
       umma::tmem_wait_ld();
       const long long gs = t * kTile + row;
-      if (cg == 0 && gs < n_total) {
+      if (gs < n_total) {
         float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
         if (__ldg(count + ray_of(gs, S)) > 0) {
           const float* bb = wt.bias + H * W;
@@ -1461,15 +1455,12 @@ cudaError_t run_fwd_nt(const FieldDesc& fd, const float* params, long long n, in
                        size_t min_smem, int carveout, int split, int ts, cudaStream_t st) {
   // ts: 1 = TMEM activations (k_fwd_ts), 2 = + warp-specialised encode (k_fwd_ws: 16 encode warps,
   // 2 CTAs/SM; measured on cfg2 split: 12 x 2 within 2%, 28 x 1 and 24 x 1 +40%: one MLP chain per SM)
-  auto kern = ts == 2   ? k_fwd_ws<INP, W, H, SPL>
-              : ts == 6 ? k_fwd_ws<INP, W, H, SPL, 12, 2, 8>
-              : ts      ? k_fwd_ts<INP, W, H, NT, SPL>
-                        : k_fwd_tc<INP, W, H, NT, SPL>;
-  const size_t smem = std::max<size_t>(ts == 2 || ts == 6 ? fwd_ts_smem<INP, W, H, SPL>() + 128 * INP * 2 * (SPL ? 2 : 1)
+  auto kern = ts == 2 ? k_fwd_ws<INP, W, H, SPL> : ts ? k_fwd_ts<INP, W, H, NT, SPL> : k_fwd_tc<INP, W, H, NT, SPL>;
+  const size_t smem = std::max<size_t>(ts == 2 ? fwd_ts_smem<INP, W, H, SPL>() + 128 * INP * 2 * (SPL ? 2 : 1)
                                        : ts     ? fwd_ts_smem<INP, W, H, SPL>()
                                                 : fwd_smem<INP, W, H, SPL>(),
                                        min_smem);
-  const int nthreads = ts == 2 || ts == 6 ? 20 * 32 : NT;
+  const int nthreads = ts == 2 ? 20 * 32 : NT;
   // shared-memory carve-out (percent of the maximum): the rest of the 256 KB
   // array is L1, which serves the encode's gathers
   cudaError_t e = set_attrs(kern, smem, carveout);
