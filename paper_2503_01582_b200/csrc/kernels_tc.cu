@@ -549,6 +549,9 @@ __global__ void __launch_bounds__(NT) k_fwd_ts(FieldDesc fd, const float* __rest
 // mbarriers); 4 MLP warps (one row per thread: TMEM lane quadrant = warp % 4)
 // issue the MMAs, run the epilogues through TMEM and write (sigma, rgb).
 // Tiles are claimed one ahead by the encode leader.
+constexpr int kWsEncWarps = 16;  // k_fwd_wx's shape (k_fwd_ws's default)
+constexpr int kWsThreads = (kWsEncWarps + 4) * 32;
+
 // NE encode warps (a multiple of 4: NE/4 threads per sample), MINB CTAs per SM.
 template <int INP, int W, int H, int SPL, int NE = 16, int MINB = 2>
 __global__ void __launch_bounds__((NE + 4) * 32, MINB) k_fwd_ws(FieldDesc fd, const float* __restrict__ params, long long n_total,
@@ -556,9 +559,9 @@ __global__ void __launch_bounds__((NE + 4) * 32, MINB) k_fwd_ws(FieldDesc fd, co
                                                     uint4* __restrict__ feat_tiles, float4* __restrict__ out, int* flag,
                                                     int* tile_ctr, int split) {
   using WT = WeightTiles<INP, W, H, SPL>;
-  constexpr int kWsEncWarps = NE;
-  constexpr int kWsThreads = (NE + 4) * 32;
-  constexpr int kEnc = kWsEncWarps * 32;
+  constexpr int kNE = NE;
+  constexpr int kNT = (NE + 4) * 32;
+  constexpr int kEnc = kNE * 32;
   constexpr int TPS = kEnc / 128;
   constexpr uint32_t XLO = SPL ? 128 * INP * 2 : 0;
   constexpr uint32_t kXBytes = 128 * INP * 2 * (SPL ? 2 : 1);
@@ -576,11 +579,11 @@ __global__ void __launch_bounds__((NE + 4) * 32, MINB) k_fwd_ws(FieldDesc fd, co
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const long long ntiles = (n_total + kTile - 1) / kTile;
   pdl_wait();  // params come from the previous step's Adam
-  wt.load(fd, params + fd.hash_params, kWsThreads);
-  for (int i = tid; i < (int)kXBytes; i += kWsThreads) {  // (both buffers; padding levels stay 0)
+  wt.load(fd, params + fd.hash_params, kNT);
+  for (int i = tid; i < (int)kXBytes; i += kNT) {  // (both buffers; padding levels stay 0)
     reinterpret_cast<__nv_bfloat16*>(Xb0)[i] = __float2bfloat16_rn(0.f);
   }
-  if (warp == kWsEncWarps) umma::tmem_alloc(&tbase, kCols);
+  if (warp == kNE) umma::tmem_alloc(&tbase, kCols);
   if (tid == 0) {
     for (int b = 0; b < 2; ++b) {
       umma::mbar_init(&full[b], kEnc);
@@ -594,7 +597,7 @@ __global__ void __launch_bounds__((NE + 4) * 32, MINB) k_fwd_ws(FieldDesc fd, co
   __syncthreads();
   umma::fence_after_sync();
   const uint32_t tm = tbase;
-  if (warp < kWsEncWarps) {
+  if (warp < kNE) {
     // ================= encode warps
     const int s = tid & (kTile - 1), part = tid >> 7;
     for (int i = 0;; ++i) {
@@ -733,6 +736,221 @@ __global__ void __launch_bounds__((NE + 4) * 32, MINB) k_fwd_ws(FieldDesc fd, co
     }
     if (mt < 32) umma::bulk_wait_all();
   }
+  __syncthreads();
+  tile_sched_exit(tile_ctr);
+  if (warp == kNE) umma::tmem_dealloc(tm, kCols);
+}
+
+// ------------------------------------------------------------------ fwd, features in TMEM
+// k_fwd_ws with the feature tile in tensor memory too: the encode threads write
+// their level pairs (bf16 hi / lo, 32-bit columns) straight into a
+// double-buffered TMEM X region with tcgen05.st (their sample row is their
+// warp's TMEM lane quadrant), layer 0 reads A from TMEM, and the MLP warps copy
+// the tile from TMEM into the stored-feature layout with 16-byte global stores.
+// Shared memory holds only the weights (~29 KB per CTA), so the two CTAs of an
+// SM leave ~190 KB of L1 to the gathers, and the encode issues no shared stores.
+// TMEM: accumulator [0, W), H hi/lo [W, 2W), X[b] hi/lo [2W + b*INP, 2W + (b+1)*INP).
+template <int INP, int W, int H, int SPL>
+__global__ void __launch_bounds__(kWsThreads, 2) k_fwd_wx(FieldDesc fd, const float* __restrict__ params,
+                                                       long long n_total, int S, const int* __restrict__ count,
+                                                       const float4* __restrict__ pos, uint4* __restrict__ feat_tiles,
+                                                       float4* __restrict__ out, int* flag, int* tile_ctr, int split) {
+  using WT = WeightTiles<INP, W, H, SPL>;
+  constexpr int kEnc = kWsEncWarps * 32;
+  constexpr int TPS = kEnc / 128;
+  constexpr int XC = INP + 8;  // stored-tile row width ([X | 1])
+  constexpr int kHhi = W, kHlo = W + W / 2;
+  constexpr int kX0 = 2 * W;            // X[b] hi at kX0 + b * INP, lo at + INP / 2
+  constexpr int kXcols = INP;           // per buffer: INP / 2 hi + INP / 2 lo columns
+  constexpr uint32_t kCols = 2 * W + 2 * kXcols <= 128 ? 128 : 256;
+  const bool sp = SPL && (split & 1);
+  extern __shared__ __align__(1024) unsigned char smem[];
+  __shared__ uint64_t full[2], empty[2], bar;
+  __shared__ uint32_t tbase;
+  __shared__ long long claim[2], tile_of[2];
+  WT wt;
+  unsigned char* p = smem;
+  wt.carve(p);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const long long ntiles = (n_total + kTile - 1) / kTile;
+  pdl_wait();  // params come from the previous step's Adam
+  wt.load(fd, params + fd.hash_params, kWsThreads);
+  if (warp == kWsEncWarps) umma::tmem_alloc(&tbase, kCols);
+  if (tid == 0) {
+    for (int b = 0; b < 2; ++b) {
+      umma::mbar_init(&full[b], kEnc);
+      umma::mbar_init(&empty[b], 1);
+    }
+    umma::mbar_init(&bar, 1);
+    umma::fence_mbar_init();
+    claim[0] = atomicAdd(tile_ctr, 1);
+  }
+  umma::fence_before_sync();
+  __syncthreads();
+  umma::fence_after_sync();
+  const uint32_t tm = tbase;
+  const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
+  if (warp < kWsEncWarps) {
+    // padding levels (L*F < INP) stay zero in both buffers: written once here
+    const int part = tid >> 7;
+    for (int b = 0; b < 2; ++b)
+      for (int l = fd.L + part; l < INP / 2; l += TPS) {
+        umma::tmem_st1(tm + lane_base + kX0 + b * kXcols + l, 0u);
+        umma::tmem_st1(tm + lane_base + kX0 + b * kXcols + INP / 2 + l, 0u);
+      }
+    umma::tmem_wait_st();
+  }
+  if (warp < kWsEncWarps) {
+    // ================= encode warps: features -> TMEM X[b]
+    const int s = tid & (kTile - 1), part = tid >> 7;
+    for (int i = 0;; ++i) {
+      const int b = i & 1;
+      umma::mbar_wait(&empty[b], ((uint32_t)(i >> 1) & 1u) ^ 1u);  // buffer b free (first pass: immediately)
+      umma::fence_after_sync();
+      named_sync(2, kEnc);  // claim[b] of this iteration is published
+      const long long t = claim[b];
+      if (tid == 0 && t < ntiles) claim[b ^ 1] = atomicAdd(tile_ctr, 1);  // next iteration's tile
+      if (t >= ntiles) {
+        if (tid == 0) tile_of[b] = -1;  // sentinel for the MLP warps
+        umma::mbar_arrive_plain(&full[b]);
+        break;
+      }
+      if (tid == 0) tile_of[b] = t;
+      const long long gs = t * kTile + s;
+      const bool valid = gs < n_total && __ldg(count + ray_of(gs, S)) > 0;
+      float4 pp = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (valid) pp = pos[gs];
+      const float px = clamp01(pp.x), py = clamp01(pp.y), pz = clamp01(pp.z);
+      const uint32_t xb = tm + lane_base + kX0 + b * kXcols;
+      for (int l = part; l < fd.L; l += TPS) {
+        float f[2] = {0.f, 0.f};
+        if (valid) encode_level<2>(fd, params, l, px, py, pz, f);
+        const __nv_bfloat162 hi = __floats2bfloat162_rn(f[0], f[1]);
+        umma::tmem_st1(xb + l, *reinterpret_cast<const uint32_t*>(&hi));
+        if (SPL) {
+          const __nv_bfloat162 lo = __floats2bfloat162_rn(f[0] - __low2float(hi), f[1] - __high2float(hi));
+          umma::tmem_st1(xb + INP / 2 + l, *reinterpret_cast<const uint32_t*>(&lo));
+        }
+      }
+      umma::tmem_wait_st();
+      umma::fence_before_sync();
+      umma::mbar_arrive_plain(&full[b]);
+    }
+  } else {
+    // ================= MLP warps: one row per thread
+    const int q = warp & 3, row = 32 * q + lane, mt = tid - kEnc;
+    uint32_t phase = 0;
+    constexpr uint32_t id_h = umma::idesc_bf16(128, W, false, false);
+    constexpr uint32_t id_out = umma::idesc_bf16(128, 16, false, false);
+    auto mlp_sync = [&]() {
+      umma::fence_before_sync();
+      named_sync(1, 128);
+      umma::fence_after_sync();
+    };
+    auto epilogue = [&](const float* bias) {
+#pragma unroll
+      for (int c = 0; c < W; c += 16) {
+        float v[16];
+        umma::tmem_ld16(tm + lane_base + c, v);
+        umma::tmem_wait_ld();
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          uint32_t hi[4], lo[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int k = 8 * h + 2 * i;
+            const float a0 = fmaxf(v[k] + bias[c + k], 0.f), a1 = fmaxf(v[k + 1] + bias[c + k + 1], 0.f);
+            const __nv_bfloat162 hh = __floats2bfloat162_rn(a0, a1);
+            hi[i] = *reinterpret_cast<const uint32_t*>(&hh);
+            if (SPL) {
+              const __nv_bfloat162 ll = __floats2bfloat162_rn(a0 - __low2float(hh), a1 - __high2float(hh));
+              lo[i] = *reinterpret_cast<const uint32_t*>(&ll);
+            }
+          }
+          umma::tmem_st4(tm + lane_base + kHhi + (c + 8 * h) / 2, hi);
+          if (SPL) umma::tmem_st4(tm + lane_base + kHlo + (c + 8 * h) / 2, lo);
+        }
+      }
+      umma::tmem_wait_st();
+      mlp_sync();
+    };
+    for (int i = 0;; ++i) {
+      const int b = i & 1;
+      umma::mbar_wait(&full[b], (uint32_t)(i >> 1) & 1u);
+      const long long t = tile_of[b];
+      if (t < 0) break;
+      umma::fence_after_sync();
+      const uint32_t xa = tm + kX0 + b * kXcols;  // X[b] (lane 0 base: the MMA reads all 128 lanes)
+      if (mt == 0) {
+        for (int ks = 0; ks < INP / 16; ++ks)
+          umma::mma_split_ts(tm, xa + ks * 8, umma::desc_kmajor(wt.w0, INP, ks), id_h, ks > 0, sp, INP / 2, WT::kLo);
+        umma::commit(&bar);
+      }
+      // stored features for the backward: this thread's row from TMEM into the [X | 1]
+      // slots of the stored tile (16-byte stores; the ones columns were written once)
+      {
+        unsigned char* dst = reinterpret_cast<unsigned char*>(feat_tiles) + (size_t)t * (128 * XC * 2 * (SPL ? 2 : 1)) +
+                             (row >> 3) * (XC / 8) * 128 + (row & 7) * 16;
+#pragma unroll
+        for (int h = 0; h < (SPL ? 2 : 1); ++h) {
+          float v[INP / 2];
+          if (INP / 2 == 16) {
+            umma::tmem_ld16(tm + lane_base + kX0 + b * kXcols + h * (INP / 2), v);
+          } else {
+            umma::tmem_ld8(tm + lane_base + kX0 + b * kXcols + h * (INP / 2), v);
+          }
+          umma::tmem_wait_ld();
+#pragma unroll
+          for (int c = 0; c < INP / 8; ++c)
+            *reinterpret_cast<uint4*>(dst + h * 128 * XC * 2 + c * 128) =
+                make_uint4(__float_as_uint(v[4 * c]), __float_as_uint(v[4 * c + 1]), __float_as_uint(v[4 * c + 2]),
+                           __float_as_uint(v[4 * c + 3]));
+        }
+      }
+      wait_mma(&bar, phase);
+      // the layer-0 MMA and the copy-out have read X[b]: the encoders may refill it
+      umma::fence_before_sync();
+      named_sync(1, 128);
+      if (mt == 0) umma::mbar_arrive_plain(&empty[b]);
+      umma::fence_after_sync();
+      epilogue(wt.bias);
+      for (int l = 1; l < H; ++l) {
+        if (mt == 0) {
+          for (int ks = 0; ks < W / 16; ++ks)
+            umma::mma_split_ts(tm, tm + kHhi + ks * 8, umma::desc_kmajor(wt.wl[l - 1], W, ks), id_h, ks > 0, sp,
+                               kHlo - kHhi, WT::kLo);
+          umma::commit(&bar);
+        }
+        wait_mma(&bar, phase);
+        epilogue(wt.bias + l * W);
+      }
+      if (mt == 0) {
+        for (int ks = 0; ks < W / 16; ++ks)
+          umma::mma_split_ts(tm, tm + kHhi + ks * 8, umma::desc_kmajor(wt.wo, W, ks), id_out, ks > 0, sp,
+                             kHlo - kHhi, WT::kLo);
+        umma::commit(&bar);
+      }
+      wait_mma(&bar, phase);
+      float v[8];
+      umma::tmem_ld8(tm + lane_base, v);
+      umma::tmem_wait_ld();
+      const long long gs = t * kTile + row;
+      if (gs < n_total) {
+        float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (__ldg(count + ray_of(gs, S)) > 0) {
+          const float* bb = wt.bias + H * W;
+          o.x = density_forward(fd.act, v[0] + bb[0]);
+          o.y = stable_sigmoid(v[1] + bb[1]);
+          o.z = stable_sigmoid(v[2] + bb[2]);
+          o.w = stable_sigmoid(v[3] + bb[3]);
+          if (!all_finite4(o.x, o.y, o.z, o.w)) atomicOr(flag, 1);
+        }
+        out[gs] = o;
+      }
+      mlp_sync();  // the accumulator is free for the next tile's layer 0
+    }
+  }
+  umma::fence_before_sync();
   __syncthreads();
   tile_sched_exit(tile_ctr);
   if (warp == kWsEncWarps) umma::tmem_dealloc(tm, kCols);
@@ -1455,12 +1673,17 @@ cudaError_t run_fwd_nt(const FieldDesc& fd, const float* params, long long n, in
                        size_t min_smem, int carveout, int split, int ts, cudaStream_t st) {
   // ts: 1 = TMEM activations (k_fwd_ts), 2 = + warp-specialised encode (k_fwd_ws: 16 encode warps,
   // 2 CTAs/SM; measured on cfg2 split: 12 x 2 within 2%, 28 x 1 and 24 x 1 +40%: one MLP chain per SM)
-  auto kern = ts == 2 ? k_fwd_ws<INP, W, H, SPL> : ts ? k_fwd_ts<INP, W, H, NT, SPL> : k_fwd_tc<INP, W, H, NT, SPL>;
-  const size_t smem = std::max<size_t>(ts == 2 ? fwd_ts_smem<INP, W, H, SPL>() + 128 * INP * 2 * (SPL ? 2 : 1)
+  // ts == 3: k_fwd_wx (features in TMEM as well; weights-only shared memory)
+  auto kern = ts == 3   ? k_fwd_wx<INP, W, H, SPL>
+              : ts == 2 ? k_fwd_ws<INP, W, H, SPL>
+              : ts      ? k_fwd_ts<INP, W, H, NT, SPL>
+                        : k_fwd_tc<INP, W, H, NT, SPL>;
+  const size_t smem = std::max<size_t>(ts == 3   ? fwd_ts_smem<INP, W, H, SPL>() - 128 * INP * 2 * (SPL ? 2 : 1)
+                                       : ts == 2 ? fwd_ts_smem<INP, W, H, SPL>() + 128 * INP * 2 * (SPL ? 2 : 1)
                                        : ts     ? fwd_ts_smem<INP, W, H, SPL>()
                                                 : fwd_smem<INP, W, H, SPL>(),
                                        min_smem);
-  const int nthreads = ts == 2 ? 20 * 32 : NT;
+  const int nthreads = ts >= 2 ? kWsThreads : NT;
   // shared-memory carve-out (percent of the maximum): the rest of the 256 KB
   // array is L1, which serves the encode's gathers
   cudaError_t e = set_attrs(kern, smem, carveout);

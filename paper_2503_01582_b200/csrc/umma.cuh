@@ -181,6 +181,11 @@ __device__ __forceinline__ void tmem_st4(uint32_t taddr, const uint32_t* v) {
                : "memory");
 }
 
+// 32 lanes x 32-bit, one column per thread.
+__device__ __forceinline__ void tmem_st1(uint32_t taddr, uint32_t v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 // TMEM address of (lane, column) relative to an allocation base.
