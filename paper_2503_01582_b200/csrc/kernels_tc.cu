@@ -39,21 +39,23 @@ constexpr int kFwdSmemKbDefault = 40;
 // encode's gathers (was 57 KB/CTA padding, 196 KB carve-out, 60 KB of L1:
 // k_fwd_tc 0.195 -> 0.186 ms on cfg2)
 constexpr int kFwdCarveoutDefault = 58;
-// bf16 forward: the warp-specialised kernel (k_fwd_ws, ~31 KB per CTA), 2 CTAs in a
-// 64 KB carve-out -> 192 KB of L1 (cfg2 0.163 ms vs 0.177 for k_fwd_tc 3 x 256)
-constexpr int kFwdTsDefault = 2;
+// bf16 forward: the warp-specialised kernel with features in TMEM (k_fwd_wx, ~15 KB
+// per CTA), 2 CTAs in a 64 KB carve-out -> 192 KB of L1 (cfg2 0.157 ms vs 0.165 for
+// k_fwd_ws, 0.177 for k_fwd_tc 3 x 256)
+constexpr int kFwdTsDefault = 3;
 constexpr int kFwdWsCarveout = 30;
 // split-bf16 forward (~62 KB per CTA): two CTAs of 512 threads per SM
 constexpr int kFwdSThreadsDefault = 512;
 constexpr int kFwdSCtasDefault = 2;
 constexpr int kFwdSCarveoutDefault = 58;  // 132 KB of shared memory, 124 KB of L1
-// split forward: warp-specialised with TMEM-resident activations (k_fwd_ws,
-// ~62 KB per CTA, 2 CTAs per SM in a 132 KB carve-out; cfg2 0.181 ms vs 0.214 for
-// k_fwd_ts at 512 x 2 and 0.250 for k_fwd_tc); PRENOM_FWDS_TS=1 / 0 select those
-constexpr int kFwdSTsDefault = 2;
+// split forward: warp-specialised with the features and activations in TMEM
+// (k_fwd_wx, weights-only shared memory, 2 CTAs per SM in a 64 KB carve-out: cfg2
+// 0.188 ms vs 0.192 for k_fwd_ws (features in smem), 0.214 for k_fwd_ts at 512 x 2,
+// 0.250 for k_fwd_tc); PRENOM_FWDS_TS=2 / 1 / 0 select those
+constexpr int kFwdSTsDefault = 3;
 constexpr int kFwdSTsThreads = 512;
 constexpr int kFwdSTsCtas = 2;
-constexpr int kFwdSTsCarveout = 58;
+constexpr int kFwdSTsCarveout = 30;
 constexpr size_t kSmemPerSm = 228 * 1024;
 constexpr int kSlack = 0;       // weight tiles are never over-read
 // M=128 MN-major views of the (features|1) and (activations|1) tiles read
@@ -1715,7 +1717,9 @@ cudaError_t run_fwd(const FieldDesc& fd, const float* params, long long n, int S
     static const int nt = env_int("PRENOM_FWDS_THREADS", ts ? kFwdSTsThreads : kFwdSThreadsDefault) == 512 ? 512 : 256;
     static const int ctas = std::max(1, std::min(8, env_int("PRENOM_FWDS_CTAS", ts ? kFwdSTsCtas : kFwdSCtasDefault)));
     static const size_t min_smem = (size_t)env_int("PRENOM_FWDS_SMEM_KB", 0) * 1024;
-    static const int carve = env_int("PRENOM_FWDS_CARVEOUT", ts ? kFwdSTsCarveout : kFwdSCarveoutDefault);
+    // carve-out per kernel: wx 64 KB (weights only), ws 132 KB (+ two feature buffers), ts 100 KB
+    static const int carve = env_int("PRENOM_FWDS_CARVEOUT", ts == 3 ? kFwdSTsCarveout : ts == 2 ? 58 : ts ? 44
+                                                                                                      : kFwdSCarveoutDefault);
     if (nt == 512)
       return run_fwd_nt<INP, W, H, 512, 1>(fd, params, n, S, count, pos, feat_tiles, out, flag, tile_ctr, ctas,
                                            min_smem, carve, split, ts, st);
@@ -1724,9 +1728,9 @@ cudaError_t run_fwd(const FieldDesc& fd, const float* params, long long n, int S
   }
   static const int ts = env_int("PRENOM_FWD_TS", kFwdTsDefault);
   static const int nt = env_int("PRENOM_FWD_THREADS", kFwdThreadsDefault) == 512 ? 512 : 256;
-  static const int ctas = std::max(1, std::min(8, env_int("PRENOM_FWD_CTAS", ts == 2 ? 2 : kFwdCtasDefault)));
+  static const int ctas = std::max(1, std::min(8, env_int("PRENOM_FWD_CTAS", ts >= 2 ? 2 : kFwdCtasDefault)));
   static const size_t min_smem = (size_t)env_int("PRENOM_FWD_SMEM_KB", ts ? 0 : kFwdSmemKbDefault) * 1024;
-  static const int carve = env_int("PRENOM_FWD_CARVEOUT", ts == 2 ? kFwdWsCarveout : kFwdCarveoutDefault);
+  static const int carve = env_int("PRENOM_FWD_CARVEOUT", ts >= 2 ? kFwdWsCarveout : kFwdCarveoutDefault);  // (ws, wx: 64 KB)
   if (nt == 512)
     return run_fwd_nt<INP, W, H, 512, 0>(fd, params, n, S, count, pos, feat_tiles, out, flag, tile_ctr, ctas, min_smem,
                                          carve, 0, ts, st);
