@@ -12,7 +12,7 @@ import json
 import sys
 from collections import defaultdict
 
-CLASSES = {"k_sample": "sample", "k_fwd_tc": "field_fwd", "k_fwd_ws": "field_fwd", "k_fwd_ts": "field_fwd",
+CLASSES = {"k_sample": "sample", "k_fwd_tc": "field_fwd", "k_fwd_ws": "field_fwd", "k_fwd_ts": "field_fwd", "k_fwd_wx": "field_fwd",
            "k_fwd_tile": "field_fwd", "k_composite": "composite",
            "k_bwd_tc": "mlp_bwd", "k_bwd_tile": "mlp_bwd", "k_encode_bwd": "encode_bwd", "k_adam": "adam"}
 
