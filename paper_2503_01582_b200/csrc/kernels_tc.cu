@@ -1646,12 +1646,16 @@ size_t bwd_smem() {
 // cudaFuncSetAttribute only when a kernel's (shared memory, carve-out) changes:
 // the attributes persist, and two driver calls per launch are host time on
 // every step (the timed region enqueues ~7 launches per step).
+// (Keyed by device too: function attributes belong to the device's context.)
 std::mutex g_attr_mu;
-std::map<const void*, std::pair<size_t, int>> g_attr;
+std::map<std::pair<int, const void*>, std::pair<size_t, int>> g_attr;
 template <class K>
 cudaError_t set_attrs(K kern, size_t smem, int carveout) {
+  int dev = 0;
+  cudaError_t ed = cudaGetDevice(&dev);
+  if (ed != cudaSuccess) return ed;
   std::lock_guard<std::mutex> lk(g_attr_mu);
-  const void* key = reinterpret_cast<const void*>(kern);
+  const std::pair<int, const void*> key{dev, reinterpret_cast<const void*>(kern)};
   auto it = g_attr.find(key);
   if (it != g_attr.end() && it->second == std::make_pair(smem, carveout)) return cudaSuccess;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
