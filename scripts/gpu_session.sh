@@ -1,16 +1,8 @@
-# round-2 final evidence: headline profile, workloads, full GPU suite, smoke, reference arm
+# loss after 200 steps at BASELINE cfg1 / cfg2 full size on the final code
 set -x
 mkdir -p gpurun_out
-T=${T:-r2v}
-timeout 1500 bash scripts/profile.sh ${T} --mlp bf16x3 > gpurun_out/${T}_profile.log 2>&1
-python scripts/bwd_trace.py bf16x3 gpurun_out/${T}_trace_x3.json > gpurun_out/${T}_trace.log 2>&1
-mkdir -p gpurun_out/${T}_workloads
-for w in cfg1 cfg3 cfg4 cfg5; do
-  timeout 900 python bench.py --workload $w --steps 50 --warmup 5 > gpurun_out/${T}_workloads/$w.json 2> gpurun_out/${T}_workloads/$w.err
-done
-timeout 600 python bench.py --mlp bf16 --steps 200 --warmup 10 --no-cpu-baseline > gpurun_out/${T}_workloads/cfg2_bf16.json 2> gpurun_out/${T}_workloads/cfg2_bf16.err
-timeout 600 python bench.py --mlp fp32 --steps 50 --warmup 5 --no-cpu-baseline --e2e-steps 0 > gpurun_out/${T}_workloads/cfg2_fp32.json 2> gpurun_out/${T}_workloads/cfg2_fp32.err
-timeout 2400 python -m pytest tests -q -m gpu > gpurun_out/${T}_gputests.log 2>&1
-python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${T}_smoke.log 2>&1
-timeout 900 python bench.py --impl reference --steps 5 --warmup 1 > gpurun_out/${T}_reference.json 2> gpurun_out/${T}_reference.err
+T=${T:-r2w}
+timeout 1200 python scripts/loss_parity.py cfg2 200 --oracle-cache profiles/r1/loss_parity_cfg2.json --modes bf16x3,bf16,fp32 --repeats 2 --tag ${T} > gpurun_out/${T}_lp_cfg2.log 2>&1
+timeout 1200 python scripts/loss_parity.py cfg1 200 --oracle-cache profiles/r1/loss_parity_cfg1.json --modes bf16x3,bf16,fp32 --repeats 2 --tag ${T} > gpurun_out/${T}_lp_cfg1.log 2>&1
+cp profiles/loss_parity_*_${T}.json gpurun_out/
 echo done
