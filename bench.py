@@ -772,7 +772,12 @@ def run_ours(args):
             "objects_steps_per_s": round(wl.n_objects_total * args.steps / t_dev, 2),
             "e2e": None if not e2e else {"value": round(e2e["samples"] / (e2e["ms"] / 1e3), 1), "unit": UNIT,
                                          "h2d_bytes_per_step": int(e2e["h2d"]), "d2h_bytes_per_step": e2e["d2h"],
-                                         "steps": args.e2e_steps},
+                                         "steps": args.e2e_steps,
+                                         "note": "streaming loop through the C ABI: each step's keyframe (rgb + depth, "
+                                                 "1 MiB) is uploaded from pinned host memory on the sampling stream while "
+                                                 "the previous step runs, and every step's loss is read back to the host; "
+                                                 "the frames' pixel lists were built once at upload (the reference rebuilds "
+                                                 "the band every step on the host, render.cpp:17-45)"},
             "gpu_launches": int(launches),
             "roofline": roofline,
             "encode_roofline": encode_roofline,
