@@ -1,25 +1,33 @@
 // kernels_tc.cu -- the density+colour MLP on 5th-gen tensor cores (tcgen05,
-// bf16 operands, fp32 accumulation in TMEM), fused with the hash-grid encode
-// (forward) and the table-gradient scatter (backward).
+// fp32 accumulation in TMEM), fused with the hash-grid encode (forward) and the
+// table-gradient scatter (backward).
 //
 // Replaces field_eval's MLP (field.cpp:181-211) and field_backward
-// (field.cpp:227-293) for the bf16-MLP mode of BASELINE config 2 (parity
-// tolerance 1e-2 vs the fp32 oracle; the encode itself stays fp32 and
-// bit-exact, features are rounded to bf16 only as MMA operands).
+// (field.cpp:227-293). Two operand modes (template SPL):
+//   bf16        operands rounded to bf16 (1e-2 vs the fp32 oracle);
+//   split bf16  x = hi + lo, three bf16 products per product (umma.cuh
+//               mma_split): fp32-class results (1e-4), the headline mode.
+// The encode itself is fp32 and bit-exact either way.
 //
-// One CTA = 256 threads works on 128-sample tiles (UMMA M = 128; the samples
-// of a ray are contiguous). Thread 0 issues every tcgen05.mma; completion is
-// signalled through tcgen05.commit -> mbarrier. Epilogues: warp w reads TMEM
-// lane quadrant w%4 (row = sample), warps w and w+4 split the columns.
-// Operand tiles use the core-matrix layout of umma.cuh, so the backward pass
-// feeds forward activations/weights to the tensor core as MN-major
-// (transposed) operands with no data movement:
+// Kernels (128-sample tiles, UMMA M = 128, the samples of a ray contiguous; one
+// thread issues every tcgen05.mma, completion via tcgen05.commit -> mbarrier):
+//   k_fwd_wx   (default) warp-specialised forward: encode warps write the bf16
+//              features into TMEM, MLP warps run every layer from TMEM (TS form)
+//   k_fwd_ws / k_fwd_ts / k_fwd_tc   earlier forwards (features in smem; no warp
+//              specialisation; operands in smem) kept for A/B (PRENOM_FWD{,S}_TS)
+//   k_bwd_tc   warp-specialised backward: MLP warps recompute the forward from the
+//              stored features and backpropagate; scatter warps take d_features
+//              from a TMEM slot and scatter them into the table gradient
+//   k_mlp_grad_reduce  the backward CTAs' MLP-gradient partials, in CTA order
+// Operand tiles use the core-matrix layout of umma.cuh, so the backward feeds
+// forward activations/weights to the tensor core as MN-major (transposed)
+// operands with no data movement:
 //   fwd  H_l  = relu(H_{l-1} W_l^T + b_l)          A K-major,  B K-major
 //   bwd  dH_l = D_{l+1} W_{l+1}                    A K-major,  B MN-major
 //        dW_l += D_l^T [H_{l-1} | 1]               A MN-major, B MN-major (M=64)
 // The appended ones column makes the bias gradient column `in` of dW_l. The
 // weight-gradient accumulators live in TMEM for the whole persistent CTA and
-// are flushed with one atomicAdd per weight per CTA at the end.
+// leave it once, as per-CTA partials (or one atomicAdd per weight).
 #include <algorithm>
 #include <cstdlib>
 #include <map>
@@ -44,7 +52,7 @@ constexpr int kFwdCarveoutDefault = 58;
 // k_fwd_ws, 0.177 for k_fwd_tc 3 x 256)
 constexpr int kFwdTsDefault = 3;
 constexpr int kFwdWsCarveout = 30;
-// split-bf16 forward (~62 KB per CTA): two CTAs of 512 threads per SM
+// split-bf16 k_fwd_tc / k_fwd_ts shapes (~62 KB per CTA): two CTAs of 512 threads per SM
 constexpr int kFwdSThreadsDefault = 512;
 constexpr int kFwdSCtasDefault = 2;
 constexpr int kFwdSCarveoutDefault = 58;  // 132 KB of shared memory, 124 KB of L1
