@@ -226,11 +226,8 @@ __device__ __forceinline__ void epi_relu(uint32_t tm, int col0, const float* bia
 // epi_relu for the backward's forward recompute (G = 2); also returns this
 // thread's ReLU gate, bit c = (bf16 H[row][half*N/2 + c] > 0), so the D_l
 // epilogue needs no shared-memory read of H_l.
-// DOT: also accumulate this thread's share of the output layer's dot products,
-// pdot[o] += relu(h)[k] * Wo[o][k] over its columns (woT[k] = Wo[0..3][k]), in fp32.
-template <int N, int MG, uint32_t LO = 0, bool DOT = false>
-__device__ __forceinline__ uint64_t epi_relu_gate(uint32_t tm, const float* bias, unsigned char* tile, int C,
-                                                  const float4* woT = nullptr, float4* pdot = nullptr) {
+template <int N, int MG, uint32_t LO = 0>
+__device__ __forceinline__ uint64_t epi_relu_gate(uint32_t tm, const float* bias, unsigned char* tile, int C) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int q = warp & 3, half = warp >> 2;
   const int row = 32 * q + lane;
@@ -252,13 +249,6 @@ __device__ __forceinline__ uint64_t epi_relu_gate(uint32_t tm, const float* bias
       if (LO) {
         const __nv_bfloat162 lo = __floats2bfloat162_rn(a0 - __low2float(b), a1 - __high2float(b));
         pl[i] = *reinterpret_cast<const uint32_t*>(&lo);
-      }
-      if (DOT) {
-        const float4 w0 = woT[col + 2 * i], w1 = woT[col + 2 * i + 1];
-        pdot->x = fmaf(a1, w1.x, fmaf(a0, w0.x, pdot->x));
-        pdot->y = fmaf(a1, w1.y, fmaf(a0, w0.y, pdot->y));
-        pdot->z = fmaf(a1, w1.z, fmaf(a0, w0.z, pdot->z));
-        pdot->w = fmaf(a1, w1.w, fmaf(a0, w0.w, pdot->w));
       }
       gate |= ((pk[i] & 0x7FFFu) ? 1ull : 0ull) << (c + 2 * i);
       gate |= ((pk[i] & 0x7FFF0000u) ? 1ull : 0ull) << (c + 2 * i + 1);
@@ -1074,8 +1064,7 @@ struct BwdCols {
   static constexpr int kR = (kDW0 + INP + 8 + 15) / 16 * 16;  // working region, 64 columns
   static constexpr int kDF = kR + 64;            // d_features of the tile being handed over
   static constexpr int kTotal = kDF + INP;
-  static constexpr int kPO = kTotal;  // 4 columns: the second column group's output-layer partial dots
-  static_assert(kPO + 4 <= 256, "TMEM budget");
+  static_assert(kTotal <= 256, "TMEM budget");
 };
 
 // Warp-specialized: warps 0-7 ("MLP warps", named barrier 1) run the
@@ -1186,11 +1175,6 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
   WT wt;
   unsigned char* p = smem;
   wt.carve(p);
-  // the output layer's weights in fp32, one float4 (Wo[0..3][k]) per input unit k:
-  // the recomputed forward forms the raw outputs on CUDA cores in the last hidden
-  // epilogue instead of one more MMA round trip (wait_mode bit 16: the MMA path)
-  float4* woT = reinterpret_cast<float4*>(p);
-  p += W * 16;
   unsigned char* X;      // [128][INP+8]: features | ones
   unsigned char* Ht[2];  // [128][W+8] per hidden layer: activations | ones
   unsigned char* G;      // [128][16] g_raw (4 used)
@@ -1219,12 +1203,7 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
   // ReLU gate is taken)
   unsigned char* zero_end = p;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (tid < kMlpThreads) {
-    wt.load(fd, params + fd.hash_params, kMlpThreads);
-    const float* wo = params + fd.hash_params + fd.w_off[H];
-    for (int k = tid; k < W; k += kMlpThreads)
-      woT[k] = make_float4(__ldg(wo + k), __ldg(wo + W + k), __ldg(wo + 2 * W + k), __ldg(wo + 3 * W + k));
-  }
+  if (tid < kMlpThreads) wt.load(fd, params + fd.hash_params, kMlpThreads);
   {
     uint4* z = reinterpret_cast<uint4*>(zero_begin);
     const int n16 = (int)((zero_end - zero_begin) / 16);
@@ -1345,10 +1324,6 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
     // prefetched into X by a second thread as soon as this tile's dW0 has read X:
     // only the first tile waits for its copy. (knob 3 keeps the plain loop.)
     const bool pf = skip_scatter != 3;
-    // output layer on CUDA cores (H >= 2 hidden layers; H == 1 keeps the MMA: its
-    // last hidden epilogue is layer 0's); wait_mode bit 16 selects the MMA path
-    const bool out_cc = H >= 2 && !(wait_mode & 16);
-    float4 pdot = make_float4(0.f, 0.f, 0.f, 0.f);
     bool prefetched = false;
     long long claim_reg = 0;
     for (long long t = fetch(); t < ntiles; ++iter) {
@@ -1392,50 +1367,22 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
         }
         wait_chain(phase);
         TRACE_MLP(2 + l);
-        if (l == H - 1 && out_cc) {
-          pdot = make_float4(0.f, 0.f, 0.f, 0.f);
-          gate[l] = epi_relu_gate<W, kMG, HLO, true>(tr, wt.bias + l * W, Ht[l], HC, woT, &pdot);
-        } else {
-          gate[l] = epi_relu_gate<W, kMG, HLO>(tr, wt.bias + l * W, Ht[l], HC);
-        }
-      }
-      if (out_cc && half == 1) {  // the second column group hands its partial dots over through TMEM
-        const uint32_t pv[4] = {__float_as_uint(pdot.x), __float_as_uint(pdot.y), __float_as_uint(pdot.z),
-                                __float_as_uint(pdot.w)};
-        umma::tmem_st4(umma::taddr(tm + CM::kPO, 32 * q, 0), pv);
-        umma::tmem_wait_st();
+        gate[l] = epi_relu_gate<W, kMG, HLO>(tr, wt.bias + l * W, Ht[l], HC);
       }
       mlp_sync_for_mma();
-      if (!out_cc) {
-        if (tid == 0) {
-          for (int ks = 0; ks < W / 16; ++ks)
-            umma::mma_split(tr, umma::desc_kmajor(Ht[H - 1], HC, ks), umma::desc_kmajor(wt.wo, W, ks),
-                            umma::idesc_bf16(128, 16, false, false), ks > 0, sp_f, HLO, WT::kLo);
-          umma::commit(&bar);
-        }
-        wait_chain(phase);
+      if (tid == 0) {
+        for (int ks = 0; ks < W / 16; ++ks)
+          umma::mma_split(tr, umma::desc_kmajor(Ht[H - 1], HC, ks), umma::desc_kmajor(wt.wo, W, ks),
+                          umma::idesc_bf16(128, 16, false, false), ks > 0, sp_f, HLO, WT::kLo);
+        umma::commit(&bar);
       }
+      wait_chain(phase);
       TRACE_MLP(4);
       // ---- g_raw (field.cpp:233-238) -> G tile
       if (warp < 4) {
         float v[8];
-        if (out_cc) {  // raw outputs = own partial dots + the other column group's
-          float o4[4];
-          uint32_t u[4];
-          asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
-                       : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3])
-                       : "r"(umma::taddr(tm + CM::kPO, 32 * q, 0)));
-          umma::tmem_wait_ld();
-#pragma unroll
-          for (int j = 0; j < 4; ++j) o4[j] = __uint_as_float(u[j]);
-          v[0] = pdot.x + o4[0];
-          v[1] = pdot.y + o4[1];
-          v[2] = pdot.z + o4[2];
-          v[3] = pdot.w + o4[3];
-        } else {
-          umma::tmem_ld8(umma::taddr(tr, 32 * q, 0), v);
-          umma::tmem_wait_ld();
-        }
+        umma::tmem_ld8(umma::taddr(tr, 32 * q, 0), v);
+        umma::tmem_wait_ld();
         float g[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         if (valid) {
           const float4 d = dpre;
@@ -1700,8 +1647,8 @@ size_t fwd_smem() {
 
 template <int INP, int W, int H, int SPL>
 size_t bwd_smem() {
-  return WeightTiles<INP, W, H, SPL>::kBytes + ((H * W + 4) * 4 + 15) / 16 * 16 + W * 16 +
-         BwdLayout<INP, W, H, SPL>::kOperandBytes + 1024;
+  return WeightTiles<INP, W, H, SPL>::kBytes + ((H * W + 4) * 4 + 15) / 16 * 16 + BwdLayout<INP, W, H, SPL>::kOperandBytes +
+         1024;
 }
 
 // cudaFuncSetAttribute only when a kernel's (shared memory, carve-out) changes:
