@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--samples", type=int, default=96)
     ap.add_argument("--e2e-steps", type=int, default=100)
     ap.add_argument("--tasks-per-gpu", type=int, default=4, help="cfg4: tasks adapted concurrently per GPU per meta-step")
+    ap.add_argument("--grouped", action="store_true",
+                    help="multi-object workloads: grouped launches (one launch per stage for each same-arch group)")
     ap.add_argument("--steady-steps", type=int, default=100,
                     help="single-object workloads: also time this many steps from object step 50 on")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -545,6 +547,8 @@ def run_ours(args):
     from paper_2503_01582_b200._capi import KERNEL_CLASSES
 
     ctx = Context(local)
+    if args.grouped:
+        ctx.set_grouping(True)
     wl = WORKLOADS[args.workload](args, ctx, rank, ws)
     stream = torch.cuda.ExternalStream(ctx.stream)
     lib = ctx.lib
@@ -766,7 +770,8 @@ def run_ours(args):
             "scaling": getattr(wl, "scaling", "weak"), "vs_baseline": None,
             "dtype": {"fp32": "f32", "bf16": "f32+bf16-mlp", "bf16x3": "f32+split-bf16-mlp (bf16x3)"}[args.mlp],
             "data": "synthetic (seeded box-union RGB-D scenes, BASELINE shapes)",
-            "config": dict({"workload": wl.desc, "mlp_precision": args.mlp, "parallelism": f"objects x{ws}"},
+            "config": dict({"workload": wl.desc, "mlp_precision": args.mlp, "parallelism": f"objects x{ws}",
+                            "multi_object_launches": "grouped" if args.grouped else "per-object on lanes"},
                            **wl.extra),
             "per_gpu": round(value / ws, 1),
             "objects_steps_per_s": round(wl.n_objects_total * args.steps / t_dev, 2),

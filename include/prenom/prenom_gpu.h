@@ -305,9 +305,21 @@ prenom_status prenom_reset_adam(prenom_object_t obj);
 prenom_status prenom_set_adam(prenom_object_t obj, const float* m, const float* v, int64_t step);
 
 /* ---- multi-object ----------------------------------------------------- */
-/* Train several objects of one context for n_steps each, launching their
- * stages back to back on the context stream (no host sync). */
+/* Train several objects of one context for n_steps each (no host sync;
+ * run_mapper's per-object train_track loop, mapper.cpp:572-585). Objects with
+ * the same arch, batch shape (rays, samples, sampler) and tensor-core MLP mode
+ * form a group; with grouping on (prenom_ctx_set_grouping) each stage of
+ * their step is ONE grouped launch over a
+ * per-object descriptor table (sampling, forward, compositing, backward +
+ * MLP-gradient reduction, Adam); groups and the other objects run concurrently
+ * on lane streams forked from / joined to the context stream. Each object's
+ * step is the one prenom_train_step runs (same Philox streams, keyframes and
+ * Adam corrections); an object may be listed once. */
 prenom_status prenom_train_step_many(prenom_object_t* objs, int n_objs, int n_steps);
+/* Grouped launches in prenom_train_step_many: on / off (default: every object
+ * on its own launches, the objects concurrently on lane streams).
+ * PRENOM_GROUPED=1 sets the default on. */
+prenom_status prenom_ctx_set_grouping(prenom_ctx_t ctx, int enable);
 
 /* ---- Reptile (meta.cpp:83-92) -------------------------------------------
  * delta_dev[i] = theta_adapted[i] - theta_meta[i] (device buffer of P floats,

@@ -145,7 +145,7 @@ EXPORTED = [
     "prenom_object_step", "prenom_object_check",
     "prenom_render", "prenom_density_query", "prenom_extract_mesh", "prenom_get_mesh", "prenom_get_mesh_grid", "prenom_nearest_sq", "prenom_field_eval",
     "prenom_get_params", "prenom_set_params", "prenom_get_grid", "prenom_set_grid",
-    "prenom_get_adam", "prenom_reset_adam", "prenom_set_adam", "prenom_train_step_many",
+    "prenom_get_adam", "prenom_reset_adam", "prenom_set_adam", "prenom_train_step_many", "prenom_ctx_set_grouping",
     "prenom_reptile_delta", "prenom_reptile_apply", "prenom_object_copy_params", "prenom_reptile_update",
     "prenom_object_set_seed",
     "prenom_comm_unique_id", "prenom_ctx_init_comm", "prenom_ctx_comm_info", "prenom_reptile_step",
@@ -228,6 +228,7 @@ def _declare(lib):
         "prenom_reset_adam": (i32, [P]),
         "prenom_set_adam": (i32, [P, f32p, f32p, C.c_int64]),
         "prenom_train_step_many": (i32, [C.POINTER(P), i32, i32]),
+        "prenom_ctx_set_grouping": (i32, [P, i32]),
         "prenom_reptile_delta": (i32, [P, P, C.c_void_p]),
         "prenom_reptile_apply": (i32, [P, C.c_void_p, i32, C.c_float]),
         "prenom_object_copy_params": (i32, [P, P]),

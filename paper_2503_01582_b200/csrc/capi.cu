@@ -52,6 +52,7 @@ prenom_status prenom_ctx_create(int device, prenom_ctx_t* out) {
   cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
   c->overlap = getenv("PRENOM_NO_OVERLAP") == nullptr;
+  if (const char* g = getenv("PRENOM_GROUPED")) c->grouping = atoi(g) != 0;
   if (e != cudaSuccess) {
     delete c;
     return fail(PRENOM_CUDA, cudaGetErrorString(e));
@@ -107,6 +108,12 @@ prenom_status prenom_ctx_launch_count(prenom_ctx_t ctx, int64_t* count) {
 prenom_status prenom_ctx_profile(prenom_ctx_t ctx, int enable) {
   if (!ctx) return fail(PRENOM_USAGE, "NULL ctx");
   ctx->prof = enable != 0;
+  return PRENOM_OK;
+}
+
+prenom_status prenom_ctx_set_grouping(prenom_ctx_t ctx, int enable) {
+  if (!ctx) return fail(PRENOM_USAGE, "NULL ctx");
+  ctx->grouping = enable != 0;
   return PRENOM_OK;
 }
 

@@ -144,9 +144,19 @@ inline uint32_t philox_first(uint64_t seed, uint32_t tag, uint32_t step, uint32_
 constexpr int kDefaultLanes = 8;  // B200, with >= 8 tiles per persistent CTA: cfg3 4 lanes 1.35e9, 8 lanes 1.41e9;
                                   // cfg5 4: 1.10e9, 8: 1.12e9 (1 lane: cfg3 1.00e9)
 constexpr int kMaxLanes = 16;
+constexpr int kGroupMaxDefault = 0;  // objects per grouped unit of the multi-object scheduler (0 = all)
 constexpr int kLaneMinTilesPerCta = 16;  // split mode, B200: cfg3 1.13 -> 1.22e9, cfg5 1.01 -> 1.06e9, cfg4 0.81 -> 0.85e9 vs 8 (32: within 1%)
 constexpr int kL2PersistDefault = 0;  // off: measured on cfg2, persisting the table (1) or its gradient (2)
                                        // slows the step 0.657 -> 0.745 / 0.772 ms (Adam 0.10 -> 0.17 ms)
+
+// Device scratch of one grouped launch sequence (multi-object scheduler): the
+// object table of the grouped forward / backward, their tile counters and the
+// per-step job arrays of the grouped sampling, compositing and Adam launches.
+struct GroupScratch {
+  DevBuf<TcObj> objs;
+  DevBuf<int> ctr;  // [fwd next, fwd done (self-resetting), bwd next, part slots of objects 0..K-1]
+  DevBuf<unsigned char> jobs;
+};
 
 struct prenom_ctx_s {
   int device = 0;
@@ -158,6 +168,16 @@ struct prenom_ctx_s {
   std::vector<cudaStream_t> lanes;
   std::vector<cudaEvent_t> lane_ev;
   cudaEvent_t fork_ev = nullptr;
+  // objects of one architecture and batch shape train through grouped launches
+  // (one launch per stage for all of them) when on: prenom_ctx_set_grouping /
+  // PRENOM_GROUPED=1. Off by default: measured on B200 the grouped launches are
+  // 13-31% faster per launch, but the lanes overlap one object's Adam with
+  // another's backward, which a grouped step cannot
+  bool grouping = false;
+  std::vector<GroupScratch*> groups;
+  ~prenom_ctx_s() {
+    for (auto* g : groups) delete g;
+  }
   int64_t launches = 0;
   // NCCL communicator of the Reptile all-reduce (prenom_ctx_init_comm; an
   // opaque ncclComm_t, NCCL is loaded at run time) and its buffers
@@ -448,6 +468,38 @@ inline cudaError_t set_l2_window(prenom_object_s* o, cudaStream_t st) {
   return cudaStreamSetAttribute(st, cudaStreamAttributeAccessPolicyWindow, &a);
 }
 
+// composite_backward + batch_loss arguments of a train step (render.cpp:156-243)
+inline CompositeArgs train_composite_args(prenom_object_s* o, StepStatsDev* stats, uint32_t step, int fi) {
+  const SampleBufs sb = bufs(o);
+  CompositeArgs ca;
+  std::memset(&ca, 0, sizeof ca);
+  ca.B = o->cfg.rays_per_iter;
+  ca.S = o->cfg.samples_per_ray;
+  ca.pos_depth = sb.pos_depth;
+  ca.delta = sb.delta;
+  ca.target = sb.target;
+  ca.kind = sb.kind;
+  ca.count = sb.count;
+  ca.out = o->out.p;
+  ca.bg_colors = nullptr;
+  ca.seed = o->seed;
+  ca.step = step;
+  ca.lambda_d = o->cfg.lambda_d;
+  ca.lambda_sigma = o->cfg.lambda_sigma;
+  ca.dout = o->dout.p;
+  ca.stats = stats;
+  ca.flag = o->flag.p;
+  ca.frame = fi;
+  return ca;
+}
+
+// Adam bias corrections of step `step` (0-based) with glibc powf, like the reference (field.cpp:300-301)
+inline void adam_corrections(const prenom_object_s* o, int64_t step, float& c1, float& c2) {
+  const float stepf = (float)(step + 1);
+  c1 = 1.f - std::pow(o->cfg.adam_beta1, stepf);
+  c2 = 1.f - std::pow(o->cfg.adam_beta2, stepf);
+}
+
 inline prenom_status enqueue_step(prenom_object_s* o, StepStatsDev* stats, bool has_next = false) {
   NvtxRange nvtx_("prenom.step");
   cudaStream_t st = o->lane ? o->lane : o->ctx->stream;
@@ -474,25 +526,7 @@ inline prenom_status enqueue_step(prenom_object_s* o, StepStatsDev* stats, bool 
     else
       CUDA_TRY(launch_field_fwd_train(o->fd, o->params.p, B, S, sb, o->feat_t.p, o->out.p, o->flag.p, st));
   }
-  CompositeArgs ca;
-  std::memset(&ca, 0, sizeof ca);
-  ca.B = B;
-  ca.S = S;
-  ca.pos_depth = sb.pos_depth;
-  ca.delta = sb.delta;
-  ca.target = sb.target;
-  ca.kind = sb.kind;
-  ca.count = sb.count;
-  ca.out = o->out.p;
-  ca.bg_colors = nullptr;
-  ca.seed = o->seed;
-  ca.step = step;
-  ca.lambda_d = c.lambda_d;
-  ca.lambda_sigma = c.lambda_sigma;
-  ca.dout = o->dout.p;
-  ca.stats = stats;
-  ca.flag = o->flag.p;
-  ca.frame = fi;
+  const CompositeArgs ca = train_composite_args(o, stats, step, fi);
   {
     ProfScope ps(o->ctx, PRENOM_K_COMPOSITE, st);
     CUDA_TRY(launch_composite(ca, st));
@@ -528,9 +562,8 @@ inline prenom_status enqueue_step(prenom_object_s* o, StepStatsDev* stats, bool 
     o->prefetch_frame = frame_of_step(o, o->step + 1);
   }
   // adam_step (field.cpp:295-310); grad zeroed in the same pass (mapper.cpp:175)
-  const float stepf = (float)(o->step + 1);
-  const float c1 = 1.f - std::pow(c.adam_beta1, stepf);
-  const float c2 = 1.f - std::pow(c.adam_beta2, stepf);
+  float c1, c2;
+  adam_corrections(o, o->step, c1, c2);
   {
     ProfScope ps(o->ctx, PRENOM_K_ADAM, st);
     CUDA_TRY(launch_adam(o->P, o->params.p, o->grad.p, o->m.p, o->v.p, c.eta, c.adam_beta1, c.adam_beta2,

@@ -5,6 +5,128 @@
 using namespace prenom;
 using namespace prenom_capi;
 
+namespace {
+// Objects that can share grouped launches: one field architecture and batch /
+// sampler shape, tensor-core MLP in the same mode (the grouped kernels are the
+// per-object ones with an object table; everything else may differ).
+bool same_group(const prenom_object_s* a, const prenom_object_s* b) {
+  return uses_tc(a) && uses_tc(b) && tc_split(a) == tc_split(b) &&
+         std::memcmp(&a->arch, &b->arch, sizeof(prenom_field_arch)) == 0 &&
+         a->cfg.rays_per_iter == b->cfg.rays_per_iter && a->cfg.samples_per_ray == b->cfg.samples_per_ray &&
+         a->cfg.prior_sampling == b->cfg.prior_sampling && a->cfg.coarse_samples == b->cfg.coarse_samples;
+}
+
+// n_steps train steps of the objects g[0..K) (same_group) through grouped
+// launches on `st`: per step k_sample_grp -> k_fwd_wx<GRP> -> k_composite_grp ->
+// k_bwd_tc<GRP> + k_mlp_grad_reduce_grp -> k_adam_grp, then each due grid refresh
+// (mapper.cpp:182-183, per object). The launches cover every object's
+// train_track step exactly as enqueue_step would (same Philox streams, keyframe
+// picks, Adam corrections); only the MLP weight-gradient partials are summed in
+// a different CTA order. Per-step job arrays for the whole call are built on the
+// host and uploaded once.
+prenom_status enqueue_group_steps(prenom_ctx_s* c, GroupScratch* gs, const std::vector<prenom_object_s*>& g,
+                                  int n_steps, cudaStream_t st) {
+  const int K = (int)g.size();
+  prenom_object_s* o0 = g[0];
+  const int B = o0->cfg.rays_per_iter, S = o0->cfg.samples_per_ray;
+  const long long per_obj_tiles = ((long long)B * S + kTile - 1) / kTile;
+  std::vector<TcObj> tab(K);
+  for (int j = 0; j < K; ++j) {
+    prenom_object_s* o = g[j];
+    TcObj& t = tab[j];
+    t.params = o->params.p;
+    t.grad = o->grad.p;
+    t.count = o->count.p;
+    t.pos = o->pos_depth.p;
+    t.feat = o->feat_tc.p;
+    t.out = o->out.p;
+    t.dout = o->dout.p;
+    t.part = o->mlp_part.p;
+    t.flag = o->flag.p;
+    t.n = (long long)B * S;
+    t.tile0 = per_obj_tiles * j;
+    if (o->upload_pending) CUDA_TRY(cudaStreamWaitEvent(st, o->ev_upload, 0));
+    o->upload_pending = false;
+  }
+  const long long ntiles = per_obj_tiles * K;
+  // [fwd next, fwd done] reset themselves after each forward; zeroed here once per call anyway
+  CUDA_TRY(gs->ctr.ensure((size_t)(3 + K)));
+  CUDA_TRY(cudaMemsetAsync(gs->ctr.p, 0, sizeof(int) * 2, st));
+  CUDA_TRY(gs->objs.ensure((size_t)K));
+  CUDA_TRY(cudaMemcpyAsync(gs->objs.p, tab.data(), sizeof(TcObj) * K, cudaMemcpyHostToDevice, st));
+  // per-step jobs: [n_steps][K] SampleJob, CompositeArgs, AdamJob
+  const size_t sj = sizeof(SampleJob) * K, cj = sizeof(CompositeArgs) * K, aj = sizeof(AdamJob) * K;
+  const size_t per_step = (sj + cj + aj + 15) / 16 * 16;
+  std::vector<unsigned char> h(per_step * n_steps);
+  std::vector<std::vector<int>> refresh(n_steps);  // objects whose grid is refreshed after step it
+  SamplerCfg cfg0{};
+  for (int it = 0; it < n_steps; ++it) {
+    SampleJob* sjob = reinterpret_cast<SampleJob*>(h.data() + per_step * it);
+    CompositeArgs* cjob = reinterpret_cast<CompositeArgs*>(h.data() + per_step * it + sj);
+    AdamJob* ajob = reinterpret_cast<AdamJob*>(h.data() + per_step * it + sj + cj);
+    for (int j = 0; j < K; ++j) {
+      prenom_object_s* o = g[j];
+      const int64_t step = o->step + it;
+      const int fi = frame_of_step(o, step);
+      sjob[j].src = frame_source(o, fi);
+      if (sjob[j].src.n_obj_px == 0) return fail(PRENOM_DATA, "generate_rays: no object pixels");
+      sjob[j].cfg = sampler_cfg(o, B, o->cfg.prior_sampling, PRENOM_TAG_FINE, (uint32_t)step);
+      sjob[j].out = bufs(o);
+      if (it == 0 && j == 0) cfg0 = sjob[j].cfg;
+      cjob[j] = train_composite_args(o, o->stats.p + it, (uint32_t)step, fi);
+      AdamJob& a = ajob[j];
+      a.n = o->P;
+      a.p = o->params.p;
+      a.g = o->grad.p;
+      a.m = o->m.p;
+      a.v = o->v.p;
+      a.lr = o->cfg.eta;
+      a.b1 = o->cfg.adam_beta1;
+      a.b2 = o->cfg.adam_beta2;
+      a.eps = o->cfg.adam_eps;
+      adam_corrections(o, step, a.c1, a.c2);
+      const int m = o->cfg.grid_refresh_every;
+      if (m > 0 && (step + 1) % m == 0) refresh[it].push_back(j);
+    }
+  }
+  CUDA_TRY(gs->jobs.ensure(h.size()));
+  CUDA_TRY(cudaMemcpyAsync(gs->jobs.p, h.data(), h.size(), cudaMemcpyHostToDevice, st));
+  const int split = tc_split(o0);
+  for (int it = 0; it < n_steps; ++it) {
+    const unsigned char* base = gs->jobs.p + per_step * it;
+    {
+      ProfScope ps(c, PRENOM_K_SAMPLE, st);
+      CUDA_TRY(launch_sample_group(reinterpret_cast<const SampleJob*>(base), K, cfg0, st));
+    }
+    {
+      ProfScope ps(c, PRENOM_K_FIELD_FWD, st);
+      CUDA_TRY(launch_fwd_tc_group(o0->fd, gs->objs.p, K, ntiles, S, gs->ctr.p, split, st));
+    }
+    {
+      ProfScope ps(c, PRENOM_K_COMPOSITE, st);
+      CUDA_TRY(launch_composite_group(reinterpret_cast<const CompositeArgs*>(base + sj), K, B, S, st));
+    }
+    {
+      ProfScope ps(c, PRENOM_K_MLP_BWD, st);
+      CUDA_TRY(launch_bwd_tc_group(o0->fd, gs->objs.p, K, ntiles, S, gs->ctr.p + 2, split, st));
+    }
+    {
+      ProfScope ps(c, PRENOM_K_ADAM, st);
+      CUDA_TRY(launch_adam_group(reinterpret_cast<const AdamJob*>(base + sj + cj), K, o0->P, st));
+    }
+    c->launches += 6;  // sample, fwd, composite, bwd, MLP-gradient reduce, Adam
+    for (int j : refresh[it]) {
+      prenom_object_s* o = g[j];
+      ProfScope ps(c, PRENOM_K_REFRESH, st);
+      CUDA_TRY(launch_refresh_grid(o->fd, o->params.p, o->R, o->grid.p, o->flag.p, st));
+      c->launches += 1;
+    }
+  }
+  for (auto* o : g) o->step += n_steps;
+  return PRENOM_OK;
+}
+}  // namespace
+
 extern "C" {
 prenom_status prenom_train_step(prenom_object_t o, int n_steps, prenom_step_stats* stats) {
   NvtxRange nvtx_("prenom.train_step");
@@ -116,6 +238,8 @@ prenom_status prenom_train_step_many(prenom_object_t* objs, int n_objs, int n_st
     if (!objs[i]) return fail(PRENOM_USAGE, "NULL object");
     if (objs[i]->ctx != objs[0]->ctx) return fail(PRENOM_USAGE, "objects must share one context");
     if (objs[i]->frames.empty()) return fail(PRENOM_DATA, "train_step: object has no frames");
+    for (int k = 0; k < i; ++k)
+      if (objs[k] == objs[i]) return fail(PRENOM_USAGE, "train_step_many: an object is listed twice");
   }
   CUDA_TRY(cudaSetDevice(objs[0]->ctx->device));
   for (int i = 0; i < n_objs; ++i) {
@@ -126,20 +250,54 @@ prenom_status prenom_train_step_many(prenom_object_t* objs, int n_objs, int n_st
     o->last_n_steps = n_steps;
   }
   // Multi-object scheduler: objects are independent (own θ, Adam, grid, rng;
-  // mapper.cpp:572-585), so their steps go round-robin onto K lane streams and
-  // the kernels of different objects overlap (filling each other's ramp and
-  // tail waves). The lanes fork from and join back to the context stream, so
-  // callers still see one ordered stream. PRENOM_LANES overrides K (1 = serial).
+  // mapper.cpp:572-585). Objects of one architecture and batch shape form a
+  // group that trains through grouped launches (one launch per stage for all of
+  // them, enqueue_group_steps); the groups and the remaining objects go
+  // round-robin onto K lane streams, so the kernels of different units overlap
+  // (filling each other's ramp and tail waves). The lanes fork from and join
+  // back to the context stream, so callers still see one ordered stream.
+  // PRENOM_LANES overrides K (1 = serial).
   prenom_ctx_s* c = objs[0]->ctx;
   static const int lanes_env = [] {
     const char* v = getenv("PRENOM_LANES");
     return v ? atoi(v) : kDefaultLanes;
   }();
+  static const int group_max = [] {  // objects per grouped unit (PRENOM_GROUP_MAX; 0 = no limit)
+    const char* v = getenv("PRENOM_GROUP_MAX");
+    return v ? atoi(v) : kGroupMaxDefault;
+  }();
+  std::vector<std::vector<prenom_object_s*>> units;  // a group (>= 2 objects) or one object
+  {
+    std::vector<bool> used(n_objs, false);
+    for (int i = 0; i < n_objs; ++i) {
+      if (used[i]) continue;
+      std::vector<prenom_object_s*> u{objs[i]};
+      used[i] = true;
+      if (c->grouping)
+        for (int k = i + 1; k < n_objs; ++k)
+          if (!used[k] && (group_max <= 0 || (int)u.size() < group_max) && same_group(objs[i], objs[k])) {
+            u.push_back(objs[k]);
+            used[k] = true;
+          }
+      units.push_back(std::move(u));
+    }
+    for (auto& u : units)
+      if (u.size() > 1)
+        for (auto* o : u) STATUS_TRY(drop_prefetch(o));  // (a group samples every step itself)
+  }
+  const int n_units = (int)units.size();
+  int n_groups = 0;
+  for (auto& u : units) n_groups += u.size() > 1;
+  while ((int)c->groups.size() < n_groups) c->groups.push_back(new GroupScratch);
   // per-kernel event timing (prenom_ctx_profile) needs serial kernels: one lane
-  const int K = c->prof ? 1 : std::max(1, std::min(n_objs, std::min(lanes_env, kMaxLanes)));
+  const int K = c->prof ? 1 : std::max(1, std::min(n_units, std::min(lanes_env, kMaxLanes)));
   if (K == 1) {
+    int gi = 0;
+    for (auto& u : units)
+      if (u.size() > 1) STATUS_TRY(enqueue_group_steps(c, c->groups[gi++], u, n_steps, c->stream));
     for (int it = 0; it < n_steps; ++it)
-      for (int i = 0; i < n_objs; ++i) STATUS_TRY(enqueue_step(objs[i], objs[i]->stats.p + it, it + 1 < n_steps));
+      for (auto& u : units)
+        if (u.size() == 1) STATUS_TRY(enqueue_step(u[0], u[0]->stats.p + it, it + 1 < n_steps));
     return PRENOM_OK;
   }
   while ((int)c->lanes.size() < K) {
@@ -153,15 +311,24 @@ prenom_status prenom_train_step_many(prenom_object_t* objs, int n_objs, int n_st
   if (!c->fork_ev) CUDA_TRY(cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming));
   CUDA_TRY(cudaEventRecord(c->fork_ev, c->stream));
   for (int k = 0; k < K; ++k) CUDA_TRY(cudaStreamWaitEvent(c->lanes[k], c->fork_ev, 0));
-  for (int i = 0; i < n_objs; ++i) objs[i]->lane = c->lanes[i % K];
   prenom_status st = PRENOM_OK;
   struct MinTiles {  // small per-object batches: fewer, fuller persistent CTAs (kernels_tc.cu)
     MinTiles() { tc_set_min_tiles_per_cta(kLaneMinTilesPerCta); }
     ~MinTiles() { tc_set_min_tiles_per_cta(1); }
   } min_tiles_;
+  {
+    int gi = 0;
+    for (int u = 0; u < n_units && st == PRENOM_OK; ++u) {
+      if (units[u].size() > 1)
+        st = enqueue_group_steps(c, c->groups[gi++], units[u], n_steps, c->lanes[u % K]);
+      else
+        units[u][0]->lane = c->lanes[u % K];
+    }
+  }
   for (int it = 0; it < n_steps && st == PRENOM_OK; ++it)
-    for (int i = 0; i < n_objs && st == PRENOM_OK; ++i)
-      st = enqueue_step(objs[i], objs[i]->stats.p + it, false);  // concurrency replaces the sample-ahead
+    for (int u = 0; u < n_units && st == PRENOM_OK; ++u)
+      if (units[u].size() == 1)
+        st = enqueue_step(units[u][0], units[u][0]->stats.p + it, false);  // concurrency replaces the sample-ahead
   for (int i = 0; i < n_objs; ++i) objs[i]->lane = nullptr;
   for (int k = 0; k < K; ++k) {
     CUDA_TRY(cudaEventRecord(c->lane_ev[k], c->lanes[k]));

@@ -23,10 +23,9 @@ __device__ __forceinline__ void adam1(float& p, float& g, float& m, float& v, fl
   p = __fsub_rn(p, __fdiv_rn(__fmul_rn(lr, mhat), __fadd_rn(__fsqrt_rn(vhat), eps)));
 }
 
-__global__ void __launch_bounds__(256) k_adam(size_t n, float* __restrict__ p, float* __restrict__ g,
-                                              float* __restrict__ m, float* __restrict__ v, float lr, float b1,
-                                              float b2, float eps, float c1, float c2, int zero_grad) {
-  pdl_wait();  // the backward's gradient
+__device__ __forceinline__ void adam_body(size_t n, float* __restrict__ p, float* __restrict__ g,
+                                          float* __restrict__ m, float* __restrict__ v, float lr, float b1, float b2,
+                                          float eps, float c1, float c2, int zero_grad) {
   const size_t n4 = n / 4;
   const size_t stride = (size_t)gridDim.x * blockDim.x;
   // two float4 groups per thread per iteration: 8 independent 16 B loads in flight
@@ -63,6 +62,20 @@ __global__ void __launch_bounds__(256) k_adam(size_t n, float* __restrict__ p, f
     adam1(p[i], gi, m[i], v[i], lr, b1, b2, eps, c1, c2);
     if (zero_grad) g[i] = 0.f;
   }
+}
+
+__global__ void __launch_bounds__(256) k_adam(size_t n, float* __restrict__ p, float* __restrict__ g,
+                                              float* __restrict__ m, float* __restrict__ v, float lr, float b1,
+                                              float b2, float eps, float c1, float c2, int zero_grad) {
+  pdl_wait();  // the backward's gradient
+  adam_body(n, p, g, m, v, lr, b1, b2, eps, c1, c2, zero_grad);
+}
+
+// grouped (multi-object scheduler): blockIdx.y = object
+__global__ void __launch_bounds__(256) k_adam_grp(const AdamJob* __restrict__ jobs) {
+  pdl_wait();
+  const AdamJob& j = jobs[blockIdx.y];
+  adam_body(j.n, j.p, j.g, j.m, j.v, j.lr, j.b1, j.b2, j.eps, j.c1, j.c2, 1);
 }
 
 // --------------------------------------------------------- device init
@@ -175,6 +188,13 @@ cudaError_t launch_adam(size_t n, float* p, float* g, float* m, float* v, float 
   const size_t n4 = std::max<size_t>(n / 4, 1);
   const unsigned grid = (unsigned)std::min<size_t>((n4 + 255) / 256, (size_t)num_sms() * 8);
   return launch_pdl(k_adam, dim3(grid), dim3(256), 0, st, n, p, g, m, v, lr, b1, b2, eps, c1, c2, zero_grad);
+}
+
+cudaError_t launch_adam_group(const AdamJob* jobs_dev, int njobs, size_t n_max, cudaStream_t st) {
+  if (njobs <= 0) return cudaSuccess;
+  const size_t n4 = std::max<size_t>(n_max / 4, 1);
+  const unsigned gx = (unsigned)std::max<size_t>(1, std::min<size_t>((n4 + 255) / 256, (size_t)num_sms() * 8 / njobs));
+  return launch_pdl(k_adam_grp, dim3(gx, (unsigned)njobs), dim3(256), 0, st, jobs_dev);
 }
 
 cudaError_t launch_init_params(const FieldDesc& fd, float* params, uint64_t seed, cudaStream_t st) {

@@ -26,10 +26,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 // K (samples per lane) is a template parameter so the per-lane arrays are
 // sized to the batch (S = 96 -> 3): registers, and so occupancy, follow S.
 template <int K>
-// 4 blocks/SM caps it at 64 registers (94 unbounded; a 32-byte spill):
-// 32 resident warps hide the fp64 scans' latency (cfg2 0.0285 -> 0.0241 ms;
-// 5 blocks/SM, 48 registers, spills more and is slower)
-__global__ void __launch_bounds__(kWarps * 32, 4) k_composite(CompositeArgs a, int frame) {
+__device__ __forceinline__ void composite_body(const CompositeArgs& a, int frame) {
   __shared__ double red[kWarps][4];
   __shared__ unsigned long long red_n[kWarps];
   __shared__ int red_e[kWarps];
@@ -209,6 +206,21 @@ __global__ void __launch_bounds__(kWarps * 32, 4) k_composite(CompositeArgs a, i
   }
 }
 
+// 4 blocks/SM caps it at 64 registers (94 unbounded; a 32-byte spill):
+// 32 resident warps hide the fp64 scans' latency (cfg2 0.0285 -> 0.0241 ms;
+// 5 blocks/SM, 48 registers, spills more and is slower)
+template <int K>
+__global__ void __launch_bounds__(kWarps * 32, 4) k_composite(CompositeArgs a, int frame) {
+  composite_body<K>(a, frame);
+}
+
+// grouped (multi-object scheduler): blockIdx.y = object, its arguments jobs[y]
+template <int K>
+__global__ void __launch_bounds__(kWarps * 32, 4) k_composite_grp(const CompositeArgs* __restrict__ jobs) {
+  const CompositeArgs a = jobs[blockIdx.y];
+  composite_body<K>(a, a.frame);
+}
+
 }  // namespace
 
 cudaError_t launch_composite(const CompositeArgs& a, cudaStream_t st) {
@@ -222,6 +234,18 @@ cudaError_t launch_composite(const CompositeArgs& a, cudaStream_t st) {
   if (k <= 3) return launch_pdl(k_composite<3>, g, b, 0, st, a, a.frame);
   if (k <= 4) return launch_pdl(k_composite<4>, g, b, 0, st, a, a.frame);
   return launch_pdl(k_composite<kMaxChunk>, g, b, 0, st, a, a.frame);
+}
+
+cudaError_t launch_composite_group(const CompositeArgs* jobs_dev, int njobs, int B, int S, cudaStream_t st) {
+  if (B <= 0 || njobs <= 0) return cudaSuccess;
+  if (S > 32 * kMaxChunk) return cudaErrorInvalidValue;
+  const dim3 g((B + kWarps - 1) / kWarps, njobs), b(kWarps * 32);
+  const int k = (S + 31) >> 5;
+  if (k <= 1) return launch_pdl(k_composite_grp<1>, g, b, 0, st, jobs_dev);
+  if (k <= 2) return launch_pdl(k_composite_grp<2>, g, b, 0, st, jobs_dev);
+  if (k <= 3) return launch_pdl(k_composite_grp<3>, g, b, 0, st, jobs_dev);
+  if (k <= 4) return launch_pdl(k_composite_grp<4>, g, b, 0, st, jobs_dev);
+  return launch_pdl(k_composite_grp<kMaxChunk>, g, b, 0, st, jobs_dev);
 }
 
 }  // namespace prenom

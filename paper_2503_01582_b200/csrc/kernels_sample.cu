@@ -139,8 +139,8 @@ __device__ __forceinline__ void sort_slots(float* SORT, int lane) {
   __syncwarp();
 }
 
-__global__ void __launch_bounds__(kWarpsPerBlock * 32)
-    k_sample(RaySource src, SamplerCfg cfg, SampleBufs out, int nc_cap, int p2) {
+__device__ __forceinline__ void sample_body(const RaySource& src, const SamplerCfg& cfg, const SampleBufs& out,
+                                            int nc_cap, int p2) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = blockIdx.x * kWarpsPerBlock + warp;
@@ -352,6 +352,17 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
   }
 }
 
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+    k_sample(RaySource src, SamplerCfg cfg, SampleBufs out, int nc_cap, int p2) {
+  sample_body(src, cfg, out, nc_cap, p2);
+}
+
+// grouped (multi-object scheduler): blockIdx.y = object
+__global__ void __launch_bounds__(kWarpsPerBlock * 32) k_sample_grp(const SampleJob* __restrict__ jobs, int nc_cap, int p2) {
+  const SampleJob& j = jobs[blockIdx.y];
+  sample_body(j.src, j.cfg, j.out, nc_cap, p2);
+}
+
 }  // namespace
 
 cudaError_t launch_sample(const RaySource& src, const SamplerCfg& cfg, SampleBufs out,
@@ -368,6 +379,22 @@ cudaError_t launch_sample(const RaySource& src, const SamplerCfg& cfg, SampleBuf
   }
   const int blocks = (cfg.B + kWarpsPerBlock - 1) / kWarpsPerBlock;
   k_sample<<<blocks, kWarpsPerBlock * 32, smem, st>>>(src, cfg, out, nc_cap, p2);
+  return cudaGetLastError();
+}
+
+// jobs of one group share B, S, prior and n_coarse (the shared-memory shape)
+cudaError_t launch_sample_group(const SampleJob* jobs_dev, int njobs, const SamplerCfg& cfg0, cudaStream_t st) {
+  if (cfg0.B <= 0 || njobs <= 0) return cudaSuccess;
+  const int nc_cap = cfg0.prior ? ((cfg0.n_coarse + 1) & ~1) : 2;
+  int p2 = 32;
+  while (p2 < cfg0.S) p2 <<= 1;
+  const size_t smem = ((size_t)nc_cap * 20 + (size_t)p2 * 4) * kWarpsPerBlock;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k_sample_grp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  const dim3 g((cfg0.B + kWarpsPerBlock - 1) / kWarpsPerBlock, njobs);
+  k_sample_grp<<<g, kWarpsPerBlock * 32, smem, st>>>(jobs_dev, nc_cap, p2);
   return cudaGetLastError();
 }
 

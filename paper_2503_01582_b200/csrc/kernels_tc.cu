@@ -111,27 +111,51 @@ struct WeightTiles {
     }
   }
 
-  // threads [0, nt) cooperate
-  __device__ void load(const FieldDesc& fd, const float* __restrict__ mlp, int nt) {
+  // threads [0, nt) cooperate (tix: this thread's index among them). One index
+  // space over [W0 | W1..W_{H-1} | W_out (16 rows, 4 used) | biases]; each thread
+  // issues 8 loads before it converts and stores them, so a reload inside a
+  // grouped launch costs a few L2 round trips, not one per element.
+  __device__ void load(const FieldDesc& fd, const float* __restrict__ mlp, int nt, int tix = -1) {
     const int IN = fd.in_dim;
-    for (int i = threadIdx.x; i < W * INP; i += nt) {
-      const int o = i / INP, k = i % INP;
-      const float v = k < IN ? __ldg(mlp + fd.w_off[0] + o * IN + k) : 0.f;
-      put(w0, umma::cm_offset(o, k, INP), v);
-    }
-    for (int l = 1; l < H; ++l)
-      for (int i = threadIdx.x; i < W * W; i += nt) {
-        const int o = i / W, k = i % W;
-        put(wl[l - 1], umma::cm_offset(o, k, W), __ldg(mlp + fd.w_off[l] + o * W + k));
+    if (tix < 0) tix = threadIdx.x;
+    constexpr int n0 = W * INP, nl = (H - 1) * W * W, no = 16 * W, nb = H * W + 4;
+    constexpr int total = n0 + nl + no + nb;
+    constexpr int U = 8;
+    for (int base = tix; base < total; base += U * nt) {
+      float v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = base + u * nt;
+        v[u] = 0.f;
+        if (i < n0) {
+          const int o = i / INP, k = i % INP;
+          if (k < IN) v[u] = __ldg(mlp + fd.w_off[0] + o * IN + k);
+        } else if (i < n0 + nl) {
+          const int r = i - n0, l = 1 + r / (W * W), e = r % (W * W);
+          v[u] = __ldg(mlp + fd.w_off[l] + e);
+        } else if (i < n0 + nl + no) {
+          const int r = i - n0 - nl, o = r / W;
+          if (o < 4) v[u] = __ldg(mlp + fd.w_off[H] + r);
+        } else if (i < total) {
+          const int r = i - n0 - nl - no, l = r / W;
+          v[u] = l < H ? __ldg(mlp + fd.b_off[l] + (r % W)) : __ldg(mlp + fd.b_off[H] + (r - H * W));
+        }
       }
-    for (int i = threadIdx.x; i < 16 * W; i += nt) {
-      const int o = i / W, k = i % W;
-      const float v = o < 4 ? __ldg(mlp + fd.w_off[H] + o * W + k) : 0.f;
-      put(wo, umma::cm_offset(o, k, W), v);
-    }
-    for (int i = threadIdx.x; i < H * W + 4; i += nt) {
-      const int l = i / W;
-      bias[i] = l < H ? __ldg(mlp + fd.b_off[l] + (i % W)) : __ldg(mlp + fd.b_off[H] + (i - H * W));
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = base + u * nt;
+        if (i < n0) {
+          put(w0, umma::cm_offset(i / INP, i % INP, INP), v[u]);
+        } else if (i < n0 + nl) {
+          const int r = i - n0, l = 1 + r / (W * W), e = r % (W * W);
+          put(wl[l - 1], umma::cm_offset(e / W, e % W, W), v[u]);
+        } else if (i < n0 + nl + no) {
+          const int r = i - n0 - nl;
+          put(wo, umma::cm_offset(r / W, r % W, W), v[u]);
+        } else if (i < total) {
+          bias[i - n0 - nl - no] = v[u];
+        }
+      }
     }
   }
 };
@@ -139,6 +163,15 @@ struct WeightTiles {
 // Ray of a sample slot: 32-bit division (batches stay far below 2^31 slots;
 // launch_*_tc check), not the ~70-instruction 64-bit one.
 __device__ __forceinline__ uint32_t ray_of(long long gs, int S) { return (uint32_t)gs / (uint32_t)S; }
+
+// Grouped launches: the object of global tile t. The tiles are object-major and
+// every caller walks its tiles in increasing order, so the search starts at its
+// previous object.
+__device__ __forceinline__ int find_obj(const TcObj* __restrict__ g, int nobj, long long t, int j) {
+  if (j < 0) j = 0;
+  while (j + 1 < nobj && t >= g[j + 1].tile0) ++j;
+  return j;
+}
 
 // Dynamic tile scheduler: CTAs pull 128-sample tiles from a global counter,
 // so the tile load balances whatever number of CTAs the hardware co-locates
@@ -760,11 +793,15 @@ __global__ void __launch_bounds__((NE + 4) * 32, MINB) k_fwd_ws(FieldDesc fd, co
 // Shared memory holds only the weights (~29 KB per CTA), so the two CTAs of an
 // SM leave ~190 KB of L1 to the gathers, and the encode issues no shared stores.
 // TMEM: accumulator [0, W), H hi/lo [W, 2W), X[b] hi/lo [2W + b*INP, 2W + (b+1)*INP).
-template <int INP, int W, int H, int SPL>
+// GRP: grouped launch over the objects gobj[0..nobj) (n_total = all their tiles
+// x 128; the per-object arguments are unused): the MLP warps reload the weight
+// tiles when their tile's object changes.
+template <int INP, int W, int H, int SPL, bool GRP = false>
 __global__ void __launch_bounds__(kWsThreads, 2) k_fwd_wx(FieldDesc fd, const float* __restrict__ params,
                                                        long long n_total, int S, const int* __restrict__ count,
                                                        const float4* __restrict__ pos, uint4* __restrict__ feat_tiles,
-                                                       float4* __restrict__ out, int* flag, int* tile_ctr, int split) {
+                                                       float4* __restrict__ out, int* flag, int* tile_ctr, int split,
+                                                       const TcObj* __restrict__ gobj, int nobj) {
   using WT = WeightTiles<INP, W, H, SPL>;
   constexpr int kEnc = kWsEncWarps * 32;
   constexpr int TPS = kEnc / 128;
@@ -784,7 +821,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_fwd_wx(FieldDesc fd, const fl
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const long long ntiles = (n_total + kTile - 1) / kTile;
   pdl_wait();  // params come from the previous step's Adam
-  wt.load(fd, params + fd.hash_params, kWsThreads);
+  if (!GRP) wt.load(fd, params + fd.hash_params, kWsThreads);
   if (warp == kWsEncWarps) umma::tmem_alloc(&tbase, kCols);
   if (tid == 0) {
     for (int b = 0; b < 2; ++b) {
@@ -813,6 +850,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_fwd_wx(FieldDesc fd, const fl
   if (warp < kWsEncWarps) {
     // ================= encode warps: features -> TMEM X[b]
     const int s = tid & (kTile - 1), part = tid >> 7;
+    int ej = 0;
     for (int i = 0;; ++i) {
       const int b = i & 1;
       umma::mbar_wait(&empty[b], ((uint32_t)(i >> 1) & 1u) ^ 1u);  // buffer b free (first pass: immediately)
@@ -826,15 +864,27 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_fwd_wx(FieldDesc fd, const fl
         break;
       }
       if (tid == 0) tile_of[b] = t;
-      const long long gs = t * kTile + s;
-      const bool valid = gs < n_total && __ldg(count + ray_of(gs, S)) > 0;
+      const float* prm = params;
+      const int* cnt = count;
+      const float4* ps = pos;
+      long long tl = t, nn = n_total;
+      if (GRP) {
+        ej = find_obj(gobj, nobj, t, ej);
+        prm = gobj[ej].params;
+        cnt = gobj[ej].count;
+        ps = gobj[ej].pos;
+        tl = t - gobj[ej].tile0;
+        nn = gobj[ej].n;
+      }
+      const long long gs = tl * kTile + s;
+      const bool valid = gs < nn && __ldg(cnt + ray_of(gs, S)) > 0;
       float4 pp = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (valid) pp = pos[gs];
+      if (valid) pp = ps[gs];
       const float px = clamp01(pp.x), py = clamp01(pp.y), pz = clamp01(pp.z);
       const uint32_t xb = tm + lane_base + kX0 + b * kXcols;
       for (int l = part; l < fd.L; l += TPS) {
         float f[2] = {0.f, 0.f};
-        if (valid) encode_level<2>(fd, params, l, px, py, pz, f);
+        if (valid) encode_level<2>(fd, prm, l, px, py, pz, f);
         const __nv_bfloat162 hi = __floats2bfloat162_rn(f[0], f[1]);
         umma::tmem_st1(xb + l, *reinterpret_cast<const uint32_t*>(&hi));
         if (SPL) {
@@ -884,11 +934,32 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_fwd_wx(FieldDesc fd, const fl
       umma::tmem_wait_st();
       mlp_sync();
     };
+    int mj = -1;  // (GRP) object whose weights are in shared memory
     for (int i = 0;; ++i) {
       const int b = i & 1;
       umma::mbar_wait(&full[b], (uint32_t)(i >> 1) & 1u);
       const long long t = tile_of[b];
       if (t < 0) break;
+      const int* cnt = count;
+      uint4* fb = feat_tiles;
+      float4* op = out;
+      int* flg = flag;
+      long long tl = t, nn = n_total;
+      if (GRP) {
+        const int j = find_obj(gobj, nobj, t, mj);
+        if (j != mj) {  // no MMA is in flight: the previous tile's output layer was waited for
+          wt.load(fd, gobj[j].params + fd.hash_params, 128, mt);
+          umma::fence_proxy_async();
+          named_sync(1, 128);
+          mj = j;
+        }
+        cnt = gobj[j].count;
+        fb = reinterpret_cast<uint4*>(gobj[j].feat);
+        op = gobj[j].out;
+        flg = gobj[j].flag;
+        tl = t - gobj[j].tile0;
+        nn = gobj[j].n;
+      }
       umma::fence_after_sync();
       const uint32_t xa = tm + kX0 + b * kXcols;  // X[b] (lane 0 base: the MMA reads all 128 lanes)
       if (mt == 0) {
@@ -899,7 +970,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_fwd_wx(FieldDesc fd, const fl
       // stored features for the backward: this thread's row from TMEM into the [X | 1]
       // slots of the stored tile (16-byte stores; the ones columns were written once)
       {
-        unsigned char* dst = reinterpret_cast<unsigned char*>(feat_tiles) + (size_t)t * (128 * XC * 2 * (SPL ? 2 : 1)) +
+        unsigned char* dst = reinterpret_cast<unsigned char*>(fb) + (size_t)tl * (128 * XC * 2 * (SPL ? 2 : 1)) +
                              (row >> 3) * (XC / 8) * 128 + (row & 7) * 16;
 #pragma unroll
         for (int h = 0; h < (SPL ? 2 : 1); ++h) {
@@ -944,18 +1015,18 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_fwd_wx(FieldDesc fd, const fl
       float v[8];
       umma::tmem_ld8(tm + lane_base, v);
       umma::tmem_wait_ld();
-      const long long gs = t * kTile + row;
-      if (gs < n_total) {
+      const long long gs = tl * kTile + row;
+      if (gs < nn) {
         float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (__ldg(count + ray_of(gs, S)) > 0) {
+        if (__ldg(cnt + ray_of(gs, S)) > 0) {
           const float* bb = wt.bias + H * W;
           o.x = density_forward(fd.act, v[0] + bb[0]);
           o.y = stable_sigmoid(v[1] + bb[1]);
           o.z = stable_sigmoid(v[2] + bb[2]);
           o.w = stable_sigmoid(v[3] + bb[3]);
-          if (!all_finite4(o.x, o.y, o.z, o.w)) atomicOr(flag, 1);
+          if (!all_finite4(o.x, o.y, o.z, o.w)) atomicOr(flg, 1);
         }
-        out[gs] = o;
+        op[gs] = o;
       }
       mlp_sync();  // the accumulator is free for the next tile's layer 0
     }
@@ -1035,6 +1106,9 @@ __device__ __forceinline__ void scatter_level(const FieldDesc& fd, float* __rest
     }
   }
   if (skip != 1 && valid && head) {  // (skip == 1: profiling, no atomics)
+    // (grouped launches load `grad` from the object table: without the hint the
+    // atomics compile to generic ATOM with a shared-window check instead of REDG)
+    __builtin_assume(__isGlobal(grad));
     float* gl = grad + (long long)l * 2 * fd.rows;
     uint32_t rows[8];
     corner_rows(fd, l, cell, rows);
@@ -1143,12 +1217,18 @@ struct BwdLayout {
 
 // SPL: split-bf16 operands; `split` bits: 0 forward recompute, 1 the data
 // products (dH, dX), 2 the weight gradients.
-template <int INP, int W, int H, int SPL>
+// GRP: grouped launch over gobj[0..nobj) (n_total = all their tiles x 128). When
+// the MLP warps' tile changes object they store the weight-gradient accumulators
+// as the CTA's partial of the old object (slot from slots[obj]), reload the
+// weight tiles and restart the accumulation; the scatter warps follow their
+// tile's object.
+template <int INP, int W, int H, int SPL, bool GRP = false>
 __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
     k_bwd_tc(FieldDesc fd, const float* __restrict__ params, float* __restrict__ grad, long long n_total, int S,
              const int* __restrict__ count, const float4* __restrict__ pos, const uint4* __restrict__ feat_tiles,
              const float4* __restrict__ dout, int* tile_ctr, int skip_scatter, int mlp_levels,
-             int pull_max, int split, int wait_mode, float* __restrict__ mlp_part) {
+             int pull_max, int split, int wait_mode, float* __restrict__ mlp_part, const TcObj* __restrict__ gobj,
+             int nobj, int* slots) {
   using CM = BwdCols<INP, W, H>;
   using WT = WeightTiles<INP, W, H, SPL>;
   constexpr int XC = INP + 8, HC = W + 8;
@@ -1170,7 +1250,7 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
   const long long t_entry = (wait_mode & 8) ? gtimer() : 0;
   __shared__ uint64_t bar, xbar, full_bar, empty_bar, xfree;
   __shared__ uint32_t tbase;
-  __shared__ int s_tile, s_next;
+  __shared__ int s_tile, s_next, s_slot;
   __shared__ long long slot_tile;
   WT wt;
   unsigned char* p = smem;
@@ -1203,7 +1283,7 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
   // ReLU gate is taken)
   unsigned char* zero_end = p;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (tid < kMlpThreads) wt.load(fd, params + fd.hash_params, kMlpThreads);
+  if (!GRP && tid < kMlpThreads) wt.load(fd, params + fd.hash_params, kMlpThreads);
   {
     uint4* z = reinterpret_cast<uint4*>(zero_begin);
     const int n16 = (int)((zero_end - zero_begin) / 16);
@@ -1239,6 +1319,7 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
     // ================= scatter warps: d_features -> table gradient
     const int r = (tid - kMlpThreads) & 127;  // sample row in the tile; warp = 32 consecutive samples
     const int lhalf = (tid - kMlpThreads) >> 7;  // levels [lhalf*L/2, ...)
+    int sj = 0;
     for (uint32_t k = 0;; ++k) {
       if (wait_mode & 1)
         umma::mbar_wait_sleep(&full_bar, k & 1u, 20000u);  // (sleeping waiters leave issue slots to the chain)
@@ -1257,10 +1338,22 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty_bar);
       TRACE_SCAT(1);
-      const long long gs = t * kTile + r;
-      const bool valid = gs < n_total && __ldg(count + ray_of(gs, S)) > 0;
+      float* gr = grad;
+      const int* cnt = count;
+      const float4* ps = pos;
+      long long tl = t, nn = n_total;
+      if (GRP) {
+        sj = find_obj(gobj, nobj, t, sj);
+        gr = gobj[sj].grad;
+        cnt = gobj[sj].count;
+        ps = gobj[sj].pos;
+        tl = t - gobj[sj].tile0;
+        nn = gobj[sj].n;
+      }
+      const long long gs = tl * kTile + r;
+      const bool valid = gs < nn && __ldg(cnt + ray_of(gs, S)) > 0;
       float4 pp = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (valid) pp = pos[gs];
+      if (valid) pp = ps[gs];
       const float px = clamp01(pp.x), py = clamp01(pp.y), pz = clamp01(pp.z);
       // levels [lhalf*LH, (lhalf+1)*LH) belong to this half; the MLP warps
       // scatter the first mlp_levels of them. The level's pair is always
@@ -1271,7 +1364,7 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
 #pragma unroll 1
       for (int l = l_lo; l < l_hi; ++l) {  // warp-uniform
         if (l >= l_lo + mlp_levels)
-          scatter_level(fd, grad, l, valid, px, py, pz, d[0], d[1], lane, skip_scatter, pull_max);
+          scatter_level(fd, gr, l, valid, px, py, pz, d[0], d[1], lane, skip_scatter, pull_max);
 #pragma unroll
         for (int i = 0; i + 2 < NH; ++i) d[i] = d[i + 2];
       }
@@ -1304,8 +1397,13 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
         *reinterpret_cast<uint4*>(tile + lo + umma::cm_offset(tid, col, C)) = zero_row;
       }
     };
+    int mj = -1, oit = 0;  // (GRP) object of the weight tiles / accumulators; its tiles in this CTA so far
     auto fetch_x = [&](long long t) {  // stored features [X | 1] (hi, lo) -> X: one bulk copy per half
       const unsigned char* src = reinterpret_cast<const unsigned char*>(feat_tiles) + (size_t)t * kFeatBytes;
+      if (GRP) {
+        const int j = find_obj(gobj, nobj, t, mj);
+        src = reinterpret_cast<const unsigned char*>(gobj[j].feat) + (size_t)(t - gobj[j].tile0) * kFeatBytes;
+      }
       umma::mbar_arrive_expect_tx(&xbar, kFeatBytes);
       if (!SPL || XLO == 128 * XC * 2) {
         umma::bulk_g2s(X, src, kFeatBytes, &xbar);  // (hi | lo contiguous in smem too)
@@ -1319,6 +1417,60 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
       named_sync(1, kMlpThreads);
       return s_tile;
     };
+    // ---- the TMEM weight-gradient accumulators -> memory (warps 0-3): row = input
+    // unit (or the ones row = bias), column = output unit. With a partial buffer,
+    // each CTA stores its partial sums (every MLP parameter once, zeros if it had
+    // no tile) and k_mlp_grad_reduce adds them in CTA order: no same-address
+    // atomics from all CTAs at once (measured 25-29 us of contention), and
+    // deterministic MLP gradients. Without it: one atomicAdd per weight per CTA.
+    auto store_dw = [&](float* part, float* gm, bool have) {
+      auto put = [&](int idx, float val) {
+        if (part) part[idx] = have ? val : 0.f;
+        else atomicAdd(gm + idx, val);
+      };
+      auto flush = [&](int col0, int ncol, int n_out, int in, int bias_row, int w_off, int b_off) {
+        for (int c = 0; c < ncol; c += 8) {
+          float v[8];
+          umma::tmem_ld8(umma::taddr(tm, 32 * warp, col0 + c), v);
+          umma::tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int o = c + j;
+            if (o >= n_out) continue;
+            if (row < in) put(w_off + o * in + row, v[j]);
+            else if (row == bias_row) put(b_off + o, v[j]);
+          }
+        }
+      };
+      // M = 64 accumulators: output unit o = 16 * warp + lane (lanes < 16), column
+      // = input unit (or the ones column = bias)
+      auto flush64 = [&](int col0, int ncol, int in, int ones_col, int w_off, int b_off) {
+        const int o = 16 * warp + lane;
+        for (int c = 0; c < ncol; c += 8) {
+          float v[8];
+          umma::tmem_ld8(umma::taddr(tm, 32 * warp, col0 + c), v);
+          umma::tmem_wait_ld();
+          if (lane >= 16 || o >= W) continue;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int k = c + j;
+            if (k < in) put(w_off + o * in + k, v[j]);
+            else if (k == ones_col) put(b_off + o, v[j]);
+          }
+        }
+      };
+      flush(CM::kDWo, 16, 4, W, W, fd.w_off[H], fd.b_off[H]);
+      for (int l = H - 1; l >= 1; --l) flush64(CM::kDWl + (H - 1 - l) * (W + 8), W + 8, W, W, fd.w_off[l], fd.b_off[l]);
+      flush64(CM::kDW0, INP + 8, fd.in_dim, INP, fd.w_off[0], fd.b_off[0]);
+    };
+    // (GRP) object j's partial: a slot of its buffer, then the accumulators;
+    // every MLP thread calls it (named barrier), after the last MMA completed
+    auto store_part = [&](int j) {
+      umma::fence_after_sync();
+      if (tid == 0) s_slot = atomicAdd(slots + j, 1);
+      named_sync(1, kMlpThreads);
+      if (warp < 4) store_dw(gobj[j].part + (size_t)s_slot * fd.mlp_params, nullptr, true);
+    };
     // The next tile is claimed at the start of this one (the atomic's result is
     // only consumed mid-tile, so its latency is hidden) and its features are
     // prefetched into X by a second thread as soon as this tile's dW0 has read X:
@@ -1327,15 +1479,35 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
     bool prefetched = false;
     long long claim_reg = 0;
     for (long long t = fetch(); t < ntiles; ++iter) {
-      const long long tile0 = t * kTile;
       TRACE_MLP(0);
       if (pf && tid == 0) claim_reg = atomicAdd(tile_ctr, 1);
-      const long long gs = tile0 + row;
-      const bool valid = gs < n_total && __ldg(count + ray_of(gs, S)) > 0;
+      const float4* dp = dout;
+      const int* cnt = count;
+      const float4* ps = pos;
+      float* gr = grad;
+      long long tl = t, nn = n_total;
+      if (GRP) {
+        const int j = find_obj(gobj, nobj, t, mj);
+        if (j != mj) {  // the previous tile's MMAs have completed (its last wait_chain)
+          if (mj >= 0 && oit > 0) store_part(mj);
+          wt.load(fd, gobj[j].params + fd.hash_params, kMlpThreads);  // (fenced by mlp_sync_for_mma below)
+          mj = j;
+          oit = 0;
+        }
+        dp = gobj[j].dout;
+        cnt = gobj[j].count;
+        ps = gobj[j].pos;
+        gr = gobj[j].grad;
+        tl = t - gobj[j].tile0;
+        nn = gobj[j].n;
+      }
+      const int acc_it = GRP ? oit : iter;  // tiles already in the weight-gradient accumulators
+      const long long gs = tl * kTile + row;
+      const bool valid = gs < nn && __ldg(cnt + ray_of(gs, S)) > 0;
       // upstream gradient of this row, loaded now: its latency would otherwise sit
       // on the chain at the g_raw epilogue (warps 0-3 own the rows there)
       float4 dpre = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (warp < 4 && valid) dpre = dout[gs];
+      if (warp < 4 && valid) dpre = dp[gs];
       // ---- stored bf16 features -> X by the TMA engine (no LSU work): one
       // bulk copy per 8-row group (the X row-group stride is longer: ones column)
       if (tid == 0 && !prefetched) fetch_x(t);  // ([X | 1]: the ones come with the tile)
@@ -1404,7 +1576,7 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
       if (tid == 0) {
         for (int ks = 0; ks < 8; ++ks)
           umma::mma_split(tm + CM::kDWo, umma::desc_mnmajor(Ht[H - 1], HC, ks), umma::desc_mnmajor(G, 16, ks),
-                          umma::idesc_bf16(128, 16, true, true), (iter > 0 || ks > 0), sp_w, HLO, GLO);
+                          umma::idesc_bf16(128, 16, true, true), (acc_it > 0 || ks > 0), sp_w, HLO, GLO);
         umma::mma_split(tr, umma::desc_kmajor(G, 16, 0), umma::desc_mnmajor(wt.wo, W, 0),
                         umma::idesc_bf16(128, W, false, true), 0u, sp_d, GLO, WT::kLo);
         umma::commit(&bar);
@@ -1445,7 +1617,7 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
           // dW_l = D_l^T [prev | 1]: A = D_l (MN-major, M = 64 units), B = prev (MN-major, N = pc)
           for (int ks = 0; ks < 8; ++ks)
             umma::mma_split_terms(tm + dwc, umma::desc_mnmajor(Ht[l], HC, ks), umma::desc_mnmajor(prev, pc, ks),
-                                  umma::idesc_bf16(64, pc, true, true), (iter > 0 || ks > 0), sp_w && !(split & 32),
+                                  umma::idesc_bf16(64, pc, true, true), (acc_it > 0 || ks > 0), sp_w && !(split & 32),
                                   sp_w && !(split & 16), HLO, plo);
           if (pf && l == 0) umma::commit(&xfree);  // dW0 is the last reader of X
           if (l > 0) {
@@ -1496,20 +1668,21 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
         if (lane == 0) mbar_arrive(&empty_bar);
         if (skip_scatter != 2) {
           float4 pp = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (valid) pp = pos[gs];
+          if (valid) pp = ps[gs];
           const float px = clamp01(pp.x), py = clamp01(pp.y), pz = clamp01(pp.z);
 #pragma unroll
           for (int k = 0; k < 2 / kMG; ++k) {
             const int l0 = (half + k) * LH;
 #pragma unroll 1
             for (int j = 0; j < mlp_levels && l0 + j < fd.L; ++j) {  // warp-uniform
-              scatter_level(fd, grad, l0 + j, valid, px, py, pz, v[k][0], v[k][1], lane, skip_scatter, pull_max);
+              scatter_level(fd, gr, l0 + j, valid, px, py, pz, v[k][0], v[k][1], lane, skip_scatter, pull_max);
 #pragma unroll
               for (int i2 = 0; i2 < 6; ++i2) v[k][i2] = v[k][i2 + 2];
             }
           }
         }
       }
+      ++oit;
       // next tile: claimed (and its features prefetched) by the issuing thread
       if (pf) {
         named_sync(1, kMlpThreads);
@@ -1527,54 +1700,11 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
       slot_tile = -1;
       mbar_arrive2(&full_bar);
     }
-    // ---- flush the TMEM weight-gradient accumulators: row = input unit (or the
-    // ones row = bias), column = output unit. With mlp_part, each CTA stores its
-    // partial sums (every MLP parameter once, zeros if it had no tile) and
-    // k_mlp_grad_reduce adds them in CTA order: no same-address atomics from
-    // all CTAs at once (measured 25-29 us of contention), and deterministic
-    // MLP gradients. Without it: one atomicAdd per weight per CTA.
     umma::fence_after_sync();
-    if (warp < 4 && (iter > 0 || mlp_part)) {
-      float* gm = grad + fd.hash_params;
-      float* part = mlp_part ? mlp_part + (size_t)blockIdx.x * fd.mlp_params : nullptr;
-      auto put = [&](int idx, float val) {
-        if (part) part[idx] = iter > 0 ? val : 0.f;
-        else atomicAdd(gm + idx, val);
-      };
-      auto flush = [&](int col0, int ncol, int n_out, int in, int bias_row, int w_off, int b_off) {
-        for (int c = 0; c < ncol; c += 8) {
-          float v[8];
-          umma::tmem_ld8(umma::taddr(tm, 32 * warp, col0 + c), v);
-          umma::tmem_wait_ld();
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int o = c + j;
-            if (o >= n_out) continue;
-            if (row < in) put(w_off + o * in + row, v[j]);
-            else if (row == bias_row) put(b_off + o, v[j]);
-          }
-        }
-      };
-      // M = 64 accumulators: output unit o = 16 * warp + lane (lanes < 16), column
-      // = input unit (or the ones column = bias)
-      auto flush64 = [&](int col0, int ncol, int in, int ones_col, int w_off, int b_off) {
-        const int o = 16 * warp + lane;
-        for (int c = 0; c < ncol; c += 8) {
-          float v[8];
-          umma::tmem_ld8(umma::taddr(tm, 32 * warp, col0 + c), v);
-          umma::tmem_wait_ld();
-          if (lane >= 16 || o >= W) continue;
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int k = c + j;
-            if (k < in) put(w_off + o * in + k, v[j]);
-            else if (k == ones_col) put(b_off + o, v[j]);
-          }
-        }
-      };
-      flush(CM::kDWo, 16, 4, W, W, fd.w_off[H], fd.b_off[H]);
-      for (int l = H - 1; l >= 1; --l) flush64(CM::kDWl + (H - 1 - l) * (W + 8), W + 8, W, W, fd.w_off[l], fd.b_off[l]);
-      flush64(CM::kDW0, INP + 8, fd.in_dim, INP, fd.w_off[0], fd.b_off[0]);
+    if (GRP) {
+      if (mj >= 0 && oit > 0) store_part(mj);
+    } else if (warp < 4 && (iter > 0 || mlp_part)) {
+      store_dw(mlp_part ? mlp_part + (size_t)blockIdx.x * fd.mlp_params : nullptr, grad + fd.hash_params, iter > 0);
     }
   }
   umma::fence_before_sync();
@@ -1587,10 +1717,9 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
 // Block = 32 parameters x 32 row groups: each thread sums every 32nd CTA row (a
 // short, independent load chain: the partials were just written and sit in L2),
 // then the 32 group sums are added in fixed order -- deterministic.
-__global__ void __launch_bounds__(1024) k_mlp_grad_reduce(const float* __restrict__ part, int nparts, int P,
-                                                          float* __restrict__ g) {
+__device__ __forceinline__ void mlp_grad_reduce(const float* __restrict__ part, int nparts, int P,
+                                                float* __restrict__ g) {
   __shared__ float red[32][33];
-  pdl_wait();
   const int c = threadIdx.x & 31, grp = threadIdx.x >> 5;
   const int i = blockIdx.x * 32 + c;
   float a0 = 0.f, a1 = 0.f;
@@ -1610,6 +1739,20 @@ __global__ void __launch_bounds__(1024) k_mlp_grad_reduce(const float* __restric
     for (int k = 1; k < 32; ++k) acc += red[k][c];
     g[i] += acc;
   }
+}
+
+__global__ void __launch_bounds__(1024) k_mlp_grad_reduce(const float* __restrict__ part, int nparts, int P,
+                                                          float* __restrict__ g) {
+  pdl_wait();
+  mlp_grad_reduce(part, nparts, P, g);
+}
+
+// grouped: blockIdx.y = object, its partials = the slots its CTAs took
+__global__ void __launch_bounds__(1024) k_mlp_grad_reduce_grp(const TcObj* __restrict__ gobj, const int* slots, int P,
+                                                              long long hash_params) {
+  pdl_wait();
+  const TcObj& o = gobj[blockIdx.y];
+  mlp_grad_reduce(o.part, slots[blockIdx.y], P, o.grad + hash_params);
 }
 
 // Persistent-grid sizing hint: under the multi-object scheduler (concurrent
@@ -1688,10 +1831,7 @@ cudaError_t run_fwd_nt(const FieldDesc& fd, const float* params, long long n, in
   // ts: 1 = TMEM activations (k_fwd_ts), 2 = + warp-specialised encode (k_fwd_ws: 16 encode warps,
   // 2 CTAs/SM; measured on cfg2 split: 12 x 2 within 2%, 28 x 1 and 24 x 1 +40%: one MLP chain per SM)
   // ts == 3: k_fwd_wx (features in TMEM as well; weights-only shared memory)
-  auto kern = ts == 3   ? k_fwd_wx<INP, W, H, SPL>
-              : ts == 2 ? k_fwd_ws<INP, W, H, SPL>
-              : ts      ? k_fwd_ts<INP, W, H, NT, SPL>
-                        : k_fwd_tc<INP, W, H, NT, SPL>;
+  auto kern = ts == 2 ? k_fwd_ws<INP, W, H, SPL> : ts ? k_fwd_ts<INP, W, H, NT, SPL> : k_fwd_tc<INP, W, H, NT, SPL>;
   const size_t smem = std::max<size_t>(ts == 3   ? fwd_ts_smem<INP, W, H, SPL>() - 128 * INP * 2 * (SPL ? 2 : 1)
                                        : ts == 2 ? fwd_ts_smem<INP, W, H, SPL>() + 128 * INP * 2 * (SPL ? 2 : 1)
                                        : ts     ? fwd_ts_smem<INP, W, H, SPL>()
@@ -1700,16 +1840,34 @@ cudaError_t run_fwd_nt(const FieldDesc& fd, const float* params, long long n, in
   const int nthreads = ts >= 2 ? kWsThreads : NT;
   // shared-memory carve-out (percent of the maximum): the rest of the 256 KB
   // array is L1, which serves the encode's gathers
-  cudaError_t e = set_attrs(kern, smem, carveout);
-  if (e != cudaSuccess) return e;
   const long long ntiles = (n + kTile - 1) / kTile;
   const long long grid = std::min<long long>((ntiles + min_tiles_per_cta() - 1) / min_tiles_per_cta(), (long long)ctas * sms());
-#ifdef PRENOM_VAR_FWD_MEMSET
-  e = cudaMemsetAsync(tile_ctr, 0, sizeof(int), st);
+  if (ts == 3) {
+    auto kx = k_fwd_wx<INP, W, H, SPL>;
+    cudaError_t e = set_attrs(kx, smem, carveout);
+    if (e != cudaSuccess) return e;
+    return launch_pdl(kx, dim3((unsigned)grid), dim3(nthreads), smem, st, fd, params, n, S, count, pos,
+                      reinterpret_cast<uint4*>(feat_tiles), out, flag, tile_ctr, split, (const TcObj*)nullptr, 0);
+  }
+  cudaError_t e = set_attrs(kern, smem, carveout);
   if (e != cudaSuccess) return e;
-#endif
   return launch_pdl(kern, dim3((unsigned)grid), dim3(nthreads), smem, st, fd, params, n, S, count, pos,
                     reinterpret_cast<uint4*>(feat_tiles), out, flag, tile_ctr, split);
+}
+
+// grouped forward (k_fwd_wx<..., GRP>): same shape and carve-out as the single-object one
+template <int INP, int W, int H>
+cudaError_t run_fwd_grp(const FieldDesc& fd, const TcObj* objs, int nobj, long long ntiles, int S, int* ctr, int split,
+                        cudaStream_t st) {
+  const int carve = split ? kFwdSTsCarveout : kFwdWsCarveout;
+  auto kx = split ? k_fwd_wx<INP, W, H, 1, true> : k_fwd_wx<INP, W, H, 0, true>;
+  const size_t smem = split ? fwd_ts_smem<INP, W, H, 1>() - 128 * INP * 2 * 2 : fwd_ts_smem<INP, W, H, 0>() - 128 * INP * 2;
+  cudaError_t e = set_attrs(kx, smem, carve);
+  if (e != cudaSuccess) return e;
+  const long long grid = std::min<long long>((ntiles + min_tiles_per_cta() - 1) / min_tiles_per_cta(), 2LL * sms());
+  return launch_pdl(kx, dim3((unsigned)grid), dim3(kWsThreads), smem, st, fd, (const float*)nullptr, ntiles * kTile,
+                    S, (const int*)nullptr, (const float4*)nullptr, (uint4*)nullptr, (float4*)nullptr, (int*)nullptr,
+                    ctr, split, objs, nobj);
 }
 
 int env_int(const char* name, int dflt) {
@@ -1782,10 +1940,45 @@ cudaError_t run_bwd_s(const FieldDesc& fd, const float* params, float* grad, lon
   float* part = mlp_part && (size_t)grid * fd.mlp_params <= part_cap ? mlp_part : nullptr;
   cudaError_t e2 = launch_pdl(kern, dim3((unsigned)grid), dim3(kBwdThreads), smem, st, fd, params, grad, n, S, count,
                               pos, reinterpret_cast<const uint4*>(feat_tiles), dout, tile_ctr, skip, mlp_levels,
-                              pull_max, split, wait_mode, part);
+                              pull_max, split, wait_mode, part, (const TcObj*)nullptr, 0, (int*)nullptr);
   if (e2 != cudaSuccess || !part) return e2;
   return launch_pdl(k_mlp_grad_reduce, dim3((unsigned)((fd.mlp_params + 31) / 32)), dim3(1024), 0, st,
                     (const float*)part, (int)grid, fd.mlp_params, grad + fd.hash_params);
+}
+
+// grouped backward + the per-object MLP-gradient reduction (blockIdx.y = object).
+// Each object's partial buffer holds tc_mlp_part_floats: one slot per CTA at most
+// (a CTA walks increasing tiles, so it leaves an object once).
+template <int INP, int W, int H, int SPL>
+cudaError_t run_bwd_grp_s(const FieldDesc& fd, const TcObj* objs, int nobj, long long ntiles, int S, int* ctr,
+                          int split, cudaStream_t st) {
+  static const size_t min_smem = (size_t)env_int("PRENOM_BWD_SMEM_KB", SPL ? 0 : 80) * 1024;
+  static const int carveout = env_int("PRENOM_BWD_CARVEOUT", -1);
+  auto kern = k_bwd_tc<INP, W, H, SPL, true>;
+  const size_t smem = std::max<size_t>(bwd_smem<INP, W, H, SPL>(), min_smem);
+  cudaError_t e = set_attrs(kern, smem, carveout);
+  if (e != cudaSuccess) return e;
+  const int per_sm = std::max(1, (int)(kSmemPerSm / (smem + 1024)));
+  const long long grid =
+      std::min<long long>((ntiles + min_tiles_per_cta() - 1) / min_tiles_per_cta(), (long long)std::min(2, per_sm) * sms());
+  const int mlp_levels = SPL ? 0 : std::min(kBwdMlpLevels, INP / 4);
+  static const int wait_mode = env_int("PRENOM_BWD_WAIT", kBwdWaitDefault);
+  e = cudaMemsetAsync(ctr, 0, sizeof(int) * (1 + nobj), st);
+  if (e != cudaSuccess) return e;
+  e = launch_pdl(kern, dim3((unsigned)grid), dim3(kBwdThreads), smem, st, fd, (const float*)nullptr, (float*)nullptr,
+                 ntiles * kTile, S, (const int*)nullptr, (const float4*)nullptr, (const uint4*)nullptr,
+                 (const float4*)nullptr, ctr, 0, mlp_levels, kBwdPullMax, split, wait_mode, (float*)nullptr, objs,
+                 nobj, ctr + 1);
+  if (e != cudaSuccess) return e;
+  return launch_pdl(k_mlp_grad_reduce_grp, dim3((unsigned)((fd.mlp_params + 31) / 32), (unsigned)nobj), dim3(1024), 0,
+                    st, objs, (const int*)(ctr + 1), fd.mlp_params, fd.hash_params);
+}
+
+template <int INP, int W, int H>
+cudaError_t run_bwd_grp(const FieldDesc& fd, const TcObj* objs, int nobj, long long ntiles, int S, int* ctr, int split,
+                        cudaStream_t st) {
+  if (split) return run_bwd_grp_s<INP, W, H, 1>(fd, objs, nobj, ntiles, S, ctr, split, st);
+  return run_bwd_grp_s<INP, W, H, 0>(fd, objs, nobj, ntiles, S, ctr, 0, st);
 }
 
 template <int INP, int W, int H>
@@ -1872,6 +2065,20 @@ cudaError_t launch_fwd_tc(const FieldDesc& fd, const float* params, long long n,
 }
 
 size_t tc_mlp_part_floats(const FieldDesc& fd) { return (size_t)2 * sms() * fd.mlp_params; }
+
+cudaError_t launch_fwd_tc_group(const FieldDesc& fd, const TcObj* objs, int nobj, long long ntiles, int S, int* ctr,
+                                int split, cudaStream_t st) {
+  if (ntiles <= 0 || nobj <= 0) return cudaSuccess;
+  split = split_mask(split);
+  PRENOM_TC_DISPATCH(run_fwd_grp, fd, objs, nobj, ntiles, S, ctr, split, st);
+}
+
+cudaError_t launch_bwd_tc_group(const FieldDesc& fd, const TcObj* objs, int nobj, long long ntiles, int S, int* ctr,
+                                int split, cudaStream_t st) {
+  if (ntiles <= 0 || nobj <= 0) return cudaSuccess;
+  split = split_mask(split);
+  PRENOM_TC_DISPATCH(run_bwd_grp, fd, objs, nobj, ntiles, S, ctr, split, st);
+}
 
 cudaError_t launch_bwd_tc(const FieldDesc& fd, const float* params, float* grad, long long n, int S,
                           const int* count, const float4* pos, const void* feat_tiles, const float4* dout,

@@ -330,6 +330,14 @@ __device__ __forceinline__ bool all_finite4(float a, float b, float c, float d) 
 // (defined in the .cu files; all enqueue on `st` and return cudaGetLastError)
 cudaError_t launch_sample(const RaySource& src, const SamplerCfg& cfg, SampleBufs out,
                           StepStatsDev* stats, cudaStream_t st);
+// One object's sampling launch inside a grouped one (multi-object scheduler).
+struct SampleJob {
+  RaySource src;
+  SamplerCfg cfg;
+  SampleBufs out;
+};
+// jobs_dev[0..njobs) on the device; they share cfg0's B, S, prior and n_coarse
+cudaError_t launch_sample_group(const SampleJob* jobs_dev, int njobs, const SamplerCfg& cfg0, cudaStream_t st);
 cudaError_t launch_field_points(const FieldDesc& fd, const float* params, int n,
                                 const float* xyz, float* sigma, float* rgb, float* raw,
                                 float* features, int* flag, cudaStream_t st);
@@ -356,6 +364,8 @@ struct CompositeArgs {
   int frame;                // keyframe index recorded in stats
 };
 cudaError_t launch_composite(const CompositeArgs& a, cudaStream_t st);
+// grouped: jobs_dev[0..njobs) (device), one per object, all with this B and S
+cudaError_t launch_composite_group(const CompositeArgs* jobs_dev, int njobs, int B, int S, cudaStream_t st);
 cudaError_t launch_mlp_bwd_train(const FieldDesc& fd, const float* params, float* grad, int B,
                                  int S, const int* count, const float* features_t,
                                  const float4* dout, float* dfeat_t, cudaStream_t st);
@@ -364,6 +374,13 @@ cudaError_t launch_encode_bwd(const FieldDesc& fd, const float* params, float* g
                               cudaStream_t st);
 cudaError_t launch_adam(size_t n, float* p, float* g, float* m, float* v, float lr, float b1,
                         float b2, float eps, float c1, float c2, int zero_grad, cudaStream_t st);
+// grouped Adam (gradient zeroed): one job per object, blockIdx.y = job
+struct AdamJob {
+  size_t n;
+  float *p, *g, *m, *v;
+  float lr, b1, b2, eps, c1, c2;
+};
+cudaError_t launch_adam_group(const AdamJob* jobs_dev, int njobs, size_t n_max, cudaStream_t st);
 cudaError_t launch_refresh_grid(const FieldDesc& fd, const float* params, int R, float* out,
                                 int* flag, cudaStream_t st);
 cudaError_t launch_init_params(const FieldDesc& fd, float* params, uint64_t seed, cudaStream_t st);
@@ -459,6 +476,31 @@ cudaError_t launch_bwd_tc(const FieldDesc& fd, const float* params, float* grad,
                           int* tile_ctr, int split, float* mlp_part, size_t part_cap, cudaStream_t st);
 // floats of per-CTA MLP-gradient partials launch_bwd_tc can use (else it flushes with atomics)
 size_t tc_mlp_part_floats(const FieldDesc& fd);
+// Grouped launches (multi-object scheduler): the objects of one architecture
+// and samples-per-ray share ONE forward / backward launch over an object-major
+// tile space; obj[j] covers tiles [tile0, tile0 + ceil(n / 128)).
+struct TcObj {
+  const float* params;
+  float* grad;
+  const int* count;
+  const float4* pos;
+  void* feat;          // stored feature tiles (tc_feature_bytes)
+  float4* out;
+  const float4* dout;
+  float* part;         // per-CTA MLP-gradient partial slots (tc_mlp_part_floats)
+  int* flag;
+  long long n;         // samples (B * S)
+  long long tile0;     // first tile in the launch
+};
+// ctr: [fwd next, fwd done] (self-resetting); ctr_bwd: [bwd next, part slots of
+// obj 0..nobj-1], zeroed by the launcher. The tile space is object-major and
+// claimed in order, so the CTAs work through the objects together (one or two
+// objects' tables hot in L2 at a time; measured: giving each CTA a home object
+// instead -- fewer weight reloads, every table hot at once -- is slower).
+cudaError_t launch_fwd_tc_group(const FieldDesc& fd, const TcObj* objs_dev, int nobj, long long ntiles, int S,
+                                int* ctr, int split, cudaStream_t st);
+cudaError_t launch_bwd_tc_group(const FieldDesc& fd, const TcObj* objs_dev, int nobj, long long ntiles, int S,
+                                int* ctr_bwd, int split, cudaStream_t st);
 cudaError_t launch_umma_gemm(int M, int N, int K, int a_mn, int b_mn, const float* A, const float* B,
                              float* D, cudaStream_t st);
 

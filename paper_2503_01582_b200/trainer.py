@@ -228,6 +228,10 @@ class Context:
     def synchronize(self):
         _check(self.lib.prenom_ctx_synchronize(self.h))
 
+    def set_grouping(self, enable: bool):
+        """Grouped launches for same-arch objects in train_many (prenom_ctx_set_grouping)."""
+        _check(self.lib.prenom_ctx_set_grouping(self.h, int(bool(enable))))
+
     def launch_count(self) -> int:
         n = C.c_int64()
         _check(self.lib.prenom_ctx_launch_count(self.h, C.byref(n)))

@@ -16,13 +16,29 @@ import bench  # noqa: E402
 from paper_2503_01582_b200 import Context, ObjectTrainer  # noqa: E402
 
 mode = sys.argv[1] if len(sys.argv) > 1 else "bf16x3"
+group = int(os.environ.get("TRACE_GROUP", "0"))  # > 0: that many cfg4 objects through grouped launches
 sys.argv = ["bench.py", "--mlp", mode]
 args = bench.parse()
 ctx = Context(0)
-sc, grid, arch, cfg = bench.make_workload(args, 0)
-o = ObjectTrainer.create(ctx, arch, theta=None, grid=grid, seed=7, cfg=cfg, box_min=sc.box_min, box_max=sc.box_max)
-o.set_frames(sc.cams, sc.rgb, sc.depth, sc.mask, 1, sc.obj_pose)
-o.train_step(20, stats=False)
+if group:
+    from paper_2503_01582_b200 import TrainConfig, scenes
+    from paper_2503_01582_b200.trainer import train_many
+
+    objs = []
+    for i in range(group):
+        sc = scenes.box_union_scene(n_views=20, res=128, seed=7000 + i)
+        cfg = TrainConfig(rays_per_iter=4096, samples_per_ray=64, prior_sampling=0, grid_refresh_every=0,
+                          mlp_precision=bench.mlp_id(mode))
+        o = ObjectTrainer.create(ctx, scenes.cfg4_arch(), theta=None, grid_res=8, seed=1 + i, cfg=cfg,
+                                 box_min=sc.box_min, box_max=sc.box_max)
+        o.set_frames(sc.cams, sc.rgb, sc.depth, sc.mask, 1, sc.obj_pose)
+        objs.append(o)
+    train_many(objs, 10)
+else:
+    sc, grid, arch, cfg = bench.make_workload(args, 0)
+    o = ObjectTrainer.create(ctx, arch, theta=None, grid=grid, seed=7, cfg=cfg, box_min=sc.box_min, box_max=sc.box_max)
+    o.set_frames(sc.cams, sc.rgb, sc.depth, sc.mask, 1, sc.obj_pose)
+    o.train_step(20, stats=False)
 ctx.synchronize()
 mlp = np.zeros((64, 16), np.int64)
 sca = np.zeros((64, 4), np.int64)
@@ -42,7 +58,9 @@ for sl in order[1:]:
     d = (rows[:, sl] - prev) / GHZ / 1e3
     res["phase_us"][names[sl]] = round(float(np.median(d)), 3)
     prev = rows[:, sl]
+res["x_in_us_per_tile"] = [round(float(v), 2) for v in (rows[:, 1] - rows[:, 0]) / GHZ / 1e3]
 tile = (rows[1:, 0] - rows[:-1, 0]) / GHZ / 1e3
+res["tile_us_per_tile"] = [round(float(v), 2) for v in tile]
 res["tile_us"] = round(float(np.median(tile)), 3)
 ns = 0
 while ns < 64 and sca[ns, 0] and sca[ns, 2]:
