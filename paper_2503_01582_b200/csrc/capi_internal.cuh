@@ -172,7 +172,7 @@ struct prenom_ctx_s {
   // (one launch per stage for all of them) when on: prenom_ctx_set_grouping /
   // PRENOM_GROUPED=1. Off by default: measured on B200 the grouped launches are
   // 13-31% faster per launch, but the lanes overlap one object's Adam with
-  // another's backward, which a grouped step cannot
+  // another's backward, which a grouped step cannot (multi-object scheduler)
   bool grouping = false;
   std::vector<GroupScratch*> groups;
   ~prenom_ctx_s() {

@@ -173,6 +173,14 @@ __device__ __forceinline__ int find_obj(const TcObj* __restrict__ g, int nobj, l
   return j;
 }
 
+// (grouped launches) pull an object's MLP parameter block into L2 ahead of the
+// weight-tile reload of its first tile; threads [0, nt) with index tix
+__device__ __forceinline__ void prefetch_mlp_l2(const FieldDesc& fd, const float* params, int tix, int nt) {
+  const char* p = reinterpret_cast<const char*>(params + fd.hash_params);
+  const int lines = (fd.mlp_params * 4 + 127) / 128;
+  for (int i = tix; i < lines; i += nt) asm volatile("prefetch.global.L2 [%0];" ::"l"(p + (size_t)i * 128));
+}
+
 // Dynamic tile scheduler: CTAs pull 128-sample tiles from a global counter,
 // so the tile load balances whatever number of CTAs the hardware co-locates
 // on an SM (static striding left SMs with more resident CTAs as stragglers).
@@ -869,7 +877,9 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_fwd_wx(FieldDesc fd, const fl
       const float4* ps = pos;
       long long tl = t, nn = n_total;
       if (GRP) {
+        const int pj = ej;
         ej = find_obj(gobj, nobj, t, ej);
+        if (ej != pj && warp == 0) prefetch_mlp_l2(fd, gobj[ej].params, lane, 32);  // the MLP warps reload soon
         prm = gobj[ej].params;
         cnt = gobj[ej].count;
         ps = gobj[ej].pos;
@@ -1489,8 +1499,11 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
       if (GRP) {
         const int j = find_obj(gobj, nobj, t, mj);
         if (j != mj) {  // the previous tile's MMAs have completed (its last wait_chain)
+          // warps 0-3 store the old object's partials while warps 4-7 load the new
+          // weight tiles (prefetched into L2 with this tile's features)
           if (mj >= 0 && oit > 0) store_part(mj);
-          wt.load(fd, gobj[j].params + fd.hash_params, kMlpThreads);  // (fenced by mlp_sync_for_mma below)
+          if (warp >= 4) wt.load(fd, gobj[j].params + fd.hash_params, kMlpThreads - 128, tid - 128);
+          // (fenced by mlp_sync_for_mma below)
           mj = j;
           oit = 0;
         }
@@ -1644,7 +1657,13 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
           // it, in parallel with the issuing thread's dX / slot hand-over
           umma::mbar_wait(&xfree, xfphase);
           xfphase ^= 1u;
-          if (s_next < ntiles) fetch_x(s_next);
+          if (s_next < ntiles) {
+            fetch_x(s_next);
+            if (GRP) {
+              const int nj = find_obj(gobj, nobj, s_next, mj);
+              if (nj != mj) prefetch_mlp_l2(fd, gobj[nj].params, 0, 1);
+            }
+          }
         }
         wait_chain(phase);
         TRACE_MLP(7 + (H - 1 - l));

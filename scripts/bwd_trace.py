@@ -33,6 +33,7 @@ if group:
                                  box_min=sc.box_min, box_max=sc.box_max)
         o.set_frames(sc.cams, sc.rgb, sc.depth, sc.mask, 1, sc.obj_pose)
         objs.append(o)
+    ctx.set_grouping(True)
     train_many(objs, 10)
 else:
     sc, grid, arch, cfg = bench.make_workload(args, 0)
