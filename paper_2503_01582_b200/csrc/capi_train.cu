@@ -6,6 +6,8 @@ using namespace prenom;
 using namespace prenom_capi;
 
 namespace {
+constexpr int kGroupJobChunk = 64;  // steps whose job arrays are uploaded at once
+
 // Objects that can share grouped launches: one field architecture and batch /
 // sampler shape, tensor-core MLP in the same mode (the grouped kernels are the
 // per-object ones with an object table; everything else may differ).
@@ -54,75 +56,80 @@ prenom_status enqueue_group_steps(prenom_ctx_s* c, GroupScratch* gs, const std::
   CUDA_TRY(cudaMemsetAsync(gs->ctr.p, 0, sizeof(int) * 2, st));
   CUDA_TRY(gs->objs.ensure((size_t)K));
   CUDA_TRY(cudaMemcpyAsync(gs->objs.p, tab.data(), sizeof(TcObj) * K, cudaMemcpyHostToDevice, st));
-  // per-step jobs: [n_steps][K] SampleJob, CompositeArgs, AdamJob
+  // per-step jobs, [steps][K] SampleJob, CompositeArgs, AdamJob, built and uploaded in
+  // chunks of kGroupJobChunk steps (the upload is stream-ordered behind the previous
+  // chunk's launches, which read the same buffer)
   const size_t sj = sizeof(SampleJob) * K, cj = sizeof(CompositeArgs) * K, aj = sizeof(AdamJob) * K;
   const size_t per_step = (sj + cj + aj + 15) / 16 * 16;
-  std::vector<unsigned char> h(per_step * n_steps);
-  std::vector<std::vector<int>> refresh(n_steps);  // objects whose grid is refreshed after step it
-  SamplerCfg cfg0{};
-  for (int it = 0; it < n_steps; ++it) {
-    SampleJob* sjob = reinterpret_cast<SampleJob*>(h.data() + per_step * it);
-    CompositeArgs* cjob = reinterpret_cast<CompositeArgs*>(h.data() + per_step * it + sj);
-    AdamJob* ajob = reinterpret_cast<AdamJob*>(h.data() + per_step * it + sj + cj);
-    for (int j = 0; j < K; ++j) {
-      prenom_object_s* o = g[j];
-      const int64_t step = o->step + it;
-      const int fi = frame_of_step(o, step);
-      sjob[j].src = frame_source(o, fi);
-      if (sjob[j].src.n_obj_px == 0) return fail(PRENOM_DATA, "generate_rays: no object pixels");
-      sjob[j].cfg = sampler_cfg(o, B, o->cfg.prior_sampling, PRENOM_TAG_FINE, (uint32_t)step);
-      sjob[j].out = bufs(o);
-      if (it == 0 && j == 0) cfg0 = sjob[j].cfg;
-      cjob[j] = train_composite_args(o, o->stats.p + it, (uint32_t)step, fi);
-      AdamJob& a = ajob[j];
-      a.n = o->P;
-      a.p = o->params.p;
-      a.g = o->grad.p;
-      a.m = o->m.p;
-      a.v = o->v.p;
-      a.lr = o->cfg.eta;
-      a.b1 = o->cfg.adam_beta1;
-      a.b2 = o->cfg.adam_beta2;
-      a.eps = o->cfg.adam_eps;
-      adam_corrections(o, step, a.c1, a.c2);
-      const int m = o->cfg.grid_refresh_every;
-      if (m > 0 && (step + 1) % m == 0) refresh[it].push_back(j);
-    }
-  }
-  CUDA_TRY(gs->jobs.ensure(h.size()));
-  CUDA_TRY(cudaMemcpyAsync(gs->jobs.p, h.data(), h.size(), cudaMemcpyHostToDevice, st));
   const int split = tc_split(o0);
-  for (int it = 0; it < n_steps; ++it) {
-    const unsigned char* base = gs->jobs.p + per_step * it;
-    {
-      ProfScope ps(c, PRENOM_K_SAMPLE, st);
-      CUDA_TRY(launch_sample_group(reinterpret_cast<const SampleJob*>(base), K, cfg0, st));
+  std::vector<unsigned char> h(per_step * std::min(n_steps, kGroupJobChunk));
+  CUDA_TRY(gs->jobs.ensure(h.size()));
+  for (int c0 = 0; c0 < n_steps; c0 += kGroupJobChunk) {
+    const int nc = std::min(kGroupJobChunk, n_steps - c0);
+    std::vector<std::vector<int>> refresh(nc);  // objects whose grid is refreshed after step it
+    SamplerCfg cfg0{};
+    for (int it = 0; it < nc; ++it) {
+      SampleJob* sjob = reinterpret_cast<SampleJob*>(h.data() + per_step * it);
+      CompositeArgs* cjob = reinterpret_cast<CompositeArgs*>(h.data() + per_step * it + sj);
+      AdamJob* ajob = reinterpret_cast<AdamJob*>(h.data() + per_step * it + sj + cj);
+      for (int j = 0; j < K; ++j) {
+        prenom_object_s* o = g[j];
+        const int64_t step = o->step + it;
+        const int fi = frame_of_step(o, step);
+        sjob[j].src = frame_source(o, fi);
+        if (sjob[j].src.n_obj_px == 0) return fail(PRENOM_DATA, "generate_rays: no object pixels");
+        sjob[j].cfg = sampler_cfg(o, B, o->cfg.prior_sampling, PRENOM_TAG_FINE, (uint32_t)step);
+        sjob[j].out = bufs(o);
+        if (it == 0 && j == 0) cfg0 = sjob[j].cfg;
+        cjob[j] = train_composite_args(o, o->stats.p + c0 + it, (uint32_t)step, fi);
+        AdamJob& a = ajob[j];
+        a.n = o->P;
+        a.p = o->params.p;
+        a.g = o->grad.p;
+        a.m = o->m.p;
+        a.v = o->v.p;
+        a.lr = o->cfg.eta;
+        a.b1 = o->cfg.adam_beta1;
+        a.b2 = o->cfg.adam_beta2;
+        a.eps = o->cfg.adam_eps;
+        adam_corrections(o, step, a.c1, a.c2);
+        const int m = o->cfg.grid_refresh_every;
+        if (m > 0 && (step + 1) % m == 0) refresh[it].push_back(j);
+      }
     }
-    {
-      ProfScope ps(c, PRENOM_K_FIELD_FWD, st);
-      CUDA_TRY(launch_fwd_tc_group(o0->fd, gs->objs.p, K, ntiles, S, gs->ctr.p, split, st));
+    CUDA_TRY(cudaMemcpyAsync(gs->jobs.p, h.data(), per_step * nc, cudaMemcpyHostToDevice, st));
+    for (int it = 0; it < nc; ++it) {
+      const unsigned char* base = gs->jobs.p + per_step * it;
+      {
+        ProfScope ps(c, PRENOM_K_SAMPLE, st);
+        CUDA_TRY(launch_sample_group(reinterpret_cast<const SampleJob*>(base), K, cfg0, st));
+      }
+      {
+        ProfScope ps(c, PRENOM_K_FIELD_FWD, st);
+        CUDA_TRY(launch_fwd_tc_group(o0->fd, gs->objs.p, K, ntiles, S, gs->ctr.p, split, st));
+      }
+      {
+        ProfScope ps(c, PRENOM_K_COMPOSITE, st);
+        CUDA_TRY(launch_composite_group(reinterpret_cast<const CompositeArgs*>(base + sj), K, B, S, st));
+      }
+      {
+        ProfScope ps(c, PRENOM_K_MLP_BWD, st);
+        CUDA_TRY(launch_bwd_tc_group(o0->fd, gs->objs.p, K, ntiles, S, gs->ctr.p + 2, split, st));
+      }
+      {
+        ProfScope ps(c, PRENOM_K_ADAM, st);
+        CUDA_TRY(launch_adam_group(reinterpret_cast<const AdamJob*>(base + sj + cj), K, o0->P, st));
+      }
+      c->launches += 6;  // sample, fwd, composite, bwd, MLP-gradient reduce, Adam
+      for (int j : refresh[it]) {
+        prenom_object_s* o = g[j];
+        ProfScope ps(c, PRENOM_K_REFRESH, st);
+        CUDA_TRY(launch_refresh_grid(o->fd, o->params.p, o->R, o->grid.p, o->flag.p, st));
+        c->launches += 1;
+      }
     }
-    {
-      ProfScope ps(c, PRENOM_K_COMPOSITE, st);
-      CUDA_TRY(launch_composite_group(reinterpret_cast<const CompositeArgs*>(base + sj), K, B, S, st));
-    }
-    {
-      ProfScope ps(c, PRENOM_K_MLP_BWD, st);
-      CUDA_TRY(launch_bwd_tc_group(o0->fd, gs->objs.p, K, ntiles, S, gs->ctr.p + 2, split, st));
-    }
-    {
-      ProfScope ps(c, PRENOM_K_ADAM, st);
-      CUDA_TRY(launch_adam_group(reinterpret_cast<const AdamJob*>(base + sj + cj), K, o0->P, st));
-    }
-    c->launches += 6;  // sample, fwd, composite, bwd, MLP-gradient reduce, Adam
-    for (int j : refresh[it]) {
-      prenom_object_s* o = g[j];
-      ProfScope ps(c, PRENOM_K_REFRESH, st);
-      CUDA_TRY(launch_refresh_grid(o->fd, o->params.p, o->R, o->grid.p, o->flag.p, st));
-      c->launches += 1;
-    }
+    for (auto* o : g) o->step += nc;
   }
-  for (auto* o : g) o->step += n_steps;
   return PRENOM_OK;
 }
 }  // namespace

@@ -118,3 +118,21 @@ def test_grouped_ragged_tiles_and_one_ray(ctx):
             assert la[0] == lb[0]
             for x, y in zip(la, lb):
                 assert abs(x["total"] - y["total"]) <= 2e-3 * abs(y["total"]) + 1e-9
+
+
+def test_grouped_long_call_spans_job_chunks(ctx):
+    """A 70-step call (job arrays uploaded 64 steps at a time): same keyframes and samples as
+    per-object training for every step, step counters advanced by 70, losses close."""
+    grouped = [make(ctx, ARCH_A, i, MLP_BF16X3, refresh=0, rays=64) for i in range(2)]
+    alone = [make(ctx, ARCH_A, i, MLP_BF16X3, refresh=0, rays=64) for i in range(2)]
+    ctx.set_grouping(True)
+    T.train_many(grouped, 70)
+    for o in alone:
+        o.train_step(70, stats=False)
+    for a, b in zip(grouped, alone):
+        assert a.step() == b.step() == 70
+        la, lb = a.last_stats(70), b.last_stats(70)
+        assert la[0] == lb[0]
+        for x, y in zip(la, lb):
+            assert x["frame"] == y["frame"] and x["n_samples"] == y["n_samples"]
+            assert abs(x["total"] - y["total"]) <= 2e-2 * abs(y["total"]) + 1e-9
