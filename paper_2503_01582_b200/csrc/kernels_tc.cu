@@ -887,9 +887,16 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_fwd_wx(FieldDesc fd, const fl
         nn = gobj[ej].n;
       }
       const long long gs = tl * kTile + s;
-      const bool valid = gs < nn && __ldg(cnt + ray_of(gs, S)) > 0;
+      // the position is loaded next to the ray's sample count, not after it (two
+      // independent L2 round trips instead of two serial ones); escaped rays'
+      // slots hold stale positions, which `valid` discards
       float4 pp = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (valid) pp = ps[gs];
+      bool valid = false;
+      if (gs < nn) {
+        pp = __ldg(ps + gs);
+        valid = __ldg(cnt + ray_of(gs, S)) > 0;
+      }
+      if (!valid) pp = make_float4(0.f, 0.f, 0.f, 0.f);
       const float px = clamp01(pp.x), py = clamp01(pp.y), pz = clamp01(pp.z);
       const uint32_t xb = tm + lane_base + kX0 + b * kXcols;
       for (int l = part; l < fd.L; l += TPS) {
@@ -1361,9 +1368,13 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
         nn = gobj[sj].n;
       }
       const long long gs = tl * kTile + r;
-      const bool valid = gs < nn && __ldg(cnt + ray_of(gs, S)) > 0;
-      float4 pp = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (valid) pp = ps[gs];
+      float4 pp = make_float4(0.f, 0.f, 0.f, 0.f);  // (loaded beside the count, as in the forward)
+      bool valid = false;
+      if (gs < nn) {
+        pp = __ldg(ps + gs);
+        valid = __ldg(cnt + ray_of(gs, S)) > 0;
+      }
+      if (!valid) pp = make_float4(0.f, 0.f, 0.f, 0.f);
       const float px = clamp01(pp.x), py = clamp01(pp.y), pz = clamp01(pp.z);
       // levels [lhalf*LH, (lhalf+1)*LH) belong to this half; the MLP warps
       // scatter the first mlp_levels of them. The level's pair is always
@@ -1516,11 +1527,15 @@ __global__ void __launch_bounds__(kBwdThreads, (SPL && H < 2) ? 1 : 2)
       }
       const int acc_it = GRP ? oit : iter;  // tiles already in the weight-gradient accumulators
       const long long gs = tl * kTile + row;
-      const bool valid = gs < nn && __ldg(cnt + ray_of(gs, S)) > 0;
-      // upstream gradient of this row, loaded now: its latency would otherwise sit
-      // on the chain at the g_raw epilogue (warps 0-3 own the rows there)
+      // upstream gradient of this row, loaded now (beside the count): its latency
+      // would otherwise sit on the chain at the g_raw epilogue (warps 0-3 own the rows there)
       float4 dpre = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (warp < 4 && valid) dpre = dp[gs];
+      bool valid = false;
+      if (gs < nn) {
+        if (warp < 4) dpre = __ldg(dp + gs);
+        valid = __ldg(cnt + ray_of(gs, S)) > 0;
+      }
+      if (!valid) dpre = make_float4(0.f, 0.f, 0.f, 0.f);
       // ---- stored bf16 features -> X by the TMA engine (no LSU work): one
       // bulk copy per 8-row group (the X row-group stride is longer: ones column)
       if (tid == 0 && !prefetched) fetch_x(t);  // ([X | 1]: the ones come with the tile)
