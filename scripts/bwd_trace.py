@@ -16,6 +16,7 @@ import bench  # noqa: E402
 from paper_2503_01582_b200 import Context, ObjectTrainer  # noqa: E402
 
 mode = sys.argv[1] if len(sys.argv) > 1 else "bf16x3"
+out_path = sys.argv[2] if len(sys.argv) > 2 else None
 group = int(os.environ.get("TRACE_GROUP", "0"))  # > 0: that many cfg4 objects through grouped launches
 sys.argv = ["bench.py", "--mlp", mode]
 args = bench.parse()
@@ -83,5 +84,5 @@ res["ctas"] = {"n": nc, "kernel_us": round((c[:, 3].max() - t0) / 1e3, 2),
                "tile_us_mean": round(float(np.mean((c[:, 2] - c[:, 1]) / np.maximum(c[:, 4], 1))) / 1e3, 3)}
 line = json.dumps(res)
 print(line)
-if len(sys.argv) > 2:
-    open(sys.argv[2], "w").write(line)
+if out_path:
+    open(out_path, "w").write(line)
