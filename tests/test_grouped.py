@@ -136,3 +136,27 @@ def test_grouped_long_call_spans_job_chunks(ctx):
         for x, y in zip(la, lb):
             assert x["frame"] == y["frame"] and x["n_samples"] == y["n_samples"]
             assert abs(x["total"] - y["total"]) <= 2e-2 * abs(y["total"]) + 1e-9
+
+
+def test_grouped_objects_at_different_steps_and_cadences(ctx):
+    """A group whose objects are at different steps (Adam bias corrections, keyframe picks,
+    Philox streams per object) and refresh their grids on different cadences."""
+    def pair(i, pre, refresh):
+        a = make(ctx, ARCH_A, i, MLP_BF16X3, refresh=refresh, rays=96)
+        b = make(ctx, ARCH_A, i, MLP_BF16X3, refresh=refresh, rays=96)
+        if pre:
+            a.train_step(pre, stats=False)
+            b.train_step(pre, stats=False)
+        return a, b
+    pairs_ = [pair(0, 0, 3), pair(1, 5, 4), pair(2, 2, 0)]
+    ctx.set_grouping(True)
+    T.train_many([a for a, _ in pairs_], 6)
+    for (a, b), pre in zip(pairs_, (0, 5, 2)):
+        b.train_step(6, stats=False)
+        assert a.step() == b.step() == pre + 6
+        la, lb = a.last_stats(6), b.last_stats(6)
+        assert la[0]["frame"] == lb[0]["frame"] and la[0]["n_samples"] == lb[0]["n_samples"]
+        assert abs(la[0]["total"] - lb[0]["total"]) <= 1e-5 * abs(lb[0]["total"])
+        for x, y in zip(la, lb):
+            assert x["frame"] == y["frame"]
+            assert abs(x["total"] - y["total"]) <= 5e-3 * abs(y["total"]) + 1e-9
