@@ -24,8 +24,8 @@ bool same_group(const prenom_object_s* a, const prenom_object_s* b) {
 // (mapper.cpp:182-183, per object). The launches cover every object's
 // train_track step exactly as enqueue_step would (same Philox streams, keyframe
 // picks, Adam corrections); only the MLP weight-gradient partials are summed in
-// a different CTA order. Per-step job arrays for the whole call are built on the
-// host and uploaded once.
+// a different CTA order. The object table is uploaded once per call, the per-step
+// job arrays once per kGroupJobChunk steps.
 prenom_status enqueue_group_steps(prenom_ctx_s* c, GroupScratch* gs, const std::vector<prenom_object_s*>& g,
                                   int n_steps, cudaStream_t st) {
   const int K = (int)g.size();
