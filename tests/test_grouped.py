@@ -160,3 +160,22 @@ def test_grouped_objects_at_different_steps_and_cadences(ctx):
         for x, y in zip(la, lb):
             assert x["frame"] == y["frame"]
             assert abs(x["total"] - y["total"]) <= 5e-3 * abs(y["total"]) + 1e-9
+
+
+@pytest.mark.parametrize("mlp", [MLP_BF16X3, MLP_BF16])
+def test_two_groups_of_different_archs(ctx, mlp):
+    """Two groups in one call (W32 H2 INP16 and W64 H1 INP32: the latter's split backward has no
+    feature overlay), on two lanes, each equal to per-object training."""
+    mk = lambda: ([make(ctx, ARCH_A, i, mlp, refresh=4) for i in range(2)]
+                  + [make(ctx, ARCH_B, 5 + i, mlp, refresh=4) for i in range(3)])
+    grouped, alone = mk(), mk()
+    ctx.set_grouping(True)
+    T.train_many(grouped, 6)
+    for o in alone:
+        o.train_step(6, stats=False)
+    for a, b in zip(grouped, alone):
+        la, lb = a.last_stats(6), b.last_stats(6)
+        assert la[0] == lb[0]
+        for x, y in zip(la, lb):
+            assert x["frame"] == y["frame"]
+            assert abs(x["total"] - y["total"]) <= 2e-3 * abs(y["total"]) + 1e-9
