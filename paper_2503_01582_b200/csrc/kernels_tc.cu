@@ -284,7 +284,8 @@ __device__ __forceinline__ uint64_t epi_relu_gate(uint32_t tm, const float* bias
     uint32_t pk[4], pl[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      const float a0 = fmaxf(v[2 * i] + bias[col + 2 * i], 0.f), a1 = fmaxf(v[2 * i + 1] + bias[col + 2 * i + 1], 0.f);
+      const float a0 = umma::operand_round(fmaxf(v[2 * i] + bias[col + 2 * i], 0.f)),
+                  a1 = umma::operand_round(fmaxf(v[2 * i + 1] + bias[col + 2 * i + 1], 0.f));
       const __nv_bfloat162 b = __floats2bfloat162_rn(a0, a1);
       pk[i] = *reinterpret_cast<const uint32_t*>(&b);
       if (LO) {
@@ -902,6 +903,8 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_fwd_wx(FieldDesc fd, const fl
       for (int l = part; l < fd.L; l += TPS) {
         float f[2] = {0.f, 0.f};
         if (valid) encode_level<2>(fd, prm, l, px, py, pz, f);
+        f[0] = umma::operand_round(f[0]);
+        f[1] = umma::operand_round(f[1]);
         const __nv_bfloat162 hi = __floats2bfloat162_rn(f[0], f[1]);
         umma::tmem_st1(xb + l, *reinterpret_cast<const uint32_t*>(&hi));
         if (SPL) {
@@ -936,7 +939,8 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_fwd_wx(FieldDesc fd, const fl
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             const int k = 8 * h + 2 * i;
-            const float a0 = fmaxf(v[k] + bias[c + k], 0.f), a1 = fmaxf(v[k + 1] + bias[c + k + 1], 0.f);
+            const float a0 = umma::operand_round(fmaxf(v[k] + bias[c + k], 0.f)),
+                        a1 = umma::operand_round(fmaxf(v[k + 1] + bias[c + k + 1], 0.f));
             const __nv_bfloat162 hh = __floats2bfloat162_rn(a0, a1);
             hi[i] = *reinterpret_cast<const uint32_t*>(&hh);
             if (SPL) {

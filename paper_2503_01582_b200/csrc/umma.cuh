@@ -246,7 +246,21 @@ __device__ __forceinline__ void st_row8(unsigned char* tile, int r, int c0, int 
 // every MMA stays kind::f16 at full bf16 tensor rate. The lo copy of a tile sits
 // `lo_off` bytes after the hi copy, so its descriptor is the hi descriptor plus
 // lo_off >> 4 in the start-address field.
+// Numerics experiment (-DPRENOM_TF32_EMUL, never in the product build): every MLP
+// operand rounded to tf32 (cvt.rna) before the hi/lo split, so the split MMAs
+// compute exact products of tf32 operands -- what a kind::tf32 MLP would do.
+__device__ __forceinline__ float operand_round(float x) {
+#ifdef PRENOM_TF32_EMUL
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+#else
+  return x;
+#endif
+}
+
 __device__ __forceinline__ void split_bf16(float x, __nv_bfloat16& hi, __nv_bfloat16& lo) {
+  x = operand_round(x);
   hi = __float2bfloat16_rn(x);
   lo = __float2bfloat16_rn(x - __bfloat162float(hi));
 }
