@@ -601,8 +601,21 @@ __global__ void __launch_bounds__(NT) k_fwd_ts(FieldDesc fd, const float* __rest
 // mbarriers); 4 MLP warps (one row per thread: TMEM lane quadrant = warp % 4)
 // issue the MMAs, run the epilogues through TMEM and write (sigma, rgb).
 // Tiles are claimed one ahead by the encode leader.
-constexpr int kWsEncWarps = 16;  // k_fwd_wx's shape (k_fwd_ws's default)
+constexpr int kWsEncWarps = 16;  // k_fwd_ws's default shape
 constexpr int kWsThreads = (kWsEncWarps + 4) * 32;
+// k_fwd_wx's shape: encode warps + MLP warps (4 per epilogue column group). With
+// two hidden layers the MLP chain bounds the split forward (cfg2: 0.124 ms without
+// the layers after L0, 0.186 with them), so half the encoders make room for a
+// second MLP warp per TMEM lane quadrant, each taking half the epilogue columns
+// (cfg2 0.186 -> 0.175 ms, cfg1 0.052 -> 0.047; 12 + 8: 0.178; 16 + 8 spills at
+// 40 registers: 0.191); one hidden layer keeps 16 + 4 (cfg3 / cfg5 archs are
+// encode-bound: 8 + 8 is 1-6% slower there).
+template <int H>
+struct WxShape {
+  static constexpr int kEnc = H >= 2 ? 8 : 16;
+  static constexpr int kMlp = H >= 2 ? 8 : 4;
+  static constexpr int kThreads = (kEnc + kMlp) * 32;
+};
 
 // NE encode warps (a multiple of 4: NE/4 threads per sample), MINB CTAs per SM.
 template <int INP, int W, int H, int SPL, int NE = 16, int MINB = 2>
@@ -806,14 +819,18 @@ __global__ void __launch_bounds__((NE + 4) * 32, MINB) k_fwd_ws(FieldDesc fd, co
 // x 128; the per-object arguments are unused): the MLP warps reload the weight
 // tiles when their tile's object changes.
 template <int INP, int W, int H, int SPL, bool GRP = false>
-__global__ void __launch_bounds__(kWsThreads, 2) k_fwd_wx(FieldDesc fd, const float* __restrict__ params,
+__global__ void __launch_bounds__(WxShape<H>::kThreads, 2) k_fwd_wx(FieldDesc fd, const float* __restrict__ params,
                                                        long long n_total, int S, const int* __restrict__ count,
                                                        const float4* __restrict__ pos, uint4* __restrict__ feat_tiles,
                                                        float4* __restrict__ out, int* flag, int* tile_ctr, int split,
                                                        const TcObj* __restrict__ gobj, int nobj) {
   using WT = WeightTiles<INP, W, H, SPL>;
-  constexpr int kEnc = kWsEncWarps * 32;
+  constexpr int kWxEncWarps = WxShape<H>::kEnc, kWxMlpWarps = WxShape<H>::kMlp, kWxThreads = WxShape<H>::kThreads;
+  constexpr int kEnc = kWxEncWarps * 32;
   constexpr int TPS = kEnc / 128;
+  constexpr int kMlpT = kWxMlpWarps * 32;  // MLP threads
+  constexpr int MG = kWxMlpWarps / 4;      // epilogue column groups per TMEM lane quadrant
+  static_assert(kEnc % 128 == 0 && kWxMlpWarps % 4 == 0 && (W / MG) % 16 == 0, "k_fwd_wx shape");
   constexpr int XC = INP + 8;  // stored-tile row width ([X | 1])
   constexpr int kHhi = W, kHlo = W + W / 2;
   constexpr int kX0 = 2 * W;            // X[b] hi at kX0 + b * INP, lo at + INP / 2
@@ -830,8 +847,8 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_fwd_wx(FieldDesc fd, const fl
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const long long ntiles = (n_total + kTile - 1) / kTile;
   pdl_wait();  // params come from the previous step's Adam
-  if (!GRP) wt.load(fd, params + fd.hash_params, kWsThreads);
-  if (warp == kWsEncWarps) umma::tmem_alloc(&tbase, kCols);
+  if (!GRP) wt.load(fd, params + fd.hash_params, kWxThreads);
+  if (warp == kWxEncWarps) umma::tmem_alloc(&tbase, kCols);
   if (tid == 0) {
     for (int b = 0; b < 2; ++b) {
       umma::mbar_init(&full[b], kEnc);
@@ -846,7 +863,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_fwd_wx(FieldDesc fd, const fl
   umma::fence_after_sync();
   const uint32_t tm = tbase;
   const uint32_t lane_base = (uint32_t)(32 * (warp & 3)) << 16;
-  if (warp < kWsEncWarps) {
+  if (warp < kWxEncWarps) {
     // padding levels (L*F < INP) stay zero in both buffers: written once here
     const int part = tid >> 7;
     for (int b = 0; b < 2; ++b)
@@ -856,7 +873,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_fwd_wx(FieldDesc fd, const fl
       }
     umma::tmem_wait_st();
   }
-  if (warp < kWsEncWarps) {
+  if (warp < kWxEncWarps) {
     // ================= encode warps: features -> TMEM X[b]
     const int s = tid & (kTile - 1), part = tid >> 7;
     int ej = 0;
@@ -918,18 +935,18 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_fwd_wx(FieldDesc fd, const fl
     }
   } else {
     // ================= MLP warps: one row per thread
-    const int q = warp & 3, row = 32 * q + lane, mt = tid - kEnc;
+    const int q = warp & 3, row = 32 * q + lane, mt = tid - kEnc, cg = mt >> 7;  // cg: column group
     uint32_t phase = 0;
     constexpr uint32_t id_h = umma::idesc_bf16(128, W, false, false);
     constexpr uint32_t id_out = umma::idesc_bf16(128, 16, false, false);
     auto mlp_sync = [&]() {
       umma::fence_before_sync();
-      named_sync(1, 128);
+      named_sync(1, kMlpT);
       umma::fence_after_sync();
     };
     auto epilogue = [&](const float* bias) {
 #pragma unroll
-      for (int c = 0; c < W; c += 16) {
+      for (int c = cg * (W / MG); c < (cg + 1) * (W / MG); c += 16) {
         float v[16];
         umma::tmem_ld16(tm + lane_base + c, v);
         umma::tmem_wait_ld();
@@ -969,9 +986,9 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_fwd_wx(FieldDesc fd, const fl
       if (GRP) {
         const int j = find_obj(gobj, nobj, t, mj);
         if (j != mj) {  // no MMA is in flight: the previous tile's output layer was waited for
-          wt.load(fd, gobj[j].params + fd.hash_params, 128, mt);
+          wt.load(fd, gobj[j].params + fd.hash_params, kMlpT, mt);
           umma::fence_proxy_async();
-          named_sync(1, 128);
+          named_sync(1, kMlpT);
           mj = j;
         }
         cnt = gobj[j].count;
@@ -995,6 +1012,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_fwd_wx(FieldDesc fd, const fl
                              (row >> 3) * (XC / 8) * 128 + (row & 7) * 16;
 #pragma unroll
         for (int h = 0; h < (SPL ? 2 : 1); ++h) {
+          if (MG > 1 && h % MG != cg) continue;  // (column groups share the hi / lo halves)
           float v[INP / 2];
           if (INP / 2 == 16) {
             umma::tmem_ld16(tm + lane_base + kX0 + b * kXcols + h * (INP / 2), v);
@@ -1012,7 +1030,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_fwd_wx(FieldDesc fd, const fl
       wait_mma(&bar, phase);
       // the layer-0 MMA and the copy-out have read X[b]: the encoders may refill it
       umma::fence_before_sync();
-      named_sync(1, 128);
+      named_sync(1, kMlpT);
       if (mt == 0) umma::mbar_arrive_plain(&empty[b]);
       umma::fence_after_sync();
       epilogue(wt.bias);
@@ -1037,7 +1055,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_fwd_wx(FieldDesc fd, const fl
       umma::tmem_ld8(tm + lane_base, v);
       umma::tmem_wait_ld();
       const long long gs = tl * kTile + row;
-      if (gs < nn) {
+      if (cg == 0 && gs < nn) {
         float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
         if (__ldg(cnt + ray_of(gs, S)) > 0) {
           const float* bb = wt.bias + H * W;
@@ -1055,7 +1073,7 @@ __global__ void __launch_bounds__(kWsThreads, 2) k_fwd_wx(FieldDesc fd, const fl
   umma::fence_before_sync();
   __syncthreads();
   tile_sched_exit(tile_ctr);
-  if (warp == kWsEncWarps) umma::tmem_dealloc(tm, kCols);
+  if (warp == kWxEncWarps) umma::tmem_dealloc(tm, kCols);
 }
 
 // One level of the table-gradient scatter for the 32 consecutive samples of a
@@ -1884,7 +1902,7 @@ cudaError_t run_fwd_nt(const FieldDesc& fd, const float* params, long long n, in
     auto kx = k_fwd_wx<INP, W, H, SPL>;
     cudaError_t e = set_attrs(kx, smem, carveout);
     if (e != cudaSuccess) return e;
-    return launch_pdl(kx, dim3((unsigned)grid), dim3(nthreads), smem, st, fd, params, n, S, count, pos,
+    return launch_pdl(kx, dim3((unsigned)grid), dim3(WxShape<H>::kThreads), smem, st, fd, params, n, S, count, pos,
                       reinterpret_cast<uint4*>(feat_tiles), out, flag, tile_ctr, split, (const TcObj*)nullptr, 0);
   }
   cudaError_t e = set_attrs(kern, smem, carveout);
@@ -1903,7 +1921,7 @@ cudaError_t run_fwd_grp(const FieldDesc& fd, const TcObj* objs, int nobj, long l
   cudaError_t e = set_attrs(kx, smem, carve);
   if (e != cudaSuccess) return e;
   const long long grid = std::min<long long>((ntiles + min_tiles_per_cta() - 1) / min_tiles_per_cta(), 2LL * sms());
-  return launch_pdl(kx, dim3((unsigned)grid), dim3(kWsThreads), smem, st, fd, (const float*)nullptr, ntiles * kTile,
+  return launch_pdl(kx, dim3((unsigned)grid), dim3(WxShape<H>::kThreads), smem, st, fd, (const float*)nullptr, ntiles * kTile,
                     S, (const int*)nullptr, (const float4*)nullptr, (uint4*)nullptr, (float4*)nullptr, (int*)nullptr,
                     ctr, split, objs, nobj);
 }
