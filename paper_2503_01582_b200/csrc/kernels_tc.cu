@@ -831,6 +831,14 @@ __global__ void __launch_bounds__(WxShape<H>::kThreads, 2) k_fwd_wx(FieldDesc fd
   constexpr int kMlpT = kWxMlpWarps * 32;  // MLP threads
   constexpr int MG = kWxMlpWarps / 4;      // epilogue column groups per TMEM lane quadrant
   static_assert(kEnc % 128 == 0 && kWxMlpWarps % 4 == 0 && (W / MG) % 16 == 0, "k_fwd_wx shape");
+  // Where the MLP chain bounds the forward (two hidden layers) and each of a sample's TPS
+  // encode threads gets at least two 4-level chunks (one 16-byte core-matrix row of the
+  // stored tile each; chunk c goes to part c % TPS, so a thread mixes coarse and fine
+  // levels), the encoders store the backward's features themselves and the MLP warps skip
+  // the copy-out (cfg2 forward 0.1752 -> 0.1725 ms; on the encode-bound one-hidden-layer
+  // archs and on one chunk per thread it costs 1-5%).
+  constexpr int NCH = INP / 8;
+  constexpr bool kEncStores = H >= 2 && NCH % TPS == 0 && NCH / TPS >= 2;
   constexpr int XC = INP + 8;  // stored-tile row width ([X | 1])
   constexpr int kHhi = W, kHlo = W + W / 2;
   constexpr int kX0 = 2 * W;            // X[b] hi at kX0 + b * INP, lo at + INP / 2
@@ -917,16 +925,47 @@ __global__ void __launch_bounds__(WxShape<H>::kThreads, 2) k_fwd_wx(FieldDesc fd
       if (!valid) pp = make_float4(0.f, 0.f, 0.f, 0.f);
       const float px = clamp01(pp.x), py = clamp01(pp.y), pz = clamp01(pp.z);
       const uint32_t xb = tm + lane_base + kX0 + b * kXcols;
-      for (int l = part; l < fd.L; l += TPS) {
-        float f[2] = {0.f, 0.f};
-        if (valid) encode_level<2>(fd, prm, l, px, py, pz, f);
-        f[0] = umma::operand_round(f[0]);
-        f[1] = umma::operand_round(f[1]);
-        const __nv_bfloat162 hi = __floats2bfloat162_rn(f[0], f[1]);
-        umma::tmem_st1(xb + l, *reinterpret_cast<const uint32_t*>(&hi));
-        if (SPL) {
-          const __nv_bfloat162 lo = __floats2bfloat162_rn(f[0] - __low2float(hi), f[1] - __high2float(hi));
-          umma::tmem_st1(xb + INP / 2 + l, *reinterpret_cast<const uint32_t*>(&lo));
+      if constexpr (kEncStores) {
+        uint4* fbp = feat_tiles;
+        if (GRP) fbp = reinterpret_cast<uint4*>(gobj[ej].feat);
+        unsigned char* dst = reinterpret_cast<unsigned char*>(fbp) + (size_t)tl * (128 * XC * 2 * (SPL ? 2 : 1)) +
+                             (s >> 3) * (XC / 8) * 128 + (s & 7) * 16;
+#pragma unroll 1
+        for (int ch = part; ch < NCH; ch += TPS) {
+          uint32_t hi4[4], lo4[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const int l = 4 * ch + k;
+            float f[2] = {0.f, 0.f};
+            if (valid && l < fd.L) encode_level<2>(fd, prm, l, px, py, pz, f);
+            f[0] = umma::operand_round(f[0]);
+            f[1] = umma::operand_round(f[1]);
+            const __nv_bfloat162 hi = __floats2bfloat162_rn(f[0], f[1]);
+            hi4[k] = *reinterpret_cast<const uint32_t*>(&hi);
+            if (SPL) {
+              const __nv_bfloat162 lo = __floats2bfloat162_rn(f[0] - __low2float(hi), f[1] - __high2float(hi));
+              lo4[k] = *reinterpret_cast<const uint32_t*>(&lo);
+            }
+          }
+          umma::tmem_st4(xb + 4 * ch, hi4);
+          *reinterpret_cast<uint4*>(dst + ch * 128) = make_uint4(hi4[0], hi4[1], hi4[2], hi4[3]);
+          if (SPL) {
+            umma::tmem_st4(xb + INP / 2 + 4 * ch, lo4);
+            *reinterpret_cast<uint4*>(dst + 128 * XC * 2 + ch * 128) = make_uint4(lo4[0], lo4[1], lo4[2], lo4[3]);
+          }
+        }
+      } else {
+        for (int l = part; l < fd.L; l += TPS) {
+          float f[2] = {0.f, 0.f};
+          if (valid) encode_level<2>(fd, prm, l, px, py, pz, f);
+          f[0] = umma::operand_round(f[0]);
+          f[1] = umma::operand_round(f[1]);
+          const __nv_bfloat162 hi = __floats2bfloat162_rn(f[0], f[1]);
+          umma::tmem_st1(xb + l, *reinterpret_cast<const uint32_t*>(&hi));
+          if (SPL) {
+            const __nv_bfloat162 lo = __floats2bfloat162_rn(f[0] - __low2float(hi), f[1] - __high2float(hi));
+            umma::tmem_st1(xb + INP / 2 + l, *reinterpret_cast<const uint32_t*>(&lo));
+          }
         }
       }
       umma::tmem_wait_st();
@@ -1005,9 +1044,10 @@ __global__ void __launch_bounds__(WxShape<H>::kThreads, 2) k_fwd_wx(FieldDesc fd
           umma::mma_split_ts(tm, xa + ks * 8, umma::desc_kmajor(wt.w0, INP, ks), id_h, ks > 0, sp, INP / 2, WT::kLo);
         umma::commit(&bar);
       }
-      // stored features for the backward: this thread's row from TMEM into the [X | 1]
-      // slots of the stored tile (16-byte stores; the ones columns were written once)
-      {
+      // stored features for the backward (unless the encoders stored them): this thread's
+      // row from TMEM into the [X | 1] slots of the stored tile (16-byte stores; the ones
+      // columns were written once)
+      if (!kEncStores) {
         unsigned char* dst = reinterpret_cast<unsigned char*>(fb) + (size_t)tl * (128 * XC * 2 * (SPL ? 2 : 1)) +
                              (row >> 3) * (XC / 8) * 128 + (row & 7) * 16;
 #pragma unroll
