@@ -4,6 +4,7 @@
 //   k_reptile_*       reptile_update (meta.cpp:83-92), its delta/apply split for NCCL
 //   k_philox          Philox4x32-10 known-answer entry point
 #include <algorithm>
+#include <cstdlib>
 
 #include "prenom_device.cuh"
 
@@ -186,7 +187,15 @@ int num_sms() {
 cudaError_t launch_adam(size_t n, float* p, float* g, float* m, float* v, float lr, float b1, float b2, float eps,
                         float c1, float c2, int zero_grad, cudaStream_t st) {
   const size_t n4 = std::max<size_t>(n / 4, 1);
-  const unsigned grid = (unsigned)std::min<size_t>((n4 + 255) / 256, (size_t)num_sms() * 8);
+  // blocks per SM (4 resident at 64 registers): 20 for a step that has the GPU to itself
+  // (cfg2: 0.1053 -> 0.1011 ms vs 8; 16-48 within 1%), 8 beside concurrent objects' kernels
+  // on the lane streams (cfg3 0.9% slower at 24); PRENOM_ADAM_BLOCKS_PER_SM overrides
+  static const int per_sm_env = [] {
+    const char* e = getenv("PRENOM_ADAM_BLOCKS_PER_SM");
+    return e ? atoi(e) : 0;
+  }();
+  const int per_sm = per_sm_env > 0 ? per_sm_env : (tc_concurrent_objects() ? 8 : 20);
+  const unsigned grid = (unsigned)std::min<size_t>((n4 + 255) / 256, (size_t)num_sms() * per_sm);
   return launch_pdl(k_adam, dim3(grid), dim3(256), 0, st, n, p, g, m, v, lr, b1, b2, eps, c1, c2, zero_grad);
 }
 

@@ -2107,6 +2107,7 @@ cudaError_t run_bwd(const FieldDesc& fd, const float* params, float* grad, long 
 // On by default (cfg2, B200, interleaved 3x: 0.7001 -> 0.6940 ms/step);
 // PRENOM_NO_PDL=1 disables for A/B.
 void tc_set_min_tiles_per_cta(int v) { t_min_tiles = v < 1 ? 1 : v; }
+bool tc_concurrent_objects() { return t_min_tiles > 1; }
 
 bool pdl_enabled() {
   static const bool on = getenv("PRENOM_NO_PDL") == nullptr;

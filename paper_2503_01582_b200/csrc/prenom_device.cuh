@@ -464,6 +464,7 @@ cudaError_t run_marching_cubes(const float* d_grid, int R, float iso, McScratch&
 bool tc_supported(const FieldDesc& fd);
 cudaError_t tc_bwd_trace(long long* mlp /* 64 x 16 */, long long* scat /* 64 x 4 */, long long* cta /* 1024 x 5 */);
 void tc_set_min_tiles_per_cta(int v);  // persistent-grid hint for the calling host thread (multi-object)
+bool tc_concurrent_objects();          // that hint is set: objects run concurrently on lane streams
 size_t tc_feature_bytes(const FieldDesc& fd, long long n, int split);
 // writes the constant ones / zero core matrices of a stored-feature buffer (once per allocation)
 cudaError_t init_feature_tiles(const FieldDesc& fd, void* feat, size_t bytes, int split, cudaStream_t st);
