@@ -518,6 +518,7 @@ inline prenom_status enqueue_step(prenom_object_s* o, StepStatsDev* stats, bool 
   }
   o->upload_pending = false;  // any later sampling is ordered after this step's
   const bool tc = uses_tc(o);
+  int mlp_nparts = 0;  // per-CTA MLP-gradient partials the backward left for Adam
   {
     ProfScope ps(o->ctx, PRENOM_K_FIELD_FWD, st);
     if (tc)
@@ -533,9 +534,10 @@ inline prenom_status enqueue_step(prenom_object_s* o, StepStatsDev* stats, bool 
   }
   if (tc) {
     ProfScope ps(o->ctx, PRENOM_K_MLP_BWD, st);  // MLP backward + fused table-gradient scatter
+    // (the MLP-gradient reduction is folded into this step's Adam: launch_adam_fused)
     CUDA_TRY(launch_bwd_tc(o->fd, o->params.p, o->grad.p, (long long)B * S, S, sb.count, sb.pos_depth,
                            o->feat_tc.p, o->dout.p, o->tile_ctr.p + 2, tc_split(o), o->mlp_part.p, o->mlp_part.n,
-                           st));
+                           st, &mlp_nparts));
   } else {
     {
       ProfScope ps(o->ctx, PRENOM_K_MLP_BWD, st);
@@ -566,10 +568,17 @@ inline prenom_status enqueue_step(prenom_object_s* o, StepStatsDev* stats, bool 
   adam_corrections(o, o->step, c1, c2);
   {
     ProfScope ps(o->ctx, PRENOM_K_ADAM, st);
-    CUDA_TRY(launch_adam(o->P, o->params.p, o->grad.p, o->m.p, o->v.p, c.eta, c.adam_beta1, c.adam_beta2,
-                         c.adam_eps, c1, c2, 1, st));
+    if (mlp_nparts > 0)
+      CUDA_TRY(launch_adam_fused(o->P, (size_t)o->fd.hash_params, o->fd.mlp_params, o->params.p, o->grad.p, o->m.p,
+                                 o->v.p, c.eta, c.adam_beta1, c.adam_beta2, c.adam_eps, c1, c2, o->mlp_part.p,
+                                 mlp_nparts, st));
+    else
+      CUDA_TRY(launch_adam(o->P, o->params.p, o->grad.p, o->m.p, o->v.p, c.eta, c.adam_beta1, c.adam_beta2,
+                           c.adam_eps, c1, c2, 1, st));
   }
-  o->ctx->launches += tc ? 6 : 6;  // sample, fwd, composite, bwd + MLP-gradient reduce (or encode_bwd), adam
+  // sample, fwd, composite, bwd (+ encode_bwd on the SIMT path, + the MLP-gradient reduce when it was not
+  // folded into Adam), adam
+  o->ctx->launches += (tc && mlp_nparts > 0) ? 5 : 6;
   o->step += 1;
   // grid refresh every m iterations (mapper.cpp:182-183)
   if (c.grid_refresh_every > 0 && o->step % c.grid_refresh_every == 0) {

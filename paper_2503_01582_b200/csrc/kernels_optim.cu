@@ -26,11 +26,15 @@ __device__ __forceinline__ void adam1(float& p, float& g, float& m, float& v, fl
 
 __device__ __forceinline__ void adam_body(size_t n, float* __restrict__ p, float* __restrict__ g,
                                           float* __restrict__ m, float* __restrict__ v, float lr, float b1, float b2,
-                                          float eps, float c1, float c2, int zero_grad) {
+                                          float eps, float c1, float c2, int zero_grad, int bid = -1, int nblk = -1) {
+  if (bid < 0) {
+    bid = blockIdx.x;
+    nblk = gridDim.x;
+  }
   const size_t n4 = n / 4;
-  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  const size_t stride = (size_t)nblk * blockDim.x;
   // two float4 groups per thread per iteration: 8 independent 16 B loads in flight
-  for (size_t i0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n4; i0 += 2 * stride) {
+  for (size_t i0 = (size_t)bid * blockDim.x + threadIdx.x; i0 < n4; i0 += 2 * stride) {
     float4 pp[2], gg[2], mm[2], vv[2];
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
@@ -57,7 +61,7 @@ __device__ __forceinline__ void adam_body(size_t n, float* __restrict__ p, float
       }
     }
   }
-  if (blockIdx.x == 0 && threadIdx.x < n - n4 * 4) {
+  if (bid == 0 && threadIdx.x < n - n4 * 4) {
     const size_t i = n4 * 4 + threadIdx.x;
     float gi = g[i];
     adam1(p[i], gi, m[i], v[i], lr, b1, b2, eps, c1, c2);
@@ -70,6 +74,46 @@ __global__ void __launch_bounds__(256) k_adam(size_t n, float* __restrict__ p, f
                                               float b2, float eps, float c1, float c2, int zero_grad) {
   pdl_wait();  // the backward's gradient
   adam_body(n, p, g, m, v, lr, b1, b2, eps, c1, c2, zero_grad);
+}
+
+// Adam + the backward's MLP-gradient reduction (k_mlp_grad_reduce's job): blocks
+// [0, nmlp) each reduce 32 MLP parameters over the nparts per-CTA partials (8 row
+// groups per parameter, summed in fixed order: deterministic) and update them; the
+// remaining blocks run the dense Adam over the hash table [0, hash_params). The
+// reducing blocks come first, so they run in the first wave under the table stream.
+__global__ void __launch_bounds__(256) k_adam_fused(size_t hash_params, int mlp_params, float* __restrict__ p,
+                                                    float* __restrict__ g, float* __restrict__ m,
+                                                    float* __restrict__ v, float lr, float b1, float b2, float eps,
+                                                    float c1, float c2, const float* __restrict__ part, int nparts,
+                                                    int nmlp) {
+  pdl_wait();  // the backward's table gradient and partials
+  if ((int)blockIdx.x >= nmlp) {
+    adam_body(hash_params, p, g, m, v, lr, b1, b2, eps, c1, c2, 1, (int)blockIdx.x - nmlp, (int)gridDim.x - nmlp);
+    return;
+  }
+  __shared__ float red[8][33];
+  const int c = threadIdx.x & 31, grp = threadIdx.x >> 5;
+  const int k = blockIdx.x * 32 + c;
+  float a0 = 0.f, a1 = 0.f;
+  if (k < mlp_params) {
+    int r = grp;
+    for (; r + 8 < nparts; r += 16) {
+      a0 += part[(size_t)r * mlp_params + k];
+      a1 += part[(size_t)(r + 8) * mlp_params + k];
+    }
+    if (r < nparts) a0 += part[(size_t)r * mlp_params + k];
+  }
+  red[grp][c] = a0 + a1;
+  __syncthreads();
+  if (grp == 0 && k < mlp_params) {
+    float acc = red[0][c];
+#pragma unroll
+    for (int q = 1; q < 8; ++q) acc += red[q][c];
+    const size_t i = hash_params + k;
+    float gi = g[i] + acc;
+    adam1(p[i], gi, m[i], v[i], lr, b1, b2, eps, c1, c2);
+    g[i] = 0.f;
+  }
 }
 
 // grouped (multi-object scheduler): blockIdx.y = object
@@ -197,6 +241,23 @@ cudaError_t launch_adam(size_t n, float* p, float* g, float* m, float* v, float 
   const int per_sm = per_sm_env > 0 ? per_sm_env : (tc_concurrent_objects() ? 8 : 20);
   const unsigned grid = (unsigned)std::min<size_t>((n4 + 255) / 256, (size_t)num_sms() * per_sm);
   return launch_pdl(k_adam, dim3(grid), dim3(256), 0, st, n, p, g, m, v, lr, b1, b2, eps, c1, c2, zero_grad);
+}
+
+cudaError_t launch_adam_fused(size_t n, size_t hash_params, int mlp_params, float* p, float* g, float* m, float* v,
+                              float lr, float b1, float b2, float eps, float c1, float c2, const float* part,
+                              int nparts, cudaStream_t st) {
+  if (!part || nparts <= 0 || hash_params % 4 != 0 || n != hash_params + (size_t)mlp_params)
+    return cudaErrorInvalidValue;
+  static const int per_sm_env = [] {
+    const char* e = getenv("PRENOM_ADAM_BLOCKS_PER_SM");
+    return e ? atoi(e) : 0;
+  }();
+  const int per_sm = per_sm_env > 0 ? per_sm_env : (tc_concurrent_objects() ? 8 : 20);
+  const size_t n4 = std::max<size_t>(hash_params / 4, 1);
+  const unsigned gmain = (unsigned)std::min<size_t>((n4 + 255) / 256, (size_t)num_sms() * per_sm);
+  const int nmlp = (mlp_params + 31) / 32;
+  return launch_pdl(k_adam_fused, dim3(gmain + (unsigned)nmlp), dim3(256), 0, st, hash_params, mlp_params, p, g, m, v,
+                    lr, b1, b2, eps, c1, c2, part, nparts, nmlp);
 }
 
 cudaError_t launch_adam_group(const AdamJob* jobs_dev, int njobs, size_t n_max, cudaStream_t st) {

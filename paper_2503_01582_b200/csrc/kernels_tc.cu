@@ -2007,7 +2007,7 @@ cudaError_t run_fwd(const FieldDesc& fd, const float* params, long long n, int S
 template <int INP, int W, int H, int SPL>
 cudaError_t run_bwd_s(const FieldDesc& fd, const float* params, float* grad, long long n, int S, const int* count,
                       const float4* pos, const void* feat_tiles, const float4* dout, int* tile_ctr, int split,
-                      float* mlp_part, size_t part_cap, cudaStream_t st) {
+                      float* mlp_part, size_t part_cap, int* defer_nparts, cudaStream_t st) {
   // plain bf16: two CTAs (2 x 256 TMEM columns) per SM, the shared-memory
   // floor keeps a third CTA out; PRENOM_BWD_SMEM_KB / PRENOM_BWD_CARVEOUT for tuning
   static const size_t min_smem = (size_t)env_int("PRENOM_BWD_SMEM_KB", SPL ? 0 : 80) * 1024;
@@ -2037,7 +2037,8 @@ cudaError_t run_bwd_s(const FieldDesc& fd, const float* params, float* grad, lon
   cudaError_t e2 = launch_pdl(kern, dim3((unsigned)grid), dim3(kBwdThreads), smem, st, fd, params, grad, n, S, count,
                               pos, reinterpret_cast<const uint4*>(feat_tiles), dout, tile_ctr, skip, mlp_levels,
                               pull_max, split, wait_mode, part, (const TcObj*)nullptr, 0, (int*)nullptr);
-  if (e2 != cudaSuccess || !part) return e2;
+  if (defer_nparts) *defer_nparts = part ? (int)grid : 0;  // the caller's Adam sums the partials
+  if (e2 != cudaSuccess || !part || defer_nparts) return e2;
   return launch_pdl(k_mlp_grad_reduce, dim3((unsigned)((fd.mlp_params + 31) / 32)), dim3(1024), 0, st,
                     (const float*)part, (int)grid, fd.mlp_params, grad + fd.hash_params);
 }
@@ -2080,12 +2081,12 @@ cudaError_t run_bwd_grp(const FieldDesc& fd, const TcObj* objs, int nobj, long l
 template <int INP, int W, int H>
 cudaError_t run_bwd(const FieldDesc& fd, const float* params, float* grad, long long n, int S, const int* count,
                     const float4* pos, const void* feat_tiles, const float4* dout, int* tile_ctr, int split,
-                    float* mlp_part, size_t part_cap, cudaStream_t st) {
+                    float* mlp_part, size_t part_cap, int* defer_nparts, cudaStream_t st) {
   if (split)
     return run_bwd_s<INP, W, H, 1>(fd, params, grad, n, S, count, pos, feat_tiles, dout, tile_ctr, split, mlp_part,
-                                   part_cap, st);
+                                   part_cap, defer_nparts, st);
   return run_bwd_s<INP, W, H, 0>(fd, params, grad, n, S, count, pos, feat_tiles, dout, tile_ctr, 0, mlp_part,
-                                 part_cap, st);
+                                 part_cap, defer_nparts, st);
 }
 
 #define PRENOM_TC_DISPATCH(FN, ...)                                                          \
@@ -2179,12 +2180,14 @@ cudaError_t launch_bwd_tc_group(const FieldDesc& fd, const TcObj* objs, int nobj
 
 cudaError_t launch_bwd_tc(const FieldDesc& fd, const float* params, float* grad, long long n, int S,
                           const int* count, const float4* pos, const void* feat_tiles, const float4* dout,
-                          int* tile_ctr, int split, float* mlp_part, size_t part_cap, cudaStream_t st) {
+                          int* tile_ctr, int split, float* mlp_part, size_t part_cap, cudaStream_t st,
+                          int* defer_nparts) {
+  if (defer_nparts) *defer_nparts = 0;
   if (n <= 0) return cudaSuccess;
   if (n + kTile >= (1LL << 31)) return cudaErrorInvalidValue;  // ray_of's 32-bit slot index
   split = split_mask(split);
   PRENOM_TC_DISPATCH(run_bwd, fd, params, grad, n, S, count, pos, feat_tiles, dout, tile_ctr, split, mlp_part,
-                     part_cap, st);
+                     part_cap, defer_nparts, st);
 }
 
 }  // namespace prenom

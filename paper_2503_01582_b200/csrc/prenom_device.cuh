@@ -374,6 +374,12 @@ cudaError_t launch_encode_bwd(const FieldDesc& fd, const float* params, float* g
                               cudaStream_t st);
 cudaError_t launch_adam(size_t n, float* p, float* g, float* m, float* v, float lr, float b1,
                         float b2, float eps, float c1, float c2, int zero_grad, cudaStream_t st);
+// Adam with the backward's MLP-gradient reduction folded in: the MLP block's gradient is
+// the sum of nparts per-CTA partials (part, [nparts][P_mlp]), summed by the first blocks
+// of the launch while the others stream the hash table
+cudaError_t launch_adam_fused(size_t n, size_t hash_params, int mlp_params, float* p, float* g, float* m, float* v,
+                              float lr, float b1, float b2, float eps, float c1, float c2, const float* part,
+                              int nparts, cudaStream_t st);
 // grouped Adam (gradient zeroed): one job per object, blockIdx.y = job
 struct AdamJob {
   size_t n;
@@ -472,9 +478,13 @@ cudaError_t init_feature_tiles(const FieldDesc& fd, void* feat, size_t bytes, in
 cudaError_t launch_fwd_tc(const FieldDesc& fd, const float* params, long long n, int S, const int* count,
                           const float4* pos, void* feat_tiles, float4* out, int* flag, int* tile_ctr, int split,
                           cudaStream_t st);
+// defer_nparts (optional): do not launch the MLP-gradient reduction; *defer_nparts =
+// the number of per-CTA partials left in mlp_part (0: flushed with atomics), for
+// launch_adam_fused to sum
 cudaError_t launch_bwd_tc(const FieldDesc& fd, const float* params, float* grad, long long n, int S,
                           const int* count, const float4* pos, const void* feat_tiles, const float4* dout,
-                          int* tile_ctr, int split, float* mlp_part, size_t part_cap, cudaStream_t st);
+                          int* tile_ctr, int split, float* mlp_part, size_t part_cap, cudaStream_t st,
+                          int* defer_nparts = nullptr);
 // floats of per-CTA MLP-gradient partials launch_bwd_tc can use (else it flushes with atomics)
 size_t tc_mlp_part_floats(const FieldDesc& fd);
 // Grouped launches (multi-object scheduler): the objects of one architecture
