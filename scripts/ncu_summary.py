@@ -14,7 +14,8 @@ from collections import defaultdict
 
 CLASSES = {"k_sample": "sample", "k_fwd_tc": "field_fwd", "k_fwd_ws": "field_fwd", "k_fwd_ts": "field_fwd", "k_fwd_wx": "field_fwd",
            "k_fwd_tile": "field_fwd", "k_composite": "composite",
-           "k_bwd_tc": "mlp_bwd", "k_bwd_tile": "mlp_bwd", "k_encode_bwd": "encode_bwd", "k_adam": "adam"}
+           "k_bwd_tc": "mlp_bwd", "k_bwd_tile": "mlp_bwd", "k_encode_bwd": "encode_bwd", "k_adam": "adam",
+           "k_adam_fused": "adam"}
 
 KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
         "lts__throughput.avg.pct_of_peak_sustained_elapsed", "l1tex__throughput.avg.pct_of_peak_sustained_elapsed",
