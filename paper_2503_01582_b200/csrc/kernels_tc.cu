@@ -2031,8 +2031,8 @@ cudaError_t run_bwd_s(const FieldDesc& fd, const float* params, float* grad, lon
   // longest run reduced by pulls (else by the shuffle tree); PRENOM_BWD_PULL_MAX overrides
   static const int pull_max = env_int("PRENOM_BWD_PULL_MAX", kBwdPullMax);
   static const int wait_mode = env_int("PRENOM_BWD_WAIT", kBwdWaitDefault);
-  cudaError_t em = cudaMemsetAsync(tile_ctr, 0, sizeof(int), st);
-  if (em != cudaSuccess) return em;
+  // tile_ctr[0] was zeroed by the forward of the same step (tile_sched_exit resets
+  // its [2], which is this counter)
   float* part = mlp_part && (size_t)grid * fd.mlp_params <= part_cap ? mlp_part : nullptr;
   cudaError_t e2 = launch_pdl(kern, dim3((unsigned)grid), dim3(kBwdThreads), smem, st, fd, params, grad, n, S, count,
                               pos, reinterpret_cast<const uint4*>(feat_tiles), dout, tile_ctr, skip, mlp_levels,

@@ -45,16 +45,20 @@ struct StepStatsDev {
   int pad_;
 };
 
-// Persistent-kernel tile scheduler counters [next tile, CTAs done] of the
-// forward: the last CTA to leave resets both, so the forward needs no memset
-// node in front of it. (Applied to the backward too, the same self-reset made
-// k_bwd_tc 2.5x slower -- unexplained, measured -- so it keeps its memset.)
+// Persistent-kernel tile scheduler counters [next tile, CTAs done, backward's next
+// tile] of the forward: the last CTA to leave resets all three, so neither the
+// forward nor the backward that follows it needs a memset node in front of it
+// (a memset between the compositing kernel and the backward would keep the
+// backward's prologue from overlapping the compositing kernel under PDL).
+// (A self-reset inside the backward itself made k_bwd_tc 2.5x slower --
+// unexplained, measured.)
 __device__ __forceinline__ void tile_sched_exit(int* ctr) {
   if (threadIdx.x == 0) {
     __threadfence();
     if (atomicAdd(ctr + 1, 1) == (int)gridDim.x - 1) {
       ctr[0] = 0;
       ctr[1] = 0;
+      ctr[2] = 0;
     }
   }
 }
@@ -474,7 +478,9 @@ bool tc_concurrent_objects();          // that hint is set: objects run concurre
 size_t tc_feature_bytes(const FieldDesc& fd, long long n, int split);
 // writes the constant ones / zero core matrices of a stored-feature buffer (once per allocation)
 cudaError_t init_feature_tiles(const FieldDesc& fd, void* feat, size_t bytes, int split, cudaStream_t st);
-// tile_ctr: one device int per launch, zeroed by the launcher (dynamic tile scheduler)
+// tile_ctr (dynamic tile scheduler): the forward uses [0], [1] and leaves [0..2]
+// zeroed; the backward of the same step gets tile_ctr + 2 (zero on entry: the
+// buffer is zeroed at allocation and after every forward)
 cudaError_t launch_fwd_tc(const FieldDesc& fd, const float* params, long long n, int S, const int* count,
                           const float4* pos, void* feat_tiles, float4* out, int* flag, int* tile_ctr, int split,
                           cudaStream_t st);
