@@ -1235,8 +1235,10 @@ constexpr int kMG = kMlpWarps / 4;
 constexpr int kMlpThreads = 32 * kMlpWarps;
 constexpr int kScatThreads = 256;  // two warps per 32-sample group: level halves
 constexpr int kBwdMlpLevels = 1;   // per half, scattered by the MLP warps (measured on cfg2)
-constexpr int kBwdPullMax = 4;     // scatter_level: pull-reduce runs up to this length (cfg2 sweeps:
-                                   // 2-4 equal, 6 / 8 / 12 slower by 0.3 / 1 / 3.5%: pulls cost ALU, the tree shuffles)
+constexpr int kBwdPullMax = 2;     // scatter_level: pull-reduce runs up to this length (round-2 split
+                                   // backward: 2 vs 4 +0.4% cfg2, +0.5% cfg1, cfg3 / bf16 equal; 3 +0.25%,
+                                   // 6 -0.9%; round 1: 6 / 8 / 12 slower by 0.3 / 1 / 3.5%: pulls cost ALU,
+                                   // the tree shuffles)
 constexpr int kBwdThreads = kMlpThreads + kScatThreads;
 // MMA / slot waits (PRENOM_BWD_WAIT bits): 1 scatter warps sleep on the slot
 // barrier, 2 one MLP warp polls each MMA barrier
